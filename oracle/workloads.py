@@ -1,0 +1,225 @@
+"""Closed-form cavity modes, projections, CFL, and the BASELINE.json configs C1-C5
+(TEST INFRASTRUCTURE ONLY).
+
+All of this is oracle-side setup: it produces the seeded inputs that both the oracle and the
+GPU path consume (d, e, b, h, j^, materials at quadrature points, geometry control points, dt).
+Random draws come from ``synth`` (no method arithmetic there).
+"""
+import numpy as np
+from scipy.sparse.linalg import LinearOperator, eigs
+
+import synth
+from . import forms
+from .splines import gauss_rule, space_values, open_knots, bspline_values
+from .structured import TierB, kron3, apply_axis, curl_dual
+
+# ------------------------------------------------------------------------------------------
+# cavity eigenmodes of the unit cube with PEC walls (readings Z10, Z11)
+# ------------------------------------------------------------------------------------------
+
+
+class CavityMode:
+    """E = alpha * (A1 c s s, A2 s c s, A3 s s c) cos(w t), k = pi m, w = pi |m|, A . m = 0;
+    B = H = -(alpha/w) (k x A) (s c c, c s c, c c s) sin(w t)   (eps = mu = 1).
+    Here "c s s" = cos(k1 x) sin(k2 y) sin(k3 z) etc.  The first cube mode is
+    m = (1,1,0), A = (0,0,1): E = (0,0,sin pi x sin pi y) cos(sqrt2 pi t) (reading Z11)."""
+
+    def __init__(self, m, A, alpha=1.0):
+        self.m = np.asarray(m, dtype=np.float64)
+        self.A = np.asarray(A, dtype=np.float64)
+        if abs(self.A @ self.m) > 1e-14:
+            raise ValueError("A must be orthogonal to m (divergence-free)")
+        self.k = np.pi * self.m
+        self.w = np.pi * np.linalg.norm(self.m)
+        self.alpha = alpha
+
+    def _trig(self, X):
+        x, y, z = X[..., 0], X[..., 1], X[..., 2]
+        k1, k2, k3 = self.k
+        s = [np.sin(k1 * x), np.sin(k2 * y), np.sin(k3 * z)]
+        c = [np.cos(k1 * x), np.cos(k2 * y), np.cos(k3 * z)]
+        return s, c
+
+    def E(self, X, t):
+        s, c = self._trig(X)
+        f = [c[0] * s[1] * s[2], s[0] * c[1] * s[2], s[0] * s[1] * c[2]]
+        return self.alpha * np.cos(self.w * t) * np.stack([self.A[i] * f[i] for i in range(3)], -1)
+
+    def B(self, X, t):
+        s, c = self._trig(X)
+        g = [s[0] * c[1] * c[2], c[0] * s[1] * c[2], c[0] * c[1] * s[2]]
+        kxA = np.cross(self.k, self.A)
+        return -(self.alpha / self.w) * np.sin(self.w * t) * np.stack([kxA[i] * g[i] for i in range(3)], -1)
+
+
+class ModeSum:
+    def __init__(self, modes):
+        self.modes = modes
+
+    def E(self, X, t):
+        return sum(m.E(X, t) for m in self.modes)
+
+    def B(self, X, t):
+        return sum(m.B(X, t) for m in self.modes)
+
+
+def c2_modes():
+    """The four modes of configs[1] with alpha = rng(2).uniform(-1,1,4)."""
+    al = synth.c2_amplitudes()
+    spec = [((1, 1, 0), (0, 0, 1)), ((1, 0, 1), (0, 1, 0)), ((0, 1, 1), (1, 0, 0)),
+            ((1, 1, 1), np.array([1, 1, -2]) / np.sqrt(6))]
+    return ModeSum([CavityMode(m, A, a) for (m, A), a in zip(spec, al)])
+
+
+# ------------------------------------------------------------------------------------------
+# quadrature grid helpers (identity geometry unless noted)
+# ------------------------------------------------------------------------------------------
+
+def qp_grid(p, n, Q=None):
+    """1D Gauss points/weights per axis and the 3D grid of points [z][y][x][3]."""
+    n = forms._n3(n)
+    Q = Q or p + 1
+    xs, ws = zip(*[gauss_rule(n[a], Q) for a in range(3)])
+    Z, Y, X = np.meshgrid(xs[2], xs[1], xs[0], indexing="ij")
+    return xs, ws, np.stack([X, Y, Z], -1)
+
+
+def grid_to_elem(arr3, n, Q):
+    """[NQz][NQy][NQx] grid array -> element-major flat layout [ez][ey][ex][qz][qy][qx]."""
+    nx, ny, nz = forms._n3(n)
+    return np.asarray(arr3).reshape(nz, Q, ny, Q, nx, Q).transpose(0, 2, 4, 1, 3, 5).reshape(-1)
+
+
+def physical_points(p, n, ctrl=None, Q=None):
+    """F(x_q) on the global grid [z][y][x][3], by sum factorisation of the spline map."""
+    n = forms._n3(n)
+    Q = Q or p + 1
+    xs, _, Xg = qp_grid(p, n, Q)
+    if ctrl is None:
+        return Xg
+    ctrl = np.asarray(ctrl, dtype=np.float64).reshape(n[2] + p, n[1] + p, n[0] + p, 3)
+    V = [bspline_values(open_knots(p, n[a]), p, xs[a]) for a in range(3)]
+    return np.stack([kron3(V[0], V[1], V[2], ctrl[..., i]) for i in range(3)], -1)
+
+
+def interpolate_map(p, n, fmap):
+    """Control points of the spline map in S_p(Xi)^3 interpolating fmap at the Greville
+    points (reading Z18).  fmap: X[...,3] -> F[...,3]."""
+    n = forms._n3(n)
+    gs, Bs = [], []
+    for a in range(3):
+        X = open_knots(p, n[a])
+        g = np.array([X[i + 1:i + p + 1].mean() for i in range(n[a] + p)])
+        gs.append(g)
+        Bs.append(bspline_values(X, p, g))
+    Z, Y, Xg = np.meshgrid(gs[2], gs[1], gs[0], indexing="ij")
+    F = fmap(np.stack([Xg, Y, Z], -1))
+    inv = [np.linalg.inv(B) for B in Bs]
+    return np.stack([kron3(inv[0], inv[1], inv[2], F[..., i]) for i in range(3)], -1)
+
+
+def c3_map(X):
+    """C3 map: x -> x + 0.1 sin(pi x) sin(pi y) sin(pi z) (1,1,1) (BASELINE.json configs[2])."""
+    s = 0.1 * np.sin(np.pi * X[..., 0]) * np.sin(np.pi * X[..., 1]) * np.sin(np.pi * X[..., 2])
+    return X + s[..., None]
+
+
+# ------------------------------------------------------------------------------------------
+# L2 projections (unweighted, parametric = physical for the identity map; reading Z12)
+# ------------------------------------------------------------------------------------------
+
+def _project(p, n, cplx, k, field_grid, Q=None):
+    """Unweighted L2 projection of a k-form given by its proxy components on the global
+    quadrature grid ([z][y][x][3]) onto the component spaces: Gram solve per component."""
+    n = forms._n3(n)
+    Q = Q or p + 1
+    xs, ws, _ = qp_grid(p, n, Q)
+    spaces = forms.component_spaces(cplx, k)
+    out = []
+    for c, sc in enumerate(spaces):
+        V = [space_values(sc[a], p, n[a], xs[a]) for a in range(3)]
+        w3 = ws[2][:, None, None] * ws[1][None, :, None] * ws[0][None, None, :]
+        rhs = kron3(V[0].T, V[1].T, V[2].T, w3 * field_grid[..., c])
+        Ginv = [np.linalg.inv(V[a].T @ (ws[a][:, None] * V[a])) for a in range(3)]
+        out.append(kron3(Ginv[0], Ginv[1], Ginv[2], rhs))
+    return forms.join(out)
+
+
+def project_dual2(p, n, field_grid, Q=None):
+    return _project(p, n, "dual", 2, field_grid, Q)
+
+
+def project_primal2(p, n, field_grid, Q=None):
+    return _project(p, n, "primal", 2, field_grid, Q)
+
+
+def project_dual1(p, n, field_grid, Q=None):
+    return _project(p, n, "dual", 1, field_grid, Q)
+
+
+def eval_form(p, n, cplx, k, v, Q=None):
+    """Parametric proxy of the discrete form v at the global quadrature grid [z][y][x][3]."""
+    n = forms._n3(n)
+    Q = Q or p + 1
+    xs, _, _ = qp_grid(p, n, Q)
+    comps = forms.split(v, cplx, k, p, n)
+    out = []
+    for c, sc in enumerate(forms.component_spaces(cplx, k)):
+        V = [space_values(sc[a], p, n[a], xs[a]) for a in range(3)]
+        out.append(kron3(V[0], V[1], V[2], comps[c]))
+    return np.stack(out, -1)
+
+
+def l2_rel_error(p, n, cplx, k, v, exact_grid, Q=None):
+    n = forms._n3(n)
+    Q = Q or p + 1
+    _, ws, _ = qp_grid(p, n, Q)
+    w3 = ws[2][:, None, None] * ws[1][None, :, None] * ws[0][None, None, :]
+    diff = eval_form(p, n, cplx, k, v, Q) - exact_grid
+    return np.sqrt(np.sum(w3[..., None] * diff ** 2) / np.sum(w3[..., None] * exact_grid ** 2))
+
+
+# ------------------------------------------------------------------------------------------
+# CFL (reading Z15: dt_max = 2 / sqrt(lambda_max(D~1 K~1^{-1} M2 D1 K1^{-1} M~2)))
+# ------------------------------------------------------------------------------------------
+
+def cfl_dt_max(tb: TierB, tol=1e-8):
+    """Leapfrog stability limit of scheme 2 (parity unpinned in absolute value, Z15).
+
+    d^{n+1} - 2 d^n + d^{n-1} = -dt^2 A d^n with A = D~1 K~1^{-1} M2 D1 K1^{-1} M~2, stable iff
+    dt^2 lambda_max(A) < 4.  lambda_max by ARPACK (a library eigen-solver) on A.
+    """
+    from .structured import curl_primal
+
+    def A(x):
+        d = tb.split_e(np.asarray(x).ravel())
+        e = tb.solve_K1(tb.mass_eps(d))
+        b = curl_primal(e)
+        h = tb.solve_Kt1(tb.mass_mu(b))
+        return forms.join(curl_dual(h))
+
+    N = tb.N_e
+    op = LinearOperator((N, N), matvec=A, dtype=np.float64)
+    v0 = synth.rng(100).standard_normal(N)
+    lam = eigs(op, k=1, which="LM", v0=v0, tol=tol, return_eigenvectors=False)
+    lam = float(np.max(np.real(lam)))
+    return 2.0 / np.sqrt(lam)
+
+
+# ------------------------------------------------------------------------------------------
+# consistent initial state
+# ------------------------------------------------------------------------------------------
+
+def consistent_state(tb: TierB, d0, bhalf):
+    """e0 = K1^{-1} M~2 d0, h^{1/2} = K~1^{-1} M2 b^{1/2} (eqs. discrete2_hodge_eps/mu)."""
+    return d0, tb.hodge_eps(d0), bhalf, tb.hodge_mu(bhalf)
+
+
+def cavity_initial_state(tb: TierB, mode, dt):
+    """d0 = projection of D(0) = E(0) onto X~2; b^{1/2} = projection of exact B(dt/2) onto
+    X2_{h,0} (reading Z8; identity geometry, eps = mu = 1)."""
+    p, n = tb.p, tb.n
+    _, _, X = qp_grid(p, n, tb.Q)
+    d0 = project_dual2(p, n, mode.E(X, 0.0), tb.Q)
+    bh = project_primal2(p, n, mode.B(X, 0.5 * dt), tb.Q)
+    return consistent_state(tb, d0, bh)

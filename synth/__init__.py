@@ -1,0 +1,45 @@
+"""Seeded synthetic input draws shared by the oracle tests, the GPU tests and bench.py.
+
+This module holds NONE of the method's arithmetic: only random draws (numpy default_rng with
+the per-config seeds of SURVEY 8(d): rng(k) for config Ck, draws in the listed order) and a
+spectral smoothing filter used to shape a random field.  Anything that needs spline spaces,
+masses, pairings or solves (projections, consistent e/h, CFL) lives in ``oracle.workloads``.
+"""
+import numpy as np
+
+
+def rng(k):
+    return np.random.default_rng(k)
+
+
+def normal(k, *sizes):
+    """Independent N(0,1) vectors of the given sizes from rng(k), drawn in order."""
+    g = rng(k)
+    return [g.standard_normal(s) for s in sizes]
+
+
+def c2_amplitudes():
+    """C2: alpha = rng(2).uniform(-1, 1, 4) (BASELINE.json configs[1])."""
+    return rng(2).uniform(-1.0, 1.0, 4)
+
+
+def c3_centres():
+    """C3: inclusion centre c_eps = rng(3).uniform(.25,.75,3), then pulse centre
+    c_J = rng(3).uniform(.2,.8,3) (second draw of the same generator)."""
+    g = rng(3)
+    c_eps = g.uniform(0.25, 0.75, 3)
+    c_J = g.uniform(0.2, 0.8, 3)
+    return c_eps, c_J
+
+
+def smooth_field(k, shape):
+    """C4 random smooth coefficients: N(0,1) from rng(k) -> orthonormal DCT-II ->
+    multiply by 1/(1+|kappa|^2) (kappa = integer DCT index triple) -> inverse DCT.
+    ``shape`` is [z][y][x]."""
+    from scipy.fft import dctn, idctn
+    g = rng(k)
+    x = g.standard_normal(shape)
+    X = dctn(x, norm="ortho")
+    kz, ky, kx = np.meshgrid(*[np.arange(s) for s in shape], indexing="ij")
+    X /= 1.0 + (kx ** 2 + ky ** 2 + kz ** 2)
+    return idctn(X, norm="ortho")

@@ -1,0 +1,241 @@
+"""Pins of the oracle's scheme-2 step (tier A and tier B).
+
+Paper facts: Hodge definition K1 e = M~2 d; Kronecker inverse equals a
+dense solve of the assembled block; energy identity eq. energy_aux;
+conservation (reading Z5/Z19 for the discrete invariant); Gauss laws;
+convergence E ~ h^p, H ~ h^(p-1); first cube mode with energy 1/8 (Z11).
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import forms
+from oracle import workloads as W
+from oracle.assemble import Quad, physical_qp
+from oracle.scheme import TierA
+from oracle.structured import TierB
+from conftest import rel
+
+
+def _rand_state(N_e, N_h, seed):
+    g = np.random.default_rng(seed)
+    return g.standard_normal(N_e), g.standard_normal(N_e), g.standard_normal(N_h), g.standard_normal(N_h)
+
+
+@pytest.mark.parametrize("p,n", [(2, 2), (3, 2), (4, 2)])
+def test_kronecker_solve_equals_dense_solve(p, n):
+    """<= 1000-DoF grids: tier-A sparse direct and tier-B mode-wise both equal numpy.linalg.solve
+    of the assembled 3D block (BJ north_star)."""
+    A = TierA(p, n)
+    B = TierB(p, n)
+    r = np.random.default_rng(5).standard_normal(A.N_e)
+    rh = np.random.default_rng(6).standard_normal(A.N_h)
+    assert A.N_e <= 1000
+    Kd, Ktd = A.K1.toarray(), A.Kt1.toarray()
+    xd = np.linalg.solve(Kd, r)
+    xdh = np.linalg.solve(Ktd, rh)
+    # backward-stable solves agree to O(eps * cond) (cond(K1 blocks) <= ~2e4)
+    tol = 20 * np.finfo(float).eps * np.linalg.cond(Kd)
+    tolh = 20 * np.finfo(float).eps * np.linalg.cond(Ktd)
+    assert rel(A.solve_K1(r), xd) < tol
+    assert rel(forms.join(B.solve_K1(B.split_e(r))), xd) < tol
+    assert rel(A.solve_Kt1(rh), xdh) < tolh
+    assert rel(forms.join(B.solve_Kt1(B.split_h(rh))), xdh) < tolh
+    # transposed solves
+    assert rel(forms.join(B.solve_K1(B.split_e(r), T=True)), np.linalg.solve(Kd.T, r)) < tol
+
+
+def _c3_like(p, n, seed=0):
+    ctrl = W.interpolate_map(p, n, W.c3_map)
+    X = physical_qp(Quad(p, n), ctrl)
+    c = np.array([0.4, 0.55, 0.5])
+    inv_eps = np.where(np.linalg.norm(X - c, axis=-1) < 0.25, 0.25, 1.0).ravel()
+    return ctrl, inv_eps
+
+
+TOL_AB = {2: 1e-14, 3: 1e-13, 4: 5e-12}   # ~ eps x cond(K blocks), cond from SURVEY A2
+
+
+@pytest.mark.parametrize("p,n", [(2, 3), (3, 3), (4, 2), (2, (3, 2, 4))])
+@pytest.mark.parametrize("geom", ["identity", "curved"])
+def test_tier_b_equals_tier_a(p, n, geom):
+    if geom == "identity":
+        A = TierA(p, n)
+        B = TierB(p, n)
+    else:
+        ctrl, ie = _c3_like(p, n)
+        A = TierA(p, n, ctrl=ctrl, inv_eps_qp=ie)
+        B = TierB(p, n, ctrl=ctrl, inv_eps=ie, inv_mu=1.0)
+    st = _rand_state(A.N_e, A.N_h, 7)
+    j = np.random.default_rng(8).standard_normal(A.N_e)
+    ra = A.step(*st, 0.013, j, 0.7)
+    rb = B.step(*st, 0.013, j, 0.7)
+    for x, y in zip(rb, ra):
+        assert rel(x, y) < TOL_AB[p]
+    assert abs(A.energy(*ra) - B.energy(*rb)) < 1e-12 * abs(A.energy(*ra))
+    assert np.allclose(A.gauss(ra[0], ra[2]), B.gauss(rb[0], rb[2]), atol=1e-13)
+
+
+@pytest.mark.parametrize("p,n", [(2, 3), (3, 2)])
+def test_hodge_defining_residual(p, n):
+    ctrl, ie = _c3_like(p, n)
+    A = TierA(p, n, ctrl=ctrl, inv_eps_qp=ie)
+    d = np.random.default_rng(9).standard_normal(A.N_e)
+    e = A.solve_K1(A.Meps @ d)
+    r = A.Meps @ d
+    assert np.linalg.norm(A.K1 @ e - r) / np.linalg.norm(r) < 1e-12
+
+
+@pytest.mark.parametrize("p,n", [(2, 3), (3, 2)])
+def test_skew_identity(p, n):
+    """e^T K~2 D~1 h = h^T K2 D1 e for any e, h (eq. energy_aux): with
+    K~2 = K1^T and K2 = K~1^T."""
+    A = TierA(p, n)
+    g = np.random.default_rng(10)
+    e, h = g.standard_normal(A.N_e), g.standard_normal(A.N_h)
+    lhs = e @ (A.K1.T @ (A.Dt1 @ h))
+    rhs = h @ (A.Kt1.T @ (A.D1 @ e))
+    assert abs(lhs - rhs) < 1e-13 * (abs(lhs) + 1)
+
+
+def _modified_energy(A, d, e, b_prev, h):
+    """E^n = 1/2 d^T K1 e + 1/2 b^{n-1/2 T} K~1 h^{n+1/2}  (reading Z19: exactly invariant)."""
+    return 0.5 * d @ (A.K1 @ e) + 0.5 * b_prev @ (A.Kt1 @ h)
+
+
+def test_modified_energy_exactly_conserved_and_gauss():
+    p, n = 3, 2
+    ctrl, ie = _c3_like(p, n)
+    A = TierA(p, n, ctrl=ctrl, inv_eps_qp=ie)
+    B = TierB(p, n, ctrl=ctrl, inv_eps=ie, inv_mu=1.0)
+    d, _, b, _ = _rand_state(A.N_e, A.N_h, 11)
+    dtmax = W.cfl_dt_max(B)
+    dt = 0.9 * dtmax
+    e = A.solve_K1(A.Meps @ d)
+    h = A.solve_Kt1(A.Mmu @ b)
+    g0 = (A.Dt2 @ d, A.D2 @ b)
+    Es = []
+    b_prev = b
+    for k in range(300):
+        b_prev = b
+        d, e, b, h = A.step(d, e, b, h, dt)
+        Es.append(_modified_energy(A, d, e, b_prev, h))
+    Es = np.array(Es)
+    assert (Es.max() - Es.min()) / abs(Es.mean()) < 1e-13
+    # Gauss laws are preserved exactly up to round-off
+    assert np.abs(A.Dt2 @ d - g0[0]).max() < 1e-11
+    assert np.abs(A.D2 @ b - g0[1]).max() < 1e-11
+
+
+def test_unstable_above_cfl():
+    """Sharpness of the computed stability limit: 1.05 dt_max blows up, 0.95 dt_max stays bounded."""
+    p, n = 2, 3
+    B = TierB(p, n)
+    dtmax = W.cfl_dt_max(B)
+    d, _, b, _ = _rand_state(B.N_e, B.N_h, 12)
+    out = {}
+    for f in (0.95, 1.05):
+        x = (d, B.hodge_eps(d), b, B.hodge_mu(b))
+        with np.errstate(all="ignore"):
+            x = B.run(*x, f * dtmax, 2000)
+            nrm = np.linalg.norm(x[0])
+        out[f] = nrm if np.isfinite(nrm) else np.inf
+    assert out[0.95] < 10 * np.linalg.norm(d)
+    assert out[1.05] > 1e3 * np.linalg.norm(d)
+
+
+def test_poynting_identity_with_divergence_free_source():
+    """With j = D~1 a (so D~2 j = 0): E^{n+1} - E^n = -(dt/2)(e^{n+1}+e^n)^T K1^T j^{n+1/2}
+    (derived from eq. energy_aux), and Gauss for d is untouched by the source."""
+    p, n = 3, 2
+    A = TierA(p, n)
+    g = np.random.default_rng(13)
+    a = g.standard_normal(A.N_h)
+    j = A.Dt1 @ a
+    assert np.abs(A.Dt2 @ j).max() < 1e-13
+    d, _, b, _ = _rand_state(A.N_e, A.N_h, 14)
+    e = A.solve_K1(A.Meps @ d)
+    h = A.solve_Kt1(A.Mmu @ b)
+    dt = 0.01
+    E_old = None
+    g0 = A.Dt2 @ d
+    for k in range(50):
+        s = np.sin(0.3 * k)
+        e_old, bm = e, b
+        d, e, b, h = A.step(d, e, b, h, dt, j, s)
+        E_new = _modified_energy(A, d, e, bm, h)
+        if E_old is not None:
+            pred = -(dt / 2) * (e + e_old) @ (A.K1.T @ (s * j))
+            assert abs((E_new - E_old) - pred) < 1e-12 * abs(E_new)
+        E_old = E_new
+    assert np.abs(A.Dt2 @ d - g0).max() < 1e-11
+
+
+def test_time_reversibility():
+    """Leapfrog is time reversible: undo b then d with the same dt."""
+    p, n = 2, 3
+    A = TierA(p, n)
+    d0, _, b0, _ = _rand_state(A.N_e, A.N_h, 15)
+    e0 = A.solve_K1(A.Meps @ d0)
+    h0 = A.solve_Kt1(A.Mmu @ b0)
+    dt = 0.02
+    d, e, b, h = A.run(d0, e0, b0, h0, dt, 30)
+    for _ in range(30):
+        b = b + dt * (A.D1 @ e)
+        h = A.solve_Kt1(A.Mmu @ b)
+        d = d - dt * (A.Dt1 @ h)
+        e = A.solve_K1(A.Meps @ d)
+    assert rel(d, d0) < 1e-12 and rel(b, b0) < 1e-12
+
+
+def test_first_cube_mode_energy_and_convergence_rates():
+    """Cube cavity, first mode (Z11), small fixed dt (reading Z22): relative L2 errors of E and H
+    at T decay with rates >= p and >= p-1 (Fig. 2) and the discrete energy tends to the
+    exact 1/8."""
+    mode = W.CavityMode((1, 1, 0), (0, 0, 1))
+    dt, T = 2e-3, 0.2
+    ns = int(round(T / dt))
+    for p in (2, 3):
+        errs, ens = [], []
+        for n in (2, 4, 8):
+            tb = TierB(p, n)
+            st = W.cavity_initial_state(tb, mode, dt)
+            ens.append(abs(st[0] @ forms.join(tb.mass_eps(tb.split_e(st[0]))) - 0.25))
+            d, e, b, h = tb.run(*st, dt, ns)
+            _, _, X = W.qp_grid(p, n)
+            errs.append((W.l2_rel_error(p, n, "primal", 1, e, mode.E(X, T)),
+                         W.l2_rel_error(p, n, "dual", 1, h, mode.B(X, T + dt / 2))))
+        errs = np.array(errs)
+        rates = np.log2(errs[:-1] / errs[1:])
+        assert rates[-1, 0] > p - 0.3, rates
+        assert rates[-1, 1] > p - 1 - 0.3, rates
+        # d^T M~2 d with d = projection of E(0) -> int |E|^2 = 1/4 (energy 1/8, eps = 1),
+        # with the error of a degree-(p-1)/(p-2) projection: O(h^(2(p-1)))
+        ens = np.array(ens)
+        assert np.all(np.log2(ens[:-1] / ens[1:]) > 2 * (p - 1) - 0.3), ens
+    tb = TierB(3, 8)
+    st = W.cavity_initial_state(tb, mode, dt)
+    assert abs(tb.energy(*st) - 0.125) < 1e-3
+
+
+def test_projection_reproduces_members():
+    p, n = 3, 3
+    tb = TierB(p, n)
+    g = np.random.default_rng(16)
+    v = g.standard_normal(tb.N_e)
+    f = W.eval_form(p, n, "dual", 2, v)
+    assert rel(W.project_dual2(p, n, f), v) < 1e-12
+    vb = g.standard_normal(tb.N_h)
+    fb = W.eval_form(p, n, "primal", 2, vb)
+    assert rel(W.project_primal2(p, n, fb), vb) < 1e-12
+
+
+def test_cfl_scalings():
+    """CFL is linear in h (Fig. 5 right) and decreases roughly like 1/p^2 (Fig. 5 left).
+    The absolute value is parity-unpinned (reading Z15)."""
+    c = {}
+    for p, n in ((2, 4), (2, 8), (3, 8), (4, 8)):
+        c[(p, n)] = W.cfl_dt_max(TierB(p, n)) * n
+    assert abs(c[(2, 4)] / c[(2, 8)] - 1) < 0.05
+    slope = np.log(c[(4, 8)] / c[(2, 8)]) / np.log(2.0)
+    assert -2.4 < slope < -1.2, slope
