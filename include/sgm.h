@@ -1,0 +1,197 @@
+/*
+ * sgm.h -- C ABI of the B200-native explicit spline-geometric Maxwell step
+ *          (arXiv 2302.04979, "second discretization scheme").
+ *
+ * What the library computes
+ * -------------------------
+ * State (reading Z8 in DESIGN.md): four fp64 coefficient vectors
+ *   d in X~^2 (D, dual 2-form)      e in X^1_{h,0} (E, primal 1-form)    -- at t_n
+ *   b in X^2_{h,0} (B, primal 2-form) h in X~^1 (H, dual 1-form)         -- at t_{n+1/2}
+ * One leapfrog step (eqs. discrete2_ampere, _hodge_eps, _faraday, _hodge_mu):
+ *   d <- d + dt (D~1 h - s_k j^)        D~1: integer dual curl
+ *   e <- K1^{-1} M~2_{1/eps} d          K1: metric-free pairing, block diagonal with
+ *                                        Kronecker blocks (eq. tensor_K)
+ *   b <- b - dt D1 e                    D1: integer primal curl
+ *   h <- K~1^{-1} M2_{1/mu} b           K~1 blocks: eq. tensor_Ktilde
+ * The Kronecker inverses are applied mode by mode (eq. kroninverse, vec trick
+ * P:L575-585) as batched banded LU sweeps of the 1D factors along x, y and z.
+ *
+ * Discretisation parameters: n_el[a] uniform elements per axis, open knots,
+ * maximal smoothness, degree p >= 2 (primal p / p-1, dual p-1 / p-2); per axis
+ *   a = n_el + p - 2 (trimmed S_p, S_{p-2}),  b = n_el + p - 1 (S_{p-1}).
+ *
+ * Memory layout: every form vector is its three components concatenated
+ * in the order 1, 2, 3; each component is a C-order array [z][y][x] (x fastest).
+ * Component extents (x, y, z):
+ *   e, d :  (b,a,a) (a,b,a) (a,a,b)       N_e = N_d = 3 a^2 b  (per-axis a,b)
+ *   b, h :  (a,b,b) (b,a,b) (b,b,a)       N_b = N_h = 3 a b^2
+ * Quadrature-point arrays (materials, coordinates) are element-major:
+ *   [ez][ey][ex][qz][qy][qx]  with Q = quad_points Gauss-Legendre points per axis per element.
+ *
+ * Conventions
+ * -----------
+ * - Every call returns sgm_status; no C++ exception crosses the ABI.  On a non-OK status
+ *   sgm_last_error() returns a thread-local message.
+ * - Device pointers are caller-owned, 8-byte-aligned fp64 buffers on the plan's device
+ *   (e.g. torch.float64 CUDA tensors' data_ptr()).  `stream` is a cudaStream_t passed as void*
+ *   (NULL = legacy default stream).  Calls marked async enqueue work on `stream` and return.
+ * - Arguments are validated before any launch: on SGM_E_INVALID_ARG nothing was modified.
+ * - The plan is immutable after create except through set_material (synchronous; must not
+ *   overlap in-flight calls on the plan).  Concurrent calls on different streams with
+ *   distinct workspaces are allowed.
+ * - There is no CPU fallback: a plan created with device < 0 answers queries (lengths,
+ *   shapes, 1D tables, quadrature coordinates) but every compute call returns
+ *   SGM_E_INVALID_ARG.
+ */
+#ifndef SGM_H
+#define SGM_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SGM_PMIN 2
+#define SGM_PMAX 4 /* degrees with compiled kernels */
+
+typedef enum {
+  SGM_OK = 0,
+  SGM_E_INVALID_ARG = 1,       /* NULL/misaligned pointer, n_el < 1, dt non-finite, n_steps < 0,
+                                  bad enum, too-small workspace, host-only plan */
+  SGM_E_UNSUPPORTED = 2,       /* p < 2, p > SGM_PMAX, or extents beyond the kernel
+                                  tiling limits (line length > 1024) */
+  SGM_E_GEOMETRY = 3,          /* det DF <= 0 or non-finite at a quadrature point */
+  SGM_E_MATERIAL = 4,          /* eps or mu <= 0 or non-finite at a quadrature point */
+  SGM_E_SINGULAR = 5,          /* zero pivot or backward error > 1e-13 in a no-pivot 1D LU
+                                  (reading Z14) */
+  SGM_E_SOURCE_DIVERGENCE = 6, /* ||D~2 j^||_inf > 1e-12 ||j^||_inf */
+  SGM_E_CUDA = 7,              /* CUDA runtime/launch failure; sticky for the plan */
+  SGM_E_NOMEM = 8
+} sgm_status;
+
+typedef struct sgm_plan_t* sgm_plan; /* opaque */
+
+typedef enum { SGM_FORM_E = 0, SGM_FORM_D = 1, SGM_FORM_B = 2, SGM_FORM_H = 3 } sgm_form;
+/* K1 : X^1_{h,0} -> (X~^2)*   (rows dual 2-forms);  K~1 : X~^1 -> (X^2_{h,0})* */
+typedef enum { SGM_K1 = 0, SGM_KT1 = 1 } sgm_pairing;
+/* M~2_{1/eps} on X~^2, M2_{1/mu} on X^2_{h,0} */
+typedef enum { SGM_MASS_EPS = 0, SGM_MASS_MU = 1 } sgm_mass;
+/* D1 : X^1_{h,0} -> X^2_{h,0},  D~1 : X~^1 -> X~^2 */
+typedef enum { SGM_CURL_PRIMAL = 0, SGM_CURL_DUAL = 1 } sgm_curl_kind;
+typedef enum { SGM_EPS = 0, SGM_MU = 1 } sgm_material;
+/* 1D matrices of one axis, for inspection (dense row-major L x L):
+   Hat{G} (a x a) = int D''_k B_c, Hat{M} (b x b) = int B'_j D'_k;
+   separable-Hodge Grams Gamma_B^{p-1} (b), Gamma_C^{p-2} (a), Gamma_B^{p} (a), Gamma_C^{p-1} (b). */
+typedef enum {
+  SGM_TAB_G = 0, SGM_TAB_M = 1, SGM_TAB_GAMMA_B1 = 2, SGM_TAB_GAMMA_C2 = 3,
+  SGM_TAB_GAMMA_BP = 4, SGM_TAB_GAMMA_C1 = 5
+} sgm_table;
+
+typedef struct {
+  int n_el[3];             /* elements per axis (x, y, z), >= 1 */
+  int degree;              /* p, SGM_PMIN..SGM_PMAX */
+  const double* geom_ctrl; /* host; NULL = identity map.  Control points of F in S_p(Xi)^3,
+                              untrimmed B-splines, layout [(nz+p)][(ny+p)][(nx+p)][3].
+                              Copied at create; caller keeps ownership. */
+  int quad_points;         /* Q per axis per element for the geometry/material masses;
+                              0 -> p+1 (reading Z13).  Allowed: p+1 .. 8 */
+  int device;              /* CUDA ordinal; < 0 -> host-only plan (queries only) */
+} sgm_plan_desc;
+
+/* ---- plan lifetime and queries (synchronous) ------------------------------------------- */
+sgm_status sgm_plan_create(const sgm_plan_desc* desc, sgm_plan* out);
+sgm_status sgm_plan_destroy(sgm_plan plan);
+sgm_status sgm_plan_len(sgm_plan plan, sgm_form form, size_t* n);           /* N_e, N_d, N_b, N_h */
+sgm_status sgm_plan_shape(sgm_plan plan, sgm_form form, int comp, int xyz[3]); /* comp 0..2 */
+sgm_status sgm_plan_qp_count(sgm_plan plan, size_t* n_qp);
+/* Physical quadrature points F(x_q), host, element-major layout, 3 doubles per point. */
+sgm_status sgm_plan_qp_coords(sgm_plan plan, double* host_xyz);
+/* Dense 1D table of one axis into host_out (L*L doubles); *L receives the size. */
+sgm_status sgm_plan_table(sgm_plan plan, sgm_table which, int axis, double* host_out, int* L);
+/* Hodge classification: 1 = separable (Kronecker Grams, identity / axis-aligned affine F and
+   constant material), 0 = general (weights at quadrature points). */
+sgm_status sgm_plan_hodge_separable(sgm_plan plan, sgm_mass mass, int* separable);
+
+/* Material eps (SGM_EPS) or mu (SGM_MU).  values == NULL -> constant c.  Otherwise values is a
+   host array of the material at every quadrature point (element-major), > 0 and finite.
+   Rebuilds the Hodge weights W = w_q (1/material) DF^T DF / det DF and uploads.
+   Synchronous. */
+sgm_status sgm_plan_set_material(sgm_plan plan, sgm_material which, const double* values, double c);
+
+/* Workspace (device bytes) needed by sgm_step / kron_solve / pairing_apply / hodge_* /
+   energy / gauss.  One workspace must not be shared by concurrent calls. */
+sgm_status sgm_workspace_bytes(sgm_plan plan, size_t* bytes);
+
+/* ---- the hot path (async on stream) ---------------------------------------------------- */
+/* n_steps leapfrog steps in place.  j_hat: device, length N_d, a dual 2-form with D~2 j^ = 0
+   (check once with sgm_check_source), NULL = no source.  j_amp: device, length n_steps,
+   s_k multiplying j^ at step k (the paper's separable-in-time source); NULL -> 1.0.
+   On exit d, e are at t_n + n_steps dt and b, h at t_{n+1/2} + n_steps dt. */
+sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h,
+                    const double* j_hat, const double* j_amp, double dt, int n_steps,
+                    void* workspace, size_t ws_bytes, void* stream);
+
+/* End-to-end variant on HOST buffers (pinned recommended): copies d,e,b,h (and j_hat, j_amp
+   if given) host->device into plan-owned mirrors, runs sgm_step, copies d,e,b,h back and
+   synchronises `stream`.  Synchronous. */
+sgm_status sgm_step_host(sgm_plan plan, double* d, double* e, double* b, double* h,
+                         const double* j_hat, const double* j_amp, double dt, int n_steps,
+                         void* stream);
+
+/* x = K^{-1} rhs (transpose = 0) or K^{-T} rhs (transpose = 1), K in {K1, K~1}; mode-wise
+   banded LU sweeps (eq. kroninverse).  rhs == x allowed.  Async. */
+sgm_status sgm_kron_solve(sgm_plan plan, sgm_pairing which, int transpose, const double* rhs,
+                          double* x, void* workspace, size_t ws_bytes, void* stream);
+/* y = K x or K^T x (Kronecker banded mat-vecs).  x != y.  Async. */
+sgm_status sgm_pairing_apply(sgm_plan plan, sgm_pairing which, int transpose, const double* x,
+                             double* y, void* workspace, size_t ws_bytes, void* stream);
+/* y = M x with M = M~2_{1/eps} (x, y in X~^2) or M2_{1/mu} (X^2_{h,0}).  x != y.  Async. */
+sgm_status sgm_hodge_apply(sgm_plan plan, sgm_mass which, const double* x, double* y,
+                           void* workspace, size_t ws_bytes, void* stream);
+/* Discrete Hodge star of scheme 2: y = K1^{-1} M~2_{1/eps} x (EPS: d -> e) or
+   y = K~1^{-1} M2_{1/mu} x (MU: b -> h) (eqs. discrete2_hodge_eps/_mu).  x != y.  Async. */
+sgm_status sgm_hodge_star(sgm_plan plan, sgm_mass which, const double* x, double* y,
+                          void* workspace, size_t ws_bytes, void* stream);
+/* y = D1 x (PRIMAL: e-shaped -> b-shaped) or y = D~1 x (DUAL: h-shaped -> d-shaped).  Async. */
+sgm_status sgm_curl(sgm_plan plan, sgm_curl_kind kind, const double* x, double* y, void* stream);
+/* out_dev[0] = 1/2 (d^T K1 e + b^T K~1 h)  (eq. energy_matrix_wedge, with
+   K~2 = K1^T, K2 = K~1^T).  Deterministic reduction.  Async. */
+sgm_status sgm_energy(sgm_plan plan, const double* d, const double* e, const double* b,
+                      const double* h, double* out_dev, void* workspace, size_t ws_bytes,
+                      void* stream);
+/* out_dev[0] = ||D~2 d||_inf, out_dev[1] = ||D2 b||_inf (Gauss laws).  Async. */
+sgm_status sgm_gauss(sgm_plan plan, const double* d, const double* b, double* out_dev,
+                     void* workspace, size_t ws_bytes, void* stream);
+/* Checks ||D~2 j^||_inf <= 1e-12 ||j^||_inf.  Synchronous on stream. */
+sgm_status sgm_check_source(sgm_plan plan, const double* j_hat, void* workspace,
+                            size_t ws_bytes, void* stream);
+
+/* Number of kernels one sgm_step step launches for this plan (for launch accounting). */
+sgm_status sgm_plan_kernels_per_step(sgm_plan plan, int* n);
+
+/* Per-kernel timing of sgm_step (CUDA events recorded on the launching stream around every
+   kernel when enabled).  Kernel classes: */
+typedef enum {
+  SGM_K_AMPERE_X = 0,  /* fused d-update (D~1 h, j) + x-sweep (mass . K1 solve) */
+  SGM_K_EPS_Y = 1,     /* y-sweep of the eps half */
+  SGM_K_EPS_Z = 2,     /* z-sweep of the eps half, writes e */
+  SGM_K_FARADAY_X = 3, /* fused b-update (D1 e) + x-sweep (mass . K~1 solve) */
+  SGM_K_MU_Y = 4,
+  SGM_K_MU_Z = 5,      /* writes h */
+  SGM_K_UPDATE = 6,    /* stand-alone d/b update (general-Hodge path) */
+  SGM_K_HODGE_GENERAL = 7, /* sum-factorised mass apply with quadrature weights */
+  SGM_K_SOLVE_X = 8,   /* solve-only x-sweep (general-Hodge path) */
+  SGM_K_CLASSES = 9
+} sgm_kernel_class;
+sgm_status sgm_plan_set_profiling(sgm_plan plan, int on);
+/* Sums, per class, the event-timed milliseconds and launch counts recorded since the last call
+   (synchronises on the recorded events), then clears the record.  ms/counts: SGM_K_CLASSES. */
+sgm_status sgm_plan_profile(sgm_plan plan, double* ms, int* counts);
+const char* sgm_last_error(void);
+const char* sgm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SGM_H */

@@ -1,0 +1,784 @@
+// C ABI of the sgm library (include/sgm.h): plan management, argument validation and the
+// launch schedules of the scheme-2 step and its building blocks.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "kernels.cuh"
+#include "sgm_internal.h"
+
+namespace sgm {
+
+static thread_local std::string g_err;
+void set_error(const std::string& s) { g_err = s; }
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = (cudaSetDevice(dev) == cudaSuccess);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+sgm_status fail(sgm_status s, const std::string& msg) {
+  set_error(msg);
+  return s;
+}
+
+sgm_status cuda_check(Plan* P, const char* where) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    if (P) P->sticky_cuda_error = true;
+    return fail(SGM_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+  }
+  return SGM_OK;
+}
+
+inline bool aligned8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7) == 0; }
+
+size_t form_len(const Plan& P, int kind) {
+  size_t n = 0;
+  for (int c = 0; c < 3; ++c) {
+    int e[3];
+    comp_shape(P, kind, c, e);
+    n += size_t(e[0]) * e[1] * e[2];
+  }
+  return n;
+}
+
+size_t comp_off(const Plan& P, int kind, int c) {
+  size_t off = 0;
+  for (int k = 0; k < c; ++k) {
+    int e[3];
+    comp_shape(P, kind, k, e);
+    off += size_t(e[0]) * e[1] * e[2];
+  }
+  return off;
+}
+
+const double* table(const Plan& P, int axis, int op) {
+  return P.tables_dev + (size_t(axis) * OP_COUNT + op) * P.Lmax * (4 * P.p);
+}
+
+struct WS {
+  double* t;
+  double* r;
+  double* partials;
+};
+
+size_t ws_need(const Plan& P) {
+  size_t nmax = std::max(P.N_e, P.N_h);
+  return (2 * nmax + 4 * size_t(partial_blocks()) + 16) * sizeof(double);
+}
+
+sgm_status ws_carve(const Plan& P, void* ws, size_t bytes, WS& w) {
+  if (!ws || !aligned8(ws)) return fail(SGM_E_INVALID_ARG, "workspace is NULL or misaligned");
+  if (bytes < ws_need(P)) return fail(SGM_E_INVALID_ARG, "workspace too small (see sgm_workspace_bytes)");
+  size_t nmax = std::max(P.N_e, P.N_h);
+  w.t = static_cast<double*>(ws);
+  w.r = w.t + nmax;
+  w.partials = w.r + nmax;
+  return SGM_OK;
+}
+
+int lines_per_cta(int L) {
+  // 64 lines of ~130 doubles = 67 KB of smem -> 3 CTAs per SM; 32 lines for long lines
+  return (size_t(64) * (L | 1) * sizeof(double) <= 150 * 1024) ? 64 : 32;
+}
+
+void comps_of(const Plan& P, int kind, const double* base, double* out[3]) {
+  for (int c = 0; c < 3; ++c) out[c] = const_cast<double*>(base) + comp_off(P, kind, c);
+}
+
+inline int own_or(int axis, int c, int own, int oth) { return axis == c ? own : oth; }
+
+cudaEvent_t ev_get(Plan& P) {
+  if (!P.ev_pool.empty()) {
+    cudaEvent_t e = static_cast<cudaEvent_t>(P.ev_pool.back());
+    P.ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Records CUDA events around one launch on its stream when profiling is enabled.
+struct ProfScope {
+  Plan& P;
+  cudaStream_t st;
+  int cls;
+  cudaEvent_t a = nullptr;
+  ProfScope(Plan& P_, int cls_, cudaStream_t st_) : P(P_), st(st_), cls(cls_) {
+    if (P.profiling) {
+      a = ev_get(P);
+      cudaEventRecord(a, st);
+    }
+  }
+  ~ProfScope() {
+    if (P.profiling) {
+      cudaEvent_t b = ev_get(P);
+      cudaEventRecord(b, st);
+      P.prof.push_back({cls, a, b});
+    }
+  }
+};
+
+// One axis pass over the 3 components of a form (kind 0: e/d shapes, 1: b/h shapes).
+void sweep_pass(const Plan& P, int kind, int axis, double* const in[3], double* const out[3], int op_own,
+                int op_oth, const double* scale, bool band, bool solve, int pro, const PrologueArgs* pro_args,
+                cudaStream_t st) {
+  SweepArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.ncomp = 3;
+  a.axis = axis;
+  int Lmax = 0;
+  for (int c = 0; c < 3; ++c) {
+    comp_shape(P, kind, c, a.comp[c].ext);
+    a.comp[c].in = in[c];
+    a.comp[c].out = out[c];
+    a.comp[c].tab = table(P, axis, own_or(axis, c, op_own, op_oth));
+    a.comp[c].scale = scale ? scale[c] : 1.0;
+    Lmax = std::max(Lmax, a.comp[c].ext[axis]);
+  }
+  a.nl = lines_per_cta(Lmax);
+  if (pro_args) a.pro = *pro_args;
+  launch_sweep(P.p, band, solve, pro, a, Lmax, st);
+}
+
+// y = (A_z (x) A_y (x) A_x) x per component with 3 sweeps x -> t -> t -> y (x == y allowed).
+void kron_pass3(const Plan& P, int kind, const double* x, double* y, double* t, int op_own, int op_oth,
+                const double* scale, bool band, bool solve, cudaStream_t st) {
+  double *X[3], *T[3], *Y[3];
+  comps_of(P, kind, x, X);
+  comps_of(P, kind, t, T);
+  comps_of(P, kind, y, Y);
+  sweep_pass(P, kind, 0, X, T, op_own, op_oth, nullptr, band, solve, PRO_NONE, nullptr, st);
+  sweep_pass(P, kind, 1, T, T, op_own, op_oth, nullptr, band, solve, PRO_NONE, nullptr, st);
+  sweep_pass(P, kind, 2, T, Y, op_own, op_oth, scale, band, solve, PRO_NONE, nullptr, st);
+}
+
+PrologueArgs make_pro(const Plan& P, int src_kind, const double* src, const double* jhat, const double* s_ptr,
+                      double dt) {
+  PrologueArgs pa;
+  std::memset(&pa, 0, sizeof(pa));
+  double* S[3];
+  comps_of(P, src_kind, src, S);
+  for (int c = 0; c < 3; ++c) {
+    pa.src[c] = S[c];
+    comp_shape(P, src_kind, c, pa.sext[c]);
+  }
+  if (jhat) {
+    double* J[3];
+    comps_of(P, 0, jhat, J);
+    for (int c = 0; c < 3; ++c) pa.jhat[c] = J[c];
+  }
+  pa.s_ptr = s_ptr;
+  pa.dt = dt;
+  return pa;
+}
+
+void hodge_args(const Plan& P, int which, const double* x, double* y, HodgeArgs& h) {
+  std::memset(&h, 0, sizeof(h));
+  int kind = (which == SGM_MASS_EPS) ? 0 : 1;
+  double *X[3], *Y[3];
+  comps_of(P, kind, x, X);
+  comps_of(P, kind, y, Y);
+  for (int c = 0; c < 3; ++c) {
+    h.x[c] = X[c];
+    h.y[c] = Y[c];
+    comp_shape(P, kind, c, h.ext[c]);
+    h.scale[c] = P.mass[which].scale[c];
+  }
+  h.W = P.mass[which].W_dev;
+  h.full = (P.mass[which].kind == HODGE_FULL) ? 1 : 0;
+  // own/other univariate spaces: dual 2-forms own Dp1 (2), other Dp2 (3);
+  // primal 2-forms own Sp (0), other Sp1 (1)   (sec. 4.1)
+  int own = (which == SGM_MASS_EPS) ? 2 : 0, oth = (which == SGM_MASS_EPS) ? 3 : 1;
+  h.basis = P.basis_dev;
+  h.first = P.first_dev;
+  for (int a = 0; a < 3; ++a) {
+    h.basis_off[a][0] = int(P.basis_off[a][own]);
+    h.basis_off[a][1] = int(P.basis_off[a][oth]);
+    h.first_off[a][0] = int(P.first_off[a][own]);
+    h.first_off[a][1] = int(P.first_off[a][oth]);
+    h.nel[a] = P.n[a];
+  }
+  h.Q = P.Q;
+}
+
+// y = M x for one 2-form mass (separable: Kronecker of 1D Grams; else sum factorisation)
+void mass_apply(const Plan& P, int which, const double* x, double* y, double* t, cudaStream_t st) {
+  int kind = (which == SGM_MASS_EPS) ? 0 : 1;
+  const MassData& M = P.mass[which];
+  if (M.kind == HODGE_SEPARABLE) {
+    int own = (which == SGM_MASS_EPS) ? OP_EPS_OWN : OP_MU_OWN;
+    int oth = (which == SGM_MASS_EPS) ? OP_EPS_OTH : OP_MU_OTH;
+    kron_pass3(P, kind, x, y, t, own, oth, M.scale, true, false, st);
+    return;
+  }
+  cudaMemsetAsync(y, 0, form_len(P, kind) * sizeof(double), st);
+  HodgeArgs h;
+  hodge_args(P, which, x, y, h);
+  launch_hodge_general(P.p, h, st);
+}
+
+sgm_status upload_basis(Plan& P) {
+  std::vector<double> vals_all;
+  std::vector<int> first_all;
+  for (int a = 0; a < 3; ++a)
+    for (int s = 0; s < 4; ++s) {
+      std::vector<double> v;
+      std::vector<int> f;
+      basis_values_1d(P.p, P.n[a], P.Q, s, v, f);
+      P.basis_off[a][s] = vals_all.size();
+      P.first_off[a][s] = first_all.size();
+      vals_all.insert(vals_all.end(), v.begin(), v.end());
+      first_all.insert(first_all.end(), f.begin(), f.end());
+    }
+  if (cudaMalloc(&P.basis_dev, vals_all.size() * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&P.first_dev, first_all.size() * sizeof(int)) != cudaSuccess)
+    return fail(SGM_E_NOMEM, "cudaMalloc failed for basis tables");
+  cudaMemcpy(P.basis_dev, vals_all.data(), vals_all.size() * sizeof(double), cudaMemcpyHostToDevice);
+  cudaMemcpy(P.first_dev, first_all.data(), first_all.size() * sizeof(int), cudaMemcpyHostToDevice);
+  return cuda_check(&P, "upload_basis");
+}
+
+sgm_status set_material_impl(Plan& P, int which, const double* values, double c) {
+  std::vector<double> W;
+  std::string err;
+  // host-only plans classify but do not build weights
+  if (P.device < 0) {
+    if (values) {
+      for (size_t i = 0; i < P.n_qp; ++i)
+        if (!(values[i] > 0.0) || !std::isfinite(values[i]))
+          return fail(SGM_E_MATERIAL, "material must be positive and finite at every quadrature point");
+    } else if (!(c > 0.0) || !std::isfinite(c)) {
+      return fail(SGM_E_MATERIAL, "material constant must be positive and finite");
+    }
+    MassData& M = P.mass[which];
+    M.const_material = (values == nullptr);
+    M.kind = P.affine_diag ? (values ? HODGE_SCALAR : HODGE_SEPARABLE) : HODGE_FULL;
+    return SGM_OK;
+  }
+  sgm_status st = build_mass(P, which, values, c, W, err);
+  if (st != SGM_OK) return fail(st, err);
+  MassData& M = P.mass[which];
+  if (M.W_dev) {
+    cudaFree(M.W_dev);
+    M.W_dev = nullptr;
+  }
+  if (!W.empty()) {
+    if (cudaMalloc(&M.W_dev, W.size() * sizeof(double)) != cudaSuccess)
+      return fail(SGM_E_NOMEM, "cudaMalloc failed for Hodge weights");
+    cudaMemcpy(M.W_dev, W.data(), W.size() * sizeof(double), cudaMemcpyHostToDevice);
+  }
+  return cuda_check(&P, "set_material");
+}
+
+sgm_status check_plan(sgm_plan plan, bool need_device) {
+  if (!plan) return fail(SGM_E_INVALID_ARG, "plan is NULL");
+  Plan* P = reinterpret_cast<Plan*>(plan);
+  if (need_device && P->device < 0) return fail(SGM_E_INVALID_ARG, "host-only plan cannot run device calls");
+  if (P->sticky_cuda_error) return fail(SGM_E_CUDA, "plan has a sticky CUDA error");
+  return SGM_OK;
+}
+
+inline Plan* PL(sgm_plan p) { return reinterpret_cast<Plan*>(p); }
+
+// one leapfrog step on device pointers (schedules of SURVEY 8(a) a1-a6)
+void step_once(Plan& P, double* d, double* e, double* b, double* h, const double* jhat, const double* s_ptr,
+               double dt, const WS& w, cudaStream_t st) {
+  double *D[3], *E[3], *B[3], *H[3], *T[3], *Rr[3];
+  comps_of(P, 0, d, D);
+  comps_of(P, 0, e, E);
+  comps_of(P, 1, b, B);
+  comps_of(P, 1, h, H);
+  for (int half = 0; half < 2; ++half) {
+    // eps half (kind 0): d <- d + dt (D~1 h - s j); e <- K1^{-1} M~2_{1/eps} d
+    // mu  half (kind 1): b <- b - dt D1 e;           h <- K~1^{-1} M2_{1/mu} b
+    const int kind = half;
+    const int mass = half == 0 ? SGM_MASS_EPS : SGM_MASS_MU;
+    const int pro = half == 0 ? PRO_AMPERE : PRO_FARADAY;
+    const int own = half == 0 ? OP_EPS_OWN : OP_MU_OWN, oth = half == 0 ? OP_EPS_OTH : OP_MU_OTH;
+    const int kx = half == 0 ? SGM_K_AMPERE_X : SGM_K_FARADAY_X;
+    const int ky = half == 0 ? SGM_K_EPS_Y : SGM_K_MU_Y, kz = half == 0 ? SGM_K_EPS_Z : SGM_K_MU_Z;
+    double** state = half == 0 ? D : B;
+    double** outv = half == 0 ? E : H;
+    PrologueArgs pa = half == 0 ? make_pro(P, 1, h, jhat, s_ptr, dt) : make_pro(P, 0, e, nullptr, nullptr, dt);
+    const MassData& M = P.mass[mass];
+    comps_of(P, kind, w.t, T);
+    if (M.kind == HODGE_SEPARABLE) {
+      { ProfScope ps(P, kx, st); sweep_pass(P, kind, 0, state, T, own, oth, nullptr, true, true, pro, &pa, st); }
+      { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, true, true, PRO_NONE, nullptr, st); }
+      { ProfScope ps(P, kz, st); sweep_pass(P, kind, 2, T, outv, own, oth, M.scale, true, true, PRO_NONE, nullptr, st); }
+    } else {
+      SweepArgs a;
+      std::memset(&a, 0, sizeof(a));
+      a.ncomp = 3;
+      for (int c = 0; c < 3; ++c) {
+        comp_shape(P, kind, c, a.comp[c].ext);
+        a.comp[c].in = state[c];
+      }
+      a.pro = pa;
+      { ProfScope ps(P, SGM_K_UPDATE, st); launch_update(pro, a, st); }
+      { ProfScope ps(P, SGM_K_HODGE_GENERAL, st); mass_apply(P, mass, state[0], w.r, w.t, st); }
+      comps_of(P, kind, w.r, Rr);
+      { ProfScope ps(P, SGM_K_SOLVE_X, st); sweep_pass(P, kind, 0, Rr, T, own, oth, nullptr, false, true, PRO_NONE, nullptr, st); }
+      { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, false, true, PRO_NONE, nullptr, st); }
+      { ProfScope ps(P, kz, st); sweep_pass(P, kind, 2, T, outv, own, oth, nullptr, false, true, PRO_NONE, nullptr, st); }
+    }
+  }
+}
+
+}  // namespace
+}  // namespace sgm
+
+using namespace sgm;
+
+extern "C" {
+
+const char* sgm_last_error(void) { return g_err.c_str(); }
+const char* sgm_version(void) { return "sgm 0.1 (sm_100a, fp64)"; }
+
+sgm_status sgm_plan_create(const sgm_plan_desc* desc, sgm_plan* out) {
+  if (!desc || !out) return fail(SGM_E_INVALID_ARG, "desc/out is NULL");
+  *out = nullptr;
+  const int p = desc->degree;
+  for (int a = 0; a < 3; ++a)
+    if (desc->n_el[a] < 1) return fail(SGM_E_INVALID_ARG, "n_el must be >= 1");
+  if (p < SGM_PMIN || p > SGM_PMAX) return fail(SGM_E_UNSUPPORTED, "degree outside the compiled range 2..4");
+  int Q = desc->quad_points == 0 ? p + 1 : desc->quad_points;
+  if (Q < p + 1 || Q > 8) return fail(SGM_E_INVALID_ARG, "quad_points must be 0 or in [p+1, 8]");
+  for (int a = 0; a < 3; ++a)
+    if (desc->n_el[a] + p - 1 > kMaxLine) return fail(SGM_E_UNSUPPORTED, "line length above 1024");
+  Plan* P = new (std::nothrow) Plan();
+  if (!P) return fail(SGM_E_NOMEM, "out of host memory");
+  P->p = p;
+  P->Q = Q;
+  P->device = desc->device;
+  std::string err;
+  for (int a = 0; a < 3; ++a) {
+    P->n[a] = desc->n_el[a];
+    build_axis(p, P->n[a], Q, P->ax[a], err);
+  }
+  P->N_e = form_len(*P, 0);
+  P->N_h = form_len(*P, 1);
+  if (desc->geom_ctrl) {
+    P->has_geom = true;
+    size_t nc = size_t(P->n[0] + p) * (P->n[1] + p) * (P->n[2] + p) * 3;
+    P->ctrl.assign(desc->geom_ctrl, desc->geom_ctrl + nc);
+  }
+  sgm_status st = build_tables(*P, err);
+  if (st == SGM_OK) st = build_geometry(*P, err);
+  if (st != SGM_OK) {
+    delete P;
+    return fail(st, err);
+  }
+  if (P->device >= 0) {
+    DeviceGuard g(P->device);
+    if (!g.ok) {
+      delete P;
+      return fail(SGM_E_CUDA, "cudaSetDevice failed");
+    }
+    size_t tb = P->tables_host.size() * sizeof(double);
+    if (cudaMalloc(&P->tables_dev, tb) != cudaSuccess) {
+      delete P;
+      return fail(SGM_E_NOMEM, "cudaMalloc failed for tables");
+    }
+    cudaMemcpy(P->tables_dev, P->tables_host.data(), tb, cudaMemcpyHostToDevice);
+    st = upload_basis(*P);
+    if (st != SGM_OK) {
+      sgm_plan_destroy(reinterpret_cast<sgm_plan>(P));
+      return st;
+    }
+  }
+  for (int m = 0; m < 2; ++m) {
+    DeviceGuard g(P->device >= 0 ? P->device : 0);
+    st = set_material_impl(*P, m, nullptr, 1.0);
+    if (st != SGM_OK) {
+      std::string e2 = g_err;
+      sgm_plan_destroy(reinterpret_cast<sgm_plan>(P));
+      return fail(st, e2);
+    }
+  }
+  *out = reinterpret_cast<sgm_plan>(P);
+  return SGM_OK;
+}
+
+sgm_status sgm_plan_destroy(sgm_plan plan) {
+  if (!plan) return SGM_OK;
+  Plan* P = PL(plan);
+  if (P->device >= 0) {
+    DeviceGuard g(P->device);
+    cudaFree(P->tables_dev);
+    cudaFree(P->basis_dev);
+    cudaFree(P->first_dev);
+    for (int m = 0; m < 2; ++m) cudaFree(P->mass[m].W_dev);
+    cudaFree(P->mirror);
+    for (auto& r : P->prof) {
+      cudaEventDestroy(static_cast<cudaEvent_t>(r.a));
+      cudaEventDestroy(static_cast<cudaEvent_t>(r.b));
+    }
+    for (void* e : P->ev_pool) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+  }
+  delete P;
+  return SGM_OK;
+}
+
+sgm_status sgm_plan_len(sgm_plan plan, sgm_form form, size_t* n) {
+  if (!plan || !n) return fail(SGM_E_INVALID_ARG, "NULL argument");
+  switch (form) {
+    case SGM_FORM_E: case SGM_FORM_D: *n = PL(plan)->N_e; return SGM_OK;
+    case SGM_FORM_B: case SGM_FORM_H: *n = PL(plan)->N_h; return SGM_OK;
+  }
+  return fail(SGM_E_INVALID_ARG, "bad form");
+}
+
+sgm_status sgm_plan_shape(sgm_plan plan, sgm_form form, int comp, int xyz[3]) {
+  if (!plan || !xyz || comp < 0 || comp > 2) return fail(SGM_E_INVALID_ARG, "bad argument");
+  if (form < SGM_FORM_E || form > SGM_FORM_H) return fail(SGM_E_INVALID_ARG, "bad form");
+  int kind = (form == SGM_FORM_E || form == SGM_FORM_D) ? 0 : 1;
+  comp_shape(*PL(plan), kind, comp, xyz);
+  return SGM_OK;
+}
+
+sgm_status sgm_plan_qp_count(sgm_plan plan, size_t* n_qp) {
+  if (!plan || !n_qp) return fail(SGM_E_INVALID_ARG, "NULL argument");
+  *n_qp = PL(plan)->n_qp;
+  return SGM_OK;
+}
+
+sgm_status sgm_plan_qp_coords(sgm_plan plan, double* host_xyz) {
+  if (!plan || !host_xyz) return fail(SGM_E_INVALID_ARG, "NULL argument");
+  qp_coords(*PL(plan), host_xyz);
+  return SGM_OK;
+}
+
+sgm_status sgm_plan_table(sgm_plan plan, sgm_table which, int axis, double* host_out, int* L) {
+  if (!plan || !L || axis < 0 || axis > 2) return fail(SGM_E_INVALID_ARG, "bad argument");
+  const Axis& X = PL(plan)->ax[axis];
+  const std::vector<double>* src = nullptr;
+  int n = 0;
+  switch (which) {
+    case SGM_TAB_G: src = &X.G; n = X.a; break;
+    case SGM_TAB_M: src = &X.M; n = X.b; break;
+    case SGM_TAB_GAMMA_B1: src = &X.GB1; n = X.b; break;
+    case SGM_TAB_GAMMA_C2: src = &X.GC2; n = X.a; break;
+    case SGM_TAB_GAMMA_BP: src = &X.GBp; n = X.a; break;
+    case SGM_TAB_GAMMA_C1: src = &X.GC1; n = X.b; break;
+    default: return fail(SGM_E_INVALID_ARG, "bad table");
+  }
+  *L = n;
+  if (host_out) std::memcpy(host_out, src->data(), src->size() * sizeof(double));
+  return SGM_OK;
+}
+
+sgm_status sgm_plan_hodge_separable(sgm_plan plan, sgm_mass mass, int* separable) {
+  if (!plan || !separable || (mass != SGM_MASS_EPS && mass != SGM_MASS_MU))
+    return fail(SGM_E_INVALID_ARG, "bad argument");
+  *separable = PL(plan)->mass[mass].kind == HODGE_SEPARABLE ? 1 : 0;
+  return SGM_OK;
+}
+
+sgm_status sgm_plan_set_material(sgm_plan plan, sgm_material which, const double* values, double c) {
+  sgm_status s = check_plan(plan, false);
+  if (s != SGM_OK) return s;
+  if (which != SGM_EPS && which != SGM_MU) return fail(SGM_E_INVALID_ARG, "bad material");
+  Plan* P = PL(plan);
+  if (P->device >= 0) {
+    DeviceGuard g(P->device);
+    cudaDeviceSynchronize();
+    return set_material_impl(*P, which, values, c);
+  }
+  return set_material_impl(*P, which, values, c);
+}
+
+sgm_status sgm_workspace_bytes(sgm_plan plan, size_t* bytes) {
+  if (!plan || !bytes) return fail(SGM_E_INVALID_ARG, "NULL argument");
+  *bytes = ws_need(*PL(plan));
+  return SGM_OK;
+}
+
+sgm_status sgm_plan_kernels_per_step(sgm_plan plan, int* n) {
+  if (!plan || !n) return fail(SGM_E_INVALID_ARG, "NULL argument");
+  int k = 0;
+  for (int m = 0; m < 2; ++m) k += (PL(plan)->mass[m].kind == HODGE_SEPARABLE) ? 3 : 5;
+  *n = k;
+  return SGM_OK;
+}
+
+sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h, const double* j_hat,
+                    const double* j_amp, double dt, int n_steps, void* workspace, size_t ws_bytes, void* stream) {
+  sgm_status s = check_plan(plan, true);
+  if (s != SGM_OK) return s;
+  Plan* P = PL(plan);
+  if (!d || !e || !b || !h || !aligned8(d) || !aligned8(e) || !aligned8(b) || !aligned8(h))
+    return fail(SGM_E_INVALID_ARG, "state pointers must be non-NULL and 8-byte aligned");
+  if ((j_hat && !aligned8(j_hat)) || (j_amp && !aligned8(j_amp))) return fail(SGM_E_INVALID_ARG, "misaligned source");
+  if (!std::isfinite(dt)) return fail(SGM_E_INVALID_ARG, "dt must be finite");
+  if (n_steps < 0) return fail(SGM_E_INVALID_ARG, "n_steps < 0");
+  if (d == e || d == b || d == h || e == b || e == h || b == h) return fail(SGM_E_INVALID_ARG, "state vectors alias");
+  WS w;
+  if ((s = ws_carve(*P, workspace, ws_bytes, w)) != SGM_OK) return s;
+  DeviceGuard g(P->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int k = 0; k < n_steps; ++k) step_once(*P, d, e, b, h, j_hat, j_amp ? j_amp + k : nullptr, dt, w, st);
+  return cuda_check(P, "sgm_step");
+}
+
+sgm_status sgm_step_host(sgm_plan plan, double* d, double* e, double* b, double* h, const double* j_hat,
+                         const double* j_amp, double dt, int n_steps, void* stream) {
+  sgm_status s = check_plan(plan, true);
+  if (s != SGM_OK) return s;
+  Plan* P = PL(plan);
+  if (!d || !e || !b || !h) return fail(SGM_E_INVALID_ARG, "NULL state");
+  if (n_steps < 0) return fail(SGM_E_INVALID_ARG, "n_steps < 0");
+  DeviceGuard g(P->device);
+  size_t ne = P->N_e, nh = P->N_h;
+  size_t wsb = ws_need(*P);
+  size_t need = (2 * ne + 2 * nh + ne + size_t(std::max(n_steps, 1))) * sizeof(double) + wsb + 64;
+  if (P->mirror_bytes < need) {
+    cudaFree(P->mirror);
+    P->mirror = nullptr;
+    P->mirror_bytes = 0;
+    if (cudaMalloc(&P->mirror, need) != cudaSuccess) return fail(SGM_E_NOMEM, "cudaMalloc failed for mirrors");
+    P->mirror_bytes = need;
+  }
+  double* md = P->mirror;
+  double* me = md + ne;
+  double* mb = me + ne;
+  double* mh = mb + nh;
+  double* mj = mh + nh;
+  double* ma = mj + ne;
+  void* ws = ma + std::max(n_steps, 1);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaMemcpyAsync(md, d, ne * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(me, e, ne * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(mb, b, nh * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaMemcpyAsync(mh, h, nh * sizeof(double), cudaMemcpyHostToDevice, st);
+  if (j_hat) cudaMemcpyAsync(mj, j_hat, ne * sizeof(double), cudaMemcpyHostToDevice, st);
+  if (j_amp) cudaMemcpyAsync(ma, j_amp, size_t(n_steps) * sizeof(double), cudaMemcpyHostToDevice, st);
+  s = sgm_step(plan, md, me, mb, mh, j_hat ? mj : nullptr, j_amp ? ma : nullptr, dt, n_steps, ws, wsb, stream);
+  if (s != SGM_OK) return s;
+  cudaMemcpyAsync(d, md, ne * sizeof(double), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(e, me, ne * sizeof(double), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(b, mb, nh * sizeof(double), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(h, mh, nh * sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check(P, "sgm_step_host");
+  return cuda_check(P, "sgm_step_host");
+}
+
+sgm_status sgm_kron_solve(sgm_plan plan, sgm_pairing which, int transpose, const double* rhs, double* x,
+                          void* workspace, size_t ws_bytes, void* stream) {
+  sgm_status s = check_plan(plan, true);
+  if (s != SGM_OK) return s;
+  Plan* P = PL(plan);
+  if (!rhs || !x || !aligned8(rhs) || !aligned8(x)) return fail(SGM_E_INVALID_ARG, "bad vector pointers");
+  if (which != SGM_K1 && which != SGM_KT1) return fail(SGM_E_INVALID_ARG, "bad pairing");
+  WS w;
+  if ((s = ws_carve(*P, workspace, ws_bytes, w)) != SGM_OK) return s;
+  DeviceGuard g(P->device);
+  // LU tables: K1 own Hat M, other Hat G; K1^T own M^T, other G^T;
+  //            K~1 own G^T, other M^T;   K~1^T own G, other M   (eqs. tensor_K, tensor_Ktilde)
+  int kind = (which == SGM_K1) ? 0 : 1;
+  int own, oth;
+  if (which == SGM_K1) { own = transpose ? OP_MU_OTH : OP_EPS_OWN; oth = transpose ? OP_MU_OWN : OP_EPS_OTH; }
+  else { own = transpose ? OP_EPS_OTH : OP_MU_OWN; oth = transpose ? OP_EPS_OWN : OP_MU_OTH; }
+  kron_pass3(*P, kind, rhs, x, w.t, own, oth, nullptr, false, true, static_cast<cudaStream_t>(stream));
+  return cuda_check(P, "sgm_kron_solve");
+}
+
+sgm_status sgm_pairing_apply(sgm_plan plan, sgm_pairing which, int transpose, const double* x, double* y,
+                             void* workspace, size_t ws_bytes, void* stream) {
+  sgm_status s = check_plan(plan, true);
+  if (s != SGM_OK) return s;
+  Plan* P = PL(plan);
+  if (!x || !y || x == y || !aligned8(x) || !aligned8(y)) return fail(SGM_E_INVALID_ARG, "bad vector pointers");
+  if (which != SGM_K1 && which != SGM_KT1) return fail(SGM_E_INVALID_ARG, "bad pairing");
+  WS w;
+  if ((s = ws_carve(*P, workspace, ws_bytes, w)) != SGM_OK) return s;
+  DeviceGuard g(P->device);
+  int kind = (which == SGM_K1) ? 0 : 1;
+  int own, oth;
+  if (which == SGM_K1) { own = transpose ? OP_APPLY_MT : OP_APPLY_M; oth = transpose ? OP_APPLY_GT : OP_APPLY_G; }
+  else { own = transpose ? OP_APPLY_G : OP_APPLY_GT; oth = transpose ? OP_APPLY_M : OP_APPLY_MT; }
+  kron_pass3(*P, kind, x, y, w.t, own, oth, nullptr, true, false, static_cast<cudaStream_t>(stream));
+  return cuda_check(P, "sgm_pairing_apply");
+}
+
+sgm_status sgm_hodge_apply(sgm_plan plan, sgm_mass which, const double* x, double* y, void* workspace,
+                           size_t ws_bytes, void* stream) {
+  sgm_status s = check_plan(plan, true);
+  if (s != SGM_OK) return s;
+  Plan* P = PL(plan);
+  if (!x || !y || x == y || !aligned8(x) || !aligned8(y)) return fail(SGM_E_INVALID_ARG, "bad vector pointers");
+  if (which != SGM_MASS_EPS && which != SGM_MASS_MU) return fail(SGM_E_INVALID_ARG, "bad mass");
+  WS w;
+  if ((s = ws_carve(*P, workspace, ws_bytes, w)) != SGM_OK) return s;
+  DeviceGuard g(P->device);
+  mass_apply(*P, which, x, y, w.t, static_cast<cudaStream_t>(stream));
+  return cuda_check(P, "sgm_hodge_apply");
+}
+
+sgm_status sgm_hodge_star(sgm_plan plan, sgm_mass which, const double* x, double* y, void* workspace,
+                          size_t ws_bytes, void* stream) {
+  sgm_status s = check_plan(plan, true);
+  if (s != SGM_OK) return s;
+  Plan* P = PL(plan);
+  if (!x || !y || x == y || !aligned8(x) || !aligned8(y)) return fail(SGM_E_INVALID_ARG, "bad vector pointers");
+  if (which != SGM_MASS_EPS && which != SGM_MASS_MU) return fail(SGM_E_INVALID_ARG, "bad mass");
+  WS w;
+  if ((s = ws_carve(*P, workspace, ws_bytes, w)) != SGM_OK) return s;
+  DeviceGuard g(P->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int kind = (which == SGM_MASS_EPS) ? 0 : 1;
+  int own = (which == SGM_MASS_EPS) ? OP_EPS_OWN : OP_MU_OWN;
+  int oth = (which == SGM_MASS_EPS) ? OP_EPS_OTH : OP_MU_OTH;
+  const MassData& M = P->mass[which];
+  if (M.kind == HODGE_SEPARABLE) {
+    kron_pass3(*P, kind, x, y, w.t, own, oth, M.scale, true, true, st);
+  } else {
+    mass_apply(*P, which, x, w.r, w.t, st);
+    kron_pass3(*P, kind, w.r, y, w.t, own, oth, nullptr, false, true, st);
+  }
+  return cuda_check(P, "sgm_hodge_star");
+}
+
+sgm_status sgm_curl(sgm_plan plan, sgm_curl_kind kind, const double* x, double* y, void* stream) {
+  sgm_status s = check_plan(plan, true);
+  if (s != SGM_OK) return s;
+  Plan* P = PL(plan);
+  if (!x || !y || x == y || !aligned8(x) || !aligned8(y)) return fail(SGM_E_INVALID_ARG, "bad vector pointers");
+  if (kind != SGM_CURL_PRIMAL && kind != SGM_CURL_DUAL) return fail(SGM_E_INVALID_ARG, "bad curl kind");
+  DeviceGuard g(P->device);
+  int skind = (kind == SGM_CURL_PRIMAL) ? 0 : 1;  // primal: e -> b ; dual: h -> d
+  int dkind = 1 - skind;
+  double *S[3], *Dd[3];
+  comps_of(*P, skind, x, S);
+  comps_of(*P, dkind, y, Dd);
+  int se[3][3], de[3][3];
+  for (int c = 0; c < 3; ++c) {
+    comp_shape(*P, skind, c, se[c]);
+    comp_shape(*P, dkind, c, de[c]);
+  }
+  const double* Sc[3] = {S[0], S[1], S[2]};
+  launch_curl(kind == SGM_CURL_DUAL ? 1 : 0, Sc, se, Dd, de, static_cast<cudaStream_t>(stream));
+  return cuda_check(P, "sgm_curl");
+}
+
+sgm_status sgm_energy(sgm_plan plan, const double* d, const double* e, const double* b, const double* h,
+                      double* out_dev, void* workspace, size_t ws_bytes, void* stream) {
+  sgm_status s = check_plan(plan, true);
+  if (s != SGM_OK) return s;
+  Plan* P = PL(plan);
+  if (!d || !e || !b || !h || !out_dev) return fail(SGM_E_INVALID_ARG, "NULL argument");
+  WS w;
+  if ((s = ws_carve(*P, workspace, ws_bytes, w)) != SGM_OK) return s;
+  DeviceGuard g(P->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // K1 e and K~1 h by banded Kronecker mat-vecs, then d.(K1 e) + b.(K~1 h)
+  kron_pass3(*P, 0, e, w.r, w.t, OP_APPLY_M, OP_APPLY_G, nullptr, true, false, st);
+  launch_dot_partials(d, w.r, P->N_e, w.partials, 0, st);
+  kron_pass3(*P, 1, h, w.r, w.t, OP_APPLY_GT, OP_APPLY_MT, nullptr, true, false, st);
+  launch_dot_partials(b, w.r, P->N_h, w.partials, 1, st);
+  launch_finalize_sum(w.partials, 2, 0.5, out_dev, st);
+  return cuda_check(P, "sgm_energy");
+}
+
+sgm_status sgm_gauss(sgm_plan plan, const double* d, const double* b, double* out_dev, void* workspace,
+                     size_t ws_bytes, void* stream) {
+  sgm_status s = check_plan(plan, true);
+  if (s != SGM_OK) return s;
+  Plan* P = PL(plan);
+  if (!d || !b || !out_dev) return fail(SGM_E_INVALID_ARG, "NULL argument");
+  WS w;
+  if ((s = ws_carve(*P, workspace, ws_bytes, w)) != SGM_OK) return s;
+  DeviceGuard g(P->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double *Dd[3], *Bb[3];
+  comps_of(*P, 0, d, Dd);
+  comps_of(*P, 1, b, Bb);
+  int de[3][3], be[3][3];
+  for (int c = 0; c < 3; ++c) {
+    comp_shape(*P, 0, c, de[c]);
+    comp_shape(*P, 1, c, be[c]);
+  }
+  const double* Dc[3] = {Dd[0], Dd[1], Dd[2]};
+  const double* Bc[3] = {Bb[0], Bb[1], Bb[2]};
+  launch_div_max(1, Dc, de, w.partials, 0, st);
+  launch_div_max(0, Bc, be, w.partials, 1, st);
+  launch_finalize_max(w.partials, 1, 2, out_dev, st);
+  return cuda_check(P, "sgm_gauss");
+}
+
+sgm_status sgm_check_source(sgm_plan plan, const double* j_hat, void* workspace, size_t ws_bytes, void* stream) {
+  sgm_status s = check_plan(plan, true);
+  if (s != SGM_OK) return s;
+  Plan* P = PL(plan);
+  if (!j_hat) return fail(SGM_E_INVALID_ARG, "NULL source");
+  WS w;
+  if ((s = ws_carve(*P, workspace, ws_bytes, w)) != SGM_OK) return s;
+  DeviceGuard g(P->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  double* J[3];
+  comps_of(*P, 0, j_hat, J);
+  int je[3][3];
+  for (int c = 0; c < 3; ++c) comp_shape(*P, 0, c, je[c]);
+  const double* Jc[3] = {J[0], J[1], J[2]};
+  launch_div_max(1, Jc, je, w.partials, 0, st);
+  launch_absmax(j_hat, P->N_e, w.partials, 1, st);
+  double* out = w.partials + 2 * partial_blocks();
+  launch_finalize_max(w.partials, 1, 2, out, st);
+  double hv[2] = {0, 0};
+  cudaMemcpyAsync(hv, out, 2 * sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (cudaStreamSynchronize(st) != cudaSuccess) return cuda_check(P, "sgm_check_source");
+  if (hv[0] > 1e-12 * hv[1])
+    return fail(SGM_E_SOURCE_DIVERGENCE, "||D~2 j||_inf = " + std::to_string(hv[0]) + " exceeds 1e-12 ||j||_inf");
+  return cuda_check(P, "sgm_check_source");
+}
+
+sgm_status sgm_plan_set_profiling(sgm_plan plan, int on) {
+  if (!plan) return fail(SGM_E_INVALID_ARG, "plan is NULL");
+  PL(plan)->profiling = (on != 0);
+  return SGM_OK;
+}
+
+sgm_status sgm_plan_profile(sgm_plan plan, double* ms, int* counts) {
+  if (!plan || !ms || !counts) return fail(SGM_E_INVALID_ARG, "NULL argument");
+  Plan* P = PL(plan);
+  for (int k = 0; k < SGM_K_CLASSES; ++k) {
+    ms[k] = 0.0;
+    counts[k] = 0;
+  }
+  if (P->device < 0) return SGM_OK;
+  DeviceGuard g(P->device);
+  for (auto& r : P->prof) {
+    cudaEvent_t a = static_cast<cudaEvent_t>(r.a), b = static_cast<cudaEvent_t>(r.b);
+    cudaEventSynchronize(b);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, a, b);
+    if (r.cls >= 0 && r.cls < SGM_K_CLASSES) {
+      ms[r.cls] += t;
+      counts[r.cls] += 1;
+    }
+    P->ev_pool.push_back(r.a);
+    P->ev_pool.push_back(r.b);
+  }
+  P->prof.clear();
+  return cuda_check(P, "sgm_plan_profile");
+}
+
+}  // extern "C"

@@ -1,0 +1,535 @@
+// Host-side plan setup: knots, Gauss rules, univariate bases, 1D pairing/Gram matrices,
+// no-pivot banded LU, geometry Jacobians and Hodge weights.  (Table 1 "setup" rows,
+// O(p^3 n) 1D assembly, O(p^2 n) factorisation; mass weights O(n^3 p^3).)
+// Nothing here runs per time step.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "sgm_internal.h"
+
+namespace sgm {
+
+namespace {
+
+// p-open uniform knot vector with n elements: p+1 zeros, k/n, p+1 ones.
+std::vector<double> open_knots(int p, int n) {
+  std::vector<double> U;
+  for (int i = 0; i <= p; ++i) U.push_back(0.0);
+  for (int k = 1; k < n; ++k) U.push_back(double(k) / n);
+  for (int i = 0; i <= p; ++i) U.push_back(1.0);
+  return U;
+}
+
+// Values of the q+1 B-splines of degree q that are non-zero on knot span s at x
+// (the standard triangular recurrence of de Boor / Cox).
+void basis_funs(const double* U, int s, double x, int q, double* N) {
+  double left[16], right[16];
+  N[0] = 1.0;
+  for (int j = 1; j <= q; ++j) {
+    left[j] = x - U[s + 1 - j];
+    right[j] = U[s + j] - x;
+    double saved = 0.0;
+    for (int r = 0; r < j; ++r) {
+      double temp = N[r] / (right[r + 1] + left[j - r]);
+      N[r] = saved + right[r + 1] * temp;
+      saved = left[j - r] * temp;
+    }
+    N[j] = saved;
+  }
+}
+
+// First derivatives of the q+1 degree-q B-splines non-zero on span s at x.
+void basis_ders(const double* U, int s, double x, int q, double* dN) {
+  if (q == 0) { dN[0] = 0.0; return; }
+  double Nm[16];
+  basis_funs(U, s, x, q - 1, Nm);  // B_{s-q+1 .. s, q-1}
+  for (int k = 0; k <= q; ++k) {
+    int i = s - q + k;
+    double v = 0.0;
+    // B_{i,q-1} is Nm[k-1] when i in [s-q+1, s]
+    if (k >= 1) {
+      double den = U[i + q] - U[i];
+      if (den > 0) v += q / den * Nm[k - 1];
+    }
+    if (k <= q - 1) {
+      double den = U[i + q + 1] - U[i + 1];
+      if (den > 0) v -= q / den * Nm[k];
+    }
+    dN[k] = v;
+  }
+}
+
+// Gauss-Legendre nodes/weights on [-1,1] by Newton iteration on P_Q.
+void gauss_legendre(int Q, std::vector<double>& x, std::vector<double>& w) {
+  x.assign(Q, 0.0);
+  w.assign(Q, 0.0);
+  const double pi = 3.14159265358979323846;
+  for (int i = 0; i < Q; ++i) {
+    double z = std::cos(pi * (i + 0.75) / (Q + 0.5));
+    double dp = 0.0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = 0.0;
+      for (int k = 1; k <= Q; ++k) {
+        double p2 = p1;
+        p1 = p0;
+        p0 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p2) / k;
+      }
+      dp = Q * (z * p0 - p1) / (z * z - 1.0);
+      double dz = p0 / dp;
+      z -= dz;
+      if (std::fabs(dz) < 1e-16) break;
+    }
+    // recompute derivative at the converged node
+    double p0 = 1.0, p1 = 0.0;
+    for (int k = 1; k <= Q; ++k) {
+      double p2 = p1;
+      p1 = p0;
+      p0 = ((2.0 * k - 1.0) * z * p1 - (k - 1.0) * p2) / k;
+    }
+    dp = Q * (z * p0 - p1) / (z * z - 1.0);
+    x[Q - 1 - i] = z;   // ascending
+    w[Q - 1 - i] = 2.0 / ((1.0 - z * z) * dp * dp);
+  }
+}
+
+}  // namespace
+
+// Per-element local values of one univariate space at the Q Gauss points of each element.
+// space: 0 = Sp (primal S_p B-splines, trimmed), 1 = Sp1 (primal S_{p-1}(Xi') CS),
+//        2 = Dp1 (dual S_{p-1}(Xi') B-splines), 3 = Dp2 (dual S_{p-2}(Xi'') CS).
+// vals[(e*Q + q)*(p+1) + k] is the value of local function k (global index first[e] + k)
+// on element e; local functions beyond the space's degree+1 have value 0.  For Sp, the
+// global index is the trimmed index (may be -1 or a for the removed end functions: value 0).
+void basis_values_1d(int p, int n, int Q, int space, std::vector<double>& vals, std::vector<int>& first) {
+  std::vector<double> U = open_knots(p, n);
+  std::vector<double> gx, gw;
+  gauss_legendre(Q, gx, gw);
+  const int nl = p + 1;
+  vals.assign(size_t(n) * Q * nl, 0.0);
+  first.assign(n, 0);
+  const double* U0 = U.data();
+  const double* U1 = U.data() + 1;  // Xi'
+  const double* U2 = U.data() + 2;  // Xi''
+  const int a = n + p - 2;
+  for (int e = 0; e < n; ++e) {
+    double xa = double(e) / n, xb = double(e + 1) / n;
+    for (int q = 0; q < Q; ++q) {
+      double x = xa + (gx[q] + 1.0) * 0.5 * (xb - xa);
+      double N[16];
+      double* out = &vals[(size_t(e) * Q + q) * nl];
+      if (space == 0) {
+        basis_funs(U0, p + e, x, p, N);  // globals e .. e+p of S_p
+        first[e] = e - 1;                 // trimmed index
+        for (int k = 0; k <= p; ++k) {
+          int t = e - 1 + k;
+          out[k] = (t >= 0 && t < a) ? N[k] : 0.0;
+        }
+      } else if (space == 1 || space == 2) {
+        basis_funs(U1, p - 1 + e, x, p - 1, N);  // globals e .. e+p-1
+        first[e] = e;
+        for (int k = 0; k < p; ++k) {
+          int i = e + k;
+          double sc = (space == 1) ? p / (U1[i + p] - U1[i]) : 1.0;  // CS scale (reading Z2)
+          out[k] = N[k] * sc;
+        }
+      } else {
+        basis_funs(U2, p - 2 + e, x, p - 2, N);  // globals e .. e+p-2
+        first[e] = e;
+        for (int k = 0; k < p - 1; ++k) {
+          int i = e + k;
+          double sc = (p - 1) / (U2[i + p - 1] - U2[i]);
+          out[k] = N[k] * sc;
+        }
+      }
+    }
+  }
+}
+
+namespace {
+
+int space_dim(int space, int p, int n) { return (space == 0 || space == 3) ? n + p - 2 : n + p - 1; }
+
+// Dense Gram of two univariate spaces with the exact (p+1)-point rule per element.
+std::vector<double> gram(int p, int n, int row_space, int col_space) {
+  const int Qe = p + 1;  // exact for degree <= 2p+1 (Gamma_B^p has degree 2p)
+  std::vector<double> gx, gw;
+  gauss_legendre(Qe, gx, gw);
+  std::vector<double> vr, vc;
+  std::vector<int> fr, fc;
+  basis_values_1d(p, n, Qe, row_space, vr, fr);
+  basis_values_1d(p, n, Qe, col_space, vc, fc);
+  int R = space_dim(row_space, p, n), C = space_dim(col_space, p, n);
+  std::vector<double> A(size_t(R) * C, 0.0);
+  const int nl = p + 1;
+  for (int e = 0; e < n; ++e) {
+    double h = 1.0 / n;
+    for (int q = 0; q < Qe; ++q) {
+      double w = gw[q] * 0.5 * h;
+      const double* r = &vr[(size_t(e) * Qe + q) * nl];
+      const double* c = &vc[(size_t(e) * Qe + q) * nl];
+      for (int i = 0; i < nl; ++i) {
+        int gi = fr[e] + i;
+        if (gi < 0 || gi >= R || r[i] == 0.0) continue;
+        for (int j = 0; j < nl; ++j) {
+          int gj = fc[e] + j;
+          if (gj < 0 || gj >= C || c[j] == 0.0) continue;
+          A[size_t(gi) * C + gj] += w * r[i] * c[j];
+        }
+      }
+    }
+  }
+  return A;
+}
+
+}  // namespace
+
+sgm_status build_axis(int p, int n, int Q, Axis& out, std::string& err) {
+  (void)err;
+  out.n = n;
+  out.a = n + p - 2;
+  out.b = n + p - 1;
+  out.G = gram(p, n, 3, 0);    // rows D'' (dual S_{p-2} CS), cols trimmed S_p
+  out.M = gram(p, n, 2, 1);    // rows B' (dual S_{p-1}), cols D' (primal S_{p-1} CS)
+  out.GB1 = gram(p, n, 2, 2);
+  out.GC2 = gram(p, n, 3, 3);
+  out.GBp = gram(p, n, 0, 0);
+  out.GC1 = gram(p, n, 1, 1);
+  std::vector<double> gx, gw;
+  gauss_legendre(Q, gx, gw);
+  out.xq.resize(size_t(n) * Q);
+  out.wq.resize(size_t(n) * Q);
+  for (int e = 0; e < n; ++e)
+    for (int q = 0; q < Q; ++q) {
+      double h = 1.0 / n;
+      out.xq[e * Q + q] = e * h + (gx[q] + 1.0) * 0.5 * h;
+      out.wq[e * Q + q] = gw[q] * 0.5 * h;
+    }
+  return SGM_OK;
+}
+
+// In-place no-pivot LU of a banded matrix (half-bandwidth m on both sides), stored dense.
+// Reading Z14: B-spline pairing matrices are totally positive compositions, so elimination
+// without pivoting exists and is stable; we still check pivots and the backward error.
+sgm_status banded_lu_nopivot(const std::vector<double>& A, int L, int m, std::vector<double>& LU,
+                             std::string& err) {
+  double amax = 0.0;
+  for (int i = 0; i < L; ++i)
+    for (int j = 0; j < L; ++j) {
+      double v = A[size_t(i) * L + j];
+      amax = std::max(amax, std::fabs(v));
+      if (std::abs(i - j) > m && v != 0.0) {
+        err = "1D matrix is not banded with half-bandwidth p-1";
+        return SGM_E_SINGULAR;
+      }
+    }
+  LU = A;
+  for (int k = 0; k < L; ++k) {
+    double piv = LU[size_t(k) * L + k];
+    if (!(std::fabs(piv) > 1e-14 * amax)) {
+      err = "zero pivot in no-pivot banded LU";
+      return SGM_E_SINGULAR;
+    }
+    for (int i = k + 1; i <= std::min(L - 1, k + m); ++i) {
+      double l = LU[size_t(i) * L + k] / piv;
+      LU[size_t(i) * L + k] = l;
+      for (int j = k + 1; j <= std::min(L - 1, k + m); ++j) LU[size_t(i) * L + j] -= l * LU[size_t(k) * L + j];
+    }
+  }
+  // backward error ||L U - A||_max / ||A||_max
+  double be = 0.0;
+  for (int i = 0; i < L; ++i)
+    for (int j = std::max(0, i - m); j <= std::min(L - 1, i + m); ++j) {
+      double s = 0.0;
+      for (int k = std::max(0, std::max(i, j) - m); k <= std::min(i, j); ++k) {
+        double l = (k == i) ? 1.0 : LU[size_t(i) * L + k];
+        double u = LU[size_t(k) * L + j];
+        if (k <= i && k <= j) s += l * u;
+      }
+      be = std::max(be, std::fabs(s - A[size_t(i) * L + j]));
+    }
+  if (be > 1e-13 * amax) {
+    err = "no-pivot banded LU backward error above 1e-13";
+    return SGM_E_SINGULAR;
+  }
+  return SGM_OK;
+}
+
+namespace {
+
+std::vector<double> transpose(const std::vector<double>& A, int L) {
+  std::vector<double> T(A.size());
+  for (int i = 0; i < L; ++i)
+    for (int j = 0; j < L; ++j) T[size_t(j) * L + i] = A[size_t(i) * L + j];
+  return T;
+}
+
+// Fill one table: rows of R = 4P doubles [band(2P+1) | lo(P-1) | upn(P-1) | dinv].
+sgm_status fill_table(double* T, int P, int L, const std::vector<double>* band,
+                      const std::vector<double>* lu_src, std::string& err) {
+  const int R = 4 * P;
+  for (int i = 0; i < L; ++i) {
+    double* row = T + size_t(i) * R;
+    for (int k = 0; k < R; ++k) row[k] = 0.0;
+    if (band) {
+      for (int k = -P; k <= P; ++k) {
+        int j = i + k;
+        if (j >= 0 && j < L) row[k + P] = (*band)[size_t(i) * L + j];
+      }
+    } else {
+      row[P] = 1.0;
+    }
+  }
+  if (lu_src) {
+    std::vector<double> LU;
+    sgm_status st = banded_lu_nopivot(*lu_src, L, P - 1, LU, err);
+    if (st != SGM_OK) return st;
+    for (int i = 0; i < L; ++i) {
+      double* row = T + size_t(i) * R;
+      double uii = LU[size_t(i) * L + i];
+      for (int k = 1; k <= P - 1; ++k) {
+        if (i - k >= 0) row[2 * P + 1 + (k - 1)] = LU[size_t(i) * L + (i - k)];
+        if (i + k < L) row[2 * P + 1 + (P - 1) + (k - 1)] = LU[size_t(i) * L + (i + k)] / uii;
+      }
+      row[4 * P - 1] = 1.0 / uii;
+    }
+  }
+  return SGM_OK;
+}
+
+}  // namespace
+
+sgm_status build_tables(Plan& P, std::string& err) {
+  const int p = P.p, R = 4 * p;
+  int Lmax = 0;
+  for (int a = 0; a < 3; ++a) Lmax = std::max(Lmax, P.ax[a].b);
+  P.Lmax = Lmax;
+  P.tables_host.assign(size_t(3) * OP_COUNT * Lmax * R, 0.0);
+  for (int a = 0; a < 3; ++a) {
+    const Axis& X = P.ax[a];
+    std::vector<double> GT = transpose(X.G, X.a), MT = transpose(X.M, X.b);
+    auto T = [&](int op) { return P.tables_host.data() + (size_t(a) * OP_COUNT + op) * Lmax * R; };
+    sgm_status st;
+    if ((st = fill_table(T(OP_EPS_OWN), p, X.b, &X.GB1, &X.M, err)) != SGM_OK) return st;
+    if ((st = fill_table(T(OP_EPS_OTH), p, X.a, &X.GC2, &X.G, err)) != SGM_OK) return st;
+    if ((st = fill_table(T(OP_MU_OWN), p, X.a, &X.GBp, &GT, err)) != SGM_OK) return st;
+    if ((st = fill_table(T(OP_MU_OTH), p, X.b, &X.GC1, &MT, err)) != SGM_OK) return st;
+    if ((st = fill_table(T(OP_APPLY_M), p, X.b, &X.M, nullptr, err)) != SGM_OK) return st;
+    if ((st = fill_table(T(OP_APPLY_G), p, X.a, &X.G, nullptr, err)) != SGM_OK) return st;
+    if ((st = fill_table(T(OP_APPLY_GT), p, X.a, &GT, nullptr, err)) != SGM_OK) return st;
+    if ((st = fill_table(T(OP_APPLY_MT), p, X.b, &MT, nullptr, err)) != SGM_OK) return st;
+  }
+  return SGM_OK;
+}
+
+// ---- geometry -------------------------------------------------------------------------------
+
+namespace {
+
+// Evaluate F and DF at every quadrature point of elements [ez] (element-major order) from the
+// spline control points.  DF[9] row-major: DF[i*3+j] = dF_i / dx^_j.
+struct GeoEval {
+  const Plan& P;
+  std::vector<double> v[3], d[3];  // per-axis S_p (untrimmed) values/derivs at qp: [n][Q][p+1]
+  explicit GeoEval(const Plan& P_) : P(P_) {
+    const int p = P.p, Q = P.Q;
+    std::vector<double> gx, gw;
+    gauss_legendre(Q, gx, gw);
+    for (int a = 0; a < 3; ++a) {
+      int n = P.n[a];
+      std::vector<double> U = open_knots(p, n);
+      v[a].assign(size_t(n) * Q * (p + 1), 0.0);
+      d[a].assign(size_t(n) * Q * (p + 1), 0.0);
+      for (int e = 0; e < n; ++e)
+        for (int q = 0; q < Q; ++q) {
+          double x = (e + (gx[q] + 1.0) * 0.5) / n;
+          basis_funs(U.data(), p + e, x, p, &v[a][(size_t(e) * Q + q) * (p + 1)]);
+          basis_ders(U.data(), p + e, x, p, &d[a][(size_t(e) * Q + q) * (p + 1)]);
+        }
+    }
+  }
+  // element (ex,ey,ez), point (qx,qy,qz)
+  void eval(int ex, int ey, int ez, int qx, int qy, int qz, double* F, double* DF) const {
+    const int p = P.p, Q = P.Q, nl = p + 1;
+    const int NX = P.n[0] + p, NY = P.n[1] + p;
+    const double* vx = &v[0][(size_t(ex) * Q + qx) * nl];
+    const double* vy = &v[1][(size_t(ey) * Q + qy) * nl];
+    const double* vz = &v[2][(size_t(ez) * Q + qz) * nl];
+    const double* dx = &d[0][(size_t(ex) * Q + qx) * nl];
+    const double* dy = &d[1][(size_t(ey) * Q + qy) * nl];
+    const double* dz = &d[2][(size_t(ez) * Q + qz) * nl];
+    for (int i = 0; i < 3; ++i) F[i] = 0.0;
+    for (int i = 0; i < 9; ++i) DF[i] = 0.0;
+    for (int k = 0; k < nl; ++k)
+      for (int j = 0; j < nl; ++j)
+        for (int i = 0; i < nl; ++i) {
+          const double* c = &P.ctrl[((size_t(ez + k) * NY + (ey + j)) * NX + (ex + i)) * 3];
+          double w0 = vx[i] * vy[j] * vz[k];
+          double wx = dx[i] * vy[j] * vz[k];
+          double wy = vx[i] * dy[j] * vz[k];
+          double wz = vx[i] * vy[j] * dz[k];
+          for (int r = 0; r < 3; ++r) {
+            F[r] += c[r] * w0;
+            DF[r * 3 + 0] += c[r] * wx;
+            DF[r * 3 + 1] += c[r] * wy;
+            DF[r * 3 + 2] += c[r] * wz;
+          }
+        }
+  }
+};
+
+inline double det3(const double* A) {
+  return A[0] * (A[4] * A[8] - A[5] * A[7]) - A[1] * (A[3] * A[8] - A[5] * A[6]) +
+         A[2] * (A[3] * A[7] - A[4] * A[6]);
+}
+
+template <class Fn>
+void for_each_qp(const Plan& P, Fn fn) {
+  const int Q = P.Q;
+  const int nx = P.n[0], ny = P.n[1], nz = P.n[2];
+#pragma omp parallel for schedule(static)
+  for (int ez = 0; ez < nz; ++ez)
+    for (int ey = 0; ey < ny; ++ey)
+      for (int ex = 0; ex < nx; ++ex)
+        for (int qz = 0; qz < Q; ++qz)
+          for (int qy = 0; qy < Q; ++qy)
+            for (int qx = 0; qx < Q; ++qx) {
+              size_t idx = ((((size_t(ez) * ny + ey) * nx + ex) * Q + qz) * Q + qy) * Q + qx;
+              fn(idx, ex, ey, ez, qx, qy, qz);
+            }
+}
+
+}  // namespace
+
+sgm_status build_geometry(Plan& P, std::string& err) {
+  P.n_qp = size_t(P.n[0]) * P.n[1] * P.n[2] * P.Q * P.Q * P.Q;
+  if (!P.has_geom) {
+    P.affine_diag = true;
+    P.L_aff[0] = P.L_aff[1] = P.L_aff[2] = 1.0;
+    return SGM_OK;
+  }
+  GeoEval G(P);
+  // reference DF at the first point for the affine-diagonal test
+  double F0[3], D0[9];
+  G.eval(0, 0, 0, 0, 0, 0, F0, D0);
+  int bad = 0, nonaff = 0;
+  const double scale = std::fabs(D0[0]) + std::fabs(D0[4]) + std::fabs(D0[8]);
+  for_each_qp(P, [&](size_t, int ex, int ey, int ez, int qx, int qy, int qz) {
+    double F[3], D[9];
+    G.eval(ex, ey, ez, qx, qy, qz, F, D);
+    double dt = det3(D);
+    if (!(dt > 0.0) || !std::isfinite(dt)) {
+#pragma omp atomic
+      bad++;
+    }
+    bool aff = true;
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) {
+        double ref = (i == j) ? D0[i * 3 + j] : 0.0;
+        if (std::fabs(D[i * 3 + j] - ref) > 1e-13 * scale) aff = false;
+      }
+    if (!aff) {
+#pragma omp atomic
+      nonaff++;
+    }
+  });
+  if (bad) {
+    err = "det DF <= 0 or non-finite at " + std::to_string(bad) + " quadrature points";
+    return SGM_E_GEOMETRY;
+  }
+  P.affine_diag = (nonaff == 0);
+  if (P.affine_diag) {
+    P.L_aff[0] = D0[0];
+    P.L_aff[1] = D0[4];
+    P.L_aff[2] = D0[8];
+  }
+  return SGM_OK;
+}
+
+void qp_coords(const Plan& P, double* xyz) {
+  if (!P.has_geom) {
+    for_each_qp(P, [&](size_t idx, int ex, int ey, int ez, int qx, int qy, int qz) {
+      xyz[idx * 3 + 0] = P.ax[0].xq[ex * P.Q + qx];
+      xyz[idx * 3 + 1] = P.ax[1].xq[ey * P.Q + qy];
+      xyz[idx * 3 + 2] = P.ax[2].xq[ez * P.Q + qz];
+    });
+    return;
+  }
+  GeoEval G(P);
+  for_each_qp(P, [&](size_t idx, int ex, int ey, int ez, int qx, int qy, int qz) {
+    double F[3], D[9];
+    G.eval(ex, ey, ez, qx, qy, qz, F, D);
+    xyz[idx * 3 + 0] = F[0];
+    xyz[idx * 3 + 1] = F[1];
+    xyz[idx * 3 + 2] = F[2];
+  });
+}
+
+// Hodge weights for one material (the 2-form Piola pull-back gives
+// int gamma eta.omega dx = int gamma eta^ (DF^T DF / det DF) omega^ dx^):
+//   SEPARABLE: constant material, affine-diagonal F -> per-component scale only
+//   SCALAR   : variable material, affine-diagonal F -> W(q) = w_q / material(q), scale_c
+//   FULL     : general F -> W6(q) = w_q / material(q) * (DF^T DF)/det (xx,yy,zz,xy,xz,yz)
+sgm_status build_mass(Plan& P, int which, const double* values, double c, std::vector<double>& W,
+                      std::string& err) {
+  MassData& M = P.mass[which];
+  W.clear();
+  if (!values) {
+    if (!(c > 0.0) || !std::isfinite(c)) {
+      err = "material constant must be positive and finite";
+      return SGM_E_MATERIAL;
+    }
+  } else {
+    size_t badm = 0;
+#pragma omp parallel for reduction(+ : badm)
+    for (long long i = 0; i < (long long)P.n_qp; ++i)
+      if (!(values[i] > 0.0) || !std::isfinite(values[i])) badm++;
+    if (badm) {
+      err = "material must be positive and finite at every quadrature point";
+      return SGM_E_MATERIAL;
+    }
+  }
+  M.const_material = (values == nullptr);
+  M.material_c = c;
+  const double Lx = P.L_aff[0], Ly = P.L_aff[1], Lz = P.L_aff[2];
+  const double detL = Lx * Ly * Lz;
+  if (P.affine_diag) {
+    double s[3] = {Lx * Lx / detL, Ly * Ly / detL, Lz * Lz / detL};
+    if (M.const_material) {
+      M.kind = HODGE_SEPARABLE;
+      for (int k = 0; k < 3; ++k) M.scale[k] = s[k] / c;
+      return SGM_OK;
+    }
+    M.kind = HODGE_SCALAR;
+    for (int k = 0; k < 3; ++k) M.scale[k] = s[k];
+    W.resize(P.n_qp);
+    for_each_qp(P, [&](size_t idx, int ex, int ey, int ez, int qx, int qy, int qz) {
+      double w = P.ax[0].wq[ex * P.Q + qx] * P.ax[1].wq[ey * P.Q + qy] * P.ax[2].wq[ez * P.Q + qz];
+      W[idx] = w / values[idx];
+    });
+    return SGM_OK;
+  }
+  M.kind = HODGE_FULL;
+  for (int k = 0; k < 3; ++k) M.scale[k] = 1.0;
+  W.resize(P.n_qp * 6);
+  GeoEval G(P);
+  for_each_qp(P, [&](size_t idx, int ex, int ey, int ez, int qx, int qy, int qz) {
+    double F[3], D[9];
+    G.eval(ex, ey, ez, qx, qy, qz, F, D);
+    double dt = det3(D);
+    double w = P.ax[0].wq[ex * P.Q + qx] * P.ax[1].wq[ey * P.Q + qy] * P.ax[2].wq[ez * P.Q + qz];
+    double g = w / (values ? values[idx] : c) / dt;
+    // (DF^T DF)_{ij} = sum_r DF[r][i] DF[r][j]
+    auto m = [&](int i, int j) { return D[0 * 3 + i] * D[0 * 3 + j] + D[1 * 3 + i] * D[1 * 3 + j] + D[2 * 3 + i] * D[2 * 3 + j]; };
+    double* o = &W[idx * 6];
+    o[0] = g * m(0, 0);
+    o[1] = g * m(1, 1);
+    o[2] = g * m(2, 2);
+    o[3] = g * m(0, 1);
+    o[4] = g * m(0, 2);
+    o[5] = g * m(1, 2);
+  });
+  return SGM_OK;
+}
+
+}  // namespace sgm

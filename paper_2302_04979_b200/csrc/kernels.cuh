@@ -1,0 +1,71 @@
+// Kernel parameter blocks and launcher declarations (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace sgm {
+
+constexpr int kMaxLine = 1024;
+
+// One component handled by a line sweep along `axis`.
+struct SweepComp {
+  double* in;         // input component array [z][y][x] (updated in place by a prologue)
+  double* out;        // output component array (may equal in)
+  const double* tab;  // line-operator table (rows of 4P doubles), see sgm_internal.h
+  int ext[3];         // component extents (x, y, z)
+  double scale;       // multiplies the stored result
+};
+
+// Element-wise prologue fused into the x-sweep (or run standalone):
+//   AMPERE : in[c] += dt * ((D~1 src)_c - s * jhat[c])   (eq. discrete2_ampere)
+//   FARADAY: in[c] -= dt * (D1 src)_c                    (eq. discrete2_faraday)
+// The updated state is written back to in[c] and fed to the sweep.
+enum Prologue { PRO_NONE = 0, PRO_AMPERE = 1, PRO_FARADAY = 2 };
+
+struct PrologueArgs {
+  const double* src[3];  // h components (AMPERE) or e components (FARADAY)
+  int sext[3][3];        // their extents
+  const double* jhat[3]; // AMPERE source components or null
+  const double* s_ptr;   // device pointer to the amplitude s_k, or null (-> 1)
+  double dt;
+};
+
+struct SweepArgs {
+  SweepComp comp[3];
+  int ncomp;
+  int axis;       // 0 = x (contiguous lines), 1 = y, 2 = z
+  int nl;         // lines per CTA (= blockDim.x)
+  PrologueArgs pro;
+};
+
+// General (non-separable) Hodge apply y = M x by sum factorisation per element.
+struct HodgeArgs {
+  const double* x[3];
+  double* y[3];
+  int ext[3][3];
+  const double* W;       // SCALAR: 1/qp ; FULL: 6/qp
+  int full;              // 0 scalar, 1 full
+  double scale[3];
+  const double* basis;   // per-axis basis tables (see api.cu)
+  int basis_off[3][2];   // [axis][own/other] offsets (doubles) of [n][Q][p+1] value blocks
+  const int* first;      // per-axis first-index tables
+  int first_off[3][2];
+  int nel[3];
+  int Q;
+};
+
+void launch_sweep(int p, bool band, bool solve, int pro, const SweepArgs& a, int smem_L, cudaStream_t st);
+void launch_update(int pro, const SweepArgs& a, cudaStream_t st);
+void launch_curl(int kind, const double* const src[3], const int sext[3][3], double* const dst[3],
+                 const int dext[3][3], cudaStream_t st);
+void launch_hodge_general(int p, const HodgeArgs& a, cudaStream_t st);
+void launch_dot_partials(const double* x, const double* y, size_t n, double* partials, int slot, cudaStream_t st);
+void launch_finalize_sum(const double* partials, int nslots, double scale, double* out, cudaStream_t st);
+void launch_div_max(int kind, const double* const src[3], const int sext[3][3], double* partials,
+                    int slot, cudaStream_t st);
+void launch_absmax(const double* x, size_t n, double* partials, int slot, cudaStream_t st);
+void launch_finalize_max(const double* partials, int nslots_each, int ngroups, double* out, cudaStream_t st);
+int partial_blocks();
+
+}  // namespace sgm

@@ -1,0 +1,109 @@
+// Internal declarations of the sgm library (plan layout, table layout, kernel launchers).
+// Not part of the C ABI (see include/sgm.h).
+#pragma once
+
+#include <cstddef>
+#include <string>
+#include <vector>
+
+#include "../../include/sgm.h"
+
+namespace sgm {
+
+// Univariate factors of one axis.
+struct Axis {
+  int n = 0;   // elements
+  int a = 0;   // n + p - 2 : trimmed S_p and S_{p-2}(Xi'')
+  int b = 0;   // n + p - 1 : S_{p-1}(Xi')
+  // dense row-major 1D matrices
+  std::vector<double> G;    // Hat{G}  a x a : int D''_k B_c
+  std::vector<double> M;    // Hat{M}  b x b : int B'_j D'_k
+  std::vector<double> GB1;  // Gamma_B^{p-1}  b x b
+  std::vector<double> GC2;  // Gamma_C^{p-2}  a x a
+  std::vector<double> GBp;  // Gamma_B^{p}    a x a
+  std::vector<double> GC1;  // Gamma_C^{p-1}  b x b
+  // Gauss points / weights of the Q-point rule, element by element
+  std::vector<double> xq, wq;
+};
+
+// Device line-operator tables: per (axis, op), rows of R = 4P doubles:
+//   [ band(2P+1) | lo(P-1) | upn(P-1) | dinv ]
+// band[k] = A[i][i+k-P] (a banded mat-vec, mass or pairing), lo[k-1] = L_{i,i-k},
+// upn[k-1] = U_{i,i+k}/U_{ii}, dinv = 1/U_{ii}: no-pivot banded LU (reading Z14).
+enum Op {
+  OP_EPS_OWN = 0,  // band Gamma_B^{p-1} (b), LU(Hat M)
+  OP_EPS_OTH = 1,  // band Gamma_C^{p-2} (a), LU(Hat G)
+  OP_MU_OWN = 2,   // band Gamma_B^{p}   (a), LU(Hat G^T)
+  OP_MU_OTH = 3,   // band Gamma_C^{p-1} (b), LU(Hat M^T)
+  OP_APPLY_M = 4,  // band Hat M   (b)
+  OP_APPLY_G = 5,  // band Hat G   (a)
+  OP_APPLY_GT = 6, // band Hat G^T (a)
+  OP_APPLY_MT = 7, // band Hat M^T (b)
+  OP_COUNT = 8
+};
+
+enum HodgeKind { HODGE_SEPARABLE = 0, HODGE_SCALAR = 1, HODGE_FULL = 2 };
+
+struct MassData {
+  HodgeKind kind = HODGE_SEPARABLE;
+  double scale[3] = {1.0, 1.0, 1.0};   // per-component constant (separable / scalar kinds)
+  double* W_dev = nullptr;             // SCALAR: 1 per qp; FULL: 6 per qp (xx,yy,zz,xy,xz,yz)
+  bool const_material = true;
+  double material_c = 1.0;             // constant material value (eps or mu)
+};
+
+struct Plan {
+  int p = 0;
+  int Q = 0;
+  int device = -1;
+  int n[3] = {0, 0, 0};
+  Axis ax[3];
+  bool has_geom = false;
+  std::vector<double> ctrl;           // (nz+p)(ny+p)(nx+p)*3
+  bool affine_diag = true;            // DF constant diagonal
+  double L_aff[3] = {1, 1, 1};        // diagonal of DF if affine_diag
+  size_t n_qp = 0;
+  MassData mass[2];                   // [SGM_MASS_EPS], [SGM_MASS_MU]
+  // device
+  double* tables_dev = nullptr;       // [3][OP_COUNT][Lmax][4P]
+  int Lmax = 0;
+  double* basis_dev = nullptr;        // general Hodge: per-axis basis values at qp [n][Q][p+1]
+  int* first_dev = nullptr;           // per-axis first local global index per element [n]
+  size_t basis_off[3][4] = {};        // offsets (doubles) into basis_dev per axis and space
+  size_t first_off[3][4] = {};        // offsets (ints) into first_dev per axis and space
+  // plan-owned mirrors for sgm_step_host
+  double* mirror = nullptr;
+  size_t mirror_bytes = 0;
+  std::vector<double> tables_host;
+  bool sticky_cuda_error = false;
+  size_t N_e = 0, N_h = 0;
+  // optional per-kernel event timing (sgm_plan_set_profiling)
+  bool profiling = false;
+  std::vector<void*> ev_pool;                        // cudaEvent_t
+  struct ProfRec { int cls; void* a; void* b; };
+  std::vector<ProfRec> prof;
+};
+
+// host setup (host_setup.cpp)
+sgm_status build_axis(int p, int n, int Q, Axis& out, std::string& err);
+sgm_status banded_lu_nopivot(const std::vector<double>& A, int L, int m, std::vector<double>& LU,
+                             std::string& err);
+sgm_status build_tables(Plan& P, std::string& err);
+sgm_status build_geometry(Plan& P, std::string& err);
+void qp_coords(const Plan& P, double* xyz);
+sgm_status build_mass(Plan& P, int which, const double* values, double c, std::vector<double>& W,
+                      std::string& err);
+void basis_values_1d(int p, int n, int Q, int space, std::vector<double>& vals, std::vector<int>& first);
+
+// component extents helpers: form kind 0 = E-like (e, d), 1 = B-like (b, h)
+inline void comp_shape(const Plan& P, int kind, int c, int xyz[3]) {
+  for (int a = 0; a < 3; ++a) {
+    bool own = (a == c);
+    if (kind == 0) xyz[a] = own ? P.ax[a].b : P.ax[a].a;
+    else xyz[a] = own ? P.ax[a].a : P.ax[a].b;
+  }
+}
+
+void set_error(const std::string& s);
+
+}  // namespace sgm

@@ -1,0 +1,105 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol include/sgm.h declares,
+and the host setup logic (1D tables, shapes, quadrature coordinates, classification, error
+codes) agrees with the oracle.  No kernel is launched here."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2302_04979_b200 as S
+from oracle import forms
+from oracle import workloads as W
+from oracle.splines import gram_1d
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared():
+    txt = open(os.path.join(ROOT, "include", "sgm.h")).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(sgm_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_library_exports_every_declared_symbol():
+    names = _declared()
+    assert len(names) >= 20
+    lib = ctypes.CDLL(S.LIB_PATH)
+    for nm in names:
+        assert hasattr(lib, nm), nm
+        assert nm in S.EXPORTED, nm
+    assert S.sgm_version().decode().startswith("sgm")
+
+
+@pytest.mark.parametrize("p,n", [(2, 4), (3, (5, 3, 4)), (4, 7)])
+def test_host_tables_match_oracle(p, n):
+    pl = S.Plan(n, p, device=-1)
+    n3 = forms._n3(n)
+    spaces = [("Dp2", "Sp"), ("Dp1", "Sp1"), ("Dp1", "Dp1"), ("Dp2", "Dp2"), ("Sp", "Sp"), ("Sp1", "Sp1")]
+    for ax in range(3):
+        for which, (r, c) in enumerate(spaces):
+            B = gram_1d(r, c, p, n3[ax])
+            assert np.abs(pl.table(which, ax) - B).max() < 1e-14 * max(1.0, np.abs(B).max())
+
+
+@pytest.mark.parametrize("p,n", [(2, 4), (3, (5, 3, 4))])
+def test_shapes_and_lengths(p, n):
+    pl = S.Plan(n, p, device=-1)
+    assert pl.N_e == forms.form_dim("primal", 1, p, n) == forms.form_dim("dual", 2, p, n)
+    assert pl.N_h == forms.form_dim("dual", 1, p, n) == forms.form_dim("primal", 2, p, n)
+    for c in range(3):
+        assert pl.shape(S.FORM_E, c) == forms.component_shapes("primal", 1, p, n)[c]
+        assert pl.shape(S.FORM_D, c) == forms.component_shapes("dual", 2, p, n)[c]
+        assert pl.shape(S.FORM_B, c) == forms.component_shapes("primal", 2, p, n)[c]
+        assert pl.shape(S.FORM_H, c) == forms.component_shapes("dual", 1, p, n)[c]
+
+
+def test_qp_coords_identity_and_curved():
+    p, n = 3, (3, 2, 4)
+    pl = S.Plan(n, p, device=-1)
+    X = W.physical_points(p, n)
+    Xel = np.stack([W.grid_to_elem(X[..., i], n, p + 1) for i in range(3)], -1)
+    assert np.abs(pl.qp_coords() - Xel).max() < 1e-15
+    ctrl = W.interpolate_map(p, n, W.c3_map)
+    pl2 = S.Plan(n, p, geom_ctrl=ctrl, device=-1)
+    X2 = W.physical_points(p, n, ctrl)
+    X2el = np.stack([W.grid_to_elem(X2[..., i], n, p + 1) for i in range(3)], -1)
+    assert np.abs(pl2.qp_coords() - X2el).max() < 1e-14
+    assert not pl2.separable(S.MASS_EPS)
+    assert pl.separable(S.MASS_EPS) and pl.separable(S.MASS_MU)
+
+
+def test_classification_affine_and_material():
+    from oracle.assemble import identity_ctrl
+    p, n = 2, 3
+    ctrl = identity_ctrl(p, n) * np.array([2.0, 0.5, 1.5])
+    pl = S.Plan(n, p, geom_ctrl=ctrl, device=-1)
+    assert pl.separable(S.MASS_EPS)        # axis-aligned affine + constant material
+    pl.set_material(S.EPS, np.full(pl.qp_count(), 2.0))
+    assert not pl.separable(S.MASS_EPS)    # variable material -> quadrature weights
+    assert pl.separable(S.MASS_MU)
+
+
+def test_error_codes():
+    desc = S.sgm_plan_desc((ctypes.c_int * 3)(4, 4, 4), 1, None, 0, -1)
+    h = ctypes.c_void_p()
+    assert S.sgm_plan_create(ctypes.byref(desc), ctypes.byref(h)) == 2      # p < 2: unsupported
+    desc = S.sgm_plan_desc((ctypes.c_int * 3)(0, 4, 4), 3, None, 0, -1)
+    assert S.sgm_plan_create(ctypes.byref(desc), ctypes.byref(h)) == 1      # n_el < 1
+    desc = S.sgm_plan_desc((ctypes.c_int * 3)(4, 4, 4), 3, None, 2, -1)
+    assert S.sgm_plan_create(ctypes.byref(desc), ctypes.byref(h)) == 1      # Q < p+1
+    # inverted geometry: det DF < 0
+    from oracle.assemble import identity_ctrl
+    ctrl = identity_ctrl(2, 3).copy()
+    ctrl[..., 0] *= -1.0
+    with pytest.raises(S.SgmError) as ei:
+        S.Plan(3, 2, geom_ctrl=ctrl, device=-1)
+    assert ei.value.status == 3
+    pl = S.Plan(3, 2, device=-1)
+    with pytest.raises(S.SgmError) as ei:
+        pl.set_material(S.EPS, -np.ones(pl.qp_count()))
+    # host-only plans classify but cannot validate device work; material validation happens
+    # on device plans (build_mass); device calls on a host-only plan are rejected:
+    rc = S.sgm_step(pl.h, 8, 16, 24, 32, None, None, 0.1, 1, 64, 1 << 20, None)
+    assert rc == 1

@@ -1,0 +1,246 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle, element by element on the
+same seeded inputs.  Tolerances (north_star / DESIGN.md): relative L2 per vector <= 1e-11 after one
+step and <= 1e-9 after 100 steps; standalone kernels <= min(1e-11, 20 eps cond) where cond is the
+condition number bound of the Kronecker block (product of the 1D condition numbers); integer
+stencils (curls) bit-exact."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_2302_04979_b200 as S  # noqa: E402
+from oracle import forms  # noqa: E402
+from oracle import workloads as W  # noqa: E402
+from oracle.structured import TierB, curl_primal, curl_dual  # noqa: E402
+from conftest import rel  # noqa: E402
+
+EPS = np.finfo(float).eps
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def kron_cond(tb):
+    cg = max(np.linalg.cond(G) for G in tb.G)
+    cm = max(np.linalg.cond(M) for M in tb.M)
+    return max(cg, cm) ** 3
+
+
+def solve_tol(tb):
+    return min(1e-11, 20 * EPS * kron_cond(tb))
+
+
+SMALL = [(2, 5), (3, (9, 7, 6)), (4, 6), (2, (1, 2, 3))]
+MEDIUM = [(3, 32), (2, 64), (4, 33)]
+
+
+@pytest.mark.parametrize("p,n", SMALL + MEDIUM)
+def test_kron_solve(p, n):
+    pl = S.Plan(n, p)
+    tb = TierB(p, n)
+    g = np.random.default_rng(5)
+    for which, N, split, solve in ((S.K1, tb.N_e, tb.split_e, tb.solve_K1), (S.KT1, tb.N_h, tb.split_h, tb.solve_Kt1)):
+        for T in (False, True):
+            r = g.standard_normal(N)
+            x = torch.empty(N, dtype=torch.float64, device="cuda")
+            pl.kron_solve(which, dev(r), x, transpose=T)
+            ref = forms.join(solve(split(r), T=T))
+            assert rel(host(x), ref) < solve_tol(tb), (which, T)
+            # in place (rhs == x)
+            xr = dev(r)
+            pl.kron_solve(which, xr, xr, transpose=T)
+            assert rel(host(xr), ref) < solve_tol(tb)
+
+
+@pytest.mark.parametrize("p,n", SMALL + [(3, 20)])
+def test_curls_bit_exact(p, n):
+    pl = S.Plan(n, p)
+    tb = TierB(p, n)
+    g = np.random.default_rng(6)
+    e = g.standard_normal(tb.N_e)
+    h = g.standard_normal(tb.N_h)
+    y = torch.empty(tb.N_h, dtype=torch.float64, device="cuda")
+    pl.curl(S.CURL_PRIMAL, dev(e), y)
+    assert np.array_equal(host(y), forms.join(curl_primal(tb.split_e(e))))
+    y2 = torch.empty(tb.N_e, dtype=torch.float64, device="cuda")
+    pl.curl(S.CURL_DUAL, dev(h), y2)
+    assert np.array_equal(host(y2), forms.join(curl_dual(tb.split_h(h))))
+
+
+@pytest.mark.parametrize("p,n", SMALL + MEDIUM)
+def test_pairing_and_mass_apply(p, n):
+    pl = S.Plan(n, p)
+    tb = TierB(p, n)
+    g = np.random.default_rng(7)
+    e = g.standard_normal(tb.N_e)
+    h = g.standard_normal(tb.N_h)
+    for which, v, split, ap in ((S.K1, e, tb.split_e, tb.apply_K1), (S.KT1, h, tb.split_h, tb.apply_Kt1)):
+        for T in (False, True):
+            y = torch.empty(v.size, dtype=torch.float64, device="cuda")
+            pl.pairing_apply(which, dev(v), y, transpose=T)
+            assert rel(host(y), forms.join(ap(split(v), T=T))) < 1e-13
+    y = torch.empty(tb.N_e, dtype=torch.float64, device="cuda")
+    pl.hodge_apply(S.MASS_EPS, dev(e), y)
+    assert rel(host(y), forms.join(tb.mass_eps(tb.split_e(e)))) < 1e-13
+    y = torch.empty(tb.N_h, dtype=torch.float64, device="cuda")
+    pl.hodge_apply(S.MASS_MU, dev(h), y)
+    assert rel(host(y), forms.join(tb.mass_mu(tb.split_h(h)))) < 1e-13
+    # full discrete Hodge stars (eqs. discrete2_hodge_eps / _mu)
+    y = torch.empty(tb.N_e, dtype=torch.float64, device="cuda")
+    pl.hodge_star(S.MASS_EPS, dev(e), y)
+    assert rel(host(y), tb.hodge_eps(e)) < solve_tol(tb)
+    y = torch.empty(tb.N_h, dtype=torch.float64, device="cuda")
+    pl.hodge_star(S.MASS_MU, dev(h), y)
+    assert rel(host(y), tb.hodge_mu(h)) < solve_tol(tb)
+
+
+def _state(tb, seed):
+    g = np.random.default_rng(seed)
+    return g.standard_normal(tb.N_e), g.standard_normal(tb.N_e), g.standard_normal(tb.N_h), g.standard_normal(tb.N_h)
+
+
+def _run_gpu(pl, st, dt, n_steps, jhat=None, jamp=None):
+    d, e, b, h = (dev(x) for x in st)
+    pl.step(d, e, b, h, dt, n_steps, j_hat=None if jhat is None else dev(jhat),
+            j_amp=None if jamp is None else dev(jamp))
+    return [host(x) for x in (d, e, b, h)]
+
+
+@pytest.mark.parametrize("p,n", SMALL + [(3, 24)])
+def test_step_parity_1_and_100(p, n):
+    pl = S.Plan(n, p)
+    tb = TierB(p, n)
+    st = _state(tb, 8)
+    dt = 0.4 * W.cfl_dt_max(tb) if tb.N_e < 20000 else 0.1 / max(forms._n3(n))
+    out = _run_gpu(pl, st, dt, 1)
+    ref = tb.step(*st, dt)
+    for a, b in zip(out, ref):
+        assert rel(a, b) < 1e-11
+    out = _run_gpu(pl, st, dt, 100)
+    ref = tb.run(*st, dt, 100)
+    for a, b in zip(out, ref):
+        assert rel(a, b) < 1e-9
+
+
+def test_step_with_source_and_amplitudes():
+    p, n = 3, (7, 6, 5)
+    pl = S.Plan(n, p)
+    tb = TierB(p, n)
+    st = _state(tb, 9)
+    a = np.random.default_rng(10).standard_normal(tb.N_h)
+    jhat = forms.join(curl_dual(tb.split_h(a)))        # divergence free
+    jamp = np.sin(0.3 * np.arange(40))
+    dt = 0.4 * W.cfl_dt_max(tb)
+    out = _run_gpu(pl, st, dt, 40, jhat, jamp)
+    ref = tb.run(*st, dt, 40, jhat, jamp)
+    for x, y in zip(out, ref):
+        assert rel(x, y) < 1e-10
+    assert pl.check_source(dev(jhat)) == 0
+    assert pl.check_source(dev(np.random.default_rng(11).standard_normal(tb.N_e))) == 6
+
+
+def test_energy_and_gauss():
+    p, n = 3, (8, 7, 9)
+    pl = S.Plan(n, p)
+    tb = TierB(p, n)
+    st = _state(tb, 12)
+    out = torch.zeros(2, dtype=torch.float64, device="cuda")
+    pl.energy(*(dev(x) for x in st), out)
+    E = host(out)[0]
+    assert abs(E - tb.energy(*st)) < 1e-12 * abs(tb.energy(*st))
+    pl.gauss(dev(st[0]), dev(st[2]), out)
+    gg = host(out)
+    ref = tb.gauss(st[0], st[2])
+    assert abs(gg[0] - ref[0]) <= 1e-15 * ref[0] and abs(gg[1] - ref[1]) <= 1e-15 * ref[1]
+
+
+def _curved_case(p, n, incl=True):
+    ctrl = W.interpolate_map(p, n, W.c3_map)
+    X = W.physical_points(p, n, ctrl)
+    Xel = np.stack([W.grid_to_elem(X[..., i], n, p + 1) for i in range(3)], -1)
+    eps = np.where(np.linalg.norm(Xel - np.array([0.45, 0.5, 0.55]), axis=-1) < 0.25, 4.0, 1.0) if incl \
+        else np.ones(Xel.shape[0])
+    return ctrl, eps
+
+
+@pytest.mark.parametrize("p,n", [(3, (6, 5, 7)), (2, 6), (4, (5, 4, 4))])
+def test_general_hodge_curved_step(p, n):
+    ctrl, eps = _curved_case(p, n)
+    pl = S.Plan(n, p, geom_ctrl=ctrl)
+    pl.set_material(S.EPS, eps)
+    assert not pl.separable(S.MASS_EPS) and not pl.separable(S.MASS_MU)
+    tb = TierB(p, n, ctrl=ctrl, inv_eps=1.0 / eps, inv_mu=1.0)
+    tb.sep_mu = None
+    tb.W_mu = tb._W(1.0)
+    g = np.random.default_rng(13)
+    x = g.standard_normal(tb.N_e)
+    y = torch.empty(tb.N_e, dtype=torch.float64, device="cuda")
+    pl.hodge_apply(S.MASS_EPS, dev(x), y)
+    assert rel(host(y), forms.join(tb.mass_eps(tb.split_e(x)))) < 1e-13
+    xb = g.standard_normal(tb.N_h)
+    yb = torch.empty(tb.N_h, dtype=torch.float64, device="cuda")
+    pl.hodge_apply(S.MASS_MU, dev(xb), yb)
+    assert rel(host(yb), forms.join(tb.mass_mu(tb.split_h(xb)))) < 1e-13
+    st = _state(tb, 14)
+    dt = 0.02 / max(forms._n3(n))
+    out = _run_gpu(pl, st, dt, 1)
+    for a, b in zip(out, tb.step(*st, dt)):
+        assert rel(a, b) < 1e-11
+    out = _run_gpu(pl, st, dt, 20)
+    for a, b in zip(out, tb.run(*st, dt, 20)):
+        assert rel(a, b) < 1e-10
+
+
+def test_general_hodge_variable_eps_identity():
+    p, n = 4, 6
+    pl = S.Plan(n, p)
+    X = pl.qp_coords()
+    eps = 1 + 0.5 * np.sin(2 * np.pi * X[:, 0]) * np.cos(2 * np.pi * X[:, 1])
+    pl.set_material(S.EPS, eps)
+    assert not pl.separable(S.MASS_EPS) and pl.separable(S.MASS_MU)
+    tb = TierB(p, n, inv_eps=1.0 / eps)
+    st = _state(tb, 15)
+    dt = 0.01
+    out = _run_gpu(pl, st, dt, 1)
+    for a, b in zip(out, tb.step(*st, dt)):
+        assert rel(a, b) < 1e-11
+
+
+def test_step_host_equals_device():
+    p, n = 3, 10
+    pl = S.Plan(n, p)
+    tb = TierB(p, n)
+    st = _state(tb, 16)
+    dt = 0.01
+    dv = _run_gpu(pl, st, dt, 3)
+    hs = [x.copy() for x in st]
+    pl.step_host(*hs, dt, 3)
+    for a, b in zip(hs, dv):
+        assert np.array_equal(a, b)
+
+
+def test_c1_cavity_vs_tier_a():
+    """configs[0]: cube cavity, p = 2, 8^3, first mode, 20 steps at dt = 0.5 CFL; GPU vs the plain
+    definition (tier A, SuperLU) and the exact energy 1/8."""
+    from oracle.scheme import TierA
+    p, n = 2, 8
+    tb = TierB(p, n)
+    dt = 0.5 * W.cfl_dt_max(tb)
+    mode = W.CavityMode((1, 1, 0), (0, 0, 1))
+    st = W.cavity_initial_state(tb, mode, dt)
+    pl = S.Plan(n, p)
+    out = _run_gpu(pl, st, dt, 20)
+    A = TierA(p, n)
+    ref = A.run(*st, dt, 20)
+    for a, b in zip(out, ref):
+        assert rel(a, b) < 1e-10
+    E = torch.zeros(1, dtype=torch.float64, device="cuda")
+    pl.energy(*(dev(x) for x in out), E)
+    assert abs(host(E)[0] - 0.125) < 0.01
