@@ -39,6 +39,7 @@ K1, KT1 = 0, 1
 MASS_EPS, MASS_MU = 0, 1
 CURL_PRIMAL, CURL_DUAL = 0, 1
 EPS, MU = 0, 1
+K_CLASSES = ["ampere_x", "eps_y", "eps_z", "faraday_x", "mu_y", "mu_z", "update", "hodge_general", "solve_x"]
 TAB_G, TAB_M, TAB_GAMMA_B1, TAB_GAMMA_C2, TAB_GAMMA_BP, TAB_GAMMA_C1 = range(6)
 
 _SIGS = {
@@ -65,6 +66,8 @@ _SIGS = {
     "sgm_gauss": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p],
     "sgm_check_source": [c_void_p, c_void_p, c_void_p, c_size_t, c_void_p],
     "sgm_plan_kernels_per_step": [c_void_p, ctypes.POINTER(c_int)],
+    "sgm_plan_set_profiling": [c_void_p, c_int],
+    "sgm_plan_profile": [c_void_p, c_void_p, c_void_p],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -196,6 +199,16 @@ class Plan:
         n = c_int()
         check(sgm_plan_kernels_per_step(self.h, ctypes.byref(n)))
         return n.value
+
+    def set_profiling(self, on=True):
+        check(sgm_plan_set_profiling(self.h, int(bool(on))), "sgm_plan_set_profiling")
+
+    def profile(self):
+        """{class name: (total ms, launches)} since the last call (event-timed on the stream)."""
+        ms = (c_double * len(K_CLASSES))()
+        cnt = (c_int * len(K_CLASSES))()
+        check(sgm_plan_profile(self.h, ms, cnt), "sgm_plan_profile")
+        return {K_CLASSES[i]: (ms[i], cnt[i]) for i in range(len(K_CLASSES)) if cnt[i]}
 
     def workspace(self):
         if self._ws is None:
