@@ -1,0 +1,377 @@
+#!/usr/bin/env python
+"""Benchmark of one scheme-2 leapfrog step (arXiv 2302.04979) on B200.
+
+Metric (BASELINE.json): fp64 DOF-updates/s per leapfrog step, DOF-updates = (N_e + N_h) per
+step, and the HBM-roofline fraction of the dominant kernel.  Default workload: configs[4] (C5)
+full step at p = 3, 128^3 elements, identity geometry, eps = mu = 1 -- the configuration the
+north-star target (>= 60 % of HBM roofline) is stated on.  Inputs: seeded N(0,1) d, b (rng(5)),
+e, h derived by the discrete Hodge stars on the device (setup, untimed).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c5 --p 3 --n 128]
+
+Multi-GPU (torchrun): the path does not shard (north_star: one GPU, no collectives), so every
+rank runs an independent replica ("replicas only", scaling "weak"); the only collective is the
+max-over-ranks of the device-timed region.
+"""
+import argparse
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fp64 DOF-updates/sec per leapfrog step and % of B200 HBM roofline"
+UNIT = "DOF-updates/s"
+# Delta t_max * n for scheme 2 on the unit cube (reading Z15 -- the oracle's CFL
+# routine reproduces these; used only to pick a stable dt for throughput runs)
+CFL_N = {2: 0.3046, 3: 0.2020, 4: 0.1205}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c5", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--p", type=int, default=3)
+    ap.add_argument("--n", type=int, default=128)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+def workload(args):
+    """(p, n, description, geometry ctrl or None, eps at qp or None, has_source)."""
+    if args.config == "c5":
+        return args.p, args.n, f"C5 full step p={args.p} n_el={args.n}^3 identity eps=mu=1", None, None, False
+    if args.config == "c2":
+        return 3, 32, "C2 full step p=3 n_el=32^3 identity eps=mu=1", None, None, False
+    if args.config == "c3":
+        return 3, 48, "C3 full step p=3 n_el=48^3 curved map, eps in {1,4} inclusion, Gaussian-pulse J", "c3", "c3", True
+    return 4, 96, "C4 full step p=4 n_el=96^3 identity, eps=1+0.5 sin(2pi x)cos(2pi y)", None, "c4", False
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        d = json.load(open(path))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, torch copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
+
+
+class ClockSampler:
+    """NVML samples of SM clock and throttle reasons while running."""
+
+    def __init__(self, dev_index):
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception:
+            self.N = None
+
+    def _run(self):
+        N = self.N
+        names = {
+            "hw_slowdown": getattr(N, "nvmlClocksThrottleReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(N, "nvmlClocksThrottleReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(N, "nvmlClocksThrottleReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(N, "nvmlClocksThrottleReasonSwPowerCap", 0x4),
+            "hw_power_brake": getattr(N, "nvmlClocksThrottleReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM))
+                r = N.nvmlDeviceGetCurrentClocksThrottleReasons(self.h)
+                for k, v in names.items():
+                    if r & v:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.N is not None:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.N is not None:
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def build_inputs(args, torch, S, dev):
+    p, n, desc, geo, mat, src = workload(args)
+    ctrl = None
+    if geo == "c3":
+        # spline interpolation of the C3 map lives on the oracle side (input generation only)
+        from oracle import workloads as W
+        ctrl = W.interpolate_map(p, n, W.c3_map)
+    pl = S.Plan(n, p, geom_ctrl=ctrl, device=dev.index or 0)
+    if mat is not None:
+        X = pl.qp_coords()
+        if mat == "c3":
+            import synth
+            c_eps, _ = synth.c3_centres()
+            eps = np.where(np.linalg.norm(X - c_eps, axis=1) < 0.25, 4.0, 1.0)
+        else:
+            eps = 1 + 0.5 * np.sin(2 * np.pi * X[:, 0]) * np.cos(2 * np.pi * X[:, 1])
+        pl.set_material(S.EPS, eps)
+        del X
+    import synth
+    d0, b0 = synth.normal(5, pl.N_e, pl.N_h)
+    d = torch.from_numpy(d0).to(dev)
+    b = torch.from_numpy(b0).to(dev)
+    e = torch.empty_like(d)
+    h = torch.empty_like(b)
+    pl.hodge_star(S.MASS_EPS, d, e)
+    pl.hodge_star(S.MASS_MU, b, h)
+    jhat = None
+    if src:
+        a = torch.from_numpy(synth.normal(33, pl.N_h)[0]).to(dev)
+        jhat = torch.empty_like(d)
+        pl.curl(S.CURL_DUAL, a, jhat)          # j = D~1 a: divergence free
+    dt = 0.5 * CFL_N[p] / n * (0.5 if geo or mat else 1.0)
+    torch.cuda.synchronize()
+    return pl, (d, e, b, h), jhat, dt, desc, p, n
+
+
+def kernel_bytes(cls, N_e, N_h, has_src):
+    """Algorithmic bytes per launch (SURVEY 8(d) per-kernel model)."""
+    return {
+        "eps_update_z": 8 * (N_h + 3 * N_e + (N_e if has_src else 0)),
+        "mu_update_z": 8 * (N_e + 3 * N_h),
+        "eps_y": 16 * N_e, "eps_x": 16 * N_e, "mu_y": 16 * N_h, "mu_x": 16 * N_h,
+        "update": 8 * (N_h + 2 * N_e), "solve_z": 16 * N_e,
+    }.get(cls)
+
+
+def cpu_baseline(args, budget_s=10.0):
+    """The oracle (tier B, as it stands) on this host: a bounded sample of the same workload."""
+    import threadpoolctl
+    from oracle.structured import TierB
+    import synth
+    p, n, desc, geo, mat, src = workload(args)
+    if geo or mat:
+        return None
+    tb = TierB(p, n)
+    d0, b0 = synth.normal(5, tb.N_e, tb.N_h)
+    st = (d0, tb.hodge_eps(d0), b0, tb.hodge_mu(b0))
+    dt = 0.5 * CFL_N[p] / n
+    st = tb.step(*st, dt)  # warm-up
+    t0 = time.perf_counter()
+    k = 0
+    while True:
+        st = tb.step(*st, dt)
+        k += 1
+        if time.perf_counter() - t0 > budget_s and k >= 2:
+            break
+    t = time.perf_counter() - t0
+    threads = max([i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()] + [1])
+    return {"value": (tb.N_e + tb.N_h) * k / t, "unit": UNIT, "cores": int(threads), "kind": "oracle",
+            "sample": f"{k} tier-B oracle steps (setup excluded) of {desc}, {t:.1f} s",
+            "host_cpus": os.cpu_count()}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the CPU oracle timed on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    p, n, desc, geo, mat, src = workload(args)
+    from oracle.structured import TierB
+    import synth
+    import threadpoolctl
+    if geo or mat:
+        print(json.dumps({"impl": "reference", "unavailable": "reference arm implemented for separable configs"}))
+        return
+    tb = TierB(p, n)
+    d0, b0 = synth.normal(5, tb.N_e, tb.N_h)
+    st = (d0, tb.hodge_eps(d0), b0, tb.hodge_mu(b0))
+    dt = 0.5 * CFL_N[p] / n
+    for _ in range(max(1, min(args.warmup, 2))):
+        st = tb.step(*st, dt)
+    budget = 120.0
+    t0 = time.perf_counter()
+    k = 0
+    while k < args.steps:
+        st = tb.step(*st, dt)
+        k += 1
+        if time.perf_counter() - t0 > budget:
+            break
+    t = time.perf_counter() - t0
+    v = (tb.N_e + tb.N_h) * k / t
+    threads = max([i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()] + [1])
+    out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": k, "warmup": args.warmup,
+           "ms_per_step": 1e3 * t / k, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic", "impl": "reference",
+           "config": {"workload": desc, "p": p, "n_el": n, "dofs_per_step": tb.N_e + tb.N_h},
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": int(threads), "kind": "oracle",
+                            "sample": f"{k} of {args.steps} requested tier-B oracle steps (120 s cap), setup excluded"},
+           "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    import paper_2302_04979_b200 as S
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    pl, state, jhat, dt, desc, p, n = build_inputs(args, torch, S, dev)
+    N_e, N_h = pl.N_e, pl.N_h
+    dofs = N_e + N_h
+    K, W = args.steps, max(3, args.warmup)
+    jamp = None
+    if jhat is not None:
+        tt = (np.arange(K + W) + 0.5) * dt
+        jamp = torch.from_numpy(np.exp(-((tt - 0.15) / 0.05) ** 2)).to(dev)
+    stream = torch.cuda.current_stream()
+
+    def steps(k0, k):
+        for i in range(k):
+            pl.step(*state, dt, 1, j_hat=jhat, j_amp=None if jamp is None else jamp[k0 + i:k0 + i + 1],
+                    stream=stream)
+
+    steps(0, W)
+    torch.cuda.synchronize()
+
+    def timed(profile):
+        pl.set_profiling(profile)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        steps(W, K)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        ms = e0.elapsed_time(e1)
+        prof = pl.profile() if profile else None
+        pl.set_profiling(False)
+        return ms, prof
+
+    with ClockSampler(local) as clk:
+        ms, _ = timed(False)
+        ms_prof, prof = timed(True)
+    if dist:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = world * dofs * K / (ms * 1e-3)
+
+    # dominant kernel roofline (profiled pass of the same K steps, events on the launching stream)
+    peak, peak_src = peaks()
+    kernels = {}
+    for cls, (kms, cnt) in prof.items():
+        by = kernel_bytes(cls, N_e, N_h, jhat is not None)
+        per = kms / cnt
+        kernels[cls] = {"launches": cnt, "ms_per_launch": per, "share": kms / sum(v[0] for v in prof.values())}
+        if by:
+            kernels[cls]["algo_bytes"] = by
+            kernels[cls]["gbs"] = by / (per * 1e-3) / 1e9
+    dom = max(prof.items(), key=lambda kv: kv[1][0])[0]
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tfile):
+        try:
+            tr = json.load(open(tfile))
+            traffic = tr.get(f"{args.config}_p{p}_n{n}", {}).get(dom)
+        except Exception:
+            traffic = None
+    achieved = kernels[dom].get("gbs")
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic, "peak_source": peak_src,
+            "algo_bytes_per_launch": kernels[dom].get("algo_bytes"),
+            "ms_per_launch": kernels[dom]["ms_per_launch"],
+            "step_model_bytes": 64 * dofs, "step_model_gbs": 64 * dofs / (ms / K * 1e-3) / 1e9,
+            "note": "per-kernel times from a second, event-profiled pass of the same K steps"}
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+           "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic",
+           "config": {"workload": desc, "p": p, "n_el": n, "dofs_per_step": dofs, "N_e": N_e, "N_h": N_h,
+                      "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                      "l2": f"no flush: working set {(2 * N_e + 2 * N_h + max(N_e, N_h)) * 8 / 1e6:.0f} MB "
+                            f"(state + workspace) vs 126 MB L2"},
+           "roofline": roof, "kernels": kernels,
+           "gpu_launches": pl.kernels_per_step() * K,
+           "clocks": clk.summary()}
+
+    # end to end through the C ABI with pinned host buffers (H2D + step + D2H every step)
+    if not args.no_e2e:
+        hs = [torch.empty(x.numel(), dtype=torch.float64, pin_memory=True) for x in state]
+        for hx, x in zip(hs, state):
+            hx.copy_(x)
+        hj = None
+        if jhat is not None:
+            hj = torch.empty(jhat.numel(), dtype=torch.float64, pin_memory=True)
+            hj.copy_(jhat)
+        ke = min(K, 10)
+        pl.step_host(*hs, dt, 1, j_hat=hj, stream=stream)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(ke):
+            pl.step_host(*hs, dt, 1, j_hat=hj, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ems = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ems], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        hb = 8 * (2 * N_e + 2 * N_h) + (8 * N_e if hj is not None else 0)
+        out["e2e"] = {"value": world * dofs * ke / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": hb,
+                      "d2h_bytes_per_step": 8 * (2 * N_e + 2 * N_h), "steps": ke,
+                      "note": "sgm_step_host: pinned host d,e,b,h -> device, 1 step, device -> host, per step"}
+
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            out["cpu_baseline"] = cpu_baseline(args)
+        except Exception as ex:  # the baseline is informational
+            out["cpu_baseline"] = {"value": None, "error": str(ex)}
+    if rank == 0:
+        print(json.dumps(out))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -39,7 +39,7 @@ K1, KT1 = 0, 1
 MASS_EPS, MASS_MU = 0, 1
 CURL_PRIMAL, CURL_DUAL = 0, 1
 EPS, MU = 0, 1
-K_CLASSES = ["ampere_x", "eps_y", "eps_z", "faraday_x", "mu_y", "mu_z", "update", "hodge_general", "solve_x"]
+K_CLASSES = ["eps_update_z", "eps_y", "eps_x", "mu_update_z", "mu_y", "mu_x", "update", "hodge_general", "solve_z"]
 TAB_G, TAB_M, TAB_GAMMA_B1, TAB_GAMMA_C2, TAB_GAMMA_BP, TAB_GAMMA_C1 = range(6)
 
 _SIGS = {

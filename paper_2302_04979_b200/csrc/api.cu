@@ -69,7 +69,7 @@ size_t comp_off(const Plan& P, int kind, int c) {
 }
 
 const double* table(const Plan& P, int axis, int op) {
-  return P.tables_dev + (size_t(axis) * OP_COUNT + op) * P.Lmax * (4 * P.p);
+  return P.tables_dev + (size_t(axis) * OP_COUNT + op) * P.Lmax * (6 * P.p - 2);
 }
 
 struct WS {
@@ -91,11 +91,6 @@ sgm_status ws_carve(const Plan& P, void* ws, size_t bytes, WS& w) {
   w.r = w.t + nmax;
   w.partials = w.r + nmax;
   return SGM_OK;
-}
-
-int lines_per_cta(int L) {
-  // 64 lines of ~130 doubles = 67 KB of smem -> 3 CTAs per SM; 32 lines for long lines
-  return (size_t(64) * (L | 1) * sizeof(double) <= 150 * 1024) ? 64 : 32;
 }
 
 void comps_of(const Plan& P, int kind, const double* base, double* out[3]) {
@@ -144,30 +139,32 @@ void sweep_pass(const Plan& P, int kind, int axis, double* const in[3], double* 
   std::memset(&a, 0, sizeof(a));
   a.ncomp = 3;
   a.axis = axis;
-  int Lmax = 0;
+  a.band = band;
+  a.solve = solve;
+  a.pro_kind = pro;
   for (int c = 0; c < 3; ++c) {
     comp_shape(P, kind, c, a.comp[c].ext);
     a.comp[c].in = in[c];
     a.comp[c].out = out[c];
     a.comp[c].tab = table(P, axis, own_or(axis, c, op_own, op_oth));
     a.comp[c].scale = scale ? scale[c] : 1.0;
-    Lmax = std::max(Lmax, a.comp[c].ext[axis]);
   }
-  a.nl = lines_per_cta(Lmax);
   if (pro_args) a.pro = *pro_args;
-  launch_sweep(P.p, band, solve, pro, a, Lmax, st);
+  launch_sweep(P.p, P.seg[axis], a, st);
 }
 
 // y = (A_z (x) A_y (x) A_x) x per component with 3 sweeps x -> t -> t -> y (x == y allowed).
+// Axis order z, y, x: the Kronecker factors commute; the strided axes go first so
+// a fused Ampere/Faraday update (first pass) reads its curl stencil coalesced.
 void kron_pass3(const Plan& P, int kind, const double* x, double* y, double* t, int op_own, int op_oth,
                 const double* scale, bool band, bool solve, cudaStream_t st) {
   double *X[3], *T[3], *Y[3];
   comps_of(P, kind, x, X);
   comps_of(P, kind, t, T);
   comps_of(P, kind, y, Y);
-  sweep_pass(P, kind, 0, X, T, op_own, op_oth, nullptr, band, solve, PRO_NONE, nullptr, st);
+  sweep_pass(P, kind, 2, X, T, op_own, op_oth, nullptr, band, solve, PRO_NONE, nullptr, st);
   sweep_pass(P, kind, 1, T, T, op_own, op_oth, nullptr, band, solve, PRO_NONE, nullptr, st);
-  sweep_pass(P, kind, 2, T, Y, op_own, op_oth, scale, band, solve, PRO_NONE, nullptr, st);
+  sweep_pass(P, kind, 0, T, Y, op_own, op_oth, scale, band, solve, PRO_NONE, nullptr, st);
 }
 
 PrologueArgs make_pro(const Plan& P, int src_kind, const double* src, const double* jhat, const double* s_ptr,
@@ -313,17 +310,17 @@ void step_once(Plan& P, double* d, double* e, double* b, double* h, const double
     const int mass = half == 0 ? SGM_MASS_EPS : SGM_MASS_MU;
     const int pro = half == 0 ? PRO_AMPERE : PRO_FARADAY;
     const int own = half == 0 ? OP_EPS_OWN : OP_MU_OWN, oth = half == 0 ? OP_EPS_OTH : OP_MU_OTH;
-    const int kx = half == 0 ? SGM_K_AMPERE_X : SGM_K_FARADAY_X;
-    const int ky = half == 0 ? SGM_K_EPS_Y : SGM_K_MU_Y, kz = half == 0 ? SGM_K_EPS_Z : SGM_K_MU_Z;
+    const int kx = half == 0 ? SGM_K_EPS_UPDATE_Z : SGM_K_MU_UPDATE_Z;
+    const int ky = half == 0 ? SGM_K_EPS_Y : SGM_K_MU_Y, kz = half == 0 ? SGM_K_EPS_X : SGM_K_MU_X;
     double** state = half == 0 ? D : B;
     double** outv = half == 0 ? E : H;
     PrologueArgs pa = half == 0 ? make_pro(P, 1, h, jhat, s_ptr, dt) : make_pro(P, 0, e, nullptr, nullptr, dt);
     const MassData& M = P.mass[mass];
     comps_of(P, kind, w.t, T);
     if (M.kind == HODGE_SEPARABLE) {
-      { ProfScope ps(P, kx, st); sweep_pass(P, kind, 0, state, T, own, oth, nullptr, true, true, pro, &pa, st); }
+      { ProfScope ps(P, kx, st); sweep_pass(P, kind, 2, state, T, own, oth, nullptr, true, true, pro, &pa, st); }
       { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, true, true, PRO_NONE, nullptr, st); }
-      { ProfScope ps(P, kz, st); sweep_pass(P, kind, 2, T, outv, own, oth, M.scale, true, true, PRO_NONE, nullptr, st); }
+      { ProfScope ps(P, kz, st); sweep_pass(P, kind, 0, T, outv, own, oth, M.scale, true, true, PRO_NONE, nullptr, st); }
     } else {
       SweepArgs a;
       std::memset(&a, 0, sizeof(a));
@@ -336,9 +333,9 @@ void step_once(Plan& P, double* d, double* e, double* b, double* h, const double
       { ProfScope ps(P, SGM_K_UPDATE, st); launch_update(pro, a, st); }
       { ProfScope ps(P, SGM_K_HODGE_GENERAL, st); mass_apply(P, mass, state[0], w.r, w.t, st); }
       comps_of(P, kind, w.r, Rr);
-      { ProfScope ps(P, SGM_K_SOLVE_X, st); sweep_pass(P, kind, 0, Rr, T, own, oth, nullptr, false, true, PRO_NONE, nullptr, st); }
+      { ProfScope ps(P, SGM_K_SOLVE_Z, st); sweep_pass(P, kind, 2, Rr, T, own, oth, nullptr, false, true, PRO_NONE, nullptr, st); }
       { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, false, true, PRO_NONE, nullptr, st); }
-      { ProfScope ps(P, kz, st); sweep_pass(P, kind, 2, T, outv, own, oth, nullptr, false, true, PRO_NONE, nullptr, st); }
+      { ProfScope ps(P, kz, st); sweep_pass(P, kind, 0, T, outv, own, oth, nullptr, false, true, PRO_NONE, nullptr, st); }
     }
   }
 }
@@ -363,7 +360,7 @@ sgm_status sgm_plan_create(const sgm_plan_desc* desc, sgm_plan* out) {
   int Q = desc->quad_points == 0 ? p + 1 : desc->quad_points;
   if (Q < p + 1 || Q > 8) return fail(SGM_E_INVALID_ARG, "quad_points must be 0 or in [p+1, 8]");
   for (int a = 0; a < 3; ++a)
-    if (desc->n_el[a] + p - 1 > kMaxLine) return fail(SGM_E_UNSUPPORTED, "line length above 1024");
+    if (desc->n_el[a] + p - 1 > kMaxLine) return fail(SGM_E_UNSUPPORTED, "line length n_el + p - 1 above 528");
   Plan* P = new (std::nothrow) Plan();
   if (!P) return fail(SGM_E_NOMEM, "out of host memory");
   P->p = p;

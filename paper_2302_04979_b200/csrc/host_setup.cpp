@@ -264,13 +264,19 @@ std::vector<double> transpose(const std::vector<double>& A, int L) {
   return T;
 }
 
-// Fill one table: rows of R = 4P doubles [band(2P+1) | lo(P-1) | upn(P-1) | dinv].
-sgm_status fill_table(double* T, int P, int L, const std::vector<double>* band,
+// Fill one line-operator table (layout: seg_sweep.cuh): Rpad rows of RS = 6P-2 doubles
+//   [band(2P+1) | lo(m) | upn(m) | dinv | F(m) | B(m)],  m = P-1.
+// Rows >= L are identity padding.  F/B are the spike tables of the partitioned solve for
+// segments of SEG rows: F[j-1] of row r = d z_r / d z_{r0-j}, B[j-1] = d u_r / d u_{r1+j}.
+sgm_status fill_table(double* T, int P, int L, int Rpad, int SEG, const std::vector<double>* band,
                       const std::vector<double>* lu_src, std::string& err) {
-  const int R = 4 * P;
-  for (int i = 0; i < L; ++i) {
-    double* row = T + size_t(i) * R;
-    for (int k = 0; k < R; ++k) row[k] = 0.0;
+  const int m = P - 1, RS = 6 * P - 2;
+  const int LO = 2 * P + 1, UP = LO + m, DI = UP + m, FF = DI + 1, BB = FF + m;
+  for (int i = 0; i < Rpad; ++i) {
+    double* row = T + size_t(i) * RS;
+    for (int k = 0; k < RS; ++k) row[k] = 0.0;
+    row[DI] = 1.0;
+    if (i >= L) continue;
     if (band) {
       for (int k = -P; k <= P; ++k) {
         int j = i + k;
@@ -280,18 +286,45 @@ sgm_status fill_table(double* T, int P, int L, const std::vector<double>* band,
       row[P] = 1.0;
     }
   }
-  if (lu_src) {
-    std::vector<double> LU;
-    sgm_status st = banded_lu_nopivot(*lu_src, L, P - 1, LU, err);
-    if (st != SGM_OK) return st;
-    for (int i = 0; i < L; ++i) {
-      double* row = T + size_t(i) * R;
-      double uii = LU[size_t(i) * L + i];
-      for (int k = 1; k <= P - 1; ++k) {
-        if (i - k >= 0) row[2 * P + 1 + (k - 1)] = LU[size_t(i) * L + (i - k)];
-        if (i + k < L) row[2 * P + 1 + (P - 1) + (k - 1)] = LU[size_t(i) * L + (i + k)] / uii;
+  if (!lu_src) return SGM_OK;
+  std::vector<double> LU;
+  sgm_status st = banded_lu_nopivot(*lu_src, L, m, LU, err);
+  if (st != SGM_OK) return st;
+  for (int i = 0; i < L; ++i) {
+    double* row = T + size_t(i) * RS;
+    double uii = LU[size_t(i) * L + i];
+    for (int k = 1; k <= m; ++k) {
+      if (i - k >= 0) row[LO + k - 1] = LU[size_t(i) * L + (i - k)];
+      if (i + k < L) row[UP + k - 1] = LU[size_t(i) * L + (i + k)] / uii;
+    }
+    row[DI] = 1.0 / uii;
+  }
+  // spikes: response of the zero-history local recurrences to unit histories
+  const int S = Rpad / SEG;
+  std::vector<double> z(SEG + m);
+  for (int s = 0; s < S; ++s) {
+    const int r0 = s * SEG;
+    for (int j = 1; j <= m; ++j) {
+      // forward: z_{r0-q} = delta_{qj}; z_r = -sum_k lo_{r,k} z_{r-k}
+      for (int q = 1; q <= m; ++q) z[m - q] = (q == j) ? 1.0 : 0.0;   // z[m-q] <-> row r0-q
+      for (int r = r0; r < r0 + SEG; ++r) {
+        const double* row = T + size_t(r) * RS;
+        double acc = 0.0;
+        for (int k = 1; k <= m; ++k) acc -= row[LO + k - 1] * z[m + (r - r0) - k];
+        z[m + (r - r0)] = acc;
+        T[size_t(r) * RS + FF + j - 1] = acc;
       }
-      row[4 * P - 1] = 1.0 / uii;
+      // backward: u_{r1+q} = delta_{qj}; u_r = -sum_k upn_{r,k} u_{r+k}
+      const int r1 = r0 + SEG - 1;
+      std::vector<double> u(SEG + m, 0.0);  // u[(r - r0)] for r in segment, u[SEG + q - 1] <-> r1+q
+      for (int q = 1; q <= m; ++q) u[SEG + q - 1] = (q == j) ? 1.0 : 0.0;
+      for (int r = r1; r >= r0; --r) {
+        const double* row = T + size_t(r) * RS;
+        double acc = 0.0;
+        for (int k = 1; k <= m; ++k) acc -= row[UP + k - 1] * u[(r - r0) + k];
+        u[r - r0] = acc;
+        T[size_t(r) * RS + BB + j - 1] = acc;
+      }
     }
   }
   return SGM_OK;
@@ -299,25 +332,42 @@ sgm_status fill_table(double* T, int P, int L, const std::vector<double>* band,
 
 }  // namespace
 
+int seg_for_line(int L) {
+  const int cands[4] = {33, 26, 22, 16};
+  int best = 33, bw = 1 << 30;
+  for (int c : cands) {
+    int S = (L + c - 1) / c;
+    if (S > 32) continue;
+    int w = S * c - L;
+    if (w < bw) { bw = w; best = c; }
+  }
+  return best;
+}
+
 sgm_status build_tables(Plan& P, std::string& err) {
-  const int p = P.p, R = 4 * p;
-  int Lmax = 0;
-  for (int a = 0; a < 3; ++a) Lmax = std::max(Lmax, P.ax[a].b);
-  P.Lmax = Lmax;
-  P.tables_host.assign(size_t(3) * OP_COUNT * Lmax * R, 0.0);
+  const int p = P.p, RS = 6 * p - 2;
+  int Rmax = 0;
+  for (int a = 0; a < 3; ++a) {
+    P.seg[a] = seg_for_line(P.ax[a].b);
+    P.rpad[a] = ((P.ax[a].b + P.seg[a] - 1) / P.seg[a]) * P.seg[a];
+    Rmax = std::max(Rmax, P.rpad[a]);
+  }
+  P.Lmax = Rmax;  // rows per table slot
+  P.tables_host.assign(size_t(3) * OP_COUNT * Rmax * RS, 0.0);
   for (int a = 0; a < 3; ++a) {
     const Axis& X = P.ax[a];
+    const int R = P.rpad[a], SEG = P.seg[a];
     std::vector<double> GT = transpose(X.G, X.a), MT = transpose(X.M, X.b);
-    auto T = [&](int op) { return P.tables_host.data() + (size_t(a) * OP_COUNT + op) * Lmax * R; };
+    auto T = [&](int op) { return P.tables_host.data() + (size_t(a) * OP_COUNT + op) * Rmax * RS; };
     sgm_status st;
-    if ((st = fill_table(T(OP_EPS_OWN), p, X.b, &X.GB1, &X.M, err)) != SGM_OK) return st;
-    if ((st = fill_table(T(OP_EPS_OTH), p, X.a, &X.GC2, &X.G, err)) != SGM_OK) return st;
-    if ((st = fill_table(T(OP_MU_OWN), p, X.a, &X.GBp, &GT, err)) != SGM_OK) return st;
-    if ((st = fill_table(T(OP_MU_OTH), p, X.b, &X.GC1, &MT, err)) != SGM_OK) return st;
-    if ((st = fill_table(T(OP_APPLY_M), p, X.b, &X.M, nullptr, err)) != SGM_OK) return st;
-    if ((st = fill_table(T(OP_APPLY_G), p, X.a, &X.G, nullptr, err)) != SGM_OK) return st;
-    if ((st = fill_table(T(OP_APPLY_GT), p, X.a, &GT, nullptr, err)) != SGM_OK) return st;
-    if ((st = fill_table(T(OP_APPLY_MT), p, X.b, &MT, nullptr, err)) != SGM_OK) return st;
+    if ((st = fill_table(T(OP_EPS_OWN), p, X.b, R, SEG, &X.GB1, &X.M, err)) != SGM_OK) return st;
+    if ((st = fill_table(T(OP_EPS_OTH), p, X.a, R, SEG, &X.GC2, &X.G, err)) != SGM_OK) return st;
+    if ((st = fill_table(T(OP_MU_OWN), p, X.a, R, SEG, &X.GBp, &GT, err)) != SGM_OK) return st;
+    if ((st = fill_table(T(OP_MU_OTH), p, X.b, R, SEG, &X.GC1, &MT, err)) != SGM_OK) return st;
+    if ((st = fill_table(T(OP_APPLY_M), p, X.b, R, SEG, &X.M, nullptr, err)) != SGM_OK) return st;
+    if ((st = fill_table(T(OP_APPLY_G), p, X.a, R, SEG, &X.G, nullptr, err)) != SGM_OK) return st;
+    if ((st = fill_table(T(OP_APPLY_GT), p, X.a, R, SEG, &GT, nullptr, err)) != SGM_OK) return st;
+    if ((st = fill_table(T(OP_APPLY_MT), p, X.b, R, SEG, &MT, nullptr, err)) != SGM_OK) return st;
   }
   return SGM_OK;
 }

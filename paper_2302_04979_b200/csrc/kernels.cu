@@ -18,6 +18,7 @@
 #include <cstdio>
 
 #include "kernels.cuh"
+#include "seg_sweep.cuh"
 
 namespace sgm {
 
@@ -25,14 +26,6 @@ namespace {
 
 constexpr int kRedThreads = 256;
 constexpr int kRedBlocks = 296;  // 2 x 148 SMs
-
-__device__ __forceinline__ void cp_async8(double* s, const double* g) {
-  unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(s));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(g) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-}
 
 // ---- integer-incidence curls (SURVEY 8.0 stencils) ---------------------------------
 // dual   (dv)_j = v_{j+1} - v_j           (free ends)
@@ -75,66 +68,123 @@ __device__ __forceinline__ double update_value(const PrologueArgs& P, int c, con
   }
 }
 
-// ---- one line: optional banded mat-vec fused with forward substitution, then backward -----
-// Table row i (4P doubles): band[0..2P] = A[i][i-P..i+P], lo[k-1] = L_{i,i-k}, upn[k-1] =
-// U_{i,i+k}/U_ii, dinv = 1/U_ii.
-template <int P, bool BAND, bool SOLVE>
-__device__ __forceinline__ void sweep_line(double* line, int es, int L, const double* __restrict__ T) {
-  constexpr int R = 4 * P;
-  double xw[2 * P + 1];
+// ---- register-segment sweep (see seg_sweep.cuh) -----------------------------------------
+template <int P, int SEG>
+__device__ __forceinline__ void seg_compute(double (&v)[SEG], const double (&hl)[P], const double (&hr)[P],
+                                            const double* __restrict__ T, int r0, int S, int s, int lane,
+                                            double* __restrict__ xch, bool band, bool solve) {
+  using RL = RowLayout<P>;
+  constexpr int M = RL::M;
+  constexpr int RS = RL::RS;
+  if (band) {
+    double w[P];
 #pragma unroll
-  for (int k = 0; k < P; ++k) xw[k] = 0.0;
+    for (int q = 0; q < P; ++q) w[q] = hl[q];
 #pragma unroll
-  for (int k = 0; k <= P; ++k) xw[P + k] = (k < L) ? line[k * es] : 0.0;
-  double zw[P - 1];
+    for (int k = 0; k < SEG; ++k) {
+      const double* row = T + size_t(r0 + k) * RS;
+      const double xk = v[k];
+      // y_k = sum_{q=-P..P} A[r][r+q] x_{r+q}, summed as a short tree
+      double lsum = 0.0, rsum = 0.0;
 #pragma unroll
-  for (int k = 0; k < P - 1; ++k) zw[k] = 0.0;
-  for (int i = 0; i < L; ++i) {
-    const double* row = T + size_t(i) * R;
-    double y;
-    if (BAND) {
-      y = 0.0;
+      for (int q = 1; q <= P; ++q) {
+        lsum = fma(__ldg(row + P - q), w[P - q], lsum);
+        const double xr = (k + q < SEG) ? v[k + q] : hr[k + q - SEG];
+        rsum = fma(__ldg(row + P + q), xr, rsum);
+      }
+      const double y = fma(__ldg(row + P), xk, lsum + rsum);
 #pragma unroll
-      for (int k = 0; k <= 2 * P; ++k) y = fma(__ldg(row + k), xw[k], y);
-    } else {
-      y = xw[P];
+      for (int q = 0; q < P - 1; ++q) w[q] = w[q + 1];
+      w[P - 1] = xk;
+      v[k] = y;
     }
-    double outv = y;
-    if (SOLVE) {
-      double z = y;
-#pragma unroll
-      for (int k = P - 1; k >= 1; --k) z = fma(-__ldg(row + 2 * P + k), zw[k - 1], z);
-#pragma unroll
-      for (int k = P - 2; k >= 1; --k) zw[k] = zw[k - 1];
-      zw[0] = z;
-      outv = z;
-    }
-    line[i * es] = outv;
-#pragma unroll
-    for (int k = 0; k < 2 * P; ++k) xw[k] = xw[k + 1];
-    int nx = i + 1 + P;
-    xw[2 * P] = (nx < L) ? line[nx * es] : 0.0;
   }
-  if (SOLVE) {
-    double uw[P - 1];
+  if (!solve) return;
+  const int nS = blockDim.x >> 5;
+  double* tails = xch;                 // [nS][M][32]
+  double* heads = xch + nS * M * 32;   // [nS][M][32]
+  // forward substitution, zero history
 #pragma unroll
-    for (int k = 0; k < P - 1; ++k) uw[k] = 0.0;
-    for (int i = L - 1; i >= 0; --i) {
-      const double* row = T + size_t(i) * R;
-      double u = line[i * es] * __ldg(row + 4 * P - 1);
+  for (int k = 0; k < SEG; ++k) {
+    const double* row = T + size_t(r0 + k) * RS;
+    double z = v[k];
 #pragma unroll
-      for (int k = P - 1; k >= 1; --k) u = fma(-__ldg(row + 3 * P - 1 + k), uw[k - 1], u);
+    for (int q = M; q >= 1; --q)
+      if (k - q >= 0) z = fma(-__ldg(row + RL::LO + q - 1), v[k - q], z);
+    v[k] = z;
+  }
 #pragma unroll
-      for (int k = P - 2; k >= 1; --k) uw[k] = uw[k - 1];
-      uw[0] = u;
-      line[i * es] = u;
+  for (int jj = 1; jj <= M; ++jj) tails[(s * M + jj - 1) * 32 + lane] = v[SEG - jj];
+  __syncthreads();
+  // true history hist[jj-1] = z_{r0-jj}: walk the previous segments' tails through the spikes
+  double hist[M];
+#pragma unroll
+  for (int q = 0; q < M; ++q) hist[q] = 0.0;
+  for (int t = 0; t < s; ++t) {
+    double nh[M];
+#pragma unroll
+    for (int jj = 1; jj <= M; ++jj) {
+      const double* row = T + size_t(t * SEG + SEG - jj) * RS;
+      double val = tails[(t * M + jj - 1) * 32 + lane];
+#pragma unroll
+      for (int q = 1; q <= M; ++q) val = fma(__ldg(row + RL::F + q - 1), hist[q - 1], val);
+      nh[jj - 1] = val;
     }
+#pragma unroll
+    for (int q = 0; q < M; ++q) hist[q] = nh[q];
+  }
+#pragma unroll
+  for (int k = 0; k < SEG; ++k) {
+    const double* row = T + size_t(r0 + k) * RS;
+    double z = v[k];
+#pragma unroll
+    for (int q = 1; q <= M; ++q) z = fma(__ldg(row + RL::F + q - 1), hist[q - 1], z);
+    v[k] = z;
+  }
+  // backward substitution, zero future
+#pragma unroll
+  for (int k = SEG - 1; k >= 0; --k) {
+    const double* row = T + size_t(r0 + k) * RS;
+    double u = v[k] * __ldg(row + RL::DINV);
+#pragma unroll
+    for (int q = M; q >= 1; --q)
+      if (k + q < SEG) u = fma(-__ldg(row + RL::UP + q - 1), v[k + q], u);
+    v[k] = u;
+  }
+#pragma unroll
+  for (int jj = 1; jj <= M; ++jj) heads[(s * M + jj - 1) * 32 + lane] = v[jj - 1];
+  __syncthreads();
+  double fut[M];
+#pragma unroll
+  for (int q = 0; q < M; ++q) fut[q] = 0.0;
+  for (int t = S - 1; t > s; --t) {
+    double nf[M];
+#pragma unroll
+    for (int jj = 1; jj <= M; ++jj) {
+      const double* row = T + size_t(t * SEG + jj - 1) * RS;
+      double val = heads[(t * M + jj - 1) * 32 + lane];
+#pragma unroll
+      for (int q = 1; q <= M; ++q) val = fma(__ldg(row + RL::B + q - 1), fut[q - 1], val);
+      nf[jj - 1] = val;
+    }
+#pragma unroll
+    for (int q = 0; q < M; ++q) fut[q] = nf[q];
+  }
+#pragma unroll
+  for (int k = 0; k < SEG; ++k) {
+    const double* row = T + size_t(r0 + k) * RS;
+    double u = v[k];
+#pragma unroll
+    for (int q = 1; q <= M; ++q) u = fma(__ldg(row + RL::B + q - 1), fut[q - 1], u);
+    v[k] = u;
   }
 }
 
-template <int P, bool BAND, bool SOLVE, int PRO>
-__global__ void __launch_bounds__(128) sweep_kernel(const __grid_constant__ SweepArgs A) {
-  extern __shared__ double S[];
+// Strided axes (y: ax = 1, z: ax = 2).  Lines are numbered with x fastest, so the 32 lanes of a
+// warp read 32 consecutive x of the same row: every load/store is coalesced.
+template <int P, int SEG>
+__global__ void __launch_bounds__(512, 1) seg_strided_kernel(const __grid_constant__ SweepArgs A) {
+  extern __shared__ double xch[];  // 2 * nS * (P-1) * 32
   const int c = blockIdx.y;
   if (c >= A.ncomp) return;
   const SweepComp& C = A.comp[c];
@@ -142,55 +192,104 @@ __global__ void __launch_bounds__(128) sweep_kernel(const __grid_constant__ Swee
   const int X = C.ext[0], Y = C.ext[1];
   const int L = C.ext[ax];
   const long nlines = long(X) * Y * C.ext[2] / L;
-  const int NL = A.nl;
-  const long l0 = long(blockIdx.x) * NL;
+  const long l0 = long(blockIdx.x) * 32;
   if (l0 >= nlines) return;
-  const int nl = int(min(long(NL), nlines - l0));
-  const int tid = threadIdx.x;
-  const int es = (ax == 0) ? 1 : NL;
-  const int ls = (ax == 0) ? (L | 1) : 1;
-  const long gstride = (ax == 0) ? 1 : (ax == 1 ? long(X) : long(X) * Y);
-
-  // ---- stage the lines (+ fused Ampere / Faraday update) ----
-  if (ax == 0) {
-    const int warp = tid >> 5, lane = tid & 31, nw = NL >> 5;
-    for (int j = warp; j < nl; j += nw) {
-      const long l = l0 + j;
-      const long base = l * X;
-      if (PRO == PRO_NONE) {
-        for (int i = lane; i < X; i += 32) cp_async8(&S[j * ls + i], C.in + base + i);
-      } else {
-        const int y = int(l % Y), z = int(l / Y);
-        for (int i = lane; i < X; i += 32) {
-          double v = update_value<PRO>(A.pro, c, C.in, base + i, i, y, z);
-          C.in[base + i] = v;  // the updated state d (or b)
-          S[j * ls + i] = v;
-        }
-      }
+  const int lane = threadIdx.x & 31, s = threadIdx.x >> 5;
+  const int S = (L + SEG - 1) / SEG;
+  const long l = l0 + lane;
+  const bool live = (l < nlines) && (s < S);
+  const int r0 = s * SEG;
+  const long gs = (ax == 1) ? long(X) : long(X) * Y;
+  const long base = (ax == 1) ? (l % X) + long(X) * Y * (l / X) : l;
+  const int lx = int(l % X);
+  const int lo_ = int(l / X);  // y (ax = 2) or z (ax = 1)
+  const int pro = A.pro_kind;
+  auto elem = [&](int i) -> double {
+    // value of line element i after the (optional) fused update
+    if (pro == PRO_NONE) return C.in[base + i * gs];
+    int x = lx, y = (ax == 2) ? lo_ : i, z = (ax == 2) ? i : lo_;
+    return (pro == PRO_AMPERE) ? update_value<PRO_AMPERE>(A.pro, c, C.in, base + i * gs, x, y, z)
+                               : update_value<PRO_FARADAY>(A.pro, c, C.in, base + i * gs, x, y, z);
+  };
+  double v[SEG], hl[P], hr[P];
+#pragma unroll
+  for (int k = 0; k < SEG; ++k) v[k] = (live && r0 + k < L) ? elem(r0 + k) : 0.0;
+  if (A.band) {
+#pragma unroll
+    for (int q = 0; q < P; ++q) {
+      int il = r0 - P + q, ir = r0 + SEG + q;
+      hl[q] = (live && il >= 0 && il < L) ? elem(il) : 0.0;
+      hr[q] = (live && ir < L) ? elem(ir) : 0.0;
     }
-  } else if (tid < nl) {
-    const long l = l0 + tid;
-    const long base = (ax == 1) ? (l % X) + long(X) * Y * (l / X) : l;
-    for (int i = 0; i < L; ++i) cp_async8(&S[i * es + tid], C.in + base + i * gstride);
+  } else {
+#pragma unroll
+    for (int q = 0; q < P; ++q) hl[q] = hr[q] = 0.0;
   }
-  cp_async_wait_all();
-  __syncthreads();
-
-  if (tid < nl) sweep_line<P, BAND, SOLVE>(S + tid * ls, es, L, C.tab);
-  __syncthreads();
-
-  // ---- store ----
-  const double sc = C.scale;
-  if (ax == 0) {
-    const int warp = tid >> 5, lane = tid & 31, nw = NL >> 5;
-    for (int j = warp; j < nl; j += nw) {
-      const long base = (l0 + j) * X;
-      for (int i = lane; i < X; i += 32) C.out[base + i] = sc * S[j * ls + i];
+  if (pro != PRO_NONE) {
+    __syncthreads();  // every warp has read its halo of the old state
+    if (live) {
+#pragma unroll
+      for (int k = 0; k < SEG; ++k)
+        if (r0 + k < L) C.in[base + (r0 + k) * gs] = v[k];  // updated state d (or b)
     }
-  } else if (tid < nl) {
-    const long l = l0 + tid;
-    const long base = (ax == 1) ? (l % X) + long(X) * Y * (l / X) : l;
-    for (int i = 0; i < L; ++i) C.out[base + i * gstride] = sc * S[i * es + tid];
+  }
+  seg_compute<P, SEG>(v, hl, hr, C.tab, r0, S, s, lane, xch, A.band, A.solve);
+  if (live) {
+    const double sc = C.scale;
+#pragma unroll
+    for (int k = 0; k < SEG; ++k)
+      if (r0 + k < L) C.out[base + (r0 + k) * gs] = sc * v[k];
+  }
+}
+
+// x axis: lines are contiguous rows; stage the 32-line slab in shared memory (coalesced global
+// traffic, odd pitch for conflict-free per-lane reads).
+template <int P, int SEG>
+__global__ void __launch_bounds__(512, 1) seg_x_kernel(const __grid_constant__ SweepArgs A) {
+  extern __shared__ double sm[];
+  const int c = blockIdx.y;
+  if (c >= A.ncomp) return;
+  const SweepComp& C = A.comp[c];
+  const int X = C.ext[0];
+  const int L = X;
+  const long nlines = long(C.ext[1]) * C.ext[2];
+  const long l0 = long(blockIdx.x) * 32;
+  if (l0 >= nlines) return;
+  const int nl = int(min(32L, nlines - l0));
+  const int lane = threadIdx.x & 31, s = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int S = (L + SEG - 1) / SEG;
+  const int pitch = (A.seg_pad | 1);
+  double* xch = sm;                       // 2 * nw * M * 32
+  double* slab = sm + 2 * nw * (P - 1) * 32;
+  for (int j = s; j < 32; j += nw) {
+    const double* src = C.in + (l0 + j) * X;
+    for (int i = lane; i < pitch; i += 32) slab[j * pitch + i] = (j < nl && i < X) ? src[i] : 0.0;
+  }
+  __syncthreads();
+  const int r0 = s * SEG;
+  const bool live = s < S;
+  double v[SEG], hl[P], hr[P];
+  const double* my = slab + lane * pitch;
+#pragma unroll
+  for (int k = 0; k < SEG; ++k) v[k] = (live && r0 + k < pitch) ? my[r0 + k] : 0.0;
+#pragma unroll
+  for (int q = 0; q < P; ++q) {
+    int il = r0 - P + q, ir = r0 + SEG + q;
+    hl[q] = (live && il >= 0) ? my[il] : 0.0;
+    hr[q] = (live && ir < pitch) ? my[ir] : 0.0;
+  }
+  seg_compute<P, SEG>(v, hl, hr, C.tab, r0, S, s, lane, xch, A.band, A.solve);
+  if (live) {
+    double* myw = slab + lane * pitch;
+#pragma unroll
+    for (int k = 0; k < SEG; ++k)
+      if (r0 + k < L) myw[r0 + k] = v[k];
+  }
+  __syncthreads();
+  const double sc = C.scale;
+  for (int j = s; j < nl; j += nw) {
+    double* dst = C.out + (l0 + j) * X;
+    for (int i = lane; i < X; i += 32) dst[i] = sc * slab[j * pitch + i];
   }
 }
 
@@ -425,37 +524,41 @@ __global__ void hodge_general_kernel(const __grid_constant__ HodgeArgs A) {
   }
 }
 
-template <int P, bool BAND, bool SOLVE, int PRO>
-void launch_sweep_t(const SweepArgs& a, int smem_L, cudaStream_t st) {
+template <int P, int SEG>
+void launch_seg_t(const SweepArgs& a, cudaStream_t st) {
   long maxlines = 0;
+  int Lmax = 0;
   for (int c = 0; c < a.ncomp; ++c) {
     const SweepComp& C = a.comp[c];
     long nlines = long(C.ext[0]) * C.ext[1] * C.ext[2] / C.ext[a.axis];
     maxlines = nlines > maxlines ? nlines : maxlines;
+    Lmax = C.ext[a.axis] > Lmax ? C.ext[a.axis] : Lmax;
   }
-  dim3 grid(unsigned((maxlines + a.nl - 1) / a.nl), unsigned(a.ncomp));
-  size_t smem = size_t(a.nl) * ((a.axis == 0) ? (smem_L | 1) : smem_L) * sizeof(double);
-  auto k = sweep_kernel<P, BAND, SOLVE, PRO>;
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
+  const int S = (Lmax + SEG - 1) / SEG;
+  dim3 grid(unsigned((maxlines + 31) / 32), unsigned(a.ncomp));
+  if (a.axis == 0) {
+    SweepArgs b = a;
+    b.seg_pad = S * SEG + P + 1;
+    size_t smem = (size_t(2) * S * (P - 1) * 32 + size_t(32) * (b.seg_pad | 1)) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(seg_x_kernel<P, SEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    seg_x_kernel<P, SEG><<<grid, 32 * S, smem, st>>>(b);
+  } else {
+    size_t smem = size_t(2) * S * (P - 1) * 32 * sizeof(double);
+    seg_strided_kernel<P, SEG><<<grid, 32 * S, smem, st>>>(a);
   }
-  k<<<grid, a.nl, smem, st>>>(a);
 }
 
 template <int P>
-void launch_sweep_p(bool band, bool solve, int pro, const SweepArgs& a, int smem_L, cudaStream_t st) {
-  if (pro == PRO_AMPERE) {
-    launch_sweep_t<P, true, true, PRO_AMPERE>(a, smem_L, st);
-  } else if (pro == PRO_FARADAY) {
-    launch_sweep_t<P, true, true, PRO_FARADAY>(a, smem_L, st);
-  } else if (band && solve) {
-    launch_sweep_t<P, true, true, PRO_NONE>(a, smem_L, st);
-  } else if (band) {
-    launch_sweep_t<P, true, false, PRO_NONE>(a, smem_L, st);
-  } else {
-    launch_sweep_t<P, false, true, PRO_NONE>(a, smem_L, st);
+void launch_seg_p(int seg, const SweepArgs& a, cudaStream_t st) {
+  switch (seg) {
+    case 16: launch_seg_t<P, 16>(a, st); break;
+    case 22: launch_seg_t<P, 22>(a, st); break;
+    case 26: launch_seg_t<P, 26>(a, st); break;
+    default: launch_seg_t<P, 33>(a, st); break;
   }
 }
 
@@ -463,11 +566,11 @@ void launch_sweep_p(bool band, bool solve, int pro, const SweepArgs& a, int smem
 
 int partial_blocks() { return kRedBlocks; }
 
-void launch_sweep(int p, bool band, bool solve, int pro, const SweepArgs& a, int smem_L, cudaStream_t st) {
+void launch_sweep(int p, int seg, const SweepArgs& a, cudaStream_t st) {
   switch (p) {
-    case 2: launch_sweep_p<2>(band, solve, pro, a, smem_L, st); break;
-    case 3: launch_sweep_p<3>(band, solve, pro, a, smem_L, st); break;
-    case 4: launch_sweep_p<4>(band, solve, pro, a, smem_L, st); break;
+    case 2: launch_seg_p<2>(seg, a, st); break;
+    case 3: launch_seg_p<3>(seg, a, st); break;
+    case 4: launch_seg_p<4>(seg, a, st); break;
     default: break;
   }
 }

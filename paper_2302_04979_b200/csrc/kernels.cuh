@@ -6,7 +6,7 @@
 
 namespace sgm {
 
-constexpr int kMaxLine = 1024;
+constexpr int kMaxLine = 16 * 33;  // S <= 16 segments of <= 33 rows (512 threads per CTA)
 
 // One component handled by a line sweep along `axis`.
 struct SweepComp {
@@ -35,7 +35,10 @@ struct SweepArgs {
   SweepComp comp[3];
   int ncomp;
   int axis;       // 0 = x (contiguous lines), 1 = y, 2 = z
-  int nl;         // lines per CTA (= blockDim.x)
+  int band;       // apply the banded mat-vec (mass / pairing factor)
+  int solve;      // apply the banded LU solve
+  int pro_kind;   // Prologue (strided axes only)
+  int seg_pad;    // x axis: padded slab row length (set by the launcher)
   PrologueArgs pro;
 };
 
@@ -55,7 +58,7 @@ struct HodgeArgs {
   int Q;
 };
 
-void launch_sweep(int p, bool band, bool solve, int pro, const SweepArgs& a, int smem_L, cudaStream_t st);
+void launch_sweep(int p, int seg, const SweepArgs& a, cudaStream_t st);
 void launch_update(int pro, const SweepArgs& a, cudaStream_t st);
 void launch_curl(int kind, const double* const src[3], const int sext[3][3], double* const dst[3],
                  const int dext[3][3], cudaStream_t st);

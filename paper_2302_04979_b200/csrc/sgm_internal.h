@@ -26,10 +26,10 @@ struct Axis {
   std::vector<double> xq, wq;
 };
 
-// Device line-operator tables: per (axis, op), rows of R = 4P doubles:
-//   [ band(2P+1) | lo(P-1) | upn(P-1) | dinv ]
-// band[k] = A[i][i+k-P] (a banded mat-vec, mass or pairing), lo[k-1] = L_{i,i-k},
-// upn[k-1] = U_{i,i+k}/U_{ii}, dinv = 1/U_{ii}: no-pivot banded LU (reading Z14).
+// Device line-operator tables: per (axis, op), rows of RS = 6P-2 doubles (seg_sweep.cuh):
+//   [ band(2P+1) | lo(P-1) | upn(P-1) | dinv | F(P-1) | B(P-1) ]
+// band = banded mat-vec (mass or pairing factor); lo/upn/dinv = no-pivot banded LU
+// (reading Z14); F/B = spikes of the partitioned (segmented) substitutions.
 enum Op {
   OP_EPS_OWN = 0,  // band Gamma_B^{p-1} (b), LU(Hat M)
   OP_EPS_OTH = 1,  // band Gamma_C^{p-2} (a), LU(Hat G)
@@ -65,8 +65,10 @@ struct Plan {
   size_t n_qp = 0;
   MassData mass[2];                   // [SGM_MASS_EPS], [SGM_MASS_MU]
   // device
-  double* tables_dev = nullptr;       // [3][OP_COUNT][Lmax][4P]
-  int Lmax = 0;
+  double* tables_dev = nullptr;       // [3][OP_COUNT][Lmax][6P-2]  (seg_sweep.cuh row layout)
+  int Lmax = 0;                       // rows per table slot (max padded line length)
+  int seg[3] = {0, 0, 0};             // register segment length per axis
+  int rpad[3] = {0, 0, 0};            // padded line length per axis (multiple of seg)
   double* basis_dev = nullptr;        // general Hodge: per-axis basis values at qp [n][Q][p+1]
   int* first_dev = nullptr;           // per-axis first local global index per element [n]
   size_t basis_off[3][4] = {};        // offsets (doubles) into basis_dev per axis and space
@@ -89,6 +91,7 @@ sgm_status build_axis(int p, int n, int Q, Axis& out, std::string& err);
 sgm_status banded_lu_nopivot(const std::vector<double>& A, int L, int m, std::vector<double>& LU,
                              std::string& err);
 sgm_status build_tables(Plan& P, std::string& err);
+int seg_for_line(int L);
 sgm_status build_geometry(Plan& P, std::string& err);
 void qp_coords(const Plan& P, double* xyz);
 sgm_status build_mass(Plan& P, int which, const double* values, double c, std::vector<double>& W,
