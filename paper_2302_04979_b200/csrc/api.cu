@@ -11,6 +11,7 @@
 
 #include "kernels.cuh"
 #include "sgm_internal.h"
+#include "seg_sweep.cuh"
 
 namespace sgm {
 
@@ -69,7 +70,7 @@ size_t comp_off(const Plan& P, int kind, int c) {
 }
 
 const double* table(const Plan& P, int axis, int op) {
-  return P.tables_dev + (size_t(axis) * OP_COUNT + op) * P.Lmax * (6 * P.p - 2);
+  return P.tables_dev + (size_t(axis) * OP_COUNT + op) * P.Lmax * RowLayoutRT(P.p).RS;
 }
 
 struct WS {
@@ -142,11 +143,15 @@ void sweep_pass(const Plan& P, int kind, int axis, double* const in[3], double* 
   a.band = band;
   a.solve = solve;
   a.pro_kind = pro;
+  a.tabs[0] = table(P, axis, op_own);
+  a.tabs[1] = table(P, axis, op_oth);
+  a.tab_rows = P.rpad[axis];
   for (int c = 0; c < 3; ++c) {
     comp_shape(P, kind, c, a.comp[c].ext);
     a.comp[c].in = in[c];
     a.comp[c].out = out[c];
     a.comp[c].tab = table(P, axis, own_or(axis, c, op_own, op_oth));
+    a.comp[c].tslot = own_or(axis, c, 0, 1);
     a.comp[c].scale = scale ? scale[c] : 1.0;
   }
   if (pro_args) a.pro = *pro_args;
@@ -360,7 +365,7 @@ sgm_status sgm_plan_create(const sgm_plan_desc* desc, sgm_plan* out) {
   int Q = desc->quad_points == 0 ? p + 1 : desc->quad_points;
   if (Q < p + 1 || Q > 8) return fail(SGM_E_INVALID_ARG, "quad_points must be 0 or in [p+1, 8]");
   for (int a = 0; a < 3; ++a)
-    if (desc->n_el[a] + p - 1 > kMaxLine) return fail(SGM_E_UNSUPPORTED, "line length n_el + p - 1 above 528");
+    if (desc->n_el[a] + p - 1 > kMaxLine) return fail(SGM_E_UNSUPPORTED, "line length n_el + p - 1 above 392");
   Plan* P = new (std::nothrow) Plan();
   if (!P) return fail(SGM_E_NOMEM, "out of host memory");
   P->p = p;

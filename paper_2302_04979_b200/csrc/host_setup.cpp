@@ -4,9 +4,11 @@
 // Nothing here runs per time step.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "sgm_internal.h"
+#include "seg_sweep.cuh"
 
 namespace sgm {
 
@@ -264,14 +266,15 @@ std::vector<double> transpose(const std::vector<double>& A, int L) {
   return T;
 }
 
-// Fill one line-operator table (layout: seg_sweep.cuh): Rpad rows of RS = 6P-2 doubles
-//   [band(2P+1) | lo(m) | upn(m) | dinv | F(m) | B(m)],  m = P-1.
+// Fill one line-operator table (layout: seg_sweep.cuh): Rpad rows of RowLayout<P>::RS doubles
+//   [band(2P+1) | lo(m) | F(m) | dinv, upn(m) | B(m)],  m = P-1, groups padded to 16 bytes.
 // Rows >= L are identity padding.  F/B are the spike tables of the partitioned solve for
 // segments of SEG rows: F[j-1] of row r = d z_r / d z_{r0-j}, B[j-1] = d u_r / d u_{r1+j}.
 sgm_status fill_table(double* T, int P, int L, int Rpad, int SEG, const std::vector<double>* band,
                       const std::vector<double>* lu_src, std::string& err) {
-  const int m = P - 1, RS = 6 * P - 2;
-  const int LO = 2 * P + 1, UP = LO + m, DI = UP + m, FF = DI + 1, BB = FF + m;
+  const RowLayoutRT RL(P);
+  const int m = RL.M, RS = RL.RS;
+  const int LO = RL.LO, UP = RL.UP, DI = RL.UP, FF = RL.F, BB = RL.B;  // DI: dinv sits at UP
   for (int i = 0; i < Rpad; ++i) {
     double* row = T + size_t(i) * RS;
     for (int k = 0; k < RS; ++k) row[k] = 0.0;
@@ -295,7 +298,7 @@ sgm_status fill_table(double* T, int P, int L, int Rpad, int SEG, const std::vec
     double uii = LU[size_t(i) * L + i];
     for (int k = 1; k <= m; ++k) {
       if (i - k >= 0) row[LO + k - 1] = LU[size_t(i) * L + (i - k)];
-      if (i + k < L) row[UP + k - 1] = LU[size_t(i) * L + (i + k)] / uii;
+      if (i + k < L) row[UP + k] = LU[size_t(i) * L + (i + k)] / uii;
     }
     row[DI] = 1.0 / uii;
   }
@@ -321,7 +324,7 @@ sgm_status fill_table(double* T, int P, int L, int Rpad, int SEG, const std::vec
       for (int r = r1; r >= r0; --r) {
         const double* row = T + size_t(r) * RS;
         double acc = 0.0;
-        for (int k = 1; k <= m; ++k) acc -= row[UP + k - 1] * u[(r - r0) + k];
+        for (int k = 1; k <= m; ++k) acc -= row[UP + k] * u[(r - r0) + k];
         u[r - r0] = acc;
         T[size_t(r) * RS + BB + j - 1] = acc;
       }
@@ -333,19 +336,21 @@ sgm_status fill_table(double* T, int P, int L, int Rpad, int SEG, const std::vec
 }  // namespace
 
 int seg_for_line(int L) {
-  const int cands[4] = {33, 26, 22, 16};
-  int best = 33, bw = 1 << 30;
-  for (int c : cands) {
-    int S = (L + c - 1) / c;
-    if (S > 32) continue;
-    int w = S * c - L;
-    if (w < bw) { bw = w; best = c; }
+  // segment length of the partitioned line solve: one consumer warp per segment, at most 14
+  // segments (16 warps per CTA with the producers); shortest segment that fits (more warps, fewer
+  // registers).  Override for tuning: SGM_SEG.
+  if (const char* e = getenv("SGM_SEG")) {
+    int v = atoi(e);
+    if ((v == 12 || v == 17 || v == 22 || v == 28) && (L + v - 1) / v <= 14) return v;
   }
-  return best;
+  const int cands[4] = {12, 17, 22, 28};
+  for (int c : cands)
+    if ((L + c - 1) / c <= 14) return c;
+  return 28;
 }
 
 sgm_status build_tables(Plan& P, std::string& err) {
-  const int p = P.p, RS = 6 * p - 2;
+  const int p = P.p, RS = RowLayoutRT(p).RS;
   int Rmax = 0;
   for (int a = 0; a < 3; ++a) {
     P.seg[a] = seg_for_line(P.ax[a].b);

@@ -19,6 +19,11 @@
 
 #include "kernels.cuh"
 #include "seg_sweep.cuh"
+#include "sweep_kernel.cuh"
+
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
 
 namespace sgm {
 
@@ -65,231 +70,6 @@ __device__ __forceinline__ double update_value(const PrologueArgs& P, int c, con
   } else {
     double cu = curl_comp<false>(P.src, P.sext, c, x, y, z);
     return state[idx] - P.dt * cu;                    // b - dt D1 e
-  }
-}
-
-// ---- register-segment sweep (see seg_sweep.cuh) -----------------------------------------
-template <int P, int SEG>
-__device__ __forceinline__ void seg_compute(double (&v)[SEG], const double (&hl)[P], const double (&hr)[P],
-                                            const double* __restrict__ T, int r0, int S, int s, int lane,
-                                            double* __restrict__ xch, bool band, bool solve) {
-  using RL = RowLayout<P>;
-  constexpr int M = RL::M;
-  constexpr int RS = RL::RS;
-  if (band) {
-    double w[P];
-#pragma unroll
-    for (int q = 0; q < P; ++q) w[q] = hl[q];
-#pragma unroll
-    for (int k = 0; k < SEG; ++k) {
-      const double* row = T + size_t(r0 + k) * RS;
-      const double xk = v[k];
-      // y_k = sum_{q=-P..P} A[r][r+q] x_{r+q}, summed as a short tree
-      double lsum = 0.0, rsum = 0.0;
-#pragma unroll
-      for (int q = 1; q <= P; ++q) {
-        lsum = fma(__ldg(row + P - q), w[P - q], lsum);
-        const double xr = (k + q < SEG) ? v[k + q] : hr[k + q - SEG];
-        rsum = fma(__ldg(row + P + q), xr, rsum);
-      }
-      const double y = fma(__ldg(row + P), xk, lsum + rsum);
-#pragma unroll
-      for (int q = 0; q < P - 1; ++q) w[q] = w[q + 1];
-      w[P - 1] = xk;
-      v[k] = y;
-    }
-  }
-  if (!solve) return;
-  const int nS = blockDim.x >> 5;
-  double* tails = xch;                 // [nS][M][32]
-  double* heads = xch + nS * M * 32;   // [nS][M][32]
-  // forward substitution, zero history
-#pragma unroll
-  for (int k = 0; k < SEG; ++k) {
-    const double* row = T + size_t(r0 + k) * RS;
-    double z = v[k];
-#pragma unroll
-    for (int q = M; q >= 1; --q)
-      if (k - q >= 0) z = fma(-__ldg(row + RL::LO + q - 1), v[k - q], z);
-    v[k] = z;
-  }
-#pragma unroll
-  for (int jj = 1; jj <= M; ++jj) tails[(s * M + jj - 1) * 32 + lane] = v[SEG - jj];
-  __syncthreads();
-  // true history hist[jj-1] = z_{r0-jj}: walk the previous segments' tails through the spikes
-  double hist[M];
-#pragma unroll
-  for (int q = 0; q < M; ++q) hist[q] = 0.0;
-  for (int t = 0; t < s; ++t) {
-    double nh[M];
-#pragma unroll
-    for (int jj = 1; jj <= M; ++jj) {
-      const double* row = T + size_t(t * SEG + SEG - jj) * RS;
-      double val = tails[(t * M + jj - 1) * 32 + lane];
-#pragma unroll
-      for (int q = 1; q <= M; ++q) val = fma(__ldg(row + RL::F + q - 1), hist[q - 1], val);
-      nh[jj - 1] = val;
-    }
-#pragma unroll
-    for (int q = 0; q < M; ++q) hist[q] = nh[q];
-  }
-#pragma unroll
-  for (int k = 0; k < SEG; ++k) {
-    const double* row = T + size_t(r0 + k) * RS;
-    double z = v[k];
-#pragma unroll
-    for (int q = 1; q <= M; ++q) z = fma(__ldg(row + RL::F + q - 1), hist[q - 1], z);
-    v[k] = z;
-  }
-  // backward substitution, zero future
-#pragma unroll
-  for (int k = SEG - 1; k >= 0; --k) {
-    const double* row = T + size_t(r0 + k) * RS;
-    double u = v[k] * __ldg(row + RL::DINV);
-#pragma unroll
-    for (int q = M; q >= 1; --q)
-      if (k + q < SEG) u = fma(-__ldg(row + RL::UP + q - 1), v[k + q], u);
-    v[k] = u;
-  }
-#pragma unroll
-  for (int jj = 1; jj <= M; ++jj) heads[(s * M + jj - 1) * 32 + lane] = v[jj - 1];
-  __syncthreads();
-  double fut[M];
-#pragma unroll
-  for (int q = 0; q < M; ++q) fut[q] = 0.0;
-  for (int t = S - 1; t > s; --t) {
-    double nf[M];
-#pragma unroll
-    for (int jj = 1; jj <= M; ++jj) {
-      const double* row = T + size_t(t * SEG + jj - 1) * RS;
-      double val = heads[(t * M + jj - 1) * 32 + lane];
-#pragma unroll
-      for (int q = 1; q <= M; ++q) val = fma(__ldg(row + RL::B + q - 1), fut[q - 1], val);
-      nf[jj - 1] = val;
-    }
-#pragma unroll
-    for (int q = 0; q < M; ++q) fut[q] = nf[q];
-  }
-#pragma unroll
-  for (int k = 0; k < SEG; ++k) {
-    const double* row = T + size_t(r0 + k) * RS;
-    double u = v[k];
-#pragma unroll
-    for (int q = 1; q <= M; ++q) u = fma(__ldg(row + RL::B + q - 1), fut[q - 1], u);
-    v[k] = u;
-  }
-}
-
-// Strided axes (y: ax = 1, z: ax = 2).  Lines are numbered with x fastest, so the 32 lanes of a
-// warp read 32 consecutive x of the same row: every load/store is coalesced.
-template <int P, int SEG>
-__global__ void __launch_bounds__(512, 1) seg_strided_kernel(const __grid_constant__ SweepArgs A) {
-  extern __shared__ double xch[];  // 2 * nS * (P-1) * 32
-  const int c = blockIdx.y;
-  if (c >= A.ncomp) return;
-  const SweepComp& C = A.comp[c];
-  const int ax = A.axis;
-  const int X = C.ext[0], Y = C.ext[1];
-  const int L = C.ext[ax];
-  const long nlines = long(X) * Y * C.ext[2] / L;
-  const long l0 = long(blockIdx.x) * 32;
-  if (l0 >= nlines) return;
-  const int lane = threadIdx.x & 31, s = threadIdx.x >> 5;
-  const int S = (L + SEG - 1) / SEG;
-  const long l = l0 + lane;
-  const bool live = (l < nlines) && (s < S);
-  const int r0 = s * SEG;
-  const long gs = (ax == 1) ? long(X) : long(X) * Y;
-  const long base = (ax == 1) ? (l % X) + long(X) * Y * (l / X) : l;
-  const int lx = int(l % X);
-  const int lo_ = int(l / X);  // y (ax = 2) or z (ax = 1)
-  const int pro = A.pro_kind;
-  auto elem = [&](int i) -> double {
-    // value of line element i after the (optional) fused update
-    if (pro == PRO_NONE) return C.in[base + i * gs];
-    int x = lx, y = (ax == 2) ? lo_ : i, z = (ax == 2) ? i : lo_;
-    return (pro == PRO_AMPERE) ? update_value<PRO_AMPERE>(A.pro, c, C.in, base + i * gs, x, y, z)
-                               : update_value<PRO_FARADAY>(A.pro, c, C.in, base + i * gs, x, y, z);
-  };
-  double v[SEG], hl[P], hr[P];
-#pragma unroll
-  for (int k = 0; k < SEG; ++k) v[k] = (live && r0 + k < L) ? elem(r0 + k) : 0.0;
-  if (A.band) {
-#pragma unroll
-    for (int q = 0; q < P; ++q) {
-      int il = r0 - P + q, ir = r0 + SEG + q;
-      hl[q] = (live && il >= 0 && il < L) ? elem(il) : 0.0;
-      hr[q] = (live && ir < L) ? elem(ir) : 0.0;
-    }
-  } else {
-#pragma unroll
-    for (int q = 0; q < P; ++q) hl[q] = hr[q] = 0.0;
-  }
-  if (pro != PRO_NONE) {
-    __syncthreads();  // every warp has read its halo of the old state
-    if (live) {
-#pragma unroll
-      for (int k = 0; k < SEG; ++k)
-        if (r0 + k < L) C.in[base + (r0 + k) * gs] = v[k];  // updated state d (or b)
-    }
-  }
-  seg_compute<P, SEG>(v, hl, hr, C.tab, r0, S, s, lane, xch, A.band, A.solve);
-  if (live) {
-    const double sc = C.scale;
-#pragma unroll
-    for (int k = 0; k < SEG; ++k)
-      if (r0 + k < L) C.out[base + (r0 + k) * gs] = sc * v[k];
-  }
-}
-
-// x axis: lines are contiguous rows; stage the 32-line slab in shared memory (coalesced global
-// traffic, odd pitch for conflict-free per-lane reads).
-template <int P, int SEG>
-__global__ void __launch_bounds__(512, 1) seg_x_kernel(const __grid_constant__ SweepArgs A) {
-  extern __shared__ double sm[];
-  const int c = blockIdx.y;
-  if (c >= A.ncomp) return;
-  const SweepComp& C = A.comp[c];
-  const int X = C.ext[0];
-  const int L = X;
-  const long nlines = long(C.ext[1]) * C.ext[2];
-  const long l0 = long(blockIdx.x) * 32;
-  if (l0 >= nlines) return;
-  const int nl = int(min(32L, nlines - l0));
-  const int lane = threadIdx.x & 31, s = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int S = (L + SEG - 1) / SEG;
-  const int pitch = (A.seg_pad | 1);
-  double* xch = sm;                       // 2 * nw * M * 32
-  double* slab = sm + 2 * nw * (P - 1) * 32;
-  for (int j = s; j < 32; j += nw) {
-    const double* src = C.in + (l0 + j) * X;
-    for (int i = lane; i < pitch; i += 32) slab[j * pitch + i] = (j < nl && i < X) ? src[i] : 0.0;
-  }
-  __syncthreads();
-  const int r0 = s * SEG;
-  const bool live = s < S;
-  double v[SEG], hl[P], hr[P];
-  const double* my = slab + lane * pitch;
-#pragma unroll
-  for (int k = 0; k < SEG; ++k) v[k] = (live && r0 + k < pitch) ? my[r0 + k] : 0.0;
-#pragma unroll
-  for (int q = 0; q < P; ++q) {
-    int il = r0 - P + q, ir = r0 + SEG + q;
-    hl[q] = (live && il >= 0) ? my[il] : 0.0;
-    hr[q] = (live && ir < pitch) ? my[ir] : 0.0;
-  }
-  seg_compute<P, SEG>(v, hl, hr, C.tab, r0, S, s, lane, xch, A.band, A.solve);
-  if (live) {
-    double* myw = slab + lane * pitch;
-#pragma unroll
-    for (int k = 0; k < SEG; ++k)
-      if (r0 + k < L) myw[r0 + k] = v[k];
-  }
-  __syncthreads();
-  const double sc = C.scale;
-  for (int j = s; j < nl; j += nw) {
-    double* dst = C.out + (l0 + j) * X;
-    for (int i = lane; i < X; i += 32) dst[i] = sc * slab[j * pitch + i];
   }
 }
 
@@ -524,41 +304,145 @@ __global__ void hodge_general_kernel(const __grid_constant__ HodgeArgs A) {
   }
 }
 
-template <int P, int SEG>
-void launch_seg_t(const SweepArgs& a, cudaStream_t st) {
-  long maxlines = 0;
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* s = getenv(name);
+  return s ? atoi(s) : dflt;
+}
+
+template <int P, int SEG, int LPT, int MODE, int OPS>
+bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
+  using sweep::Cfg;
+  Cfg cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  constexpr int TW = 32 * LPT;
   int Lmax = 0;
-  for (int c = 0; c < a.ncomp; ++c) {
+  for (int c = 0; c < 3; ++c) {
+    if (c >= a.ncomp) continue;
     const SweepComp& C = a.comp[c];
-    long nlines = long(C.ext[0]) * C.ext[1] * C.ext[2] / C.ext[a.axis];
-    maxlines = nlines > maxlines ? nlines : maxlines;
-    Lmax = C.ext[a.axis] > Lmax ? C.ext[a.axis] : Lmax;
+    sweep::CompGeom& g = cfg.g[c];
+    const int X = C.ext[0], Y = C.ext[1], Z = C.ext[2];
+    g.L = C.ext[a.axis];
+    g.magic = 0xffffffffu / unsigned(X);
+    g.nlines = X * Y * Z / g.L;
+    g.X = X;
+    g.rowlen = X;
+    g.gs = (a.axis == 0) ? 1 : (a.axis == 1 ? X : X * Y);
+    g.os = (a.axis == 1) ? X * Y : X;  // transverse index l / X: z (y pass) or y (z pass)
+    cfg.tiles[c] = (g.nlines + TW - 1) / TW;
+    cfg.nitems += cfg.tiles[c];
+    Lmax = g.L > Lmax ? g.L : Lmax;
   }
-  const int S = (Lmax + SEG - 1) / SEG;
-  dim3 grid(unsigned((maxlines + 31) / 32), unsigned(a.ncomp));
-  if (a.axis == 0) {
-    SweepArgs b = a;
-    b.seg_pad = S * SEG + P + 1;
-    size_t smem = (size_t(2) * S * (P - 1) * 32 + size_t(32) * (b.seg_pad | 1)) * sizeof(double);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(seg_x_kernel<P, SEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
-    }
-    seg_x_kernel<P, SEG><<<grid, 32 * S, smem, st>>>(b);
+  cfg.NC = (Lmax + SEG - 1) / SEG;
+  cfg.rows = cfg.NC * SEG + P;
+  // x axis: a tile of whole lines is one contiguous range -> one bulk copy in and one out (TMA
+  // engine), if the component bases are 16-byte aligned and the component has an even size.
+  // (Strided tiles are many small row runs: measured slower on the bulk engine than cp.async.)
+  bool bulk = (MODE == 3) && env_int("SGM_BULK", 1) != 0;
+  for (int c = 0; c < a.ncomp && bulk; ++c) {
+    const SweepComp& C = a.comp[c];
+    if ((reinterpret_cast<uintptr_t>(C.in) & 15) || (reinterpret_cast<uintptr_t>(C.out) & 15)) bulk = false;
+    if ((long(C.ext[0]) * C.ext[1] * C.ext[2]) & 1) bulk = false;
+  }
+  cfg.bulk = bulk ? 1 : 0;
+  if (bulk) cfg.NP = 1;
+  else cfg.NP = (MODE == 1 || MODE == 2) ? env_int("SGM_NP_UPD", 16 - cfg.NC) : env_int("SGM_NP", MODE == 3 ? 4 : 2);
+  if (cfg.NP < 1) cfg.NP = 1;
+  if (cfg.NC + cfg.NP > 16) cfg.NP = 16 - cfg.NC;
+  if (cfg.NP < 1) return false;
+  if (MODE == 3) {
+    cfg.pitch = bulk ? Lmax : (cfg.rows | 1);  // bulk: whole-tile copy, pitch = line length
+    cfg.W = 0;
+    cfg.slab = TW * cfg.pitch + cfg.rows + 2;
   } else {
-    size_t smem = size_t(2) * S * (P - 1) * 32 * sizeof(double);
-    seg_strided_kernel<P, SEG><<<grid, 32 * S, smem, st>>>(a);
+    cfg.pitch = 0;
+    cfg.W = TW;
+    cfg.slab = cfg.W * cfg.rows;
   }
+  cfg.slab = (cfg.slab + 1) & ~1;  // keep every slab 16-byte aligned
+  cfg.ntabs = (a.tabs[1] != nullptr && a.tabs[1] != a.tabs[0]) ? 2 : 1;
+  cfg.tab_dbl = a.tab_rows * RowLayout<P>::RS;
+  cfg.dbg = env_int("SGM_PIPE_DBG", 0);
+  if (MODE == 1 || MODE == 2) {
+    for (int c = 0; c < 3; ++c) {
+      // (D x)_c = d_{a1} x_{c1} - d_{a2} x_{c2}, (a1, c1) = (c+1, c+2), (a2, c2) = (c+2, c+1)
+      const int a1 = (c + 1) % 3, c1 = (c + 2) % 3, a2 = (c + 2) % 3, c2 = (c + 1) % 3;
+      const int aa[2] = {a1, a2}, cc[2] = {c1, c2};
+      for (int t = 0; t < 2; ++t) {
+        auto& T = cfg.term[c][t];
+        T.src = a.pro.src[cc[t]];
+        T.X = a.pro.sext[cc[t]][0];
+        T.Y = a.pro.sext[cc[t]][1];
+        T.a = aa[t];
+        T.ext_a = a.pro.sext[cc[t]][aa[t]];
+        T.sign = t == 0 ? 1 : -1;
+      }
+    }
+  }
+  constexpr int M = P - 1;
+  const size_t smem = (size_t(cfg.ntabs) * cfg.tab_dbl + size_t(2) * cfg.slab + size_t(2) * cfg.NC * M * TW + 2) *
+                      sizeof(double);
+  if (smem > 227 * 1024) return false;
+  const int NT = (cfg.NC + cfg.NP) * 32;
+  static int attr_done = 0;
+  if (!attr_done) {
+    cudaFuncSetAttribute(sweep::sweep_kernel<P, SEG, LPT, MODE, OPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    attr_done = 1;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep::sweep_kernel<P, SEG, LPT, MODE, OPS>, NT, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int cap = env_int("SGM_CTAS_PER_SM", 0);
+  if (cap > 0 && cap < per_sm) per_sm = cap;
+  long grid = long(per_sm) * sm_count();
+  if (grid > cfg.nitems) grid = cfg.nitems;
+  if (grid < 1) grid = 1;
+  sweep::sweep_kernel<P, SEG, LPT, MODE, OPS><<<unsigned(grid), NT, smem, st>>>(a, cfg);
+  return true;
+}
+
+template <int P, int SEG, int MODE, int OPS>
+void launch_sweep_m(const SweepArgs& a, cudaStream_t st) {
+  // two lines per thread when the register budget allows (SEG <= 17) and the slabs fit
+  if constexpr (SEG <= 17) {
+    if (env_int("SGM_LPT", 2) == 2 && launch_sweep_t<P, SEG, 2, MODE, OPS>(a, st)) return;
+  }
+  launch_sweep_t<P, SEG, 1, MODE, OPS>(a, st);
+}
+
+template <int P, int SEG, int MODE>
+void launch_sweep_o(const SweepArgs& a, cudaStream_t st) {
+  if (a.band && a.solve) launch_sweep_m<P, SEG, MODE, 3>(a, st);
+  else if (a.solve) launch_sweep_m<P, SEG, MODE, 2>(a, st);
+  else launch_sweep_m<P, SEG, MODE, 1>(a, st);
+}
+
+template <int P, int SEG>
+void launch_sweep_s(const SweepArgs& a, cudaStream_t st) {
+  if (a.axis == 0) launch_sweep_o<P, SEG, 3>(a, st);
+  else if (a.pro_kind == PRO_AMPERE) launch_sweep_m<P, SEG, 1, 3>(a, st);
+  else if (a.pro_kind == PRO_FARADAY) launch_sweep_m<P, SEG, 2, 3>(a, st);
+  else launch_sweep_o<P, SEG, 0>(a, st);
 }
 
 template <int P>
-void launch_seg_p(int seg, const SweepArgs& a, cudaStream_t st) {
+void launch_sweep_p(int seg, const SweepArgs& a, cudaStream_t st) {
   switch (seg) {
-    case 16: launch_seg_t<P, 16>(a, st); break;
-    case 22: launch_seg_t<P, 22>(a, st); break;
-    case 26: launch_seg_t<P, 26>(a, st); break;
-    default: launch_seg_t<P, 33>(a, st); break;
+    case 12: launch_sweep_s<P, 12>(a, st); break;
+    case 17: launch_sweep_s<P, 17>(a, st); break;
+    case 22: launch_sweep_s<P, 22>(a, st); break;
+    default: launch_sweep_s<P, 28>(a, st); break;
   }
 }
 
@@ -568,9 +452,9 @@ int partial_blocks() { return kRedBlocks; }
 
 void launch_sweep(int p, int seg, const SweepArgs& a, cudaStream_t st) {
   switch (p) {
-    case 2: launch_seg_p<2>(seg, a, st); break;
-    case 3: launch_seg_p<3>(seg, a, st); break;
-    case 4: launch_seg_p<4>(seg, a, st); break;
+    case 2: launch_sweep_p<2>(seg, a, st); break;
+    case 3: launch_sweep_p<3>(seg, a, st); break;
+    case 4: launch_sweep_p<4>(seg, a, st); break;
     default: break;
   }
 }

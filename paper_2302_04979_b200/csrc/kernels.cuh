@@ -6,13 +6,14 @@
 
 namespace sgm {
 
-constexpr int kMaxLine = 16 * 33;  // S <= 16 segments of <= 33 rows (512 threads per CTA)
+constexpr int kMaxLine = 392;  // <= 14 segments of <= 28 rows (sweep_kernel.cuh)
 
 // One component handled by a line sweep along `axis`.
 struct SweepComp {
   double* in;         // input component array [z][y][x] (updated in place by a prologue)
   double* out;        // output component array (may equal in)
-  const double* tab;  // line-operator table (rows of 4P doubles), see sgm_internal.h
+  const double* tab;  // line-operator table (seg_sweep.cuh rows), global memory
+  int tslot;          // which of SweepArgs::tabs this component uses (staged in shared memory)
   int ext[3];         // component extents (x, y, z)
   double scale;       // multiplies the stored result
 };
@@ -38,7 +39,9 @@ struct SweepArgs {
   int band;       // apply the banded mat-vec (mass / pairing factor)
   int solve;      // apply the banded LU solve
   int pro_kind;   // Prologue (strided axes only)
-  int seg_pad;    // x axis: padded slab row length (set by the launcher)
+  int seg_pad;    // unused (kept for layout stability)
+  const double* tabs[2];  // the (at most two) distinct line-operator tables of this pass
+  int tab_rows;           // rows per table (padded line length of this axis)
   PrologueArgs pro;
 };
 

@@ -26,8 +26,8 @@ struct Axis {
   std::vector<double> xq, wq;
 };
 
-// Device line-operator tables: per (axis, op), rows of RS = 6P-2 doubles (seg_sweep.cuh):
-//   [ band(2P+1) | lo(P-1) | upn(P-1) | dinv | F(P-1) | B(P-1) ]
+// Device line-operator tables: per (axis, op), rows of RowLayout<P>::RS doubles (seg_sweep.cuh):
+//   [ band(2P+1) | lo(P-1) | F(P-1) | dinv, upn(P-1) | B(P-1) ]  (groups padded to 16 bytes)
 // band = banded mat-vec (mass or pairing factor); lo/upn/dinv = no-pivot banded LU
 // (reading Z14); F/B = spikes of the partitioned (segmented) substitutions.
 enum Op {
@@ -65,7 +65,7 @@ struct Plan {
   size_t n_qp = 0;
   MassData mass[2];                   // [SGM_MASS_EPS], [SGM_MASS_MU]
   // device
-  double* tables_dev = nullptr;       // [3][OP_COUNT][Lmax][6P-2]  (seg_sweep.cuh row layout)
+  double* tables_dev = nullptr;       // [3][OP_COUNT][Lmax][RS]  (seg_sweep.cuh row layout)
   int Lmax = 0;                       // rows per table slot (max padded line length)
   int seg[3] = {0, 0, 0};             // register segment length per axis
   int rpad[3] = {0, 0, 0};            // padded line length per axis (multiple of seg)
