@@ -5,6 +5,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <string>
@@ -146,6 +147,9 @@ void sweep_pass(const Plan& P, int kind, int axis, double* const in[3], double* 
   a.tabs[0] = table(P, axis, op_own);
   a.tabs[1] = table(P, axis, op_oth);
   a.tab_rows = P.rpad[axis];
+  a.band_hw = std::max(P.band_hw[axis][op_own], P.band_hw[axis][op_oth]);
+  a.spike_kh = std::max(P.spike_kh[axis][op_own], P.spike_kh[axis][op_oth]);
+  a.spike_kf = std::max(P.spike_kf[axis][op_own], P.spike_kf[axis][op_oth]);
   for (int c = 0; c < 3; ++c) {
     comp_shape(P, kind, c, a.comp[c].ext);
     a.comp[c].in = in[c];
@@ -323,7 +327,17 @@ void step_once(Plan& P, double* d, double* e, double* b, double* h, const double
     const MassData& M = P.mass[mass];
     comps_of(P, kind, w.t, T);
     if (M.kind == HODGE_SEPARABLE) {
-      { ProfScope ps(P, kx, st); sweep_pass(P, kind, 2, state, T, own, oth, nullptr, true, true, pro, &pa, st); }
+      // streaming update kernel, then the three mass . solve sweeps (z, y, x)
+      SweepArgs a;
+      std::memset(&a, 0, sizeof(a));
+      a.ncomp = 3;
+      for (int c = 0; c < 3; ++c) {
+        comp_shape(P, kind, c, a.comp[c].ext);
+        a.comp[c].in = state[c];
+      }
+      a.pro = pa;
+      { ProfScope ps(P, SGM_K_UPDATE, st); launch_update(pro, a, st); }
+      { ProfScope ps(P, kx, st); sweep_pass(P, kind, 2, state, T, own, oth, nullptr, true, true, PRO_NONE, nullptr, st); }
       { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, true, true, PRO_NONE, nullptr, st); }
       { ProfScope ps(P, kz, st); sweep_pass(P, kind, 0, T, outv, own, oth, M.scale, true, true, PRO_NONE, nullptr, st); }
     } else {
@@ -517,7 +531,8 @@ sgm_status sgm_workspace_bytes(sgm_plan plan, size_t* bytes) {
 sgm_status sgm_plan_kernels_per_step(sgm_plan plan, int* n) {
   if (!plan || !n) return fail(SGM_E_INVALID_ARG, "NULL argument");
   int k = 0;
-  for (int m = 0; m < 2; ++m) k += (PL(plan)->mass[m].kind == HODGE_SEPARABLE) ? 3 : 5;
+  for (int m = 0; m < 2; ++m)
+    k += (PL(plan)->mass[m].kind == HODGE_SEPARABLE) ? 4 : 5;
   *n = k;
   return SGM_OK;
 }

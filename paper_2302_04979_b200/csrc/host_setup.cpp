@@ -285,6 +285,11 @@ sgm_status fill_table(double* T, int P, int L, int Rpad, int SEG, const std::vec
         int j = i + k;
         if (j >= 0 && j < L) row[k + P] = (*band)[size_t(i) * L + j];
       }
+      for (int j = 0; j < L; ++j)  // entries outside the stored band must vanish exactly
+        if (std::abs(j - i) > P && (*band)[size_t(i) * L + j] != 0.0) {
+          err = "1D band matrix wider than the compiled band";
+          return SGM_E_UNSUPPORTED;
+        }
     } else {
       row[P] = 1.0;
     }
@@ -333,6 +338,68 @@ sgm_status fill_table(double* T, int P, int L, int Rpad, int SEG, const std::vec
   return SGM_OK;
 }
 
+// Largest |q| with a nonzero band coefficient in any row (the table's band half-width).
+int table_band_hw(const double* T, int P, int L) {
+  const RowLayoutRT RL(P);
+  int hw = 0;
+  for (int i = 0; i < L; ++i)
+    for (int q = -P; q <= P; ++q)
+      if (T[size_t(i) * RL.RS + RL.BAND + q + P] != 0.0) hw = std::max(hw, std::abs(q));
+  return hw;
+}
+
+// Truncated SPIKE reach (reading Z23 in DESIGN.md): the true history of segment s is
+//   hist_s = tail_{s-1} + Fm_{s-1} hist_{s-1},   Fm_t[jj][q] = F[t*SEG + SEG - jj][q]
+// so starting the scan K segments back with a zero history leaves the error
+// (Fm_{s-1} ... Fm_{s-K}) hist_{s-K}.  The spikes of the B-spline pairing factors decay
+// geometrically; K is the smallest reach with every such product below 1e-17 in the infinity
+// norm (likewise for the backward spikes Bm_t[jj][q] = B[t*SEG + jj - 1][q]).  K >= S means no
+// truncation.
+void spike_reach(const double* T, int P, int L, int SEG, int& kh, int& kf) {
+  const RowLayoutRT RL(P);
+  const int m = RL.M, RS = RL.RS;
+  const int S = (L + SEG - 1) / SEG;
+  auto mat = [&](int t, bool fwd, std::vector<double>& A) {
+    A.assign(size_t(m) * m, 0.0);
+    for (int jj = 1; jj <= m; ++jj)
+      for (int q = 1; q <= m; ++q) {
+        const int row = fwd ? t * SEG + SEG - jj : t * SEG + jj - 1;
+        A[size_t(jj - 1) * m + (q - 1)] = T[size_t(row) * RS + (fwd ? RL.F : RL.B) + q - 1];
+      }
+  };
+  auto reach = [&](bool fwd) {
+    std::vector<double> A, Pm, Q;
+    for (int K = 1; K < S; ++K) {
+      double worst = 0.0;
+      for (int s = 0; s < S; ++s) {
+        // fwd: Fm_{s-1} ... Fm_{s-K} (exact when s - K <= 0); bwd: Bm_{s+1} ... Bm_{s+K} (exact when s + K >= S - 1)
+        if (fwd ? (s - K <= 0) : (s + K >= S - 1)) continue;
+        Pm.assign(size_t(m) * m, 0.0);
+        for (int i = 0; i < m; ++i) Pm[size_t(i) * m + i] = 1.0;
+        for (int i = 1; i <= K; ++i) {
+          mat(fwd ? s - i : s + i, fwd, A);
+          Q.assign(size_t(m) * m, 0.0);
+          for (int x = 0; x < m; ++x)
+            for (int y = 0; y < m; ++y)
+              for (int z = 0; z < m; ++z) Q[size_t(x) * m + y] += Pm[size_t(x) * m + z] * A[size_t(z) * m + y];
+          Pm = Q;
+        }
+        double nrm = 0.0;
+        for (int x = 0; x < m; ++x) {
+          double r = 0.0;
+          for (int y = 0; y < m; ++y) r += std::fabs(Pm[size_t(x) * m + y]);
+          nrm = std::max(nrm, r);
+        }
+        worst = std::max(worst, nrm);
+      }
+      if (worst <= 1e-17) return K;
+    }
+    return S;
+  };
+  kh = reach(true);
+  kf = reach(false);
+}
+
 }  // namespace
 
 int seg_for_line(int L) {
@@ -341,9 +408,9 @@ int seg_for_line(int L) {
   // registers).  Override for tuning: SGM_SEG.
   if (const char* e = getenv("SGM_SEG")) {
     int v = atoi(e);
-    if ((v == 12 || v == 17 || v == 22 || v == 28) && (L + v - 1) / v <= 14) return v;
+    if ((v == 12 || v == 17 || v == 28) && (L + v - 1) / v <= 14) return v;
   }
-  const int cands[4] = {12, 17, 22, 28};
+  const int cands[3] = {12, 17, 28};
   for (int c : cands)
     if ((L + c - 1) / c <= 14) return c;
   return 28;
@@ -359,6 +426,7 @@ sgm_status build_tables(Plan& P, std::string& err) {
   }
   P.Lmax = Rmax;  // rows per table slot
   P.tables_host.assign(size_t(3) * OP_COUNT * Rmax * RS, 0.0);
+  const char* noskip = getenv("SGM_SPIKE_FULL");
   for (int a = 0; a < 3; ++a) {
     const Axis& X = P.ax[a];
     const int R = P.rpad[a], SEG = P.seg[a];
@@ -373,6 +441,16 @@ sgm_status build_tables(Plan& P, std::string& err) {
     if ((st = fill_table(T(OP_APPLY_G), p, X.a, R, SEG, &X.G, nullptr, err)) != SGM_OK) return st;
     if ((st = fill_table(T(OP_APPLY_GT), p, X.a, R, SEG, &GT, nullptr, err)) != SGM_OK) return st;
     if ((st = fill_table(T(OP_APPLY_MT), p, X.b, R, SEG, &MT, nullptr, err)) != SGM_OK) return st;
+    const int Ls[OP_COUNT] = {X.b, X.a, X.a, X.b, X.b, X.a, X.a, X.b};
+    for (int op = 0; op < OP_COUNT; ++op) {
+      const int S = (Ls[op] + SEG - 1) / SEG;
+      P.band_hw[a][op] = table_band_hw(T(op), p, Ls[op]);
+      if (noskip || op >= OP_APPLY_M) {
+        P.spike_kh[a][op] = P.spike_kf[a][op] = S;
+      } else {
+        spike_reach(T(op), p, Ls[op], SEG, P.spike_kh[a][op], P.spike_kf[a][op]);
+      }
+    }
   }
   return SGM_OK;
 }

@@ -24,6 +24,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <utility>
 
 namespace sgm {
 
@@ -73,18 +74,98 @@ __device__ __forceinline__ double update_value(const PrologueArgs& P, int c, con
   }
 }
 
-// element-wise update (general-Hodge path): same arithmetic as the fused prologue
+// ---- element-wise Ampere / Faraday update (eqs. discrete2_ampere / _faraday) ----
+//   AMPERE : d_c <- d_c + dt ((D~1 h)_c - s j_c)     dual   (dv)_k = v_{k+1} - v_k
+//   FARADAY: b_c <- b_c - dt (D1 e)_c                primal (du)_k = u_k - u_{k-1}, u_{-1} = u_a = 0
+// Streaming kernel: consecutive threads take consecutive elements of a component (coalesced),
+// each thread U elements 256 apart with all loads issued before use (U * 6 loads in flight).
+struct UpdTerm {
+  const double* src;
+  int X, Y;   // src extents x, y
+  int ext_a;  // src extent along the differentiated axis
+  int a;      // differentiated axis
+};
+struct UpdComp {
+  double* state;
+  const double* jhat;
+  int X, Y, N;          // component extents x, y and size
+  unsigned mX, mY;      // floor((2^32-1)/X), floor((2^32-1)/Y)
+  int chunk0;           // first chunk (256*U elements) of this component
+  UpdTerm t[2];         // (D x)_c = d_{a1} x_{c1} - d_{a2} x_{c2}
+};
+struct UpdArgs {
+  UpdComp c[3];
+  const double* s_ptr;
+  double dt;
+  int nchunks;
+};
+
+__device__ __forceinline__ unsigned fdiv(unsigned n, unsigned d, unsigned m, unsigned& r) {
+  unsigned q = __umulhi(n, m);
+  r = n - q * d;
+  if (r >= d) { ++q; r -= d; }
+  return q;
+}
+
 template <int PRO>
-__global__ void update_kernel(const __grid_constant__ SweepArgs A) {
-  const int c = blockIdx.y;
-  const SweepComp& C = A.comp[c];
-  const int X = C.ext[0], Y = C.ext[1], Z = C.ext[2];
-  const long N = long(X) * Y * Z;
-  for (long idx = long(blockIdx.x) * blockDim.x + threadIdx.x; idx < N; idx += long(gridDim.x) * blockDim.x) {
-    int x = int(idx % X);
-    long r = idx / X;
-    int y = int(r % Y), z = int(r / Y);
-    C.in[idx] = update_value<PRO>(A.pro, c, C.in, idx, x, y, z);
+__global__ void __launch_bounds__(256) update_kernel(const __grid_constant__ UpdArgs A) {
+  constexpr bool DUAL = (PRO == PRO_AMPERE);
+  constexpr int U = 4;
+  pipe::griddep_launch_dependents();
+  pipe::griddep_wait();
+  for (int ch = blockIdx.x; ch < A.nchunks; ch += gridDim.x) {
+    const int c = (ch >= A.c[2].chunk0) ? 2 : (ch >= A.c[1].chunk0 ? 1 : 0);
+    const UpdComp& C = A.c[c];
+    const int e0 = (ch - C.chunk0) * (256 * U) + threadIdx.x;
+    double vh[U][2], vl[U][2], old[U], jv[U];
+    bool okh[U][2], okl[U][2];
+    int idx[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int e = min(e0 + 256 * k, C.N - 1);
+      idx[k] = e;
+      unsigned x, y, z, r;
+      const unsigned q = fdiv(unsigned(e), unsigned(C.X), C.mX, x);
+      z = fdiv(q, unsigned(C.Y), C.mY, y);
+      (void)r;
+      const int p[3] = {int(x), int(y), int(z)};
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const UpdTerm& T = C.t[t];
+        const int base = p[0] + T.X * (p[1] + T.Y * p[2]);
+        const int da = (T.a == 0) ? 1 : (T.a == 1 ? T.X : T.X * T.Y);
+        const int pa = p[T.a];
+        int ih, il;
+        if (DUAL) {
+          ih = base + da;
+          il = base;
+          okh[k][t] = okl[k][t] = true;
+        } else {
+          okh[k][t] = pa < T.ext_a;
+          okl[k][t] = pa >= 1;
+          ih = okh[k][t] ? base : base - da;
+          il = okl[k][t] ? base - da : base;
+        }
+        vh[k][t] = __ldg(T.src + ih);
+        vl[k][t] = __ldg(T.src + il);
+      }
+      old[k] = C.state[e];
+      jv[k] = (DUAL && C.jhat) ? __ldg(C.jhat + e) : 0.0;
+    }
+    const double dt = A.dt;
+    const double sdt = (DUAL && C.jhat) ? dt * (A.s_ptr ? __ldg(A.s_ptr) : 1.0) : 0.0;
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      double d[2];
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+        const double h = okh[k][t] ? vh[k][t] : 0.0, l = okl[k][t] ? vl[k][t] : 0.0;
+        d[t] = h - l;
+      }
+      const double cu = d[0] - d[1];
+      const double val = DUAL ? fma(-sdt, jv[k], fma(dt, cu, old[k])) : fma(-dt, cu, old[k]);
+      if (e0 + 256 * k < C.N) C.state[idx[k]] = val;
+    }
   }
 }
 
@@ -304,6 +385,30 @@ __global__ void hodge_general_kernel(const __grid_constant__ HodgeArgs A) {
   }
 }
 
+int env_int(const char* name, int dflt) {
+  const char* s = getenv(name);
+  return s ? atoi(s) : dflt;
+}
+
+// Launch with programmatic stream serialization (PDL): the kernel may be scheduled while the
+// previous kernel in the stream drains; it calls griddepcontrol.wait before touching its inputs.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                Args&&... args) {
+  cudaLaunchConfig_t lc;
+  std::memset(&lc, 0, sizeof(lc));
+  lc.gridDim = dim3(grid);
+  lc.blockDim = dim3(block);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = env_int("SGM_PDL", 1) ? 1 : 0;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  cudaLaunchKernelEx(&lc, kernel, std::forward<Args>(args)...);
+}
+
 int sm_count() {
   static int n = 0;
   if (!n) {
@@ -315,12 +420,8 @@ int sm_count() {
   return n;
 }
 
-int env_int(const char* name, int dflt) {
-  const char* s = getenv(name);
-  return s ? atoi(s) : dflt;
-}
 
-template <int P, int SEG, int LPT, int MODE, int OPS>
+template <int P, int HB, int SEG, int LPT, int MODE, int OPS>
 bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
   using sweep::Cfg;
   Cfg cfg;
@@ -356,7 +457,7 @@ bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
   }
   cfg.bulk = bulk ? 1 : 0;
   if (bulk) cfg.NP = 1;
-  else cfg.NP = (MODE == 1 || MODE == 2) ? env_int("SGM_NP_UPD", 16 - cfg.NC) : env_int("SGM_NP", MODE == 3 ? 4 : 2);
+  else cfg.NP = env_int("SGM_NP", 4);
   if (cfg.NP < 1) cfg.NP = 1;
   if (cfg.NC + cfg.NP > 16) cfg.NP = 16 - cfg.NC;
   if (cfg.NP < 1) return false;
@@ -373,66 +474,55 @@ bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
   cfg.ntabs = (a.tabs[1] != nullptr && a.tabs[1] != a.tabs[0]) ? 2 : 1;
   cfg.tab_dbl = a.tab_rows * RowLayout<P>::RS;
   cfg.dbg = env_int("SGM_PIPE_DBG", 0);
-  if (MODE == 1 || MODE == 2) {
-    for (int c = 0; c < 3; ++c) {
-      // (D x)_c = d_{a1} x_{c1} - d_{a2} x_{c2}, (a1, c1) = (c+1, c+2), (a2, c2) = (c+2, c+1)
-      const int a1 = (c + 1) % 3, c1 = (c + 2) % 3, a2 = (c + 2) % 3, c2 = (c + 1) % 3;
-      const int aa[2] = {a1, a2}, cc[2] = {c1, c2};
-      for (int t = 0; t < 2; ++t) {
-        auto& T = cfg.term[c][t];
-        T.src = a.pro.src[cc[t]];
-        T.X = a.pro.sext[cc[t]][0];
-        T.Y = a.pro.sext[cc[t]][1];
-        T.a = aa[t];
-        T.ext_a = a.pro.sext[cc[t]][aa[t]];
-        T.sign = t == 0 ? 1 : -1;
-      }
-    }
-  }
   constexpr int M = P - 1;
-  const size_t smem = (size_t(cfg.ntabs) * cfg.tab_dbl + size_t(2) * cfg.slab + size_t(2) * cfg.NC * M * TW + 2) *
+  const size_t smem = (size_t(cfg.ntabs) * cfg.tab_dbl + size_t(2) * cfg.slab + size_t(2) * cfg.NC * M * TW + 4) *
                       sizeof(double);
   if (smem > 227 * 1024) return false;
   const int NT = (cfg.NC + cfg.NP) * 32;
   static int attr_done = 0;
   if (!attr_done) {
-    cudaFuncSetAttribute(sweep::sweep_kernel<P, SEG, LPT, MODE, OPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(sweep::sweep_kernel<P, HB, SEG, LPT, MODE, OPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          227 * 1024);
     attr_done = 1;
   }
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep::sweep_kernel<P, SEG, LPT, MODE, OPS>, NT, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep::sweep_kernel<P, HB, SEG, LPT, MODE, OPS>, NT, smem);
   if (per_sm < 1) per_sm = 1;
   const int cap = env_int("SGM_CTAS_PER_SM", 0);
   if (cap > 0 && cap < per_sm) per_sm = cap;
   long grid = long(per_sm) * sm_count();
   if (grid > cfg.nitems) grid = cfg.nitems;
   if (grid < 1) grid = 1;
-  sweep::sweep_kernel<P, SEG, LPT, MODE, OPS><<<unsigned(grid), NT, smem, st>>>(a, cfg);
+  launch_pdl(sweep::sweep_kernel<P, HB, SEG, LPT, MODE, OPS>, unsigned(grid), unsigned(NT), smem, st, a, cfg);
   return true;
 }
 
-template <int P, int SEG, int MODE, int OPS>
+template <int P, int HB, int SEG, int MODE, int OPS>
 void launch_sweep_m(const SweepArgs& a, cudaStream_t st) {
   // two lines per thread when the register budget allows (SEG <= 17) and the slabs fit
   if constexpr (SEG <= 17) {
-    if (env_int("SGM_LPT", 2) == 2 && launch_sweep_t<P, SEG, 2, MODE, OPS>(a, st)) return;
+    if (env_int("SGM_LPT", 2) == 2 && launch_sweep_t<P, HB, SEG, 2, MODE, OPS>(a, st)) return;
   }
-  launch_sweep_t<P, SEG, 1, MODE, OPS>(a, st);
+  launch_sweep_t<P, HB, SEG, 1, MODE, OPS>(a, st);
 }
 
 template <int P, int SEG, int MODE>
 void launch_sweep_o(const SweepArgs& a, cudaStream_t st) {
-  if (a.band && a.solve) launch_sweep_m<P, SEG, MODE, 3>(a, st);
-  else if (a.solve) launch_sweep_m<P, SEG, MODE, 2>(a, st);
-  else launch_sweep_m<P, SEG, MODE, 1>(a, st);
+  // band half-width: P - 1 for the eps-side Grams and the pairing factors, P for the mu-side Gram
+  if (a.band && a.solve) {
+    if (a.band_hw >= P) launch_sweep_m<P, P, SEG, MODE, 3>(a, st);
+    else launch_sweep_m<P, P - 1, SEG, MODE, 3>(a, st);
+  } else if (a.solve) {
+    launch_sweep_m<P, P - 1, SEG, MODE, 2>(a, st);
+  } else {
+    if (a.band_hw >= P) launch_sweep_m<P, P, SEG, MODE, 1>(a, st);
+    else launch_sweep_m<P, P - 1, SEG, MODE, 1>(a, st);
+  }
 }
 
 template <int P, int SEG>
 void launch_sweep_s(const SweepArgs& a, cudaStream_t st) {
   if (a.axis == 0) launch_sweep_o<P, SEG, 3>(a, st);
-  else if (a.pro_kind == PRO_AMPERE) launch_sweep_m<P, SEG, 1, 3>(a, st);
-  else if (a.pro_kind == PRO_FARADAY) launch_sweep_m<P, SEG, 2, 3>(a, st);
   else launch_sweep_o<P, SEG, 0>(a, st);
 }
 
@@ -441,7 +531,6 @@ void launch_sweep_p(int seg, const SweepArgs& a, cudaStream_t st) {
   switch (seg) {
     case 12: launch_sweep_s<P, 12>(a, st); break;
     case 17: launch_sweep_s<P, 17>(a, st); break;
-    case 22: launch_sweep_s<P, 22>(a, st); break;
     default: launch_sweep_s<P, 28>(a, st); break;
   }
 }
@@ -460,9 +549,38 @@ void launch_sweep(int p, int seg, const SweepArgs& a, cudaStream_t st) {
 }
 
 void launch_update(int pro, const SweepArgs& a, cudaStream_t st) {
-  dim3 grid(4 * 148, a.ncomp);
-  if (pro == PRO_AMPERE) update_kernel<PRO_AMPERE><<<grid, 256, 0, st>>>(a);
-  else update_kernel<PRO_FARADAY><<<grid, 256, 0, st>>>(a);
+  UpdArgs U;
+  std::memset(&U, 0, sizeof(U));
+  constexpr int CH = 256 * 4;
+  int chunk = 0;
+  for (int c = 0; c < 3; ++c) {
+    UpdComp& C = U.c[c];
+    C.state = a.comp[c].in;
+    C.jhat = (pro == PRO_AMPERE) ? a.pro.jhat[c] : nullptr;
+    C.X = a.comp[c].ext[0];
+    C.Y = a.comp[c].ext[1];
+    C.N = a.comp[c].ext[0] * a.comp[c].ext[1] * a.comp[c].ext[2];
+    C.mX = 0xffffffffu / unsigned(C.X);
+    C.mY = 0xffffffffu / unsigned(C.Y);
+    C.chunk0 = chunk;
+    chunk += (C.N + CH - 1) / CH;
+    const int a1 = (c + 1) % 3, c1 = (c + 2) % 3, a2 = (c + 2) % 3, c2 = (c + 1) % 3;
+    const int aa[2] = {a1, a2}, cc[2] = {c1, c2};
+    for (int t = 0; t < 2; ++t) {
+      C.t[t].src = a.pro.src[cc[t]];
+      C.t[t].X = a.pro.sext[cc[t]][0];
+      C.t[t].Y = a.pro.sext[cc[t]][1];
+      C.t[t].a = aa[t];
+      C.t[t].ext_a = a.pro.sext[cc[t]][aa[t]];
+    }
+  }
+  U.nchunks = chunk;
+  U.s_ptr = a.pro.s_ptr;
+  U.dt = a.pro.dt;
+  int grid = 8 * sm_count();
+  if (grid > chunk) grid = chunk;
+  if (pro == PRO_AMPERE) launch_pdl(update_kernel<PRO_AMPERE>, unsigned(grid), 256u, 0, st, U);
+  else launch_pdl(update_kernel<PRO_FARADAY>, unsigned(grid), 256u, 0, st, U);
 }
 
 void launch_curl(int kind, const double* const src[3], const int sext[3][3], double* const dst[3],

@@ -42,6 +42,8 @@ struct SweepArgs {
   int seg_pad;    // unused (kept for layout stability)
   const double* tabs[2];  // the (at most two) distinct line-operator tables of this pass
   int tab_rows;           // rows per table (padded line length of this axis)
+  int band_hw;            // half-bandwidth of the banded mat-vec of this pass (<= P)
+  int spike_kh, spike_kf; // truncated-SPIKE reach of the history / future scans (segments)
   PrologueArgs pro;
 };
 

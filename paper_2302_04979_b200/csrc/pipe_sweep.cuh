@@ -114,5 +114,12 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// ---- programmatic dependent launch (PDL) ---------------------------------------------------------
+// launch_dependents: let the next kernel in the stream be scheduled (its own griddep_wait still
+// waits for this grid's completion and memory flush); griddep_wait: block until the previous
+// kernel in the stream has completed.  Both are no-ops for launches without the PDL attribute.
+__device__ __forceinline__ void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 }  // namespace pipe
 }  // namespace sgm

@@ -69,6 +69,9 @@ struct Plan {
   int Lmax = 0;                       // rows per table slot (max padded line length)
   int seg[3] = {0, 0, 0};             // register segment length per axis
   int rpad[3] = {0, 0, 0};            // padded line length per axis (multiple of seg)
+  int band_hw[3][OP_COUNT] = {};      // actual half-bandwidth of each table's band part
+  int spike_kh[3][OP_COUNT] = {};     // truncated-SPIKE reach (segments) of the history scan
+  int spike_kf[3][OP_COUNT] = {};     // ... and of the future scan (host_setup.cpp spike_reach)
   double* basis_dev = nullptr;        // general Hodge: per-axis basis values at qp [n][Q][p+1]
   int* first_dev = nullptr;           // per-axis first local global index per element [n]
   size_t basis_off[3][4] = {};        // offsets (doubles) into basis_dev per axis and space

@@ -11,9 +11,8 @@
 // Work unit: a tile of TW = 32*LPT lines of one component; lane j of a consumer warp owns lines
 // j, j+32, ... (LPT lines: independent recurrences interleave, coefficient loads are shared).
 // A CTA is persistent and loops over tiles with two shared-memory slabs:
-//   * producer warps stage tile t+1 into slab[(t+1)&1]: cp.async (LDGSTS) copies, or, for the
-//     first pass of a half step, the fused Ampere/Faraday update (eqs. discrete2_ampere /
-//     discrete2_faraday) computed from global loads, written to the state and slab;
+//   * producer warps stage tile t+1 into slab[(t+1)&1]: cp.async (LDGSTS) copies for strided axes,
+//     one bulk copy (TMA engine, mbarrier completion) per tile of whole x-lines;
 //   * consumer warp s owns rows [s*SEG, (s+1)*SEG) of every line of the tile (SPIKE segment s) and
 //     runs: band mat-vec fused with the zero-history forward substitution -> tail exchange ->
 //     history scan -> spike-corrected backward substitution -> head exchange -> future scan ->
@@ -69,15 +68,6 @@ struct Cfg {
   int nitems;     // tiles over all components
   int tiles[3];   // tiles per component
   CompGeom g[3];
-  // fused update (MODE 1/2): per output component c, the two curl terms
-  // term t: sign * (src[t][idx_hi] - src[t][idx_lo]); see host make_update_terms
-  struct Term {
-    const double* src;
-    int X, Y;     // src extents x, y (for index arithmetic)
-    int ext_a;    // src extent along the differentiated axis (primal bound checks)
-    int a;        // differentiated axis
-    int sign;     // +1 / -1
-  } term[3][2];
 };
 
 // l -> (l % X, l / X) without a division instruction sequence
@@ -98,124 +88,7 @@ __device__ __forceinline__ int line_base(const CompGeom& g, int mode3, int l) {
 }
 
 // ---------------------------------------------------------------------------------------------
-// fused Ampere / Faraday update of LPT lines of one tile (strided axis `ax`), rows pw, pw+NP, ...
-//   AMPERE : d_c <- d_c + dt ((D~1 h)_c - s j_c)     dual   (dv)_k = v_{k+1} - v_k
-//   FARADAY: b_c <- b_c - dt (D1 e)_c                primal (du)_k = u_k - u_{k-1}, u_{-1} = u_a = 0
-// (P:L201 incidence; SURVEY 8.0 stencils).  (x, y, z) of element i of line l: ax = 2: (l%X, l/X, i);
-// ax = 1: (l%X, i, l/X).
-template <int PRO, int LPT>
-__device__ __forceinline__ void produce_update(const SweepArgs& A, const Cfg& cfg, int c, int l0, int pw, int NP,
-                                               int lane, int ax, int W, double* slab) {
-  const CompGeom& g = cfg.g[c];
-  const SweepComp& C = A.comp[c];
-  constexpr bool DUAL = (PRO == PRO_AMPERE);
-  const double dt = A.pro.dt;
-  const double* jh = DUAL ? A.pro.jhat[c] : nullptr;
-  const double sdt = jh ? dt * (A.pro.s_ptr ? __ldg(A.pro.s_ptr) : 1.0) : 0.0;
-  const double* __restrict__ src0 = cfg.term[c][0].src;
-  const double* __restrict__ src1 = cfg.term[c][1].src;
-  // Per line q and term t: element offsets (from the term's src) of the "hi" and "lo" values at
-  // line element 0, and masks that zero invalid primal neighbours (loads are always in bounds:
-  // invalid ones are redirected to the element itself).  Along the line axis, bounds are per row.
-  int st[LPT], hio[LPT][2], loo[LPT][2];
-  double mhi[LPT][2], mlo[LPT][2];
-  bool live[LPT];
-  int tgs[2], along[2], ext_a[2];
-#pragma unroll
-  for (int t = 0; t < 2; ++t) {
-    const auto& T = cfg.term[c][t];
-    tgs[t] = (ax == 1) ? T.X : T.X * T.Y;
-    along[t] = (T.a == ax);
-    ext_a[t] = T.ext_a;
-  }
-#pragma unroll
-  for (int q = 0; q < LPT; ++q) {
-    const int l = l0 + lane + 32 * q;
-    live[q] = l < g.nlines;
-    const int lc = live[q] ? l : g.nlines - 1;
-    int x, o;
-    divmod_x(g, lc, x, o);  // o = y (ax = 2) or z (ax = 1)
-    st[q] = x + o * g.os;
-    const int y = (ax == 2) ? o : 0, z = (ax == 2) ? 0 : o;  // line element 0
-#pragma unroll
-    for (int t = 0; t < 2; ++t) {
-      const auto& T = cfg.term[c][t];
-      const int base = x + T.X * (y + T.Y * z);
-      const int da = (T.a == 0) ? 1 : (T.a == 1 ? T.X : T.X * T.Y);
-      const int pa = (T.a == 0) ? x : (T.a == 1 ? y : z);
-      if (DUAL) {
-        hio[q][t] = base + da;  // v(pos + e_a)
-        loo[q][t] = base;       // v(pos)
-        mhi[q][t] = mlo[q][t] = 1.0;
-      } else {
-        const bool okh = along[t] || pa < T.ext_a, okl = along[t] || pa >= 1;
-        hio[q][t] = okh ? base : (okl ? base - da : 0);  // u(pos)
-        loo[q][t] = okl ? base - da : hio[q][t];          // u(pos - e_a)
-        mhi[q][t] = okh ? 1.0 : 0.0;
-        mlo[q][t] = okl ? 1.0 : 0.0;
-      }
-    }
-  }
-  double* __restrict__ state = C.in;
-  constexpr int U = 4;
-  for (int i0 = pw; i0 < g.L; i0 += U * NP) {
-    double vh[U][LPT][2], vl[U][LPT][2], old[U][LPT], jv[U][LPT];
-    // all loads of the batch first (straight-line code: U*LPT*6 loads in flight)
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int i = min(i0 + k * NP, g.L - 1);
-#pragma unroll
-      for (int q = 0; q < LPT; ++q) {
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          const double* __restrict__ sp = t == 0 ? src0 : src1;
-          int ih = hio[q][t] + i * tgs[t], il = loo[q][t] + i * tgs[t];
-          if (!DUAL && along[t]) {
-            // primal along the line: u_i (i < ext_a) and u_{i-1} (i >= 1)
-            ih = (i < ext_a[t]) ? ih : il;
-            il = (i >= 1) ? il : ih;
-          }
-          vh[k][q][t] = __ldg(sp + ih);
-          vl[k][q][t] = __ldg(sp + il);
-        }
-        old[k][q] = state[st[q] + i * g.gs];
-        jv[k][q] = jh ? __ldg(jh + st[q] + i * g.gs) : 0.0;
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int i = i0 + k * NP;
-#pragma unroll
-      for (int q = 0; q < LPT; ++q) {
-        double cu = 0.0;
-#pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          double h = vh[k][q][t], l = vl[k][q][t];
-          if (!DUAL) {
-            double mh = mhi[q][t], ml = mlo[q][t];
-            if (along[t]) {
-              mh = (i < ext_a[t]) ? 1.0 : 0.0;
-              ml = (i >= 1) ? 1.0 : 0.0;
-            }
-            h *= mh;
-            l *= ml;
-          }
-          cu = (t == 0) ? (h - l) : cu - (h - l);
-        }
-        double val;
-        if (DUAL) val = fma(-sdt, jv[k][q], fma(dt, cu, old[k][q]));
-        else val = fma(-dt, cu, old[k][q]);
-        if (i < g.L) {
-          if (live[q]) state[st[q] + i * g.gs] = val;
-          slab[i * W + q * 32 + lane] = val;
-        }
-      }
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------------------------
-template <int P, int SEG, int LPT, int MODE, int OPS>
+template <int P, int HB, int SEG, int LPT, int MODE, int OPS>
 __global__ void __launch_bounds__(512, 1) sweep_kernel(const __grid_constant__ SweepArgs A, const __grid_constant__ Cfg cfg) {
   using RL = RowLayout<P>;
   constexpr int M = RL::M;
@@ -223,6 +96,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const __grid_constant__ S
   constexpr int TW = 32 * LPT;
   constexpr bool XAX = (MODE == 3);
   constexpr bool band = (OPS & 1) != 0, solve = (OPS & 2) != 0;
+  static_assert(HB >= 1 && HB <= P, "band half-width");
   extern __shared__ __align__(16) double sm[];
   const int NC = cfg.NC, NP = cfg.NP;
   const int NT = (NC + NP) * 32;
@@ -233,25 +107,30 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const __grid_constant__ S
   double* slabs = sm + cfg.ntabs * cfg.tab_dbl;   // [2][slab]
   double* tails = slabs + 2 * cfg.slab;           // [NC][M][TW]
   double* heads = tails + NC * M * TW;            // [NC][M][TW]
-  unsigned long long* full_mb = reinterpret_cast<unsigned long long*>(heads + NC * M * TW);  // [2]
+  unsigned long long* full_mb = reinterpret_cast<unsigned long long*>(heads + NC * M * TW);  // [2] + tables
   const int G = gridDim.x;
   const int R = cfg.rows;
   const int W = cfg.W;  // strided slab row width
 
-  for (int t = 0; t < cfg.ntabs; ++t) {
-    const double2* src = reinterpret_cast<const double2*>(A.tabs[t]);
-    double2* dst = reinterpret_cast<double2*>(tabs + t * cfg.tab_dbl);
-    for (int i = threadIdx.x; i < cfg.tab_dbl / 2; i += blockDim.x) dst[i] = __ldg(src + i);
-  }
+  unsigned long long* tab_mb = full_mb + 2;
+  pipe::griddep_launch_dependents();
   // slabs start zeroed: positions never written by a copy hold finite values (zero or stale data),
   // and every coefficient that multiplies such a position is exactly zero
   for (int i = threadIdx.x; i < cfg.slab; i += blockDim.x) slabs[i] = slabs[cfg.slab + i] = 0.0;
   if (threadIdx.x == 0) {
     pipe::mbar_init(full_mb, 1);
     pipe::mbar_init(full_mb + 1, 1);
+    pipe::mbar_init(tab_mb, 1);
   }
   pipe::fence_proxy_async_smem();
   __syncthreads();
+  // the line-operator table(s) of this pass (constant: staged before waiting on the previous kernel)
+  if (threadIdx.x == 0) {
+    pipe::mbar_arrive_expect_tx(tab_mb, unsigned(cfg.ntabs * cfg.tab_dbl) * 8u);
+    for (int t = 0; t < cfg.ntabs; ++t)
+      pipe::bulk_g2s(tabs + t * cfg.tab_dbl, A.tabs[t], unsigned(cfg.tab_dbl) * 8u, tab_mb);
+  }
+  pipe::griddep_wait();  // inputs are written by the previous kernel in the stream
 
   if (warp >= NC) {
     // ================================ producers ================================
@@ -292,22 +171,35 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const __grid_constant__ S
         }
       } else {
         if (MODE == 0) {
+          // rows [i0, i1) of every line of the tile; a lane copies its LPT lines, 4 rows per step
+          const int rpw = (g.L + NP - 1) / NP;
+          const int i0 = pw * rpw, i1 = min(g.L, i0 + rpw);
+          const double* src[LPT];
+          bool ok[LPT];
 #pragma unroll
           for (int q = 0; q < LPT; ++q) {
             const int l = l0 + lane + 32 * q;
-            double* dst = slab + pw * W + q * 32 + lane;
-            if (l < g.nlines) {
-              const long gstep = long(NP) * g.gs;
-              const double* src = C.in + line_base(g, 0, l) + long(pw) * g.gs;
-              for (int i = pw; i < g.L; i += NP, src += gstep, dst += NP * W) pipe::cp_async8(dst, src);
-            } else {
-              for (int i = pw; i < g.L; i += NP, dst += NP * W) *dst = 0.0;
-            }
+            ok[q] = l < g.nlines;
+            src[q] = C.in + line_base(g, 0, ok[q] ? l : 0) + long(i0) * g.gs;
           }
-        } else if (MODE == 1) {
-          produce_update<PRO_AMPERE, LPT>(A, cfg, c, l0, pw, NP, lane, ax, W, slab);
-        } else {
-          produce_update<PRO_FARADAY, LPT>(A, cfg, c, l0, pw, NP, lane, ax, W, slab);
+          const long gs = g.gs;
+          double* dst = slab + i0 * TW + lane;
+          int i = i0;
+          for (; i + 4 <= i1; i += 4, dst += 4 * TW) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+              for (int q = 0; q < LPT; ++q) {
+                if (ok[q]) pipe::cp_async8(dst + k * TW + 32 * q, src[q]);
+                src[q] += gs;
+              }
+          }
+          for (; i < i1; ++i, dst += TW)
+#pragma unroll
+            for (int q = 0; q < LPT; ++q) {
+              if (ok[q]) pipe::cp_async8(dst + 32 * q, src[q]);
+              src[q] += gs;
+            }
         }
         for (int i = g.L + pw; i < R; i += NP)
 #pragma unroll
@@ -322,6 +214,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const __grid_constant__ S
   // ================================ consumers ================================
   const int s = warp;
   const int r0 = s * SEG;
+  pipe::mbar_wait(tab_mb, 0);
   int it = 0;
   for (int item = blockIdx.x; item < cfg.nitems; item += G, ++it) {
     const int buf = it & 1;
@@ -342,41 +235,31 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const __grid_constant__ S
       if (item + 2 * G < cfg.nitems) pipe::bar_arrive(pipe::kBarEmpty0 + buf, NT);
       continue;
     }
-    // ---- where line q's element r lives in the slab: base[q][parity of r] + r * ES
-    int cbase[LPT][2];
-    constexpr int ESX = 1;
-    const int ES = XAX ? ESX : W;
+    // ---- my lines' segment start in the slab; consecutive line elements are ES apart
+    constexpr int ES = XAX ? 1 : TW;
+    const int pitch = XAX ? (bulk ? g.X : cfg.pitch) : 0;  // x bulk: whole-tile copy, pitch X
+    const double* cp[LPT];
 #pragma unroll
-    for (int q = 0; q < LPT; ++q) {
-      const int j = lane + 32 * q;
-      if (XAX) {
-        cbase[q][0] = cbase[q][1] = j * (bulk ? g.X : cfg.pitch);  // bulk: whole-tile copy, pitch X
-      } else {
-        cbase[q][0] = cbase[q][1] = j;
-      }
-    }
-    // slab index of line q, segment row k (k may be negative or >= SEG for halos); the column
-    // depends on the parity of the global row r0 + k
-    int cA[LPT], cB[LPT];
-#pragma unroll
-    for (int q = 0; q < LPT; ++q) {
-      cA[q] = (r0 & 1) ? cbase[q][1] : cbase[q][0];
-      cB[q] = (r0 & 1) ? cbase[q][0] : cbase[q][1];
-    }
-    auto sidx = [&](int q, int k) -> int { return ((k & 1) ? cB[q] : cA[q]) + (r0 + k) * ES; };
-    // ---- load segment + halos
+    for (int q = 0; q < LPT; ++q) cp[q] = slab + (XAX ? (lane + 32 * q) * pitch : lane + 32 * q) + r0 * ES;
+    // ---- load segment + halos.  Segments past the line end (s >= S) compute on finite padding
+    // and store nothing; their spikes are never used by live segments.
     // w: the P original values left of the current row, in rotating slots: original row r (r >= -P,
-    // relative to the segment) lives in w[(r + P) % P] (compile-time indices: no register moves).
-    double v[SEG][LPT], hr[P][LPT], w[P][LPT];
+    // relative to the segment) lives in w[(r + HB) % HB] (compile-time indices: no register moves).
+    // HB: half-bandwidth of this pass's banded mat-vec (<= P).
+    double v[SEG][LPT], hr[HB][LPT], w[HB][LPT];
 #pragma unroll
     for (int q = 0; q < LPT; ++q) {
 #pragma unroll
-      for (int k = 0; k < SEG; ++k) v[k][q] = live ? slab[sidx(q, k)] : 0.0;
+      for (int k = 0; k < SEG; ++k) v[k][q] = cp[q][k * ES];
       if (band) {
 #pragma unroll
-        for (int j = 0; j < P; ++j) {
-          hr[j][q] = live ? slab[sidx(q, SEG + j)] : 0.0;
-          w[j][q] = (live && s > 0) ? slab[sidx(q, j - P)] : 0.0;  // row j - P -> slot j
+        for (int j = 0; j < HB; ++j) hr[j][q] = cp[q][(SEG + j) * ES];
+        if (s > 0) {
+#pragma unroll
+          for (int j = 0; j < HB; ++j) w[j][q] = cp[q][(j - HB) * ES];  // row j - HB -> slot j
+        } else {
+#pragma unroll
+          for (int j = 0; j < HB; ++j) w[j][q] = 0.0;
         }
       }
     }
@@ -386,19 +269,26 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const __grid_constant__ S
       const double* row = T + k * RS;
       double y[LPT];
       if (band) {
+        // coefficients B[r][r+j], j = -HB..HB, sit at band[P + j]: load the 16-byte pairs covering them
+        constexpr int PA = (P - HB) / 2, PB = (P + HB) / 2;
         double cb[2 * P + 2];
-        ldrow(cb, row + RL::BAND);
+#pragma unroll
+        for (int t = PA; t <= PB; ++t) {
+          const double2 c2 = ld2(row + RL::BAND + 2 * t);
+          cb[2 * t] = c2.x;
+          cb[2 * t + 1] = c2.y;
+        }
 #pragma unroll
         for (int q = 0; q < LPT; ++q) {
           double ls = 0.0, rs = 0.0;
 #pragma unroll
-          for (int j = 1; j <= P; ++j) {
-            ls = fma(cb[P - j], w[(k - j + P) % P][q], ls);  // original row k - j
+          for (int j = 1; j <= HB; ++j) {
+            ls = fma(cb[P - j], w[(k - j + HB) % HB][q], ls);  // original row k - j
             const double xr = (k + j < SEG) ? v[k + j][q] : hr[k + j - SEG][q];
             rs = fma(cb[P + j], xr, rs);
           }
           y[q] = fma(cb[P], v[k][q], ls + rs);
-          w[k % P][q] = v[k][q];  // original row k replaces row k - P
+          w[k % HB][q] = v[k][q];  // original row k replaces row k - HB
         }
       } else {
 #pragma unroll
@@ -433,15 +323,19 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const __grid_constant__ S
 #pragma unroll
         for (int q = 0; q < LPT; ++q) hist[j][q] = 0.0;
       const double* T0 = tabs + (cfg.ntabs > 1 ? C.tslot : 0) * cfg.tab_dbl;
-      for (int t = 0; t < s; ++t) {
+      // (truncated SPIKE: segments more than spike_kh back contribute below rounding, host-checked)
+      const int tb = max(0, s - A.spike_kh);
+      const double* tr = T0 + (tb * SEG + SEG - 1) * RS + RL::F;  // row SEG - 1 of segment tb
+      const double* tl = tails + tb * M * TW + lane;
+      for (int t = tb; t < s; ++t, tr += SEG * RS, tl += M * TW) {
         double nh[M][LPT];
 #pragma unroll
         for (int j = 1; j <= M; ++j) {
           double f[RL::LW];
-          ldrow(f, T0 + (t * SEG + SEG - j) * RS + RL::F);
+          ldrow(f, tr - (j - 1) * RS);
 #pragma unroll
           for (int q = 0; q < LPT; ++q) {
-            double val = tails[(t * M + j - 1) * TW + q * 32 + lane];
+            double val = tl[(j - 1) * TW + q * 32];
 #pragma unroll
             for (int i = 1; i <= M; ++i) val = fma(f[i - 1], hist[i - 1][q], val);
             nh[j - 1][q] = val;
@@ -484,15 +378,18 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const __grid_constant__ S
         for (int j = 0; j < M; ++j)
 #pragma unroll
           for (int q = 0; q < LPT; ++q) fut[j][q] = 0.0;
-        for (int t = S - 1; t > s; --t) {
+        const int te = min(S - 1, s + A.spike_kf);
+        const double* br = T0 + te * SEG * RS + RL::B;  // row 0 of segment te
+        const double* hd = heads + te * M * TW + lane;
+        for (int t = te; t > s; --t, br -= SEG * RS, hd -= M * TW) {
           double nf[M][LPT];
 #pragma unroll
           for (int j = 1; j <= M; ++j) {
             double b[RL::LW];
-            ldrow(b, T0 + (t * SEG + j - 1) * RS + RL::B);
+            ldrow(b, br + (j - 1) * RS);
 #pragma unroll
             for (int q = 0; q < LPT; ++q) {
-              double val = heads[(t * M + j - 1) * TW + q * 32 + lane];
+              double val = hd[(j - 1) * TW + q * 32];
 #pragma unroll
               for (int i = 1; i <= M; ++i) val = fma(b[i - 1], fut[i - 1][q], val);
               nf[j - 1][q] = val;
@@ -529,11 +426,11 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const __grid_constant__ S
             const long gs = g.gs;
             if (r0 + SEG <= L) {
 #pragma unroll
-              for (int k = 0; k < SEG; ++k) dst[k * gs] = sc * v[k][q];
+              for (int k = 0; k < SEG; ++k, dst += gs) *dst = sc * v[k][q];
             } else {
 #pragma unroll
-              for (int k = 0; k < SEG; ++k)
-                if (r0 + k < L) dst[k * gs] = sc * v[k][q];
+              for (int k = 0; k < SEG; ++k, dst += gs)
+                if (r0 + k < L) *dst = sc * v[k][q];
             }
           }
         }
@@ -542,10 +439,12 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const __grid_constant__ S
       if (!solve) pipe::bar_sync(pipe::kBarCons, NC * 32);  // every halo read before in-place writes
       if (live) {
 #pragma unroll
-        for (int q = 0; q < LPT; ++q)
+        for (int q = 0; q < LPT; ++q) {
+          double* cw = const_cast<double*>(cp[q]);
 #pragma unroll
           for (int k = 0; k < SEG; ++k)
-            if (r0 + SEG <= L || r0 + k < L) slab[sidx(q, k)] = sc * v[k][q];
+            if (r0 + SEG <= L || r0 + k < L) cw[k] = sc * v[k][q];
+        }
       }
       if (bulk) {
         pipe::fence_proxy_async_smem();
