@@ -60,7 +60,7 @@ typedef enum {
   SGM_E_INVALID_ARG = 1,       /* NULL/misaligned pointer, n_el < 1, dt non-finite, n_steps < 0,
                                   bad enum, too-small workspace, host-only plan */
   SGM_E_UNSUPPORTED = 2,       /* p < 2, p > SGM_PMAX, or extents beyond the kernel
-                                  tiling limits (n_el + p - 1 > 528 along an axis) */
+                                  tiling limits (n_el + p - 1 > 392 along an axis) */
   SGM_E_GEOMETRY = 3,          /* det DF <= 0 or non-finite at a quadrature point */
   SGM_E_MATERIAL = 4,          /* eps or mu <= 0 or non-finite at a quadrature point */
   SGM_E_SINGULAR = 5,          /* zero pivot or backward error > 1e-13 in a no-pivot 1D LU
@@ -173,15 +173,15 @@ sgm_status sgm_plan_kernels_per_step(sgm_plan plan, int* n);
 /* Per-kernel timing of sgm_step (CUDA events recorded on the launching stream around every
    kernel when enabled).  Kernel classes: */
 typedef enum {
-  SGM_K_EPS_UPDATE_Z = 0, /* fused d-update (D~1 h, j) + z-sweep (Gram mat-vec . K1 solve) */
-  SGM_K_EPS_Y = 1,     /* y-sweep of the eps half */
-  SGM_K_EPS_X = 2,     /* x-sweep of the eps half, writes e */
-  SGM_K_MU_UPDATE_Z = 3, /* fused b-update (D1 e) + z-sweep (Gram mat-vec . K~1 solve) */
+  SGM_K_EPS_Z = 0,     /* z sweep of the eps half (Gram mat-vec . K1 factor solve), d -> t */
+  SGM_K_EPS_Y = 1,     /* y sweep of the eps half, t -> t */
+  SGM_K_EPS_X = 2,     /* x sweep of the eps half, t -> e */
+  SGM_K_MU_Z = 3,      /* z sweep of the mu half (Gram mat-vec . K~1 factor solve), b -> t */
   SGM_K_MU_Y = 4,
-  SGM_K_MU_X = 5,      /* writes h */
-  SGM_K_UPDATE = 6,    /* stand-alone d/b update (general-Hodge path) */
-  SGM_K_HODGE_GENERAL = 7, /* sum-factorised mass apply with quadrature weights */
-  SGM_K_SOLVE_Z = 8,   /* solve-only z-sweep (general-Hodge path) */
+  SGM_K_MU_X = 5,      /* t -> h */
+  SGM_K_UPDATE = 6,    /* Ampere / Faraday update d += dt (D~1 h - s j), b -= dt D1 e (both halves) */
+  SGM_K_HODGE_GENERAL = 7, /* sum-factorised mass apply with quadrature weights (general Hodge) */
+  SGM_K_SOLVE_Z = 8,   /* solve-only z sweep (general-Hodge path) */
   SGM_K_CLASSES = 9
 } sgm_kernel_class;
 sgm_status sgm_plan_set_profiling(sgm_plan plan, int on);

@@ -39,7 +39,7 @@ K1, KT1 = 0, 1
 MASS_EPS, MASS_MU = 0, 1
 CURL_PRIMAL, CURL_DUAL = 0, 1
 EPS, MU = 0, 1
-K_CLASSES = ["eps_update_z", "eps_y", "eps_x", "mu_update_z", "mu_y", "mu_x", "update", "hodge_general", "solve_z"]
+K_CLASSES = ["eps_z", "eps_y", "eps_x", "mu_z", "mu_y", "mu_x", "update", "hodge_general", "solve_z"]
 TAB_G, TAB_M, TAB_GAMMA_B1, TAB_GAMMA_C2, TAB_GAMMA_BP, TAB_GAMMA_C1 = range(6)
 
 _SIGS = {
@@ -122,6 +122,7 @@ class Plan:
         n = (n_el,) * 3 if np.isscalar(n_el) else tuple(n_el)
         self.n_el, self.p, self.device = n, degree, device
         self._ctrl = None if geom_ctrl is None else np.ascontiguousarray(geom_ctrl, dtype=np.float64)
+        self.geom = geom_ctrl is not None
         desc = sgm_plan_desc((c_int * 3)(*n), degree,
                              None if self._ctrl is None else self._ctrl.ctypes.data, quad_points, device)
         h = c_void_p()

@@ -319,7 +319,7 @@ void step_once(Plan& P, double* d, double* e, double* b, double* h, const double
     const int mass = half == 0 ? SGM_MASS_EPS : SGM_MASS_MU;
     const int pro = half == 0 ? PRO_AMPERE : PRO_FARADAY;
     const int own = half == 0 ? OP_EPS_OWN : OP_MU_OWN, oth = half == 0 ? OP_EPS_OTH : OP_MU_OTH;
-    const int kx = half == 0 ? SGM_K_EPS_UPDATE_Z : SGM_K_MU_UPDATE_Z;
+    const int kx = half == 0 ? SGM_K_EPS_Z : SGM_K_MU_Z;
     const int ky = half == 0 ? SGM_K_EPS_Y : SGM_K_MU_Y, kz = half == 0 ? SGM_K_EPS_X : SGM_K_MU_X;
     double** state = half == 0 ? D : B;
     double** outv = half == 0 ? E : H;

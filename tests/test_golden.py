@@ -1,0 +1,93 @@
+"""Oracle pins against the fixtures in tests/golden/ (each fixture cites its passage).
+
+* cavity_spectrum.json: the discrete scheme-2 operator reproduces the exact PEC-cube spectrum
+   with the right multiplicities, converges at the rate of the H-side spaces, and has the
+  discrete gradients as its exact null space.
+* bernstein_1d.json / dimensions.json: closed forms and worked examples of the 1D factors and the
+  complexes.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import forms
+from oracle.splines import gram_1d, open_knots
+from oracle.structured import TierB, curl_primal, curl_dual
+
+G = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def load(name):
+    return json.load(open(os.path.join(G, name)))
+
+
+def leapfrog_operator(p, n):
+    """Dense A = D~1 K~1^{-1} M2 D1 K1^{-1} M~2 on X~2 (the d-form of scheme 2)."""
+    tb = TierB(p, n)
+    N = tb.N_e
+    A = np.zeros((N, N))
+    I = np.eye(N)
+    for i in range(N):
+        e = tb.solve_K1(tb.mass_eps(tb.split_e(I[:, i])))
+        h = tb.solve_Kt1(tb.mass_mu(curl_primal(e)))
+        A[:, i] = forms.join(curl_dual(h))
+    return A
+
+
+@pytest.mark.parametrize("p,n,tol", [(2, 4, 0.12), (3, 4, 2e-3), (4, 3, 1e-3)])
+def test_cavity_spectrum(p, n, tol):
+    gold = load("cavity_spectrum.json")
+    ev = np.linalg.eigvals(leapfrog_operator(p, n))
+    assert np.max(np.abs(ev.imag)) < 1e-9 * np.max(np.abs(ev))
+    ev = np.sort(ev.real)
+    a = n + p - 2
+    scale = np.max(ev)
+    zeros = np.sum(np.abs(ev) < 1e-10 * scale)
+    assert zeros == eval(gold["null_space_dim_formula"], {"n": n, "p": p})  # = dim im D0 = a^3
+    nz = ev[ev > 1e-10 * scale]
+    ref = np.array(gold["eigenvalues_over_pi2"], dtype=float) * np.pi ** 2
+    got = nz[:len(ref)]
+    # the two lowest families (2 pi^2, three-fold; 3 pi^2, two-fold) to the mesh accuracy
+    assert np.all(np.abs(got[:5] - ref[:5]) / ref[:5] < tol), (got / np.pi ** 2)
+    # approximation from above, and the exact multiplicities of the first three families
+    assert np.all(got[:5] >= ref[:5] * (1 - 1e-12))
+    for lo, hi in ((0, 3), (3, 5), (5, 11)):
+        cl = got[lo:hi]
+        assert np.ptp(cl) < 1e-9 * cl[0], (lo, hi, cl)
+    assert got[5] > got[4] * (1 + 1e-6) and got[11] > got[10] * (1 + 1e-6)
+    assert a ** 3 == zeros
+
+
+def test_cavity_spectrum_convergence_rate():
+    """Eigenvalue error of the first mode ~ h^(2(p-1)) (the H-side spaces have degree p-1)."""
+    gold = load("cavity_spectrum.json")
+    lam = gold["eigenvalues_over_pi2"][0] * np.pi ** 2
+    errs = []
+    for n in (3, 4):
+        ev = np.sort(np.linalg.eigvals(leapfrog_operator(3, n)).real)
+        nz = ev[ev > 1e-10 * ev[-1]]
+        errs.append(nz[0] - lam)
+    rate = np.log(errs[0] / errs[1]) / np.log(4 / 3)
+    assert 3.3 < rate < 5.0, rate
+
+
+def test_bernstein_1d():
+    gold = load("bernstein_1d.json")
+    assert np.allclose(gram_1d("Dp2", "Sp", 2, 1), gold["p2"]["G"], rtol=0, atol=1e-15)
+    assert np.allclose(gram_1d("Dp1", "Sp1", 2, 1), gold["p2"]["M"], rtol=0, atol=1e-15)
+    assert abs(gram_1d("Sp", "Sp", 2, 1)[0, 0] - gold["p2_gamma_Bp_n1"]) < 1e-15
+
+
+def test_dimensions():
+    gold = load("dimensions.json")
+    for k in gold["knots"]:
+        kv = open_knots(k["p"], k["n"])
+        if "knots" in k:
+            assert np.allclose(kv, k["knots"])
+        assert len(kv) - k["p"] - 1 == k["dim"]
+    for f in gold["forms"]:
+        assert forms.form_dim(f["cplx"], f["k"], f["p"], f["n"]) == f["dim"], f
+    c = gold["K1_block_C1"]
+    assert int(np.prod(forms.component_shapes("primal", 1, c["p"], c["n"])[0])) == c["size"]
