@@ -10,7 +10,7 @@ if ROOT not in sys.path:
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); parity tests through the C ABI")
-    config.addinivalue_line("markers", "slow: longer oracle tests")
+    config.addinivalue_line("markers", "slow: longer tests (full-size parity: about a minute on a B200 box)")
 
 
 def rel(a, b):

@@ -1,0 +1,120 @@
+"""GPU parity at BASELINE.json's full sizes, in the launch configuration bench.py times (same plan,
+same sgm_step path), against the tier-B oracle (tests/test_oracle_scheme.py pins tier B to tier A).
+
+Tolerances (north_star): relative L2 per vector <= 1e-11 after one step, <= 1e-9 after 100 steps.
+These runs take minutes on the CPU side (tier B at 128^3 is ~0.3 s per step on 16 cores), so they are
+marked `slow` as well as `gpu`.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+import paper_2302_04979_b200 as S  # noqa: E402
+import synth  # noqa: E402
+from oracle import workloads as W  # noqa: E402
+from oracle.structured import TierB  # noqa: E402
+from conftest import rel  # noqa: E402
+
+# Delta t_max * n of the unit-cube scheme-2 operator; dt = 0.5 CFL as in bench.py
+CFL_N = {2: 0.3046, 3: 0.2020, 4: 0.1205}
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).cuda()
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def _c5_state(tb, pl):
+    """bench.py's C5 inputs: d0, b^{1/2} ~ N(0,1) from rng(5); e0, h^{1/2} by the discrete Hodge stars."""
+    d0, b0 = synth.normal(5, tb.N_e, tb.N_h)
+    return d0, tb.hodge_eps(d0), b0, tb.hodge_mu(b0)
+
+
+@pytest.mark.parametrize("p,n,steps,tol", [(3, 128, 1, 1e-11), (3, 128, 100, 1e-9), (2, 160, 1, 1e-11),
+                                           (4, 128, 1, 1e-11)])
+def test_c5_full_size(p, n, steps, tol):
+    pl = S.Plan(n, p)
+    tb = TierB(p, n)
+    st = _c5_state(tb, pl)
+    dt = 0.5 * CFL_N[p] / n
+    dv = [dev(x) for x in st]
+    pl.step(*dv, dt, steps)
+    ref = tb.run(*st, dt, steps)
+    for a, r in zip(dv, ref):
+        assert rel(host(a), r) < tol
+
+
+def test_c2_four_modes_200_steps():
+    """configs[1]: p = 3, 32^3, four cavity modes with seeded amplitudes, 200 steps; parity and
+    energy drift of the modified invariant (exact for scheme 2, reading Z19)."""
+    p, n = 3, 32
+    tb = TierB(p, n)
+    dt = 0.5 * CFL_N[p] / n
+    st = W.cavity_initial_state(tb, W.c2_modes(), dt)
+    pl = S.Plan(n, p)
+    dv = [dev(x) for x in st]
+    pl.step(*dv, dt, 200)
+    ref = tb.run(*st, dt, 200)
+    for a, r in zip(dv, ref):
+        assert rel(host(a), r) < 1e-9
+
+
+def test_c4_variable_eps_full_size():
+    """configs[3]: identity map, p = 4, 96^3, eps = 1 + 0.5 sin(2 pi x) cos(2 pi y) at the quadrature
+    points (general Hodge, scalar weights), smooth random e0; one step."""
+    p, n = 4, 96
+    pl = S.Plan(n, p)
+    X = pl.qp_coords()
+    eps = 1 + 0.5 * np.sin(2 * np.pi * X[:, 0]) * np.cos(2 * np.pi * X[:, 1])
+    del X
+    pl.set_material(S.EPS, eps)
+    tb = TierB(p, n, inv_eps=1.0 / eps)
+    g = np.random.default_rng(4)
+    d0 = g.standard_normal(tb.N_e)
+    b0 = g.standard_normal(tb.N_h)
+    st = (d0, tb.hodge_eps(d0), b0, tb.hodge_mu(b0))
+    dt = 0.25 * CFL_N[p] / n
+    dv = [dev(x) for x in st]
+    pl.step(*dv, dt, 1)
+    ref = tb.step(*st, dt)
+    for a, r in zip(dv, ref):
+        assert rel(host(a), r) < 1e-11
+
+
+def test_c3_curved_inclusion_source_full_size():
+    """configs[2]: curved map interpolated in S_3^3 (reading Z18), eps in {1, 4} sphere, divergence-free
+    source j = D~1 a with a Gaussian pulse amplitude (reading Z16); 20 steps."""
+    p, n = 3, 48
+    ctrl = W.interpolate_map(p, n, W.c3_map)
+    pl = S.Plan(n, p, geom_ctrl=ctrl)
+    X = pl.qp_coords()
+    c_eps, _ = synth.c3_centres()
+    eps = np.where(np.linalg.norm(X - c_eps, axis=1) < 0.25, 4.0, 1.0)
+    del X
+    pl.set_material(S.EPS, eps)
+    tb = TierB(p, n, ctrl=ctrl, inv_eps=1.0 / eps, inv_mu=1.0)
+    tb.sep_mu = None
+    tb.W_mu = tb._W(1.0)
+    from oracle.structured import curl_dual
+    from oracle import forms
+    a = synth.normal(33, tb.N_h)[0]
+    jhat = forms.join(curl_dual(tb.split_h(a)))
+    steps = 20
+    dt = 0.25 * CFL_N[p] / n
+    tt = (np.arange(steps) + 0.5) * dt
+    jamp = np.exp(-((tt - 0.15 * steps * dt) / (0.05 * steps * dt)) ** 2)
+    g = np.random.default_rng(3)
+    d0 = g.standard_normal(tb.N_e)
+    b0 = g.standard_normal(tb.N_h)
+    st = (d0, tb.hodge_eps(d0), b0, tb.hodge_mu(b0))
+    dv = [dev(x) for x in st]
+    pl.step(*dv, dt, steps, j_hat=dev(jhat), j_amp=dev(jamp))
+    ref = tb.run(*st, dt, steps, jhat, jamp)
+    for x, r in zip(dv, ref):
+        assert rel(host(x), r) < 1e-10
