@@ -223,6 +223,7 @@ void hodge_args(const Plan& P, int which, const double* x, double* y, HodgeArgs&
     h.nel[a] = P.n[a];
   }
   h.Q = P.Q;
+  h.dual = (which == SGM_MASS_EPS) ? 1 : 0;
 }
 
 // y = M x for one 2-form mass (separable: Kronecker of 1D Grams; else sum factorisation)

@@ -20,6 +20,7 @@
 #include "kernels.cuh"
 #include "seg_sweep.cuh"
 #include "sweep_kernel.cuh"
+#include "hodge_kernel.cuh"
 
 #include <cstdint>
 #include <cstdlib>
@@ -597,7 +598,86 @@ void launch_curl(int kind, const double* const src[3], const int sext[3][3], dou
     curl_kernel<false><<<grid, 256, 0, st>>>(src[0], src[1], src[2], e[0], e[1], e[2], dst[0], dst[1], dst[2], f[0], f[1], f[2]);
 }
 
+template <int P, int Q, bool DUAL, bool FULL>
+void launch_hodge_pencil(const HodgeArgs& a, cudaStream_t st) {
+  constexpr int XB = hodge::max_box<P, DUAL>(), AB = (P + 1) * (P + 1) * Q, BB = (P + 1) * Q * Q;
+  const size_t smem = size_t(8) * (6 * XB + AB + BB) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(hodge::hodge_pencil_kernel<P, Q, DUAL, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    attr = true;
+  }
+  const long npen = long(a.nel[0]) * a.nel[1];
+  long grid = (npen + 7) / 8;
+  const long cap = 16L * sm_count();
+  if (grid > cap) grid = cap;
+  hodge::hodge_pencil_kernel<P, Q, DUAL, FULL><<<unsigned(grid), 256, smem, st>>>(a);
+}
+
+template <int P, int Q, bool DUAL, bool FULL>
+void launch_hodge_v3(const HodgeArgs& a, cudaStream_t st) {
+  constexpr int NL = P + 1, XB = hodge::max_box<P, DUAL>(), VB = Q * NL, CB = (P + 1) * Q * Q,
+                TB = (P + 1) * (P + 1) * Q;
+  const size_t smem = size_t(8) * (6 * XB + 9 * VB + CB + TB) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(hodge::hodge_v3_kernel<P, Q, DUAL, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    attr = true;
+  }
+  const long npen = long(a.nel[0]) * a.nel[1];
+  long grid = (npen + 7) / 8;
+  const long cap = 16L * sm_count();
+  if (grid > cap) grid = cap;
+  hodge::hodge_v3_kernel<P, Q, DUAL, FULL><<<unsigned(grid), 256, smem, st>>>(a);
+}
+
+template <int P, int Q>
+void launch_hodge2(const HodgeArgs& a, cudaStream_t st) {
+  if (env_int("SGM_HODGE_V", 3) == 3) {
+    if (a.dual) {
+      if (a.full) launch_hodge_v3<P, Q, true, true>(a, st);
+      else launch_hodge_v3<P, Q, true, false>(a, st);
+    } else {
+      if (a.full) launch_hodge_v3<P, Q, false, true>(a, st);
+      else launch_hodge_v3<P, Q, false, false>(a, st);
+    }
+    return;
+  }
+  if (env_int("SGM_HODGE_PENCIL", 1)) {
+    if (a.dual) {
+      if (a.full) launch_hodge_pencil<P, Q, true, true>(a, st);
+      else launch_hodge_pencil<P, Q, true, false>(a, st);
+    } else {
+      if (a.full) launch_hodge_pencil<P, Q, false, true>(a, st);
+      else launch_hodge_pencil<P, Q, false, false>(a, st);
+    }
+    return;
+  }
+  const long nel = long(a.nel[0]) * a.nel[1] * a.nel[2];
+  long grid = (nel + 7) / 8;
+  const long cap = 16L * sm_count();
+  if (grid > cap) grid = cap;
+  if (a.dual) {
+    if (a.full) hodge::hodge2_kernel<P, Q, true, true><<<unsigned(grid), 256, 0, st>>>(a);
+    else hodge::hodge2_kernel<P, Q, true, false><<<unsigned(grid), 256, 0, st>>>(a);
+  } else {
+    if (a.full) hodge::hodge2_kernel<P, Q, false, true><<<unsigned(grid), 256, 0, st>>>(a);
+    else hodge::hodge2_kernel<P, Q, false, false><<<unsigned(grid), 256, 0, st>>>(a);
+  }
+}
+
 void launch_hodge_general(int p, const HodgeArgs& a, cudaStream_t st) {
+  // warp-per-element sum factorisation (hodge_kernel.cuh) for the default rule Q = p + 1
+  if (a.Q == p + 1 && env_int("SGM_HODGE_V1", 0) == 0) {
+    switch (p) {
+      case 2: launch_hodge2<2, 3>(a, st); return;
+      case 3: launch_hodge2<3, 4>(a, st); return;
+      case 4: launch_hodge2<4, 5>(a, st); return;
+      default: break;
+    }
+  }
   long nel = long(a.nel[0]) * a.nel[1] * a.nel[2];
   int Q = a.Q;
   int M = (p + 1 > Q) ? p + 1 : Q;

@@ -61,6 +61,7 @@ struct HodgeArgs {
   int first_off[3][2];
   int nel[3];
   int Q;
+  int dual;              // 1: dual 2-forms (M~2_{1/eps}), 0: primal 2-forms (M2_{1/mu})
 };
 
 void launch_sweep(int p, int seg, const SweepArgs& a, cudaStream_t st);

@@ -116,7 +116,12 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const __grid_constant__ S
   pipe::griddep_launch_dependents();
   // slabs start zeroed: positions never written by a copy hold finite values (zero or stale data),
   // and every coefficient that multiplies such a position is exactly zero
-  for (int i = threadIdx.x; i < cfg.slab; i += blockDim.x) slabs[i] = slabs[cfg.slab + i] = 0.0;
+  {
+    double2* s2 = reinterpret_cast<double2*>(slabs);
+    const double2 z2 = make_double2(0.0, 0.0);
+#pragma unroll 4
+    for (int i = threadIdx.x; i < cfg.slab; i += blockDim.x) s2[i] = z2;  // 2 slabs = cfg.slab double2
+  }
   if (threadIdx.x == 0) {
     pipe::mbar_init(full_mb, 1);
     pipe::mbar_init(full_mb + 1, 1);
@@ -424,7 +429,10 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const __grid_constant__ S
           if (l < g.nlines) {
             double* dst = C.out + line_base(g, 0, l) + long(r0) * g.gs;
             const long gs = g.gs;
-            if (r0 + SEG <= L) {
+            if (r0 + SEG <= L && sc == 1.0) {
+#pragma unroll
+              for (int k = 0; k < SEG; ++k, dst += gs) *dst = v[k][q];
+            } else if (r0 + SEG <= L) {
 #pragma unroll
               for (int k = 0; k < SEG; ++k, dst += gs) *dst = sc * v[k][q];
             } else {

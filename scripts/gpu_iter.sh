@@ -8,7 +8,7 @@ for V in "${VS[@]}"; do
   python -c "
 import json
 d=json.load(open('gpurun_out/bench_v$i.json'))
-print('[$V] value %.3g ms/step %.4f step_gbs %.0f'%(d['value'],d['ms_per_step'],d['roofline']['step_model_gbs']))
+print('[$V] value %.3g ms/step %.4f step_gbs %.0f'%(d['value'],d['ms_per_step'],d['roofline']['step_gbs']))
 for k,v in d['kernels'].items(): print('  %-14s %.1f us %6.0f GB/s'%(k,1e3*v['ms_per_launch'],v.get('gbs',0)))
 " || tail -5 gpurun_out/bench_v$i.err
   i=$((i+1))
