@@ -4,6 +4,7 @@
 // Nothing here runs per time step.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -450,6 +451,9 @@ sgm_status build_tables(Plan& P, std::string& err) {
       } else {
         spike_reach(T(op), p, Ls[op], SEG, P.spike_kh[a][op], P.spike_kf[a][op]);
       }
+      if (getenv("SGM_DEBUG_PLAN"))
+        fprintf(stderr, "sgm plan: axis %d op %d L %d SEG %d S %d band_hw %d spike reach hist %d fut %d\n", a, op,
+                Ls[op], SEG, S, P.band_hw[a][op], P.spike_kh[a][op], P.spike_kf[a][op]);
     }
   }
   return SGM_OK;

@@ -108,10 +108,9 @@ __device__ __forceinline__ unsigned fdiv(unsigned n, unsigned d, unsigned m, uns
   return q;
 }
 
-template <int PRO>
-__global__ void __launch_bounds__(256) update_kernel(const __grid_constant__ UpdArgs A) {
+template <int PRO, int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) update_kernel(const __grid_constant__ UpdArgs A) {
   constexpr bool DUAL = (PRO == PRO_AMPERE);
-  constexpr int U = 4;
   pipe::griddep_launch_dependents();
   pipe::griddep_wait();
   for (int ch = blockIdx.x; ch < A.nchunks; ch += gridDim.x) {
@@ -552,7 +551,12 @@ void launch_sweep(int p, int seg, const SweepArgs& a, cudaStream_t st) {
 void launch_update(int pro, const SweepArgs& a, cudaStream_t st) {
   UpdArgs U;
   std::memset(&U, 0, sizeof(U));
-  constexpr int CH = 256 * 4;
+  const int minb = env_int("SGM_UPD_MINB", 1);
+  int UU = env_int("SGM_UPD_U", 4);
+  if (!((UU == 4 && minb == 1) || (UU == 8 && minb == 1) || (UU == 4 && minb == 4) || (UU == 8 && minb == 2) ||
+        (UU == 2 && minb == 4)))
+    UU = 4;
+  const int CH = 256 * UU;
   int chunk = 0;
   for (int c = 0; c < 3; ++c) {
     UpdComp& C = U.c[c];
@@ -578,10 +582,19 @@ void launch_update(int pro, const SweepArgs& a, cudaStream_t st) {
   U.nchunks = chunk;
   U.s_ptr = a.pro.s_ptr;
   U.dt = a.pro.dt;
-  int grid = 8 * sm_count();
+  int grid = env_int("SGM_UPD_GRID", 8) * sm_count();
   if (grid > chunk) grid = chunk;
-  if (pro == PRO_AMPERE) launch_pdl(update_kernel<PRO_AMPERE>, unsigned(grid), 256u, 0, st, U);
-  else launch_pdl(update_kernel<PRO_FARADAY>, unsigned(grid), 256u, 0, st, U);
+  // U elements per thread (all loads issued before use); MINB: minimum resident blocks per SM
+#define SGM_UPD(UV, MB)                                                                                   \
+  if (UU == UV && minb == MB) {                                                                           \
+    if (pro == PRO_AMPERE) launch_pdl(update_kernel<PRO_AMPERE, UV, MB>, unsigned(grid), 256u, 0, st, U); \
+    else launch_pdl(update_kernel<PRO_FARADAY, UV, MB>, unsigned(grid), 256u, 0, st, U);                  \
+    return;                                                                                               \
+  }
+  SGM_UPD(4, 1) SGM_UPD(8, 1) SGM_UPD(4, 4) SGM_UPD(8, 2) SGM_UPD(2, 4)
+#undef SGM_UPD
+  if (pro == PRO_AMPERE) launch_pdl(update_kernel<PRO_AMPERE, 4, 1>, unsigned(grid), 256u, 0, st, U);
+  else launch_pdl(update_kernel<PRO_FARADAY, 4, 1>, unsigned(grid), 256u, 0, st, U);
 }
 
 void launch_curl(int kind, const double* const src[3], const int sext[3][3], double* const dst[3],

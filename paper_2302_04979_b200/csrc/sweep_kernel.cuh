@@ -89,7 +89,7 @@ __device__ __forceinline__ int line_base(const CompGeom& g, int mode3, int l) {
 
 // ---------------------------------------------------------------------------------------------
 template <int P, int HB, int SEG, int LPT, int MODE, int OPS>
-__global__ void __launch_bounds__(512, 1) sweep_kernel(const __grid_constant__ SweepArgs A, const __grid_constant__ Cfg cfg) {
+__global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __grid_constant__ SweepArgs A, const __grid_constant__ Cfg cfg) {
   using RL = RowLayout<P>;
   constexpr int M = RL::M;
   constexpr int RS = RL::RS;
@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const __grid_constant__ S
         for (int q = 0; q < LPT; ++q) hist[j][q] = 0.0;
       const double* T0 = tabs + (cfg.ntabs > 1 ? C.tslot : 0) * cfg.tab_dbl;
       // (truncated SPIKE: segments more than spike_kh back contribute below rounding, host-checked)
-      const int tb = max(0, s - A.spike_kh);
+      const int tb = (cfg.dbg & 4) ? s : max(0, s - A.spike_kh);  // dbg bit 2: no history scan (timing only)
       const double* tr = T0 + (tb * SEG + SEG - 1) * RS + RL::F;  // row SEG - 1 of segment tb
       const double* tl = tails + tb * M * TW + lane;
       for (int t = tb; t < s; ++t, tr += SEG * RS, tl += M * TW) {
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const __grid_constant__ S
         for (int j = 0; j < M; ++j)
 #pragma unroll
           for (int q = 0; q < LPT; ++q) fut[j][q] = 0.0;
-        const int te = min(S - 1, s + A.spike_kf);
+        const int te = (cfg.dbg & 4) ? s : min(S - 1, s + A.spike_kf);
         const double* br = T0 + te * SEG * RS + RL::B;  // row 0 of segment te
         const double* hd = heads + te * M * TW + lane;
         for (int t = te; t > s; --t, br -= SEG * RS, hd -= M * TW) {
@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(512, 1) sweep_kernel(const __grid_constant__ S
     // ---- phase E: scaled store
     const double sc = C.scale;
     if (!XAX) {
-      if (live) {
+      if (live && !(cfg.dbg & 8)) {  // dbg bit 3: no stores (timing only)
 #pragma unroll
         for (int q = 0; q < LPT; ++q) {
           const int l = l0 + lane + 32 * q;
