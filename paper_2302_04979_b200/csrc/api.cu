@@ -135,15 +135,13 @@ struct ProfScope {
 
 // One axis pass over the 3 components of a form (kind 0: e/d shapes, 1: b/h shapes).
 void sweep_pass(const Plan& P, int kind, int axis, double* const in[3], double* const out[3], int op_own,
-                int op_oth, const double* scale, bool band, bool solve, int pro, const PrologueArgs* pro_args,
-                cudaStream_t st) {
+                int op_oth, const double* scale, bool band, bool solve, cudaStream_t st) {
   SweepArgs a;
   std::memset(&a, 0, sizeof(a));
   a.ncomp = 3;
   a.axis = axis;
   a.band = band;
   a.solve = solve;
-  a.pro_kind = pro;
   a.tabs[0] = table(P, axis, op_own);
   a.tabs[1] = table(P, axis, op_oth);
   a.tab_rows = P.rpad[axis];
@@ -158,7 +156,6 @@ void sweep_pass(const Plan& P, int kind, int axis, double* const in[3], double* 
     a.comp[c].tslot = own_or(axis, c, 0, 1);
     a.comp[c].scale = scale ? scale[c] : 1.0;
   }
-  if (pro_args) a.pro = *pro_args;
   launch_sweep(P.p, P.seg[axis], a, st);
 }
 
@@ -171,9 +168,9 @@ void kron_pass3(const Plan& P, int kind, const double* x, double* y, double* t, 
   comps_of(P, kind, x, X);
   comps_of(P, kind, t, T);
   comps_of(P, kind, y, Y);
-  sweep_pass(P, kind, 2, X, T, op_own, op_oth, nullptr, band, solve, PRO_NONE, nullptr, st);
-  sweep_pass(P, kind, 1, T, T, op_own, op_oth, nullptr, band, solve, PRO_NONE, nullptr, st);
-  sweep_pass(P, kind, 0, T, Y, op_own, op_oth, scale, band, solve, PRO_NONE, nullptr, st);
+  sweep_pass(P, kind, 2, X, T, op_own, op_oth, nullptr, band, solve, st);
+  sweep_pass(P, kind, 1, T, T, op_own, op_oth, nullptr, band, solve, st);
+  sweep_pass(P, kind, 0, T, Y, op_own, op_oth, scale, band, solve, st);
 }
 
 PrologueArgs make_pro(const Plan& P, int src_kind, const double* src, const double* jhat, const double* s_ptr,
@@ -338,9 +335,9 @@ void step_once(Plan& P, double* d, double* e, double* b, double* h, const double
       }
       a.pro = pa;
       { ProfScope ps(P, SGM_K_UPDATE, st); launch_update(pro, a, st); }
-      { ProfScope ps(P, kx, st); sweep_pass(P, kind, 2, state, T, own, oth, nullptr, true, true, PRO_NONE, nullptr, st); }
-      { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, true, true, PRO_NONE, nullptr, st); }
-      { ProfScope ps(P, kz, st); sweep_pass(P, kind, 0, T, outv, own, oth, M.scale, true, true, PRO_NONE, nullptr, st); }
+      { ProfScope ps(P, kx, st); sweep_pass(P, kind, 2, state, T, own, oth, nullptr, true, true, st); }
+      { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, true, true, st); }
+      { ProfScope ps(P, kz, st); sweep_pass(P, kind, 0, T, outv, own, oth, M.scale, true, true, st); }
     } else {
       SweepArgs a;
       std::memset(&a, 0, sizeof(a));
@@ -353,9 +350,9 @@ void step_once(Plan& P, double* d, double* e, double* b, double* h, const double
       { ProfScope ps(P, SGM_K_UPDATE, st); launch_update(pro, a, st); }
       { ProfScope ps(P, SGM_K_HODGE_GENERAL, st); mass_apply(P, mass, state[0], w.r, w.t, st); }
       comps_of(P, kind, w.r, Rr);
-      { ProfScope ps(P, SGM_K_SOLVE_Z, st); sweep_pass(P, kind, 2, Rr, T, own, oth, nullptr, false, true, PRO_NONE, nullptr, st); }
-      { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, false, true, PRO_NONE, nullptr, st); }
-      { ProfScope ps(P, kz, st); sweep_pass(P, kind, 0, T, outv, own, oth, nullptr, false, true, PRO_NONE, nullptr, st); }
+      { ProfScope ps(P, SGM_K_SOLVE_Z, st); sweep_pass(P, kind, 2, Rr, T, own, oth, nullptr, false, true, st); }
+      { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, false, true, st); }
+      { ProfScope ps(P, kz, st); sweep_pass(P, kind, 0, T, outv, own, oth, nullptr, false, true, st); }
     }
   }
 }

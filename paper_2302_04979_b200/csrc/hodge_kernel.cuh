@@ -1,16 +1,22 @@
 // General (non-separable) 2-form Hodge apply y = M x (P:L360 M~2_{1/eps}, P:L366 M2_{1/mu}) by
-// element-wise sum factorisation, one warp per element (sm_100a, fp64).
+// element-wise sum factorisation (sm_100a, fp64).
 //
 // On element e the 2-form mass is  y_c += sum_{c'} V_c^T W_{cc'} V_{c'} x_{c'}  where V_c is the
 // tensor product of the 1D element bases at the Q Gauss points per axis (component c uses the
 // "own" space along axis c and the "other" space along the two other axes) and
 // W holds, per quadrature point, w_q / material * DF^T DF / det DF (FULL, 6 symmetric entries) or
 // w_q / material with a per-component constant (SCALAR; identity / axis-aligned affine map).
-// Interpolation and testing are staged axis by axis (x, y, z and back) through per-warp shared
-// memory with compile-time extents: the exact local box sizes of each component are used
-// (dual 2-forms: p along the own axis, p-1 along the others; primal: p+1 and p).
-// Lane (qx, qy) owns the z-column of quadrature values of its (qx, qy); W is streamed from HBM
-// coalesced (element-major [e][qz][qy][qx]).  Outputs are scatter-added with fp64 atomics.
+// The exact local box of each component is used (dual 2-forms: p functions along the own axis,
+// p-1 along the others; primal: p+1 and p).
+//
+// One warp walks a z-pencil of elements (ex, ey, 0..nz-1).  Consecutive elements share all but one
+// coefficient layer along z, so the coefficient boxes shift by one layer per element (the new layer
+// is prefetched into registers while the previous element is computed) and the output boxes are
+// accumulated in shared memory; after each element the lowest output layer is complete and is
+// flushed with fp64 atomics (only neighbouring pencils share it).  Interpolation: lane (qx, qy)
+// computes its z-column of quadrature values; testing: lanes take the roles (qx, jy) and (jx, jy)
+// so every reduction over quadrature points is a per-lane loop over shared memory.  W is streamed
+// from HBM coalesced (element-major [e][qz][qy][qx]).
 #pragma once
 
 #include "kernels.cuh"
@@ -32,99 +38,6 @@ struct ElemBasis {
   int first[3];        // global index of local function 0 per axis
 };
 
-// u[qz] (lane (qx,qy)) = (V_z (x) V_y (x) V_x) X at the element's quadrature points
-template <int P, int Q, bool DUAL, int C>
-__device__ __forceinline__ void interp(const ElemBasis& B, const double* __restrict__ xg, const int* ext,
-                                       double* X, double* Abuf, double* Bbuf, int lane, double (&u)[Q]) {
-  constexpr int NX = nloc<P, DUAL, C, 0>(), NY = nloc<P, DUAL, C, 1>(), NZ = nloc<P, DUAL, C, 2>();
-  constexpr int NL = P + 1;
-  // gather the coefficient box (out-of-range indices are trimmed functions: zero)
-  for (int o = lane; o < NX * NY * NZ; o += 32) {
-    const int jx = o % NX, jy = (o / NX) % NY, jz = o / (NX * NY);
-    const int gx = B.first[0] + jx, gy = B.first[1] + jy, gz = B.first[2] + jz;
-    double val = 0.0;
-    if (gx >= 0 && gx < ext[0] && gy >= 0 && gy < ext[1] && gz >= 0 && gz < ext[2])
-      val = __ldg(xg + gx + long(ext[0]) * (gy + long(ext[1]) * gz));
-    X[o] = val;
-  }
-  __syncwarp();
-  // x: A[jz][jy][qx] = sum_jx Vx[qx][jx] X[jz][jy][jx]
-  for (int o = lane; o < NZ * NY * Q; o += 32) {
-    const int qx = o % Q, r = o / Q;  // r = jz*NY + jy
-    const double* vx = B.v[0] + qx * NL;
-    double s = 0.0;
-#pragma unroll
-    for (int jx = 0; jx < NX; ++jx) s = fma(__ldg(vx + jx), X[r * NX + jx], s);
-    Abuf[o] = s;
-  }
-  __syncwarp();
-  // y: B[jz][qy][qx] = sum_jy Vy[qy][jy] A[jz][jy][qx]
-  for (int o = lane; o < NZ * Q * Q; o += 32) {
-    const int qx = o % Q, qy = (o / Q) % Q, jz = o / (Q * Q);
-    const double* vy = B.v[1] + qy * NL;
-    double s = 0.0;
-#pragma unroll
-    for (int jy = 0; jy < NY; ++jy) s = fma(__ldg(vy + jy), Abuf[(jz * NY + jy) * Q + qx], s);
-    Bbuf[o] = s;
-  }
-  __syncwarp();
-  // z: u[qz] = sum_jz Vz[qz][jz] B[jz][qy][qx]
-  if (lane < Q * Q) {
-    double b[NZ];
-#pragma unroll
-    for (int jz = 0; jz < NZ; ++jz) b[jz] = Bbuf[jz * Q * Q + lane];
-#pragma unroll
-    for (int qz = 0; qz < Q; ++qz) {
-      const double* vz = B.v[2] + qz * NL;
-      double s = 0.0;
-#pragma unroll
-      for (int jz = 0; jz < NZ; ++jz) s = fma(__ldg(vz + jz), b[jz], s);
-      u[qz] = s;
-    }
-  }
-  __syncwarp();
-}
-
-// y += (V_z (x) V_y (x) V_x)^T v   (lane (qx,qy) holds v[qz])
-template <int P, int Q, bool DUAL, int C>
-__device__ __forceinline__ void test(const ElemBasis& B, double* __restrict__ yg, const int* ext, double* Abuf,
-                                     double* Bbuf, int lane, const double (&v)[Q]) {
-  constexpr int NX = nloc<P, DUAL, C, 0>(), NY = nloc<P, DUAL, C, 1>(), NZ = nloc<P, DUAL, C, 2>();
-  constexpr int NL = P + 1;
-  // z^T: B[jz][qy][qx] = sum_qz Vz[qz][jz] v[qz]
-  if (lane < Q * Q) {
-#pragma unroll
-    for (int jz = 0; jz < NZ; ++jz) {
-      double s = 0.0;
-#pragma unroll
-      for (int qz = 0; qz < Q; ++qz) s = fma(__ldg(B.v[2] + qz * NL + jz), v[qz], s);
-      Bbuf[jz * Q * Q + lane] = s;
-    }
-  }
-  __syncwarp();
-  // y^T: A[jz][jy][qx] = sum_qy Vy[qy][jy] B[jz][qy][qx]
-  for (int o = lane; o < NZ * NY * Q; o += 32) {
-    const int qx = o % Q, jy = (o / Q) % NY, jz = o / (Q * NY);
-    double s = 0.0;
-#pragma unroll
-    for (int qy = 0; qy < Q; ++qy) s = fma(__ldg(B.v[1] + qy * NL + jy), Bbuf[(jz * Q + qy) * Q + qx], s);
-    Abuf[o] = s;
-  }
-  __syncwarp();
-  // x^T and scatter-add: Y[jz][jy][jx] = sum_qx Vx[qx][jx] A[jz][jy][qx]
-  for (int o = lane; o < NX * NY * NZ; o += 32) {
-    const int jx = o % NX, r = o / NX;  // r = jz*NY + jy
-    const int jy = r % NY, jz = r / NY;
-    const int gx = B.first[0] + jx, gy = B.first[1] + jy, gz = B.first[2] + jz;
-    if (gx < 0 || gx >= ext[0] || gy < 0 || gy >= ext[1] || gz < 0 || gz >= ext[2]) continue;
-    double s = 0.0;
-#pragma unroll
-    for (int qx = 0; qx < Q; ++qx) s = fma(__ldg(B.v[0] + qx * NL + jx), Abuf[r * Q + qx], s);
-    atomicAdd(yg + gx + long(ext[0]) * (gy + long(ext[1]) * gz), s);
-  }
-  __syncwarp();
-}
-
 template <int P, bool DUAL, int C>
 __device__ __forceinline__ ElemBasis elem_basis(const HodgeArgs& A, int ex, int ey, int ez) {
   constexpr int NL = P + 1;
@@ -139,150 +52,12 @@ __device__ __forceinline__ ElemBasis elem_basis(const HodgeArgs& A, int ex, int 
   return B;
 }
 
-template <int P, int Q, bool DUAL, bool FULL>
-__global__ void __launch_bounds__(256) hodge2_kernel(const __grid_constant__ HodgeArgs A) {
-  constexpr int QQQ = Q * Q * Q;
-  constexpr int XB = max_box<P, DUAL>();
-  constexpr int AB = (P + 1) * (P + 1) * Q;  // >= NZ*NY*Q for every component
-  constexpr int BB = (P + 1) * Q * Q;        // >= NZ*Q*Q
-  static_assert(Q * Q <= 32, "one warp per element needs Q*Q <= 32");
-  __shared__ double sm[8][XB + AB + BB];
-  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* X = sm[wib];
-  double* Ab = X + XB;
-  double* Bb = Ab + AB;
-  const int nx = A.nel[0], ny = A.nel[1];
-  const long nel = long(A.nel[0]) * A.nel[1] * A.nel[2];
-  const long wstride = long(gridDim.x) * (blockDim.x >> 5);
-  for (long e = long(blockIdx.x) * (blockDim.x >> 5) + wib; e < nel; e += wstride) {
-    const int ex = int(e % nx), ey = int((e / nx) % ny), ez = int(e / (long(nx) * ny));
-    double u0[Q], u1[Q], u2[Q];
-    {
-      const ElemBasis B0 = elem_basis<P, DUAL, 0>(A, ex, ey, ez);
-      interp<P, Q, DUAL, 0>(B0, A.x[0], A.ext[0], X, Ab, Bb, lane, u0);
-      const ElemBasis B1 = elem_basis<P, DUAL, 1>(A, ex, ey, ez);
-      interp<P, Q, DUAL, 1>(B1, A.x[1], A.ext[1], X, Ab, Bb, lane, u1);
-      const ElemBasis B2 = elem_basis<P, DUAL, 2>(A, ex, ey, ez);
-      interp<P, Q, DUAL, 2>(B2, A.x[2], A.ext[2], X, Ab, Bb, lane, u2);
-    }
-    double v0[Q], v1[Q], v2[Q];
-    if (lane < Q * Q) {
-      if (FULL) {
-        const double* w = A.W + (e * QQQ + lane) * 6;
-#pragma unroll
-        for (int qz = 0; qz < Q; ++qz) {
-          const double* wq = w + qz * Q * Q * 6;
-          const double wxx = __ldg(wq), wyy = __ldg(wq + 1), wzz = __ldg(wq + 2), wxy = __ldg(wq + 3),
-                       wxz = __ldg(wq + 4), wyz = __ldg(wq + 5);
-          v0[qz] = wxx * u0[qz] + wxy * u1[qz] + wxz * u2[qz];
-          v1[qz] = wxy * u0[qz] + wyy * u1[qz] + wyz * u2[qz];
-          v2[qz] = wxz * u0[qz] + wyz * u1[qz] + wzz * u2[qz];
-        }
-      } else {
-        const double* w = A.W + e * QQQ + lane;
-#pragma unroll
-        for (int qz = 0; qz < Q; ++qz) {
-          const double wq = __ldg(w + qz * Q * Q);
-          v0[qz] = A.scale[0] * wq * u0[qz];
-          v1[qz] = A.scale[1] * wq * u1[qz];
-          v2[qz] = A.scale[2] * wq * u2[qz];
-        }
-      }
-    }
-    {
-      const ElemBasis B0 = elem_basis<P, DUAL, 0>(A, ex, ey, ez);
-      test<P, Q, DUAL, 0>(B0, A.y[0], A.ext[0], Ab, Bb, lane, v0);
-      const ElemBasis B1 = elem_basis<P, DUAL, 1>(A, ex, ey, ez);
-      test<P, Q, DUAL, 1>(B1, A.y[1], A.ext[1], Ab, Bb, lane, v1);
-      const ElemBasis B2 = elem_basis<P, DUAL, 2>(A, ex, ey, ez);
-      test<P, Q, DUAL, 2>(B2, A.y[2], A.ext[2], Ab, Bb, lane, v2);
-    }
-  }
-}
 
-
-// ---- z-pencil variant: a warp walks the elements (ex, ey, 0..nz-1).  Consecutive elements share
-// all but one coefficient layer along z (the first local function index advances by one), so the
-// coefficient box is shifted by one layer per element (one new layer loaded), and the output box is
-// accumulated in shared memory: after element ez its lowest layer is complete and is flushed to
-// global memory with atomics (neighbouring pencils share it); atomics and gathers drop by NZ.
 template <int P, bool DUAL, int C>
 struct Box {
   static constexpr int NX = nloc<P, DUAL, C, 0>(), NY = nloc<P, DUAL, C, 1>(), NZ = nloc<P, DUAL, C, 2>();
   static constexpr int LAYER = NX * NY, SIZE = LAYER * NZ;
 };
-
-template <int P, int Q, bool DUAL, int C>
-__device__ __forceinline__ void interp_box(const ElemBasis& B, const double* X, double* Abuf, double* Bbuf,
-                                           int lane, double (&u)[Q]) {
-  using BX = Box<P, DUAL, C>;
-  constexpr int NX = BX::NX, NY = BX::NY, NZ = BX::NZ, NL = P + 1;
-  for (int o = lane; o < NZ * NY * Q; o += 32) {
-    const int qx = o % Q, r = o / Q;
-    const double* vx = B.v[0] + qx * NL;
-    double s = 0.0;
-#pragma unroll
-    for (int jx = 0; jx < NX; ++jx) s = fma(__ldg(vx + jx), X[r * NX + jx], s);
-    Abuf[o] = s;
-  }
-  __syncwarp();
-  for (int o = lane; o < NZ * Q * Q; o += 32) {
-    const int qx = o % Q, qy = (o / Q) % Q, jz = o / (Q * Q);
-    const double* vy = B.v[1] + qy * NL;
-    double s = 0.0;
-#pragma unroll
-    for (int jy = 0; jy < NY; ++jy) s = fma(__ldg(vy + jy), Abuf[(jz * NY + jy) * Q + qx], s);
-    Bbuf[o] = s;
-  }
-  __syncwarp();
-  if (lane < Q * Q) {
-    double b[NZ];
-#pragma unroll
-    for (int jz = 0; jz < NZ; ++jz) b[jz] = Bbuf[jz * Q * Q + lane];
-#pragma unroll
-    for (int qz = 0; qz < Q; ++qz) {
-      const double* vz = B.v[2] + qz * NL;
-      double s = 0.0;
-#pragma unroll
-      for (int jz = 0; jz < NZ; ++jz) s = fma(__ldg(vz + jz), b[jz], s);
-      u[qz] = s;
-    }
-  }
-  __syncwarp();
-}
-
-template <int P, int Q, bool DUAL, int C>
-__device__ __forceinline__ void test_box(const ElemBasis& B, double* Y, double* Abuf, double* Bbuf, int lane,
-                                         const double (&v)[Q]) {
-  using BX = Box<P, DUAL, C>;
-  constexpr int NX = BX::NX, NY = BX::NY, NZ = BX::NZ, NL = P + 1;
-  if (lane < Q * Q) {
-#pragma unroll
-    for (int jz = 0; jz < NZ; ++jz) {
-      double s = 0.0;
-#pragma unroll
-      for (int qz = 0; qz < Q; ++qz) s = fma(__ldg(B.v[2] + qz * NL + jz), v[qz], s);
-      Bbuf[jz * Q * Q + lane] = s;
-    }
-  }
-  __syncwarp();
-  for (int o = lane; o < NZ * NY * Q; o += 32) {
-    const int qx = o % Q, jy = (o / Q) % NY, jz = o / (Q * NY);
-    double s = 0.0;
-#pragma unroll
-    for (int qy = 0; qy < Q; ++qy) s = fma(__ldg(B.v[1] + qy * NL + jy), Bbuf[(jz * Q + qy) * Q + qx], s);
-    Abuf[o] = s;
-  }
-  __syncwarp();
-  for (int o = lane; o < NX * NY * NZ; o += 32) {
-    const int jx = o % NX, r = o / NX;
-    double s = 0.0;
-#pragma unroll
-    for (int qx = 0; qx < Q; ++qx) s = fma(__ldg(B.v[0] + qx * NL + jx), Abuf[r * Q + qx], s);
-    Y[o] += s;
-  }
-  __syncwarp();
-}
 
 // load coefficient layer jz (global z index gz) of component C into X (zero outside the component)
 template <int P, bool DUAL, int C>
@@ -333,105 +108,11 @@ __device__ __forceinline__ void flush_shift(const ElemBasis& B, double* __restri
   __syncwarp();
 }
 
-template <int P, int Q, bool DUAL, bool FULL>
-__global__ void __launch_bounds__(256) hodge_pencil_kernel(const __grid_constant__ HodgeArgs A) {
-  constexpr int QQQ = Q * Q * Q;
-  constexpr int XB = max_box<P, DUAL>();
-  constexpr int AB = (P + 1) * (P + 1) * Q;
-  constexpr int BB = (P + 1) * Q * Q;
-  static_assert(Q * Q <= 32, "one warp per element needs Q*Q <= 32");
-  extern __shared__ double smp[];
-  const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  double* base = smp + wib * (6 * XB + AB + BB);
-  double* X[3] = {base, base + XB, base + 2 * XB};
-  double* Y[3] = {base + 3 * XB, base + 4 * XB, base + 5 * XB};
-  double* Ab = base + 6 * XB;
-  double* Bb = Ab + AB;
-  const int nx = A.nel[0], ny = A.nel[1], nz = A.nel[2];
-  const long npen = long(nx) * ny;
-  const long wstride = long(gridDim.x) * (blockDim.x >> 5);
-  for (long pen = long(blockIdx.x) * (blockDim.x >> 5) + wib; pen < npen; pen += wstride) {
-    const int ex = int(pen % nx), ey = int(pen / nx);
-    ElemBasis B0 = elem_basis<P, DUAL, 0>(A, ex, ey, 0);
-    ElemBasis B1 = elem_basis<P, DUAL, 1>(A, ex, ey, 0);
-    ElemBasis B2 = elem_basis<P, DUAL, 2>(A, ex, ey, 0);
-    // initial boxes: layers 0 .. NZ-2 of element 0 (the top layer is loaded at each element)
-    for (int o = lane; o < 3 * XB; o += 32) Y[0][o] = 0.0;  // Y[0..2] are contiguous
-    __syncwarp();
-    for (int jz = 0; jz + 1 < Box<P, DUAL, 0>::NZ; ++jz)
-      load_layer<P, DUAL, 0>(B0, A.x[0], A.ext[0], B0.first[2] + jz, X[0] + jz * Box<P, DUAL, 0>::LAYER, lane);
-    for (int jz = 0; jz + 1 < Box<P, DUAL, 1>::NZ; ++jz)
-      load_layer<P, DUAL, 1>(B1, A.x[1], A.ext[1], B1.first[2] + jz, X[1] + jz * Box<P, DUAL, 1>::LAYER, lane);
-    for (int jz = 0; jz + 1 < Box<P, DUAL, 2>::NZ; ++jz)
-      load_layer<P, DUAL, 2>(B2, A.x[2], A.ext[2], B2.first[2] + jz, X[2] + jz * Box<P, DUAL, 2>::LAYER, lane);
-    for (int ez = 0; ez < nz; ++ez) {
-      const long e = ex + long(nx) * (ey + long(ny) * ez);
-      B0 = elem_basis<P, DUAL, 0>(A, ex, ey, ez);
-      B1 = elem_basis<P, DUAL, 1>(A, ex, ey, ez);
-      B2 = elem_basis<P, DUAL, 2>(A, ex, ey, ez);
-      load_layer<P, DUAL, 0>(B0, A.x[0], A.ext[0], B0.first[2] + Box<P, DUAL, 0>::NZ - 1,
-                             X[0] + (Box<P, DUAL, 0>::NZ - 1) * Box<P, DUAL, 0>::LAYER, lane);
-      load_layer<P, DUAL, 1>(B1, A.x[1], A.ext[1], B1.first[2] + Box<P, DUAL, 1>::NZ - 1,
-                             X[1] + (Box<P, DUAL, 1>::NZ - 1) * Box<P, DUAL, 1>::LAYER, lane);
-      load_layer<P, DUAL, 2>(B2, A.x[2], A.ext[2], B2.first[2] + Box<P, DUAL, 2>::NZ - 1,
-                             X[2] + (Box<P, DUAL, 2>::NZ - 1) * Box<P, DUAL, 2>::LAYER, lane);
-      __syncwarp();
-      double u0[Q], u1[Q], u2[Q];
-      interp_box<P, Q, DUAL, 0>(B0, X[0], Ab, Bb, lane, u0);
-      interp_box<P, Q, DUAL, 1>(B1, X[1], Ab, Bb, lane, u1);
-      interp_box<P, Q, DUAL, 2>(B2, X[2], Ab, Bb, lane, u2);
-      double v0[Q], v1[Q], v2[Q];
-      if (lane < Q * Q) {
-        if (FULL) {
-          const double* w = A.W + (e * QQQ + lane) * 6;
-#pragma unroll
-          for (int qz = 0; qz < Q; ++qz) {
-            const double* wq = w + qz * Q * Q * 6;
-            const double wxx = __ldg(wq), wyy = __ldg(wq + 1), wzz = __ldg(wq + 2), wxy = __ldg(wq + 3),
-                         wxz = __ldg(wq + 4), wyz = __ldg(wq + 5);
-            v0[qz] = wxx * u0[qz] + wxy * u1[qz] + wxz * u2[qz];
-            v1[qz] = wxy * u0[qz] + wyy * u1[qz] + wyz * u2[qz];
-            v2[qz] = wxz * u0[qz] + wyz * u1[qz] + wzz * u2[qz];
-          }
-        } else {
-          const double* w = A.W + e * QQQ + lane;
-#pragma unroll
-          for (int qz = 0; qz < Q; ++qz) {
-            const double wq = __ldg(w + qz * Q * Q);
-            v0[qz] = A.scale[0] * wq * u0[qz];
-            v1[qz] = A.scale[1] * wq * u1[qz];
-            v2[qz] = A.scale[2] * wq * u2[qz];
-          }
-        }
-      }
-      test_box<P, Q, DUAL, 0>(B0, Y[0], Ab, Bb, lane, v0);
-      test_box<P, Q, DUAL, 1>(B1, Y[1], Ab, Bb, lane, v1);
-      test_box<P, Q, DUAL, 2>(B2, Y[2], Ab, Bb, lane, v2);
-      // the lowest layer of every box is complete: flush it, shift boxes down one layer
-      flush_shift<P, DUAL, 0>(B0, A.y[0], A.ext[0], B0.first[2], Y[0], X[0], lane, true);
-      flush_shift<P, DUAL, 1>(B1, A.y[1], A.ext[1], B1.first[2], Y[1], X[1], lane, true);
-      flush_shift<P, DUAL, 2>(B2, A.y[2], A.ext[2], B2.first[2], Y[2], X[2], lane, true);
-    }
-    // flush the remaining NZ - 1 layers of the last element
-    ElemBasis L0 = elem_basis<P, DUAL, 0>(A, ex, ey, nz - 1);
-    ElemBasis L1 = elem_basis<P, DUAL, 1>(A, ex, ey, nz - 1);
-    ElemBasis L2 = elem_basis<P, DUAL, 2>(A, ex, ey, nz - 1);
-    for (int jz = 1; jz < Box<P, DUAL, 0>::NZ; ++jz)
-      flush_shift<P, DUAL, 0>(L0, A.y[0], A.ext[0], L0.first[2] + jz, Y[0], X[0], lane, false);
-    for (int jz = 1; jz < Box<P, DUAL, 1>::NZ; ++jz)
-      flush_shift<P, DUAL, 1>(L1, A.y[1], A.ext[1], L1.first[2] + jz, Y[1], X[1], lane, false);
-    for (int jz = 1; jz < Box<P, DUAL, 2>::NZ; ++jz)
-      flush_shift<P, DUAL, 2>(L2, A.y[2], A.ext[2], L2.first[2] + jz, Y[2], X[2], lane, false);
-  }
-}
 
-// ---- v3: z-pencil with lane roles.  Interpolation: lane (qx, qy) computes its z-column directly
-// (x and y contractions fused per lane, coefficients read by broadcast); testing: lanes take the
-// roles (qx, jy) and then (jx, jy) so that every reduction over quadrature points is a per-lane
-// loop over shared memory (no atomics inside the warp, no redundant work).  The pencil's x and y
-// bases live in shared memory for the whole pencil, the element's z bases are staged per element.
+// ---- interpolation / testing of one component (lane roles above); the pencil's x and y bases
+// live in shared memory for the whole pencil, the element's z bases are staged per element.
 template <int P, int Q, bool DUAL, int C>
-__device__ __forceinline__ void interp_v3(const double* X, const double* Vx, const double* Vy, const double* Vz,
+__device__ __forceinline__ void interp_pencil(const double* X, const double* Vx, const double* Vy, const double* Vz,
                                           int lane, double (&u)[Q]) {
   using BX = Box<P, DUAL, C>;
   constexpr int NX = BX::NX, NY = BX::NY, NZ = BX::NZ, NL = P + 1;
@@ -466,7 +147,7 @@ __device__ __forceinline__ void interp_v3(const double* X, const double* Vx, con
 }
 
 template <int P, int Q, bool DUAL, int C>
-__device__ __forceinline__ void test_v3(double* Y, const double* Vx, const double* Vy, const double* Vz, double* Cb,
+__device__ __forceinline__ void test_pencil(double* Y, const double* Vx, const double* Vy, const double* Vz, double* Cb,
                                         double* Tb, int lane, const double (&v)[Q]) {
   using BX = Box<P, DUAL, C>;
   constexpr int NX = BX::NX, NY = BX::NY, NZ = BX::NZ, NL = P + 1;
@@ -514,7 +195,7 @@ __device__ __forceinline__ void test_v3(double* Y, const double* Vx, const doubl
 }
 
 template <int P, int Q, bool DUAL, bool FULL>
-__global__ void __launch_bounds__(256, 2) hodge_v3_kernel(const __grid_constant__ HodgeArgs A) {
+__global__ void __launch_bounds__(256, 2) hodge_pencil_kernel(const __grid_constant__ HodgeArgs A) {
   constexpr int QQQ = Q * Q * Q, NL = P + 1;
   constexpr int XB = max_box<P, DUAL>();
   constexpr int VB = Q * NL;                 // one 1D element basis [Q][NL]
@@ -590,9 +271,9 @@ __global__ void __launch_bounds__(256, 2) hodge_v3_kernel(const __grid_constant_
       if (ez + 1 < nz) prefetch(ez + 1);
       __syncwarp();
       double u0[Q], u1[Q], u2[Q];
-      interp_v3<P, Q, DUAL, 0>(X[0], Vb + 0 * VB, Vb + 1 * VB, Vb + 2 * VB, lane, u0);
-      interp_v3<P, Q, DUAL, 1>(X[1], Vb + 3 * VB, Vb + 4 * VB, Vb + 5 * VB, lane, u1);
-      interp_v3<P, Q, DUAL, 2>(X[2], Vb + 6 * VB, Vb + 7 * VB, Vb + 8 * VB, lane, u2);
+      interp_pencil<P, Q, DUAL, 0>(X[0], Vb + 0 * VB, Vb + 1 * VB, Vb + 2 * VB, lane, u0);
+      interp_pencil<P, Q, DUAL, 1>(X[1], Vb + 3 * VB, Vb + 4 * VB, Vb + 5 * VB, lane, u1);
+      interp_pencil<P, Q, DUAL, 2>(X[2], Vb + 6 * VB, Vb + 7 * VB, Vb + 8 * VB, lane, u2);
       double v0[Q], v1[Q], v2[Q];
       if (lane < Q * Q) {
         if (FULL) {
@@ -617,9 +298,9 @@ __global__ void __launch_bounds__(256, 2) hodge_v3_kernel(const __grid_constant_
           }
         }
       }
-      test_v3<P, Q, DUAL, 0>(Y[0], Vb + 0 * VB, Vb + 1 * VB, Vb + 2 * VB, Cb, Tb, lane, v0);
-      test_v3<P, Q, DUAL, 1>(Y[1], Vb + 3 * VB, Vb + 4 * VB, Vb + 5 * VB, Cb, Tb, lane, v1);
-      test_v3<P, Q, DUAL, 2>(Y[2], Vb + 6 * VB, Vb + 7 * VB, Vb + 8 * VB, Cb, Tb, lane, v2);
+      test_pencil<P, Q, DUAL, 0>(Y[0], Vb + 0 * VB, Vb + 1 * VB, Vb + 2 * VB, Cb, Tb, lane, v0);
+      test_pencil<P, Q, DUAL, 1>(Y[1], Vb + 3 * VB, Vb + 4 * VB, Vb + 5 * VB, Cb, Tb, lane, v1);
+      test_pencil<P, Q, DUAL, 2>(Y[2], Vb + 6 * VB, Vb + 7 * VB, Vb + 8 * VB, Cb, Tb, lane, v2);
       flush_shift<P, DUAL, 0>(B0, A.y[0], A.ext[0], B0.first[2], Y[0], X[0], lane, true);
       flush_shift<P, DUAL, 1>(B1, A.y[1], A.ext[1], B1.first[2], Y[1], X[1], lane, true);
       flush_shift<P, DUAL, 2>(B2, A.y[2], A.ext[2], B2.first[2], Y[2], X[2], lane, true);

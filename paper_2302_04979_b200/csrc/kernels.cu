@@ -1,18 +1,13 @@
-// sm_100a kernels of the scheme-2 leapfrog step (arXiv 2302.04979).
+// sm_100a kernels of the scheme-2 leapfrog step (arXiv 2302.04979) and their launchers.
 //
-// * Line sweeps (Kronecker factors applied mode by mode, eq. kroninverse P:L571 with the vec
-//   trick P:L575-585): a CTA stages `nl` whole lines of one component in shared memory
-//   (cp.async, no register staging), each thread then walks one line: an optional banded
-//   mat-vec (separable Hodge Gram or pairing factor) fused with the forward substitution of a
-//   no-pivot banded LU, then the backward substitution, in place in shared memory; the result
-//   is stored coalesced.  x-lines are contiguous and use an odd smem pitch (conflict-free
-//   line walks); y/z lines are strided and are staged element-major so that the 32 lanes of
-//   a warp touch 32 consecutive x.
-// * The Ampere / Faraday updates (integer +-1 curls, eqs. discrete2_ampere / _faraday,
-//   P:L201) are fused into the load of the first (x) sweep of each half step.
-// * General Hodge (curved F or variable material): per-element sum factorisation with the
-//   quadrature weights W streamed from HBM, accumulated with fp64 atomics.
-// * Deterministic two-pass reductions for the energy and Gauss residuals.
+// * Line sweeps (sweep_kernel.cuh): the Kronecker factors applied mode by mode (eq. kroninverse
+//   P:L571 with the vec trick P:L575-585): per line, a banded 1D mat-vec (separable Hodge Gram or
+//   pairing factor) and a partitioned no-pivot banded LU solve, in persistent warp-specialised CTAs.
+// * Ampere / Faraday updates (integer +-1 curls, eqs. discrete2_ampere / _faraday):
+//   a streaming element-wise kernel.
+// * General Hodge (curved F or variable material, hodge_kernel.cuh): element-wise sum
+//   factorisation with the quadrature weights W streamed from HBM.
+// * Curls, divergences (Gauss laws) and deterministic two-pass reductions (energy).
 #include <cuda_runtime.h>
 
 #include <cstdio>
@@ -59,21 +54,6 @@ __device__ __forceinline__ double curl_comp(const double* const* src, const int 
   return dterm_primal(src[c1], sext[c1], a1, x, y, z) - dterm_primal(src[c2], sext[c2], a2, x, y, z);
 }
 
-template <int PRO>
-__device__ __forceinline__ double update_value(const PrologueArgs& P, int c, const double* state, long idx, int x, int y,
-                                               int z) {
-  if (PRO == PRO_AMPERE) {
-    double cu = curl_comp<true>(P.src, P.sext, c, x, y, z);
-    if (P.jhat[c]) {
-      double s = P.s_ptr ? __ldg(P.s_ptr) : 1.0;
-      cu -= s * __ldg(P.jhat[c] + idx);
-    }
-    return state[idx] + P.dt * cu;                    // d + dt (D~1 h - s j)
-  } else {
-    double cu = curl_comp<false>(P.src, P.sext, c, x, y, z);
-    return state[idx] - P.dt * cu;                    // b - dt D1 e
-  }
-}
 
 // ---- element-wise Ampere / Faraday update (eqs. discrete2_ampere / _faraday) ----
 //   AMPERE : d_c <- d_c + dt ((D~1 h)_c - s j_c)     dual   (dv)_k = v_{k+1} - v_k
@@ -613,8 +593,9 @@ void launch_curl(int kind, const double* const src[3], const int sext[3][3], dou
 
 template <int P, int Q, bool DUAL, bool FULL>
 void launch_hodge_pencil(const HodgeArgs& a, cudaStream_t st) {
-  constexpr int XB = hodge::max_box<P, DUAL>(), AB = (P + 1) * (P + 1) * Q, BB = (P + 1) * Q * Q;
-  const size_t smem = size_t(8) * (6 * XB + AB + BB) * sizeof(double);
+  constexpr int NL = P + 1, XB = hodge::max_box<P, DUAL>(), VB = Q * NL, CB = (P + 1) * Q * Q,
+                TB = (P + 1) * (P + 1) * Q;
+  const size_t smem = size_t(8) * (6 * XB + 9 * VB + CB + TB) * sizeof(double);
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(hodge::hodge_pencil_kernel<P, Q, DUAL, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -628,62 +609,21 @@ void launch_hodge_pencil(const HodgeArgs& a, cudaStream_t st) {
   hodge::hodge_pencil_kernel<P, Q, DUAL, FULL><<<unsigned(grid), 256, smem, st>>>(a);
 }
 
-template <int P, int Q, bool DUAL, bool FULL>
-void launch_hodge_v3(const HodgeArgs& a, cudaStream_t st) {
-  constexpr int NL = P + 1, XB = hodge::max_box<P, DUAL>(), VB = Q * NL, CB = (P + 1) * Q * Q,
-                TB = (P + 1) * (P + 1) * Q;
-  const size_t smem = size_t(8) * (6 * XB + 9 * VB + CB + TB) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(hodge::hodge_v3_kernel<P, Q, DUAL, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
-    attr = true;
-  }
-  const long npen = long(a.nel[0]) * a.nel[1];
-  long grid = (npen + 7) / 8;
-  const long cap = 16L * sm_count();
-  if (grid > cap) grid = cap;
-  hodge::hodge_v3_kernel<P, Q, DUAL, FULL><<<unsigned(grid), 256, smem, st>>>(a);
-}
-
 template <int P, int Q>
 void launch_hodge2(const HodgeArgs& a, cudaStream_t st) {
-  if (env_int("SGM_HODGE_V", 3) == 3) {
-    if (a.dual) {
-      if (a.full) launch_hodge_v3<P, Q, true, true>(a, st);
-      else launch_hodge_v3<P, Q, true, false>(a, st);
-    } else {
-      if (a.full) launch_hodge_v3<P, Q, false, true>(a, st);
-      else launch_hodge_v3<P, Q, false, false>(a, st);
-    }
-    return;
-  }
-  if (env_int("SGM_HODGE_PENCIL", 1)) {
-    if (a.dual) {
-      if (a.full) launch_hodge_pencil<P, Q, true, true>(a, st);
-      else launch_hodge_pencil<P, Q, true, false>(a, st);
-    } else {
-      if (a.full) launch_hodge_pencil<P, Q, false, true>(a, st);
-      else launch_hodge_pencil<P, Q, false, false>(a, st);
-    }
-    return;
-  }
-  const long nel = long(a.nel[0]) * a.nel[1] * a.nel[2];
-  long grid = (nel + 7) / 8;
-  const long cap = 16L * sm_count();
-  if (grid > cap) grid = cap;
   if (a.dual) {
-    if (a.full) hodge::hodge2_kernel<P, Q, true, true><<<unsigned(grid), 256, 0, st>>>(a);
-    else hodge::hodge2_kernel<P, Q, true, false><<<unsigned(grid), 256, 0, st>>>(a);
+    if (a.full) launch_hodge_pencil<P, Q, true, true>(a, st);
+    else launch_hodge_pencil<P, Q, true, false>(a, st);
   } else {
-    if (a.full) hodge::hodge2_kernel<P, Q, false, true><<<unsigned(grid), 256, 0, st>>>(a);
-    else hodge::hodge2_kernel<P, Q, false, false><<<unsigned(grid), 256, 0, st>>>(a);
+    if (a.full) launch_hodge_pencil<P, Q, false, true>(a, st);
+    else launch_hodge_pencil<P, Q, false, false>(a, st);
   }
 }
 
 void launch_hodge_general(int p, const HodgeArgs& a, cudaStream_t st) {
-  // warp-per-element sum factorisation (hodge_kernel.cuh) for the default rule Q = p + 1
-  if (a.Q == p + 1 && env_int("SGM_HODGE_V1", 0) == 0) {
+  // z-pencil warp kernel (hodge_kernel.cuh) for the default rule Q = p + 1; the generic
+  // CTA-per-element kernel for larger rules (quad_points > p + 1)
+  if (a.Q == p + 1) {
     switch (p) {
       case 2: launch_hodge2<2, 3>(a, st); return;
       case 3: launch_hodge2<3, 4>(a, st); return;

@@ -8,9 +8,9 @@ namespace sgm {
 
 constexpr int kMaxLine = 392;  // <= 14 segments of <= 28 rows (sweep_kernel.cuh)
 
-// One component handled by a line sweep along `axis`.
+// One component handled by a line sweep along `axis` (or by the update kernel: `in` = state).
 struct SweepComp {
-  double* in;         // input component array [z][y][x] (updated in place by a prologue)
+  double* in;         // input component array [z][y][x] (the state, for the update kernel)
   double* out;        // output component array (may equal in)
   const double* tab;  // line-operator table (seg_sweep.cuh rows), global memory
   int tslot;          // which of SweepArgs::tabs this component uses (staged in shared memory)
@@ -18,10 +18,9 @@ struct SweepComp {
   double scale;       // multiplies the stored result
 };
 
-// Element-wise prologue fused into the x-sweep (or run standalone):
-//   AMPERE : in[c] += dt * ((D~1 src)_c - s * jhat[c])   (eq. discrete2_ampere)
-//   FARADAY: in[c] -= dt * (D1 src)_c                    (eq. discrete2_faraday)
-// The updated state is written back to in[c] and fed to the sweep.
+// Element-wise state update of a half step (launch_update):
+//   AMPERE : in[c] += dt * ((D~1 src)_c - s * jhat[c])   (eq. discrete2_ampere, P:L369)
+//   FARADAY: in[c] -= dt * (D1 src)_c                    (eq. discrete2_faraday, P:L371)
 enum Prologue { PRO_NONE = 0, PRO_AMPERE = 1, PRO_FARADAY = 2 };
 
 struct PrologueArgs {
@@ -38,13 +37,11 @@ struct SweepArgs {
   int axis;       // 0 = x (contiguous lines), 1 = y, 2 = z
   int band;       // apply the banded mat-vec (mass / pairing factor)
   int solve;      // apply the banded LU solve
-  int pro_kind;   // Prologue (strided axes only)
-  int seg_pad;    // unused (kept for layout stability)
   const double* tabs[2];  // the (at most two) distinct line-operator tables of this pass
   int tab_rows;           // rows per table (padded line length of this axis)
   int band_hw;            // half-bandwidth of the banded mat-vec of this pass (<= P)
   int spike_kh, spike_kf; // truncated-SPIKE reach of the history / future scans (segments)
-  PrologueArgs pro;
+  PrologueArgs pro;       // update kernel only
 };
 
 // General (non-separable) Hodge apply y = M x by sum factorisation per element.

@@ -1,23 +1,6 @@
-// Persistent, warp-specialised, double-buffered line sweeps (sm_100a).
-//
-// What one sweep computes (eq. kroninverse P:L571 applied mode by mode with the vec trick
-// P:L575-585): for every line of every component along axis `ax`,
-//     out_line = scale * A^{-1} (B in_line)
-// with B a banded 1D matrix (separable Hodge Gram or pairing factor) and A = LU a banded 1D
-// pairing factor (no-pivot LU, reading Z14).  The solve is the partitioned (SPIKE) form of the
-// sequential banded substitution: segment-local recurrences plus spike corrections (exact
-// algebra; seg_sweep.cuh documents the table layout).
-//
-// Work unit: a tile of 32 lines of one component (lane j <-> line j).  A CTA is persistent and
-// loops over tiles with two shared-memory slabs:
-//   * producer warps (NP) stage tile t+1 into slab[(t+1)&1] -- cp.async (LDGSTS) copies, or, for
-//     the first pass of a half step, the fused Ampere/Faraday update d <- d + dt (D~1 h - s j)
-//     (b <- b - dt D1 e) computed from global loads, written back to the state and to the slab;
-//   * consumer warps (NC = segments) run the banded mat-vec + SPIKE solve on slab[t&1] and store.
-// Producer/consumer hand-off uses named barriers (FULL[b] / EMPTY[b]); the SPIKE exchanges use a
-// consumer-only barrier.  Strided axes (y, z): slab row i holds element i of the 32 lines (lanes
-// read consecutive doubles); x axis: slab row j holds line j with an odd pitch (conflict-free
-// per-lane walks) and results go back through the slab for coalesced row stores.
+// Synchronisation and copy primitives of the pipelined sweeps (sm_100a): named barriers for the
+// producer/consumer hand-off, cp.async (LDGSTS) 8-byte copies, mbarriers with bulk copies (TMA
+// engine) global <-> shared, proxy fences, and programmatic dependent launch controls.
 #pragma once
 
 #include "kernels.cuh"
@@ -39,31 +22,6 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-
-// Geometry of one component for a sweep along `ax`.
-struct LineGeom {
-  long nlines;  // lines of this component
-  long gs;      // element stride along the line
-  int L;        // line length
-  int X, Y;     // component extents x, y
-};
-
-__device__ __forceinline__ LineGeom line_geom(const SweepComp& C, int ax) {
-  LineGeom g;
-  g.X = C.ext[0];
-  g.Y = C.ext[1];
-  g.L = C.ext[ax];
-  g.nlines = long(C.ext[0]) * C.ext[1] * C.ext[2] / g.L;
-  g.gs = (ax == 0) ? 1 : (ax == 1 ? long(g.X) : long(g.X) * g.Y);
-  return g;
-}
-
-// flat index of element 0 of line l, and its (x, y, z) decomposition helpers
-__device__ __forceinline__ long line_base(const LineGeom& g, int ax, long l) {
-  if (ax == 0) return l * g.X;
-  if (ax == 1) return (l % g.X) + long(g.X) * g.Y * (l / g.X);
-  return l;
-}
 
 }  // namespace pipe
 }  // namespace sgm
