@@ -279,7 +279,8 @@ def main():
     if jhat is not None:
         tt = (np.arange(K + W) + 0.5) * dt
         jamp = torch.from_numpy(np.exp(-((tt - 0.15) / 0.05) ** 2)).to(dev)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()          # a dedicated stream (sgm_step graph-captures its launches)
+    torch.cuda.set_stream(stream)
 
     def steps(k0, k):
         # one C-ABI call for k steps (the library loops on the device stream)

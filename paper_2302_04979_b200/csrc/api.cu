@@ -383,6 +383,7 @@ sgm_status sgm_plan_create(const sgm_plan_desc* desc, sgm_plan* out) {
   P->p = p;
   P->Q = Q;
   P->device = desc->device;
+  if (const char* ge = getenv("SGM_GRAPH")) P->graph_enabled = atoi(ge) != 0;
   std::string err;
   for (int a = 0; a < 3; ++a) {
     P->n[a] = desc->n_el[a];
@@ -437,6 +438,7 @@ sgm_status sgm_plan_destroy(sgm_plan plan) {
   Plan* P = PL(plan);
   if (P->device >= 0) {
     DeviceGuard g(P->device);
+    if (P->graph_exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec));
     cudaFree(P->tables_dev);
     cudaFree(P->basis_dev);
     cudaFree(P->first_dev);
@@ -508,6 +510,11 @@ sgm_status sgm_plan_hodge_separable(sgm_plan plan, sgm_mass mass, int* separable
 }
 
 sgm_status sgm_plan_set_material(sgm_plan plan, sgm_material which, const double* values, double c) {
+  if (plan && PL(plan)->graph_exec) {  // captured launches embed the old weights and kinds
+    DeviceGuard g0(PL(plan)->device);
+    cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(PL(plan)->graph_exec));
+    PL(plan)->graph_exec = nullptr;
+  }
   sgm_status s = check_plan(plan, false);
   if (s != SGM_OK) return s;
   if (which != SGM_EPS && which != SGM_MU) return fail(SGM_E_INVALID_ARG, "bad material");
@@ -550,6 +557,34 @@ sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h, c
   if ((s = ws_carve(*P, workspace, ws_bytes, w)) != SGM_OK) return s;
   DeviceGuard g(P->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n_steps == 0) return SGM_OK;
+  // CUDA graph: the launch sequence of ONE step is captured once per argument set and replayed
+  // n_steps times (removes the per-kernel host enqueue cost, which dominates on small meshes).
+  // Used when every step has identical arguments (no per-step source amplitudes), not on the
+  // legacy default stream (capture is not allowed there) and not while profiling records events.
+  const bool use_graph = !P->profiling && stream != nullptr && P->graph_enabled && j_amp == nullptr;
+  if (use_graph) {
+    const GraphKey key{d, e, b, h, j_hat, nullptr, dt, 1, workspace};
+    if (!(P->graph_exec && P->graph_key == key)) {
+      if (P->graph_exec) {
+        cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec));
+        P->graph_exec = nullptr;
+      }
+      cudaGraph_t graph = nullptr;
+      if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+        return cuda_check(P, "sgm_step: begin capture");
+      step_once(*P, d, e, b, h, j_hat, nullptr, dt, w, st);
+      if (cudaStreamEndCapture(st, &graph) != cudaSuccess) return cuda_check(P, "sgm_step: end capture");
+      cudaGraphExec_t exec = nullptr;
+      const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ie != cudaSuccess) return cuda_check(P, "sgm_step: graph instantiate");
+      P->graph_exec = exec;
+      P->graph_key = key;
+    }
+    for (int k = 0; k < n_steps; ++k) cudaGraphLaunch(static_cast<cudaGraphExec_t>(P->graph_exec), st);
+    return cuda_check(P, "sgm_step (graph)");
+  }
   for (int k = 0; k < n_steps; ++k) step_once(*P, d, e, b, h, j_hat, j_amp ? j_amp + k : nullptr, dt, w, st);
   return cuda_check(P, "sgm_step");
 }

@@ -52,6 +52,18 @@ struct MassData {
   double material_c = 1.0;             // constant material value (eps or mu)
 };
 
+// Arguments a captured sgm_step graph was recorded with (replayed only for identical calls).
+struct GraphKey {
+  const void *d, *e, *b, *h, *jhat, *jamp;
+  double dt;
+  int n_steps;
+  const void* ws;
+  bool operator==(const GraphKey& o) const {
+    return d == o.d && e == o.e && b == o.b && h == o.h && jhat == o.jhat && jamp == o.jamp && dt == o.dt &&
+           n_steps == o.n_steps && ws == o.ws;
+  }
+};
+
 struct Plan {
   int p = 0;
   int Q = 0;
@@ -81,6 +93,9 @@ struct Plan {
   size_t mirror_bytes = 0;
   std::vector<double> tables_host;
   bool sticky_cuda_error = false;
+  bool graph_enabled = true;          // SGM_GRAPH=0 disables the sgm_step graph cache
+  void* graph_exec = nullptr;         // cudaGraphExec_t of the last captured sgm_step call
+  GraphKey graph_key{};
   size_t N_e = 0, N_h = 0;
   // optional per-kernel event timing (sgm_plan_set_profiling)
   bool profiling = false;

@@ -244,3 +244,31 @@ def test_c1_cavity_vs_tier_a():
     E = torch.zeros(1, dtype=torch.float64, device="cuda")
     pl.energy(*(dev(x) for x in out), E)
     assert abs(host(E)[0] - 0.125) < 0.01
+
+
+def test_nan_poisoned_workspace_and_graph_replay():
+    """The workspace (inter-sweep temporary and reduction partials) is fully overwritten before it
+    is read: poisoning it with NaN changes nothing.  Also: sgm_step on a non-default stream replays a
+    captured CUDA graph for identical calls; results equal the oracle both times."""
+    p, n = 3, (33, 7, 9)
+    pl = S.Plan(n, p)
+    tb = TierB(p, n)
+    st = _state(tb, 21)
+    dt = 0.01
+    ws = torch.full(((pl.workspace_bytes() + 7) // 8,), float("nan"), dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        d, e, b, h = (dev(x) for x in st)
+        pl.step(d, e, b, h, dt, 2, ws=ws, stream=s)          # captured
+        ref = tb.run(*st, dt, 2)
+        out = [host(x) for x in (d, e, b, h)]
+        for a, r in zip(out, ref):
+            assert np.all(np.isfinite(a)) and rel(a, r) < 1e-11
+        d2, e2, b2, h2 = (dev(x) for x in st)
+        ws.fill_(float("nan"))
+        # different pointers -> re-capture; then the same pointers again -> replay
+        pl.step(d2, e2, b2, h2, dt, 2, ws=ws, stream=s)
+        pl.step(d2, e2, b2, h2, dt, 2, ws=ws, stream=s)
+        ref2 = tb.run(*ref, dt, 2)
+        for a, r in zip((d2, e2, b2, h2), ref2):
+            assert rel(host(a), r) < 1e-11
