@@ -135,7 +135,7 @@ struct ProfScope {
 
 // One axis pass over the 3 components of a form (kind 0: e/d shapes, 1: b/h shapes).
 void sweep_pass(const Plan& P, int kind, int axis, double* const in[3], double* const out[3], int op_own,
-                int op_oth, const double* scale, bool band, bool solve, cudaStream_t st) {
+                int op_oth, const double* scale, bool band, bool solve, cudaStream_t st, int reverse = 0) {
   SweepArgs a;
   std::memset(&a, 0, sizeof(a));
   a.ncomp = 3;
@@ -146,6 +146,7 @@ void sweep_pass(const Plan& P, int kind, int axis, double* const in[3], double* 
   a.tabs[1] = table(P, axis, op_oth);
   a.tab_rows = P.rpad[axis];
   a.band_hw = std::max(P.band_hw[axis][op_own], P.band_hw[axis][op_oth]);
+  a.reverse = reverse;
   a.spike_kh = std::max(P.spike_kh[axis][op_own], P.spike_kh[axis][op_oth]);
   a.spike_kf = std::max(P.spike_kf[axis][op_own], P.spike_kf[axis][op_oth]);
   for (int c = 0; c < 3; ++c) {
@@ -335,9 +336,11 @@ void step_once(Plan& P, double* d, double* e, double* b, double* h, const double
       }
       a.pro = pa;
       { ProfScope ps(P, SGM_K_UPDATE, st); launch_update(pro, a, st); }
-      { ProfScope ps(P, kx, st); sweep_pass(P, kind, 2, state, T, own, oth, nullptr, true, true, st); }
-      { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, true, true, st); }
-      { ProfScope ps(P, kz, st); sweep_pass(P, kind, 0, T, outv, own, oth, M.scale, true, true, st); }
+      // snake order: update forward, z backward, y forward, x backward (each kernel starts on the
+      // tiles its predecessor wrote last)
+      { ProfScope ps(P, kx, st); sweep_pass(P, kind, 2, state, T, own, oth, nullptr, true, true, st, 1); }
+      { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, true, true, st, 0); }
+      { ProfScope ps(P, kz, st); sweep_pass(P, kind, 0, T, outv, own, oth, M.scale, true, true, st, 1); }
     } else {
       SweepArgs a;
       std::memset(&a, 0, sizeof(a));

@@ -79,6 +79,7 @@ struct UpdArgs {
   const double* s_ptr;
   double dt;
   int nchunks;
+  int reverse;  // walk the chunks last-to-first
 };
 
 __device__ __forceinline__ unsigned fdiv(unsigned n, unsigned d, unsigned m, unsigned& r) {
@@ -93,7 +94,8 @@ __global__ void __launch_bounds__(256, MINB) update_kernel(const __grid_constant
   constexpr bool DUAL = (PRO == PRO_AMPERE);
   pipe::griddep_launch_dependents();
   pipe::griddep_wait();
-  for (int ch = blockIdx.x; ch < A.nchunks; ch += gridDim.x) {
+  for (int ch0 = blockIdx.x; ch0 < A.nchunks; ch0 += gridDim.x) {
+    const int ch = A.reverse ? A.nchunks - 1 - ch0 : ch0;
     const int c = (ch >= A.c[2].chunk0) ? 2 : (ch >= A.c[1].chunk0 ? 1 : 0);
     const UpdComp& C = A.c[c];
     const int e0 = (ch - C.chunk0) * (256 * U) + threadIdx.x;
@@ -454,6 +456,7 @@ bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
   cfg.ntabs = (a.tabs[1] != nullptr && a.tabs[1] != a.tabs[0]) ? 2 : 1;
   cfg.tab_dbl = a.tab_rows * RowLayout<P>::RS;
   cfg.dbg = env_int("SGM_PIPE_DBG", 0);
+  cfg.reverse = env_int("SGM_SNAKE", 1) ? a.reverse : 0;
   constexpr int M = P - 1;
   const size_t smem = (size_t(cfg.ntabs) * cfg.tab_dbl + size_t(2) * cfg.slab + size_t(2) * cfg.NC * M * TW + 4) *
                       sizeof(double);
@@ -560,6 +563,7 @@ void launch_update(int pro, const SweepArgs& a, cudaStream_t st) {
     }
   }
   U.nchunks = chunk;
+  U.reverse = env_int("SGM_SNAKE", 1) ? a.reverse : 0;
   U.s_ptr = a.pro.s_ptr;
   U.dt = a.pro.dt;
   int grid = env_int("SGM_UPD_GRID", 8) * sm_count();

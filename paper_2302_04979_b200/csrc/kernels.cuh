@@ -41,6 +41,8 @@ struct SweepArgs {
   int tab_rows;           // rows per table (padded line length of this axis)
   int band_hw;            // half-bandwidth of the banded mat-vec of this pass (<= P)
   int spike_kh, spike_kf; // truncated-SPIKE reach of the history / future scans (segments)
+  int reverse;            // process the work items last-to-first ("snake" order across kernels:
+                          // a kernel starts on what its predecessor wrote last, still in L2)
   PrologueArgs pro;       // update kernel only
 };
 

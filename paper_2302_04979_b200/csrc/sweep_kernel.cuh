@@ -65,6 +65,7 @@ struct Cfg {
   int tab_dbl;    // doubles per staged table
   int ntabs;      // distinct tables (1 or 2)
   int dbg;        // tuning only (SGM_PIPE_DBG): bit 0 consumers skip work, bit 1 producers skip loads
+  int reverse;    // walk the tiles last-to-first (L2 reuse of what the previous kernel wrote last)
   int nitems;     // tiles over all components
   int tiles[3];   // tiles per component
   CompGeom g[3];
@@ -144,7 +145,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
     for (int item = blockIdx.x; item < cfg.nitems; item += G, ++it) {
       const int buf = it & 1;
       if (it >= 2) pipe::bar_sync(pipe::kBarEmpty0 + buf, NT);
-      int c = 0, tile = item;
+      int c = 0, tile = cfg.reverse ? cfg.nitems - 1 - item : item;
       while (c < 2 && tile >= cfg.tiles[c]) tile -= cfg.tiles[c++];
       const CompGeom& g = cfg.g[c];
       const SweepComp& C = A.comp[c];
@@ -225,7 +226,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
     const int buf = it & 1;
     if (bulk) pipe::mbar_wait(full_mb + buf, unsigned(it >> 1) & 1u);
     else pipe::bar_sync(pipe::kBarFull0 + buf, NT);
-    int c = 0, tile = item;
+    int c = 0, tile = cfg.reverse ? cfg.nitems - 1 - item : item;
     while (c < 2 && tile >= cfg.tiles[c]) tile -= cfg.tiles[c++];
     const CompGeom& g = cfg.g[c];
     const SweepComp& C = A.comp[c];
