@@ -272,3 +272,36 @@ def test_nan_poisoned_workspace_and_graph_replay():
         ref2 = tb.run(*ref, dt, 2)
         for a, r in zip((d2, e2, b2, h2), ref2):
             assert rel(host(a), r) < 1e-11
+
+
+def test_gpu_invariants_over_many_steps():
+    """Through the GPU path only (no oracle): the scheme-2 invariants hold over 400 steps of a
+    16^3 p = 3 cavity with a random state: the modified energy
+    E^ = 1/2 d^{n+1}.K1 e^{n+1} + 1/2 b^{n+1/2}.K~1 h^{n+3/2} is constant (reading Z19)
+    and the discrete Gauss laws D~2 d, D2 b are preserved."""
+    p, n = 3, 16
+    pl = S.Plan(n, p)
+    tb = TierB(p, n)
+    g = np.random.default_rng(30)
+    dt = 0.45 * 0.2020 / n
+    d, b = dev(g.standard_normal(tb.N_e)), dev(g.standard_normal(tb.N_h))
+    e, h = torch.empty_like(d), torch.empty_like(b)
+    pl.hodge_star(S.MASS_EPS, d, e)
+    pl.hodge_star(S.MASS_MU, b, h)
+    out = torch.zeros(2, dtype=torch.float64, device="cuda")
+    pl.gauss(d, b, out)
+    g0 = host(out).copy()
+    K1e, Kt1h = torch.empty_like(d), torch.empty_like(b)
+    energies = []
+    for _ in range(40):
+        pl.step(d, e, b, h, dt, 9)
+        b_prev = b.clone()
+        pl.step(d, e, b, h, dt, 1)
+        pl.pairing_apply(S.K1, e, K1e)
+        pl.pairing_apply(S.KT1, h, Kt1h)
+        energies.append(0.5 * float(torch.dot(d, K1e)) + 0.5 * float(torch.dot(b_prev, Kt1h)))
+    energies = np.array(energies)
+    assert np.ptp(energies) < 1e-12 * abs(energies.mean())
+    pl.gauss(d, b, out)
+    scale = max(float(torch.max(torch.abs(d))), float(torch.max(torch.abs(b))))
+    assert np.all(np.abs(host(out) - g0) <= 1e-11 * scale)
