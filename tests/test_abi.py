@@ -103,3 +103,22 @@ def test_error_codes():
     # on device plans (build_mass); device calls on a host-only plan are rejected:
     rc = S.sgm_step(pl.h, 8, 16, 24, 32, None, None, 0.1, 1, 64, 1 << 20, None)
     assert rc == 1
+
+
+def test_plain_c_consumer(tmp_path):
+    """The library is a C ABI: a plain C program compiled against include/sgm.h links libsgm.so and
+    runs host-side queries (no Python, no torch)."""
+    import shutil
+    import subprocess
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("gcc not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_2302_04979_b200")
+    exe = str(tmp_path / "abi_smoke")
+    subprocess.run([gcc, "-std=c99", "-O1", os.path.join(root, "tests", "c", "abi_smoke.c"), "-I",
+                    os.path.join(root, "include"), "-L", libdir, "-lsgm", "-Wl,-rpath," + libdir, "-o", exe],
+                   check=True)
+    r = subprocess.run([exe], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "abi_smoke ok" in r.stdout
