@@ -206,6 +206,48 @@ def cfl_dt_max(tb: TierB, tol=1e-8):
     return 2.0 / np.sqrt(lam)
 
 
+def cfl_power(tb, x0, n_iter):
+    """Power iteration for the same lambda_max, in the form SURVEY 8(d) fixes for reproducible dt
+    ("start vector rng(100+k), 300 iterations, Rayleigh quotient"; K8, NEXT #3).
+
+    A = D~1 K~1^{-1} M2 D1 K1^{-1} M~2 is self-adjoint and positive semi-definite in the M~2 inner
+    product: K1^T D~1 = D1^T K~1 (the pairing identity behind eq. P:L240) gives
+    M~2 A = C^T M2 C with C = D1 K1^{-1} M~2.  The Rayleigh quotient in that inner product is
+    x.M~2 A x / x.M~2 x = (b.K~1 h) / (x.K1 e) with e = K1^{-1} M~2 x, b = D1 e,
+    h = K~1^{-1} M2 b (K1 e = M~2 x, K~1 h = M2 b).  Each iteration:
+        e = K1^{-1} M~2 x;  b = D1 e;  h = K~1^{-1} M2 b;
+        lam_k = (b.K~1 h) / (x.K1 e);   y = D~1 h;   x = y / |y|_2
+    after normalising x0 to unit 2-norm.  Works with tier A or tier B (`tb` needs solve_K1,
+    solve_Kt1, mass_eps/mass_mu or Meps/Mmu, K1/Kt1 applies and the curls).
+    Returns (lam_{n_iter-1}, 2/sqrt(lam), x_{n_iter}, [lam_0 .. lam_{n_iter-1}])."""
+    hodge_eps, hodge_mu, K1e, Kt1h, D1, Dt1 = _ops(tb)
+    x = np.asarray(x0, dtype=np.float64) / np.sqrt(np.dot(x0, x0))
+    lams = []
+    for _ in range(n_iter):
+        e = hodge_eps(x)
+        b = D1(e)
+        h = hodge_mu(b)
+        lams.append(float(np.dot(b, Kt1h(h)) / np.dot(x, K1e(e))))
+        y = Dt1(h)
+        x = y / np.sqrt(np.dot(y, y))
+    lam = lams[-1]
+    return lam, 2.0 / np.sqrt(lam), x, lams
+
+
+def _ops(tb):
+    """(e <- K1^{-1}M~2 x, h <- K~1^{-1}M2 b, K1 e, K~1 h, D1, D~1) for tier A or tier B."""
+    if hasattr(tb, "Meps"):  # tier A: assembled sparse matrices
+        return (lambda x: tb.solve_K1(tb.Meps @ x), lambda b: tb.solve_Kt1(tb.Mmu @ b),
+                lambda e: tb.K1 @ e, lambda h: tb.Kt1 @ h,
+                lambda e: tb.D1 @ e, lambda h: tb.Dt1 @ h)
+    from .structured import curl_primal
+    return (tb.hodge_eps, tb.hodge_mu,
+            lambda e: forms.join(tb.apply_K1(tb.split_e(e))),
+            lambda h: forms.join(tb.apply_Kt1(tb.split_h(h))),
+            lambda e: forms.join(curl_primal(tb.split_e(e))),
+            lambda h: forms.join(curl_dual(tb.split_h(h))))
+
+
 # ------------------------------------------------------------------------------------------
 # consistent initial state
 # ------------------------------------------------------------------------------------------

@@ -239,3 +239,50 @@ def test_cfl_scalings():
     assert abs(c[(2, 4)] / c[(2, 8)] - 1) < 0.05
     slope = np.log(c[(4, 8)] / c[(2, 8)]) / np.log(2.0)
     assert -2.4 < slope < -1.2, slope
+
+
+def _dense_lambda_max(A):
+    """Brute force: the largest eigenvalue of the generalized symmetric problem
+    (C^T M2 C) v = lam M~2 v, C = D1 K1^{-1} M~2, from dense assembled tier-A matrices (LAPACK)."""
+    import scipy.linalg as sl
+    Meps = A.Meps.toarray()
+    C = A.D1.toarray() @ np.linalg.solve(A.K1.toarray(), Meps)
+    return sl.eigh(C.T @ A.Mmu.toarray() @ C, Meps, eigvals_only=True)[-1]
+
+
+@pytest.mark.parametrize("case", ["cube_p2", "aniso_p2", "curved_p3"])
+def test_cfl_power_pins(case):
+    """cfl_power: the Rayleigh quotients are nondecreasing and bounded by the
+    brute-force lambda_max (A is M~2-self-adjoint PSD), converge to it, and tier B iterates the same."""
+    if case == "cube_p2":
+        p, n, kw = 2, 3, {}
+    elif case == "aniso_p2":
+        p, n, kw = 2, (4, 5, 3), {}
+    else:
+        p, n = 2, (2, 3, 2)
+        ctrl, ie = _c3_like(p, n)
+        kw = dict(ctrl=ctrl, inv_eps_qp=ie)
+    A = TierA(p, n, **kw)
+    lam_d = _dense_lambda_max(A)
+    x0 = synth.rng(100).standard_normal(A.N_e)
+    iters = 3000 if case == "curved_p3" else 400   # smaller spectral gap on the curved map
+    lam, dt, x, lams = W.cfl_power(A, x0, iters)
+    lams = np.array(lams)
+    assert np.all(np.diff(lams) >= -1e-13 * lam_d)
+    assert lams.max() <= lam_d * (1 + 1e-12)
+    assert abs(lam / lam_d - 1) < 1e-6, (lam, lam_d)
+    assert dt == 2.0 / np.sqrt(lam)
+    if case != "curved_p3":
+        lamB, _, xB, _ = W.cfl_power(TierB(p, n), x0, 400)
+        assert abs(lamB / lam - 1) < 1e-12 and np.abs(xB - x).max() < 1e-10
+    else:
+        lamB, _, xB, _ = W.cfl_power(TierB(p, n, ctrl=kw["ctrl"], inv_eps=kw["inv_eps_qp"]), x0, iters)
+        assert abs(lamB / lam - 1) < 1e-11 and np.abs(xB - x).max() < 1e-8
+
+
+def test_cfl_p2_closed_form():
+    """Derived fact (DESIGN.md readings): on the identity cube with eps = mu = 1 and p = 2,
+    lambda_max = (72/5) (n_x^2 + n_y^2 + n_z^2) exactly; checked by dense brute force."""
+    for n in (2, 4, (4, 5, 3)):
+        nn = np.array(forms._n3(n), dtype=float)
+        assert abs(_dense_lambda_max(TierA(2, n)) / (14.4 * (nn ** 2).sum()) - 1) < 1e-12
