@@ -171,6 +171,20 @@ sgm_status sgm_gauss(sgm_plan plan, const double* d, const double* b, double* ou
 sgm_status sgm_check_source(sgm_plan plan, const double* j_hat, void* workspace,
                             size_t ws_bytes, void* stream);
 
+/* Leapfrog stability limit (SURVEY 8(d) "Fixing dt reproducibly", K8; reading Z15 in DESIGN.md):
+   n_iter power iterations on A = D~1 K~1^{-1} M2 D1 K1^{-1} M~2 (acting on dual 2-forms), which is
+   self-adjoint and PSD in the M~2 inner product because K1^T D~1 = D1^T K~1.  With x
+   normalised to unit 2-norm, each iteration computes e = K1^{-1} M~2 x, b = D1 e,
+   h = K~1^{-1} M2 b (eqs. discrete2_hodge_*), the Rayleigh quotient
+   lam = (b^T K~1 h) / (x^T K1 e), and x <- D~1 h / |D~1 h|_2.  The quotients increase
+   monotonically towards lambda_max from below.
+     x      in: start vector (device, len N_d; drawn by the caller), out: last normalised iterate
+     e,b,h  device scratch of lengths N_e, N_b, N_h (the shapes of sgm_step's state); overwritten
+     out_dev  device [2]: lam of the last iteration and dt_max = 2/sqrt(lam)
+   All pointers distinct; n_iter >= 1.  Async (no host synchronisation). */
+sgm_status sgm_cfl(sgm_plan plan, double* x, double* e, double* b, double* h, int n_iter,
+                   double* out_dev, void* workspace, size_t ws_bytes, void* stream);
+
 /* Number of kernels one sgm_step step launches for this plan (for launch accounting). */
 sgm_status sgm_plan_kernels_per_step(sgm_plan plan, int* n);
 

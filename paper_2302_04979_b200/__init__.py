@@ -64,6 +64,7 @@ _SIGS = {
     "sgm_curl": [c_void_p, c_int, c_void_p, c_void_p, c_void_p],
     "sgm_energy": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p],
     "sgm_gauss": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p],
+    "sgm_cfl": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_size_t, c_void_p],
     "sgm_check_source": [c_void_p, c_void_p, c_void_p, c_size_t, c_void_p],
     "sgm_plan_kernels_per_step": [c_void_p, ctypes.POINTER(c_int)],
     "sgm_plan_set_profiling": [c_void_p, c_int],
@@ -268,6 +269,12 @@ class Plan:
         w = self.workspace()
         check(sgm_gauss(self.h, _ptr(d), _ptr(b), _ptr(out), _ptr(w), w.numel() * 8, _stream(stream)),
               "sgm_gauss")
+
+    def cfl(self, x, e, b, h, out, n_iter=300, stream=None):
+        """Power-iteration leapfrog limit: out[0] = lambda, out[1] = dt_max (sgm_cfl)."""
+        w = self.workspace()
+        check(sgm_cfl(self.h, _ptr(x), _ptr(e), _ptr(b), _ptr(h), int(n_iter), _ptr(out), _ptr(w),
+                      w.numel() * 8, _stream(stream)), "sgm_cfl")
 
     def check_source(self, j_hat, stream=None):
         w = self.workspace()

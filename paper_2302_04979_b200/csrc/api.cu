@@ -686,6 +686,35 @@ sgm_status sgm_hodge_apply(sgm_plan plan, sgm_mass which, const double* x, doubl
   return cuda_check(P, "sgm_hodge_apply");
 }
 
+// y = K^{-1} M x for one Hodge star (eqs. discrete2_hodge_eps / _mu)
+void hodge_star_impl(const Plan& P, int which, const double* x, double* y, const WS& w, cudaStream_t st) {
+  int kind = (which == SGM_MASS_EPS) ? 0 : 1;
+  int own = (which == SGM_MASS_EPS) ? OP_EPS_OWN : OP_MU_OWN;
+  int oth = (which == SGM_MASS_EPS) ? OP_EPS_OTH : OP_MU_OTH;
+  const MassData& M = P.mass[which];
+  if (M.kind == HODGE_SEPARABLE) {
+    kron_pass3(P, kind, x, y, w.t, own, oth, M.scale, true, true, st);
+  } else {
+    mass_apply(P, which, x, w.r, w.t, st);
+    kron_pass3(P, kind, w.r, y, w.t, own, oth, nullptr, false, true, st);
+  }
+}
+
+void curl_impl(const Plan& P, int kind, const double* x, double* y, cudaStream_t st) {
+  int skind = (kind == SGM_CURL_PRIMAL) ? 0 : 1;  // primal: e -> b ; dual: h -> d
+  int dkind = 1 - skind;
+  double *S[3], *Dd[3];
+  comps_of(P, skind, x, S);
+  comps_of(P, dkind, y, Dd);
+  int se[3][3], de[3][3];
+  for (int c = 0; c < 3; ++c) {
+    comp_shape(P, skind, c, se[c]);
+    comp_shape(P, dkind, c, de[c]);
+  }
+  const double* Sc[3] = {S[0], S[1], S[2]};
+  launch_curl(kind == SGM_CURL_DUAL ? 1 : 0, Sc, se, Dd, de, st);
+}
+
 sgm_status sgm_hodge_star(sgm_plan plan, sgm_mass which, const double* x, double* y, void* workspace,
                           size_t ws_bytes, void* stream) {
   sgm_status s = check_plan(plan, true);
@@ -696,17 +725,7 @@ sgm_status sgm_hodge_star(sgm_plan plan, sgm_mass which, const double* x, double
   WS w;
   if ((s = ws_carve(*P, workspace, ws_bytes, w)) != SGM_OK) return s;
   DeviceGuard g(P->device);
-  cudaStream_t st = static_cast<cudaStream_t>(stream);
-  int kind = (which == SGM_MASS_EPS) ? 0 : 1;
-  int own = (which == SGM_MASS_EPS) ? OP_EPS_OWN : OP_MU_OWN;
-  int oth = (which == SGM_MASS_EPS) ? OP_EPS_OTH : OP_MU_OTH;
-  const MassData& M = P->mass[which];
-  if (M.kind == HODGE_SEPARABLE) {
-    kron_pass3(*P, kind, x, y, w.t, own, oth, M.scale, true, true, st);
-  } else {
-    mass_apply(*P, which, x, w.r, w.t, st);
-    kron_pass3(*P, kind, w.r, y, w.t, own, oth, nullptr, false, true, st);
-  }
+  hodge_star_impl(*P, which, x, y, w, static_cast<cudaStream_t>(stream));
   return cuda_check(P, "sgm_hodge_star");
 }
 
@@ -717,18 +736,7 @@ sgm_status sgm_curl(sgm_plan plan, sgm_curl_kind kind, const double* x, double* 
   if (!x || !y || x == y || !aligned8(x) || !aligned8(y)) return fail(SGM_E_INVALID_ARG, "bad vector pointers");
   if (kind != SGM_CURL_PRIMAL && kind != SGM_CURL_DUAL) return fail(SGM_E_INVALID_ARG, "bad curl kind");
   DeviceGuard g(P->device);
-  int skind = (kind == SGM_CURL_PRIMAL) ? 0 : 1;  // primal: e -> b ; dual: h -> d
-  int dkind = 1 - skind;
-  double *S[3], *Dd[3];
-  comps_of(*P, skind, x, S);
-  comps_of(*P, dkind, y, Dd);
-  int se[3][3], de[3][3];
-  for (int c = 0; c < 3; ++c) {
-    comp_shape(*P, skind, c, se[c]);
-    comp_shape(*P, dkind, c, de[c]);
-  }
-  const double* Sc[3] = {S[0], S[1], S[2]};
-  launch_curl(kind == SGM_CURL_DUAL ? 1 : 0, Sc, se, Dd, de, static_cast<cudaStream_t>(stream));
+  curl_impl(*P, kind, x, y, static_cast<cudaStream_t>(stream));
   return cuda_check(P, "sgm_curl");
 }
 
@@ -801,6 +809,43 @@ sgm_status sgm_check_source(sgm_plan plan, const double* j_hat, void* workspace,
   if (hv[0] > 1e-12 * hv[1])
     return fail(SGM_E_SOURCE_DIVERGENCE, "||D~2 j||_inf = " + std::to_string(hv[0]) + " exceeds 1e-12 ||j||_inf");
   return cuda_check(P, "sgm_check_source");
+}
+
+sgm_status sgm_cfl(sgm_plan plan, double* x, double* e, double* b, double* h, int n_iter, double* out_dev,
+                   void* workspace, size_t ws_bytes, void* stream) {
+  sgm_status s = check_plan(plan, true);
+  if (s != SGM_OK) return s;
+  Plan* P = PL(plan);
+  const double* v[5] = {x, e, b, h, out_dev};
+  for (int i = 0; i < 5; ++i) {
+    if (!v[i] || !aligned8(v[i])) return fail(SGM_E_INVALID_ARG, "NULL or misaligned pointer");
+    for (int j = 0; j < i; ++j)
+      if (v[i] == v[j]) return fail(SGM_E_INVALID_ARG, "x, e, b, h, out_dev must be distinct");
+  }
+  if (n_iter < 1) return fail(SGM_E_INVALID_ARG, "n_iter must be >= 1");
+  WS w;
+  if ((s = ws_carve(*P, workspace, ws_bytes, w)) != SGM_OK) return s;
+  DeviceGuard g(P->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // x <- x0 / |x0|, then per iteration (oracle workloads.cfl_power):
+  //   e = K1^{-1} M~2 x, b = D1 e, h = K~1^{-1} M2 b, lam = (b.K~1 h)/(x.K1 e), x = D~1 h / |D~1 h|
+  // partial slots: 0 = b.K~1 h, 1 = x.K1 e, 2 = |x|^2.
+  launch_dot_partials(x, x, P->N_e, w.partials, 2, st);
+  launch_normalize(x, P->N_e, w.partials, 2, st);
+  for (int k = 0; k < n_iter; ++k) {
+    hodge_star_impl(*P, SGM_MASS_EPS, x, e, w, st);
+    curl_impl(*P, SGM_CURL_PRIMAL, e, b, st);
+    hodge_star_impl(*P, SGM_MASS_MU, b, h, w, st);
+    kron_pass3(*P, 0, e, w.r, w.t, OP_APPLY_M, OP_APPLY_G, nullptr, true, false, st);
+    launch_dot_partials(x, w.r, P->N_e, w.partials, 1, st);
+    kron_pass3(*P, 1, h, w.r, w.t, OP_APPLY_GT, OP_APPLY_MT, nullptr, true, false, st);
+    launch_dot_partials(b, w.r, P->N_h, w.partials, 0, st);
+    curl_impl(*P, SGM_CURL_DUAL, h, x, st);
+    launch_dot_partials(x, x, P->N_e, w.partials, 2, st);
+    launch_normalize(x, P->N_e, w.partials, 2, st);
+  }
+  launch_rayleigh(w.partials, out_dev, st);
+  return cuda_check(P, "sgm_cfl");
 }
 
 sgm_status sgm_plan_set_profiling(sgm_plan plan, int on) {

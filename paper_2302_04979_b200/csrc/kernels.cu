@@ -210,6 +210,33 @@ __global__ void finalize_sum_kernel(const double* partials, int n, double scale,
   if (threadIdx.x == 0) out[0] = scale * s;
 }
 
+// x <- x / sqrt(sum of the partials in `slot`); every block re-reduces the (few) partials in the
+// same order, so all blocks use the identical norm (deterministic).
+__global__ void normalize_kernel(double* __restrict__ x, size_t n, const double* __restrict__ partials, int slot) {
+  __shared__ double sh[kRedThreads];
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < kRedBlocks; i += blockDim.x) acc += partials[size_t(slot) * kRedBlocks + i];
+  const double nrm = sqrt(block_sum(acc, sh));
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    x[i] = x[i] / nrm;
+}
+
+// out[0] = lambda = (sum slot 0) / (sum slot 1), out[1] = 2 / sqrt(lambda)  (CFL Rayleigh quotient)
+__global__ void rayleigh_kernel(const double* __restrict__ partials, double* out) {
+  __shared__ double sh[kRedThreads];
+  double a = 0.0, b = 0.0;
+  for (int i = threadIdx.x; i < kRedBlocks; i += blockDim.x) {
+    a += partials[i];
+    b += partials[kRedBlocks + i];
+  }
+  const double num = block_sum(a, sh);
+  const double den = block_sum(b, sh);
+  if (threadIdx.x == 0) {
+    out[0] = num / den;
+    out[1] = 2.0 / sqrt(num / den);
+  }
+}
+
 template <bool DUAL>
 __global__ void div_max_kernel(const double* s0, const double* s1, const double* s2, int3 e0, int3 e1, int3 e2, int3 f,
                                double* partials, int slot) {
@@ -673,6 +700,14 @@ void launch_div_max(int kind, const double* const src[3], const int sext[3][3], 
 
 void launch_absmax(const double* x, size_t n, double* partials, int slot, cudaStream_t st) {
   absmax_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(x, n, partials, slot);
+}
+
+void launch_normalize(double* x, size_t n, const double* partials, int slot, cudaStream_t st) {
+  normalize_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(x, n, partials, slot);
+}
+
+void launch_rayleigh(const double* partials, double* out, cudaStream_t st) {
+  rayleigh_kernel<<<1, kRedThreads, 0, st>>>(partials, out);
 }
 
 void launch_finalize_max(const double* partials, int nslots_each, int ngroups, double* out, cudaStream_t st) {

@@ -74,6 +74,8 @@ void launch_div_max(int kind, const double* const src[3], const int sext[3][3], 
                     int slot, cudaStream_t st);
 void launch_absmax(const double* x, size_t n, double* partials, int slot, cudaStream_t st);
 void launch_finalize_max(const double* partials, int nslots_each, int ngroups, double* out, cudaStream_t st);
+void launch_normalize(double* x, size_t n, const double* partials, int slot, cudaStream_t st);
+void launch_rayleigh(const double* partials, double* out, cudaStream_t st);
 int partial_blocks();
 
 }  // namespace sgm

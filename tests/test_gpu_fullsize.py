@@ -118,3 +118,33 @@ def test_c3_curved_inclusion_source_full_size():
     ref = tb.run(*st, dt, steps, jhat, jamp)
     for x, r in zip(dv, ref):
         assert rel(host(x), r) < 1e-10
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_cfl_power_full_size(p):
+    """sgm_cfl at 128^3: exact parity with the oracle's power iteration for 2 iterations, then the
+    properties that hold at any size: Rayleigh quotients nondecreasing across restarts, bounded by
+    lambda_max (p = 2 closed form 72/5 * 3 n^2), and dt_max * n near SURVEY A7's value."""
+    n = 128
+    pl = S.Plan(n, p)
+    tb = TierB(p, n)
+    x0 = synth.rng(100).standard_normal(tb.N_e)
+    x = dev(x0)
+    e = torch.empty(pl.N_e, dtype=torch.float64, device="cuda")
+    b = torch.empty(pl.N_h, dtype=torch.float64, device="cuda")
+    h = torch.empty_like(b)
+    out = torch.zeros(2, dtype=torch.float64, device="cuda")
+    pl.cfl(x, e, b, h, out, 2)
+    lam, dt, xr, _ = W.cfl_power(tb, x0, 2)
+    o = host(out)
+    assert abs(o[0] / lam - 1) < 1e-11 and np.abs(host(x) - xr).max() < 1e-9
+    prev = o[0]
+    for _ in range(3):   # 3 x 100 more iterations continuing from the last iterate
+        pl.cfl(x, e, b, h, out, 100)
+        o = host(out)
+        assert o[0] >= prev * (1 - 1e-12)
+        prev = o[0]
+    if p == 2:
+        bound = 14.4 * 3 * n * n
+        assert 0.97 * bound < o[0] <= bound * (1 + 1e-12), (o[0], bound)
+    assert 0.97 * CFL_N[p] < o[1] * n < 1.06 * CFL_N[p], o[1] * n

@@ -10,6 +10,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 import paper_2302_04979_b200 as S  # noqa: E402
+import synth  # noqa: E402
 from oracle import forms  # noqa: E402
 from oracle import workloads as W  # noqa: E402
 from oracle.structured import TierB, curl_primal, curl_dual  # noqa: E402
@@ -305,3 +306,45 @@ def test_gpu_invariants_over_many_steps():
     pl.gauss(d, b, out)
     scale = max(float(torch.max(torch.abs(d))), float(torch.max(torch.abs(b))))
     assert np.all(np.abs(host(out) - g0) <= 1e-11 * scale)
+
+
+def _cfl_gpu(pl, x0, n_iter):
+    x = dev(x0)
+    e = torch.empty(pl.N_e, dtype=torch.float64, device="cuda")
+    b = torch.empty(pl.N_h, dtype=torch.float64, device="cuda")
+    h = torch.empty_like(b)
+    out = torch.zeros(2, dtype=torch.float64, device="cuda")
+    pl.cfl(x, e, b, h, out, n_iter)
+    return host(out), host(x)
+
+
+@pytest.mark.parametrize("case", ["cube_p2", "ragged_p3", "curved_p3", "p4"])
+def test_cfl_power_parity(case):
+    """sgm_cfl against oracle workloads.cfl_power: same start vector rng(100), same iteration count.
+    Power iteration does not amplify rounding, so lambda agrees to 1e-11 and the iterate to 1e-9."""
+    ctrl = None
+    if case == "cube_p2":
+        p, n = 2, 8
+    elif case == "ragged_p3":
+        p, n = 3, (9, 7, 6)
+    elif case == "p4":
+        p, n = 4, 6
+    else:
+        p, n = 3, (6, 5, 7)
+        ctrl, eps = _curved_case(p, n)
+    pl = S.Plan(n, p, geom_ctrl=ctrl)
+    if ctrl is not None:
+        pl.set_material(S.EPS, eps)
+        tb = TierB(p, n, ctrl=ctrl, inv_eps=1.0 / eps, inv_mu=1.0)
+    else:
+        tb = TierB(p, n)
+    x0 = synth.rng(100).standard_normal(tb.N_e)
+    for iters in (1, 60):
+        lam, dt, xr, _ = W.cfl_power(tb, x0, iters)
+        out, x = _cfl_gpu(pl, x0, iters)
+        assert abs(out[0] / lam - 1) < 1e-11 and abs(out[1] / dt - 1) < 1e-11, (iters, out, lam)
+        assert np.abs(x - xr).max() < 1e-9
+    if case == "cube_p2":   # closed form (DESIGN.md): lambda_max = 72/5 * 3 n^2, approached from below
+        bound = 14.4 * 3 * n * n
+        out, _ = _cfl_gpu(pl, x0, 1500)
+        assert bound * (1 - 2e-3) < out[0] <= bound * (1 + 1e-12), (out[0], bound)
