@@ -286,3 +286,49 @@ def test_cfl_p2_closed_form():
     for n in (2, 4, (4, 5, 3)):
         nn = np.array(forms._n3(n), dtype=float)
         assert abs(_dense_lambda_max(TierA(2, n)) / (14.4 * (nn ** 2).sum()) - 1) < 1e-12
+
+
+def test_composed_w1_is_staggered_leapfrog():
+    """compose.run_composed with w = (1,) (velocity Verlet, synchronous b) equals the paper's
+    staggered leapfrog started from b^{1/2} = b^0 - dt/2 D1 e^0 and read back with
+    b^n = b^{n+1/2} + dt/2 D1 e^n."""
+    from oracle import compose
+    p, n = 3, (3, 2, 4)
+    A = TierA(p, n)
+    d, _, b, _ = _rand_state(A.N_e, A.N_h, 21)
+    e = A.solve_K1(A.Meps @ d)
+    h = A.solve_Kt1(A.Mmu @ b)
+    dt, steps = 0.01, 7
+    out = compose.run_composed(A, d, e, b, h, dt, steps, weights=(1.0,))
+    bh = b - 0.5 * dt * (A.D1 @ e)
+    st = A.run(d, e, bh, A.solve_Kt1(A.Mmu @ bh), dt, steps)
+    bn = st[2] + 0.5 * dt * (A.D1 @ st[1])
+    assert rel(out[0], st[0]) < 1e-13 and rel(out[1], st[1]) < 1e-13
+    assert rel(out[2], bn) < 1e-13 and rel(out[3], A.solve_Kt1(A.Mmu @ bn)) < 1e-13
+
+
+@pytest.mark.parametrize("weights,order", [("yoshida", 4), ("verlet", 2)])
+def test_composed_time_order_vs_exact_semidiscrete(weights, order):
+    """Time order of the composition against the exact solution of the semi-discrete system
+    d' = D~1 h, b' = -D1 e (e = K1^{-1} M~2 d, h = K~1^{-1} M2 b; P:L355-372 before the leapfrog),
+    y(T) = expm(T L) y(0) from the dense tier-A operator: halving dt divides the error by 2^order."""
+    import scipy.linalg as sl
+    from oracle import compose
+    w = compose.YOSHIDA4 if weights == "yoshida" else (1.0,)
+    p, n = 2, 2
+    A = TierA(p, n)
+    He = np.linalg.solve(A.K1.toarray(), A.Meps.toarray())
+    Hm = np.linalg.solve(A.Kt1.toarray(), A.Mmu.toarray())
+    Ne, Nh = A.N_e, A.N_h
+    L = np.zeros((Ne + Nh, Ne + Nh))
+    L[:Ne, Ne:] = A.Dt1.toarray() @ Hm
+    L[Ne:, :Ne] = -A.D1.toarray() @ He
+    d, _, b, _ = _rand_state(Ne, Nh, 22)
+    T = 0.2
+    yT = sl.expm(T * L) @ np.concatenate([d, b])
+    errs = []
+    for m in (16, 32, 64):
+        out = compose.run_composed(A, d, He @ d, b, Hm @ b, T / m, m, weights=w)
+        errs.append(np.linalg.norm(np.concatenate([out[0], out[2]]) - yT) / np.linalg.norm(yT))
+    rates = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    assert np.all(np.abs(rates - order) < 0.15), (errs, rates)
