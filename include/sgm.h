@@ -136,6 +136,24 @@ sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h,
                     const double* j_hat, const double* j_amp, double dt, int n_steps,
                     void* workspace, size_t ws_bytes, void* stream);
 
+/* Higher-order time integration by symmetric composition of leapfrog sub-steps (the paper's
+   future work; reading Z25 in DESIGN.md).  Each of the n_steps steps
+   applies the kick-drift-kick sub-steps S(w_0 dt) ... S(w_{n_w-1} dt), where S(tau) is
+     b <- b - (tau/2) D1 e;  h <- K~1^{-1} M2 b;           (eq. discrete2_faraday / _hodge_mu)
+     d <- d + tau (D~1 h - s j^);  e <- K1^{-1} M~2 d;      (eq. discrete2_ampere / _hodge_eps)
+     b <- b - (tau/2) D1 e;  h <- K~1^{-1} M2 b.
+   Adjacent half kicks are merged (n_steps*n_w + 1 kicks and n_steps*n_w drifts in total).
+   Yoshida's 4th-order triple jump: n_w = 3, w = {x1, x0, x1}, x1 = 1/(2 - 2^(1/3)),
+   x0 = -2^(1/3)/(2 - 2^(1/3)); n_w = 1, w = {1} is velocity Verlet.
+   Unlike sgm_step, the state is SYNCHRONOUS: d, e, b, h at t_n on entry and at t_n + n_steps dt
+   on exit.  weights: host [n_w], finite, 1 <= n_w <= SGM_MAX_STAGES.  j_amp: device
+   [n_steps * n_w], s for drift i of step k at j_amp[k*n_w + i] (NULL -> 1).  Other arguments,
+   aliasing rules and errors as sgm_step.  Async; no graph capture. */
+#define SGM_MAX_STAGES 16
+sgm_status sgm_step_composed(sgm_plan plan, double* d, double* e, double* b, double* h,
+                             const double* j_hat, const double* j_amp, const double* weights,
+                             int n_w, double dt, int n_steps, void* workspace, size_t ws_bytes,
+                             void* stream);
 /* End-to-end variant on HOST buffers (pinned recommended): copies d,e,b,h (and j_hat, j_amp
    if given) host->device into plan-owned mirrors, runs sgm_step, copies d,e,b,h back and
    synchronises `stream`.  Synchronous. */

@@ -57,6 +57,8 @@ _SIGS = {
                  c_void_p, c_size_t, c_void_p],
     "sgm_step_host": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int,
                       c_void_p],
+    "sgm_step_composed": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
+                          c_double, c_int, c_void_p, c_size_t, c_void_p],
     "sgm_kron_solve": [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p],
     "sgm_pairing_apply": [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p],
     "sgm_hodge_apply": [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_size_t, c_void_p],
@@ -114,6 +116,11 @@ def _stream(stream):
         return stream if isinstance(stream, int) else stream.cuda_stream
     import torch
     return torch.cuda.current_stream().cuda_stream
+
+
+# Yoshida's 4th-order symmetric composition ("triple jump") of leapfrog sub-steps
+_CBRT2 = 2.0 ** (1.0 / 3.0)
+YOSHIDA4 = (1.0 / (2.0 - _CBRT2), -_CBRT2 / (2.0 - _CBRT2), 1.0 / (2.0 - _CBRT2))
 
 
 class Plan:
@@ -224,6 +231,16 @@ class Plan:
         w = self.workspace() if ws is None else ws
         check(sgm_step(self.h, _ptr(d), _ptr(e), _ptr(b), _ptr(h), _ptr(j_hat), _ptr(j_amp), float(dt),
                        int(n_steps), _ptr(w), w.numel() * 8, _stream(stream)), "sgm_step")
+
+    def step_composed(self, d, e, b, h, dt, weights=None, n_steps=1, j_hat=None, j_amp=None, stream=None,
+                      ws=None):
+        """Composition of kick-drift-kick sub-steps (sgm_step_composed); synchronous state.
+        weights default: Yoshida's 4th-order triple jump (YOSHIDA4)."""
+        w = self.workspace() if ws is None else ws
+        wt = np.ascontiguousarray(YOSHIDA4 if weights is None else weights, dtype=np.float64)
+        check(sgm_step_composed(self.h, _ptr(d), _ptr(e), _ptr(b), _ptr(h), _ptr(j_hat), _ptr(j_amp),
+                                wt.ctypes.data, int(wt.size), float(dt), int(n_steps), _ptr(w), w.numel() * 8,
+                                _stream(stream)), "sgm_step_composed")
 
     def step_host(self, d, e, b, h, dt, n_steps=1, j_hat=None, j_amp=None, stream=None):
         """d, e, b, h: numpy float64 arrays or pinned CPU torch tensors (updated in place)."""

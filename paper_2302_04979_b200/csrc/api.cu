@@ -303,61 +303,57 @@ sgm_status check_plan(sgm_plan plan, bool need_device) {
 
 inline Plan* PL(sgm_plan p) { return reinterpret_cast<Plan*>(p); }
 
-// one leapfrog step on device pointers (schedules of SURVEY 8(a) a1-a6)
-void step_once(Plan& P, double* d, double* e, double* b, double* h, const double* jhat, const double* s_ptr,
-               double dt, const WS& w, cudaStream_t st) {
+// one half step on device pointers (SURVEY 8(a) a1-a3 for half 0, a4-a6 for half 1):
+//   half 0 (eps, kind 0): d <- d + tau (D~1 h - s j); e <- K1^{-1} M~2_{1/eps} d
+//   half 1 (mu,  kind 1): b <- b - tau D1 e;          h <- K~1^{-1} M2_{1/mu} b
+void half_step(Plan& P, int half, double* d, double* e, double* b, double* h, const double* jhat,
+               const double* s_ptr, double tau, const WS& w, cudaStream_t st) {
   double *D[3], *E[3], *B[3], *H[3], *T[3], *Rr[3];
   comps_of(P, 0, d, D);
   comps_of(P, 0, e, E);
   comps_of(P, 1, b, B);
   comps_of(P, 1, h, H);
-  for (int half = 0; half < 2; ++half) {
-    // eps half (kind 0): d <- d + dt (D~1 h - s j); e <- K1^{-1} M~2_{1/eps} d
-    // mu  half (kind 1): b <- b - dt D1 e;           h <- K~1^{-1} M2_{1/mu} b
-    const int kind = half;
-    const int mass = half == 0 ? SGM_MASS_EPS : SGM_MASS_MU;
-    const int pro = half == 0 ? PRO_AMPERE : PRO_FARADAY;
-    const int own = half == 0 ? OP_EPS_OWN : OP_MU_OWN, oth = half == 0 ? OP_EPS_OTH : OP_MU_OTH;
-    const int kx = half == 0 ? SGM_K_EPS_Z : SGM_K_MU_Z;
-    const int ky = half == 0 ? SGM_K_EPS_Y : SGM_K_MU_Y, kz = half == 0 ? SGM_K_EPS_X : SGM_K_MU_X;
-    double** state = half == 0 ? D : B;
-    double** outv = half == 0 ? E : H;
-    PrologueArgs pa = half == 0 ? make_pro(P, 1, h, jhat, s_ptr, dt) : make_pro(P, 0, e, nullptr, nullptr, dt);
-    const MassData& M = P.mass[mass];
-    comps_of(P, kind, w.t, T);
-    if (M.kind == HODGE_SEPARABLE) {
-      // streaming update kernel, then the three mass . solve sweeps (z, y, x)
-      SweepArgs a;
-      std::memset(&a, 0, sizeof(a));
-      a.ncomp = 3;
-      for (int c = 0; c < 3; ++c) {
-        comp_shape(P, kind, c, a.comp[c].ext);
-        a.comp[c].in = state[c];
-      }
-      a.pro = pa;
-      { ProfScope ps(P, SGM_K_UPDATE, st); launch_update(pro, a, st); }
-      // snake order: update forward, z backward, y forward, x backward (each kernel starts on the
-      // tiles its predecessor wrote last)
-      { ProfScope ps(P, kx, st); sweep_pass(P, kind, 2, state, T, own, oth, nullptr, true, true, st, 1); }
-      { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, true, true, st, 0); }
-      { ProfScope ps(P, kz, st); sweep_pass(P, kind, 0, T, outv, own, oth, M.scale, true, true, st, 1); }
-    } else {
-      SweepArgs a;
-      std::memset(&a, 0, sizeof(a));
-      a.ncomp = 3;
-      for (int c = 0; c < 3; ++c) {
-        comp_shape(P, kind, c, a.comp[c].ext);
-        a.comp[c].in = state[c];
-      }
-      a.pro = pa;
-      { ProfScope ps(P, SGM_K_UPDATE, st); launch_update(pro, a, st); }
-      { ProfScope ps(P, SGM_K_HODGE_GENERAL, st); mass_apply(P, mass, state[0], w.r, w.t, st); }
-      comps_of(P, kind, w.r, Rr);
-      { ProfScope ps(P, SGM_K_SOLVE_Z, st); sweep_pass(P, kind, 2, Rr, T, own, oth, nullptr, false, true, st); }
-      { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, false, true, st); }
-      { ProfScope ps(P, kz, st); sweep_pass(P, kind, 0, T, outv, own, oth, nullptr, false, true, st); }
-    }
+  const int kind = half;
+  const int mass = half == 0 ? SGM_MASS_EPS : SGM_MASS_MU;
+  const int pro = half == 0 ? PRO_AMPERE : PRO_FARADAY;
+  const int own = half == 0 ? OP_EPS_OWN : OP_MU_OWN, oth = half == 0 ? OP_EPS_OTH : OP_MU_OTH;
+  const int kx = half == 0 ? SGM_K_EPS_Z : SGM_K_MU_Z;
+  const int ky = half == 0 ? SGM_K_EPS_Y : SGM_K_MU_Y, kz = half == 0 ? SGM_K_EPS_X : SGM_K_MU_X;
+  double** state = half == 0 ? D : B;
+  double** outv = half == 0 ? E : H;
+  PrologueArgs pa = half == 0 ? make_pro(P, 1, h, jhat, s_ptr, tau) : make_pro(P, 0, e, nullptr, nullptr, tau);
+  const MassData& M = P.mass[mass];
+  comps_of(P, kind, w.t, T);
+  SweepArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.ncomp = 3;
+  for (int c = 0; c < 3; ++c) {
+    comp_shape(P, kind, c, a.comp[c].ext);
+    a.comp[c].in = state[c];
   }
+  a.pro = pa;
+  { ProfScope ps(P, SGM_K_UPDATE, st); launch_update(pro, a, st); }
+  if (M.kind == HODGE_SEPARABLE) {
+    // streaming update kernel, then the three mass . solve sweeps (z, y, x); snake order: update
+    // forward, z backward, y forward, x backward (each kernel starts on the tiles its predecessor
+    // wrote last)
+    { ProfScope ps(P, kx, st); sweep_pass(P, kind, 2, state, T, own, oth, nullptr, true, true, st, 1); }
+    { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, true, true, st, 0); }
+    { ProfScope ps(P, kz, st); sweep_pass(P, kind, 0, T, outv, own, oth, M.scale, true, true, st, 1); }
+  } else {
+    { ProfScope ps(P, SGM_K_HODGE_GENERAL, st); mass_apply(P, mass, state[0], w.r, w.t, st); }
+    comps_of(P, kind, w.r, Rr);
+    { ProfScope ps(P, SGM_K_SOLVE_Z, st); sweep_pass(P, kind, 2, Rr, T, own, oth, nullptr, false, true, st); }
+    { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, false, true, st); }
+    { ProfScope ps(P, kz, st); sweep_pass(P, kind, 0, T, outv, own, oth, nullptr, false, true, st); }
+  }
+}
+
+// one leapfrog step (eqs. discrete2_*)
+void step_once(Plan& P, double* d, double* e, double* b, double* h, const double* jhat, const double* s_ptr,
+               double dt, const WS& w, cudaStream_t st) {
+  half_step(P, 0, d, e, b, h, jhat, s_ptr, dt, w, st);
+  half_step(P, 1, d, e, b, h, jhat, s_ptr, dt, w, st);
 }
 
 }  // namespace
@@ -590,6 +586,43 @@ sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h, c
   }
   for (int k = 0; k < n_steps; ++k) step_once(*P, d, e, b, h, j_hat, j_amp ? j_amp + k : nullptr, dt, w, st);
   return cuda_check(P, "sgm_step");
+}
+
+sgm_status sgm_step_composed(sgm_plan plan, double* d, double* e, double* b, double* h, const double* j_hat,
+                             const double* j_amp, const double* weights, int n_w, double dt, int n_steps,
+                             void* workspace, size_t ws_bytes, void* stream) {
+  sgm_status s = check_plan(plan, true);
+  if (s != SGM_OK) return s;
+  Plan* P = PL(plan);
+  if (!d || !e || !b || !h || !aligned8(d) || !aligned8(e) || !aligned8(b) || !aligned8(h))
+    return fail(SGM_E_INVALID_ARG, "state pointers must be non-NULL and 8-byte aligned");
+  if ((j_hat && !aligned8(j_hat)) || (j_amp && !aligned8(j_amp))) return fail(SGM_E_INVALID_ARG, "misaligned source");
+  if (d == e || d == b || d == h || e == b || e == h || b == h) return fail(SGM_E_INVALID_ARG, "state vectors alias");
+  if (!weights || n_w < 1 || n_w > SGM_MAX_STAGES) return fail(SGM_E_INVALID_ARG, "need 1 <= n_w <= SGM_MAX_STAGES weights");
+  for (int i = 0; i < n_w; ++i)
+    if (!std::isfinite(weights[i])) return fail(SGM_E_INVALID_ARG, "weights must be finite");
+  if (!std::isfinite(dt)) return fail(SGM_E_INVALID_ARG, "dt must be finite");
+  if (n_steps < 0) return fail(SGM_E_INVALID_ARG, "n_steps < 0");
+  WS w;
+  if ((s = ws_carve(*P, workspace, ws_bytes, w)) != SGM_OK) return s;
+  DeviceGuard g(P->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n_steps == 0) return SGM_OK;
+  // kick-drift-kick sub-steps S(w_i dt) in sequence; adjacent half kicks of b are merged
+  // (b -= a D1 e; b -= c D1 e with the same e is b -= (a + c) D1 e)
+  const double* W = weights;
+  half_step(*P, 1, d, e, b, h, nullptr, nullptr, 0.5 * W[0] * dt, w, st);
+  for (int k = 0; k < n_steps; ++k)
+    for (int i = 0; i < n_w; ++i) {
+      const double* s_ptr = j_amp ? j_amp + size_t(k) * n_w + i : nullptr;
+      half_step(*P, 0, d, e, b, h, j_hat, s_ptr, W[i] * dt, w, st);
+      double kick;
+      if (i + 1 < n_w) kick = 0.5 * (W[i] + W[i + 1]);
+      else if (k + 1 < n_steps) kick = 0.5 * (W[i] + W[0]);
+      else kick = 0.5 * W[i];
+      half_step(*P, 1, d, e, b, h, nullptr, nullptr, kick * dt, w, st);
+    }
+  return cuda_check(P, "sgm_step_composed");
 }
 
 sgm_status sgm_step_host(sgm_plan plan, double* d, double* e, double* b, double* h, const double* j_hat,
