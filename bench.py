@@ -182,7 +182,9 @@ def launch_bytes(pl, S, N_e, N_h, has_src):
         src = 8 * N if (half == 0 and has_src) else 0
         out.append(("update", 8 * (Ns + 2 * N) + src))
         if pl.separable(S.MASS_EPS if half == 0 else S.MASS_MU):
-            out += [(pre + "_z", 16 * N), (pre + "_y", 16 * N), (pre + "_x", 16 * N)]
+            # reduced schedule: an eps pass sweeps 2 of the 3 (equal-size) components, a mu pass 1
+            f = (2 if half == 0 else 1) / 3 if pl.reduced_schedule() else 1.0
+            out += [(pre + "_z", 16 * N * f), (pre + "_y", 16 * N * f), (pre + "_x", 16 * N * f)]
         else:
             wq = pl.qp_count() * (6 if pl.geom else 1) * 8
             out += [("hodge_general", 24 * N + wq), ("solve_z", 16 * N), (pre + "_y", 16 * N), (pre + "_x", 16 * N)]

@@ -203,6 +203,11 @@ sgm_status sgm_check_source(sgm_plan plan, const double* j_hat, void* workspace,
 sgm_status sgm_cfl(sgm_plan plan, double* x, double* e, double* b, double* h, int n_iter,
                    double* out_dev, void* workspace, size_t ws_bytes, void* stream);
 
+/* *on = 1 if separable Hodge stars use the reduced schedule (the diagonal 1D
+   factors Hat M^{-1} Gamma_B^{p-1} = diag(1/s) and Hat M^{-T} Gamma_C^{p-1} = diag(s), verified at
+   plan creation, replace their line sweeps by per-line scalings), 0 if every axis is swept. */
+sgm_status sgm_plan_reduced_schedule(sgm_plan plan, int* on);
+
 /* Number of kernels one sgm_step step launches for this plan (for launch accounting). */
 sgm_status sgm_plan_kernels_per_step(sgm_plan plan, int* n);
 

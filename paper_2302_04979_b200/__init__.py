@@ -69,6 +69,7 @@ _SIGS = {
     "sgm_cfl": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_void_p, c_size_t, c_void_p],
     "sgm_check_source": [c_void_p, c_void_p, c_void_p, c_size_t, c_void_p],
     "sgm_plan_kernels_per_step": [c_void_p, ctypes.POINTER(c_int)],
+    "sgm_plan_reduced_schedule": [c_void_p, ctypes.POINTER(c_int)],
     "sgm_plan_set_profiling": [c_void_p, c_int],
     "sgm_plan_profile": [c_void_p, c_void_p, c_void_p],
 }
@@ -203,6 +204,11 @@ class Plan:
         n = c_size_t()
         check(sgm_workspace_bytes(self.h, ctypes.byref(n)))
         return n.value
+
+    def reduced_schedule(self):
+        v = c_int(0)
+        check(sgm_plan_reduced_schedule(self.h, ctypes.byref(v)), "sgm_plan_reduced_schedule")
+        return bool(v.value)
 
     def kernels_per_step(self):
         n = c_int()

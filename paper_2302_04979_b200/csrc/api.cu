@@ -160,6 +160,88 @@ void sweep_pass(const Plan& P, int kind, int axis, double* const in[3], double* 
   launch_sweep(P.p, P.seg[axis], a, st);
 }
 
+// diagonal 1D factor of axis `axis`: kind 0 = 1/s (eps own axis), 1 = s (mu other axes)
+const double* diag_factor(const Plan& P, int axis, int kind) {
+  return P.tables_dev + P.diag_off + size_t(axis * 2 + kind) * P.Lmax;
+}
+
+// One axis pass over a subset of components (the reduced separable schedule).
+struct PassComp {
+  int c;              // component
+  const double* in;   // component arrays
+  double* out;
+  int op;             // line-operator table
+  int dg[3];          // per axis: -1 = no diagonal, else the diag_factor kind applied along it
+  double scale;
+};
+
+void sweep_pass_list(const Plan& P, int kind, int axis, const PassComp* pc, int n, cudaStream_t st, int reverse) {
+  SweepArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.ncomp = n;
+  a.axis = axis;
+  a.band = 1;
+  a.solve = 1;
+  a.tabs[0] = table(P, axis, pc[0].op);
+  a.tabs[1] = nullptr;
+  for (int i = 1; i < n; ++i)
+    if (pc[i].op != pc[0].op) a.tabs[1] = table(P, axis, pc[i].op);
+  a.tab_rows = P.rpad[axis];
+  a.reverse = reverse;
+  // transverse coordinate slots: z-lines (x, y), y-lines (x, z), x-lines (y, z)
+  const int t0 = (axis == 0) ? 1 : 0, t1 = (axis == 2) ? 1 : 2;
+  for (int i = 0; i < n; ++i) {
+    const PassComp& q = pc[i];
+    a.band_hw = std::max(a.band_hw, P.band_hw[axis][q.op]);
+    a.spike_kh = std::max(a.spike_kh, P.spike_kh[axis][q.op]);
+    a.spike_kf = std::max(a.spike_kf, P.spike_kf[axis][q.op]);
+    SweepComp& C = a.comp[i];
+    comp_shape(P, kind, q.c, C.ext);
+    C.in = const_cast<double*>(q.in);
+    C.out = q.out;
+    C.tab = table(P, axis, q.op);
+    C.tslot = (a.tabs[1] && q.op != pc[0].op) ? 1 : 0;
+    C.scale = q.scale;
+    C.dline[0] = q.dg[t0] >= 0 ? diag_factor(P, t0, q.dg[t0]) : nullptr;
+    C.dline[1] = q.dg[t1] >= 0 ? diag_factor(P, t1, q.dg[t1]) : nullptr;
+  }
+  launch_sweep(P.p, P.seg[axis], a, st);
+}
+
+// Reduced separable Hodge star y = K^{-1} M x using the diagonal 1D factors (host_setup.cpp):
+//   eps (kind 0): component c is swept (Gamma_C^{p-2}, LU Hat G) along the two axes != c and
+//                 scaled by 1/s along axis c: z pass {0,1}, y pass {0 -> y, 2}, x pass {1,2 -> y};
+//   mu  (kind 1): component c is swept (Gamma_B^{p}, LU Hat G^T) along axis c only and scaled by
+//                 s along the other two: z pass {2}, y pass {1}, x pass {0}.
+// Returns the number of launches (3).  The sweep classes are recorded when profiling.
+void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* t, cudaStream_t st) {
+  const int kind = (which == SGM_MASS_EPS) ? 0 : 1;
+  const MassData& M = P.mass[which];
+  double *X[3], *Y[3], *T[3];
+  comps_of(P, kind, x, X);
+  comps_of(P, kind, y, Y);
+  comps_of(P, kind, t, T);
+  const int kz = kind == 0 ? SGM_K_EPS_Z : SGM_K_MU_Z, ky = kind == 0 ? SGM_K_EPS_Y : SGM_K_MU_Y,
+            kx = kind == 0 ? SGM_K_EPS_X : SGM_K_MU_X;
+  if (kind == 0) {
+    const int op = OP_EPS_OTH;
+    PassComp z[2] = {{0, X[0], T[0], op, {-1, -1, -1}, 1.0}, {1, X[1], T[1], op, {-1, -1, -1}, 1.0}};
+    PassComp yy[2] = {{0, T[0], Y[0], op, {0, -1, -1}, M.scale[0]}, {2, X[2], T[2], op, {-1, -1, -1}, 1.0}};
+    PassComp xx[2] = {{1, T[1], Y[1], op, {-1, 0, -1}, M.scale[1]}, {2, T[2], Y[2], op, {-1, -1, 0}, M.scale[2]}};
+    { ProfScope ps(P, kz, st); sweep_pass_list(P, 0, 2, z, 2, st, 1); }
+    { ProfScope ps(P, ky, st); sweep_pass_list(P, 0, 1, yy, 2, st, 0); }
+    { ProfScope ps(P, kx, st); sweep_pass_list(P, 0, 0, xx, 2, st, 1); }
+  } else {
+    const int op = OP_MU_OWN;
+    PassComp z[1] = {{2, X[2], Y[2], op, {1, 1, -1}, M.scale[2]}};
+    PassComp yy[1] = {{1, X[1], Y[1], op, {1, -1, 1}, M.scale[1]}};
+    PassComp xx[1] = {{0, X[0], Y[0], op, {-1, 1, 1}, M.scale[0]}};
+    { ProfScope ps(P, kz, st); sweep_pass_list(P, 1, 2, z, 1, st, 1); }
+    { ProfScope ps(P, ky, st); sweep_pass_list(P, 1, 1, yy, 1, st, 0); }
+    { ProfScope ps(P, kx, st); sweep_pass_list(P, 1, 0, xx, 1, st, 1); }
+  }
+}
+
 // y = (A_z (x) A_y (x) A_x) x per component with 3 sweeps x -> t -> t -> y (x == y allowed).
 // Axis order z, y, x: the Kronecker factors commute; the strided axes go first so
 // a fused Ampere/Faraday update (first pass) reads its curl stencil coalesced.
@@ -333,7 +415,9 @@ void half_step(Plan& P, int half, double* d, double* e, double* b, double* h, co
   }
   a.pro = pa;
   { ProfScope ps(P, SGM_K_UPDATE, st); launch_update(pro, a, st); }
-  if (M.kind == HODGE_SEPARABLE) {
+  if (M.kind == HODGE_SEPARABLE && P.diag_ok) {
+    hodge_star_reduced(P, mass, state[0], outv[0], w.t, st);
+  } else if (M.kind == HODGE_SEPARABLE) {
     // streaming update kernel, then the three mass . solve sweeps (z, y, x); snake order: update
     // forward, z backward, y forward, x backward (each kernel starts on the tiles its predecessor
     // wrote last)
@@ -505,6 +589,12 @@ sgm_status sgm_plan_hodge_separable(sgm_plan plan, sgm_mass mass, int* separable
   if (!plan || !separable || (mass != SGM_MASS_EPS && mass != SGM_MASS_MU))
     return fail(SGM_E_INVALID_ARG, "bad argument");
   *separable = PL(plan)->mass[mass].kind == HODGE_SEPARABLE ? 1 : 0;
+  return SGM_OK;
+}
+
+sgm_status sgm_plan_reduced_schedule(sgm_plan plan, int* on) {
+  if (!plan || !on) return fail(SGM_E_INVALID_ARG, "NULL argument");
+  *on = PL(plan)->diag_ok ? 1 : 0;
   return SGM_OK;
 }
 
@@ -725,7 +815,9 @@ void hodge_star_impl(const Plan& P, int which, const double* x, double* y, const
   int own = (which == SGM_MASS_EPS) ? OP_EPS_OWN : OP_MU_OWN;
   int oth = (which == SGM_MASS_EPS) ? OP_EPS_OTH : OP_MU_OTH;
   const MassData& M = P.mass[which];
-  if (M.kind == HODGE_SEPARABLE) {
+  if (M.kind == HODGE_SEPARABLE && P.diag_ok) {
+    hodge_star_reduced(const_cast<Plan&>(P), which, x, y, w.t, st);
+  } else if (M.kind == HODGE_SEPARABLE) {
     kron_pass3(P, kind, x, y, w.t, own, oth, M.scale, true, true, st);
   } else {
     mass_apply(P, which, x, w.r, w.t, st);

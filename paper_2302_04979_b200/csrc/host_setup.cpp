@@ -418,6 +418,7 @@ int seg_for_line(int L) {
 }
 
 sgm_status build_tables(Plan& P, std::string& err) {
+  P.diag_ok = getenv("SGM_NODIAG") == nullptr || atoi(getenv("SGM_NODIAG")) == 0;
   const int p = P.p, RS = RowLayoutRT(p).RS;
   int Rmax = 0;
   for (int a = 0; a < 3; ++a) {
@@ -426,7 +427,8 @@ sgm_status build_tables(Plan& P, std::string& err) {
     Rmax = std::max(Rmax, P.rpad[a]);
   }
   P.Lmax = Rmax;  // rows per table slot
-  P.tables_host.assign(size_t(3) * OP_COUNT * Rmax * RS, 0.0);
+  P.diag_off = size_t(3) * OP_COUNT * Rmax * RS;
+  P.tables_host.assign(P.diag_off + size_t(3) * 2 * Rmax, 0.0);
   const char* noskip = getenv("SGM_SPIKE_FULL");
   for (int a = 0; a < 3; ++a) {
     const Axis& X = P.ax[a];
@@ -442,6 +444,37 @@ sgm_status build_tables(Plan& P, std::string& err) {
     if ((st = fill_table(T(OP_APPLY_G), p, X.a, R, SEG, &X.G, nullptr, err)) != SGM_OK) return st;
     if ((st = fill_table(T(OP_APPLY_GT), p, X.a, R, SEG, &GT, nullptr, err)) != SGM_OK) return st;
     if ((st = fill_table(T(OP_APPLY_MT), p, X.b, R, SEG, &MT, nullptr, err)) != SGM_OK) return st;
+    // Diagonal 1D factors ("reduced separable schedule"): with the CS normalisation
+    // D'_k = s_k B'_k, Hat M = Gamma_B^{p-1} diag(s) and Gamma_C^{p-1} =
+    // diag(s) Gamma_B^{p-1} diag(s), so the own-axis factor of the eps Hodge star,
+    // Hat M^{-1} Gamma_B^{p-1} = diag(1/s), and the other-axis factor of the mu Hodge star,
+    // Hat M^{-T} Gamma_C^{p-1} = diag(s), are diagonal.  Checked here; the schedule falls back to
+    // full sweeps on every axis if an identity fails (or with SGM_NODIAG=1).
+    {
+      const int L = X.b;
+      double* dg_eps = P.tables_host.data() + P.diag_off + size_t(a * 2 + 0) * Rmax;
+      double* dg_mu = P.tables_host.data() + P.diag_off + size_t(a * 2 + 1) * Rmax;
+      double mM = 0.0, mC = 0.0, eM = 0.0, eC = 0.0;
+      std::vector<double> sk(L);
+      for (int k = 0; k < L; ++k) sk[k] = X.M[size_t(k) * L + k] / X.GB1[size_t(k) * L + k];
+      for (int i = 0; i < L; ++i)
+        for (int j = 0; j < L; ++j) {
+          const double m = X.M[size_t(i) * L + j], c = X.GC1[size_t(i) * L + j], g = X.GB1[size_t(i) * L + j];
+          mM = std::max(mM, std::fabs(m));
+          mC = std::max(mC, std::fabs(c));
+          eM = std::max(eM, std::fabs(m - g * sk[j]));
+          eC = std::max(eC, std::fabs(c - sk[i] * g * sk[j]));
+        }
+      const bool ok = std::isfinite(eM) && std::isfinite(eC) && eM <= 1e-13 * mM && eC <= 1e-13 * mC;
+      if (!ok) P.diag_ok = false;
+      for (int k = 0; k < L; ++k) {
+        dg_eps[k] = 1.0 / sk[k];
+        dg_mu[k] = sk[k];
+      }
+      if (getenv("SGM_DEBUG_PLAN"))
+        fprintf(stderr, "sgm plan: axis %d diagonal factors: |M - G diag(s)| %.3g, |Gc - diag(s) G diag(s)| %.3g\n", a,
+                eM / mM, eC / mC);
+    }
     const int Ls[OP_COUNT] = {X.b, X.a, X.a, X.b, X.b, X.a, X.a, X.b};
     for (int op = 0; op < OP_COUNT; ++op) {
       const int S = (Ls[op] + SEG - 1) / SEG;

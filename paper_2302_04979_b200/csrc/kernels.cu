@@ -449,6 +449,8 @@ bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
     g.rowlen = X;
     g.gs = (a.axis == 0) ? 1 : (a.axis == 1 ? X : X * Y);
     g.os = (a.axis == 1) ? X * Y : X;  // transverse index l / X: z (y pass) or y (z pass)
+    g.TD = (a.axis == 0) ? Y : X;      // transverse coordinates of line l: (l % TD, l / TD)
+    g.tmagic = 0xffffffffu / unsigned(g.TD);
     cfg.tiles[c] = (g.nlines + TW - 1) / TW;
     cfg.nitems += cfg.tiles[c];
     Lmax = g.L > Lmax ? g.L : Lmax;

@@ -16,6 +16,10 @@ struct SweepComp {
   int tslot;          // which of SweepArgs::tabs this component uses (staged in shared memory)
   int ext[3];         // component extents (x, y, z)
   double scale;       // multiplies the stored result
+  // optional per-line diagonal factors: the stored line is also multiplied by dline[0][t0] and
+  // dline[1][t1], (t0, t1) its transverse coordinates: (x, y) for z-lines, (x, z) for y-lines,
+  // (y, z) for x-lines (the diagonal 1D factors of the reduced separable schedule, api.cu)
+  const double* dline[2];
 };
 
 // Element-wise state update of a half step (launch_update):

@@ -77,8 +77,11 @@ struct Plan {
   size_t n_qp = 0;
   MassData mass[2];                   // [SGM_MASS_EPS], [SGM_MASS_MU]
   // device
-  double* tables_dev = nullptr;       // [3][OP_COUNT][Lmax][RS]  (seg_sweep.cuh row layout)
+  double* tables_dev = nullptr;       // [3][OP_COUNT][Lmax][RS] (seg_sweep.cuh row layout), then diag factors
   int Lmax = 0;                       // rows per table slot (max padded line length)
+  size_t diag_off = 0;                // offset (doubles) of the diagonal factors [3][2][Lmax]:
+                                      // [axis][0] = 1/s (eps own axis), [axis][1] = s (mu other axes)
+  bool diag_ok = true;                // reduced separable schedule usable (host_setup.cpp)
   int seg[3] = {0, 0, 0};             // register segment length per axis
   int rpad[3] = {0, 0, 0};            // padded line length per axis (multiple of seg)
   int band_hw[3][OP_COUNT] = {};      // actual half-bandwidth of each table's band part

@@ -53,6 +53,8 @@ struct CompGeom {
   int gs;      // element stride along the line
   int os;      // strided: stride of the transverse index l / X
   int rowlen;  // x axis: row length (= L)
+  int TD;      // transverse divisor: line l -> (t0, t1) = (l % TD, l / TD)
+  unsigned tmagic;  // floor((2^32 - 1) / TD)
 };
 
 struct Cfg {
@@ -420,8 +422,22 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
         }
       }
     }
-    // ---- phase E: scaled store
+    // ---- phase E: scaled store (constant component scale times optional per-line diagonals)
     const double sc = C.scale;
+    const bool unit = (sc == 1.0) && !C.dline[0] && !C.dline[1];
+    double scq[LPT];
+#pragma unroll
+    for (int q = 0; q < LPT; ++q) {
+      scq[q] = sc;
+      if (C.dline[0] || C.dline[1]) {
+        const unsigned l = unsigned(min(l0 + lane + 32 * q, g.nlines - 1));
+        unsigned t1 = __umulhi(l, g.tmagic);
+        unsigned t0 = l - t1 * unsigned(g.TD);
+        if (t0 >= unsigned(g.TD)) { ++t1; t0 -= unsigned(g.TD); }
+        if (C.dline[0]) scq[q] *= __ldg(C.dline[0] + t0);
+        if (C.dline[1]) scq[q] *= __ldg(C.dline[1] + t1);
+      }
+    }
     if (!XAX) {
       if (live && !(cfg.dbg & 8)) {  // dbg bit 3: no stores (timing only)
 #pragma unroll
@@ -430,16 +446,16 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
           if (l < g.nlines) {
             double* dst = C.out + line_base(g, 0, l) + long(r0) * g.gs;
             const long gs = g.gs;
-            if (r0 + SEG <= L && sc == 1.0) {
+            if (r0 + SEG <= L && unit) {
 #pragma unroll
               for (int k = 0; k < SEG; ++k, dst += gs) *dst = v[k][q];
             } else if (r0 + SEG <= L) {
 #pragma unroll
-              for (int k = 0; k < SEG; ++k, dst += gs) *dst = sc * v[k][q];
+              for (int k = 0; k < SEG; ++k, dst += gs) *dst = scq[q] * v[k][q];
             } else {
 #pragma unroll
               for (int k = 0; k < SEG; ++k, dst += gs)
-                if (r0 + k < L) *dst = sc * v[k][q];
+                if (r0 + k < L) *dst = scq[q] * v[k][q];
             }
           }
         }
@@ -452,7 +468,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
           double* cw = const_cast<double*>(cp[q]);
 #pragma unroll
           for (int k = 0; k < SEG; ++k)
-            if (r0 + SEG <= L || r0 + k < L) cw[k] = sc * v[k][q];
+            if (r0 + SEG <= L || r0 + k < L) cw[k] = scq[q] * v[k][q];
         }
       }
       if (bulk) {
