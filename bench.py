@@ -183,8 +183,15 @@ def launch_bytes(pl, S, N_e, N_h, has_src):
         out.append(("update", 8 * (Ns + 2 * N) + src))
         if pl.separable(S.MASS_EPS if half == 0 else S.MASS_MU):
             # reduced schedule: an eps pass sweeps 2 of the 3 (equal-size) components, a mu pass 1
-            f = (2 if half == 0 else 1) / 3 if pl.reduced_schedule() else 1.0
-            out += [(pre + "_z", 16 * N * f), (pre + "_y", 16 * N * f), (pre + "_x", 16 * N * f)]
+            if not pl.reduced_schedule():
+                out += [(pre + "_z", 16 * N), (pre + "_y", 16 * N), (pre + "_x", 16 * N)]
+            elif half == 0:
+                out += [(pre + "_z", 16 * N * 2 / 3), (pre + "_y", 16 * N * 2 / 3), (pre + "_x", 16 * N * 2 / 3)]
+            elif pl.kernels_per_step() - (4 if pl.separable(S.MASS_EPS) else 5) == 3:
+                # mu: z-lines of component 2 and y-lines of component 1 in one launch, then x
+                out += [(pre + "_z", 16 * N * 2 / 3), (pre + "_x", 16 * N / 3)]
+            else:
+                out += [(pre + "_z", 16 * N / 3), (pre + "_y", 16 * N / 3), (pre + "_x", 16 * N / 3)]
         else:
             wq = pl.qp_count() * (6 if pl.geom else 1) * 8
             out += [("hodge_general", 24 * N + wq), ("solve_z", 16 * N), (pre + "_y", 16 * N), (pre + "_x", 16 * N)]

@@ -167,6 +167,7 @@ const double* diag_factor(const Plan& P, int axis, int kind) {
 
 // One axis pass over a subset of components (the reduced separable schedule).
 struct PassComp {
+  int axis;           // sweep axis of this component (a strided pass may mix y and z)
   int c;              // component
   const double* in;   // component arrays
   double* out;
@@ -175,23 +176,28 @@ struct PassComp {
   double scale;
 };
 
-void sweep_pass_list(const Plan& P, int kind, int axis, const PassComp* pc, int n, cudaStream_t st, int reverse) {
+// Components of one launch share the line mode (x, or strided y/z) and the padded table rows and
+// segment length of their axes (checked by the caller); at most two distinct tables.
+void sweep_pass_list(const Plan& P, int kind, const PassComp* pc, int n, cudaStream_t st, int reverse) {
   SweepArgs a;
   std::memset(&a, 0, sizeof(a));
   a.ncomp = n;
-  a.axis = axis;
+  a.axis = pc[0].axis;
   a.band = 1;
   a.solve = 1;
-  a.tabs[0] = table(P, axis, pc[0].op);
+  a.tabs[0] = table(P, pc[0].axis, pc[0].op);
   a.tabs[1] = nullptr;
-  for (int i = 1; i < n; ++i)
-    if (pc[i].op != pc[0].op) a.tabs[1] = table(P, axis, pc[i].op);
-  a.tab_rows = P.rpad[axis];
+  for (int i = 1; i < n; ++i) {
+    const double* t = table(P, pc[i].axis, pc[i].op);
+    if (t != a.tabs[0]) a.tabs[1] = t;
+  }
+  a.tab_rows = P.rpad[pc[0].axis];
   a.reverse = reverse;
-  // transverse coordinate slots: z-lines (x, y), y-lines (x, z), x-lines (y, z)
-  const int t0 = (axis == 0) ? 1 : 0, t1 = (axis == 2) ? 1 : 2;
   for (int i = 0; i < n; ++i) {
     const PassComp& q = pc[i];
+    const int axis = q.axis;
+    // transverse coordinate slots: z-lines (x, y), y-lines (x, z), x-lines (y, z)
+    const int t0 = (axis == 0) ? 1 : 0, t1 = (axis == 2) ? 1 : 2;
     a.band_hw = std::max(a.band_hw, P.band_hw[axis][q.op]);
     a.spike_kh = std::max(a.spike_kh, P.spike_kh[axis][q.op]);
     a.spike_kf = std::max(a.spike_kf, P.spike_kf[axis][q.op]);
@@ -200,20 +206,25 @@ void sweep_pass_list(const Plan& P, int kind, int axis, const PassComp* pc, int 
     C.in = const_cast<double*>(q.in);
     C.out = q.out;
     C.tab = table(P, axis, q.op);
-    C.tslot = (a.tabs[1] && q.op != pc[0].op) ? 1 : 0;
+    C.tslot = (a.tabs[1] && C.tab == a.tabs[1]) ? 1 : 0;
+    C.axis = axis;
     C.scale = q.scale;
     C.dline[0] = q.dg[t0] >= 0 ? diag_factor(P, t0, q.dg[t0]) : nullptr;
     C.dline[1] = q.dg[t1] >= 0 ? diag_factor(P, t1, q.dg[t1]) : nullptr;
   }
-  launch_sweep(P.p, P.seg[axis], a, st);
+  launch_sweep(P.p, P.seg[pc[0].axis], a, st);
+}
+
+// The mu star's z and y sweeps share one launch when their axes have equal table geometry.
+bool mu_merged(const Plan& P) {
+  return P.seg[1] == P.seg[2] && P.rpad[1] == P.rpad[2] && !getenv("SGM_NOMERGE");
 }
 
 // Reduced separable Hodge star y = K^{-1} M x using the diagonal 1D factors (host_setup.cpp):
 //   eps (kind 0): component c is swept (Gamma_C^{p-2}, LU Hat G) along the two axes != c and
 //                 scaled by 1/s along axis c: z pass {0,1}, y pass {0 -> y, 2}, x pass {1,2 -> y};
 //   mu  (kind 1): component c is swept (Gamma_B^{p}, LU Hat G^T) along axis c only and scaled by
-//                 s along the other two: z pass {2}, y pass {1}, x pass {0}.
-// Returns the number of launches (3).  The sweep classes are recorded when profiling.
+//                 s along the other two: strided pass {2 along z, 1 along y} (or two passes), x pass {0}.
 void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* t, cudaStream_t st) {
   const int kind = (which == SGM_MASS_EPS) ? 0 : 1;
   const MassData& M = P.mass[which];
@@ -225,20 +236,26 @@ void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* 
             kx = kind == 0 ? SGM_K_EPS_X : SGM_K_MU_X;
   if (kind == 0) {
     const int op = OP_EPS_OTH;
-    PassComp z[2] = {{0, X[0], T[0], op, {-1, -1, -1}, 1.0}, {1, X[1], T[1], op, {-1, -1, -1}, 1.0}};
-    PassComp yy[2] = {{0, T[0], Y[0], op, {0, -1, -1}, M.scale[0]}, {2, X[2], T[2], op, {-1, -1, -1}, 1.0}};
-    PassComp xx[2] = {{1, T[1], Y[1], op, {-1, 0, -1}, M.scale[1]}, {2, T[2], Y[2], op, {-1, -1, 0}, M.scale[2]}};
-    { ProfScope ps(P, kz, st); sweep_pass_list(P, 0, 2, z, 2, st, 1); }
-    { ProfScope ps(P, ky, st); sweep_pass_list(P, 0, 1, yy, 2, st, 0); }
-    { ProfScope ps(P, kx, st); sweep_pass_list(P, 0, 0, xx, 2, st, 1); }
+    PassComp z[2] = {{2, 0, X[0], T[0], op, {-1, -1, -1}, 1.0}, {2, 1, X[1], T[1], op, {-1, -1, -1}, 1.0}};
+    PassComp yy[2] = {{1, 0, T[0], Y[0], op, {0, -1, -1}, M.scale[0]}, {1, 2, X[2], T[2], op, {-1, -1, -1}, 1.0}};
+    PassComp xx[2] = {{0, 1, T[1], Y[1], op, {-1, 0, -1}, M.scale[1]}, {0, 2, T[2], Y[2], op, {-1, -1, 0}, M.scale[2]}};
+    { ProfScope ps(P, kz, st); sweep_pass_list(P, 0, z, 2, st, 1); }
+    { ProfScope ps(P, ky, st); sweep_pass_list(P, 0, yy, 2, st, 0); }
+    { ProfScope ps(P, kx, st); sweep_pass_list(P, 0, xx, 2, st, 1); }
   } else {
     const int op = OP_MU_OWN;
-    PassComp z[1] = {{2, X[2], Y[2], op, {1, 1, -1}, M.scale[2]}};
-    PassComp yy[1] = {{1, X[1], Y[1], op, {1, -1, 1}, M.scale[1]}};
-    PassComp xx[1] = {{0, X[0], Y[0], op, {-1, 1, 1}, M.scale[0]}};
-    { ProfScope ps(P, kz, st); sweep_pass_list(P, 1, 2, z, 1, st, 1); }
-    { ProfScope ps(P, ky, st); sweep_pass_list(P, 1, 1, yy, 1, st, 0); }
-    { ProfScope ps(P, kx, st); sweep_pass_list(P, 1, 0, xx, 1, st, 1); }
+    PassComp z[1] = {{2, 2, X[2], Y[2], op, {1, 1, -1}, M.scale[2]}};
+    PassComp yy[1] = {{1, 1, X[1], Y[1], op, {1, -1, 1}, M.scale[1]}};
+    PassComp xx[1] = {{0, 0, X[0], Y[0], op, {-1, 1, 1}, M.scale[0]}};
+    if (mu_merged(P)) {
+      // z-lines of component 2 and y-lines of component 1 in one strided launch
+      PassComp zy[2] = {z[0], yy[0]};
+      { ProfScope ps(P, kz, st); sweep_pass_list(P, 1, zy, 2, st, 1); }
+    } else {
+      { ProfScope ps(P, kz, st); sweep_pass_list(P, 1, z, 1, st, 1); }
+      { ProfScope ps(P, ky, st); sweep_pass_list(P, 1, yy, 1, st, 0); }
+    }
+    { ProfScope ps(P, kx, st); sweep_pass_list(P, 1, xx, 1, st, 1); }
   }
 }
 
@@ -625,8 +642,9 @@ sgm_status sgm_workspace_bytes(sgm_plan plan, size_t* bytes) {
 sgm_status sgm_plan_kernels_per_step(sgm_plan plan, int* n) {
   if (!plan || !n) return fail(SGM_E_INVALID_ARG, "NULL argument");
   int k = 0;
+  const Plan& P = *PL(plan);
   for (int m = 0; m < 2; ++m)
-    k += (PL(plan)->mass[m].kind == HODGE_SEPARABLE) ? 4 : 5;
+    k += (P.mass[m].kind == HODGE_SEPARABLE) ? ((m == SGM_MASS_MU && P.diag_ok && mu_merged(P)) ? 3 : 4) : 5;
   *n = k;
   return SGM_OK;
 }

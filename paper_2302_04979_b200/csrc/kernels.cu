@@ -442,14 +442,16 @@ bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
     const SweepComp& C = a.comp[c];
     sweep::CompGeom& g = cfg.g[c];
     const int X = C.ext[0], Y = C.ext[1], Z = C.ext[2];
-    g.L = C.ext[a.axis];
+    // per-component axis (strided passes may mix y- and z-lines of different components)
+    const int ax = (MODE != 3 && C.axis > 0) ? C.axis : a.axis;
+    g.L = C.ext[ax];
     g.magic = 0xffffffffu / unsigned(X);
     g.nlines = X * Y * Z / g.L;
     g.X = X;
     g.rowlen = X;
-    g.gs = (a.axis == 0) ? 1 : (a.axis == 1 ? X : X * Y);
-    g.os = (a.axis == 1) ? X * Y : X;  // transverse index l / X: z (y pass) or y (z pass)
-    g.TD = (a.axis == 0) ? Y : X;      // transverse coordinates of line l: (l % TD, l / TD)
+    g.gs = (ax == 0) ? 1 : (ax == 1 ? X : X * Y);
+    g.os = (ax == 1) ? X * Y : X;  // transverse index l / X: z (y pass) or y (z pass)
+    g.TD = (ax == 0) ? Y : X;      // transverse coordinates of line l: (l % TD, l / TD)
     g.tmagic = 0xffffffffu / unsigned(g.TD);
     cfg.tiles[c] = (g.nlines + TW - 1) / TW;
     cfg.nitems += cfg.tiles[c];

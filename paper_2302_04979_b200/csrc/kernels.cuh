@@ -20,6 +20,7 @@ struct SweepComp {
   // dline[1][t1], (t0, t1) its transverse coordinates: (x, y) for z-lines, (x, z) for y-lines,
   // (y, z) for x-lines (the diagonal 1D factors of the reduced separable schedule, api.cu)
   const double* dline[2];
+  int axis;           // strided passes: this component's sweep axis (1 or 2); 0 = SweepArgs::axis
 };
 
 // Element-wise state update of a half step (launch_update):

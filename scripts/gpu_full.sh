@@ -15,8 +15,10 @@ ARGS="--steps 3 --warmup 3 --no-cpu --no-e2e"
 python bench.py $ARGS > gpurun_out/plain_$TAG.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$TAG.csv \
     python bench.py $ARGS > gpurun_out/ncu_launch_$TAG.log 2>&1
-# one step = update, z, y, x (eps) + update, z, y, x (mu); skip setup + warm-up launches
+# one step = update, z, y, x (eps) + update, zy, x (mu); skip setup + warm-up launches, capture
+# two steps (scripts/ncu_traffic.py picks one step starting at an Ampere update)
 ncu --set full --clock-control none --import-source on -k "regex:sweep_kernel|update_kernel" \
-    --launch-skip ${SKIP:-30} --launch-count 8 -o gpurun_out/full_$TAG -f python bench.py $ARGS > gpurun_out/ncu_full_$TAG.log 2>&1
+    --launch-skip ${SKIP:-26} --launch-count 14 -o gpurun_out/full_$TAG -f python bench.py $ARGS > gpurun_out/ncu_full_$TAG.log 2>&1
 ncu -i gpurun_out/full_$TAG.ncu-rep --page raw --csv > gpurun_out/full_${TAG}_raw.csv 2>/dev/null
+ncu -i gpurun_out/full_$TAG.ncu-rep --page source --csv > gpurun_out/full_${TAG}_source.csv 2>/dev/null
 ls -la gpurun_out | tail -30

@@ -9,11 +9,19 @@ import os
 import sys
 
 UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-CLASSES = ["update", "eps_z", "eps_y", "eps_x", "update", "mu_z", "mu_y", "mu_x"]
-
 raw, key = sys.argv[1], sys.argv[2]
 rows = list(csv.reader(open(raw)))
 hdr, units, data = rows[0], rows[1], rows[2:]
+
+# one step from the first Ampere update: update, eps passes, update, mu passes.  The eps half has
+# 3 sweep launches; the mu half 3, or 2 when its z and y sweeps share a launch (reduced schedule).
+names = [d[hdr.index("Kernel Name")] for d in data]
+start = next(i for i, nm in enumerate(names) if "update_kernel<1" in nm)
+nxt = next(i for i in range(start + 1, len(names)) if "update_kernel<2" in names[i])
+end = next((i for i in range(nxt + 1, len(names)) if "update_kernel" in names[i]), len(names))
+n_mu = end - nxt - 1
+CLASSES = ["update", "eps_z", "eps_y", "eps_x", "update"] + (["mu_z", "mu_x"] if n_mu == 2 else ["mu_z", "mu_y", "mu_x"])
+data = data[start:end]
 
 
 def col(name, d):

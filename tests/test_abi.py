@@ -122,3 +122,12 @@ def test_plain_c_consumer(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "abi_smoke ok" in r.stdout
+
+
+@pytest.mark.parametrize("p,n", [(2, 5), (3, (9, 7, 6)), (4, 6), (3, 128)])
+def test_reduced_schedule_identities_hold(p, n, monkeypatch):
+    """The plan verifies Hat M = Gamma_B^{p-1} diag(s) and Gamma_C^{p-1} = diag(s) Gamma_B^{p-1} diag(s)
+    on every axis (host_setup.cpp) and enables the reduced separable schedule; SGM_NODIAG=1 disables it."""
+    assert S.Plan(n, p, device=-1).reduced_schedule()
+    monkeypatch.setenv("SGM_NODIAG", "1")
+    assert not S.Plan(n, p, device=-1).reduced_schedule()
