@@ -1,6 +1,8 @@
 # quick iteration: GPU parity tests, then bench variants (env VARIANTS="SGM_SEG=12 SGM_LPT=1;...")
-python -m pytest tests -m gpu -x -q 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
-cat gpurun_out/pytest_gpu.log
+if [ -z "$SKIP_TESTS" ]; then
+  python -m pytest tests -m gpu -x -q 2>&1 | tail -15 > gpurun_out/pytest_gpu.log
+  cat gpurun_out/pytest_gpu.log
+fi
 IFS=';' read -ra VS <<< "${VARIANTS:-SGM_SEG=12}"
 i=0
 for V in "${VS[@]}"; do
