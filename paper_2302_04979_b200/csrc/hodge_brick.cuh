@@ -1,0 +1,478 @@
+// General (non-separable) 2-form Hodge apply y += M x by brick-tiled sum factorisation
+// (sm_100a, fp64).  Same operator as hodge_kernel.cuh (P:L360 M~2_{1/eps}, P:L366 M2_{1/mu}):
+// on element e,  y_c += V_c^T W_{cc'} V_{c'} x_{c'},  V_c the tensor product of the 1D element
+// bases at the Q Gauss points per axis, W = w_q / material * DF^T DF / det DF (FULL) or
+// w_q / material times a per-component constant (SCALAR).
+//
+// A CTA owns a brick of E x E elements in (x, y) and walks a range of element layers in z.  The
+// brick's coefficients of each component form a patch of PX x PY functions (consecutive elements
+// share all but one function per axis: PX = E - 1 + NX); along z a window of NZ coefficient layers
+// slides by one layer per element, and the output window accumulates in shared memory, its lowest
+// layer complete (and flushed with fp64 atomics) after each element.  Per element layer the three
+// interpolation stages (z, y, x), the quadrature-point multiply and the three testing stages
+// (x, y, z) each run over the whole brick with all threads: every 1D contraction is a small
+// register-blocked loop (one thread produces a whole row of outputs from one row of inputs), the
+// basis values are shared-memory broadcasts.  Only the brick's border functions are shared with
+// neighbouring bricks, so far fewer atomics than element-wise accumulation.
+#pragma once
+
+#include "kernels.cuh"
+#include "pipe_sweep.cuh"
+
+namespace sgm {
+namespace brick {
+
+template <int P, bool DUAL, int C, int AX>
+__host__ __device__ constexpr int nloc() {
+  return (C == AX) ? (DUAL ? P : P + 1) : (DUAL ? P - 1 : P);
+}
+
+template <int P, int Q, bool DUAL, int E, int C>
+struct Geo {
+  static constexpr int NX = nloc<P, DUAL, C, 0>(), NY = nloc<P, DUAL, C, 1>(), NZ = nloc<P, DUAL, C, 2>();
+  static constexpr int PX = E - 1 + NX, PY = E - 1 + NY;
+  static constexpr int EQ = E * Q;
+  static constexpr int WIN = NZ * PY * PX;   // coefficient / output window
+  static constexpr int Z1 = Q * PY * PX;     // after the z stage: [qz][py][px]
+  static constexpr int Z2 = Q * EQ * PX;     // after the y stage: [qz][Y][px]
+  static constexpr int U = Q * EQ * EQ;      // quadrature values: [qz][Y][X]
+  static constexpr int TOT = 2 * WIN + Z1 + Z2 + U;
+};
+
+template <int P, int Q, bool DUAL, int E>
+struct Layout {
+  using G0 = Geo<P, Q, DUAL, E, 0>;
+  using G1 = Geo<P, Q, DUAL, E, 1>;
+  using G2 = Geo<P, Q, DUAL, E, 2>;
+  static constexpr int NL = P + 1;
+  static constexpr int VXY = E * Q * NL;  // brick basis table of one axis and role: [e][q][k]
+  static constexpr int VZ = Q * NL;       // one element's z basis of one role
+  // per component: Xw, Yw, Z1, Z2, U; then tables [role][axis x, y] and [role] z
+  static constexpr int OFF1 = G0::TOT, OFF2 = OFF1 + G1::TOT, TAB = OFF2 + G2::TOT;
+  static constexpr int WB = TAB + 2 * 2 * VXY + 2 * VZ;  // W of one element layer (cp.async staged)
+  template <bool FULL>
+  static constexpr int total() { return WB + E * E * Q * Q * Q * (FULL ? 6 : 1); }
+};
+
+struct Brick {
+  int ex0, ey0, nex, ney;  // first element and number of live elements of the brick
+  int ez0, ez1;            // element layers [ez0, ez1)
+};
+
+// quadrature values are stored element-major, U[(ey*E + ex)][qz][qy][qx], the order of W in HBM
+template <int Q, int E>
+__device__ __forceinline__ int uidx(int qz, int Yq, int ex, int qx) {
+  const int ey = Yq / Q, qy = Yq - ey * Q;
+  return (ey * E + ex) * Q * Q * Q + (qz * Q + qy) * Q + qx;
+}
+
+// per-component pointers into shared memory
+template <int P, int Q, bool DUAL, int E, int C>
+struct CompSm {
+  using G = Geo<P, Q, DUAL, E, C>;
+  double *Xw, *Yw, *Z1, *Z2, *U;
+  const double *Vx, *Vy, *Vz;  // role-selected basis tables
+  __device__ CompSm(double* sm) {
+    using L = Layout<P, Q, DUAL, E>;
+    double* b = sm + (C == 0 ? 0 : (C == 1 ? L::OFF1 : L::OFF2));
+    Xw = b;
+    Yw = Xw + G::WIN;
+    Z1 = Yw + G::WIN;
+    Z2 = Z1 + G::Z1;
+    U = Z2 + G::Z2;
+    const double* tab = sm + L::TAB;
+    // role 0 = own (axis == C), 1 = other
+    Vx = tab + ((C == 0 ? 0 : 1) * 2 + 0) * L::VXY;
+    Vy = tab + ((C == 1 ? 0 : 1) * 2 + 1) * L::VXY;
+    Vz = tab + 4 * L::VXY + (C == 2 ? 0 : 1) * L::VZ;
+  }
+};
+
+// first global function index of element e along `axis` for `role`
+__device__ __forceinline__ int first_of(const HodgeArgs& A, int axis, int role, int e) {
+  return __ldg(A.first + A.first_off[axis][role] + e);
+}
+
+// load coefficient layer jz (global z index gz) of component C's patch into the window
+template <int P, int Q, bool DUAL, int E, int C>
+__device__ __forceinline__ void load_layer(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int gx0, int gy0,
+                                           int gz, int jz) {
+  using G = Geo<P, Q, DUAL, E, C>;
+  const int* ext = A.ext[C];
+  const double* __restrict__ x = A.x[C];
+  for (int o = threadIdx.x; o < G::PY * G::PX; o += blockDim.x) {
+    const int px = o % G::PX, py = o / G::PX;
+    const int gx = gx0 + px, gy = gy0 + py;
+    double v = 0.0;
+    if (gx >= 0 && gx < ext[0] && gy >= 0 && gy < ext[1] && gz >= 0 && gz < ext[2])
+      v = __ldg(x + gx + long(ext[0]) * (gy + long(ext[1]) * gz));
+    S.Xw[jz * G::PY * G::PX + o] = v;
+  }
+}
+
+// atomically add output layer 0 (global z index gz) of component C's patch, then shift both
+// windows down one layer (the X shift only while more elements follow)
+template <int P, int Q, bool DUAL, int E, int C>
+__device__ __forceinline__ void flush_layer(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int gx0, int gy0,
+                                            int gz) {
+  using G = Geo<P, Q, DUAL, E, C>;
+  const int* ext = A.ext[C];
+  double* __restrict__ y = A.y[C];
+  for (int o = threadIdx.x; o < G::PY * G::PX; o += blockDim.x) {
+    const int px = o % G::PX, py = o / G::PX;
+    const int gx = gx0 + px, gy = gy0 + py;
+    if (gx >= 0 && gx < ext[0] && gy >= 0 && gy < ext[1] && gz >= 0 && gz < ext[2])
+      atomicAdd(y + gx + long(ext[0]) * (gy + long(ext[1]) * gz), S.Yw[o]);
+  }
+}
+
+template <int P, int Q, bool DUAL, int E, int C>
+__device__ __forceinline__ void shift_windows(const CompSm<P, Q, DUAL, E, C>& S) {
+  using G = Geo<P, Q, DUAL, E, C>;
+  constexpr int LAY = G::PY * G::PX;
+  // read all, barrier, write all (in-place shift by one layer)
+  double xv[(G::WIN + 255) / 256], yv[(G::WIN + 255) / 256];
+#pragma unroll
+  for (int r = 0; r < (G::WIN + 255) / 256; ++r) {
+    const int o = threadIdx.x + 256 * r;
+    xv[r] = (o + LAY < G::WIN) ? S.Xw[o + LAY] : 0.0;
+    yv[r] = (o + LAY < G::WIN) ? S.Yw[o + LAY] : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < (G::WIN + 255) / 256; ++r) {
+    const int o = threadIdx.x + 256 * r;
+    if (o < G::WIN) {
+      S.Xw[o] = xv[r];
+      S.Yw[o] = yv[r];
+    }
+  }
+}
+
+// ---- interpolation stages of component C (tasks numbered from 0; `t` is this thread's task) ----
+// z: Z1[qz][py][px] = sum_jz Vz[qz][jz] Xw[jz][py][px]          (tasks: py, px)
+template <int P, int Q, bool DUAL, int E, int C>
+__device__ __forceinline__ void interp_z(const CompSm<P, Q, DUAL, E, C>& S, int t) {
+  using G = Geo<P, Q, DUAL, E, C>;
+  constexpr int NL = P + 1, LAY = G::PY * G::PX;
+  if (t >= LAY) return;
+  double xv[G::NZ];
+#pragma unroll
+  for (int jz = 0; jz < G::NZ; ++jz) xv[jz] = S.Xw[jz * LAY + t];
+#pragma unroll
+  for (int qz = 0; qz < Q; ++qz) {
+    double s = 0.0;
+#pragma unroll
+    for (int jz = 0; jz < G::NZ; ++jz) s = fma(S.Vz[qz * NL + jz], xv[jz], s);
+    S.Z1[qz * LAY + t] = s;
+  }
+}
+
+// y: Z2[qz][ey*Q+qy][px] = sum_jy Vy[ey][qy][jy] Z1[qz][ey+jy][px]   (tasks: qz, px)
+// UNI: every element of the brick has the same 1D basis table along this axis (interior
+// elements of a uniform mesh): the Q x N coefficients live in registers for the whole task.
+template <int Q, int N, int NL, bool UNI>
+struct Coef {
+  double c[UNI ? Q * N : 1];
+  __device__ __forceinline__ Coef(const double* V) {
+    if (UNI) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q)
+#pragma unroll
+        for (int j = 0; j < N; ++j) c[q * N + j] = V[q * NL + j];
+    }
+  }
+  __device__ __forceinline__ double operator()(const double* V, int e, int q, int j) const {
+    return UNI ? c[q * N + j] : V[(e * Q + q) * NL + j];
+  }
+};
+
+// (tasks: half, qz, px -- each half of the brick's elements along y is a separate task)
+template <int P, int Q, bool DUAL, int E, int C, bool UNI>
+__device__ __forceinline__ void interp_y(const CompSm<P, Q, DUAL, E, C>& S, int t) {
+  using G = Geo<P, Q, DUAL, E, C>;
+  constexpr int NL = P + 1, EH = E / 2;
+  if (t >= 2 * Q * G::PX) return;
+  const int hf = t / (Q * G::PX);
+  t -= hf * Q * G::PX;
+  const int px = t % G::PX, qz = t / G::PX;
+  const Coef<Q, G::NY, NL, UNI> V(S.Vy);
+  double zv[EH - 1 + G::NY];
+#pragma unroll
+  for (int py = 0; py < EH - 1 + G::NY; ++py) zv[py] = S.Z1[(qz * G::PY + hf * EH + py) * G::PX + px];
+#pragma unroll
+  for (int el = 0; el < EH; ++el)
+#pragma unroll
+    for (int qy = 0; qy < Q; ++qy) {
+      double s = 0.0;
+#pragma unroll
+      for (int jy = 0; jy < G::NY; ++jy) s = fma(V(S.Vy, hf * EH + el, qy, jy), zv[el + jy], s);
+      S.Z2[(qz * G::EQ + (hf * EH + el) * Q + qy) * G::PX + px] = s;
+    }
+}
+
+// x: U[qz][Y][ex*Q+qx] = sum_jx Vx[ex][qx][jx] Z2[qz][Y][ex+jx]    (tasks: qz, Y)
+template <int P, int Q, bool DUAL, int E, int C, bool UNI>
+__device__ __forceinline__ void interp_x(const CompSm<P, Q, DUAL, E, C>& S, int t) {
+  using G = Geo<P, Q, DUAL, E, C>;
+  constexpr int NL = P + 1;
+  if (t >= Q * G::EQ) return;
+  const Coef<Q, G::NX, NL, UNI> V(S.Vx);
+  double zv[G::PX];
+#pragma unroll
+  for (int px = 0; px < G::PX; ++px) zv[px] = S.Z2[t * G::PX + px];
+#pragma unroll
+  for (int ex = 0; ex < E; ++ex)
+#pragma unroll
+    for (int qx = 0; qx < Q; ++qx) {
+      double s = 0.0;
+#pragma unroll
+      for (int jx = 0; jx < G::NX; ++jx) s = fma(V(S.Vx, ex, qx, jx), zv[ex + jx], s);
+      S.U[uidx<Q, E>(t / G::EQ, t % G::EQ, ex, qx)] = s;
+    }
+}
+
+// ---- testing stages (transposes of the above) ----
+// x: Z2[qz][Y][px] = sum_{ex,qx} Vx[ex][qx][px-ex] U[qz][Y][ex*Q+qx]   (tasks: qz, Y)
+template <int P, int Q, bool DUAL, int E, int C, bool UNI>
+__device__ __forceinline__ void test_x(const CompSm<P, Q, DUAL, E, C>& S, int t) {
+  using G = Geo<P, Q, DUAL, E, C>;
+  constexpr int NL = P + 1;
+  if (t >= Q * G::EQ) return;
+  const Coef<Q, G::NX, NL, UNI> V(S.Vx);
+  double acc[G::PX];
+#pragma unroll
+  for (int px = 0; px < G::PX; ++px) acc[px] = 0.0;
+#pragma unroll
+  for (int ex = 0; ex < E; ++ex)
+#pragma unroll
+    for (int qx = 0; qx < Q; ++qx) {
+      const double u = S.U[uidx<Q, E>(t / G::EQ, t % G::EQ, ex, qx)];
+#pragma unroll
+      for (int jx = 0; jx < G::NX; ++jx) acc[ex + jx] = fma(V(S.Vx, ex, qx, jx), u, acc[ex + jx]);
+    }
+#pragma unroll
+  for (int px = 0; px < G::PX; ++px) S.Z2[t * G::PX + px] = acc[px];
+}
+
+// y: Z1[qz][py][px] = sum_{ey,qy} Vy[ey][qy][py-ey] Z2[qz][ey*Q+qy][px]   (tasks: qz, px)
+template <int P, int Q, bool DUAL, int E, int C, bool UNI>
+__device__ __forceinline__ void test_y(const CompSm<P, Q, DUAL, E, C>& S, int t) {
+  using G = Geo<P, Q, DUAL, E, C>;
+  constexpr int NL = P + 1;
+  if (t >= Q * G::PX) return;
+  const Coef<Q, G::NY, NL, UNI> V(S.Vy);
+  const int px = t % G::PX, qz = t / G::PX;
+  double acc[G::PY];
+#pragma unroll
+  for (int py = 0; py < G::PY; ++py) acc[py] = 0.0;
+#pragma unroll
+  for (int ey = 0; ey < E; ++ey)
+#pragma unroll
+    for (int qy = 0; qy < Q; ++qy) {
+      const double z = S.Z2[(qz * G::EQ + ey * Q + qy) * G::PX + px];
+#pragma unroll
+      for (int jy = 0; jy < G::NY; ++jy) acc[ey + jy] = fma(V(S.Vy, ey, qy, jy), z, acc[ey + jy]);
+    }
+#pragma unroll
+  for (int py = 0; py < G::PY; ++py) S.Z1[(qz * G::PY + py) * G::PX + px] = acc[py];
+}
+
+// z: Yw[jz][py][px] += sum_qz Vz[qz][jz] Z1[qz][py][px]      (tasks: py, px)
+template <int P, int Q, bool DUAL, int E, int C>
+__device__ __forceinline__ void test_z(const CompSm<P, Q, DUAL, E, C>& S, int t) {
+  using G = Geo<P, Q, DUAL, E, C>;
+  constexpr int NL = P + 1, LAY = G::PY * G::PX;
+  if (t >= LAY) return;
+  double zv[Q];
+#pragma unroll
+  for (int qz = 0; qz < Q; ++qz) zv[qz] = S.Z1[qz * LAY + t];
+#pragma unroll
+  for (int jz = 0; jz < G::NZ; ++jz) {
+    double s = S.Yw[jz * LAY + t];
+#pragma unroll
+    for (int qz = 0; qz < Q; ++qz) s = fma(S.Vz[qz * NL + jz], zv[qz], s);
+    S.Yw[jz * LAY + t] = s;
+  }
+}
+
+// run stage F for the three components, tasks of component c offset so that all threads work
+#define SGM_BRICK_STAGE3(F, N0, N1, N2)                                     \
+  {                                                                         \
+    for (int t = threadIdx.x; t < (N0) + (N1) + (N2); t += 256) {           \
+      if (t < (N0)) F<P, Q, DUAL, E, 0>(S0, t);                             \
+      else if (t < (N0) + (N1)) F<P, Q, DUAL, E, 1>(S1, t - (N0));          \
+      else F<P, Q, DUAL, E, 2>(S2, t - (N0) - (N1));                        \
+    }                                                                       \
+    __syncthreads();                                                        \
+  }
+// the same with the per-axis uniform-basis flags (own role of component c along the axis when
+// the axis is c's own, else the other role)
+#define SGM_BRICK_STAGE3U(F, AXIS, N0, N1, N2)                                                       \
+  {                                                                                                  \
+    const bool u0 = uni[(AXIS == 0 ? 0 : 1) * 2 + AXIS], u1 = uni[(AXIS == 1 ? 0 : 1) * 2 + AXIS],  \
+               u2 = uni[1 * 2 + AXIS];                                                               \
+    for (int t = threadIdx.x; t < (N0) + (N1) + (N2); t += 256) {                                    \
+      if (t < (N0)) {                                                                                \
+        if (u0) F<P, Q, DUAL, E, 0, true>(S0, t); else F<P, Q, DUAL, E, 0, false>(S0, t);            \
+      } else if (t < (N0) + (N1)) {                                                                  \
+        if (u1) F<P, Q, DUAL, E, 1, true>(S1, t - (N0)); else F<P, Q, DUAL, E, 1, false>(S1, t - (N0)); \
+      } else {                                                                                       \
+        if (u2) F<P, Q, DUAL, E, 2, true>(S2, t - (N0) - (N1));                                      \
+        else F<P, Q, DUAL, E, 2, false>(S2, t - (N0) - (N1));                                        \
+      }                                                                                              \
+    }                                                                                                \
+    __syncthreads();                                                                                 \
+  }
+
+template <int P, int Q, bool DUAL, bool FULL, int E>
+__global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_constant__ HodgeArgs A, int zchunk) {
+  using L = Layout<P, Q, DUAL, E>;
+  using G0 = Geo<P, Q, DUAL, E, 0>;
+  using G1 = Geo<P, Q, DUAL, E, 1>;
+  using G2 = Geo<P, Q, DUAL, E, 2>;
+  constexpr int NL = P + 1, QQQ = Q * Q * Q, EQ = E * Q;
+  extern __shared__ double sm[];
+  const CompSm<P, Q, DUAL, E, 0> S0(sm);
+  const CompSm<P, Q, DUAL, E, 1> S1(sm);
+  const CompSm<P, Q, DUAL, E, 2> S2(sm);
+  double* tab = sm + L::TAB;
+  double* Wsm = sm + L::WB;
+  const int nx = A.nel[0], ny = A.nel[1], nz = A.nel[2];
+  const int bx = (nx + E - 1) / E, by = (ny + E - 1) / E, bzn = (nz + zchunk - 1) / zchunk;
+  const long items = long(bx) * by * bzn;
+  for (long it = blockIdx.x; it < items; it += gridDim.x) {
+    Brick B;
+    {
+      const int ib = int(it % (long(bx) * by)), iz = int(it / (long(bx) * by));
+      B.ex0 = (ib % bx) * E;
+      B.ey0 = (ib / bx) * E;
+      B.nex = min(E, nx - B.ex0);
+      B.ney = min(E, ny - B.ey0);
+      B.ez0 = iz * zchunk;
+      B.ez1 = min(nz, B.ez0 + zchunk);
+    }
+    // brick x / y basis tables [role][axis][e][q][k] (elements past the mesh edge: zeros)
+    for (int o = threadIdx.x; o < 2 * 2 * L::VXY; o += 256) {
+      const int role = o / (2 * L::VXY), r = o % (2 * L::VXY), axis = r / L::VXY, i = r % L::VXY;
+      const int e = i / (Q * NL), rem = i % (Q * NL);
+      const int eg = (axis == 0 ? B.ex0 : B.ey0) + e;
+      const int ng = axis == 0 ? nx : ny;
+      tab[o] = (eg < ng) ? __ldg(A.basis + A.basis_off[axis][role] + size_t(eg) * Q * NL + rem) : 0.0;
+    }
+    __syncthreads();
+    // uni[role*2 + axis]: all live elements of the brick share element 0's table (and the brick is full)
+    bool uni[4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const double* T = tab + r * L::VXY;
+      bool same = (r % 2 == 0 ? B.nex : B.ney) == E;
+      // (interior elements of the uniform mesh: equal up to the rounding of their construction)
+      for (int i = threadIdx.x; i < (E - 1) * Q * NL; i += 256)
+        same = same && fabs(T[Q * NL + i] - T[i % (Q * NL)]) <= 1e-14 * (1.0 + fabs(T[i % (Q * NL)]));
+      uni[r] = __syncthreads_and(same) != 0;
+    }
+    const int fx[3] = {first_of(A, 0, 0, B.ex0), first_of(A, 0, 1, B.ex0), 0};  // own / other
+    const int fy[3] = {first_of(A, 1, 0, B.ey0), first_of(A, 1, 1, B.ey0), 0};
+    // patch origins per component: own role along its own axis
+    const int gx0[3] = {fx[0], fx[1], fx[1]}, gy0[3] = {fy[1], fy[0], fy[1]};
+    auto zfirst = [&](int c, int ez) { return first_of(A, 2, c == 2 ? 0 : 1, ez); };
+    // zero output windows, load the first NZ-1 coefficient layers
+    for (int o = threadIdx.x; o < G0::WIN; o += 256) S0.Yw[o] = 0.0;
+    for (int o = threadIdx.x; o < G1::WIN; o += 256) S1.Yw[o] = 0.0;
+    for (int o = threadIdx.x; o < G2::WIN; o += 256) S2.Yw[o] = 0.0;
+    for (int jz = 0; jz + 1 < G0::NZ; ++jz) load_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, B.ez0) + jz, jz);
+    for (int jz = 0; jz + 1 < G1::NZ; ++jz) load_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, B.ez0) + jz, jz);
+    for (int jz = 0; jz + 1 < G2::NZ; ++jz) load_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, B.ez0) + jz, jz);
+    // W of element layer ez -> Wsm (8-byte cp.async; elements past the mesh edge are skipped)
+    auto stage_w = [&](int ez) {
+      constexpr int NW = FULL ? 6 : 1;
+      for (int i = threadIdx.x; i < E * E * QQQ * NW; i += 256) {
+        const int qi = i / NW, k = i - qi * NW;
+        const int el = qi / QQQ, lq = qi - el * QQQ;
+        const int ex = el % E, ey = el / E;
+        if (ex < B.nex && ey < B.ney) {
+          const long e = (B.ex0 + ex) + long(nx) * ((B.ey0 + ey) + long(ny) * ez);
+          pipe::cp_async8(Wsm + i, A.W + (e * QQQ + lq) * NW + k);
+        }
+      }
+    };
+    stage_w(B.ez0);
+    for (int ez = B.ez0; ez < B.ez1; ++ez) {
+      // top coefficient layer and z bases of this element layer
+      load_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, ez) + G0::NZ - 1, G0::NZ - 1);
+      load_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, ez) + G1::NZ - 1, G1::NZ - 1);
+      load_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, ez) + G2::NZ - 1, G2::NZ - 1);
+      for (int o = threadIdx.x; o < 2 * L::VZ; o += 256) {
+        const int role = o / L::VZ;
+        tab[4 * L::VXY + o] = __ldg(A.basis + A.basis_off[2][role] + size_t(ez) * Q * NL + (o % L::VZ));
+      }
+      __syncthreads();
+      SGM_BRICK_STAGE3(interp_z, G0::PY * G0::PX, G1::PY * G1::PX, G2::PY * G2::PX)
+      SGM_BRICK_STAGE3U(interp_y, 1, 2 * Q * G0::PX, 2 * Q * G1::PX, 2 * Q * G2::PX)
+      SGM_BRICK_STAGE3U(interp_x, 0, Q * EQ, Q * EQ, Q * EQ)
+      // quadrature points: v_c = sum_c' W_cc' u_c' (FULL) or scale_c w u_c (SCALAR); W was staged
+      // into shared memory (element-major, the layout of U) while the interpolation ran
+      pipe::cp_async_wait_all();
+      __syncthreads();
+#pragma unroll 4
+      for (int i = threadIdx.x; i < E * E * QQQ; i += 256) {
+        const int el = i / QQQ;
+        const bool live = (el % E) < B.nex && (el / E) < B.ney;
+        const double u0 = S0.U[i], u1 = S1.U[i], u2 = S2.U[i];
+        if (FULL) {
+          const double* w = Wsm + i * 6;
+          const double wxx = live ? w[0] : 0.0, wyy = live ? w[1] : 0.0, wzz = live ? w[2] : 0.0,
+                       wxy = live ? w[3] : 0.0, wxz = live ? w[4] : 0.0, wyz = live ? w[5] : 0.0;
+          S0.U[i] = wxx * u0 + wxy * u1 + wxz * u2;
+          S1.U[i] = wxy * u0 + wyy * u1 + wyz * u2;
+          S2.U[i] = wxz * u0 + wyz * u1 + wzz * u2;
+        } else {
+          const double w = live ? Wsm[i] : 0.0;
+          S0.U[i] = A.scale[0] * w * u0;
+          S1.U[i] = A.scale[1] * w * u1;
+          S2.U[i] = A.scale[2] * w * u2;
+        }
+      }
+      __syncthreads();
+      if (ez + 1 < B.ez1) stage_w(ez + 1);
+      SGM_BRICK_STAGE3U(test_x, 0, Q * EQ, Q * EQ, Q * EQ)
+      SGM_BRICK_STAGE3U(test_y, 1, Q * G0::PX, Q * G1::PX, Q * G2::PX)
+      SGM_BRICK_STAGE3(test_z, G0::PY * G0::PX, G1::PY * G1::PX, G2::PY * G2::PX)
+      // the lowest output layer of each component is complete
+      flush_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, ez));
+      flush_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, ez));
+      flush_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, ez));
+      __syncthreads();
+      shift_windows<P, Q, DUAL, E, 0>(S0);
+      shift_windows<P, Q, DUAL, E, 1>(S1);
+      shift_windows<P, Q, DUAL, E, 2>(S2);
+      __syncthreads();
+    }
+    // the remaining NZ-1 output layers of the last element layer
+    for (int jz = 1; jz < G0::NZ; ++jz) {
+      flush_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, B.ez1 - 1) + jz);
+      __syncthreads();
+      shift_windows<P, Q, DUAL, E, 0>(S0);
+      __syncthreads();
+    }
+    for (int jz = 1; jz < G1::NZ; ++jz) {
+      flush_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, B.ez1 - 1) + jz);
+      __syncthreads();
+      shift_windows<P, Q, DUAL, E, 1>(S1);
+      __syncthreads();
+    }
+    for (int jz = 1; jz < G2::NZ; ++jz) {
+      flush_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, B.ez1 - 1) + jz);
+      __syncthreads();
+      shift_windows<P, Q, DUAL, E, 2>(S2);
+      __syncthreads();
+    }
+  }
+}
+
+#undef SGM_BRICK_STAGE3
+#undef SGM_BRICK_STAGE3U
+
+}  // namespace brick
+}  // namespace sgm

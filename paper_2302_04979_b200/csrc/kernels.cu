@@ -16,6 +16,7 @@
 #include "seg_sweep.cuh"
 #include "sweep_kernel.cuh"
 #include "hodge_kernel.cuh"
+#include "hodge_brick.cuh"
 
 #include <cstdint>
 #include <cstdlib>
@@ -682,8 +683,44 @@ void launch_hodge_pencil(const HodgeArgs& a, cudaStream_t st) {
   hodge::hodge_pencil_kernel<P, Q, DUAL, FULL><<<unsigned(grid), 256, smem, st>>>(a);
 }
 
+template <int P, int Q, bool DUAL, bool FULL>
+void launch_hodge_brick(const HodgeArgs& a, cudaStream_t st) {
+  constexpr int E = 4;
+  using L = brick::Layout<P, Q, DUAL, E>;
+  const size_t smem = size_t(L::template total<FULL>()) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(brick::hodge_brick_kernel<P, Q, DUAL, FULL, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    attr = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, brick::hodge_brick_kernel<P, Q, DUAL, FULL, E>, 256, smem);
+  if (per_sm < 1) per_sm = 1;
+  const long slots = long(per_sm) * sm_count();
+  const long bricks = long((a.nel[0] + E - 1) / E) * ((a.nel[1] + E - 1) / E);
+  // z chunks: about four work items per resident CTA, at least 4 element layers per chunk
+  long bzn = (4 * slots + bricks - 1) / bricks;
+  int zchunk = int((a.nel[2] + bzn - 1) / bzn);
+  if (zchunk < 4) zchunk = 4;
+  if (const int zc = env_int("SGM_HODGE_ZCHUNK", 0)) zchunk = zc;
+  const long items = bricks * ((a.nel[2] + zchunk - 1) / zchunk);
+  const long grid = items < slots ? items : slots;
+  brick::hodge_brick_kernel<P, Q, DUAL, FULL, E><<<unsigned(grid), 256, smem, st>>>(a, zchunk);
+}
+
 template <int P, int Q>
 void launch_hodge2(const HodgeArgs& a, cudaStream_t st) {
+  if (env_int("SGM_HODGE_PENCIL", 0) == 0) {
+    if (a.dual) {
+      if (a.full) launch_hodge_brick<P, Q, true, true>(a, st);
+      else launch_hodge_brick<P, Q, true, false>(a, st);
+    } else {
+      if (a.full) launch_hodge_brick<P, Q, false, true>(a, st);
+      else launch_hodge_brick<P, Q, false, false>(a, st);
+    }
+    return;
+  }
   if (a.dual) {
     if (a.full) launch_hodge_pencil<P, Q, true, true>(a, st);
     else launch_hodge_pencil<P, Q, true, false>(a, st);

@@ -104,7 +104,6 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
   const int NC = cfg.NC, NP = cfg.NP;
   const int NT = (NC + NP) * 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ax = XAX ? 0 : A.axis;
   const bool bulk = cfg.bulk != 0;
   double* tabs = sm;                              // [ntabs][tab_dbl]
   double* slabs = sm + cfg.ntabs * cfg.tab_dbl;   // [2][slab]
