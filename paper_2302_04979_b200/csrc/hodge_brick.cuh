@@ -387,13 +387,14 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
     // W of element layer ez -> Wsm (8-byte cp.async; elements past the mesh edge are skipped)
     auto stage_w = [&](int ez) {
       constexpr int NW = FULL ? 6 : 1;
-      for (int i = threadIdx.x; i < E * E * QQQ * NW; i += 256) {
-        const int qi = i / NW, k = i - qi * NW;
-        const int el = qi / QQQ, lq = qi - el * QQQ;
+      // warp w copies elements w, w + 8, ...: each element's W is contiguous in HBM and in Wsm
+      for (int el = threadIdx.x >> 5; el < E * E; el += 8) {
         const int ex = el % E, ey = el / E;
         if (ex < B.nex && ey < B.ney) {
           const long e = (B.ex0 + ex) + long(nx) * ((B.ey0 + ey) + long(ny) * ez);
-          pipe::cp_async8(Wsm + i, A.W + (e * QQQ + lq) * NW + k);
+          const double* src = A.W + e * QQQ * NW;
+          double* dst = Wsm + el * QQQ * NW;
+          for (int i = threadIdx.x & 31; i < QQQ * NW; i += 32) pipe::cp_async8(dst + i, src + i);
         }
       }
     };
@@ -415,23 +416,23 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
       // into shared memory (element-major, the layout of U) while the interpolation ran
       pipe::cp_async_wait_all();
       __syncthreads();
-#pragma unroll 4
-      for (int i = threadIdx.x; i < E * E * QQQ; i += 256) {
-        const int el = i / QQQ;
-        const bool live = (el % E) < B.nex && (el / E) < B.ney;
-        const double u0 = S0.U[i], u1 = S1.U[i], u2 = S2.U[i];
-        if (FULL) {
-          const double* w = Wsm + i * 6;
-          const double wxx = live ? w[0] : 0.0, wyy = live ? w[1] : 0.0, wzz = live ? w[2] : 0.0,
-                       wxy = live ? w[3] : 0.0, wxz = live ? w[4] : 0.0, wyz = live ? w[5] : 0.0;
-          S0.U[i] = wxx * u0 + wxy * u1 + wxz * u2;
-          S1.U[i] = wxy * u0 + wyy * u1 + wyz * u2;
-          S2.U[i] = wxz * u0 + wyz * u1 + wzz * u2;
-        } else {
-          const double w = live ? Wsm[i] : 0.0;
-          S0.U[i] = A.scale[0] * w * u0;
-          S1.U[i] = A.scale[1] * w * u1;
-          S2.U[i] = A.scale[2] * w * u2;
+      for (int el = threadIdx.x >> 5; el < E * E; el += 8) {
+        const bool live = (el % E) < B.nex && (el / E) < B.ney;  // warp-uniform
+        for (int i = el * QQQ + (threadIdx.x & 31); i < (el + 1) * QQQ; i += 32) {
+          const double u0 = S0.U[i], u1 = S1.U[i], u2 = S2.U[i];
+          if (FULL) {
+            const double* w = Wsm + i * 6;
+            const double wxx = live ? w[0] : 0.0, wyy = live ? w[1] : 0.0, wzz = live ? w[2] : 0.0,
+                         wxy = live ? w[3] : 0.0, wxz = live ? w[4] : 0.0, wyz = live ? w[5] : 0.0;
+            S0.U[i] = wxx * u0 + wxy * u1 + wxz * u2;
+            S1.U[i] = wxy * u0 + wyy * u1 + wyz * u2;
+            S2.U[i] = wxz * u0 + wyz * u1 + wzz * u2;
+          } else {
+            const double w = live ? Wsm[i] : 0.0;
+            S0.U[i] = A.scale[0] * w * u0;
+            S1.U[i] = A.scale[1] * w * u1;
+            S2.U[i] = A.scale[2] * w * u2;
+          }
         }
       }
       __syncthreads();
