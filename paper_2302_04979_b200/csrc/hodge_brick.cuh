@@ -8,7 +8,8 @@
 // brick's coefficients of each component form a patch of PX x PY functions (consecutive elements
 // share all but one function per axis: PX = E - 1 + NX); along z a window of NZ coefficient layers
 // slides by one layer per element, and the output window accumulates in shared memory, its lowest
-// layer complete (and flushed with fp64 atomics) after each element.  Per element layer the three
+// layer complete (and flushed with fp64 atomics) after each element; both windows are circular
+// (layer jz of the current element in slot (base + jz) % NZ), so nothing is copied.  Per element layer the three
 // interpolation stages (z, y, x), the quadrature-point multiply and the three testing stages
 // (x, y, z) each run over the whole brick with all threads: every 1D contraction is a small
 // register-blocked loop (one thread produces a whole row of outputs from one row of inputs), the
@@ -72,6 +73,11 @@ struct CompSm {
   using G = Geo<P, Q, DUAL, E, C>;
   double *Xw, *Yw, *Z1, *Z2, *U;
   const double *Vx, *Vy, *Vz;  // role-selected basis tables
+  int base = 0;                // window slot of layer 0 (circular: layer jz lives in slot (base + jz) % NZ)
+  __device__ __forceinline__ int slot(int jz) const {
+    const int s = base + jz;
+    return s >= G::NZ ? s - G::NZ : s;
+  }
   __device__ CompSm(double* sm) {
     using L = Layout<P, Q, DUAL, E>;
     double* b = sm + (C == 0 ? 0 : (C == 1 ? L::OFF1 : L::OFF2));
@@ -110,42 +116,21 @@ __device__ __forceinline__ void load_layer(const HodgeArgs& A, const CompSm<P, Q
   }
 }
 
-// atomically add output layer 0 (global z index gz) of component C's patch, then shift both
-// windows down one layer (the X shift only while more elements follow)
+// atomically add the output window slot `sl` (global z index gz) of component C's patch to y and
+// clear the slot for reuse as the top layer
 template <int P, int Q, bool DUAL, int E, int C>
 __device__ __forceinline__ void flush_layer(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int gx0, int gy0,
-                                            int gz) {
+                                            int gz, int sl) {
   using G = Geo<P, Q, DUAL, E, C>;
+  constexpr int LAY = G::PY * G::PX;
   const int* ext = A.ext[C];
   double* __restrict__ y = A.y[C];
-  for (int o = threadIdx.x; o < G::PY * G::PX; o += blockDim.x) {
+  for (int o = threadIdx.x; o < LAY; o += blockDim.x) {
     const int px = o % G::PX, py = o / G::PX;
     const int gx = gx0 + px, gy = gy0 + py;
     if (gx >= 0 && gx < ext[0] && gy >= 0 && gy < ext[1] && gz >= 0 && gz < ext[2])
-      atomicAdd(y + gx + long(ext[0]) * (gy + long(ext[1]) * gz), S.Yw[o]);
-  }
-}
-
-template <int P, int Q, bool DUAL, int E, int C>
-__device__ __forceinline__ void shift_windows(const CompSm<P, Q, DUAL, E, C>& S) {
-  using G = Geo<P, Q, DUAL, E, C>;
-  constexpr int LAY = G::PY * G::PX;
-  // read all, barrier, write all (in-place shift by one layer)
-  double xv[(G::WIN + 255) / 256], yv[(G::WIN + 255) / 256];
-#pragma unroll
-  for (int r = 0; r < (G::WIN + 255) / 256; ++r) {
-    const int o = threadIdx.x + 256 * r;
-    xv[r] = (o + LAY < G::WIN) ? S.Xw[o + LAY] : 0.0;
-    yv[r] = (o + LAY < G::WIN) ? S.Yw[o + LAY] : 0.0;
-  }
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < (G::WIN + 255) / 256; ++r) {
-    const int o = threadIdx.x + 256 * r;
-    if (o < G::WIN) {
-      S.Xw[o] = xv[r];
-      S.Yw[o] = yv[r];
-    }
+      atomicAdd(y + gx + long(ext[0]) * (gy + long(ext[1]) * gz), S.Yw[sl * LAY + o]);
+    S.Yw[sl * LAY + o] = 0.0;
   }
 }
 
@@ -158,7 +143,7 @@ __device__ __forceinline__ void interp_z(const CompSm<P, Q, DUAL, E, C>& S, int 
   if (t >= LAY) return;
   double xv[G::NZ];
 #pragma unroll
-  for (int jz = 0; jz < G::NZ; ++jz) xv[jz] = S.Xw[jz * LAY + t];
+  for (int jz = 0; jz < G::NZ; ++jz) xv[jz] = S.Xw[S.slot(jz) * LAY + t];
 #pragma unroll
   for (int qz = 0; qz < Q; ++qz) {
     double s = 0.0;
@@ -214,21 +199,24 @@ __device__ __forceinline__ void interp_y(const CompSm<P, Q, DUAL, E, C>& S, int 
 // x: U[qz][Y][ex*Q+qx] = sum_jx Vx[ex][qx][jx] Z2[qz][Y][ex+jx]    (tasks: qz, Y)
 template <int P, int Q, bool DUAL, int E, int C, bool UNI>
 __device__ __forceinline__ void interp_x(const CompSm<P, Q, DUAL, E, C>& S, int t) {
+  // (tasks: half, qz, Y -- each half of the brick's elements along x is a separate task)
   using G = Geo<P, Q, DUAL, E, C>;
-  constexpr int NL = P + 1;
-  if (t >= Q * G::EQ) return;
+  constexpr int NL = P + 1, EH = E / 2;
+  if (t >= 2 * Q * G::EQ) return;
+  const int hf = t / (Q * G::EQ);
+  t -= hf * Q * G::EQ;
   const Coef<Q, G::NX, NL, UNI> V(S.Vx);
-  double zv[G::PX];
+  double zv[EH - 1 + G::NX];
 #pragma unroll
-  for (int px = 0; px < G::PX; ++px) zv[px] = S.Z2[t * G::PX + px];
+  for (int px = 0; px < EH - 1 + G::NX; ++px) zv[px] = S.Z2[t * G::PX + hf * EH + px];
 #pragma unroll
-  for (int ex = 0; ex < E; ++ex)
+  for (int el = 0; el < EH; ++el)
 #pragma unroll
     for (int qx = 0; qx < Q; ++qx) {
       double s = 0.0;
 #pragma unroll
-      for (int jx = 0; jx < G::NX; ++jx) s = fma(V(S.Vx, ex, qx, jx), zv[ex + jx], s);
-      S.U[uidx<Q, E>(t / G::EQ, t % G::EQ, ex, qx)] = s;
+      for (int jx = 0; jx < G::NX; ++jx) s = fma(V(S.Vx, hf * EH + el, qx, jx), zv[el + jx], s);
+      S.U[uidx<Q, E>(t / G::EQ, t % G::EQ, hf * EH + el, qx)] = s;
     }
 }
 
@@ -289,10 +277,11 @@ __device__ __forceinline__ void test_z(const CompSm<P, Q, DUAL, E, C>& S, int t)
   for (int qz = 0; qz < Q; ++qz) zv[qz] = S.Z1[qz * LAY + t];
 #pragma unroll
   for (int jz = 0; jz < G::NZ; ++jz) {
-    double s = S.Yw[jz * LAY + t];
+    const int sl = S.slot(jz);
+    double s = S.Yw[sl * LAY + t];
 #pragma unroll
     for (int qz = 0; qz < Q; ++qz) s = fma(S.Vz[qz * NL + jz], zv[qz], s);
-    S.Yw[jz * LAY + t] = s;
+    S.Yw[sl * LAY + t] = s;
   }
 }
 
@@ -333,9 +322,9 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
   using G2 = Geo<P, Q, DUAL, E, 2>;
   constexpr int NL = P + 1, QQQ = Q * Q * Q, EQ = E * Q;
   extern __shared__ double sm[];
-  const CompSm<P, Q, DUAL, E, 0> S0(sm);
-  const CompSm<P, Q, DUAL, E, 1> S1(sm);
-  const CompSm<P, Q, DUAL, E, 2> S2(sm);
+  CompSm<P, Q, DUAL, E, 0> S0(sm);
+  CompSm<P, Q, DUAL, E, 1> S1(sm);
+  CompSm<P, Q, DUAL, E, 2> S2(sm);
   double* tab = sm + L::TAB;
   double* Wsm = sm + L::WB;
   const int nx = A.nel[0], ny = A.nel[1], nz = A.nel[2];
@@ -377,13 +366,21 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
     // patch origins per component: own role along its own axis
     const int gx0[3] = {fx[0], fx[1], fx[1]}, gy0[3] = {fy[1], fy[0], fy[1]};
     auto zfirst = [&](int c, int ez) { return first_of(A, 2, c == 2 ? 0 : 1, ez); };
-    // zero output windows, load the first NZ-1 coefficient layers
+    // zero output windows, load the NZ coefficient layers and z bases of the first element layer
+    S0.base = S1.base = S2.base = 0;
     for (int o = threadIdx.x; o < G0::WIN; o += 256) S0.Yw[o] = 0.0;
     for (int o = threadIdx.x; o < G1::WIN; o += 256) S1.Yw[o] = 0.0;
     for (int o = threadIdx.x; o < G2::WIN; o += 256) S2.Yw[o] = 0.0;
-    for (int jz = 0; jz + 1 < G0::NZ; ++jz) load_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, B.ez0) + jz, jz);
-    for (int jz = 0; jz + 1 < G1::NZ; ++jz) load_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, B.ez0) + jz, jz);
-    for (int jz = 0; jz + 1 < G2::NZ; ++jz) load_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, B.ez0) + jz, jz);
+    for (int jz = 0; jz < G0::NZ; ++jz) load_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, B.ez0) + jz, jz);
+    for (int jz = 0; jz < G1::NZ; ++jz) load_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, B.ez0) + jz, jz);
+    for (int jz = 0; jz < G2::NZ; ++jz) load_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, B.ez0) + jz, jz);
+    auto load_vz = [&](int ez) {
+      for (int o = threadIdx.x; o < 2 * L::VZ; o += 256) {
+        const int role = o / L::VZ;
+        tab[4 * L::VXY + o] = __ldg(A.basis + A.basis_off[2][role] + size_t(ez) * Q * NL + (o % L::VZ));
+      }
+    };
+    load_vz(B.ez0);
     // W of element layer ez -> Wsm (8-byte cp.async; elements past the mesh edge are skipped)
     auto stage_w = [&](int ez) {
       constexpr int NW = FULL ? 6 : 1;
@@ -399,19 +396,11 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
       }
     };
     stage_w(B.ez0);
+    __syncthreads();
     for (int ez = B.ez0; ez < B.ez1; ++ez) {
-      // top coefficient layer and z bases of this element layer
-      load_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, ez) + G0::NZ - 1, G0::NZ - 1);
-      load_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, ez) + G1::NZ - 1, G1::NZ - 1);
-      load_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, ez) + G2::NZ - 1, G2::NZ - 1);
-      for (int o = threadIdx.x; o < 2 * L::VZ; o += 256) {
-        const int role = o / L::VZ;
-        tab[4 * L::VXY + o] = __ldg(A.basis + A.basis_off[2][role] + size_t(ez) * Q * NL + (o % L::VZ));
-      }
-      __syncthreads();
       SGM_BRICK_STAGE3(interp_z, G0::PY * G0::PX, G1::PY * G1::PX, G2::PY * G2::PX)
       SGM_BRICK_STAGE3U(interp_y, 1, 2 * Q * G0::PX, 2 * Q * G1::PX, 2 * Q * G2::PX)
-      SGM_BRICK_STAGE3U(interp_x, 0, Q * EQ, Q * EQ, Q * EQ)
+      SGM_BRICK_STAGE3U(interp_x, 0, 2 * Q * EQ, 2 * Q * EQ, 2 * Q * EQ)
       // quadrature points: v_c = sum_c' W_cc' u_c' (FULL) or scale_c w u_c (SCALAR); W was staged
       // into shared memory (element-major, the layout of U) while the interpolation ran
       pipe::cp_async_wait_all();
@@ -440,35 +429,30 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
       SGM_BRICK_STAGE3U(test_x, 0, Q * EQ, Q * EQ, Q * EQ)
       SGM_BRICK_STAGE3U(test_y, 1, Q * G0::PX, Q * G1::PX, Q * G2::PX)
       SGM_BRICK_STAGE3(test_z, G0::PY * G0::PX, G1::PY * G1::PX, G2::PY * G2::PX)
-      // the lowest output layer of each component is complete
-      flush_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, ez));
-      flush_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, ez));
-      flush_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, ez));
-      __syncthreads();
-      shift_windows<P, Q, DUAL, E, 0>(S0);
-      shift_windows<P, Q, DUAL, E, 1>(S1);
-      shift_windows<P, Q, DUAL, E, 2>(S2);
-      __syncthreads();
-    }
-    // the remaining NZ-1 output layers of the last element layer
-    for (int jz = 1; jz < G0::NZ; ++jz) {
-      flush_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, B.ez1 - 1) + jz);
-      __syncthreads();
-      shift_windows<P, Q, DUAL, E, 0>(S0);
-      __syncthreads();
-    }
-    for (int jz = 1; jz < G1::NZ; ++jz) {
-      flush_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, B.ez1 - 1) + jz);
-      __syncthreads();
-      shift_windows<P, Q, DUAL, E, 1>(S1);
+      // the lowest output layer of each component is complete: flush and clear its slot; the
+      // freed coefficient slot (this element's layer 0) takes the next element's top layer
+      flush_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, ez), S0.slot(0));
+      flush_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, ez), S1.slot(0));
+      flush_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, ez), S2.slot(0));
+      if (ez + 1 < B.ez1) {
+        load_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, ez + 1) + G0::NZ - 1, S0.slot(0));
+        load_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, ez + 1) + G1::NZ - 1, S1.slot(0));
+        load_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, ez + 1) + G2::NZ - 1, S2.slot(0));
+        load_vz(ez + 1);
+      }
+      S0.base = S0.slot(1);
+      S1.base = S1.slot(1);
+      S2.base = S2.slot(1);
       __syncthreads();
     }
-    for (int jz = 1; jz < G2::NZ; ++jz) {
-      flush_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, B.ez1 - 1) + jz);
-      __syncthreads();
-      shift_windows<P, Q, DUAL, E, 2>(S2);
-      __syncthreads();
-    }
+    // the remaining NZ-1 output layers of the last element layer (layer jz now sits in slot jz-1)
+    for (int jz = 1; jz < G0::NZ; ++jz)
+      flush_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, B.ez1 - 1) + jz, S0.slot(jz - 1));
+    for (int jz = 1; jz < G1::NZ; ++jz)
+      flush_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, B.ez1 - 1) + jz, S1.slot(jz - 1));
+    for (int jz = 1; jz < G2::NZ; ++jz)
+      flush_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, B.ez1 - 1) + jz, S2.slot(jz - 1));
+    __syncthreads();
   }
 }
 
