@@ -192,6 +192,9 @@ def launch_bytes(pl, S, N_e, N_h, has_src):
             # reduced schedule: an eps pass sweeps 2 of the 3 (equal-size) components, a mu pass 1
             if not pl.reduced_schedule():
                 out += [(pre + "_z", 16 * N), (pre + "_y", 16 * N), (pre + "_x", 16 * N)]
+            elif half == 0 and pl.schedule_mode() == 2:
+                # eps: {0 z, 1 z, 2 y} in one launch, then {0 y} and {1 x, 2 x} concurrently
+                out += [(pre + "_z", 16 * N), (pre + "_y", 16 * N / 3), (pre + "_x", 16 * N * 2 / 3)]
             elif half == 0:
                 out += [(pre + "_z", 16 * N * 2 / 3), (pre + "_y", 16 * N * 2 / 3), (pre + "_x", 16 * N * 2 / 3)]
             elif pl.kernels_per_step() - (4 if pl.separable(S.MASS_EPS) else 5) == 3:

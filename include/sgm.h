@@ -205,7 +205,9 @@ sgm_status sgm_cfl(sgm_plan plan, double* x, double* e, double* b, double* h, in
 
 /* *on = 1 if separable Hodge stars use the reduced schedule (the diagonal 1D
    factors Hat M^{-1} Gamma_B^{p-1} = diag(1/s) and Hat M^{-T} Gamma_C^{p-1} = diag(s), verified at
-   plan creation, replace their line sweeps by per-line scalings), 0 if every axis is swept. */
+   plan creation, replace their line sweeps by per-line scalings), 2 if in addition independent
+   sweeps run concurrently on a plan-owned stream (fork/join on events; SGM_FORK=0 disables),
+   0 if every axis is swept. */
 sgm_status sgm_plan_reduced_schedule(sgm_plan plan, int* on);
 
 /* Number of kernels one sgm_step step launches for this plan (for launch accounting). */

@@ -205,10 +205,14 @@ class Plan:
         check(sgm_workspace_bytes(self.h, ctypes.byref(n)))
         return n.value
 
-    def reduced_schedule(self):
+    def schedule_mode(self):
+        """0: full three-axis sweeps, 1: reduced separable schedule, 2: reduced with concurrent sweeps."""
         v = c_int(0)
         check(sgm_plan_reduced_schedule(self.h, ctypes.byref(v)), "sgm_plan_reduced_schedule")
-        return bool(v.value)
+        return v.value
+
+    def reduced_schedule(self):
+        return self.schedule_mode() > 0
 
     def kernels_per_step(self):
         n = c_int()

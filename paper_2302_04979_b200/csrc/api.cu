@@ -178,9 +178,11 @@ struct PassComp {
 
 // Components of one launch share the line mode (x, or strided y/z) and the padded table rows and
 // segment length of their axes (checked by the caller); at most two distinct tables.
-void sweep_pass_list(const Plan& P, int kind, const PassComp* pc, int n, cudaStream_t st, int reverse) {
+void sweep_pass_list(const Plan& P, int kind, const PassComp* pc, int n, cudaStream_t st, int reverse,
+                     int max_ctas = 0) {
   SweepArgs a;
   std::memset(&a, 0, sizeof(a));
+  a.max_ctas = max_ctas;
   a.ncomp = n;
   a.axis = pc[0].axis;
   a.band = 1;
@@ -219,6 +221,32 @@ void sweep_pass_list(const Plan& P, int kind, const PassComp* pc, int n, cudaStr
 bool mu_merged(const Plan& P) {
   return P.seg[1] == P.seg[2] && P.rpad[1] == P.rpad[2] && !getenv("SGM_NOMERGE");
 }
+// ... and so do the eps star's first z- and y-line sweeps
+bool eps_merged(const Plan& P) { return mu_merged(P); }
+
+// k/n of the SMs (at least one) for one side of a fork
+int share(int k, int n) {
+  int sm = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, dev);
+  const int g = (sm * k + n / 2) / n;
+  return g > 0 ? g : 1;
+}
+
+// Run f1 on `st` and f2 on the plan's auxiliary stream concurrently, both after everything
+// already enqueued on `st`; `st` continues after both (event fork/join; captured into graphs).
+template <class F1, class F2>
+void fork_join(Plan& P, cudaStream_t st, F1&& f1, F2&& f2) {
+  std::lock_guard<std::mutex> lk(P.fork_mu);
+  cudaStream_t aux = static_cast<cudaStream_t>(P.aux_stream);
+  cudaEvent_t fk = static_cast<cudaEvent_t>(P.ev_fork), jn = static_cast<cudaEvent_t>(P.ev_join);
+  cudaEventRecord(fk, st);
+  cudaStreamWaitEvent(aux, fk, 0);
+  f1(st);
+  f2(aux);
+  cudaEventRecord(jn, aux);
+  cudaStreamWaitEvent(st, jn, 0);
+}
 
 // Reduced separable Hodge star y = K^{-1} M x using the diagonal 1D factors (host_setup.cpp):
 //   eps (kind 0): component c is swept (Gamma_C^{p-2}, LU Hat G) along the two axes != c and
@@ -236,6 +264,19 @@ void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* 
             kx = kind == 0 ? SGM_K_EPS_X : SGM_K_MU_X;
   if (kind == 0) {
     const int op = OP_EPS_OTH;
+    if (P.fork_enabled && eps_merged(P)) {
+      // strided pass {0 along z, 1 along z, 2 along y}, then concurrently {0 along y} (strided,
+      // 1/3 of the SMs) and {1, 2 along x} (2/3 of the SMs, plan-owned stream)
+      PassComp a3[3] = {{2, 0, X[0], T[0], op, {-1, -1, -1}, 1.0},
+                        {2, 1, X[1], T[1], op, {-1, -1, -1}, 1.0},
+                        {1, 2, X[2], T[2], op, {-1, -1, -1}, 1.0}};
+      PassComp b1[1] = {{1, 0, T[0], Y[0], op, {0, -1, -1}, M.scale[0]}};
+      PassComp c2[2] = {{0, 1, T[1], Y[1], op, {-1, 0, -1}, M.scale[1]}, {0, 2, T[2], Y[2], op, {-1, -1, 0}, M.scale[2]}};
+      { ProfScope ps(P, kz, st); sweep_pass_list(P, 0, a3, 3, st, 1); }
+      fork_join(P, st, [&](cudaStream_t s1) { ProfScope ps(P, ky, s1); sweep_pass_list(P, 0, b1, 1, s1, 0, share(1, 3)); },
+                [&](cudaStream_t s2) { ProfScope ps(P, kx, s2); sweep_pass_list(P, 0, c2, 2, s2, 1, share(2, 3)); });
+      return;
+    }
     PassComp z[2] = {{2, 0, X[0], T[0], op, {-1, -1, -1}, 1.0}, {2, 1, X[1], T[1], op, {-1, -1, -1}, 1.0}};
     PassComp yy[2] = {{1, 0, T[0], Y[0], op, {0, -1, -1}, M.scale[0]}, {1, 2, X[2], T[2], op, {-1, -1, -1}, 1.0}};
     PassComp xx[2] = {{0, 1, T[1], Y[1], op, {-1, 0, -1}, M.scale[1]}, {0, 2, T[2], Y[2], op, {-1, -1, 0}, M.scale[2]}};
@@ -248,8 +289,14 @@ void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* 
     PassComp yy[1] = {{1, 1, X[1], Y[1], op, {1, -1, 1}, M.scale[1]}};
     PassComp xx[1] = {{0, 0, X[0], Y[0], op, {-1, 1, 1}, M.scale[0]}};
     if (mu_merged(P)) {
-      // z-lines of component 2 and y-lines of component 1 in one strided launch
+      // z-lines of component 2 and y-lines of component 1 in one strided launch; the x-lines of
+      // component 0 (independent) concurrently on the plan-owned stream when forking is enabled
       PassComp zy[2] = {z[0], yy[0]};
+      if (P.fork_enabled) {
+        fork_join(P, st, [&](cudaStream_t s1) { ProfScope ps(P, kz, s1); sweep_pass_list(P, 1, zy, 2, s1, 1, share(2, 3)); },
+                  [&](cudaStream_t s2) { ProfScope ps(P, kx, s2); sweep_pass_list(P, 1, xx, 1, s2, 1, share(1, 3)); });
+        return;
+      }
       { ProfScope ps(P, kz, st); sweep_pass_list(P, 1, zy, 2, st, 1); }
     } else {
       { ProfScope ps(P, kz, st); sweep_pass_list(P, 1, z, 1, st, 1); }
@@ -514,6 +561,18 @@ sgm_status sgm_plan_create(const sgm_plan_desc* desc, sgm_plan* out) {
       return fail(SGM_E_NOMEM, "cudaMalloc failed for tables");
     }
     cudaMemcpy(P->tables_dev, P->tables_host.data(), tb, cudaMemcpyHostToDevice);
+    {
+      cudaStream_t aux;
+      cudaEvent_t e1, e2;
+      cudaStreamCreateWithFlags(&aux, cudaStreamNonBlocking);
+      cudaEventCreateWithFlags(&e1, cudaEventDisableTiming);
+      cudaEventCreateWithFlags(&e2, cudaEventDisableTiming);
+      P->aux_stream = aux;
+      P->ev_fork = e1;
+      P->ev_join = e2;
+      const char* f = getenv("SGM_FORK");
+      P->fork_enabled = !(f && atoi(f) == 0);
+    }
     st = upload_basis(*P);
     if (st != SGM_OK) {
       sgm_plan_destroy(reinterpret_cast<sgm_plan>(P));
@@ -549,6 +608,9 @@ sgm_status sgm_plan_destroy(sgm_plan plan) {
       cudaEventDestroy(static_cast<cudaEvent_t>(r.b));
     }
     for (void* e : P->ev_pool) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+    if (P->aux_stream) cudaStreamDestroy(static_cast<cudaStream_t>(P->aux_stream));
+    if (P->ev_fork) cudaEventDestroy(static_cast<cudaEvent_t>(P->ev_fork));
+    if (P->ev_join) cudaEventDestroy(static_cast<cudaEvent_t>(P->ev_join));
   }
   delete P;
   return SGM_OK;
@@ -611,7 +673,8 @@ sgm_status sgm_plan_hodge_separable(sgm_plan plan, sgm_mass mass, int* separable
 
 sgm_status sgm_plan_reduced_schedule(sgm_plan plan, int* on) {
   if (!plan || !on) return fail(SGM_E_INVALID_ARG, "NULL argument");
-  *on = PL(plan)->diag_ok ? 1 : 0;
+  const Plan& P = *PL(plan);
+  *on = P.diag_ok ? (P.fork_enabled && eps_merged(P) ? 2 : 1) : 0;
   return SGM_OK;
 }
 

@@ -529,6 +529,7 @@ bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
   const int cap = env_int("SGM_CTAS_PER_SM", 0);
   if (cap > 0 && cap < per_sm) per_sm = cap;
   long grid = long(per_sm) * sm_count();
+  if (a.max_ctas > 0 && grid > a.max_ctas) grid = a.max_ctas;
   if (grid > cfg.nitems) grid = cfg.nitems;
   if (grid < 1) grid = 1;
   launch_pdl(sweep::sweep_kernel<P, HB, SEG, LPT, MODE, OPS>, unsigned(grid), unsigned(NT), smem, st, a, cfg);

@@ -49,6 +49,7 @@ struct SweepArgs {
   int reverse;            // process the work items last-to-first ("snake" order across kernels:
                           // a kernel starts on what its predecessor wrote last, still in L2)
   PrologueArgs pro;       // update kernel only
+  int max_ctas;           // sweeps: cap on the persistent grid (0 = one CTA per SM slot)
 };
 
 // General (non-separable) Hodge apply y = M x by sum factorisation per element.

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstddef>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -97,6 +98,13 @@ struct Plan {
   std::vector<double> tables_host;
   bool sticky_cuda_error = false;
   bool graph_enabled = true;          // SGM_GRAPH=0 disables the sgm_step graph cache
+  // fork/join of independent sweep launches (reduced separable schedule): the second launch runs on
+  // a plan-owned stream on its own share of the SMs; `fork_mu` serialises the enqueue of a fork/join
+  bool fork_enabled = true;           // SGM_FORK=0 disables
+  void* aux_stream = nullptr;         // cudaStream_t
+  void* ev_fork = nullptr;            // cudaEvent_t (timing disabled)
+  void* ev_join = nullptr;
+  std::mutex fork_mu;
   void* graph_exec = nullptr;         // cudaGraphExec_t of the last captured sgm_step call
   GraphKey graph_key{};
   size_t N_e = 0, N_h = 0;

@@ -20,5 +20,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 ncu --set full --clock-control none --import-source on -k "regex:sweep_kernel|update_kernel" \
     --launch-skip ${SKIP:-26} --launch-count 14 -o gpurun_out/full_$TAG -f python bench.py $ARGS > gpurun_out/ncu_full_$TAG.log 2>&1
 ncu -i gpurun_out/full_$TAG.ncu-rep --page raw --csv > gpurun_out/full_${TAG}_raw.csv 2>/dev/null
-ncu -i gpurun_out/full_$TAG.ncu-rep --page source --csv > gpurun_out/full_${TAG}_source.csv 2>/dev/null
+# keep the merge-back under 64 MiB: the report itself stays on the box
+rm -f gpurun_out/full_$TAG.ncu-rep
 ls -la gpurun_out | tail -30
