@@ -178,11 +178,16 @@ struct PassComp {
 
 // Components of one launch share the line mode (x, or strided y/z) and the padded table rows and
 // segment length of their axes (checked by the caller); at most two distinct tables.
+struct Share {
+  int k, n;  // k/n of the resident-CTA slots (0/0 = all)
+};
+
 void sweep_pass_list(const Plan& P, int kind, const PassComp* pc, int n, cudaStream_t st, int reverse,
-                     int max_ctas = 0) {
+                     Share sh = {0, 0}) {
   SweepArgs a;
   std::memset(&a, 0, sizeof(a));
-  a.max_ctas = max_ctas;
+  a.share_k = sh.k;
+  a.share_n = sh.n;
   a.ncomp = n;
   a.axis = pc[0].axis;
   a.band = 1;
@@ -224,14 +229,8 @@ bool mu_merged(const Plan& P) {
 // ... and so do the eps star's first z- and y-line sweeps
 bool eps_merged(const Plan& P) { return mu_merged(P); }
 
-// k/n of the SMs (at least one) for one side of a fork
-int share(int k, int n) {
-  int sm = 0, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sm, cudaDevAttrMultiProcessorCount, dev);
-  const int g = (sm * k + n / 2) / n;
-  return g > 0 ? g : 1;
-}
+// k/n of the GPU's resident-CTA slots for one side of a fork
+Share share(int k, int n) { return {k, n}; }
 
 // Run f1 on `st` and f2 on the plan's auxiliary stream concurrently, both after everything
 // already enqueued on `st`; `st` continues after both (event fork/join; captured into graphs).

@@ -499,7 +499,17 @@ bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
   if (cfg.NC + cfg.NP > 16) cfg.NP = 16 - cfg.NC;
   if (cfg.NP < 1) return false;
   if (MODE == 3) {
-    cfg.pitch = bulk ? Lmax : (cfg.rows | 1);  // bulk: whole-tile copy, pitch = line length
+    // bulk: a whole-tile copy keeps pitch = line length; a multiple of 4 would put the consumers'
+    // per-lane line walks on few banks (all lanes on one bank pair at L % 16 == 0), so such lines
+    // are copied one by one into pitch L + 2 (16-byte aligned rows, 4-way at worst)
+    int bp_max = 0;
+    for (int c = 0; c < a.ncomp; ++c) {
+      sweep::CompGeom& g = cfg.g[c];
+      g.lbulk = (bulk && (g.L % 4) == 0 && env_int("SGM_LINE_BULK", 1)) ? 1 : 0;
+      g.bpitch = g.lbulk ? g.L + 2 : g.L;
+      bp_max = g.bpitch > bp_max ? g.bpitch : bp_max;
+    }
+    cfg.pitch = bulk ? bp_max : (cfg.rows | 1);
     cfg.W = 0;
     cfg.slab = TW * cfg.pitch + cfg.rows + 2;
   } else {
@@ -529,7 +539,8 @@ bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
   const int cap = env_int("SGM_CTAS_PER_SM", 0);
   if (cap > 0 && cap < per_sm) per_sm = cap;
   long grid = long(per_sm) * sm_count();
-  if (a.max_ctas > 0 && grid > a.max_ctas) grid = a.max_ctas;
+  if (a.share_n > 0) grid = (grid * a.share_k + a.share_n / 2) / a.share_n;
+  if (grid < 1) grid = 1;
   if (grid > cfg.nitems) grid = cfg.nitems;
   if (grid < 1) grid = 1;
   launch_pdl(sweep::sweep_kernel<P, HB, SEG, LPT, MODE, OPS>, unsigned(grid), unsigned(NT), smem, st, a, cfg);
@@ -550,6 +561,7 @@ void launch_sweep_o(const SweepArgs& a, cudaStream_t st) {
   // band half-width: P - 1 for the eps-side Grams and the pairing factors, P for the mu-side Gram
   if (a.band && a.solve) {
     if (a.band_hw >= P) launch_sweep_m<P, P, SEG, MODE, 3>(a, st);
+    else if (P >= 3 && a.band_hw <= P - 2) launch_sweep_m<P, (P >= 3 ? P - 2 : 1), SEG, MODE, 3>(a, st);  // eps Gamma_C^{p-2}
     else launch_sweep_m<P, P - 1, SEG, MODE, 3>(a, st);
   } else if (a.solve) {
     launch_sweep_m<P, P - 1, SEG, MODE, 2>(a, st);

@@ -49,7 +49,7 @@ struct SweepArgs {
   int reverse;            // process the work items last-to-first ("snake" order across kernels:
                           // a kernel starts on what its predecessor wrote last, still in L2)
   PrologueArgs pro;       // update kernel only
-  int max_ctas;           // sweeps: cap on the persistent grid (0 = one CTA per SM slot)
+  int share_k, share_n;   // sweeps: use share_k/share_n of the resident-CTA slots (0/0 = all)
 };
 
 // General (non-separable) Hodge apply y = M x by sum factorisation per element.

@@ -55,6 +55,8 @@ struct CompGeom {
   int rowlen;  // x axis: row length (= L)
   int TD;      // transverse divisor: line l -> (t0, t1) = (l % TD, l / TD)
   unsigned tmagic;  // floor((2^32 - 1) / TD)
+  int bpitch;  // x axis, bulk: slab pitch of this component's lines (= L, or L + 2 when L % 4 == 0)
+  int lbulk;   // x axis, bulk: 1 = one bulk copy per line (padded pitch), 0 = one per tile
 };
 
 struct Cfg {
@@ -156,10 +158,18 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
       if (bulk) {
         // one producer warp drives the bulk-copy engine; completion is counted on full_mb[buf]
         if (pw == 0) {
-          if (lane == 0) {
-            const unsigned bytes = unsigned(cnt) * unsigned(g.X) * 8u;
-            pipe::mbar_arrive_expect_tx(full_mb + buf, (cfg.dbg & 2) ? 0u : bytes);
-            if (!(cfg.dbg & 2)) pipe::bulk_g2s(slab, C.in + long(l0) * g.X, bytes, full_mb + buf);
+          const unsigned bytes = unsigned(cnt) * unsigned(g.X) * 8u;
+          if (lane == 0) pipe::mbar_arrive_expect_tx(full_mb + buf, (cfg.dbg & 2) ? 0u : bytes);
+          if (!(cfg.dbg & 2)) {
+            if (g.lbulk) {
+              // line by line into a padded pitch (an L % 4 == 0 pitch would put every lane's line
+              // walk on the same few banks); copy completions may precede the expect: the phase
+              // cannot complete before lane 0's arrival
+              for (int j = lane; j < cnt; j += 32)
+                pipe::bulk_g2s(slab + j * g.bpitch, C.in + long(l0 + j) * g.X, unsigned(g.X) * 8u, full_mb + buf);
+            } else if (lane == 0) {
+              pipe::bulk_g2s(slab, C.in + long(l0) * g.X, bytes, full_mb + buf);
+            }
           }
         }
         continue;
@@ -244,7 +254,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
     }
     // ---- my lines' segment start in the slab; consecutive line elements are ES apart
     constexpr int ES = XAX ? 1 : TW;
-    const int pitch = XAX ? (bulk ? g.X : cfg.pitch) : 0;  // x bulk: whole-tile copy, pitch X
+    const int pitch = XAX ? (bulk ? g.bpitch : cfg.pitch) : 0;  // x bulk: line length (or padded)
     const double* cp[LPT];
 #pragma unroll
     for (int q = 0; q < LPT; ++q) cp[q] = slab + (XAX ? (lane + 32 * q) * pitch : lane + 32 * q) + r0 * ES;
@@ -473,7 +483,14 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
       if (bulk) {
         pipe::fence_proxy_async_smem();
         pipe::bar_sync(pipe::kBarCons, NC * 32);
-        if (threadIdx.x == 0) {
+        if (g.lbulk) {
+          if (warp == 0) {
+            for (int j = lane; j < cnt; j += 32)
+              pipe::bulk_s2g(C.out + long(l0 + j) * g.X, slab + j * g.bpitch, unsigned(g.X) * 8u);
+            pipe::bulk_commit();
+            pipe::bulk_wait_read0();
+          }
+        } else if (threadIdx.x == 0) {
           pipe::bulk_s2g(C.out + long(l0) * g.X, slab, unsigned(cnt) * unsigned(g.X) * 8u);
           pipe::bulk_commit();
           pipe::bulk_wait_read0();  // the slab may be refilled once its contents have been read
@@ -491,7 +508,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
     }
     if (item + 2 * G < cfg.nitems) pipe::bar_arrive(pipe::kBarEmpty0 + buf, NT);
   }
-  if (XAX && bulk && threadIdx.x == 0) pipe::bulk_wait0();
+  if (XAX && bulk && warp == 0) pipe::bulk_wait0();
 }
 
 }  // namespace sweep
