@@ -128,10 +128,13 @@ sgm_status sgm_workspace_bytes(sgm_plan plan, size_t* bytes);
    (check once with sgm_check_source), NULL = no source.  j_amp: device, length n_steps,
    s_k multiplying j^ at step k (the paper's separable-in-time source); NULL -> 1.0.
    On exit d, e are at t_n + n_steps dt and b, h at t_{n+1/2} + n_steps dt.
-   Launches: per step 8 kernels (4 per half step: update, z, y and x sweeps) with programmatic
-   dependent launch.  On a non-default stream and with j_amp == NULL the launch sequence of one
+   Launches: per step sgm_plan_kernels_per_step kernels (separable Hodge stars with the reduced
+   schedule: 7 -- an update and three sweeps for the eps half, an update and two sweeps for the mu
+   half, independent sweeps concurrently on a plan-owned stream) with programmatic dependent
+   launch.  On a non-default stream, with j_amp == NULL or n_steps == 1, the launch sequence of one
    step is captured into a CUDA graph on first use and replayed for later calls with identical
-   arguments (the plan keeps one graph; set_material invalidates it; SGM_GRAPH=0 disables). */
+   arguments (pointers, dt; a replay reads the current value of j_amp[0]) -- the plan keeps one
+   graph; set_material invalidates it; SGM_GRAPH=0 disables. */
 sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h,
                     const double* j_hat, const double* j_amp, double dt, int n_steps,
                     void* workspace, size_t ws_bytes, void* stream);

@@ -731,9 +731,11 @@ sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h, c
   // n_steps times (removes the per-kernel host enqueue cost, which dominates on small meshes).
   // Used when every step has identical arguments (no per-step source amplitudes), not on the
   // legacy default stream (capture is not allowed there) and not while profiling records events.
-  const bool use_graph = !P->profiling && stream != nullptr && P->graph_enabled && j_amp == nullptr;
+  // With per-step amplitudes the captured step reads s from j_amp[0]: replayable for n_steps == 1
+  // (a caller that refreshes the same device scalar every step, as a simulation loop does).
+  const bool use_graph = !P->profiling && stream != nullptr && P->graph_enabled && (j_amp == nullptr || n_steps == 1);
   if (use_graph) {
-    const GraphKey key{d, e, b, h, j_hat, nullptr, dt, 1, workspace};
+    const GraphKey key{d, e, b, h, j_hat, j_amp, dt, 1, workspace};
     if (!(P->graph_exec && P->graph_key == key)) {
       if (P->graph_exec) {
         cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec));
@@ -742,7 +744,7 @@ sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h, c
       cudaGraph_t graph = nullptr;
       if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
         return cuda_check(P, "sgm_step: begin capture");
-      step_once(*P, d, e, b, h, j_hat, nullptr, dt, w, st);
+      step_once(*P, d, e, b, h, j_hat, j_amp, dt, w, st);
       if (cudaStreamEndCapture(st, &graph) != cudaSuccess) return cuda_check(P, "sgm_step: end capture");
       cudaGraphExec_t exec = nullptr;
       const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);

@@ -413,3 +413,28 @@ def test_reduced_and_full_schedules(p, n, nodiag, monkeypatch):
     out = _run_gpu(pl, st, dt, 30)
     for a, b in zip(out, tb.run(*st, dt, 30)):
         assert rel(a, b) < 1e-10
+
+
+def test_graph_replay_with_per_step_amplitude():
+    """A simulation loop that refreshes one device scalar s_k and calls sgm_step(n_steps=1, j_amp=s)
+    on a non-default stream: the captured step is replayed and reads the current s every step."""
+    p, n = 3, (7, 6, 8)
+    pl = S.Plan(n, p)
+    tb = TierB(p, n)
+    st = _state(tb, 23)
+    a = np.random.default_rng(24).standard_normal(tb.N_h)
+    jhat = forms.join(curl_dual(tb.split_h(a)))
+    amps = np.sin(0.4 * np.arange(12)) + 0.5
+    dt = 0.3 * W.cfl_dt_max(tb)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        d, e, b, h = (dev(x) for x in st)
+        jh = dev(jhat)
+        sbuf = torch.empty(1, dtype=torch.float64, device="cuda")
+        for k in range(len(amps)):
+            sbuf.fill_(float(amps[k]))
+            pl.step(d, e, b, h, dt, 1, j_hat=jh, j_amp=sbuf, stream=s)
+        out = [host(x) for x in (d, e, b, h)]
+    ref = tb.run(*st, dt, len(amps), jhat, amps)
+    for x, y in zip(out, ref):
+        assert rel(x, y) < 1e-10
