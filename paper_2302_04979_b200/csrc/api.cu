@@ -192,10 +192,15 @@ void sweep_pass_list(const Plan& P, int kind, const PassComp* pc, int n, cudaStr
   a.axis = pc[0].axis;
   a.band = 1;
   a.solve = 1;
-  a.tabs[0] = table(P, pc[0].axis, pc[0].op);
+  // axes with the same element count have bitwise identical tables: use the first axis's copy so a
+  // launch mixing such axes stages one table (shared memory decides whether two lines per thread fit)
+  auto tab_of = [&](const PassComp& q) {
+    return table(P, P.n[q.axis] == P.n[pc[0].axis] ? pc[0].axis : q.axis, q.op);
+  };
+  a.tabs[0] = tab_of(pc[0]);
   a.tabs[1] = nullptr;
   for (int i = 1; i < n; ++i) {
-    const double* t = table(P, pc[i].axis, pc[i].op);
+    const double* t = tab_of(pc[i]);
     if (t != a.tabs[0]) a.tabs[1] = t;
   }
   a.tab_rows = P.rpad[pc[0].axis];
@@ -212,7 +217,7 @@ void sweep_pass_list(const Plan& P, int kind, const PassComp* pc, int n, cudaStr
     comp_shape(P, kind, q.c, C.ext);
     C.in = const_cast<double*>(q.in);
     C.out = q.out;
-    C.tab = table(P, axis, q.op);
+    C.tab = tab_of(q);
     C.tslot = (a.tabs[1] && C.tab == a.tabs[1]) ? 1 : 0;
     C.axis = axis;
     C.scale = q.scale;

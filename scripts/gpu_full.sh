@@ -11,6 +11,7 @@ python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$TA
 for cfg in "--p 2 --n 160" "--p 4 --n 128" "--p 3 --n 64" "--config c4" "--config c3"; do
   python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e $cfg >> gpurun_out/bench_sweep_$TAG.jsonl 2>> gpurun_out/bench_sweep_$TAG.err
 done
+python scripts/c5_sweep.py --out gpurun_out/c5_sweep_$TAG.jsonl > gpurun_out/c5_sweep_$TAG.log 2>&1
 ARGS="--steps 3 --warmup 3 --no-cpu --no-e2e"
 python bench.py $ARGS > gpurun_out/plain_$TAG.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$TAG.csv \

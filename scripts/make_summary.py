@@ -90,6 +90,24 @@ def main(tag):
         rr = d["roofline"]
         L.append(f"| {d['config']['workload']} | {d['value']:.3g} | {d['ms_per_step']:.3f} | {rr['kernel']} "
                  f"{rr['achieved']:.3g} {rr['unit']} ({rr['frac']:.2f}) | {rr.get('step_frac', 0):.2f} |")
+    c5 = os.path.join(G, f"c5_sweep_{tag}.jsonl")
+    if os.path.exists(c5):
+        shutil.copy(c5, os.path.join(PR, "r1_c5_sweep.jsonl"))
+    c5p = os.path.join(PR, "r1_c5_sweep.jsonl")
+    if os.path.exists(c5p):
+        L.append("\n### configs[4]: Kronecker wedge solve and full step over p and n (`scripts/c5_sweep.py`, `r1_c5_sweep.jsonl`)\n")
+        L.append("K1 solve = `sgm_kron_solve` (three sweeps; 48 B/element algorithmic, L2 flushed before each rep); "
+                 "step = `sgm_step` graph replay. Fractions of the measured HBM peak.\n")
+        L.append("| p | n_el | K1 solve µs | solve GB/s (frac) | step µs | DOF-updates/s | step GB/s (frac) |")
+        L.append("|---|---|---|---|---|---|---|")
+        for l in open(c5p):
+            d = json.loads(l)
+            k, s_ = d["kron_solve"], d["step"]
+            L.append(f"| {d['p']} | {d['n_el']} | {k['us']:.1f} | {k['gbs']:.0f} ({k['frac']:.2f}) | {s_['us']:.1f} | "
+                     f"{s_['dof_updates_per_s']:.3g} | {s_['gbs']:.0f} ({s_['frac']:.2f}) |")
+        L.append("\nAt 32³ and 64³ the working set sits in L2 and the kernels are launch/latency bound; at 160³ with "
+                 "p ≥ 3 the strided sweeps have only two producer warps (14 consumer segments fill the 16-warp CTA) "
+                 "and p = 4 no longer fits two lines per thread in shared memory.")
     L.append("\nC4/C3 report the general Hodge against the fp64 peak (`bound: alu`, 37.2 TFLOP/s, DESIGN.md §6); its "
              "HBM view is in each line's `roofline.hbm_view`.\n")
     L.append("## Per-kernel ncu, one step of C5 p=3 128³ (serialised replay: compare shares, not absolutes)\n")
