@@ -5,7 +5,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsgm.so")
-SOURCES = ["host_setup.cpp", "kernels.cu", "api.cu"]
+SOURCES = ["host_setup.cpp", "kernels.cu", "hodge.cu", "sweep_p2.cu", "sweep_p3.cu", "sweep_p4.cu", "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC,-fopenmp", "-shared", "-lgomp"]
@@ -21,9 +21,27 @@ def needs_build():
 
 
 def build(force=False, verbose=False):
+    """Compile every translation unit to an object in parallel (the sweep instantiations are split
+    per degree), then link the shared library."""
     if not force and not needs_build():
         return LIB
-    cmd = [NVCC] + FLAGS + [os.path.join(CSRC, s) for s in SOURCES] + ["-o", LIB + ".tmp"]
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = os.path.join(HERE, "_obj")
+    os.makedirs(objdir, exist_ok=True)
+    cflags = [f for f in FLAGS if f not in ("-shared", "-lgomp")]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, src + ".o")
+        cmd = [NVCC] + cflags + ["-c", os.path.join(CSRC, src), "-o", obj]
+        if verbose:
+            print(" ".join(cmd))
+        subprocess.run(cmd, check=True, cwd=CSRC)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
+    cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xcompiler", "-fopenmp", "-lgomp"] + objs \
+        + ["-o", LIB + ".tmp"]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True, cwd=CSRC)

@@ -1,0 +1,222 @@
+// General (non-separable) Hodge launchers: brick-tiled sum factorisation (hodge_brick.cuh), the
+// warp-per-pencil kernel (hodge_kernel.cuh, SGM_HODGE_PENCIL=1) and a generic CTA-per-element
+// kernel for quadrature rules other than p+1 points.
+#include <cuda_runtime.h>
+
+#include "hodge_brick.cuh"
+#include "hodge_kernel.cuh"
+#include "kernels.cuh"
+#include "launch_util.cuh"
+
+namespace sgm {
+namespace {
+
+// ---- general Hodge: one CTA per element, Q^3 threads, sum factorisation ------------------
+// y_c[i] += sum_q phi_{c,i}(x_q) sum_c' W_{cc'}(q) sum_j phi_{c',j}(x_q) x_{c'}[j]
+template <int P>
+__global__ void hodge_general_kernel(const __grid_constant__ HodgeArgs A) {
+  constexpr int NL = P + 1;
+  const int Q = A.Q;
+  const int nx = A.nel[0], ny = A.nel[1];
+  const long e = blockIdx.x;
+  const int ex = int(e % nx), ey = int((e / nx) % ny), ez = int(e / (long(nx) * ny));
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int M = (NL > Q ? NL : Q);
+  extern __shared__ double sm[];
+  double* U = sm;                   // [3][M^3]
+  double* V = sm + 3 * M * M * M;   // [3][M^3]
+  const int MM = M * M * M;
+  // basis pointers per comp per axis
+  const double* B[3][3];
+  int f[3][3];
+  for (int c = 0; c < 3; ++c)
+    for (int a = 0; a < 3; ++a) {
+      int role = (a == c) ? 0 : 1;
+      int el = (a == 0) ? ex : (a == 1 ? ey : ez);
+      B[c][a] = A.basis + A.basis_off[a][role] + size_t(el) * Q * NL;
+      f[c][a] = A.first[A.first_off[a][role] + el];
+    }
+  // load local coefficient boxes U0[c][k][j][i]
+  for (int idx = t; idx < 3 * NL * NL * NL; idx += nt) {
+    int c = idx / (NL * NL * NL), r = idx % (NL * NL * NL);
+    int i = r % NL, j = (r / NL) % NL, k = r / (NL * NL);
+    int gi = f[c][0] + i, gj = f[c][1] + j, gk = f[c][2] + k;
+    double v = 0.0;
+    if (gi >= 0 && gi < A.ext[c][0] && gj >= 0 && gj < A.ext[c][1] && gk >= 0 && gk < A.ext[c][2])
+      v = __ldg(A.x[c] + gi + long(A.ext[c][0]) * (gj + long(A.ext[c][1]) * gk));
+    U[c * MM + (k * NL + j) * NL + i] = v;
+  }
+  __syncthreads();
+  // x: V[c][k][j][qx] = sum_i Bx[qx][i] U[c][k][j][i]
+  for (int idx = t; idx < 3 * NL * NL * Q; idx += nt) {
+    int c = idx / (NL * NL * Q), r = idx % (NL * NL * Q);
+    int qx = r % Q, jk = r / Q;
+    double s = 0.0;
+#pragma unroll
+    for (int i = 0; i < NL; ++i) s = fma(__ldg(B[c][0] + qx * NL + i), U[c * MM + jk * NL + i], s);
+    V[c * MM + jk * Q + qx] = s;
+  }
+  __syncthreads();
+  // y: U[c][k][qy][qx] = sum_j By[qy][j] V[c][k][j][qx]
+  for (int idx = t; idx < 3 * NL * Q * Q; idx += nt) {
+    int c = idx / (NL * Q * Q), r = idx % (NL * Q * Q);
+    int qx = r % Q, qy = (r / Q) % Q, k = r / (Q * Q);
+    double s = 0.0;
+#pragma unroll
+    for (int j = 0; j < NL; ++j) s = fma(__ldg(B[c][1] + qy * NL + j), V[c * MM + (k * NL + j) * Q + qx], s);
+    U[c * MM + (k * Q + qy) * Q + qx] = s;
+  }
+  __syncthreads();
+  // z + weights: one thread per quadrature point
+  const long qbase = e * long(Q) * Q * Q;
+  for (int q = t; q < Q * Q * Q; q += nt) {
+    int qx = q % Q, qy = (q / Q) % Q, qz = q / (Q * Q);
+    double u[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < NL; ++k) s = fma(__ldg(B[c][2] + qz * NL + k), U[c * MM + (k * Q + qy) * Q + qx], s);
+      u[c] = s;
+    }
+    double v[3];
+    if (A.full) {
+      const double* w = A.W + (qbase + q) * 6;
+      double wxx = __ldg(w), wyy = __ldg(w + 1), wzz = __ldg(w + 2), wxy = __ldg(w + 3), wxz = __ldg(w + 4),
+             wyz = __ldg(w + 5);
+      v[0] = wxx * u[0] + wxy * u[1] + wxz * u[2];
+      v[1] = wxy * u[0] + wyy * u[1] + wyz * u[2];
+      v[2] = wxz * u[0] + wyz * u[1] + wzz * u[2];
+    } else {
+      double w = __ldg(A.W + qbase + q);
+      v[0] = A.scale[0] * w * u[0];
+      v[1] = A.scale[1] * w * u[1];
+      v[2] = A.scale[2] * w * u[2];
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) V[c * MM + q] = v[c];
+  }
+  __syncthreads();
+  // test z: U[c][k][qy][qx] = sum_qz Bz[qz][k] V[c][qz][qy][qx]
+  for (int idx = t; idx < 3 * NL * Q * Q; idx += nt) {
+    int c = idx / (NL * Q * Q), r = idx % (NL * Q * Q);
+    int qx = r % Q, qy = (r / Q) % Q, k = r / (Q * Q);
+    double s = 0.0;
+    for (int qz = 0; qz < Q; ++qz) s = fma(__ldg(B[c][2] + qz * NL + k), V[c * MM + (qz * Q + qy) * Q + qx], s);
+    U[c * MM + (k * Q + qy) * Q + qx] = s;
+  }
+  __syncthreads();
+  // test y: V[c][k][j][qx] = sum_qy By[qy][j] U[c][k][qy][qx]
+  for (int idx = t; idx < 3 * NL * NL * Q; idx += nt) {
+    int c = idx / (NL * NL * Q), r = idx % (NL * NL * Q);
+    int qx = r % Q, j = (r / Q) % NL, k = r / (Q * NL);
+    double s = 0.0;
+    for (int qy = 0; qy < Q; ++qy) s = fma(__ldg(B[c][1] + qy * NL + j), U[c * MM + (k * Q + qy) * Q + qx], s);
+    V[c * MM + (k * NL + j) * Q + qx] = s;
+  }
+  __syncthreads();
+  // test x + scatter-add
+  for (int idx = t; idx < 3 * NL * NL * NL; idx += nt) {
+    int c = idx / (NL * NL * NL), r = idx % (NL * NL * NL);
+    int i = r % NL, j = (r / NL) % NL, k = r / (NL * NL);
+    int gi = f[c][0] + i, gj = f[c][1] + j, gk = f[c][2] + k;
+    if (gi < 0 || gi >= A.ext[c][0] || gj < 0 || gj >= A.ext[c][1] || gk < 0 || gk >= A.ext[c][2]) continue;
+    double s = 0.0;
+    for (int qx = 0; qx < Q; ++qx) s = fma(__ldg(B[c][0] + qx * NL + i), V[c * MM + (k * NL + j) * Q + qx], s);
+    atomicAdd(A.y[c] + gi + long(A.ext[c][0]) * (gj + long(A.ext[c][1]) * gk), s);
+  }
+}
+
+template <int P, int Q, bool DUAL, bool FULL>
+void launch_hodge_pencil(const HodgeArgs& a, cudaStream_t st) {
+  constexpr int NL = P + 1, XB = hodge::max_box<P, DUAL>(), VB = Q * NL, CB = (P + 1) * Q * Q,
+                TB = (P + 1) * (P + 1) * Q;
+  const size_t smem = size_t(8) * (6 * XB + 9 * VB + CB + TB) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(hodge::hodge_pencil_kernel<P, Q, DUAL, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    attr = true;
+  }
+  const long npen = long(a.nel[0]) * a.nel[1];
+  long grid = (npen + 7) / 8;
+  const long cap = 16L * sm_count();
+  if (grid > cap) grid = cap;
+  hodge::hodge_pencil_kernel<P, Q, DUAL, FULL><<<unsigned(grid), 256, smem, st>>>(a);
+}
+
+template <int P, int Q, bool DUAL, bool FULL>
+void launch_hodge_brick(const HodgeArgs& a, cudaStream_t st) {
+  constexpr int E = 4;
+  using L = brick::Layout<P, Q, DUAL, E>;
+  const size_t smem = size_t(L::template total<FULL>()) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(brick::hodge_brick_kernel<P, Q, DUAL, FULL, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(smem));
+    attr = true;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, brick::hodge_brick_kernel<P, Q, DUAL, FULL, E>, 256, smem);
+  if (per_sm < 1) per_sm = 1;
+  const long slots = long(per_sm) * sm_count();
+  const long bricks = long((a.nel[0] + E - 1) / E) * ((a.nel[1] + E - 1) / E);
+  // z chunks: about four work items per resident CTA, at least 4 element layers per chunk
+  long bzn = (4 * slots + bricks - 1) / bricks;
+  int zchunk = int((a.nel[2] + bzn - 1) / bzn);
+  if (zchunk < 4) zchunk = 4;
+  if (const int zc = env_int("SGM_HODGE_ZCHUNK", 0)) zchunk = zc;
+  const long items = bricks * ((a.nel[2] + zchunk - 1) / zchunk);
+  const long grid = items < slots ? items : slots;
+  brick::hodge_brick_kernel<P, Q, DUAL, FULL, E><<<unsigned(grid), 256, smem, st>>>(a, zchunk);
+}
+
+template <int P, int Q>
+void launch_hodge2(const HodgeArgs& a, cudaStream_t st) {
+  if (env_int("SGM_HODGE_PENCIL", 0) == 0) {
+    if (a.dual) {
+      if (a.full) launch_hodge_brick<P, Q, true, true>(a, st);
+      else launch_hodge_brick<P, Q, true, false>(a, st);
+    } else {
+      if (a.full) launch_hodge_brick<P, Q, false, true>(a, st);
+      else launch_hodge_brick<P, Q, false, false>(a, st);
+    }
+    return;
+  }
+  if (a.dual) {
+    if (a.full) launch_hodge_pencil<P, Q, true, true>(a, st);
+    else launch_hodge_pencil<P, Q, true, false>(a, st);
+  } else {
+    if (a.full) launch_hodge_pencil<P, Q, false, true>(a, st);
+    else launch_hodge_pencil<P, Q, false, false>(a, st);
+  }
+}
+
+}  // namespace
+
+void launch_hodge_general(int p, const HodgeArgs& a, cudaStream_t st) {
+  // z-pencil warp kernel (hodge_kernel.cuh) for the default rule Q = p + 1; the generic
+  // CTA-per-element kernel for larger rules (quad_points > p + 1)
+  if (a.Q == p + 1) {
+    switch (p) {
+      case 2: launch_hodge2<2, 3>(a, st); return;
+      case 3: launch_hodge2<3, 4>(a, st); return;
+      case 4: launch_hodge2<4, 5>(a, st); return;
+      default: break;
+    }
+  }
+  long nel = long(a.nel[0]) * a.nel[1] * a.nel[2];
+  int Q = a.Q;
+  int M = (p + 1 > Q) ? p + 1 : Q;
+  size_t smem = size_t(6) * M * M * M * sizeof(double);
+  int threads = Q * Q * Q;
+  if (threads < 32) threads = 32;
+  switch (p) {
+    case 2: hodge_general_kernel<2><<<unsigned(nel), threads, smem, st>>>(a); break;
+    case 3: hodge_general_kernel<3><<<unsigned(nel), threads, smem, st>>>(a); break;
+    case 4: hodge_general_kernel<4><<<unsigned(nel), threads, smem, st>>>(a); break;
+    default: break;
+  }
+}
+
+}  // namespace sgm

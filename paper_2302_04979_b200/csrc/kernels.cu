@@ -14,9 +14,8 @@
 
 #include "kernels.cuh"
 #include "seg_sweep.cuh"
-#include "sweep_kernel.cuh"
-#include "hodge_kernel.cuh"
-#include "hodge_brick.cuh"
+#include "launch_util.cuh"
+#include "pipe_sweep.cuh"
 
 #include <cstdint>
 #include <cstdlib>
@@ -302,299 +301,15 @@ __global__ void finalize_max_kernel(const double* partials, int n_each, int ngro
   }
 }
 
-// ---- general Hodge: one CTA per element, Q^3 threads, sum factorisation ------------------
-// y_c[i] += sum_q phi_{c,i}(x_q) sum_c' W_{cc'}(q) sum_j phi_{c',j}(x_q) x_{c'}[j]
-template <int P>
-__global__ void hodge_general_kernel(const __grid_constant__ HodgeArgs A) {
-  constexpr int NL = P + 1;
-  const int Q = A.Q;
-  const int nx = A.nel[0], ny = A.nel[1];
-  const long e = blockIdx.x;
-  const int ex = int(e % nx), ey = int((e / nx) % ny), ez = int(e / (long(nx) * ny));
-  const int t = threadIdx.x, nt = blockDim.x;
-  const int M = (NL > Q ? NL : Q);
-  extern __shared__ double sm[];
-  double* U = sm;                   // [3][M^3]
-  double* V = sm + 3 * M * M * M;   // [3][M^3]
-  const int MM = M * M * M;
-  // basis pointers per comp per axis
-  const double* B[3][3];
-  int f[3][3];
-  for (int c = 0; c < 3; ++c)
-    for (int a = 0; a < 3; ++a) {
-      int role = (a == c) ? 0 : 1;
-      int el = (a == 0) ? ex : (a == 1 ? ey : ez);
-      B[c][a] = A.basis + A.basis_off[a][role] + size_t(el) * Q * NL;
-      f[c][a] = A.first[A.first_off[a][role] + el];
-    }
-  // load local coefficient boxes U0[c][k][j][i]
-  for (int idx = t; idx < 3 * NL * NL * NL; idx += nt) {
-    int c = idx / (NL * NL * NL), r = idx % (NL * NL * NL);
-    int i = r % NL, j = (r / NL) % NL, k = r / (NL * NL);
-    int gi = f[c][0] + i, gj = f[c][1] + j, gk = f[c][2] + k;
-    double v = 0.0;
-    if (gi >= 0 && gi < A.ext[c][0] && gj >= 0 && gj < A.ext[c][1] && gk >= 0 && gk < A.ext[c][2])
-      v = __ldg(A.x[c] + gi + long(A.ext[c][0]) * (gj + long(A.ext[c][1]) * gk));
-    U[c * MM + (k * NL + j) * NL + i] = v;
-  }
-  __syncthreads();
-  // x: V[c][k][j][qx] = sum_i Bx[qx][i] U[c][k][j][i]
-  for (int idx = t; idx < 3 * NL * NL * Q; idx += nt) {
-    int c = idx / (NL * NL * Q), r = idx % (NL * NL * Q);
-    int qx = r % Q, jk = r / Q;
-    double s = 0.0;
-#pragma unroll
-    for (int i = 0; i < NL; ++i) s = fma(__ldg(B[c][0] + qx * NL + i), U[c * MM + jk * NL + i], s);
-    V[c * MM + jk * Q + qx] = s;
-  }
-  __syncthreads();
-  // y: U[c][k][qy][qx] = sum_j By[qy][j] V[c][k][j][qx]
-  for (int idx = t; idx < 3 * NL * Q * Q; idx += nt) {
-    int c = idx / (NL * Q * Q), r = idx % (NL * Q * Q);
-    int qx = r % Q, qy = (r / Q) % Q, k = r / (Q * Q);
-    double s = 0.0;
-#pragma unroll
-    for (int j = 0; j < NL; ++j) s = fma(__ldg(B[c][1] + qy * NL + j), V[c * MM + (k * NL + j) * Q + qx], s);
-    U[c * MM + (k * Q + qy) * Q + qx] = s;
-  }
-  __syncthreads();
-  // z + weights: one thread per quadrature point
-  const long qbase = e * long(Q) * Q * Q;
-  for (int q = t; q < Q * Q * Q; q += nt) {
-    int qx = q % Q, qy = (q / Q) % Q, qz = q / (Q * Q);
-    double u[3];
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      double s = 0.0;
-#pragma unroll
-      for (int k = 0; k < NL; ++k) s = fma(__ldg(B[c][2] + qz * NL + k), U[c * MM + (k * Q + qy) * Q + qx], s);
-      u[c] = s;
-    }
-    double v[3];
-    if (A.full) {
-      const double* w = A.W + (qbase + q) * 6;
-      double wxx = __ldg(w), wyy = __ldg(w + 1), wzz = __ldg(w + 2), wxy = __ldg(w + 3), wxz = __ldg(w + 4),
-             wyz = __ldg(w + 5);
-      v[0] = wxx * u[0] + wxy * u[1] + wxz * u[2];
-      v[1] = wxy * u[0] + wyy * u[1] + wyz * u[2];
-      v[2] = wxz * u[0] + wyz * u[1] + wzz * u[2];
-    } else {
-      double w = __ldg(A.W + qbase + q);
-      v[0] = A.scale[0] * w * u[0];
-      v[1] = A.scale[1] * w * u[1];
-      v[2] = A.scale[2] * w * u[2];
-    }
-#pragma unroll
-    for (int c = 0; c < 3; ++c) V[c * MM + q] = v[c];
-  }
-  __syncthreads();
-  // test z: U[c][k][qy][qx] = sum_qz Bz[qz][k] V[c][qz][qy][qx]
-  for (int idx = t; idx < 3 * NL * Q * Q; idx += nt) {
-    int c = idx / (NL * Q * Q), r = idx % (NL * Q * Q);
-    int qx = r % Q, qy = (r / Q) % Q, k = r / (Q * Q);
-    double s = 0.0;
-    for (int qz = 0; qz < Q; ++qz) s = fma(__ldg(B[c][2] + qz * NL + k), V[c * MM + (qz * Q + qy) * Q + qx], s);
-    U[c * MM + (k * Q + qy) * Q + qx] = s;
-  }
-  __syncthreads();
-  // test y: V[c][k][j][qx] = sum_qy By[qy][j] U[c][k][qy][qx]
-  for (int idx = t; idx < 3 * NL * NL * Q; idx += nt) {
-    int c = idx / (NL * NL * Q), r = idx % (NL * NL * Q);
-    int qx = r % Q, j = (r / Q) % NL, k = r / (Q * NL);
-    double s = 0.0;
-    for (int qy = 0; qy < Q; ++qy) s = fma(__ldg(B[c][1] + qy * NL + j), U[c * MM + (k * Q + qy) * Q + qx], s);
-    V[c * MM + (k * NL + j) * Q + qx] = s;
-  }
-  __syncthreads();
-  // test x + scatter-add
-  for (int idx = t; idx < 3 * NL * NL * NL; idx += nt) {
-    int c = idx / (NL * NL * NL), r = idx % (NL * NL * NL);
-    int i = r % NL, j = (r / NL) % NL, k = r / (NL * NL);
-    int gi = f[c][0] + i, gj = f[c][1] + j, gk = f[c][2] + k;
-    if (gi < 0 || gi >= A.ext[c][0] || gj < 0 || gj >= A.ext[c][1] || gk < 0 || gk >= A.ext[c][2]) continue;
-    double s = 0.0;
-    for (int qx = 0; qx < Q; ++qx) s = fma(__ldg(B[c][0] + qx * NL + i), V[c * MM + (k * NL + j) * Q + qx], s);
-    atomicAdd(A.y[c] + gi + long(A.ext[c][0]) * (gj + long(A.ext[c][1]) * gk), s);
-  }
-}
-
-int env_int(const char* name, int dflt) {
-  const char* s = getenv(name);
-  return s ? atoi(s) : dflt;
-}
-
-// Launch with programmatic stream serialization (PDL): the kernel may be scheduled while the
-// previous kernel in the stream drains; it calls griddepcontrol.wait before touching its inputs.
-template <typename... KArgs, typename... Args>
-void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
-                Args&&... args) {
-  cudaLaunchConfig_t lc;
-  std::memset(&lc, 0, sizeof(lc));
-  lc.gridDim = dim3(grid);
-  lc.blockDim = dim3(block);
-  lc.dynamicSmemBytes = smem;
-  lc.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = env_int("SGM_PDL", 1) ? 1 : 0;
-  lc.attrs = at;
-  lc.numAttrs = 1;
-  cudaLaunchKernelEx(&lc, kernel, std::forward<Args>(args)...);
-}
-
-int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
-
-
-template <int P, int HB, int SEG, int LPT, int MODE, int OPS>
-bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
-  using sweep::Cfg;
-  Cfg cfg;
-  std::memset(&cfg, 0, sizeof(cfg));
-  constexpr int TW = 32 * LPT;
-  int Lmax = 0;
-  for (int c = 0; c < 3; ++c) {
-    if (c >= a.ncomp) continue;
-    const SweepComp& C = a.comp[c];
-    sweep::CompGeom& g = cfg.g[c];
-    const int X = C.ext[0], Y = C.ext[1], Z = C.ext[2];
-    // per-component axis (strided passes may mix y- and z-lines of different components)
-    const int ax = (MODE != 3 && C.axis > 0) ? C.axis : a.axis;
-    g.L = C.ext[ax];
-    g.magic = 0xffffffffu / unsigned(X);
-    g.nlines = X * Y * Z / g.L;
-    g.X = X;
-    g.rowlen = X;
-    g.gs = (ax == 0) ? 1 : (ax == 1 ? X : X * Y);
-    g.os = (ax == 1) ? X * Y : X;  // transverse index l / X: z (y pass) or y (z pass)
-    g.TD = (ax == 0) ? Y : X;      // transverse coordinates of line l: (l % TD, l / TD)
-    g.tmagic = 0xffffffffu / unsigned(g.TD);
-    cfg.tiles[c] = (g.nlines + TW - 1) / TW;
-    cfg.nitems += cfg.tiles[c];
-    Lmax = g.L > Lmax ? g.L : Lmax;
-  }
-  cfg.NC = (Lmax + SEG - 1) / SEG;
-  cfg.rows = cfg.NC * SEG + P;
-  // x axis: a tile of whole lines is one contiguous range -> one bulk copy in and one out (TMA
-  // engine), if the component bases are 16-byte aligned and the component has an even size.
-  // (Strided tiles are many small row runs: measured slower on the bulk engine than cp.async.)
-  bool bulk = (MODE == 3) && env_int("SGM_BULK", 1) != 0;
-  for (int c = 0; c < a.ncomp && bulk; ++c) {
-    const SweepComp& C = a.comp[c];
-    if ((reinterpret_cast<uintptr_t>(C.in) & 15) || (reinterpret_cast<uintptr_t>(C.out) & 15)) bulk = false;
-    if ((long(C.ext[0]) * C.ext[1] * C.ext[2]) & 1) bulk = false;
-  }
-  cfg.bulk = bulk ? 1 : 0;
-  if (bulk) cfg.NP = 1;
-  else cfg.NP = env_int("SGM_NP", 4);
-  if (cfg.NP < 1) cfg.NP = 1;
-  if (cfg.NC + cfg.NP > 16) cfg.NP = 16 - cfg.NC;
-  if (cfg.NP < 1) return false;
-  if (MODE == 3) {
-    // bulk: a whole-tile copy keeps pitch = line length; a multiple of 4 would put the consumers'
-    // per-lane line walks on few banks (all lanes on one bank pair at L % 16 == 0), so such lines
-    // are copied one by one into pitch L + 2 (16-byte aligned rows, 4-way at worst)
-    int bp_max = 0;
-    for (int c = 0; c < a.ncomp; ++c) {
-      sweep::CompGeom& g = cfg.g[c];
-      g.lbulk = (bulk && (g.L % 4) == 0 && env_int("SGM_LINE_BULK", 1)) ? 1 : 0;
-      g.bpitch = g.lbulk ? g.L + 2 : g.L;
-      bp_max = g.bpitch > bp_max ? g.bpitch : bp_max;
-    }
-    cfg.pitch = bulk ? bp_max : (cfg.rows | 1);
-    cfg.W = 0;
-    cfg.slab = TW * cfg.pitch + cfg.rows + 2;
-  } else {
-    cfg.pitch = 0;
-    cfg.W = TW;
-    cfg.slab = cfg.W * cfg.rows;
-  }
-  cfg.slab = (cfg.slab + 1) & ~1;  // keep every slab 16-byte aligned
-  cfg.ntabs = (a.tabs[1] != nullptr && a.tabs[1] != a.tabs[0]) ? 2 : 1;
-  cfg.tab_dbl = a.tab_rows * RowLayout<P>::RS;
-  cfg.dbg = env_int("SGM_PIPE_DBG", 0);
-  cfg.reverse = env_int("SGM_SNAKE", 1) ? a.reverse : 0;
-  constexpr int M = P - 1;
-  const size_t smem = (size_t(cfg.ntabs) * cfg.tab_dbl + size_t(2) * cfg.slab + size_t(2) * cfg.NC * M * TW + 4) *
-                      sizeof(double);
-  if (smem > 227 * 1024) return false;
-  const int NT = (cfg.NC + cfg.NP) * 32;
-  static int attr_done = 0;
-  if (!attr_done) {
-    cudaFuncSetAttribute(sweep::sweep_kernel<P, HB, SEG, LPT, MODE, OPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         227 * 1024);
-    attr_done = 1;
-  }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep::sweep_kernel<P, HB, SEG, LPT, MODE, OPS>, NT, smem);
-  if (per_sm < 1) per_sm = 1;
-  const int cap = env_int("SGM_CTAS_PER_SM", 0);
-  if (cap > 0 && cap < per_sm) per_sm = cap;
-  long grid = long(per_sm) * sm_count();
-  if (a.share_n > 0) grid = (grid * a.share_k + a.share_n / 2) / a.share_n;
-  if (grid < 1) grid = 1;
-  if (grid > cfg.nitems) grid = cfg.nitems;
-  if (grid < 1) grid = 1;
-  launch_pdl(sweep::sweep_kernel<P, HB, SEG, LPT, MODE, OPS>, unsigned(grid), unsigned(NT), smem, st, a, cfg);
-  return true;
-}
-
-template <int P, int HB, int SEG, int MODE, int OPS>
-void launch_sweep_m(const SweepArgs& a, cudaStream_t st) {
-  // two lines per thread when the register budget allows (SEG <= 17) and the slabs fit
-  if constexpr (SEG <= 17) {
-    if (env_int("SGM_LPT", 2) == 2 && launch_sweep_t<P, HB, SEG, 2, MODE, OPS>(a, st)) return;
-  }
-  launch_sweep_t<P, HB, SEG, 1, MODE, OPS>(a, st);
-}
-
-template <int P, int SEG, int MODE>
-void launch_sweep_o(const SweepArgs& a, cudaStream_t st) {
-  // band half-width: P - 1 for the eps-side Grams and the pairing factors, P for the mu-side Gram
-  if (a.band && a.solve) {
-    if (a.band_hw >= P) launch_sweep_m<P, P, SEG, MODE, 3>(a, st);
-    else if (P >= 3 && a.band_hw <= P - 2) launch_sweep_m<P, (P >= 3 ? P - 2 : 1), SEG, MODE, 3>(a, st);  // eps Gamma_C^{p-2}
-    else launch_sweep_m<P, P - 1, SEG, MODE, 3>(a, st);
-  } else if (a.solve) {
-    launch_sweep_m<P, P - 1, SEG, MODE, 2>(a, st);
-  } else {
-    if (a.band_hw >= P) launch_sweep_m<P, P, SEG, MODE, 1>(a, st);
-    else launch_sweep_m<P, P - 1, SEG, MODE, 1>(a, st);
-  }
-}
-
-template <int P, int SEG>
-void launch_sweep_s(const SweepArgs& a, cudaStream_t st) {
-  if (a.axis == 0) launch_sweep_o<P, SEG, 3>(a, st);
-  else launch_sweep_o<P, SEG, 0>(a, st);
-}
-
-template <int P>
-void launch_sweep_p(int seg, const SweepArgs& a, cudaStream_t st) {
-  switch (seg) {
-    case 12: launch_sweep_s<P, 12>(a, st); break;
-    case 17: launch_sweep_s<P, 17>(a, st); break;
-    default: launch_sweep_s<P, 28>(a, st); break;
-  }
-}
-
 }  // namespace
 
 int partial_blocks() { return kRedBlocks; }
 
 void launch_sweep(int p, int seg, const SweepArgs& a, cudaStream_t st) {
   switch (p) {
-    case 2: launch_sweep_p<2>(seg, a, st); break;
-    case 3: launch_sweep_p<3>(seg, a, st); break;
-    case 4: launch_sweep_p<4>(seg, a, st); break;
+    case 2: launch_sweep_p2(seg, a, st); break;
+    case 3: launch_sweep_p3(seg, a, st); break;
+    case 4: launch_sweep_p4(seg, a, st); break;
     default: break;
   }
 }
@@ -676,96 +391,6 @@ void launch_curl(int kind, const double* const src[3], const int sext[3][3], dou
     curl_kernel<true><<<grid, 256, 0, st>>>(src[0], src[1], src[2], e[0], e[1], e[2], dst[0], dst[1], dst[2], f[0], f[1], f[2]);
   else
     curl_kernel<false><<<grid, 256, 0, st>>>(src[0], src[1], src[2], e[0], e[1], e[2], dst[0], dst[1], dst[2], f[0], f[1], f[2]);
-}
-
-template <int P, int Q, bool DUAL, bool FULL>
-void launch_hodge_pencil(const HodgeArgs& a, cudaStream_t st) {
-  constexpr int NL = P + 1, XB = hodge::max_box<P, DUAL>(), VB = Q * NL, CB = (P + 1) * Q * Q,
-                TB = (P + 1) * (P + 1) * Q;
-  const size_t smem = size_t(8) * (6 * XB + 9 * VB + CB + TB) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(hodge::hodge_pencil_kernel<P, Q, DUAL, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
-    attr = true;
-  }
-  const long npen = long(a.nel[0]) * a.nel[1];
-  long grid = (npen + 7) / 8;
-  const long cap = 16L * sm_count();
-  if (grid > cap) grid = cap;
-  hodge::hodge_pencil_kernel<P, Q, DUAL, FULL><<<unsigned(grid), 256, smem, st>>>(a);
-}
-
-template <int P, int Q, bool DUAL, bool FULL>
-void launch_hodge_brick(const HodgeArgs& a, cudaStream_t st) {
-  constexpr int E = 4;
-  using L = brick::Layout<P, Q, DUAL, E>;
-  const size_t smem = size_t(L::template total<FULL>()) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(brick::hodge_brick_kernel<P, Q, DUAL, FULL, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
-    attr = true;
-  }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, brick::hodge_brick_kernel<P, Q, DUAL, FULL, E>, 256, smem);
-  if (per_sm < 1) per_sm = 1;
-  const long slots = long(per_sm) * sm_count();
-  const long bricks = long((a.nel[0] + E - 1) / E) * ((a.nel[1] + E - 1) / E);
-  // z chunks: about four work items per resident CTA, at least 4 element layers per chunk
-  long bzn = (4 * slots + bricks - 1) / bricks;
-  int zchunk = int((a.nel[2] + bzn - 1) / bzn);
-  if (zchunk < 4) zchunk = 4;
-  if (const int zc = env_int("SGM_HODGE_ZCHUNK", 0)) zchunk = zc;
-  const long items = bricks * ((a.nel[2] + zchunk - 1) / zchunk);
-  const long grid = items < slots ? items : slots;
-  brick::hodge_brick_kernel<P, Q, DUAL, FULL, E><<<unsigned(grid), 256, smem, st>>>(a, zchunk);
-}
-
-template <int P, int Q>
-void launch_hodge2(const HodgeArgs& a, cudaStream_t st) {
-  if (env_int("SGM_HODGE_PENCIL", 0) == 0) {
-    if (a.dual) {
-      if (a.full) launch_hodge_brick<P, Q, true, true>(a, st);
-      else launch_hodge_brick<P, Q, true, false>(a, st);
-    } else {
-      if (a.full) launch_hodge_brick<P, Q, false, true>(a, st);
-      else launch_hodge_brick<P, Q, false, false>(a, st);
-    }
-    return;
-  }
-  if (a.dual) {
-    if (a.full) launch_hodge_pencil<P, Q, true, true>(a, st);
-    else launch_hodge_pencil<P, Q, true, false>(a, st);
-  } else {
-    if (a.full) launch_hodge_pencil<P, Q, false, true>(a, st);
-    else launch_hodge_pencil<P, Q, false, false>(a, st);
-  }
-}
-
-void launch_hodge_general(int p, const HodgeArgs& a, cudaStream_t st) {
-  // z-pencil warp kernel (hodge_kernel.cuh) for the default rule Q = p + 1; the generic
-  // CTA-per-element kernel for larger rules (quad_points > p + 1)
-  if (a.Q == p + 1) {
-    switch (p) {
-      case 2: launch_hodge2<2, 3>(a, st); return;
-      case 3: launch_hodge2<3, 4>(a, st); return;
-      case 4: launch_hodge2<4, 5>(a, st); return;
-      default: break;
-    }
-  }
-  long nel = long(a.nel[0]) * a.nel[1] * a.nel[2];
-  int Q = a.Q;
-  int M = (p + 1 > Q) ? p + 1 : Q;
-  size_t smem = size_t(6) * M * M * M * sizeof(double);
-  int threads = Q * Q * Q;
-  if (threads < 32) threads = 32;
-  switch (p) {
-    case 2: hodge_general_kernel<2><<<unsigned(nel), threads, smem, st>>>(a); break;
-    case 3: hodge_general_kernel<3><<<unsigned(nel), threads, smem, st>>>(a); break;
-    case 4: hodge_general_kernel<4><<<unsigned(nel), threads, smem, st>>>(a); break;
-    default: break;
-  }
 }
 
 void launch_dot_partials(const double* x, const double* y, size_t n, double* partials, int slot, cudaStream_t st) {

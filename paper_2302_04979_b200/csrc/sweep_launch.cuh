@@ -1,0 +1,149 @@
+// Host launchers of the line sweeps (template machinery; instantiated per degree in sweep_p*.cu so
+// the three degrees compile in parallel).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.cuh"
+#include "launch_util.cuh"
+#include "seg_sweep.cuh"
+#include "sweep_kernel.cuh"
+
+namespace sgm {
+namespace sweeplaunch {
+
+template <int P, int HB, int SEG, int LPT, int MODE, int OPS>
+bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
+  using sweep::Cfg;
+  Cfg cfg;
+  std::memset(&cfg, 0, sizeof(cfg));
+  constexpr int TW = 32 * LPT;
+  int Lmax = 0;
+  for (int c = 0; c < 3; ++c) {
+    if (c >= a.ncomp) continue;
+    const SweepComp& C = a.comp[c];
+    sweep::CompGeom& g = cfg.g[c];
+    const int X = C.ext[0], Y = C.ext[1], Z = C.ext[2];
+    // per-component axis (strided passes may mix y- and z-lines of different components)
+    const int ax = (MODE != 3 && C.axis > 0) ? C.axis : a.axis;
+    g.L = C.ext[ax];
+    g.magic = 0xffffffffu / unsigned(X);
+    g.nlines = X * Y * Z / g.L;
+    g.X = X;
+    g.rowlen = X;
+    g.gs = (ax == 0) ? 1 : (ax == 1 ? X : X * Y);
+    g.os = (ax == 1) ? X * Y : X;  // transverse index l / X: z (y pass) or y (z pass)
+    g.TD = (ax == 0) ? Y : X;      // transverse coordinates of line l: (l % TD, l / TD)
+    g.tmagic = 0xffffffffu / unsigned(g.TD);
+    cfg.tiles[c] = (g.nlines + TW - 1) / TW;
+    cfg.nitems += cfg.tiles[c];
+    Lmax = g.L > Lmax ? g.L : Lmax;
+  }
+  cfg.NC = (Lmax + SEG - 1) / SEG;
+  cfg.rows = cfg.NC * SEG + P;
+  // x axis: a tile of whole lines is one contiguous range -> one bulk copy in and one out (TMA
+  // engine), if the component bases are 16-byte aligned and the component has an even size.
+  // (Strided tiles are many small row runs: measured slower on the bulk engine than cp.async.)
+  bool bulk = (MODE == 3) && env_int("SGM_BULK", 1) != 0;
+  for (int c = 0; c < a.ncomp && bulk; ++c) {
+    const SweepComp& C = a.comp[c];
+    if ((reinterpret_cast<uintptr_t>(C.in) & 15) || (reinterpret_cast<uintptr_t>(C.out) & 15)) bulk = false;
+    if ((long(C.ext[0]) * C.ext[1] * C.ext[2]) & 1) bulk = false;
+  }
+  cfg.bulk = bulk ? 1 : 0;
+  if (bulk) cfg.NP = 1;
+  else cfg.NP = env_int("SGM_NP", 4);
+  if (cfg.NP < 1) cfg.NP = 1;
+  if (cfg.NC + cfg.NP > 16) cfg.NP = 16 - cfg.NC;
+  if (cfg.NP < 1) return false;
+  if (MODE == 3) {
+    // bulk: a whole-tile copy keeps pitch = line length; a multiple of 4 would put the consumers'
+    // per-lane line walks on few banks (all lanes on one bank pair at L % 16 == 0), so such lines
+    // are copied one by one into pitch L + 2 (16-byte aligned rows, 4-way at worst)
+    int bp_max = 0;
+    for (int c = 0; c < a.ncomp; ++c) {
+      sweep::CompGeom& g = cfg.g[c];
+      g.lbulk = (bulk && (g.L % 4) == 0 && env_int("SGM_LINE_BULK", 1)) ? 1 : 0;
+      g.bpitch = g.lbulk ? g.L + 2 : g.L;
+      bp_max = g.bpitch > bp_max ? g.bpitch : bp_max;
+    }
+    cfg.pitch = bulk ? bp_max : (cfg.rows | 1);
+    cfg.W = 0;
+    cfg.slab = TW * cfg.pitch + cfg.rows + 2;
+  } else {
+    cfg.pitch = 0;
+    cfg.W = TW;
+    cfg.slab = cfg.W * cfg.rows;
+  }
+  cfg.slab = (cfg.slab + 1) & ~1;  // keep every slab 16-byte aligned
+  cfg.ntabs = (a.tabs[1] != nullptr && a.tabs[1] != a.tabs[0]) ? 2 : 1;
+  cfg.tab_dbl = a.tab_rows * RowLayout<P>::RS;
+  cfg.dbg = env_int("SGM_PIPE_DBG", 0);
+  cfg.reverse = env_int("SGM_SNAKE", 1) ? a.reverse : 0;
+  constexpr int M = P - 1;
+  const size_t smem = (size_t(cfg.ntabs) * cfg.tab_dbl + size_t(2) * cfg.slab + size_t(2) * cfg.NC * M * TW + 4) *
+                      sizeof(double);
+  if (smem > 227 * 1024) return false;
+  const int NT = (cfg.NC + cfg.NP) * 32;
+  static int attr_done = 0;
+  if (!attr_done) {
+    cudaFuncSetAttribute(sweep::sweep_kernel<P, HB, SEG, LPT, MODE, OPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         227 * 1024);
+    attr_done = 1;
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep::sweep_kernel<P, HB, SEG, LPT, MODE, OPS>, NT, smem);
+  if (per_sm < 1) per_sm = 1;
+  const int cap = env_int("SGM_CTAS_PER_SM", 0);
+  if (cap > 0 && cap < per_sm) per_sm = cap;
+  long grid = long(per_sm) * sm_count();
+  if (a.share_n > 0) grid = (grid * a.share_k + a.share_n / 2) / a.share_n;
+  if (grid < 1) grid = 1;
+  if (grid > cfg.nitems) grid = cfg.nitems;
+  if (grid < 1) grid = 1;
+  launch_pdl(sweep::sweep_kernel<P, HB, SEG, LPT, MODE, OPS>, unsigned(grid), unsigned(NT), smem, st, a, cfg);
+  return true;
+}
+
+template <int P, int HB, int SEG, int MODE, int OPS>
+void launch_sweep_m(const SweepArgs& a, cudaStream_t st) {
+  // two lines per thread when the register budget allows (SEG <= 17) and the slabs fit
+  if constexpr (SEG <= 17) {
+    if (env_int("SGM_LPT", 2) == 2 && launch_sweep_t<P, HB, SEG, 2, MODE, OPS>(a, st)) return;
+  }
+  launch_sweep_t<P, HB, SEG, 1, MODE, OPS>(a, st);
+}
+
+template <int P, int SEG, int MODE>
+void launch_sweep_o(const SweepArgs& a, cudaStream_t st) {
+  // band half-width: P - 1 for the eps-side Grams and the pairing factors, P for the mu-side Gram
+  if (a.band && a.solve) {
+    if (a.band_hw >= P) launch_sweep_m<P, P, SEG, MODE, 3>(a, st);
+    else if (P >= 3 && a.band_hw <= P - 2) launch_sweep_m<P, (P >= 3 ? P - 2 : 1), SEG, MODE, 3>(a, st);  // eps Gamma_C^{p-2}
+    else launch_sweep_m<P, P - 1, SEG, MODE, 3>(a, st);
+  } else if (a.solve) {
+    launch_sweep_m<P, P - 1, SEG, MODE, 2>(a, st);
+  } else {
+    if (a.band_hw >= P) launch_sweep_m<P, P, SEG, MODE, 1>(a, st);
+    else launch_sweep_m<P, P - 1, SEG, MODE, 1>(a, st);
+  }
+}
+
+template <int P, int SEG>
+void launch_sweep_s(const SweepArgs& a, cudaStream_t st) {
+  if (a.axis == 0) launch_sweep_o<P, SEG, 3>(a, st);
+  else launch_sweep_o<P, SEG, 0>(a, st);
+}
+
+template <int P>
+void launch_sweep_p(int seg, const SweepArgs& a, cudaStream_t st) {
+  switch (seg) {
+    case 12: launch_sweep_s<P, 12>(a, st); break;
+    case 17: launch_sweep_s<P, 17>(a, st); break;
+    default: launch_sweep_s<P, 28>(a, st); break;
+  }
+}
+
+}  // namespace sweeplaunch
+}  // namespace sgm
