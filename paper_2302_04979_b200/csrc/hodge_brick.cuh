@@ -198,8 +198,10 @@ __device__ __forceinline__ void interp_y(const CompSm<P, Q, DUAL, E, C>& S, int 
 
 // x: U[qz][Y][ex*Q+qx] = sum_jx Vx[ex][qx][jx] Z2[qz][Y][ex+jx]    (tasks: qz, Y)
 template <int P, int Q, bool DUAL, int E, int C, bool UNI>
-__device__ __forceinline__ void interp_x(const CompSm<P, Q, DUAL, E, C>& S, int t) {
-  // (tasks: half, qz, Y -- each half of the brick's elements along x is a separate task)
+__device__ __forceinline__ void interp_x(const CompSm<P, Q, DUAL, E, C>& S, int t, const double* Wm = nullptr,
+                                         double wsc = 1.0, int nex = E, int ney = E) {
+  // (tasks: half, qz, Y -- each half of the brick's elements along x is a separate task).  With Wm
+  // (scalar W, staged element-major like U) the quadrature multiply u *= wsc * w is fused here.
   using G = Geo<P, Q, DUAL, E, C>;
   constexpr int NL = P + 1, EH = E / 2;
   if (t >= 2 * Q * G::EQ) return;
@@ -216,7 +218,12 @@ __device__ __forceinline__ void interp_x(const CompSm<P, Q, DUAL, E, C>& S, int 
       double s = 0.0;
 #pragma unroll
       for (int jx = 0; jx < G::NX; ++jx) s = fma(V(S.Vx, hf * EH + el, qx, jx), zv[el + jx], s);
-      S.U[uidx<Q, E>(t / G::EQ, t % G::EQ, hf * EH + el, qx)] = s;
+      const int ui = uidx<Q, E>(t / G::EQ, t % G::EQ, hf * EH + el, qx);
+      if (Wm) {
+        const bool live = (hf * EH + el) < nex && (t % G::EQ) / Q < ney;
+        s = live ? wsc * Wm[ui] * s : 0.0;
+      }
+      S.U[ui] = s;
     }
 }
 
@@ -282,6 +289,55 @@ __device__ __forceinline__ void test_z(const CompSm<P, Q, DUAL, E, C>& S, int t)
 #pragma unroll
     for (int qz = 0; qz < Q; ++qz) s = fma(S.Vz[qz * NL + jz], zv[qz], s);
     S.Yw[sl * LAY + t] = s;
+  }
+}
+
+// One (py, px) column of component C at the end of element layer ez (no block barrier inside: the
+// same thread owns the column in every step):  test along z of layer ez, flush of the completed
+// output slot (atomics to y, slot cleared), then -- if another layer follows -- the new top
+// coefficient into the freed slot and the z interpolation of the next layer.  vz_*: the z bases
+// (global, [Q][NL]) of this layer and of the next.
+template <int P, int Q, bool DUAL, int E, int C>
+__device__ __forceinline__ void column_phase(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int t, int gx0,
+                                             int gy0, int gz_flush, bool next, int gz_load,
+                                             const double* __restrict__ vz_cur, const double* __restrict__ vz_next) {
+  using G = Geo<P, Q, DUAL, E, C>;
+  constexpr int NL = P + 1, LAY = G::PY * G::PX;
+  if (t >= LAY) return;
+  const int px = t % G::PX, py = t / G::PX;
+  const int gx = gx0 + px, gy = gy0 + py;
+  const int* ext = A.ext[C];
+  const bool inxy = gx >= 0 && gx < ext[0] && gy >= 0 && gy < ext[1];
+  double zv[Q];
+#pragma unroll
+  for (int qz = 0; qz < Q; ++qz) zv[qz] = S.Z1[qz * LAY + t];
+#pragma unroll
+  for (int jz = 0; jz < G::NZ; ++jz) {
+    const int sl = S.slot(jz);
+    double acc = S.Yw[sl * LAY + t];
+#pragma unroll
+    for (int qz = 0; qz < Q; ++qz) acc = fma(__ldg(vz_cur + qz * NL + jz), zv[qz], acc);
+    if (jz == 0) {
+      if (inxy && gz_flush >= 0 && gz_flush < ext[2])
+        atomicAdd(A.y[C] + gx + long(ext[0]) * (gy + long(ext[1]) * gz_flush), acc);
+      S.Yw[sl * LAY + t] = 0.0;
+    } else {
+      S.Yw[sl * LAY + t] = acc;
+    }
+  }
+  if (!next) return;
+  double v = 0.0;
+  if (inxy && gz_load >= 0 && gz_load < ext[2]) v = __ldg(A.x[C] + gx + long(ext[0]) * (gy + long(ext[1]) * gz_load));
+  S.Xw[S.slot(0) * LAY + t] = v;
+  double xv[G::NZ];
+#pragma unroll
+  for (int jz = 0; jz < G::NZ; ++jz) xv[jz] = (jz + 1 < G::NZ) ? S.Xw[S.slot(jz + 1) * LAY + t] : v;
+#pragma unroll
+  for (int qz = 0; qz < Q; ++qz) {
+    double s = 0.0;
+#pragma unroll
+    for (int jz = 0; jz < G::NZ; ++jz) s = fma(__ldg(vz_next + qz * NL + jz), xv[jz], s);
+    S.Z1[qz * LAY + t] = s;
   }
 }
 
@@ -397,48 +453,70 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
     };
     stage_w(B.ez0);
     __syncthreads();
+    SGM_BRICK_STAGE3(interp_z, G0::PY * G0::PX, G1::PY * G1::PX, G2::PY * G2::PX)
+    auto vzp = [&](int c, int ez) {
+      return A.basis + A.basis_off[2][c == 2 ? 0 : 1] + size_t(ez) * Q * NL;
+    };
     for (int ez = B.ez0; ez < B.ez1; ++ez) {
-      SGM_BRICK_STAGE3(interp_z, G0::PY * G0::PX, G1::PY * G1::PX, G2::PY * G2::PX)
       SGM_BRICK_STAGE3U(interp_y, 1, 2 * Q * G0::PX, 2 * Q * G1::PX, 2 * Q * G2::PX)
-      SGM_BRICK_STAGE3U(interp_x, 0, 2 * Q * EQ, 2 * Q * EQ, 2 * Q * EQ)
-      // quadrature points: v_c = sum_c' W_cc' u_c' (FULL) or scale_c w u_c (SCALAR); W was staged
-      // into shared memory (element-major, the layout of U) while the interpolation ran
+      // W of this layer (staged by cp.async since the previous layer) must be in shared memory
+      // before the x interpolation (scalar W is multiplied there) or the quadrature stage (full W)
       pipe::cp_async_wait_all();
       __syncthreads();
-      for (int el = threadIdx.x >> 5; el < E * E; el += 8) {
-        const bool live = (el % E) < B.nex && (el / E) < B.ney;  // warp-uniform
-        for (int i = el * QQQ + (threadIdx.x & 31); i < (el + 1) * QQQ; i += 32) {
-          const double u0 = S0.U[i], u1 = S1.U[i], u2 = S2.U[i];
-          if (FULL) {
+      {
+        const bool u0 = uni[0 * 2 + 0], u1 = uni[1 * 2 + 0], u2 = uni[1 * 2 + 0];
+        const double* Wm = FULL ? nullptr : Wsm;
+        for (int t = threadIdx.x; t < 3 * 2 * Q * EQ; t += 256) {
+          const int c = t / (2 * Q * EQ), tt = t % (2 * Q * EQ);
+          if (c == 0) {
+            if (u0) interp_x<P, Q, DUAL, E, 0, true>(S0, tt, Wm, A.scale[0], B.nex, B.ney);
+            else interp_x<P, Q, DUAL, E, 0, false>(S0, tt, Wm, A.scale[0], B.nex, B.ney);
+          } else if (c == 1) {
+            if (u1) interp_x<P, Q, DUAL, E, 1, true>(S1, tt, Wm, A.scale[1], B.nex, B.ney);
+            else interp_x<P, Q, DUAL, E, 1, false>(S1, tt, Wm, A.scale[1], B.nex, B.ney);
+          } else {
+            if (u2) interp_x<P, Q, DUAL, E, 2, true>(S2, tt, Wm, A.scale[2], B.nex, B.ney);
+            else interp_x<P, Q, DUAL, E, 2, false>(S2, tt, Wm, A.scale[2], B.nex, B.ney);
+          }
+        }
+        __syncthreads();
+      }
+      if (FULL) {
+        // quadrature points: v_c = sum_c' W_cc' u_c' (the 3 x 3 W couples the components)
+        for (int el = threadIdx.x >> 5; el < E * E; el += 8) {
+          const bool live = (el % E) < B.nex && (el / E) < B.ney;  // warp-uniform
+          for (int i = el * QQQ + (threadIdx.x & 31); i < (el + 1) * QQQ; i += 32) {
+            const double u0 = S0.U[i], u1 = S1.U[i], u2 = S2.U[i];
             const double* w = Wsm + i * 6;
             const double wxx = live ? w[0] : 0.0, wyy = live ? w[1] : 0.0, wzz = live ? w[2] : 0.0,
                          wxy = live ? w[3] : 0.0, wxz = live ? w[4] : 0.0, wyz = live ? w[5] : 0.0;
             S0.U[i] = wxx * u0 + wxy * u1 + wxz * u2;
             S1.U[i] = wxy * u0 + wyy * u1 + wyz * u2;
             S2.U[i] = wxz * u0 + wyz * u1 + wzz * u2;
-          } else {
-            const double w = live ? Wsm[i] : 0.0;
-            S0.U[i] = A.scale[0] * w * u0;
-            S1.U[i] = A.scale[1] * w * u1;
-            S2.U[i] = A.scale[2] * w * u2;
           }
         }
+        __syncthreads();
       }
-      __syncthreads();
       if (ez + 1 < B.ez1) stage_w(ez + 1);
       SGM_BRICK_STAGE3U(test_x, 0, Q * EQ, Q * EQ, Q * EQ)
       SGM_BRICK_STAGE3U(test_y, 1, Q * G0::PX, Q * G1::PX, Q * G2::PX)
-      SGM_BRICK_STAGE3(test_z, G0::PY * G0::PX, G1::PY * G1::PX, G2::PY * G2::PX)
-      // the lowest output layer of each component is complete: flush and clear its slot; the
-      // freed coefficient slot (this element's layer 0) takes the next element's top layer
-      flush_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, ez), S0.slot(0));
-      flush_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, ez), S1.slot(0));
-      flush_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, ez), S2.slot(0));
-      if (ez + 1 < B.ez1) {
-        load_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, ez + 1) + G0::NZ - 1, S0.slot(0));
-        load_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, ez + 1) + G1::NZ - 1, S1.slot(0));
-        load_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, ez + 1) + G2::NZ - 1, S2.slot(0));
-        load_vz(ez + 1);
+      // per column: test along z, flush the completed layer, load the next top layer, interpolate
+      // the next layer along z -- no barrier between these steps
+      {
+        const bool nx1 = ez + 1 < B.ez1;
+        const int ezn = nx1 ? ez + 1 : ez;
+        constexpr int N0 = G0::PY * G0::PX, N1 = G1::PY * G1::PX, N2 = G2::PY * G2::PX;
+        for (int t = threadIdx.x; t < N0 + N1 + N2; t += 256) {
+          if (t < N0)
+            column_phase<P, Q, DUAL, E, 0>(A, S0, t, gx0[0], gy0[0], zfirst(0, ez), nx1, zfirst(0, ezn) + G0::NZ - 1,
+                                           vzp(0, ez), vzp(0, ezn));
+          else if (t < N0 + N1)
+            column_phase<P, Q, DUAL, E, 1>(A, S1, t - N0, gx0[1], gy0[1], zfirst(1, ez), nx1,
+                                           zfirst(1, ezn) + G1::NZ - 1, vzp(1, ez), vzp(1, ezn));
+          else
+            column_phase<P, Q, DUAL, E, 2>(A, S2, t - N0 - N1, gx0[2], gy0[2], zfirst(2, ez), nx1,
+                                           zfirst(2, ezn) + G2::NZ - 1, vzp(2, ez), vzp(2, ezn));
+        }
       }
       S0.base = S0.slot(1);
       S1.base = S1.slot(1);
