@@ -76,13 +76,40 @@ def identity_ctrl(p, n):
     return np.stack([gx, gy, gz], axis=-1)
 
 
+class Rational:
+    """A rational (NURBS) map F = sum_i w_i P_i N_i / sum_i w_i N_i over the untrimmed S_p basis
+    (F is "a (rational) spline").  P: control points
+    [(nz+p)][(ny+p)][(nx+p)][3]; w: positive weights [(nz+p)][(ny+p)][(nx+p)]."""
+
+    def __init__(self, P, w):
+        self.P = np.asarray(P, dtype=np.float64)
+        self.w = np.asarray(w, dtype=np.float64)
+
+
 def geometry_at_qp(quad, ctrl):
-    """Physical points F(x_q) [nqp,3] and Jacobians DF(x_q) [nqp,3,3] (DF[i,j] = dF_i/dx^_j)."""
+    """Physical points F(x_q) [nqp,3] and Jacobians DF(x_q) [nqp,3,3] (DF[i,j] = dF_i/dx^_j).
+    ``ctrl``: None (identity), control points (polynomial map) or a ``Rational``.  For a rational
+    map with numerator N = sum w P B and denominator W = sum w B: F = N / W and
+    dF/dx^_j = (dN/dx^_j - F dW/dx^_j) / W (quotient rule)."""
     p, n = quad.p, quad.n
     if ctrl is None:
         X = np.stack(np.meshgrid(quad.x1d[2], quad.x1d[1], quad.x1d[0], indexing="ij")[::-1], -1)
         DF = np.broadcast_to(np.eye(3), (quad.nqp, 3, 3)).copy()
         return X.reshape(-1, 3), DF
+    if isinstance(ctrl, Rational):
+        V, D = [], []
+        for a in range(3):
+            X = open_knots(p, n[a])
+            V.append(bspline_values(X, p, quad.x1d[a]))
+            D.append(bspline_derivatives(X, p, quad.x1d[a]))
+        w = ctrl.w.reshape(-1)
+        wP = ctrl.P.reshape(-1, 3) * w[:, None]
+        Phi = _kron3(V[0], V[1], V[2])
+        dPhi = [_kron3(D[0], V[1], V[2]), _kron3(V[0], D[1], V[2]), _kron3(V[0], V[1], D[2])]
+        Wq = Phi @ w
+        F = (Phi @ wP) / Wq[:, None]
+        DF = np.stack([(dPhi[j] @ wP - F * (dPhi[j] @ w)[:, None]) / Wq[:, None] for j in range(3)], axis=-1)
+        return F, DF
     ctrl = np.asarray(ctrl, dtype=np.float64).reshape(n[2] + p, n[1] + p, n[0] + p, 3)
     V, D = [], []
     for a in range(3):

@@ -17,7 +17,7 @@ import numpy as np
 
 from . import forms
 from .splines import gram_1d, space_values, open_knots, bspline_values, bspline_derivatives
-from .assemble import Quad, qp_elem_to_grid
+from .assemble import Quad, qp_elem_to_grid, Rational
 
 
 def apply_axis(A, X, axis):
@@ -106,15 +106,29 @@ class TierB:
         return None
 
     def _geometry(self):
+        """DF on the global quadrature grid by sum factorisation; a ``Rational`` map uses the
+        quotient rule on numerator sum w P B and denominator sum w B."""
         quad = Quad(self.p, self.n, self.Q)
-        ctrl = np.asarray(self.ctrl, dtype=np.float64).reshape(self.n[2] + self.p, self.n[1] + self.p,
-                                                                self.n[0] + self.p, 3)
+        shp = (self.n[2] + self.p, self.n[1] + self.p, self.n[0] + self.p)
         V, D = [], []
         for a in range(3):
             X = open_knots(self.p, self.n[a])
             V.append(bspline_values(X, self.p, quad.x1d[a]))
             D.append(bspline_derivatives(X, self.p, quad.x1d[a]))
         DF = np.empty((len(quad.x1d[2]), len(quad.x1d[1]), len(quad.x1d[0]), 3, 3))
+        if isinstance(self.ctrl, Rational):
+            w = self.ctrl.w.reshape(shp)
+            wP = self.ctrl.P.reshape(shp + (3,)) * w[..., None]
+            Wq = kron3(V[0], V[1], V[2], w)
+            dW = [kron3(D[0], V[1], V[2], w), kron3(V[0], D[1], V[2], w), kron3(V[0], V[1], D[2], w)]
+            for i in range(3):
+                C = wP[..., i]
+                Fi = kron3(V[0], V[1], V[2], C) / Wq
+                DF[..., i, 0] = (kron3(D[0], V[1], V[2], C) - Fi * dW[0]) / Wq
+                DF[..., i, 1] = (kron3(V[0], D[1], V[2], C) - Fi * dW[1]) / Wq
+                DF[..., i, 2] = (kron3(V[0], V[1], D[2], C) - Fi * dW[2]) / Wq
+            return quad, DF
+        ctrl = np.asarray(self.ctrl, dtype=np.float64).reshape(shp + (3,))
         for i in range(3):
             C = ctrl[..., i]
             DF[..., i, 0] = kron3(D[0], V[1], V[2], C)

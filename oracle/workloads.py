@@ -12,6 +12,7 @@ import synth
 from . import forms
 from .splines import gauss_rule, space_values, open_knots, bspline_values
 from .structured import TierB, kron3, apply_axis, curl_dual
+from .assemble import Rational
 
 # ------------------------------------------------------------------------------------------
 # cavity eigenmodes of the unit cube with PEC walls (readings Z10, Z11)
@@ -97,9 +98,64 @@ def physical_points(p, n, ctrl=None, Q=None):
     xs, _, Xg = qp_grid(p, n, Q)
     if ctrl is None:
         return Xg
-    ctrl = np.asarray(ctrl, dtype=np.float64).reshape(n[2] + p, n[1] + p, n[0] + p, 3)
     V = [bspline_values(open_knots(p, n[a]), p, xs[a]) for a in range(3)]
+    shp = (n[2] + p, n[1] + p, n[0] + p)
+    if isinstance(ctrl, Rational):
+        w = ctrl.w.reshape(shp)
+        Wq = kron3(V[0], V[1], V[2], w)
+        wP = ctrl.P.reshape(shp + (3,)) * w[..., None]
+        return np.stack([kron3(V[0], V[1], V[2], wP[..., i]) / Wq for i in range(3)], -1)
+    ctrl = np.asarray(ctrl, dtype=np.float64).reshape(shp + (3,))
     return np.stack([kron3(V[0], V[1], V[2], ctrl[..., i]) for i in range(3)], -1)
+
+
+# ------------------------------------------------------------------------------------------
+# quarter-annulus (coaxial-cable cross-section) geometry: a degree-2 NURBS map (NEXT #2 input)
+# ------------------------------------------------------------------------------------------
+
+def insert_knot(U, p, Pw, u):
+    """Boehm's knot insertion on a curve with homogeneous control points Pw [m][d] (weights last):
+    the curve is unchanged, one more control point (The NURBS Book, algorithm A5.1)."""
+    U = np.asarray(U, dtype=np.float64)
+    k = np.searchsorted(U, u, side="right") - 1
+    m = len(Pw)
+    Q = np.zeros((m + 1, Pw.shape[1]))
+    for i in range(m + 1):
+        if i <= k - p:
+            Q[i] = Pw[i]
+        elif i >= k + 1:
+            Q[i] = Pw[i - 1]
+        else:
+            a = (u - U[i]) / (U[i + p] - U[i])
+            Q[i] = a * Pw[i] + (1 - a) * Pw[i - 1]
+    return np.insert(U, k + 1, u), Q
+
+
+def quarter_annulus(n, r1=0.5, r2=1.0, height=1.0):
+    """Rational degree-2 map of (0,1)^3 onto {r1 <= r <= r2, 0 <= theta <= pi/2, 0 <= z <= height}:
+    x^ -> radius r1 + (r2 - r1) x^ (affine), y^ -> angle along the exact NURBS quarter circle
+    (control points (1,0), (1,1), (0,1), weights 1, 1/sqrt2, 1), z^ -> z (affine); the circle is
+    refined to n_y elements by knot insertion, the affine directions use Greville points.  The
+    order (radial, angular, axial) gives det DF > 0.  Returns a ``Rational`` for p = 2."""
+    n = forms._n3(n)
+    p = 2
+    U = np.array([0.0, 0, 0, 1, 1, 1])
+    Pw = np.array([[1.0, 0.0, 1.0], [1.0, 1.0, 1.0], [0.0, 1.0, 1.0]])
+    Pw[:, :2] *= Pw[:, 2:3] * np.array([[1.0], [1.0 / np.sqrt(2.0)], [1.0]])
+    Pw[1, 2] = 1.0 / np.sqrt(2.0)
+    for k in range(1, n[1]):
+        U, Pw = insert_knot(U, p, Pw, k / n[1])
+    arc_w = Pw[:, 2]
+    arc = Pw[:, :2] / arc_w[:, None]
+    g = [np.array([open_knots(p, n[a])[i + 1:i + p + 1].mean() for i in range(n[a] + p)]) for a in (0, 2)]
+    r = r1 + (r2 - r1) * g[0]
+    z = height * g[1]
+    P = np.zeros((n[2] + p, n[1] + p, n[0] + p, 3))
+    P[..., 0] = r[None, None, :] * arc[None, :, 0:1]
+    P[..., 1] = r[None, None, :] * arc[None, :, 1:2]
+    P[..., 2] = z[:, None, None]
+    w = np.broadcast_to(arc_w[None, :, None], (n[2] + p, n[1] + p, n[0] + p)).copy()
+    return Rational(P, w)
 
 
 def interpolate_map(p, n, fmap):

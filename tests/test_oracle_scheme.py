@@ -332,3 +332,54 @@ def test_composed_time_order_vs_exact_semidiscrete(weights, order):
         errs.append(np.linalg.norm(np.concatenate([out[0], out[2]]) - yT) / np.linalg.norm(yT))
     rates = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
     assert np.all(np.abs(rates - order) < 0.15), (errs, rates)
+
+
+# ---- rational (NURBS) maps: the quarter annulus of the coaxial-cable experiment (NEXT #2) ----
+
+def _bernstein_quarter_circle(t):
+    """The single-segment rational quadratic quarter circle (control points (1,0), (1,1), (0,1),
+    weights 1, 1/sqrt2, 1) evaluated directly in Bernstein form."""
+    B = np.stack([(1 - t) ** 2, 2 * t * (1 - t), t ** 2], -1)
+    w = np.array([1.0, 1.0 / np.sqrt(2.0), 1.0])
+    P = np.array([[1.0, 0.0], [1.0, 1.0], [0.0, 1.0]])
+    return (B * w) @ P / (B @ w)[..., None]
+
+
+@pytest.mark.parametrize("n", [1, (2, 3, 2), (1, 5, 1)])
+def test_quarter_annulus_is_exact(n):
+    """The NURBS quarter annulus maps onto exact circles r = r1 + (r2 - r1) x^ (closed form), its
+    angle follows the single-segment circle after knot insertion (pins Boehm insertion), z is affine."""
+    from oracle.workloads import qp_grid
+    g = W.quarter_annulus(n, r1=0.5, r2=1.0, height=1.0)
+    X = W.physical_points(2, n, g)
+    _, _, Xg = qp_grid(2, n, 3)
+    r = np.hypot(X[..., 0], X[..., 1])
+    assert np.abs(r - (0.5 + 0.5 * Xg[..., 0])).max() < 1e-14
+    assert np.abs(X[..., 2] - Xg[..., 2]).max() < 1e-14
+    C = _bernstein_quarter_circle(Xg[..., 1])
+    assert np.abs(X[..., :2] / r[..., None] - C).max() < 1e-14
+
+
+@pytest.mark.parametrize("n", [(2, 3, 2), 2])
+def test_rational_map_tier_b_equals_tier_a(n):
+    """Tier A (3D quadrature with the quotient-rule Jacobian at every point) and tier B (sum
+    factorised) agree on the quarter annulus; det DF > 0; the step conserves the modified energy."""
+    p = 2
+    g = W.quarter_annulus(n)
+    A = TierA(p, n, ctrl=g)
+    B = TierB(p, n, ctrl=g)
+    from oracle.assemble import geometry_at_qp, Quad as Qd
+    _, DF = geometry_at_qp(Qd(p, forms._n3(n)), g)
+    assert np.linalg.det(DF).min() > 0
+    st = _rand_state(A.N_e, A.N_h, 51)
+    ra, rb = A.step(*st, 0.01), B.step(*st, 0.01)
+    for x, y in zip(rb, ra):
+        assert rel(x, y) < 1e-13
+    d, e, b, h = st[0], A.solve_K1(A.Meps @ st[0]), st[2], A.solve_Kt1(A.Mmu @ st[2])
+    dt = 0.5 * W.cfl_dt_max(B)
+    Es = []
+    for _ in range(100):
+        bp = b
+        d, e, b, h = A.step(d, e, b, h, dt)
+        Es.append(0.5 * d @ (A.K1 @ e) + 0.5 * bp @ (A.Kt1 @ h))
+    assert (max(Es) - min(Es)) / abs(np.mean(Es)) < 1e-12
