@@ -97,6 +97,11 @@ typedef struct {
   int quad_points;         /* Q per axis per element for the geometry/material masses;
                               0 -> p+1 (reading Z13).  Allowed: p+1 .. 8 */
   int device;              /* CUDA ordinal; < 0 -> host-only plan (queries only) */
+  const double* geom_weights; /* host; NULL = polynomial map.  Else positive weights, layout
+                              [(nz+p)][(ny+p)][(nx+p)], of a rational (NURBS) map
+                              F = sum w_i P_i N_i / sum w_i N_i with P_i = geom_ctrl (P:L136-137,
+                              "a (rational) spline").  Copied at create; non-positive or non-finite
+                              weights -> SGM_E_GEOMETRY. */
 } sgm_plan_desc;
 
 /* ---- plan lifetime and queries (synchronous) ------------------------------------------- */

@@ -28,7 +28,7 @@ c_dp = ctypes.POINTER(ctypes.c_double)
 
 class sgm_plan_desc(ctypes.Structure):
     _fields_ = [("n_el", c_int * 3), ("degree", c_int), ("geom_ctrl", c_void_p),
-                ("quad_points", c_int), ("device", c_int)]
+                ("quad_points", c_int), ("device", c_int), ("geom_weights", c_void_p)]
 
 
 STATUS = {0: "SGM_OK", 1: "SGM_E_INVALID_ARG", 2: "SGM_E_UNSUPPORTED", 3: "SGM_E_GEOMETRY",
@@ -127,13 +127,19 @@ YOSHIDA4 = (1.0 / (2.0 - _CBRT2), -_CBRT2 / (2.0 - _CBRT2), 1.0 / (2.0 - _CBRT2)
 class Plan:
     """Owning wrapper of an ``sgm_plan`` (marshalling only)."""
 
-    def __init__(self, n_el, degree, geom_ctrl=None, quad_points=0, device=0):
+    def __init__(self, n_el, degree, geom_ctrl=None, quad_points=0, device=0, geom_weights=None):
+        """geom_ctrl: control points [(nz+p)][(ny+p)][(nx+p)][3], or any object with arrays .P (points)
+        and .w (weights) describing a rational map; geom_weights: weights of a rational map."""
         n = (n_el,) * 3 if np.isscalar(n_el) else tuple(n_el)
         self.n_el, self.p, self.device = n, degree, device
+        if geom_ctrl is not None and hasattr(geom_ctrl, "P") and hasattr(geom_ctrl, "w"):
+            geom_ctrl, geom_weights = geom_ctrl.P, geom_ctrl.w
         self._ctrl = None if geom_ctrl is None else np.ascontiguousarray(geom_ctrl, dtype=np.float64)
+        self._wts = None if geom_weights is None else np.ascontiguousarray(geom_weights, dtype=np.float64)
         self.geom = geom_ctrl is not None
         desc = sgm_plan_desc((c_int * 3)(*n), degree,
-                             None if self._ctrl is None else self._ctrl.ctypes.data, quad_points, device)
+                             None if self._ctrl is None else self._ctrl.ctypes.data, quad_points, device,
+                             None if self._wts is None else self._wts.ctypes.data)
         h = c_void_p()
         check(sgm_plan_create(ctypes.byref(desc), ctypes.byref(h)), "sgm_plan_create")
         self.h = h.value

@@ -546,6 +546,14 @@ sgm_status sgm_plan_create(const sgm_plan_desc* desc, sgm_plan* out) {
     P->has_geom = true;
     size_t nc = size_t(P->n[0] + p) * (P->n[1] + p) * (P->n[2] + p) * 3;
     P->ctrl.assign(desc->geom_ctrl, desc->geom_ctrl + nc);
+    if (desc->geom_weights) {
+      P->wts.assign(desc->geom_weights, desc->geom_weights + nc / 3);
+      for (double w : P->wts)
+        if (!(w > 0.0) || !std::isfinite(w)) {
+          delete P;
+          return fail(SGM_E_GEOMETRY, "rational map weights must be positive and finite");
+        }
+    }
   }
   sgm_status st = build_tables(*P, err);
   if (st == SGM_OK) st = build_geometry(*P, err);

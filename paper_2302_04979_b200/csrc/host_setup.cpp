@@ -530,21 +530,35 @@ struct GeoEval {
     const double* dz = &d[2][(size_t(ez) * Q + qz) * nl];
     for (int i = 0; i < 3; ++i) F[i] = 0.0;
     for (int i = 0; i < 9; ++i) DF[i] = 0.0;
+    const bool rat = !P.wts.empty();
+    double W = 0.0, dW[3] = {0.0, 0.0, 0.0};  // rational map: denominator sum w N and its gradient
     for (int k = 0; k < nl; ++k)
       for (int j = 0; j < nl; ++j)
         for (int i = 0; i < nl; ++i) {
-          const double* c = &P.ctrl[((size_t(ez + k) * NY + (ey + j)) * NX + (ex + i)) * 3];
-          double w0 = vx[i] * vy[j] * vz[k];
-          double wx = dx[i] * vy[j] * vz[k];
-          double wy = vx[i] * dy[j] * vz[k];
-          double wz = vx[i] * vy[j] * dz[k];
+          const size_t id = (size_t(ez + k) * NY + (ey + j)) * NX + (ex + i);
+          const double* c = &P.ctrl[id * 3];
+          const double wt = rat ? P.wts[id] : 1.0;
+          double w0 = wt * vx[i] * vy[j] * vz[k];
+          double wx = wt * dx[i] * vy[j] * vz[k];
+          double wy = wt * vx[i] * dy[j] * vz[k];
+          double wz = wt * vx[i] * vy[j] * dz[k];
           for (int r = 0; r < 3; ++r) {
             F[r] += c[r] * w0;
             DF[r * 3 + 0] += c[r] * wx;
             DF[r * 3 + 1] += c[r] * wy;
             DF[r * 3 + 2] += c[r] * wz;
           }
+          W += w0;
+          dW[0] += wx;
+          dW[1] += wy;
+          dW[2] += wz;
         }
+    if (rat) {
+      // F = N / W,  dF_r/dx^_j = (dN_r/dx^_j - F_r dW/dx^_j) / W   (quotient rule)
+      for (int r = 0; r < 3; ++r) F[r] /= W;
+      for (int r = 0; r < 3; ++r)
+        for (int j = 0; j < 3; ++j) DF[r * 3 + j] = (DF[r * 3 + j] - F[r] * dW[j]) / W;
+    }
   }
 };
 

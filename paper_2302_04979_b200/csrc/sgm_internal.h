@@ -73,6 +73,7 @@ struct Plan {
   Axis ax[3];
   bool has_geom = false;
   std::vector<double> ctrl;           // (nz+p)(ny+p)(nx+p)*3
+  std::vector<double> wts;            // rational map weights (nz+p)(ny+p)(nx+p); empty = polynomial
   bool affine_diag = true;            // DF constant diagonal
   double L_aff[3] = {1, 1, 1};        // diagonal of DF if affine_diag
   size_t n_qp = 0;

@@ -131,3 +131,21 @@ def test_reduced_schedule_identities_hold(p, n, monkeypatch):
     assert S.Plan(n, p, device=-1).reduced_schedule()
     monkeypatch.setenv("SGM_NODIAG", "1")
     assert not S.Plan(n, p, device=-1).reduced_schedule()
+
+
+def test_rational_map_host_geometry():
+    """A rational (NURBS) map through the C ABI: the plan's physical quadrature points equal the
+    oracle's quotient-rule evaluation (quarter annulus), the Hodge stars are general, and
+    non-positive weights are refused with SGM_E_GEOMETRY."""
+    from oracle import workloads as W
+    from oracle.assemble import Quad, physical_qp
+    n = (2, 3, 2)
+    g = W.quarter_annulus(n)
+    pl = S.Plan(n, 2, geom_ctrl=g, device=-1)
+    assert np.abs(pl.qp_coords() - physical_qp(Quad(2, n), g).reshape(-1, 3)).max() < 1e-15
+    assert not pl.separable(S.MASS_EPS) and not pl.separable(S.MASS_MU)
+    w = g.w.copy()
+    w[0, 1, 1] = -1.0
+    with pytest.raises(S.SgmError) as ei:
+        S.Plan(n, 2, geom_ctrl=g.P, geom_weights=w, device=-1)
+    assert "SGM_E_GEOMETRY" in str(ei.value)

@@ -438,3 +438,28 @@ def test_graph_replay_with_per_step_amplitude():
     ref = tb.run(*st, dt, len(amps), jhat, amps)
     for x, y in zip(out, ref):
         assert rel(x, y) < 1e-10
+
+
+@pytest.mark.parametrize("n", [(6, 7, 5), 8])
+def test_rational_quarter_annulus(n):
+    """The coaxial-cable cross-section as an exact degree-2 NURBS map (quarter annulus): general
+    Hodge applies and 1 / 20 steps against tier B (which evaluates the same rational map itself)."""
+    p = 2
+    g = W.quarter_annulus(n)
+    pl = S.Plan(n, p, geom_ctrl=g)
+    tb = TierB(p, n, ctrl=g)
+    rng = np.random.default_rng(61)
+    x = rng.standard_normal(tb.N_e)
+    y = torch.empty(tb.N_e, dtype=torch.float64, device="cuda")
+    pl.hodge_apply(S.MASS_EPS, dev(x), y)
+    assert rel(host(y), forms.join(tb.mass_eps(tb.split_e(x)))) < 1e-13
+    xb = rng.standard_normal(tb.N_h)
+    yb = torch.empty(tb.N_h, dtype=torch.float64, device="cuda")
+    pl.hodge_apply(S.MASS_MU, dev(xb), yb)
+    assert rel(host(yb), forms.join(tb.mass_mu(tb.split_h(xb)))) < 1e-13
+    st = _state(tb, 62)
+    dt = 0.4 * W.cfl_dt_max(tb)
+    for k, tol in ((1, 1e-11), (20, 1e-10)):
+        out = _run_gpu(pl, st, dt, k)
+        for a, b in zip(out, tb.run(*st, dt, k)):
+            assert rel(a, b) < tol
