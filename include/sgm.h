@@ -224,12 +224,16 @@ sgm_status sgm_plan_kernels_per_step(sgm_plan plan, int* n);
 /* Per-kernel timing of sgm_step (CUDA events recorded on the launching stream around every
    kernel when enabled).  Kernel classes: */
 typedef enum {
-  SGM_K_EPS_Z = 0,     /* z sweep of the eps half (Gram mat-vec . K1 factor solve), d -> t */
-  SGM_K_EPS_Y = 1,     /* y sweep of the eps half, t -> t */
-  SGM_K_EPS_X = 2,     /* x sweep of the eps half, t -> e */
-  SGM_K_MU_Z = 3,      /* z sweep of the mu half (Gram mat-vec . K~1 factor solve), b -> t */
-  SGM_K_MU_Y = 4,
-  SGM_K_MU_X = 5,      /* t -> h */
+  /* Separable Hodge stars, reduced schedule with concurrent launches:
+     EPS_Z = strided launch {0, 1 along z; 2 along y}, EPS_Y = {0 along y} and EPS_X = {1, 2 along x}
+     (concurrent), MU_Z = {2 along z, 1 along y} and MU_X = {0 along x} (concurrent; MU_Y unused).
+     Full three-axis schedule (SGM_NODIAG=1) and general-Hodge solves: the z, y, x sweeps. */
+  SGM_K_EPS_Z = 0,     /* eps half, first sweep launch (Gram mat-vec . K1 factor solve), d -> t */
+  SGM_K_EPS_Y = 1,     /* eps half, y-line sweep */
+  SGM_K_EPS_X = 2,     /* eps half, x-line sweep (writes e) */
+  SGM_K_MU_Z = 3,      /* mu half, strided sweep (Gram mat-vec . K~1 factor solve), b -> h */
+  SGM_K_MU_Y = 4,      /* mu half, y-line sweep (unmerged or full schedule only) */
+  SGM_K_MU_X = 5,      /* mu half, x-line sweep (writes h) */
   SGM_K_UPDATE = 6,    /* Ampere / Faraday update d += dt (D~1 h - s j), b -= dt D1 e (both halves) */
   SGM_K_HODGE_GENERAL = 7, /* sum-factorised mass apply with quadrature weights (general Hodge) */
   SGM_K_SOLVE_Z = 8,   /* solve-only z sweep (general-Hodge path) */
