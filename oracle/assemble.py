@@ -219,6 +219,24 @@ def mass2(quad, cplx, gamma_qp=None, ctrl=None):
     return _blocks_to_sparse(blocks)
 
 
+def mass1(quad, cplx, gamma_qp=None, ctrl=None):
+    """1-form mass matrix with weight gamma (scheme 1: M^1_eps for cplx='primal' on
+    X^1_{h,0}, M~^1_mu for cplx='dual' on X~^1):  M[i,j] = int gamma phys(phi_i) . phys(phi_j) dx
+    with the 1-form pull-back phys(phi) = DF^{-T} phi^, i.e. the weight DF^{-1} DF^{-T} det DF.
+    gamma_qp: gamma (eps or mu) at the quadrature points, element-major; None = 1."""
+    Phi = [basis_at_qp(quad, cplx, 1, c) for c in range(3)]
+    _, DF = geometry_at_qp(quad, ctrl)
+    det = np.linalg.det(DF)
+    Dinv = np.linalg.inv(DF)
+    G = np.einsum("qik,qjk->qij", Dinv, Dinv) * det[:, None, None]   # DF^{-1} DF^{-T} det
+    g = np.ones(quad.nqp) if gamma_qp is None else qp_elem_to_grid(gamma_qp, quad.n, quad.Q)
+    blocks = [[None] * 3 for _ in range(3)]
+    for c in range(3):
+        for c2 in range(3):
+            blocks[c][c2] = Phi[c].T @ sp.diags(G[:, c, c2] * g * quad.w) @ Phi[c2]
+    return _blocks_to_sparse(blocks)
+
+
 def physical_qp(quad, ctrl=None):
     """Physical coordinates F(x_q) in element-major layout [ez][ey][ex][qz][qy][qx][3]."""
     F, _ = geometry_at_qp(quad, ctrl)

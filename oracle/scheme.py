@@ -17,7 +17,7 @@ import scipy.sparse as sp
 import scipy.sparse.linalg as spla
 
 from . import forms
-from .assemble import Quad, pairing, mass2
+from .assemble import Quad, pairing, mass1, mass2
 
 
 class TierA:
@@ -77,3 +77,31 @@ class TierA:
     def gauss(self, d, b):
         """(||D~2 d||_inf, ||D2 b||_inf): discrete Gauss laws."""
         return float(np.max(np.abs(self.Dt2 @ d), initial=0.0)), float(np.max(np.abs(self.D2 @ b), initial=0.0))
+
+
+class TierA1(TierA):
+    """Tier A of the FIRST scheme (eqs. discrete1_*): the Hodge stars solve the 1-form
+    mass matrices,
+        M^1_eps e = K~2 d,     M~^1_mu h = K2 b,      K~2 = K1^T, K2 = K~1^T,
+    by SuperLU on the assembled masses; Ampere / Faraday updates as in scheme 2.  eps_qp, mu_qp:
+    the materials themselves (not their inverses) at the quadrature points, element-major."""
+
+    def __init__(self, p, n, ctrl=None, eps_qp=None, mu_qp=None, Q=None):
+        super().__init__(p, n, ctrl=ctrl, Q=Q)
+        self.M1eps = mass1(self.quad, "primal", eps_qp, ctrl)
+        self.M1mu = mass1(self.quad, "dual", mu_qp, ctrl)
+        self._lu_M1eps = spla.splu(self.M1eps.tocsc())
+        self._lu_M1mu = spla.splu(self.M1mu.tocsc())
+
+    def hodge_eps(self, d):
+        return self._lu_M1eps.solve(self.K1.T @ d)        # eq. discrete1_hodge_eps
+
+    def hodge_mu(self, b):
+        return self._lu_M1mu.solve(self.Kt1.T @ b)        # eq. discrete1_hodge_mu
+
+    def step(self, d, e, b, h, dt, jhat=None, s=1.0):
+        d = d + dt * (self.Dt1 @ h - (s * jhat if jhat is not None else 0.0))   # eq. discrete1_ampere
+        e = self.hodge_eps(d)
+        b = b - dt * (self.D1 @ e)                                            # eq. discrete1_faraday
+        h = self.hodge_mu(b)
+        return d, e, b, h

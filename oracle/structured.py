@@ -252,3 +252,50 @@ class TierB:
     def gauss(self, d, b):
         return (float(np.max(np.abs(div_dual(self.split_e(d))), initial=0.0)),
                 float(np.max(np.abs(div_primal(self.split_h(b))), initial=0.0)))
+
+
+class TierB1(TierB):
+    """Tier B of the first scheme for separable Hodge stars (identity map, constant eps, mu):
+    M^1_eps and M~^1_mu are Kronecker products of 1D Grams (primal 1-forms: Gamma of the CS basis of
+    S_{p-1} along the own axis, Gamma of trimmed S_p along the others; dual 1-forms: Gamma of the CS
+    basis of S_{p-2} own, Gamma of S_{p-1} B-splines others), inverted mode by mode with dense 1D
+    inverses; e = M^1_eps^{-1} K1^T d, h = M~^1_mu^{-1} K~1^T b."""
+
+    def __init__(self, p, n, eps=1.0, mu=1.0, Q=None):
+        super().__init__(p, n, Q=Q)
+        self.eps, self.mu = float(eps), float(mu)
+        self.GCinv1 = [np.linalg.inv(G) for G in self.GamC1]
+        self.GBinvp = [np.linalg.inv(G) for G in self.GamBp]
+        self.GCinv2 = [np.linalg.inv(G) for G in self.GamC2]
+        self.GBinv1 = [np.linalg.inv(G) for G in self.GamB1]
+
+    def hodge_eps(self, d):
+        r = self.apply_K1(self.split_e(d), T=True)
+        out = []
+        for c in range(3):
+            A = [self.GCinv1[a] if a == c else self.GBinvp[a] for a in range(3)]
+            out.append(kron3(A[0], A[1], A[2], r[c]) / self.eps)
+        return forms.join(out)
+
+    def hodge_mu(self, b):
+        r = self.apply_Kt1(self.split_h(b), T=True)
+        out = []
+        for c in range(3):
+            A = [self.GCinv2[a] if a == c else self.GBinv1[a] for a in range(3)]
+            out.append(kron3(A[0], A[1], A[2], r[c]) / self.mu)
+        return forms.join(out)
+
+    def step(self, d, e, b, h, dt, jhat=None, s=1.0):
+        dd, bb = self.split_e(d), self.split_h(b)
+        cd = curl_dual(self.split_h(h))
+        if jhat is not None:
+            j = self.split_e(jhat)
+            dd = [dd[c] + dt * (cd[c] - s * j[c]) for c in range(3)]
+        else:
+            dd = [dd[c] + dt * cd[c] for c in range(3)]
+        d = forms.join(dd)
+        e = self.hodge_eps(d)
+        ce = curl_primal(self.split_e(e))
+        b = forms.join([bb[c] - dt * ce[c] for c in range(3)])
+        h = self.hodge_mu(b)
+        return d, e, b, h

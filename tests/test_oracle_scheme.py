@@ -383,3 +383,62 @@ def test_rational_map_tier_b_equals_tier_a(n):
         d, e, b, h = A.step(d, e, b, h, dt)
         Es.append(0.5 * d @ (A.K1 @ e) + 0.5 * bp @ (A.Kt1 @ h))
     assert (max(Es) - min(Es)) / abs(np.mean(Es)) < 1e-12
+
+
+# ---- the first scheme (mass-matrix Hodge stars) ----
+
+@pytest.mark.parametrize("p,n,tol", [(2, 3, 1e-14), (3, (3, 2, 4), 1e-12), (4, 2, 5e-11)])
+def test_scheme1_tier_b_equals_tier_a(p, n, tol):
+    """Tier A (assembled 1-form masses M^1_eps, M~^1_mu, SuperLU; eqs. discrete1_*) and tier B
+    (Kronecker Grams, dense 1D inverses) agree; tolerance ~ eps x cond of the 1D Grams."""
+    from oracle.scheme import TierA1
+    from oracle.structured import TierB1
+    A, B = TierA1(p, n), TierB1(p, n)
+    st = _rand_state(A.N_e, A.N_h, 71)
+    j = np.random.default_rng(72).standard_normal(A.N_e)
+    for x, y in zip(B.step(*st, 0.01, j, 0.6), A.step(*st, 0.01, j, 0.6)):
+        assert rel(x, y) < tol
+
+
+def test_mass1_affine_scaling():
+    """For F(x) = diag(L) x the 1-form mass pulls back with DF^{-1} DF^{-T} det DF = diag(L)^{-2} prod L:
+    block c of M^1 equals prod(L) / L_c^2 times the identity-geometry block (closed form)."""
+    from oracle.assemble import mass1, Quad as Qd, identity_ctrl
+    p, n = 2, (2, 3, 2)
+    L = np.array([2.0, 0.5, 1.5])
+    q = Qd(p, n)
+    M0 = mass1(q, "primal").toarray()
+    ML = mass1(q, "primal", ctrl=identity_ctrl(p, n) * L).toarray()
+    off = forms.offsets("primal", 1, p, n)
+    for c in range(3):
+        s = slice(off[c], off[c + 1])
+        assert np.abs(ML[s, s] - np.prod(L) / L[c] ** 2 * M0[s, s]).max() < 1e-14 * np.abs(M0[s, s]).max()
+
+
+def test_scheme1_energy_and_better_cfl():
+    """Scheme 1 conserves the modified energy 1/2 d.K1 e + 1/2 b^{n-1/2}.K~1 h^{n+1/2} (its energy
+    e.M^1 e = d.K1 e) and has the larger stable step (O(1/p^{3/2}) against
+    O(1/p^2) for scheme 2): dense leapfrog-operator spectra on a tiny grid."""
+    import scipy.linalg as sl
+    from oracle.scheme import TierA1
+    ratios = []
+    for p in (2, 3, 4):
+        A1, A = TierA1(p, 3), TierA(p, 3)
+        D1, Dt1 = A1.D1.toarray(), A1.Dt1.toarray()
+        H1e = np.linalg.solve(A1.M1eps.toarray(), A1.K1.T.toarray())
+        H1m = np.linalg.solve(A1.M1mu.toarray(), A1.Kt1.T.toarray())
+        H2e = np.linalg.solve(A.K1.toarray(), A.Meps.toarray())
+        H2m = np.linalg.solve(A.Kt1.toarray(), A.Mmu.toarray())
+        l1 = np.linalg.eigvals(Dt1 @ H1m @ D1 @ H1e).real.max()
+        l2 = np.linalg.eigvals(Dt1 @ H2m @ D1 @ H2e).real.max()
+        ratios.append(np.sqrt(l2 / l1))
+        if p == 3:
+            d, _, b, _ = _rand_state(A1.N_e, A1.N_h, 73)
+            e, h = A1.hodge_eps(d), A1.hodge_mu(b)
+            Es = []
+            for _ in range(200):
+                bp = b
+                d, e, b, h = A1.step(d, e, b, h, 0.9 * 2 / np.sqrt(l1))
+                Es.append(0.5 * d @ (A1.K1 @ e) + 0.5 * bp @ (A1.Kt1 @ h))
+            assert (max(Es) - min(Es)) / abs(np.mean(Es)) < 1e-13
+    assert ratios[0] > 1 and ratios[1] > ratios[0] and ratios[2] > ratios[1], ratios
