@@ -58,11 +58,20 @@ def parse():
     ap.add_argument("--n", type=int, default=128)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--scheme", type=int, default=2, choices=[1, 2],
+                    help="Hodge stars: 2 = pairing solves (the paper's method, default), 1 = mass solves")
     return ap.parse_args()
 
 
 def workload(args):
     """(p, n, description, geometry ctrl or None, eps at qp or None, has_source)."""
+    p, n, desc, geo, mat, src = _workload(args)
+    if getattr(args, "scheme", 2) == 1:
+        desc += ", scheme 1 (mass-matrix Hodge stars)"
+    return p, n, desc, geo, mat, src
+
+
+def _workload(args):
     if args.config == "c5":
         return args.p, args.n, f"C5 full step p={args.p} n_el={args.n}^3 identity eps=mu=1", None, None, False
     if args.config == "c2":
@@ -151,6 +160,8 @@ def build_inputs(args, torch, S, dev):
         from oracle import workloads as W
         ctrl = W.interpolate_map(p, n, W.c3_map)
     pl = S.Plan(n, p, geom_ctrl=ctrl, device=dev.index or 0)
+    if getattr(args, "scheme", 2) == 1:
+        pl.set_scheme(1)
     if mat is not None:
         X = pl.qp_coords()
         if mat == "c3":

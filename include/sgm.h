@@ -211,6 +211,16 @@ sgm_status sgm_check_source(sgm_plan plan, const double* j_hat, void* workspace,
 sgm_status sgm_cfl(sgm_plan plan, double* x, double* e, double* b, double* h, int n_iter,
                    double* out_dev, void* workspace, size_t ws_bytes, void* stream);
 
+/* Select the discretization scheme of the Hodge stars used by sgm_step / sgm_step_composed /
+   sgm_hodge_star / sgm_cfl: 2 (default) = the paper's second scheme, pairing
+   solves e = K1^{-1} M~2_{1/eps} d, h = K~1^{-1} M2_{1/mu} b; 1 = the first scheme,
+   mass solves M^1_eps e = K~2 d, M~^1_mu h = K2 b with K~2 = K1^T, K2 = K~1^T.
+   Scheme 1 is built for the identity map, constant materials and p <= 3 (its 1-form masses are then
+   Kronecker products of 1D Grams, inverted mode by mode with the same sweeps; the own-axis factor
+   of e and the other-axis factors of h are again exactly diagonal); otherwise SGM_E_UNSUPPORTED.
+   While scheme 1 is selected, sgm_plan_set_material with per-point values is refused. */
+sgm_status sgm_plan_set_scheme(sgm_plan plan, int scheme);
+
 /* *on = 1 if separable Hodge stars use the reduced schedule (the diagonal 1D
    factors Hat M^{-1} Gamma_B^{p-1} = diag(1/s) and Hat M^{-T} Gamma_C^{p-1} = diag(s), verified at
    plan creation, replace their line sweeps by per-line scalings), 2 if in addition independent

@@ -70,6 +70,7 @@ _SIGS = {
     "sgm_check_source": [c_void_p, c_void_p, c_void_p, c_size_t, c_void_p],
     "sgm_plan_kernels_per_step": [c_void_p, ctypes.POINTER(c_int)],
     "sgm_plan_reduced_schedule": [c_void_p, ctypes.POINTER(c_int)],
+    "sgm_plan_set_scheme": [c_void_p, c_int],
     "sgm_plan_set_profiling": [c_void_p, c_int],
     "sgm_plan_profile": [c_void_p, c_void_p, c_void_p],
 }
@@ -210,6 +211,10 @@ class Plan:
         n = c_size_t()
         check(sgm_workspace_bytes(self.h, ctypes.byref(n)))
         return n.value
+
+    def set_scheme(self, scheme):
+        """1: mass-matrix Hodge stars (first scheme), 2: pairing solves (second scheme, default)."""
+        check(sgm_plan_set_scheme(self.h, int(scheme)), "sgm_plan_set_scheme")
 
     def schedule_mode(self):
         """0: full three-axis sweeps, 1: reduced separable schedule, 2: reduced with concurrent sweeps."""

@@ -194,8 +194,10 @@ void sweep_pass_list(const Plan& P, int kind, const PassComp* pc, int n, cudaStr
   a.solve = 1;
   // axes with the same element count have bitwise identical tables: use the first axis's copy so a
   // launch mixing such axes stages one table (shared memory decides whether two lines per thread fit)
+  const bool wide = pc[0].op == OP_S1_EPS_OTH_W;  // scheme-1 eps tables: layout p + 1
   auto tab_of = [&](const PassComp& q) {
-    return table(P, P.n[q.axis] == P.n[pc[0].axis] ? pc[0].axis : q.axis, q.op);
+    const int ax = P.n[q.axis] == P.n[pc[0].axis] ? pc[0].axis : q.axis;
+    return wide ? P.wide_dev + size_t(ax) * P.Lmax * RowLayoutRT(P.p + 1).RS : table(P, ax, q.op);
   };
   a.tabs[0] = tab_of(pc[0]);
   a.tabs[1] = nullptr;
@@ -210,9 +212,9 @@ void sweep_pass_list(const Plan& P, int kind, const PassComp* pc, int n, cudaStr
     const int axis = q.axis;
     // transverse coordinate slots: z-lines (x, y), y-lines (x, z), x-lines (y, z)
     const int t0 = (axis == 0) ? 1 : 0, t1 = (axis == 2) ? 1 : 2;
-    a.band_hw = std::max(a.band_hw, P.band_hw[axis][q.op]);
-    a.spike_kh = std::max(a.spike_kh, P.spike_kh[axis][q.op]);
-    a.spike_kf = std::max(a.spike_kf, P.spike_kf[axis][q.op]);
+    a.band_hw = std::max(a.band_hw, wide ? P.wide_band_hw[axis] : P.band_hw[axis][q.op]);
+    a.spike_kh = std::max(a.spike_kh, wide ? P.wide_kh[axis] : P.spike_kh[axis][q.op]);
+    a.spike_kf = std::max(a.spike_kf, wide ? P.wide_kf[axis] : P.spike_kf[axis][q.op]);
     SweepComp& C = a.comp[i];
     comp_shape(P, kind, q.c, C.ext);
     C.in = const_cast<double*>(q.in);
@@ -224,7 +226,7 @@ void sweep_pass_list(const Plan& P, int kind, const PassComp* pc, int n, cudaStr
     C.dline[0] = q.dg[t0] >= 0 ? diag_factor(P, t0, q.dg[t0]) : nullptr;
     C.dline[1] = q.dg[t1] >= 0 ? diag_factor(P, t1, q.dg[t1]) : nullptr;
   }
-  launch_sweep(P.p, P.seg[pc[0].axis], a, st);
+  launch_sweep(wide ? P.p + 1 : P.p, P.seg[pc[0].axis], a, st);
 }
 
 // The mu star's z and y sweeps share one launch when their axes have equal table geometry.
@@ -275,7 +277,8 @@ void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* 
   const int kz = kind == 0 ? SGM_K_EPS_Z : SGM_K_MU_Z, ky = kind == 0 ? SGM_K_EPS_Y : SGM_K_MU_Y,
             kx = kind == 0 ? SGM_K_EPS_X : SGM_K_MU_X;
   if (kind == 0) {
-    const int op = OP_EPS_OTH;
+    // scheme 2: Hat G^{-1} Gamma_C^{p-2}; scheme 1: Gamma_B^p^{-1} Hat G^T (own axis: diag(1/s) in both)
+    const int op = P.scheme == 1 ? OP_S1_EPS_OTH_W : OP_EPS_OTH;
     if (P.fork_enabled && eps_merged(P)) {
       // strided pass {0 along z, 1 along z, 2 along y}, then concurrently {0 along y} (strided,
       // 1/3 of the SMs) and {1, 2 along x} (2/3 of the SMs, plan-owned stream)
@@ -297,7 +300,8 @@ void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* 
     { ProfScope ps(P, ky, st); sweep_pass_list(P, 0, yy, 2, st, 0); }
     { ProfScope ps(P, kx, st); sweep_pass_list(P, 0, xx, 2, st, 1); }
   } else {
-    const int op = OP_MU_OWN;
+    // scheme 2: Hat G^{-T} Gamma_B^p; scheme 1: Gamma_C^{p-2}^{-1} Hat G (other axes: diag(s) in both)
+    const int op = P.scheme == 1 ? OP_S1_MU_OWN : OP_MU_OWN;
     PassComp z[1] = {{2, 2, X[2], Y[2], op, {1, 1, -1}, M.scale[2]}};
     PassComp yy[1] = {{1, 1, X[1], Y[1], op, {1, -1, 1}, M.scale[1]}};
     PassComp xx[1] = {{0, 0, X[0], Y[0], op, {-1, 1, 1}, M.scale[0]}};
@@ -583,6 +587,14 @@ sgm_status sgm_plan_create(const sgm_plan_desc* desc, sgm_plan* out) {
       return fail(SGM_E_NOMEM, "cudaMalloc failed for tables");
     }
     cudaMemcpy(P->tables_dev, P->tables_host.data(), tb, cudaMemcpyHostToDevice);
+    if (!P->wide_host.empty()) {
+      const size_t wb = P->wide_host.size() * sizeof(double);
+      if (cudaMalloc(&P->wide_dev, wb) != cudaSuccess) {
+        delete P;
+        return fail(SGM_E_NOMEM, "cudaMalloc failed for tables");
+      }
+      cudaMemcpy(P->wide_dev, P->wide_host.data(), wb, cudaMemcpyHostToDevice);
+    }
     {
       cudaStream_t aux;
       cudaEvent_t e1, e2;
@@ -621,6 +633,7 @@ sgm_status sgm_plan_destroy(sgm_plan plan) {
     DeviceGuard g(P->device);
     if (P->graph_exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec));
     cudaFree(P->tables_dev);
+    cudaFree(P->wide_dev);
     cudaFree(P->basis_dev);
     cudaFree(P->first_dev);
     for (int m = 0; m < 2; ++m) cudaFree(P->mass[m].W_dev);
@@ -693,6 +706,27 @@ sgm_status sgm_plan_hodge_separable(sgm_plan plan, sgm_mass mass, int* separable
   return SGM_OK;
 }
 
+sgm_status sgm_plan_set_scheme(sgm_plan plan, int scheme) {
+  if (!plan) return fail(SGM_E_INVALID_ARG, "plan is NULL");
+  Plan* P = PL(plan);
+  if (scheme != 1 && scheme != 2) return fail(SGM_E_INVALID_ARG, "scheme must be 1 or 2");
+  if (scheme == 1) {
+    if (P->has_geom) return fail(SGM_E_UNSUPPORTED, "scheme 1 is built for the identity map only");
+    if (P->wide_host.empty()) return fail(SGM_E_UNSUPPORTED, "scheme 1 is built for p <= 3");
+    if (!P->diag_ok) return fail(SGM_E_UNSUPPORTED, "scheme 1 needs the reduced separable schedule");
+    for (int m = 0; m < 2; ++m)
+      if (P->mass[m].kind != HODGE_SEPARABLE)
+        return fail(SGM_E_UNSUPPORTED, "scheme 1 is built for constant materials (separable stars) only");
+  }
+  if (P->scheme != scheme && P->graph_exec) {
+    DeviceGuard g(P->device);
+    cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec));
+    P->graph_exec = nullptr;
+  }
+  P->scheme = scheme;
+  return SGM_OK;
+}
+
 sgm_status sgm_plan_reduced_schedule(sgm_plan plan, int* on) {
   if (!plan || !on) return fail(SGM_E_INVALID_ARG, "NULL argument");
   const Plan& P = *PL(plan);
@@ -701,6 +735,8 @@ sgm_status sgm_plan_reduced_schedule(sgm_plan plan, int* on) {
 }
 
 sgm_status sgm_plan_set_material(sgm_plan plan, sgm_material which, const double* values, double c) {
+  if (plan && values && PL(plan)->scheme == 1)
+    return fail(SGM_E_UNSUPPORTED, "scheme 1 is built for constant materials; sgm_plan_set_scheme(plan, 2) first");
   if (plan && PL(plan)->graph_exec) {  // captured launches embed the old weights and kinds
     DeviceGuard g0(PL(plan)->device);
     cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(PL(plan)->graph_exec));

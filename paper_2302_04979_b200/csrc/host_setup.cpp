@@ -444,6 +444,18 @@ sgm_status build_tables(Plan& P, std::string& err) {
     if ((st = fill_table(T(OP_APPLY_G), p, X.a, R, SEG, &X.G, nullptr, err)) != SGM_OK) return st;
     if ((st = fill_table(T(OP_APPLY_GT), p, X.a, R, SEG, &GT, nullptr, err)) != SGM_OK) return st;
     if ((st = fill_table(T(OP_APPLY_MT), p, X.b, R, SEG, &MT, nullptr, err)) != SGM_OK) return st;
+    // scheme 1: h_c own factor Gamma_C^{p-2}^{-1} Hat G; e_c other factor
+    // Gamma_B^p^{-1} Hat G^T, whose LU has half-bandwidth p -> wide layout p + 1 (p <= 3 only)
+    if ((st = fill_table(T(OP_S1_MU_OWN), p, X.a, R, SEG, &X.G, &X.GC2, err)) != SGM_OK) return st;
+    if (p <= 3) {
+      const int RSw = RowLayoutRT(p + 1).RS;
+      if (P.wide_host.empty()) P.wide_host.assign(size_t(3) * Rmax * RSw, 0.0);
+      double* Tw = P.wide_host.data() + size_t(a) * Rmax * RSw;
+      if ((st = fill_table(Tw, p + 1, X.a, R, SEG, &GT, &X.GBp, err)) != SGM_OK) return st;
+      P.wide_band_hw[a] = table_band_hw(Tw, p + 1, X.a);
+      if (noskip) P.wide_kh[a] = P.wide_kf[a] = (X.a + SEG - 1) / SEG;
+      else spike_reach(Tw, p + 1, X.a, SEG, P.wide_kh[a], P.wide_kf[a]);
+    }
     // Diagonal 1D factors ("reduced separable schedule"): with the CS normalisation
     // D'_k = s_k B'_k, Hat M = Gamma_B^{p-1} diag(s) and Gamma_C^{p-1} =
     // diag(s) Gamma_B^{p-1} diag(s), so the own-axis factor of the eps Hodge star,
@@ -475,11 +487,11 @@ sgm_status build_tables(Plan& P, std::string& err) {
         fprintf(stderr, "sgm plan: axis %d diagonal factors: |M - G diag(s)| %.3g, |Gc - diag(s) G diag(s)| %.3g\n", a,
                 eM / mM, eC / mC);
     }
-    const int Ls[OP_COUNT] = {X.b, X.a, X.a, X.b, X.b, X.a, X.a, X.b};
+    const int Ls[OP_COUNT] = {X.b, X.a, X.a, X.b, X.b, X.a, X.a, X.b, X.a};
     for (int op = 0; op < OP_COUNT; ++op) {
       const int S = (Ls[op] + SEG - 1) / SEG;
       P.band_hw[a][op] = table_band_hw(T(op), p, Ls[op]);
-      if (noskip || op >= OP_APPLY_M) {
+      if (noskip || (op >= OP_APPLY_M && op <= OP_APPLY_MT)) {
         P.spike_kh[a][op] = P.spike_kf[a][op] = S;
       } else {
         spike_reach(T(op), p, Ls[op], SEG, P.spike_kh[a][op], P.spike_kf[a][op]);

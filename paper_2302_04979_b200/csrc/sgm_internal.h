@@ -40,7 +40,10 @@ enum Op {
   OP_APPLY_G = 5,  // band Hat G   (a)
   OP_APPLY_GT = 6, // band Hat G^T (a)
   OP_APPLY_MT = 7, // band Hat M^T (b)
-  OP_COUNT = 8
+  OP_S1_MU_OWN = 8,  // scheme 1, mu star own axis: band Hat G (a), LU(Gamma_C^{p-2})
+  OP_COUNT = 9,
+  OP_S1_EPS_OTH_W = 100  // scheme 1, eps star other axes: band Hat G^T (a), LU(Gamma_B^p) -- the
+                         // LU has half-bandwidth p: stored in the "wide" tables (layout p + 1)
 };
 
 enum HodgeKind { HODGE_SEPARABLE = 0, HODGE_SCALAR = 1, HODGE_FULL = 2 };
@@ -81,6 +84,10 @@ struct Plan {
   // device
   double* tables_dev = nullptr;       // [3][OP_COUNT][Lmax][RS] (seg_sweep.cuh row layout), then diag factors
   int Lmax = 0;                       // rows per table slot (max padded line length)
+  int scheme = 2;                     // 2: pairing solves; 1: mass solves
+  std::vector<double> wide_host;      // scheme-1 eps tables [3][Lmax][RowLayout<p+1>::RS] (p <= 3)
+  double* wide_dev = nullptr;
+  int wide_band_hw[3] = {}, wide_kh[3] = {}, wide_kf[3] = {};
   size_t diag_off = 0;                // offset (doubles) of the diagonal factors [3][2][Lmax]:
                                       // [axis][0] = 1/s (eps own axis), [axis][1] = s (mu other axes)
   bool diag_ok = true;                // reduced separable schedule usable (host_setup.cpp)

@@ -149,3 +149,27 @@ def test_rational_map_host_geometry():
     with pytest.raises(S.SgmError) as ei:
         S.Plan(n, 2, geom_ctrl=g.P, geom_weights=w, device=-1)
     assert "SGM_E_GEOMETRY" in str(ei.value)
+
+
+def test_scheme_selection_rules():
+    """sgm_plan_set_scheme: scheme 1 needs the identity map, constant materials and p <= 3."""
+    S.Plan(6, 3, device=-1).set_scheme(1)
+    S.Plan((3, 4, 5), 2, device=-1).set_scheme(1)
+    for make in (lambda: S.Plan(6, 4, device=-1),
+                 lambda: S.Plan(3, 2, geom_ctrl=W_curved(2, 3), device=-1)):
+        with pytest.raises(S.SgmError) as ei:
+            make().set_scheme(1)
+        assert "SGM_E_UNSUPPORTED" in str(ei.value)
+    pl = S.Plan(3, 2, device=-1)
+    pl.set_scheme(1)
+    with pytest.raises(S.SgmError):
+        pl.set_material(S.EPS, np.ones(pl.qp_count()))
+    pl.set_scheme(2)
+    pl.set_material(S.EPS, np.ones(pl.qp_count()))
+    with pytest.raises(S.SgmError):
+        pl.set_scheme(3)
+
+
+def W_curved(p, n):
+    from oracle import workloads as W
+    return W.interpolate_map(p, n, W.c3_map)

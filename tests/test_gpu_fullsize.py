@@ -148,3 +148,19 @@ def test_cfl_power_full_size(p):
         bound = 14.4 * 3 * n * n
         assert 0.97 * bound < o[0] <= bound * (1 + 1e-12), (o[0], bound)
     assert 0.97 * CFL_N[p] < o[1] * n < 1.06 * CFL_N[p], o[1] * n
+
+
+def test_scheme1_full_size():
+    """The first scheme at 128^3 p = 3 (bench --scheme 1 configuration) against oracle tier B1."""
+    from oracle.structured import TierB1
+    p, n = 3, 128
+    pl = S.Plan(n, p)
+    pl.set_scheme(1)
+    tb = TierB1(p, n)
+    d0, b0 = synth.normal(5, tb.N_e, tb.N_h)
+    st = (d0, tb.hodge_eps(d0), b0, tb.hodge_mu(b0))
+    dt = 0.5 * CFL_N[p] / n
+    dv = [dev(x) for x in st]
+    pl.step(*dv, dt, 1)
+    for a, r in zip(dv, tb.step(*st, dt)):
+        assert rel(host(a), r) < 1e-11

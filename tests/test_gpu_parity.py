@@ -463,3 +463,32 @@ def test_rational_quarter_annulus(n):
         out = _run_gpu(pl, st, dt, k)
         for a, b in zip(out, tb.run(*st, dt, k)):
             assert rel(a, b) < tol
+
+
+@pytest.mark.parametrize("p,n", [(2, (5, 9, 7)), (3, 11), (3, (9, 7, 6))])
+def test_scheme1_parity(p, n):
+    """The first scheme (mass-matrix Hodge stars) on the GPU against oracle tier B1:
+    the two Hodge stars, 1 and 30 steps, and the power-iteration stability limit."""
+    from oracle.structured import TierB1
+    pl = S.Plan(n, p)
+    pl.set_scheme(1)
+    tb = TierB1(p, n)
+    rng = np.random.default_rng(81)
+    x = rng.standard_normal(tb.N_e)
+    y = torch.empty(tb.N_e, dtype=torch.float64, device="cuda")
+    pl.hodge_star(S.MASS_EPS, dev(x), y)
+    assert rel(host(y), tb.hodge_eps(x)) < 1e-11
+    xb = rng.standard_normal(tb.N_h)
+    yb = torch.empty(tb.N_h, dtype=torch.float64, device="cuda")
+    pl.hodge_star(S.MASS_MU, dev(xb), yb)
+    assert rel(host(yb), tb.hodge_mu(xb)) < 1e-11
+    x0 = synth.rng(100).standard_normal(tb.N_e)
+    lam, dtmax, _, _ = W.cfl_power(tb, x0, 40)
+    out, _ = _cfl_gpu(pl, x0, 40)
+    assert abs(out[0] / lam - 1) < 1e-10
+    st = (x, tb.hodge_eps(x), xb, tb.hodge_mu(xb))
+    dt = 0.4 * dtmax
+    for k, tol in ((1, 1e-11), (30, 1e-10)):
+        o = _run_gpu(pl, st, dt, k)
+        for a, b in zip(o, tb.run(*st, dt, k)):
+            assert rel(a, b) < tol
