@@ -246,12 +246,12 @@ def fp64_peak_tflops(sm_mhz):
 def cpu_baseline(args, budget_s=10.0):
     """The oracle (tier B, as it stands) on this host: a bounded sample of the same workload."""
     import threadpoolctl
-    from oracle.structured import TierB
+    from oracle.structured import TierB, TierB1
     import synth
     p, n, desc, geo, mat, src = workload(args)
     if geo or mat:
         return None
-    tb = TierB(p, n)
+    tb = TierB(p, n) if getattr(args, "scheme", 2) == 2 else TierB1(p, n)
     d0, b0 = synth.normal(5, tb.N_e, tb.N_h)
     st = (d0, tb.hodge_eps(d0), b0, tb.hodge_mu(b0))
     dt = 0.5 * CFL_N[p] / n
@@ -275,13 +275,13 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     p, n, desc, geo, mat, src = workload(args)
-    from oracle.structured import TierB
+    from oracle.structured import TierB, TierB1
     import synth
     import threadpoolctl
     if geo or mat:
         print(json.dumps({"impl": "reference", "unavailable": "reference arm implemented for separable configs"}))
         return
-    tb = TierB(p, n)
+    tb = TierB(p, n) if getattr(args, "scheme", 2) == 2 else TierB1(p, n)
     d0, b0 = synth.normal(5, tb.N_e, tb.N_h)
     st = (d0, tb.hodge_eps(d0), b0, tb.hodge_mu(b0))
     dt = 0.5 * CFL_N[p] / n

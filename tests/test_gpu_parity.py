@@ -492,3 +492,21 @@ def test_scheme1_parity(p, n):
         o = _run_gpu(pl, st, dt, k)
         for a, b in zip(o, tb.run(*st, dt, k)):
             assert rel(a, b) < tol
+
+
+def test_scheme1_composed_yoshida():
+    """sgm_step_composed with the first scheme's Hodge stars against oracle compose.run_composed
+    on tier B1 (the composition only calls the stars and the curls)."""
+    from oracle import compose
+    from oracle.structured import TierB1
+    p, n = 3, (7, 6, 8)
+    pl = S.Plan(n, p)
+    pl.set_scheme(1)
+    tb = TierB1(p, n)
+    st = _state(tb, 91)
+    dt = 0.2 * W.cfl_dt_max(TierB(p, n))
+    d, e, b, h = (dev(x) for x in st)
+    pl.step_composed(d, e, b, h, dt, compose.YOSHIDA4, 6)
+    ref = compose.run_composed(tb, *st, dt, 6)
+    for x, y in zip((d, e, b, h), ref):
+        assert rel(host(x), y) < 1e-10
