@@ -108,6 +108,17 @@ def main(tag):
         L.append("\nAt 32³ and 64³ the working set sits in L2 and the kernels are launch/latency bound; at 160³ with "
                  "p ≥ 3 the strided sweeps have only two producer warps (14 consumer segments fill the 16-warp CTA) "
                  "and p = 4 no longer fits two lines per thread in shared memory.")
+    co = os.path.join(PR, "r1_cpu_oracle.jsonl")
+    if os.path.exists(co):
+        L.append("\n### CPU oracle per step on the GPU box's host (`scripts/oracle_timing.py`, `r1_cpu_oracle.jsonl`)\n")
+        L.append("The oracle as it stands (setup excluded, median of >= 3 steps after a warm-up); a reported "
+                 "baseline, not the target. Tier A = assembled matrices + SuperLU, tier B = Kronecker.\n")
+        L.append("| config | tier | s/step | DOF-updates/s | BLAS threads / cores |")
+        L.append("|---|---|---|---|---|")
+        for l in open(co):
+            d = json.loads(l)
+            L.append(f"| {d['config']} | {d['tier']} | {d['s_per_step']:.3g} | {d['dof_updates_per_s']:.3g} | "
+                     f"{d['blas_threads']}/{d['cores']} |")
     L.append("\nC4/C3 report the general Hodge against the fp64 peak (`bound: alu`, 37.2 TFLOP/s, DESIGN.md §6); its "
              "HBM view is in each line's `roofline.hbm_view`.\n")
     L.append("## Per-kernel ncu, one step of C5 p=3 128³ (serialised replay: compare shares, not absolutes)\n")
