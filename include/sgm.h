@@ -215,10 +215,14 @@ sgm_status sgm_cfl(sgm_plan plan, double* x, double* e, double* b, double* h, in
    sgm_hodge_star / sgm_cfl: 2 (default) = the paper's second scheme, pairing
    solves e = K1^{-1} M~2_{1/eps} d, h = K~1^{-1} M2_{1/mu} b; 1 = the first scheme,
    mass solves M^1_eps e = K~2 d, M~^1_mu h = K2 b with K~2 = K1^T, K2 = K~1^T.
-   Scheme 1 is built for the identity map, constant materials and p <= 3 (its 1-form masses are then
-   Kronecker products of 1D Grams, inverted mode by mode with the same sweeps; the own-axis factor
-   of e and the other-axis factors of h are again exactly diagonal); otherwise SGM_E_UNSUPPORTED.
-   While scheme 1 is selected, sgm_plan_set_material with per-point values is refused. */
+   Scheme 1 is built for p <= 3 (else SGM_E_UNSUPPORTED).  With the identity (axis-aligned affine)
+   map and constant materials its 1-form masses are Kronecker products of 1D Grams, inverted mode by
+   mode with the same sweeps (the own-axis factor of e and the other-axis factors of h are again
+   exactly diagonal).  Otherwise (curved map or variable material) each star solves its 1-form mass
+   by preconditioned conjugate gradients on the device: sum-factorised 1-form mass applies
+   (weights w gamma DF^{-1} DF^{-T} det DF), the separable star with the mean material as
+   preconditioner, a fixed iteration count (40; SGM_PCG_ITERS), no host synchronisation.  The 1-form
+   weights are rebuilt by sgm_plan_set_material while scheme 1 is selected. */
 sgm_status sgm_plan_set_scheme(sgm_plan plan, int scheme);
 
 /* *on = 1 if separable Hodge stars use the reduced schedule (the diagonal 1D

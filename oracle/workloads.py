@@ -292,9 +292,10 @@ def cfl_power(tb, x0, n_iter):
 
 def _ops(tb):
     """(e <- K1^{-1}M~2 x, h <- K~1^{-1}M2 b, K1 e, K~1 h, D1, D~1) for tier A or tier B."""
-    if hasattr(tb, "Meps"):  # tier A: assembled sparse matrices
-        return (lambda x: tb.solve_K1(tb.Meps @ x), lambda b: tb.solve_Kt1(tb.Mmu @ b),
-                lambda e: tb.K1 @ e, lambda h: tb.Kt1 @ h,
+    if hasattr(tb, "Meps"):  # tier A: assembled sparse matrices (TierA1: the scheme-1 stars)
+        he = tb.hodge_eps if hasattr(tb, "hodge_eps") else (lambda x: tb.solve_K1(tb.Meps @ x))
+        hm = tb.hodge_mu if hasattr(tb, "hodge_mu") else (lambda b: tb.solve_Kt1(tb.Mmu @ b))
+        return (he, hm, lambda e: tb.K1 @ e, lambda h: tb.Kt1 @ h,
                 lambda e: tb.D1 @ e, lambda h: tb.Dt1 @ h)
     from .structured import curl_primal
     return (tb.hodge_eps, tb.hodge_mu,

@@ -267,9 +267,12 @@ void fork_join(Plan& P, cudaStream_t st, F1&& f1, F2&& f2) {
 //                 scaled by 1/s along axis c: z pass {0,1}, y pass {0 -> y, 2}, x pass {1,2 -> y};
 //   mu  (kind 1): component c is swept (Gamma_B^{p}, LU Hat G^T) along axis c only and scaled by
 //                 s along the other two: strided pass {2 along z, 1 along y} (or two passes), x pass {0}.
-void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* t, cudaStream_t st) {
+void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* t, cudaStream_t st,
+                        const double* scale = nullptr) {
   const int kind = (which == SGM_MASS_EPS) ? 0 : 1;
-  const MassData& M = P.mass[which];
+  struct {
+    const double* scale;
+  } M{scale ? scale : P.mass[which].scale};
   double *X[3], *Y[3], *T[3];
   comps_of(P, kind, x, X);
   comps_of(P, kind, y, Y);
@@ -358,9 +361,12 @@ PrologueArgs make_pro(const Plan& P, int src_kind, const double* src, const doub
   return pa;
 }
 
-void hodge_args(const Plan& P, int which, const double* x, double* y, HodgeArgs& h) {
+// form1 = false: the 2-form masses of scheme 2 (eps: dual 2-forms, mu: primal 2-forms);
+// form1 = true:  the 1-form masses of scheme 1 (eps: primal 1-forms of e, mu: dual 1-forms of h)
+void hodge_args(const Plan& P, int which, const double* x, double* y, HodgeArgs& h, bool form1 = false) {
   std::memset(&h, 0, sizeof(h));
   int kind = (which == SGM_MASS_EPS) ? 0 : 1;
+  const MassData& MD = form1 ? P.mass1[which] : P.mass[which];
   double *X[3], *Y[3];
   comps_of(P, kind, x, X);
   comps_of(P, kind, y, Y);
@@ -368,13 +374,21 @@ void hodge_args(const Plan& P, int which, const double* x, double* y, HodgeArgs&
     h.x[c] = X[c];
     h.y[c] = Y[c];
     comp_shape(P, kind, c, h.ext[c]);
-    h.scale[c] = P.mass[which].scale[c];
+    h.scale[c] = MD.scale[c];
   }
-  h.W = P.mass[which].W_dev;
-  h.full = (P.mass[which].kind == HODGE_FULL) ? 1 : 0;
-  // own/other univariate spaces: dual 2-forms own Dp1 (2), other Dp2 (3);
-  // primal 2-forms own Sp (0), other Sp1 (1)   (sec. 4.1)
-  int own = (which == SGM_MASS_EPS) ? 2 : 0, oth = (which == SGM_MASS_EPS) ? 3 : 1;
+  h.W = MD.W_dev;
+  h.full = (MD.kind == HODGE_FULL) ? 1 : 0;
+  // own/other univariate spaces (space ids of basis_values_1d: Sp 0, Sp1 1, Dp1 2, Dp2 3):
+  //   dual 2-forms own Dp1, other Dp2; primal 2-forms own Sp, other Sp1   (sec. 4.1)
+  //   primal 1-forms own Sp1, other Sp;  dual 1-forms own Dp2, other Dp1
+  int own, oth;
+  if (!form1) {
+    own = (which == SGM_MASS_EPS) ? 2 : 0;
+    oth = (which == SGM_MASS_EPS) ? 3 : 1;
+  } else {
+    own = (which == SGM_MASS_EPS) ? 1 : 3;
+    oth = (which == SGM_MASS_EPS) ? 0 : 2;
+  }
   h.basis = P.basis_dev;
   h.first = P.first_dev;
   for (int a = 0; a < 3; ++a) {
@@ -386,6 +400,7 @@ void hodge_args(const Plan& P, int which, const double* x, double* y, HodgeArgs&
   }
   h.Q = P.Q;
   h.dual = (which == SGM_MASS_EPS) ? 1 : 0;
+  h.form = form1 ? (which == SGM_MASS_EPS ? 2 : 3) : h.dual;
 }
 
 // y = M x for one 2-form mass (separable: Kronecker of 1D Grams; else sum factorisation)
@@ -402,6 +417,105 @@ void mass_apply(const Plan& P, int which, const double* x, double* y, double* t,
   HodgeArgs h;
   hodge_args(P, which, x, y, h);
   launch_hodge_general(P.p, h, st);
+}
+
+// y = M^1 x for one scheme-1 1-form mass (sum factorisation with the 1-form weights)
+void mass1_apply(const Plan& P, int which, const double* x, double* y, cudaStream_t st) {
+  const int kind = (which == SGM_MASS_EPS) ? 0 : 1;
+  cudaMemsetAsync(y, 0, form_len(P, kind) * sizeof(double), st);
+  HodgeArgs h;
+  hodge_args(P, which, x, y, h, true);
+  launch_hodge_general(P.p, h, st);
+}
+
+// Scheme 1 with a non-separable 1-form mass (curved map or variable material): the Hodge star
+// M^1 y = K^T x (K = K1 for eps, K~1 for mu) by preconditioned conjugate gradients,
+// entirely on the device (scalars stay in device memory, a fixed iteration count).  Preconditioner:
+// the separable scheme-1 star with the mean material, P^{-1} v = S1(K^{-T} v) where
+// S1 = M^1_sep^{-1} K^T is the reduced sweep schedule, so P = M^1_sep (Kronecker Grams).
+void pcg_star(Plan& P, int which, const double* x, double* y, const WS& w, cudaStream_t st) {
+  const int kind = (which == SGM_MASS_EPS) ? 0 : 1;
+  const size_t N = form_len(P, kind);
+  double* res = P.pcg_buf;
+  double* z = res + P.pcg_n;
+  double* pv = z + P.pcg_n;
+  double* q = pv + P.pcg_n;
+  double* scal = w.partials + 4 * partial_blocks();  // [0..3]: rz (two slots), pq
+  // transposed pairing apply and solve tables: K1^T = Hat M^T (own) x Hat G^T (other);
+  // K~1^T = Hat G (own) x Hat M (other)
+  const int app_own = kind == 0 ? OP_APPLY_MT : OP_APPLY_G, app_oth = kind == 0 ? OP_APPLY_GT : OP_APPLY_M;
+  const int sol_own = kind == 0 ? OP_MU_OTH : OP_EPS_OTH, sol_oth = kind == 0 ? OP_MU_OWN : OP_EPS_OWN;
+  const MassData& M1 = P.mass1[which];
+  double gbar = M1.material_c;
+  if (!M1.const_material && !P.mass[which].values_host.empty()) {
+    double s = 0.0;
+    for (double v : P.mass[which].values_host) s += v;
+    gbar = s / double(P.mass[which].values_host.size());
+  }
+  const double psc[3] = {1.0 / gbar, 1.0 / gbar, 1.0 / gbar};
+  auto precond = [&](const double* v, double* out) {
+    kron_pass3(P, kind, v, out, w.t, sol_own, sol_oth, nullptr, false, true, st);  // K^{-T} v
+    hodge_star_reduced(P, which, out, out, w.t, st, psc);                          // S1 (in place)
+  };
+  kron_pass3(P, kind, x, res, w.t, app_own, app_oth, nullptr, true, false, st);  // r = K^T x
+  cudaMemsetAsync(y, 0, N * sizeof(double), st);
+  precond(res, z);
+  cudaMemcpyAsync(pv, z, N * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  int a = 0;
+  launch_dot_partials(res, z, N, w.partials, 0, st);
+  launch_finalize_sum(w.partials, 1, 1.0, scal + a, st);
+  for (int k = 0; k < P.pcg_iters; ++k) {
+    mass1_apply(P, which, pv, q, st);
+    launch_dot_partials(pv, q, N, w.partials, 0, st);
+    launch_finalize_sum(w.partials, 1, 1.0, scal + 2, st);
+    launch_axpy_ratio(y, pv, N, scal + a, scal + 2, 1.0, st);
+    launch_axpy_ratio(res, q, N, scal + a, scal + 2, -1.0, st);
+    precond(res, z);
+    launch_dot_partials(res, z, N, w.partials, 0, st);
+    launch_finalize_sum(w.partials, 1, 1.0, scal + (1 - a), st);
+    launch_xpby_ratio(pv, z, N, scal + (1 - a), scal + a, st);
+    a = 1 - a;
+  }
+}
+
+sgm_status ensure_pcg(Plan& P) {
+  const size_t n = std::max(P.N_e, P.N_h);
+  if (P.pcg_buf && P.pcg_n >= n) return SGM_OK;
+  if (P.pcg_buf) cudaFree(P.pcg_buf);
+  P.pcg_buf = nullptr;
+  if (cudaMalloc(&P.pcg_buf, 4 * n * sizeof(double)) != cudaSuccess) return fail(SGM_E_NOMEM, "cudaMalloc failed for PCG");
+  P.pcg_n = n;
+  return SGM_OK;
+}
+
+// build and upload the scheme-1 1-form weights of both masses (host-only plans: classification)
+sgm_status upload_mass1(Plan& P) {
+  if (P.device < 0) {
+    for (int m = 0; m < 2; ++m) {
+      P.mass1[m].const_material = P.mass[m].const_material;
+      P.mass1[m].kind = P.mass[m].kind;
+    }
+    return SGM_OK;
+  }
+  for (int m = 0; m < 2; ++m) {
+    std::vector<double> W;
+    std::string err;
+    sgm_status st = build_mass1(P, m, W, err);
+    if (st != SGM_OK) return fail(st, err);
+    MassData& M = P.mass1[m];
+    if (M.W_dev) cudaFree(M.W_dev);
+    M.W_dev = nullptr;
+    if (!W.empty() && P.device >= 0) {
+      if (cudaMalloc(&M.W_dev, W.size() * sizeof(double)) != cudaSuccess)
+        return fail(SGM_E_NOMEM, "cudaMalloc failed for scheme-1 weights");
+      cudaMemcpy(M.W_dev, W.data(), W.size() * sizeof(double), cudaMemcpyHostToDevice);
+    }
+  }
+  if (P.device >= 0) {
+    for (int m = 0; m < 2; ++m)
+      if (P.mass1[m].kind != HODGE_SEPARABLE) return ensure_pcg(P);
+  }
+  return SGM_OK;
 }
 
 sgm_status upload_basis(Plan& P) {
@@ -497,7 +611,9 @@ void half_step(Plan& P, int half, double* d, double* e, double* b, double* h, co
   }
   a.pro = pa;
   { ProfScope ps(P, SGM_K_UPDATE, st); launch_update(pro, a, st); }
-  if (M.kind == HODGE_SEPARABLE && P.diag_ok) {
+  if (P.scheme == 1 && P.mass1[mass].kind != HODGE_SEPARABLE) {
+    { ProfScope ps(P, SGM_K_HODGE_GENERAL, st); pcg_star(P, mass, state[0], outv[0], w, st); }
+  } else if (M.kind == HODGE_SEPARABLE && P.diag_ok) {
     hodge_star_reduced(P, mass, state[0], outv[0], w.t, st);
   } else if (M.kind == HODGE_SEPARABLE) {
     // streaming update kernel, then the three mass . solve sweeps (z, y, x); snake order: update
@@ -606,6 +722,7 @@ sgm_status sgm_plan_create(const sgm_plan_desc* desc, sgm_plan* out) {
       P->ev_join = e2;
       const char* f = getenv("SGM_FORK");
       P->fork_enabled = !(f && atoi(f) == 0);
+      if (const char* it = getenv("SGM_PCG_ITERS")) P->pcg_iters = std::max(1, atoi(it));
     }
     st = upload_basis(*P);
     if (st != SGM_OK) {
@@ -637,6 +754,8 @@ sgm_status sgm_plan_destroy(sgm_plan plan) {
     cudaFree(P->basis_dev);
     cudaFree(P->first_dev);
     for (int m = 0; m < 2; ++m) cudaFree(P->mass[m].W_dev);
+    for (int m = 0; m < 2; ++m) cudaFree(P->mass1[m].W_dev);
+    cudaFree(P->pcg_buf);
     cudaFree(P->mirror);
     for (auto& r : P->prof) {
       cudaEventDestroy(static_cast<cudaEvent_t>(r.a));
@@ -711,12 +830,11 @@ sgm_status sgm_plan_set_scheme(sgm_plan plan, int scheme) {
   Plan* P = PL(plan);
   if (scheme != 1 && scheme != 2) return fail(SGM_E_INVALID_ARG, "scheme must be 1 or 2");
   if (scheme == 1) {
-    if (P->has_geom) return fail(SGM_E_UNSUPPORTED, "scheme 1 is built for the identity map only");
     if (P->wide_host.empty()) return fail(SGM_E_UNSUPPORTED, "scheme 1 is built for p <= 3");
     if (!P->diag_ok) return fail(SGM_E_UNSUPPORTED, "scheme 1 needs the reduced separable schedule");
-    for (int m = 0; m < 2; ++m)
-      if (P->mass[m].kind != HODGE_SEPARABLE)
-        return fail(SGM_E_UNSUPPORTED, "scheme 1 is built for constant materials (separable stars) only");
+    DeviceGuard g(P->device >= 0 ? P->device : 0);
+    sgm_status st = upload_mass1(*P);
+    if (st != SGM_OK) return st;
   }
   if (P->scheme != scheme && P->graph_exec) {
     DeviceGuard g(P->device);
@@ -735,8 +853,6 @@ sgm_status sgm_plan_reduced_schedule(sgm_plan plan, int* on) {
 }
 
 sgm_status sgm_plan_set_material(sgm_plan plan, sgm_material which, const double* values, double c) {
-  if (plan && values && PL(plan)->scheme == 1)
-    return fail(SGM_E_UNSUPPORTED, "scheme 1 is built for constant materials; sgm_plan_set_scheme(plan, 2) first");
   if (plan && PL(plan)->graph_exec) {  // captured launches embed the old weights and kinds
     DeviceGuard g0(PL(plan)->device);
     cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(PL(plan)->graph_exec));
@@ -749,9 +865,15 @@ sgm_status sgm_plan_set_material(sgm_plan plan, sgm_material which, const double
   if (P->device >= 0) {
     DeviceGuard g(P->device);
     cudaDeviceSynchronize();
-    return set_material_impl(*P, which, values, c);
+    s = set_material_impl(*P, which, values, c);
+  } else {
+    s = set_material_impl(*P, which, values, c);
   }
-  return set_material_impl(*P, which, values, c);
+  if (s == SGM_OK && P->scheme == 1) {
+    DeviceGuard g(P->device >= 0 ? P->device : 0);
+    s = upload_mass1(*P);
+  }
+  return s;
 }
 
 sgm_status sgm_workspace_bytes(sgm_plan plan, size_t* bytes) {
@@ -956,7 +1078,9 @@ void hodge_star_impl(const Plan& P, int which, const double* x, double* y, const
   int own = (which == SGM_MASS_EPS) ? OP_EPS_OWN : OP_MU_OWN;
   int oth = (which == SGM_MASS_EPS) ? OP_EPS_OTH : OP_MU_OTH;
   const MassData& M = P.mass[which];
-  if (M.kind == HODGE_SEPARABLE && P.diag_ok) {
+  if (P.scheme == 1 && P.mass1[which].kind != HODGE_SEPARABLE) {
+    pcg_star(const_cast<Plan&>(P), which, x, y, w, st);
+  } else if (M.kind == HODGE_SEPARABLE && P.diag_ok) {
     hodge_star_reduced(const_cast<Plan&>(P), which, x, y, w.t, st);
   } else if (M.kind == HODGE_SEPARABLE) {
     kron_pass3(P, kind, x, y, w.t, own, oth, M.scale, true, true, st);

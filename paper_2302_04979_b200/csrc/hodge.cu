@@ -145,7 +145,7 @@ void launch_hodge_pencil(const HodgeArgs& a, cudaStream_t st) {
   hodge::hodge_pencil_kernel<P, Q, DUAL, FULL><<<unsigned(grid), 256, smem, st>>>(a);
 }
 
-template <int P, int Q, bool DUAL, bool FULL>
+template <int P, int Q, int DUAL, bool FULL>
 void launch_hodge_brick(const HodgeArgs& a, cudaStream_t st) {
   constexpr int E = 4;
   using L = brick::Layout<P, Q, DUAL, E>;
@@ -173,13 +173,24 @@ void launch_hodge_brick(const HodgeArgs& a, cudaStream_t st) {
 
 template <int P, int Q>
 void launch_hodge2(const HodgeArgs& a, cudaStream_t st) {
+  if (a.form >= 2) {
+    // 1-form masses (scheme 1): brick kernel only
+    if (a.form == 2) {
+      if (a.full) launch_hodge_brick<P, Q, 2, true>(a, st);
+      else launch_hodge_brick<P, Q, 2, false>(a, st);
+    } else {
+      if (a.full) launch_hodge_brick<P, Q, 3, true>(a, st);
+      else launch_hodge_brick<P, Q, 3, false>(a, st);
+    }
+    return;
+  }
   if (env_int("SGM_HODGE_PENCIL", 0) == 0) {
     if (a.dual) {
-      if (a.full) launch_hodge_brick<P, Q, true, true>(a, st);
-      else launch_hodge_brick<P, Q, true, false>(a, st);
+      if (a.full) launch_hodge_brick<P, Q, 1, true>(a, st);
+      else launch_hodge_brick<P, Q, 1, false>(a, st);
     } else {
-      if (a.full) launch_hodge_brick<P, Q, false, true>(a, st);
-      else launch_hodge_brick<P, Q, false, false>(a, st);
+      if (a.full) launch_hodge_brick<P, Q, 0, true>(a, st);
+      else launch_hodge_brick<P, Q, 0, false>(a, st);
     }
     return;
   }

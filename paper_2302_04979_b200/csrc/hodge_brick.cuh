@@ -23,12 +23,18 @@
 namespace sgm {
 namespace brick {
 
-template <int P, bool DUAL, int C, int AX>
+// Local functions per element of component C along axis AX.  DUAL is the form type:
+//   0 primal 2-form (own S_p: p+1, other S_{p-1} CS: p)   1 dual 2-form (own S_{p-1}: p, other S_{p-2}: p-1)
+//   2 primal 1-form (own S_{p-1} CS: p, other S_p: p+1)   3 dual 1-form (own S_{p-2}: p-1, other S_{p-1}: p)
+template <int P, int DUAL, int C, int AX>
 __host__ __device__ constexpr int nloc() {
-  return (C == AX) ? (DUAL ? P : P + 1) : (DUAL ? P - 1 : P);
+  return DUAL == 0 ? (C == AX ? P + 1 : P)
+       : DUAL == 1 ? (C == AX ? P : P - 1)
+       : DUAL == 2 ? (C == AX ? P : P + 1)
+                   : (C == AX ? P - 1 : P);
 }
 
-template <int P, int Q, bool DUAL, int E, int C>
+template <int P, int Q, int DUAL, int E, int C>
 struct Geo {
   static constexpr int NX = nloc<P, DUAL, C, 0>(), NY = nloc<P, DUAL, C, 1>(), NZ = nloc<P, DUAL, C, 2>();
   static constexpr int PX = E - 1 + NX, PY = E - 1 + NY;
@@ -40,7 +46,7 @@ struct Geo {
   static constexpr int TOT = 2 * WIN + Z1 + Z2 + U;
 };
 
-template <int P, int Q, bool DUAL, int E>
+template <int P, int Q, int DUAL, int E>
 struct Layout {
   using G0 = Geo<P, Q, DUAL, E, 0>;
   using G1 = Geo<P, Q, DUAL, E, 1>;
@@ -68,7 +74,7 @@ __device__ __forceinline__ int uidx(int qz, int Yq, int ex, int qx) {
 }
 
 // per-component pointers into shared memory
-template <int P, int Q, bool DUAL, int E, int C>
+template <int P, int Q, int DUAL, int E, int C>
 struct CompSm {
   using G = Geo<P, Q, DUAL, E, C>;
   double *Xw, *Yw, *Z1, *Z2, *U;
@@ -100,7 +106,7 @@ __device__ __forceinline__ int first_of(const HodgeArgs& A, int axis, int role, 
 }
 
 // load coefficient layer jz (global z index gz) of component C's patch into the window
-template <int P, int Q, bool DUAL, int E, int C>
+template <int P, int Q, int DUAL, int E, int C>
 __device__ __forceinline__ void load_layer(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int gx0, int gy0,
                                            int gz, int jz) {
   using G = Geo<P, Q, DUAL, E, C>;
@@ -118,7 +124,7 @@ __device__ __forceinline__ void load_layer(const HodgeArgs& A, const CompSm<P, Q
 
 // atomically add the output window slot `sl` (global z index gz) of component C's patch to y and
 // clear the slot for reuse as the top layer
-template <int P, int Q, bool DUAL, int E, int C>
+template <int P, int Q, int DUAL, int E, int C>
 __device__ __forceinline__ void flush_layer(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int gx0, int gy0,
                                             int gz, int sl) {
   using G = Geo<P, Q, DUAL, E, C>;
@@ -136,7 +142,7 @@ __device__ __forceinline__ void flush_layer(const HodgeArgs& A, const CompSm<P, 
 
 // ---- interpolation stages of component C (tasks numbered from 0; `t` is this thread's task) ----
 // z: Z1[qz][py][px] = sum_jz Vz[qz][jz] Xw[jz][py][px]          (tasks: py, px)
-template <int P, int Q, bool DUAL, int E, int C>
+template <int P, int Q, int DUAL, int E, int C>
 __device__ __forceinline__ void interp_z(const CompSm<P, Q, DUAL, E, C>& S, int t) {
   using G = Geo<P, Q, DUAL, E, C>;
   constexpr int NL = P + 1, LAY = G::PY * G::PX;
@@ -173,7 +179,7 @@ struct Coef {
 };
 
 // (tasks: half, qz, px -- each half of the brick's elements along y is a separate task)
-template <int P, int Q, bool DUAL, int E, int C, bool UNI>
+template <int P, int Q, int DUAL, int E, int C, bool UNI>
 __device__ __forceinline__ void interp_y(const CompSm<P, Q, DUAL, E, C>& S, int t) {
   using G = Geo<P, Q, DUAL, E, C>;
   constexpr int NL = P + 1, EH = E / 2;
@@ -197,7 +203,7 @@ __device__ __forceinline__ void interp_y(const CompSm<P, Q, DUAL, E, C>& S, int 
 }
 
 // x: U[qz][Y][ex*Q+qx] = sum_jx Vx[ex][qx][jx] Z2[qz][Y][ex+jx]    (tasks: qz, Y)
-template <int P, int Q, bool DUAL, int E, int C, bool UNI>
+template <int P, int Q, int DUAL, int E, int C, bool UNI>
 __device__ __forceinline__ void interp_x(const CompSm<P, Q, DUAL, E, C>& S, int t, const double* Wm = nullptr,
                                          double wsc = 1.0, int nex = E, int ney = E) {
   // (tasks: half, qz, Y -- each half of the brick's elements along x is a separate task).  With Wm
@@ -229,7 +235,7 @@ __device__ __forceinline__ void interp_x(const CompSm<P, Q, DUAL, E, C>& S, int 
 
 // ---- testing stages (transposes of the above) ----
 // x: Z2[qz][Y][px] = sum_{ex,qx} Vx[ex][qx][px-ex] U[qz][Y][ex*Q+qx]   (tasks: qz, Y)
-template <int P, int Q, bool DUAL, int E, int C, bool UNI>
+template <int P, int Q, int DUAL, int E, int C, bool UNI>
 __device__ __forceinline__ void test_x(const CompSm<P, Q, DUAL, E, C>& S, int t) {
   using G = Geo<P, Q, DUAL, E, C>;
   constexpr int NL = P + 1;
@@ -251,7 +257,7 @@ __device__ __forceinline__ void test_x(const CompSm<P, Q, DUAL, E, C>& S, int t)
 }
 
 // y: Z1[qz][py][px] = sum_{ey,qy} Vy[ey][qy][py-ey] Z2[qz][ey*Q+qy][px]   (tasks: qz, px)
-template <int P, int Q, bool DUAL, int E, int C, bool UNI>
+template <int P, int Q, int DUAL, int E, int C, bool UNI>
 __device__ __forceinline__ void test_y(const CompSm<P, Q, DUAL, E, C>& S, int t) {
   using G = Geo<P, Q, DUAL, E, C>;
   constexpr int NL = P + 1;
@@ -274,7 +280,7 @@ __device__ __forceinline__ void test_y(const CompSm<P, Q, DUAL, E, C>& S, int t)
 }
 
 // z: Yw[jz][py][px] += sum_qz Vz[qz][jz] Z1[qz][py][px]      (tasks: py, px)
-template <int P, int Q, bool DUAL, int E, int C>
+template <int P, int Q, int DUAL, int E, int C>
 __device__ __forceinline__ void test_z(const CompSm<P, Q, DUAL, E, C>& S, int t) {
   using G = Geo<P, Q, DUAL, E, C>;
   constexpr int NL = P + 1, LAY = G::PY * G::PX;
@@ -297,7 +303,7 @@ __device__ __forceinline__ void test_z(const CompSm<P, Q, DUAL, E, C>& S, int t)
 // output slot (atomics to y, slot cleared), then -- if another layer follows -- the new top
 // coefficient into the freed slot and the z interpolation of the next layer.  vz_*: the z bases
 // (global, [Q][NL]) of this layer and of the next.
-template <int P, int Q, bool DUAL, int E, int C>
+template <int P, int Q, int DUAL, int E, int C>
 __device__ __forceinline__ void column_phase(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int t, int gx0,
                                              int gy0, int gz_flush, bool next, int gz_load,
                                              const double* __restrict__ vz_cur, const double* __restrict__ vz_next) {
@@ -370,7 +376,7 @@ __device__ __forceinline__ void column_phase(const HodgeArgs& A, const CompSm<P,
     __syncthreads();                                                                                 \
   }
 
-template <int P, int Q, bool DUAL, bool FULL, int E>
+template <int P, int Q, int DUAL, bool FULL, int E>
 __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_constant__ HodgeArgs A, int zchunk) {
   using L = Layout<P, Q, DUAL, E>;
   using G0 = Geo<P, Q, DUAL, E, 0>;

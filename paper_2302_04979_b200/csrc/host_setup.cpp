@@ -687,6 +687,8 @@ sgm_status build_mass(Plan& P, int which, const double* values, double c, std::v
   }
   M.const_material = (values == nullptr);
   M.material_c = c;
+  if (values) M.values_host.assign(values, values + P.n_qp);
+  else M.values_host.clear();
   const double Lx = P.L_aff[0], Ly = P.L_aff[1], Lz = P.L_aff[2];
   const double detL = Lx * Ly * Lz;
   if (P.affine_diag) {
@@ -717,6 +719,74 @@ sgm_status build_mass(Plan& P, int which, const double* values, double c, std::v
     double g = w / (values ? values[idx] : c) / dt;
     // (DF^T DF)_{ij} = sum_r DF[r][i] DF[r][j]
     auto m = [&](int i, int j) { return D[0 * 3 + i] * D[0 * 3 + j] + D[1 * 3 + i] * D[1 * 3 + j] + D[2 * 3 + i] * D[2 * 3 + j]; };
+    double* o = &W[idx * 6];
+    o[0] = g * m(0, 0);
+    o[1] = g * m(1, 1);
+    o[2] = g * m(2, 2);
+    o[3] = g * m(0, 1);
+    o[4] = g * m(0, 2);
+    o[5] = g * m(1, 2);
+  });
+  return SGM_OK;
+}
+
+// Scheme 1: weights of the 1-form masses M^1_eps (which = EPS, primal 1-forms) and
+// M~^1_mu (which = MU, dual 1-forms) from the material stored by build_mass:
+//   W = w_q gamma(q) DF^{-1} DF^{-T} det DF  (1-form pull-back; FULL, 6 symmetric entries), or for
+//   an axis-aligned affine map w_q gamma(q) with the per-component scale prod(L) / L_c^2 (SCALAR),
+//   or nothing for a constant material on such a map (SEPARABLE: Kronecker Grams).
+sgm_status build_mass1(Plan& P, int which, std::vector<double>& W, std::string& err) {
+  const MassData& M2 = P.mass[which];
+  MassData& M = P.mass1[which];
+  W.clear();
+  M.const_material = M2.const_material;
+  M.material_c = M2.material_c;
+  const double* values = M2.const_material ? nullptr : M2.values_host.data();
+  const double c = M2.material_c;
+  if (!M2.const_material && M2.values_host.size() != P.n_qp) {
+    err = "scheme 1: material values missing";
+    return SGM_E_MATERIAL;
+  }
+  const double Lx = P.L_aff[0], Ly = P.L_aff[1], Lz = P.L_aff[2];
+  const double detL = Lx * Ly * Lz;
+  if (P.affine_diag) {
+    const double s[3] = {detL / (Lx * Lx), detL / (Ly * Ly), detL / (Lz * Lz)};
+    if (M.const_material) {
+      M.kind = HODGE_SEPARABLE;
+      for (int k = 0; k < 3; ++k) M.scale[k] = s[k] * c;
+      return SGM_OK;
+    }
+    M.kind = HODGE_SCALAR;
+    for (int k = 0; k < 3; ++k) M.scale[k] = s[k];
+    W.resize(P.n_qp);
+    for_each_qp(P, [&](size_t idx, int ex, int ey, int ez, int qx, int qy, int qz) {
+      double w = P.ax[0].wq[ex * P.Q + qx] * P.ax[1].wq[ey * P.Q + qy] * P.ax[2].wq[ez * P.Q + qz];
+      W[idx] = w * values[idx];
+    });
+    return SGM_OK;
+  }
+  M.kind = HODGE_FULL;
+  for (int k = 0; k < 3; ++k) M.scale[k] = 1.0;
+  W.resize(P.n_qp * 6);
+  GeoEval G(P);
+  for_each_qp(P, [&](size_t idx, int ex, int ey, int ez, int qx, int qy, int qz) {
+    double F[3], D[9];
+    G.eval(ex, ey, ez, qx, qy, qz, F, D);
+    const double dt = det3(D);
+    double w = P.ax[0].wq[ex * P.Q + qx] * P.ax[1].wq[ey * P.Q + qy] * P.ax[2].wq[ez * P.Q + qz];
+    const double g = w * (values ? values[idx] : c);
+    // DF^{-1} = adj(DF) / det; DF^{-1} DF^{-T} det = adj adj^T / det
+    double A[9];
+    A[0] = D[4] * D[8] - D[5] * D[7];
+    A[1] = D[2] * D[7] - D[1] * D[8];
+    A[2] = D[1] * D[5] - D[2] * D[4];
+    A[3] = D[5] * D[6] - D[3] * D[8];
+    A[4] = D[0] * D[8] - D[2] * D[6];
+    A[5] = D[2] * D[3] - D[0] * D[5];
+    A[6] = D[3] * D[7] - D[4] * D[6];
+    A[7] = D[1] * D[6] - D[0] * D[7];
+    A[8] = D[0] * D[4] - D[1] * D[3];
+    auto m = [&](int i, int j) { return (A[i * 3 + 0] * A[j * 3 + 0] + A[i * 3 + 1] * A[j * 3 + 1] + A[i * 3 + 2] * A[j * 3 + 2]) / dt; };
     double* o = &W[idx * 6];
     o[0] = g * m(0, 0);
     o[1] = g * m(1, 1);

@@ -244,6 +244,21 @@ __global__ void normalize_kernel(double* __restrict__ x, size_t n, const double*
     x[i] = x[i] / nrm;
 }
 
+// PCG vector updates with device-resident scalars (no host synchronisation):
+//   x += sign * (num / den) * p        and        p = z + (num / den) * p
+__global__ void axpy_ratio_kernel(double* __restrict__ x, const double* __restrict__ p, size_t n,
+                                  const double* num, const double* den, double sign) {
+  const double a = sign * (__ldg(num) / __ldg(den));
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    x[i] = fma(a, p[i], x[i]);
+}
+__global__ void xpby_ratio_kernel(double* __restrict__ p, const double* __restrict__ z, size_t n,
+                                  const double* num, const double* den) {
+  const double b = __ldg(num) / __ldg(den);
+  for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+    p[i] = fma(b, p[i], z[i]);
+}
+
 // out[0] = lambda = (sum slot 0) / (sum slot 1), out[1] = 2 / sqrt(lambda)  (CFL Rayleigh quotient)
 __global__ void rayleigh_kernel(const double* __restrict__ partials, double* out) {
   __shared__ double sh[kRedThreads];
@@ -421,6 +436,15 @@ void launch_absmax(const double* x, size_t n, double* partials, int slot, cudaSt
 
 void launch_normalize(double* x, size_t n, const double* partials, int slot, cudaStream_t st) {
   normalize_kernel<<<kRedBlocks, kRedThreads, 0, st>>>(x, n, partials, slot);
+}
+
+void launch_axpy_ratio(double* x, const double* p, size_t n, const double* num, const double* den, double sign,
+                       cudaStream_t st) {
+  axpy_ratio_kernel<<<4 * kRedBlocks, kRedThreads, 0, st>>>(x, p, n, num, den, sign);
+}
+
+void launch_xpby_ratio(double* p, const double* z, size_t n, const double* num, const double* den, cudaStream_t st) {
+  xpby_ratio_kernel<<<4 * kRedBlocks, kRedThreads, 0, st>>>(p, z, n, num, den);
 }
 
 void launch_rayleigh(const double* partials, double* out, cudaStream_t st) {

@@ -67,6 +67,8 @@ struct HodgeArgs {
   int nel[3];
   int Q;
   int dual;              // 1: dual 2-forms (M~2_{1/eps}), 0: primal 2-forms (M2_{1/mu})
+  int form;              // brick kernel form type: 0 primal 2-form, 1 dual 2-form, 2 primal 1-form
+                         // (M^1_eps, scheme 1), 3 dual 1-form (M~^1_mu, scheme 1)
 };
 
 void launch_sweep(int p, int seg, const SweepArgs& a, cudaStream_t st);
@@ -85,6 +87,9 @@ void launch_absmax(const double* x, size_t n, double* partials, int slot, cudaSt
 void launch_finalize_max(const double* partials, int nslots_each, int ngroups, double* out, cudaStream_t st);
 void launch_normalize(double* x, size_t n, const double* partials, int slot, cudaStream_t st);
 void launch_rayleigh(const double* partials, double* out, cudaStream_t st);
+void launch_axpy_ratio(double* x, const double* p, size_t n, const double* num, const double* den, double sign,
+                       cudaStream_t st);
+void launch_xpby_ratio(double* p, const double* z, size_t n, const double* num, const double* den, cudaStream_t st);
 int partial_blocks();
 
 }  // namespace sgm

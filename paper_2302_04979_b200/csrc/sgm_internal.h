@@ -54,6 +54,7 @@ struct MassData {
   double* W_dev = nullptr;             // SCALAR: 1 per qp; FULL: 6 per qp (xx,yy,zz,xy,xz,yz)
   bool const_material = true;
   double material_c = 1.0;             // constant material value (eps or mu)
+  std::vector<double> values_host;     // the material at the quadrature points (variable case)
 };
 
 // Arguments a captured sgm_step graph was recorded with (replayed only for identical calls).
@@ -81,6 +82,10 @@ struct Plan {
   double L_aff[3] = {1, 1, 1};        // diagonal of DF if affine_diag
   size_t n_qp = 0;
   MassData mass[2];                   // [SGM_MASS_EPS], [SGM_MASS_MU]
+  MassData mass1[2];                  // scheme 1: 1-form masses M^1_eps, M~^1_mu (weights: material)
+  double* pcg_buf = nullptr;          // scheme 1 with non-separable stars: 4 PCG vectors
+  int pcg_iters = 40;                 // fixed PCG iteration count (SGM_PCG_ITERS)
+  size_t pcg_n = 0;
   // device
   double* tables_dev = nullptr;       // [3][OP_COUNT][Lmax][RS] (seg_sweep.cuh row layout), then diag factors
   int Lmax = 0;                       // rows per table slot (max padded line length)
@@ -125,6 +130,7 @@ struct Plan {
 
 // host setup (host_setup.cpp)
 sgm_status build_axis(int p, int n, int Q, Axis& out, std::string& err);
+sgm_status build_mass1(Plan& P, int which, std::vector<double>& W, std::string& err);
 sgm_status banded_lu_nopivot(const std::vector<double>& A, int L, int m, std::vector<double>& LU,
                              std::string& err);
 sgm_status build_tables(Plan& P, std::string& err);

@@ -510,3 +510,43 @@ def test_scheme1_composed_yoshida():
     ref = compose.run_composed(tb, *st, dt, 6)
     for x, y in zip((d, e, b, h), ref):
         assert rel(host(x), y) < 1e-10
+
+
+@pytest.mark.parametrize("case", ["var_eps", "curved"])
+def test_scheme1_pcg_parity(case):
+    """Scheme 1 with non-separable 1-form masses (variable eps on the identity map; the curved C3-type
+    map with an eps inclusion): the GPU's preconditioned-CG Hodge stars (separable scheme-1 star as
+    preconditioner, fixed 40 iterations) against tier A1's SuperLU solves of the assembled masses,
+    then 1 and 10 steps and the stability limit."""
+    from oracle.scheme import TierA1
+    p = 3
+    if case == "var_eps":
+        n, ctrl = (5, 6, 4), None
+        pl = S.Plan(n, p)
+        X = pl.qp_coords()
+        eps = 1 + 0.5 * np.sin(2 * np.pi * X[:, 0]) * np.cos(2 * np.pi * X[:, 1])
+    else:
+        n = (4, 5, 4)
+        ctrl, eps = _curved_case(p, n)
+        pl = S.Plan(n, p, geom_ctrl=ctrl)
+    pl.set_material(S.EPS, eps)
+    pl.set_scheme(1)
+    A = TierA1(p, n, ctrl=ctrl, eps_qp=eps)
+    rng = np.random.default_rng(95)
+    x = rng.standard_normal(A.N_e)
+    y = torch.empty(A.N_e, dtype=torch.float64, device="cuda")
+    pl.hodge_star(S.MASS_EPS, dev(x), y)
+    assert rel(host(y), A.hodge_eps(x)) < 1e-11
+    xb = rng.standard_normal(A.N_h)
+    yb = torch.empty(A.N_h, dtype=torch.float64, device="cuda")
+    pl.hodge_star(S.MASS_MU, dev(xb), yb)
+    assert rel(host(yb), A.hodge_mu(xb)) < 1e-11
+    st = (x, A.hodge_eps(x), xb, A.hodge_mu(xb))
+    lam, dtmax, _, _ = W.cfl_power(A, synth.rng(100).standard_normal(A.N_e), 30)
+    out, _ = _cfl_gpu(pl, synth.rng(100).standard_normal(A.N_e), 30)
+    assert abs(out[0] / lam - 1) < 1e-9
+    dt = 0.4 * dtmax
+    for k, tol in ((1, 1e-11), (10, 1e-10)):
+        o = _run_gpu(pl, st, dt, k)
+        for a_, b_ in zip(o, A.run(*st, dt, k)):
+            assert rel(a_, b_) < tol
