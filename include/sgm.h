@@ -215,7 +215,7 @@ sgm_status sgm_cfl(sgm_plan plan, double* x, double* e, double* b, double* h, in
    sgm_hodge_star / sgm_cfl: 2 (default) = the paper's second scheme, pairing
    solves e = K1^{-1} M~2_{1/eps} d, h = K~1^{-1} M2_{1/mu} b; 1 = the first scheme,
    mass solves M^1_eps e = K~2 d, M~^1_mu h = K2 b with K~2 = K1^T, K2 = K~1^T.
-   Scheme 1 is built for p <= 3 (else SGM_E_UNSUPPORTED).  With the identity (axis-aligned affine)
+   Scheme 1 is built for every compiled degree (its eps star uses a p+1 table layout).  With the identity (axis-aligned affine)
    map and constant materials its 1-form masses are Kronecker products of 1D Grams, inverted mode by
    mode with the same sweeps (the own-axis factor of e and the other-axis factors of h are again
    exactly diagonal).  Otherwise (curved map or variable material) each star solves its 1-form mass

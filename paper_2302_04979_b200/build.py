@@ -5,7 +5,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsgm.so")
-SOURCES = ["host_setup.cpp", "kernels.cu", "hodge.cu", "sweep_p2.cu", "sweep_p3.cu", "sweep_p4.cu", "api.cu"]
+SOURCES = ["host_setup.cpp", "kernels.cu", "hodge.cu", "sweep_p2.cu", "sweep_p3.cu", "sweep_p4.cu", "sweep_p5.cu", "api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
          "-Xcompiler", "-fPIC,-fopenmp", "-shared", "-lgomp"]

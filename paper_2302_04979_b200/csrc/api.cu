@@ -830,7 +830,7 @@ sgm_status sgm_plan_set_scheme(sgm_plan plan, int scheme) {
   Plan* P = PL(plan);
   if (scheme != 1 && scheme != 2) return fail(SGM_E_INVALID_ARG, "scheme must be 1 or 2");
   if (scheme == 1) {
-    if (P->wide_host.empty()) return fail(SGM_E_UNSUPPORTED, "scheme 1 is built for p <= 3");
+    if (P->wide_host.empty()) return fail(SGM_E_UNSUPPORTED, "scheme 1 tables missing");
     if (!P->diag_ok) return fail(SGM_E_UNSUPPORTED, "scheme 1 needs the reduced separable schedule");
     DeviceGuard g(P->device >= 0 ? P->device : 0);
     sgm_status st = upload_mass1(*P);

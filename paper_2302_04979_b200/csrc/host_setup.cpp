@@ -445,9 +445,9 @@ sgm_status build_tables(Plan& P, std::string& err) {
     if ((st = fill_table(T(OP_APPLY_GT), p, X.a, R, SEG, &GT, nullptr, err)) != SGM_OK) return st;
     if ((st = fill_table(T(OP_APPLY_MT), p, X.b, R, SEG, &MT, nullptr, err)) != SGM_OK) return st;
     // scheme 1: h_c own factor Gamma_C^{p-2}^{-1} Hat G; e_c other factor
-    // Gamma_B^p^{-1} Hat G^T, whose LU has half-bandwidth p -> wide layout p + 1 (p <= 3 only)
+    // Gamma_B^p^{-1} Hat G^T, whose LU has half-bandwidth p -> wide layout p + 1
     if ((st = fill_table(T(OP_S1_MU_OWN), p, X.a, R, SEG, &X.G, &X.GC2, err)) != SGM_OK) return st;
-    if (p <= 3) {
+    if (p <= 4) {
       const int RSw = RowLayoutRT(p + 1).RS;
       if (P.wide_host.empty()) P.wide_host.assign(size_t(3) * Rmax * RSw, 0.0);
       double* Tw = P.wide_host.data() + size_t(a) * Rmax * RSw;

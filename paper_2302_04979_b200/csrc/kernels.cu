@@ -325,6 +325,7 @@ void launch_sweep(int p, int seg, const SweepArgs& a, cudaStream_t st) {
     case 2: launch_sweep_p2(seg, a, st); break;
     case 3: launch_sweep_p3(seg, a, st); break;
     case 4: launch_sweep_p4(seg, a, st); break;
+    case 5: launch_sweep_p5(seg, a, st); break;
     default: break;
   }
 }

@@ -75,6 +75,7 @@ void launch_sweep(int p, int seg, const SweepArgs& a, cudaStream_t st);
 void launch_sweep_p2(int seg, const SweepArgs& a, cudaStream_t st);  // sweep_p2.cu
 void launch_sweep_p3(int seg, const SweepArgs& a, cudaStream_t st);  // sweep_p3.cu
 void launch_sweep_p4(int seg, const SweepArgs& a, cudaStream_t st);  // sweep_p4.cu
+void launch_sweep_p5(int seg, const SweepArgs& a, cudaStream_t st);  // sweep_p5.cu (scheme-1 layout at p = 4)
 void launch_update(int pro, const SweepArgs& a, cudaStream_t st);
 void launch_curl(int kind, const double* const src[3], const int sext[3][3], double* const dst[3],
                  const int dext[3][3], cudaStream_t st);

@@ -465,7 +465,7 @@ def test_rational_quarter_annulus(n):
             assert rel(a, b) < tol
 
 
-@pytest.mark.parametrize("p,n", [(2, (5, 9, 7)), (3, 11), (3, (9, 7, 6))])
+@pytest.mark.parametrize("p,n", [(2, (5, 9, 7)), (3, 11), (3, (9, 7, 6)), (4, (6, 7, 5))])
 def test_scheme1_parity(p, n):
     """The first scheme (mass-matrix Hodge stars) on the GPU against oracle tier B1:
     the two Hodge stars, 1 and 30 steps, and the power-iteration stability limit."""
@@ -512,15 +512,15 @@ def test_scheme1_composed_yoshida():
         assert rel(host(x), y) < 1e-10
 
 
-@pytest.mark.parametrize("case", ["var_eps", "curved"])
+@pytest.mark.parametrize("case", ["var_eps", "curved", "var_eps_p4"])
 def test_scheme1_pcg_parity(case):
     """Scheme 1 with non-separable 1-form masses (variable eps on the identity map; the curved C3-type
     map with an eps inclusion): the GPU's preconditioned-CG Hodge stars (separable scheme-1 star as
     preconditioner, fixed 40 iterations) against tier A1's SuperLU solves of the assembled masses,
     then 1 and 10 steps and the stability limit."""
     from oracle.scheme import TierA1
-    p = 3
-    if case == "var_eps":
+    p = 4 if case == "var_eps_p4" else 3
+    if case.startswith("var_eps"):
         n, ctrl = (5, 6, 4), None
         pl = S.Plan(n, p)
         X = pl.qp_coords()
