@@ -445,13 +445,7 @@ void pcg_star(Plan& P, int which, const double* x, double* y, const WS& w, cudaS
   // K~1^T = Hat G (own) x Hat M (other)
   const int app_own = kind == 0 ? OP_APPLY_MT : OP_APPLY_G, app_oth = kind == 0 ? OP_APPLY_GT : OP_APPLY_M;
   const int sol_own = kind == 0 ? OP_MU_OTH : OP_EPS_OTH, sol_oth = kind == 0 ? OP_MU_OWN : OP_EPS_OWN;
-  const MassData& M1 = P.mass1[which];
-  double gbar = M1.material_c;
-  if (!M1.const_material && !P.mass[which].values_host.empty()) {
-    double s = 0.0;
-    for (double v : P.mass[which].values_host) s += v;
-    gbar = s / double(P.mass[which].values_host.size());
-  }
+  const double gbar = P.mass1[which].material_c;  // the material's mean (upload_mass1)
   const double psc[3] = {1.0 / gbar, 1.0 / gbar, 1.0 / gbar};
   auto precond = [&](const double* v, double* out) {
     kron_pass3(P, kind, v, out, w.t, sol_own, sol_oth, nullptr, false, true, st);  // K^{-T} v
@@ -503,6 +497,11 @@ sgm_status upload_mass1(Plan& P) {
     sgm_status st = build_mass1(P, m, W, err);
     if (st != SGM_OK) return fail(st, err);
     MassData& M = P.mass1[m];
+    if (!M.const_material) {  // preconditioner material: the mean over the quadrature points
+      double s = 0.0;
+      for (double v : P.mass[m].values_host) s += v;
+      M.material_c = s / double(P.mass[m].values_host.size());
+    }
     if (M.W_dev) cudaFree(M.W_dev);
     M.W_dev = nullptr;
     if (!W.empty() && P.device >= 0) {
