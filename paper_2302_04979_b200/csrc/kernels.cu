@@ -373,7 +373,7 @@ void launch_update(int pro, const SweepArgs& a, cudaStream_t st) {
   auto launch = [&](auto kern) {
     int per_sm = env_int("SGM_UPD_GRID", 0);
     if (per_sm <= 0) {
-      static std::map<const void*, int> occ;  // per kernel instance
+      static thread_local std::map<const void*, int> occ;  // per kernel instance (per host thread)
       int& o = occ[reinterpret_cast<const void*>(kern)];
       if (o == 0) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, 256, 0);
       per_sm = o > 0 ? o : 1;
