@@ -67,7 +67,9 @@ def main(tag):
     L.append("* `r1_ncu_launches.csv` — `ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv python bench.py --steps 3 --warmup 3 --no-cpu --no-e2e`")
     L.append("* `r1_ncu_full_raw.csv` — `ncu --set full --clock-control none --import-source on -k \"regex:sweep_kernel|update_kernel\" --launch-skip 26 --launch-count 14` (two steps)")
     L.append("* `r1_ncu_hodge_brick_c4_raw.csv`, `r1_ncu_hodge_brick_c3_raw.csv` — `TAG=... KREGEX=hodge_brick ARGS=\"--config c4|c3 ...\" bash scripts/ncu_one.sh` (separate call): the general-Hodge brick kernel (C4 ε-Hodge 1.63 ms, IPC 1.25, fp64 pipe 17 %, 0.94 GB DRAM; C3 0.155 ms, IPC 0.98, fp64 pipe 10 %)")
-    L.append("* `traffic.json` — per-class DRAM bytes per launch from the full capture (`scripts/ncu_traffic.py`, read by bench.py)\n")
+    L.append("* `traffic.json` — per-class DRAM bytes per launch from the full capture (`scripts/ncu_traffic.py`, read by bench.py)")
+    L.append("* `r1_cpu_oracle.jsonl` — `scripts/oracle_timing.py` (separate call): the CPU oracle per step for every config")
+    L.append("* `r1_scheme_compare.md` — scheme 1 (mass-matrix Hodge stars) against scheme 2 on this GPU (separate calls)\n")
     L.append(f"Same call: `pytest -m gpu` → {pyt}; `smoke()` → {smoke}\n")
     L.append("## Headline (unprofiled, live)\n")
     c = b["clocks"]
