@@ -221,8 +221,10 @@ sgm_status sgm_cfl(sgm_plan plan, double* x, double* e, double* b, double* h, in
    exactly diagonal).  Otherwise (curved map or variable material) each star solves its 1-form mass
    by preconditioned conjugate gradients on the device: sum-factorised 1-form mass applies
    (weights w gamma DF^{-1} DF^{-T} det DF), the separable star with the mean material as
-   preconditioner, a fixed iteration count (40; SGM_PCG_ITERS), no host synchronisation.  The 1-form
-   weights are rebuilt by sgm_plan_set_material while scheme 1 is selected. */
+   preconditioner, no host synchronisation; the iteration count is calibrated per star when the
+   weights are built (one solve with residual read-back, relative preconditioned residual 1e-14,
+   plus 3; SGM_PCG_ITERS fixes it instead).  The 1-form weights (and the calibration) are redone by
+   sgm_plan_set_material while scheme 1 is selected. */
 sgm_status sgm_plan_set_scheme(sgm_plan plan, int scheme);
 
 /* *on = 1 if separable Hodge stars use the reduced schedule (the diagonal 1D

@@ -433,7 +433,8 @@ void mass1_apply(const Plan& P, int which, const double* x, double* y, cudaStrea
 // entirely on the device (scalars stay in device memory, a fixed iteration count).  Preconditioner:
 // the separable scheme-1 star with the mean material, P^{-1} v = S1(K^{-T} v) where
 // S1 = M^1_sep^{-1} K^T is the reduced sweep schedule, so P = M^1_sep (Kronecker Grams).
-void pcg_star(Plan& P, int which, const double* x, double* y, const WS& w, cudaStream_t st) {
+void pcg_star(Plan& P, int which, const double* x, double* y, const WS& w, cudaStream_t st,
+              std::vector<double>* trace = nullptr) {
   const int kind = (which == SGM_MASS_EPS) ? 0 : 1;
   const size_t N = form_len(P, kind);
   double* res = P.pcg_buf;
@@ -458,7 +459,16 @@ void pcg_star(Plan& P, int which, const double* x, double* y, const WS& w, cudaS
   int a = 0;
   launch_dot_partials(res, z, N, w.partials, 0, st);
   launch_finalize_sum(w.partials, 1, 1.0, scal + a, st);
-  for (int k = 0; k < P.pcg_iters; ++k) {
+  // calibration (plan time): record r.z after every iteration (host synchronisation)
+  auto record = [&](const double* dev_scalar) {
+    double v = 0.0;
+    cudaMemcpyAsync(&v, dev_scalar, sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    trace->push_back(v);
+  };
+  if (trace) record(scal + a);
+  const int iters = trace ? 200 : (P.pcg_fixed > 0 ? P.pcg_fixed : P.pcg_iters_m[which]);
+  for (int k = 0; k < iters; ++k) {
     mass1_apply(P, which, pv, q, st);
     launch_dot_partials(pv, q, N, w.partials, 0, st);
     launch_finalize_sum(w.partials, 1, 1.0, scal + 2, st);
@@ -469,7 +479,49 @@ void pcg_star(Plan& P, int which, const double* x, double* y, const WS& w, cudaS
     launch_finalize_sum(w.partials, 1, 1.0, scal + (1 - a), st);
     launch_xpby_ratio(pv, z, N, scal + (1 - a), scal + a, st);
     a = 1 - a;
+    if (trace) {
+      record(scal + a);
+      if (!(trace->back() > 1e-28 * trace->front())) break;  // preconditioned residual 1e-14 relative
+    }
   }
+}
+
+// Plan-time choice of the PCG iteration count of each non-separable scheme-1 star: solve once for a
+// deterministic right-hand side with the residual read back after every iteration; the count that
+// reaches a relative preconditioned residual of 1e-14, plus 3, is used from then on.
+sgm_status calibrate_pcg(Plan& P) {
+  std::vector<double> xh(std::max(P.N_e, P.N_h));
+  uint64_t st64 = 0x9e3779b97f4a7c15ULL;
+  for (double& v : xh) {  // splitmix64 uniforms in (-1, 1): any RHS exciting all modes will do
+    st64 += 0x9e3779b97f4a7c15ULL;
+    uint64_t z = st64;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    z ^= z >> 31;
+    v = double(z >> 11) * (2.0 / 9007199254740992.0) - 1.0;
+  }
+  double *x = nullptr, *y = nullptr;
+  void* ws = nullptr;
+  const size_t n = xh.size(), wb = ws_need(P);
+  if (cudaMalloc(&x, n * 8) != cudaSuccess || cudaMalloc(&y, n * 8) != cudaSuccess || cudaMalloc(&ws, wb) != cudaSuccess) {
+    cudaFree(x);
+    cudaFree(y);
+    cudaFree(ws);
+    return fail(SGM_E_NOMEM, "cudaMalloc failed for the PCG calibration");
+  }
+  cudaMemcpy(x, xh.data(), n * 8, cudaMemcpyHostToDevice);
+  WS w;
+  ws_carve(P, ws, wb, w);
+  for (int m = 0; m < 2; ++m) {
+    if (P.mass1[m].kind == HODGE_SEPARABLE) continue;
+    std::vector<double> tr;
+    pcg_star(P, m, x, y, w, nullptr, &tr);
+    P.pcg_iters_m[m] = std::min(200, std::max(5, int(tr.size()) - 1 + 3));
+  }
+  cudaFree(x);
+  cudaFree(y);
+  cudaFree(ws);
+  return cuda_check(&P, "calibrate_pcg");
 }
 
 sgm_status ensure_pcg(Plan& P) {
@@ -512,7 +564,11 @@ sgm_status upload_mass1(Plan& P) {
   }
   if (P.device >= 0) {
     for (int m = 0; m < 2; ++m)
-      if (P.mass1[m].kind != HODGE_SEPARABLE) return ensure_pcg(P);
+      if (P.mass1[m].kind != HODGE_SEPARABLE) {
+        sgm_status st = ensure_pcg(P);
+        if (st != SGM_OK) return st;
+        return calibrate_pcg(P);
+      }
   }
   return SGM_OK;
 }
@@ -721,7 +777,7 @@ sgm_status sgm_plan_create(const sgm_plan_desc* desc, sgm_plan* out) {
       P->ev_join = e2;
       const char* f = getenv("SGM_FORK");
       P->fork_enabled = !(f && atoi(f) == 0);
-      if (const char* it = getenv("SGM_PCG_ITERS")) P->pcg_iters = std::max(1, atoi(it));
+      if (const char* it = getenv("SGM_PCG_ITERS")) P->pcg_fixed = std::max(1, atoi(it));
     }
     st = upload_basis(*P);
     if (st != SGM_OK) {

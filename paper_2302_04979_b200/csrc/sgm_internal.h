@@ -84,7 +84,8 @@ struct Plan {
   MassData mass[2];                   // [SGM_MASS_EPS], [SGM_MASS_MU]
   MassData mass1[2];                  // scheme 1: 1-form masses M^1_eps, M~^1_mu (weights: material)
   double* pcg_buf = nullptr;          // scheme 1 with non-separable stars: 4 PCG vectors
-  int pcg_iters = 40;                 // fixed PCG iteration count (SGM_PCG_ITERS)
+  int pcg_iters_m[2] = {40, 40};      // PCG iterations per star (plan-time calibration)
+  int pcg_fixed = 0;                  // SGM_PCG_ITERS: fixed count instead
   size_t pcg_n = 0;
   // device
   double* tables_dev = nullptr;       // [3][OP_COUNT][Lmax][RS] (seg_sweep.cuh row layout), then diag factors
