@@ -91,3 +91,29 @@ def test_dimensions():
         assert forms.form_dim(f["cplx"], f["k"], f["p"], f["n"]) == f["dim"], f
     c = gold["K1_block_C1"]
     assert int(np.prod(forms.component_shapes("primal", 1, c["p"], c["n"])[0])) == c["size"]
+
+
+def test_curved_map_converges_to_cube_spectrum():
+    """SURVEY 8(c) physics pin: the C3 map sends the unit cube onto itself, so with eps = mu = 1 the
+    discrete spectrum on the curved mesh converges to the same exact cavity spectrum:
+    the five lowest eigenvalues -> (2, 2, 2, 3, 3) pi^2 with error ~ h^(2(p-1)) (the map breaks the
+    cube's symmetry, so the multiplicities split at finite h)."""
+    from oracle import workloads as W
+    gold = load("cavity_spectrum.json")
+    ref = np.array(gold["eigenvalues_over_pi2"][:5], dtype=float) * np.pi ** 2
+    p, errs = 3, []
+    for n in (3, 4, 5):
+        tb = TierB(p, n, ctrl=W.interpolate_map(p, n, W.c3_map))
+        N = tb.N_e
+        A = np.zeros((N, N))
+        I = np.eye(N)
+        for i in range(N):
+            e = tb.solve_K1(tb.mass_eps(tb.split_e(I[:, i])))
+            h = tb.solve_Kt1(tb.mass_mu(curl_primal(e)))
+            A[:, i] = forms.join(curl_dual(h))
+        ev = np.sort(np.linalg.eigvals(A).real)
+        got = ev[ev > 1e-10 * ev[-1]][:5]
+        assert np.all(got >= ref * (1 - 1e-12))
+        errs.append(np.max(np.abs(got - ref) / ref))
+    rates = [np.log(errs[0] / errs[1]) / np.log(4 / 3), np.log(errs[1] / errs[2]) / np.log(5 / 4)]
+    assert errs[-1] < 2e-3 and all(3.3 < r < 5.0 for r in rates), (errs, rates)
