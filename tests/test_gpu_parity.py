@@ -550,3 +550,28 @@ def test_scheme1_pcg_parity(case):
         o = _run_gpu(pl, st, dt, k)
         for a_, b_ in zip(o, A.run(*st, dt, k)):
             assert rel(a_, b_) < tol
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_shapes(seed):
+    """Seeded random degrees and anisotropic element counts (including single-element axes and long
+    thin boxes that change the sweep tiling, segment counts and fork/merge decisions): Hodge stars
+    and 5 steps of both schemes against the oracle."""
+    from oracle.structured import TierB1
+    g = np.random.default_rng(1000 + seed)
+    p = int(g.integers(2, 5))
+    n = tuple(int(v) for v in g.choice([1, 2, 3, 5, 8, 13, 21, 34], size=3))
+    for scheme in (2, 1):
+        pl = S.Plan(n, p)
+        if scheme == 1:
+            pl.set_scheme(1)
+        tb = TierB(p, n) if scheme == 2 else TierB1(p, n)
+        st = _state(tb, 2000 + seed)
+        x = st[0]
+        y = torch.empty(tb.N_e, dtype=torch.float64, device="cuda")
+        pl.hodge_star(S.MASS_EPS, dev(x), y)
+        assert rel(host(y), tb.hodge_eps(x)) < 1e-11, (p, n, scheme)
+        dt = 0.02 / max(n)
+        out = _run_gpu(pl, st, dt, 5)
+        for a_, b_ in zip(out, tb.run(*st, dt, 5)):
+            assert rel(a_, b_) < 1e-10, (p, n, scheme)
