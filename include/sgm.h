@@ -156,7 +156,9 @@ sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h,
    Unlike sgm_step, the state is SYNCHRONOUS: d, e, b, h at t_n on entry and at t_n + n_steps dt
    on exit.  weights: host [n_w], finite, 1 <= n_w <= SGM_MAX_STAGES.  j_amp: device
    [n_steps * n_w], s for drift i of step k at j_amp[k*n_w + i] (NULL -> 1).  Other arguments,
-   aliasing rules and errors as sgm_step.  Async; no graph capture. */
+   aliasing rules and errors as sgm_step.  Async.  On a non-default stream, for n_steps <= 4, the
+   call's launch sequence is captured into a CUDA graph on first use and replayed for later calls
+   with identical arguments (pointers, weights, dt, n_steps); invalidated like sgm_step's graph. */
 #define SGM_MAX_STAGES 16
 sgm_status sgm_step_composed(sgm_plan plan, double* d, double* e, double* b, double* h,
                              const double* j_hat, const double* j_amp, const double* weights,

@@ -804,6 +804,7 @@ sgm_status sgm_plan_destroy(sgm_plan plan) {
   if (P->device >= 0) {
     DeviceGuard g(P->device);
     if (P->graph_exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec));
+    if (P->graph_exec_c) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec_c));
     cudaFree(P->tables_dev);
     cudaFree(P->wide_dev);
     cudaFree(P->basis_dev);
@@ -891,10 +892,12 @@ sgm_status sgm_plan_set_scheme(sgm_plan plan, int scheme) {
     sgm_status st = upload_mass1(*P);
     if (st != SGM_OK) return st;
   }
-  if (P->scheme != scheme && P->graph_exec) {
+  if (P->scheme != scheme && (P->graph_exec || P->graph_exec_c)) {
     DeviceGuard g(P->device);
-    cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec));
+    if (P->graph_exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec));
+    if (P->graph_exec_c) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec_c));
     P->graph_exec = nullptr;
+    P->graph_exec_c = nullptr;
   }
   P->scheme = scheme;
   return SGM_OK;
@@ -908,10 +911,12 @@ sgm_status sgm_plan_reduced_schedule(sgm_plan plan, int* on) {
 }
 
 sgm_status sgm_plan_set_material(sgm_plan plan, sgm_material which, const double* values, double c) {
-  if (plan && PL(plan)->graph_exec) {  // captured launches embed the old weights and kinds
+  if (plan && (PL(plan)->graph_exec || PL(plan)->graph_exec_c)) {  // captured launches embed the old weights
     DeviceGuard g0(PL(plan)->device);
-    cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(PL(plan)->graph_exec));
+    if (PL(plan)->graph_exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(PL(plan)->graph_exec));
+    if (PL(plan)->graph_exec_c) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(PL(plan)->graph_exec_c));
     PL(plan)->graph_exec = nullptr;
+    PL(plan)->graph_exec_c = nullptr;
   }
   sgm_status s = check_plan(plan, false);
   if (s != SGM_OK) return s;
@@ -1018,18 +1023,47 @@ sgm_status sgm_step_composed(sgm_plan plan, double* d, double* e, double* b, dou
   if (n_steps == 0) return SGM_OK;
   // kick-drift-kick sub-steps S(w_i dt) in sequence; adjacent half kicks of b are merged
   // (b -= a D1 e; b -= c D1 e with the same e is b -= (a + c) D1 e)
-  const double* W = weights;
-  half_step(*P, 1, d, e, b, h, nullptr, nullptr, 0.5 * W[0] * dt, w, st);
-  for (int k = 0; k < n_steps; ++k)
-    for (int i = 0; i < n_w; ++i) {
-      const double* s_ptr = j_amp ? j_amp + size_t(k) * n_w + i : nullptr;
-      half_step(*P, 0, d, e, b, h, j_hat, s_ptr, W[i] * dt, w, st);
-      double kick;
-      if (i + 1 < n_w) kick = 0.5 * (W[i] + W[i + 1]);
-      else if (k + 1 < n_steps) kick = 0.5 * (W[i] + W[0]);
-      else kick = 0.5 * W[i];
-      half_step(*P, 1, d, e, b, h, nullptr, nullptr, kick * dt, w, st);
+  auto enqueue = [&]() {
+    const double* W = weights;
+    half_step(*P, 1, d, e, b, h, nullptr, nullptr, 0.5 * W[0] * dt, w, st);
+    for (int k = 0; k < n_steps; ++k)
+      for (int i = 0; i < n_w; ++i) {
+        const double* s_ptr = j_amp ? j_amp + size_t(k) * n_w + i : nullptr;
+        half_step(*P, 0, d, e, b, h, j_hat, s_ptr, W[i] * dt, w, st);
+        double kick;
+        if (i + 1 < n_w) kick = 0.5 * (W[i] + W[i + 1]);
+        else if (k + 1 < n_steps) kick = 0.5 * (W[i] + W[0]);
+        else kick = 0.5 * W[i];
+        half_step(*P, 1, d, e, b, h, nullptr, nullptr, kick * dt, w, st);
+      }
+  };
+  // the whole call's launch sequence is captured once per argument set and replayed (non-default
+  // stream, not profiling, at most 4 composed steps per call so the graph stays small)
+  if (!P->profiling && stream != nullptr && P->graph_enabled && n_steps <= 4) {
+    const GraphKey key{d, e, b, h, j_hat, j_amp, dt, n_steps, workspace};
+    const std::vector<double> wv(weights, weights + n_w);
+    if (!(P->graph_exec_c && P->graph_key_c == key && P->graph_w_c == wv)) {
+      if (P->graph_exec_c) {
+        cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec_c));
+        P->graph_exec_c = nullptr;
+      }
+      cudaGraph_t graph = nullptr;
+      if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+        return cuda_check(P, "sgm_step_composed: begin capture");
+      enqueue();
+      if (cudaStreamEndCapture(st, &graph) != cudaSuccess) return cuda_check(P, "sgm_step_composed: end capture");
+      cudaGraphExec_t exec = nullptr;
+      const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ie != cudaSuccess) return cuda_check(P, "sgm_step_composed: graph instantiate");
+      P->graph_exec_c = exec;
+      P->graph_key_c = key;
+      P->graph_w_c = wv;
     }
+    cudaGraphLaunch(static_cast<cudaGraphExec_t>(P->graph_exec_c), st);
+    return cuda_check(P, "sgm_step_composed (graph)");
+  }
+  enqueue();
   return cuda_check(P, "sgm_step_composed");
 }
 

@@ -121,6 +121,9 @@ struct Plan {
   std::mutex fork_mu;
   void* graph_exec = nullptr;         // cudaGraphExec_t of the last captured sgm_step call
   GraphKey graph_key{};
+  void* graph_exec_c = nullptr;       // ... of the last captured sgm_step_composed call
+  GraphKey graph_key_c{};
+  std::vector<double> graph_w_c;      // its weights
   size_t N_e = 0, N_h = 0;
   // optional per-kernel event timing (sgm_plan_set_profiling)
   bool profiling = false;

@@ -575,3 +575,25 @@ def test_random_shapes(seed):
         out = _run_gpu(pl, st, dt, 5)
         for a_, b_ in zip(out, tb.run(*st, dt, 5)):
             assert rel(a_, b_) < 1e-10, (p, n, scheme)
+
+
+def test_step_composed_graph_replay():
+    """sgm_step_composed on a non-default stream: the first call captures its launch sequence, later
+    identical calls replay it; 8 calls of one Yoshida step equal the oracle's 8 composed steps."""
+    from oracle import compose
+    p, n = 3, (6, 7, 5)
+    pl = S.Plan(n, p)
+    tb = TierB(p, n)
+    st = _state(tb, 97)
+    dt = 0.2 * W.cfl_dt_max(tb)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        d, e, b, h = (dev(x) for x in st)
+        for _ in range(8):
+            pl.step_composed(d, e, b, h, dt, compose.YOSHIDA4, 1, stream=s)
+        out = [host(x) for x in (d, e, b, h)]
+    ref = st
+    for _ in range(8):
+        ref = compose.run_composed(tb, *ref, dt, 1)
+    for x, y in zip(out, ref):
+        assert rel(x, y) < 1e-10
