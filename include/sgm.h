@@ -36,9 +36,14 @@
  *   (e.g. torch.float64 CUDA tensors' data_ptr()).  `stream` is a cudaStream_t passed as void*
  *   (NULL = legacy default stream).  Calls marked async enqueue work on `stream` and return.
  * - Arguments are validated before any launch: on SGM_E_INVALID_ARG nothing was modified.
- * - The plan is immutable after create except through set_material (synchronous; must not
- *   overlap in-flight calls on the plan).  Concurrent calls on different streams with
- *   distinct workspaces are allowed.
+ * - The plan is immutable after create except through set_material / set_scheme (synchronous;
+ *   must not overlap in-flight calls on the plan).  Concurrent calls on different streams with
+ *   distinct workspaces are allowed (the plan-owned helper stream of the concurrent sweep pairs
+ *   is fork/joined under a lock).
+ * - Beyond the step: sgm_plan_set_scheme selects the paper's first scheme
+ *   (mass-matrix Hodge stars); sgm_step_composed composes leapfrog sub-steps into
+ *   higher-order symplectic steps; sgm_cfl estimates the stability limit; rational
+ *   (NURBS) maps enter through sgm_plan_desc.geom_weights.
  * - There is no CPU fallback: a plan created with device < 0 answers queries (lengths,
  *   shapes, 1D tables, quadrature coordinates) but every compute call returns
  *   SGM_E_INVALID_ARG.
