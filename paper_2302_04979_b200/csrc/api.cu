@@ -240,10 +240,14 @@ bool eps_merged(const Plan& P) { return mu_merged(P); }
 // strided side weighted 1.25 when its lines need so many segment warps that fewer than four
 // producer warps fit the 16-warp CTA (measured at p = 3, 160^3: strided tiles ~25 % slower than x
 // tiles; at p = 4 and such lengths both sides drop to one line per thread and the plain split wins)
-Share strided_share(const Plan& P, int axis, int n_strided, int n_x) {
+// The x side is weighted 1.25 when its lines have even length (16-byte-aligned slab rows then give
+// 4-way instead of 2-way bank conflicts in the consumers' line walks; measured at p = 2, 128^3:
+// 145 -> 138 us per step), except at p = 4 where the strided side stays the slower one.
+Share strided_share(const Plan& P, int axis, int n_strided, int n_x, bool x_even) {
   const int L = P.rpad[axis], nc = (L + P.seg[axis] - 1) / P.seg[axis];
   const double ws = n_strided * ((16 - nc) < 4 && P.p <= 3 ? 1.25 : 1.0);
-  const int k = int(1000.0 * ws / (ws + n_x) + 0.5);
+  const double wx = n_x * (x_even && P.p <= 3 ? 1.25 : 1.0);  // at p = 4 the strided side is the slower one
+  const int k = int(1000.0 * ws / (ws + wx) + 0.5);
   return {k, 1000};
 }
 
@@ -291,7 +295,8 @@ void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* 
       PassComp b1[1] = {{1, 0, T[0], Y[0], op, {0, -1, -1}, M.scale[0]}};
       PassComp c2[2] = {{0, 1, T[1], Y[1], op, {-1, 0, -1}, M.scale[1]}, {0, 2, T[2], Y[2], op, {-1, -1, 0}, M.scale[2]}};
       { ProfScope ps(P, kz, st); sweep_pass_list(P, 0, a3, 3, st, 1); }
-      const Share sb = strided_share(P, 1, 1, 2), sc = {sb.n - sb.k, sb.n};
+      // x side: components 1, 2 of e/d, x-extent a (P.ax[0].a)
+      const Share sb = strided_share(P, 1, 1, 2, (P.ax[0].a % 2) == 0), sc = {sb.n - sb.k, sb.n};
       fork_join(P, st, [&](cudaStream_t s1) { ProfScope ps(P, ky, s1); sweep_pass_list(P, 0, b1, 1, s1, 0, sb); },
                 [&](cudaStream_t s2) { ProfScope ps(P, kx, s2); sweep_pass_list(P, 0, c2, 2, s2, 1, sc); });
       return;
@@ -313,7 +318,8 @@ void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* 
       // component 0 (independent) concurrently on the plan-owned stream when forking is enabled
       PassComp zy[2] = {z[0], yy[0]};
       if (P.fork_enabled) {
-        const Share sd = strided_share(P, 2, 2, 1), se = {sd.n - sd.k, sd.n};
+        // x side: component 0 of b/h, x-extent a
+        const Share sd = strided_share(P, 2, 2, 1, (P.ax[0].a % 2) == 0), se = {sd.n - sd.k, sd.n};
         fork_join(P, st, [&](cudaStream_t s1) { ProfScope ps(P, kz, s1); sweep_pass_list(P, 1, zy, 2, s1, 1, sd); },
                   [&](cudaStream_t s2) { ProfScope ps(P, kx, s2); sweep_pass_list(P, 1, xx, 1, s2, 1, se); });
         return;
