@@ -164,3 +164,33 @@ def test_scheme1_full_size():
     pl.step(*dv, dt, 1)
     for a, r in zip(dv, tb.step(*st, dt)):
         assert rel(host(a), r) < 1e-11
+
+
+def test_standalone_operators_full_size():
+    """SURVEY 8(c) parity for the standalone entry points at 128^3 p = 3: K1 / K~1 solves (and their
+    transposes), pairing applies, the separable mass applies and both curls against tier B."""
+    from oracle import forms
+    from oracle.structured import curl_primal, curl_dual
+    p, n = 3, 128
+    pl = S.Plan(n, p)
+    tb = TierB(p, n)
+    g = np.random.default_rng(17)
+    r = g.standard_normal(tb.N_e)
+    rh = g.standard_normal(tb.N_h)
+    x = torch.empty(tb.N_e, dtype=torch.float64, device="cuda")
+    xh = torch.empty(tb.N_h, dtype=torch.float64, device="cuda")
+    for T in (False, True):
+        pl.kron_solve(S.K1, dev(r), x, transpose=T)
+        assert rel(host(x), forms.join(tb.solve_K1(tb.split_e(r), T=T))) < 1e-12
+        pl.kron_solve(S.KT1, dev(rh), xh, transpose=T)
+        assert rel(host(xh), forms.join(tb.solve_Kt1(tb.split_h(rh), T=T))) < 1e-12
+        pl.pairing_apply(S.K1, dev(r), x, transpose=T)
+        assert rel(host(x), forms.join(tb.apply_K1(tb.split_e(r), T=T))) < 1e-13
+    pl.hodge_apply(S.MASS_EPS, dev(r), x)
+    assert rel(host(x), forms.join(tb.mass_eps(tb.split_e(r)))) < 1e-13
+    pl.hodge_apply(S.MASS_MU, dev(rh), xh)
+    assert rel(host(xh), forms.join(tb.mass_mu(tb.split_h(rh)))) < 1e-13
+    pl.curl(S.CURL_PRIMAL, dev(r), xh)
+    assert np.array_equal(host(xh), forms.join(curl_primal(tb.split_e(r))))
+    pl.curl(S.CURL_DUAL, dev(rh), x)
+    assert np.array_equal(host(x), forms.join(curl_dual(tb.split_h(rh))))
