@@ -597,3 +597,32 @@ def test_step_composed_graph_replay():
         ref = compose.run_composed(tb, *ref, dt, 1)
     for x, y in zip(out, ref):
         assert rel(x, y) < 1e-10
+
+
+def test_abi_argument_validation_on_device():
+    """Device plans validate before launching (SGM_E_INVALID_ARG = 1, nothing modified): aliasing
+    state vectors, a too-small workspace, non-finite dt, negative n_steps, bad composition weights,
+    distinctness in sgm_cfl; a non-divergence-free source is reported by sgm_check_source."""
+    import ctypes
+    p, n = 2, 4
+    pl = S.Plan(n, p)
+    st = _state(TierB(p, n), 3)
+    d, e, b, h = (dev(x) for x in st)
+    keep = [host(x) for x in (d, e, b, h)]
+    ws = pl.workspace()
+    P = S._ptr
+    nb = ws.numel() * 8
+    assert S.sgm_step(pl.h, P(d), P(d), P(b), P(h), None, None, 0.01, 1, P(ws), nb, None) == 1
+    assert S.sgm_step(pl.h, P(d), P(e), P(b), P(h), None, None, 0.01, 1, P(ws), 64, None) == 1
+    assert S.sgm_step(pl.h, P(d), P(e), P(b), P(h), None, None, float("nan"), 1, P(ws), nb, None) == 1
+    assert S.sgm_step(pl.h, P(d), P(e), P(b), P(h), None, None, 0.01, -1, P(ws), nb, None) == 1
+    w = np.array([1.0, float("inf")])
+    assert S.sgm_step_composed(pl.h, P(d), P(e), P(b), P(h), None, None, w.ctypes.data, 2, 0.01, 1,
+                               P(ws), nb, None) == 1
+    out = torch.zeros(2, dtype=torch.float64, device="cuda")
+    assert S.sgm_cfl(pl.h, P(d), P(d), P(b), P(h), 3, P(out), P(ws), nb, None) == 1
+    for a, k in zip((d, e, b, h), keep):
+        assert np.array_equal(host(a), k)
+    assert "alias" in S._lib.sgm_last_error().decode() or "distinct" in S._lib.sgm_last_error().decode()
+    # a non-solenoidal source is refused by the check (SGM_E_SOURCE_DIVERGENCE = 6)
+    assert pl.check_source(dev(np.random.default_rng(5).standard_normal(pl.N_e))) == 6
