@@ -8,7 +8,7 @@ python -m pytest tests -m gpu -q 2>&1 | tail -5 > gpurun_out/pytest_gpu_$TAG.log
 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1
 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err
 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err
-for cfg in "--p 2 --n 160" "--p 4 --n 128" "--p 3 --n 64" "--config c4" "--config c3"; do
+for cfg in "--p 2 --n 160" "--p 4 --n 128" "--p 3 --n 64" "--config c2" "--config c4" "--config c3"; do
   python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e $cfg >> gpurun_out/bench_sweep_$TAG.jsonl 2>> gpurun_out/bench_sweep_$TAG.err
 done
 python scripts/c5_sweep.py --out gpurun_out/c5_sweep_$TAG.jsonl > gpurun_out/c5_sweep_$TAG.log 2>&1
