@@ -156,9 +156,9 @@ def build_inputs(args, torch, S, dev):
     p, n, desc, geo, mat, src = workload(args)
     ctrl = None
     if geo == "c3":
-        # spline interpolation of the C3 map lives on the oracle side (input generation only)
-        from oracle import workloads as W
-        ctrl = W.interpolate_map(p, n, W.c3_map)
+        # the closed-form C3 map interpolated at the Greville points by the library (reading Z18)
+        import synth
+        ctrl = S.interpolate_geometry(n, p, synth.c3_map)
     pl = S.Plan(n, p, geom_ctrl=ctrl, device=dev.index or 0)
     if getattr(args, "scheme", 2) == 1:
         pl.set_scheme(1)

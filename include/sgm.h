@@ -234,6 +234,16 @@ sgm_status sgm_cfl(sgm_plan plan, double* x, double* e, double* b, double* h, in
    sgm_plan_set_material while scheme 1 is selected. */
 sgm_status sgm_plan_set_scheme(sgm_plan plan, int scheme);
 
+/* Geometry input helpers (reading Z18: a map is represented in S_p(Xi)^3 by interpolation at the
+   Greville points of the untrimmed basis).  Host-only, synchronous.
+   sgm_geometry_greville: the n_el + p Greville abscissae of one axis into g_host.
+   sgm_geometry_interpolate: control points (layout of sgm_plan_desc.geom_ctrl) whose spline
+   interpolates the map values given at the tensor Greville grid, values_host laid out
+   [(nz+p)][(ny+p)][(nx+p)][3] with x fastest (dense collocation LU per axis, mode by mode). */
+sgm_status sgm_geometry_greville(int n_el, int degree, double* g_host);
+sgm_status sgm_geometry_interpolate(const int n_el[3], int degree, const double* values_host,
+                                    double* ctrl_host);
+
 /* *on = 1 if separable Hodge stars use the reduced schedule (the diagonal 1D
    factors Hat M^{-1} Gamma_B^{p-1} = diag(1/s) and Hat M^{-T} Gamma_C^{p-1} = diag(s), verified at
    plan creation, replace their line sweeps by per-line scalings), 2 if in addition independent

@@ -71,6 +71,8 @@ _SIGS = {
     "sgm_plan_kernels_per_step": [c_void_p, ctypes.POINTER(c_int)],
     "sgm_plan_reduced_schedule": [c_void_p, ctypes.POINTER(c_int)],
     "sgm_plan_set_scheme": [c_void_p, c_int],
+    "sgm_geometry_greville": [c_int, c_int, c_void_p],
+    "sgm_geometry_interpolate": [c_void_p, c_int, c_void_p, c_void_p],
     "sgm_plan_set_profiling": [c_void_p, c_int],
     "sgm_plan_profile": [c_void_p, c_void_p, c_void_p],
 }
@@ -118,6 +120,23 @@ def _stream(stream):
         return stream if isinstance(stream, int) else stream.cuda_stream
     import torch
     return torch.cuda.current_stream().cuda_stream
+
+
+def interpolate_geometry(n_el, degree, fmap):
+    """Control points of a map F: X[..., 3] -> F[..., 3] interpolated in S_p(Xi)^3 at the Greville
+    points (sgm_geometry_greville / sgm_geometry_interpolate)."""
+    n = (n_el,) * 3 if np.isscalar(n_el) else tuple(n_el)
+    gs = []
+    for a in range(3):
+        g = np.empty(n[a] + degree)
+        check(sgm_geometry_greville(n[a], degree, g.ctypes.data), "sgm_geometry_greville")
+        gs.append(g)
+    Z, Y, X = np.meshgrid(gs[2], gs[1], gs[0], indexing="ij")
+    vals = np.ascontiguousarray(fmap(np.stack([X, Y, Z], -1)), dtype=np.float64)
+    ctrl = np.empty_like(vals)
+    nn = (c_int * 3)(*n)
+    check(sgm_geometry_interpolate(nn, degree, vals.ctypes.data, ctrl.ctypes.data), "sgm_geometry_interpolate")
+    return ctrl
 
 
 # Yoshida's 4th-order symmetric composition ("triple jump") of leapfrog sub-steps

@@ -909,6 +909,23 @@ sgm_status sgm_plan_set_scheme(sgm_plan plan, int scheme) {
   return SGM_OK;
 }
 
+sgm_status sgm_geometry_greville(int n_el, int degree, double* g_host) {
+  if (!g_host || n_el < 1) return fail(SGM_E_INVALID_ARG, "NULL output or n_el < 1");
+  if (degree < SGM_PMIN || degree > SGM_PMAX) return fail(SGM_E_UNSUPPORTED, "degree outside the compiled range");
+  const std::vector<double> g = greville(degree, n_el);
+  std::copy(g.begin(), g.end(), g_host);
+  return SGM_OK;
+}
+
+sgm_status sgm_geometry_interpolate(const int n_el[3], int degree, const double* values_host, double* ctrl_host) {
+  if (!n_el || !values_host || !ctrl_host) return fail(SGM_E_INVALID_ARG, "NULL argument");
+  if (n_el[0] < 1 || n_el[1] < 1 || n_el[2] < 1) return fail(SGM_E_INVALID_ARG, "n_el < 1");
+  if (degree < SGM_PMIN || degree > SGM_PMAX) return fail(SGM_E_UNSUPPORTED, "degree outside the compiled range");
+  std::string err;
+  const sgm_status st = interpolate_geometry(n_el, degree, values_host, ctrl_host, err);
+  return st == SGM_OK ? st : fail(st, err);
+}
+
 sgm_status sgm_plan_reduced_schedule(sgm_plan plan, int* on) {
   if (!plan || !on) return fail(SGM_E_INVALID_ARG, "NULL argument");
   const Plan& P = *PL(plan);

@@ -798,4 +798,83 @@ sgm_status build_mass1(Plan& P, int which, std::vector<double>& W, std::string& 
   return SGM_OK;
 }
 
+// Greville abscissae of the untrimmed S_p on n uniform elements: g_i = mean(U[i+1 .. i+p]).
+std::vector<double> greville(int p, int n) {
+  const std::vector<double> U = open_knots(p, n);
+  std::vector<double> g(n + p);
+  for (int i = 0; i < n + p; ++i) {
+    double s = 0.0;
+    for (int k = 1; k <= p; ++k) s += U[i + k];
+    g[i] = s / p;
+  }
+  return g;
+}
+
+// Geometry control points interpolating map values given at the Greville grid (reading Z18):
+// per axis the collocation matrix C[j][i] = N_i(g_j) of the untrimmed S_p is inverted (dense LU
+// with partial pivoting, applied mode by mode); layout [(nz+p)][(ny+p)][(nx+p)][3] in and out.
+sgm_status interpolate_geometry(const int n_el[3], int p, const double* values, double* ctrl, std::string& err) {
+  const int m[3] = {n_el[0] + p, n_el[1] + p, n_el[2] + p};
+  std::vector<double> cur(values, values + size_t(m[0]) * m[1] * m[2] * 3), nxt(cur.size());
+  for (int a = 0; a < 3; ++a) {
+    const int L = m[a], n = n_el[a];
+    const std::vector<double> U = open_knots(p, n), g = greville(p, n);
+    std::vector<double> C(size_t(L) * L, 0.0);
+    for (int j = 0; j < L; ++j) {
+      int sp = p;  // knot span of g_j: U[sp] <= x < U[sp+1] (the last point uses the last span)
+      while (sp < n + p - 1 && g[j] >= U[sp + 1]) ++sp;
+      double N[16];
+      basis_funs(U.data(), sp, g[j], p, N);
+      for (int k = 0; k <= p; ++k) C[size_t(j) * L + (sp - p + k)] = N[k];
+    }
+    // LU with partial pivoting
+    std::vector<int> piv(L);
+    for (int k = 0; k < L; ++k) {
+      int r = k;
+      for (int i = k + 1; i < L; ++i)
+        if (std::fabs(C[size_t(i) * L + k]) > std::fabs(C[size_t(r) * L + k])) r = i;
+      if (!(std::fabs(C[size_t(r) * L + k]) > 0.0)) {
+        err = "singular geometry collocation matrix";
+        return SGM_E_SINGULAR;
+      }
+      piv[k] = r;
+      if (r != k)
+        for (int j = 0; j < L; ++j) std::swap(C[size_t(k) * L + j], C[size_t(r) * L + j]);
+      for (int i = k + 1; i < L; ++i) {
+        const double f = C[size_t(i) * L + k] / C[size_t(k) * L + k];
+        C[size_t(i) * L + k] = f;
+        for (int j = k + 1; j < L; ++j) C[size_t(i) * L + j] -= f * C[size_t(k) * L + j];
+      }
+    }
+    // solve along axis a for every line and coordinate
+    const long stride = (a == 0) ? 3 : (a == 1 ? 3L * m[0] : 3L * m[0] * m[1]);
+    const long lines = long(cur.size()) / L;
+    std::vector<double> v(L);
+    for (long l = 0; l < lines; ++l) {
+      // line l -> base offset: decompose l over the other indices (coordinate fastest)
+      long rem = l, base = 0, mult = 1;
+      const int dims[4] = {3, m[0], m[1], m[2]};
+      for (int d = 0; d < 4; ++d) {
+        if (d == a + 1) { mult *= dims[d]; continue; }
+        const long idx = rem % dims[d];
+        rem /= dims[d];
+        base += idx * mult;
+        mult *= dims[d];
+      }
+      for (int i = 0; i < L; ++i) v[i] = cur[base + i * stride];
+      for (int k = 0; k < L; ++k) std::swap(v[k], v[piv[k]]);
+      for (int i = 1; i < L; ++i)
+        for (int k = 0; k < i; ++k) v[i] -= C[size_t(i) * L + k] * v[k];
+      for (int i = L - 1; i >= 0; --i) {
+        for (int k = i + 1; k < L; ++k) v[i] -= C[size_t(i) * L + k] * v[k];
+        v[i] /= C[size_t(i) * L + i];
+      }
+      for (int i = 0; i < L; ++i) nxt[base + i * stride] = v[i];
+    }
+    cur.swap(nxt);
+  }
+  std::copy(cur.begin(), cur.end(), ctrl);
+  return SGM_OK;
+}
+
 }  // namespace sgm

@@ -135,6 +135,8 @@ struct Plan {
 // host setup (host_setup.cpp)
 sgm_status build_axis(int p, int n, int Q, Axis& out, std::string& err);
 sgm_status build_mass1(Plan& P, int which, std::vector<double>& W, std::string& err);
+std::vector<double> greville(int p, int n);
+sgm_status interpolate_geometry(const int n_el[3], int p, const double* values, double* ctrl, std::string& err);
 sgm_status banded_lu_nopivot(const std::vector<double>& A, int L, int m, std::vector<double>& LU,
                              std::string& err);
 sgm_status build_tables(Plan& P, std::string& err);

@@ -43,3 +43,10 @@ def smooth_field(k, shape):
     kz, ky, kx = np.meshgrid(*[np.arange(s) for s in shape], indexing="ij")
     X /= 1.0 + (kx ** 2 + ky ** 2 + kz ** 2)
     return idctn(X, norm="ortho")
+
+
+def c3_map(X):
+    """BASELINE.json configs[2] geometry, a closed-form input: x -> x + 0.1 sin(pi x) sin(pi y)
+    sin(pi z) (1, 1, 1) on the unit cube (X[..., 3] -> F[..., 3])."""
+    s = 0.1 * np.sin(np.pi * X[..., 0]) * np.sin(np.pi * X[..., 1]) * np.sin(np.pi * X[..., 2])
+    return X + s[..., None]

@@ -169,3 +169,15 @@ def test_scheme_selection_rules():
 def W_curved(p, n):
     from oracle import workloads as W
     return W.interpolate_map(p, n, W.c3_map)
+
+
+@pytest.mark.parametrize("p,n", [(2, 3), (3, (4, 5, 3)), (4, 6)])
+def test_library_geometry_interpolation(p, n):
+    """sgm_geometry_interpolate (used by bench.py for the C3 map) equals the oracle's Greville
+    interpolation, and synth.c3_map equals the oracle's C3 map."""
+    import synth
+    from oracle import workloads as W
+    a = S.interpolate_geometry(n, p, synth.c3_map)
+    assert np.abs(a - W.interpolate_map(p, n, W.c3_map)).max() < 1e-13
+    X = np.random.default_rng(3).uniform(size=(7, 3))
+    assert np.array_equal(synth.c3_map(X), W.c3_map(X))
