@@ -58,6 +58,8 @@ def parse():
     ap.add_argument("--n", type=int, default=128)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--opts", type=lambda v: int(v, 0), default=0,
+                    help="SGM_OPT_* schedule option bits (0 = the production schedule)")
     ap.add_argument("--scheme", type=int, default=2, choices=[1, 2],
                     help="Hodge stars: 2 = pairing solves (the paper's method, default), 1 = mass solves")
     return ap.parse_args()
@@ -162,6 +164,7 @@ def build_inputs(args, torch, S, dev):
     pl = S.Plan(n, p, geom_ctrl=ctrl, device=dev.index or 0)
     if getattr(args, "scheme", 2) == 1:
         pl.set_scheme(1)
+    pl.set_options(getattr(args, "opts", 0))
     if mat is not None:
         X = pl.qp_coords()
         if mat == "c3":
@@ -196,23 +199,32 @@ def launch_bytes(pl, S, N_e, N_h, has_src):
     reads the curl source, the state (and j^) and writes the state; the general Hodge reads x and the
     quadrature weights W and read-modify-writes y ("Kernels and their rooflines")."""
     out = []
+    mode = pl.schedule_mode()
     for half, (N, Ns, pre) in enumerate(((N_e, N_h, "eps"), (N_h, N_e, "mu"))):
         src = 8 * N if (half == 0 and has_src) else 0
+        sep = pl.separable(S.MASS_EPS if half == 0 else S.MASS_MU)
+        if sep and (mode == 3 or (mode == 0 and pl.options() & S.OPT_FUSED)):
+            # fused schedule: the update runs inside the first sweep launch, which reads the curl
+            # source (N_s) and the state (N) and writes the state and the sweep output (2 N)
+            out.append(("fused_" + pre, 8 * (Ns + 3 * N) + src))
+            if mode == 3:
+                if half == 0:  # {0 along y} || {1, 2 along x}
+                    out += [("eps_y", 16 * N / 3), ("eps_x", 16 * N * 2 / 3)]
+            else:
+                out += [(pre + "_y", 16 * N), (pre + "_x", 16 * N)]
+            continue
         out.append(("update", 8 * (Ns + 2 * N) + src))
-        if pl.separable(S.MASS_EPS if half == 0 else S.MASS_MU):
+        if sep:
             # reduced schedule: an eps pass sweeps 2 of the 3 (equal-size) components, a mu pass 1
             if not pl.reduced_schedule():
                 out += [(pre + "_z", 16 * N), (pre + "_y", 16 * N), (pre + "_x", 16 * N)]
-            elif half == 0 and pl.schedule_mode() == 2:
+            elif half == 0 and mode == 2:
                 # eps: {0 z, 1 z, 2 y} in one launch, then {0 y} and {1 x, 2 x} concurrently
                 out += [(pre + "_z", 16 * N), (pre + "_y", 16 * N / 3), (pre + "_x", 16 * N * 2 / 3)]
             elif half == 0:
                 out += [(pre + "_z", 16 * N * 2 / 3), (pre + "_y", 16 * N * 2 / 3), (pre + "_x", 16 * N * 2 / 3)]
-            elif pl.kernels_per_step() - (4 if pl.separable(S.MASS_EPS) else 5) == 3:
-                # mu: z-lines of component 2 and y-lines of component 1 in one launch, then x
-                out += [(pre + "_z", 16 * N * 2 / 3), (pre + "_x", 16 * N / 3)]
             else:
-                out += [(pre + "_z", 16 * N / 3), (pre + "_y", 16 * N / 3), (pre + "_x", 16 * N / 3)]
+                out += [(pre + "_z", 16 * N * 2 / 3), (pre + "_x", 16 * N / 3)]
         else:
             wq = pl.qp_count() * (6 if pl.geom else 1) * 8
             out += [("hodge_general", 24 * N + wq), ("solve_z", 16 * N), (pre + "_y", 16 * N), (pre + "_x", 16 * N)]

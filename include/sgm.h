@@ -138,13 +138,16 @@ sgm_status sgm_workspace_bytes(sgm_plan plan, size_t* bytes);
    (check once with sgm_check_source), NULL = no source.  j_amp: device, length n_steps,
    s_k multiplying j^ at step k (the paper's separable-in-time source); NULL -> 1.0.
    On exit d, e are at t_n + n_steps dt and b, h at t_{n+1/2} + n_steps dt.
-   Launches: per step sgm_plan_kernels_per_step kernels (separable Hodge stars with the reduced
-   schedule: 7 -- an update and three sweeps for the eps half, an update and two sweeps for the mu
-   half, independent sweeps concurrently on a plan-owned stream) with programmatic dependent
-   launch.  On a non-default stream, with j_amp == NULL or n_steps == 1, the launch sequence of one
+   Launches: per step sgm_plan_kernels_per_step kernels with programmatic dependent launch
+   (separable Hodge stars, reduced schedule: 7 -- an update and three sweeps for the eps half, an
+   update and two sweeps for the mu half, independent sweeps concurrently on a plan-owned stream;
+   SGM_OPT_FUSED: 4; see sgm_kernel_class).  On a non-default stream, with j_amp == NULL or n_steps == 1, the launch sequence of one
    step is captured into a CUDA graph on first use and replayed for later calls with identical
    arguments (pointers, dt; a replay reads the current value of j_amp[0]) -- the plan keeps one
-   graph; set_material invalidates it; SGM_GRAPH=0 disables. */
+   graph; set_material / set_scheme / set_options invalidate it; SGM_OPT_NO_GRAPH disables; a call
+   on a stream that is being captured by the caller enqueues directly into the caller's capture.
+   SGM_E_UNSUPPORTED after launch: no compiled kernel configuration fits the plan's line lengths
+   (the state may be partially updated). */
 sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h,
                     const double* j_hat, const double* j_amp, double dt, int n_steps,
                     void* workspace, size_t ws_bytes, void* stream);
@@ -230,7 +233,7 @@ sgm_status sgm_cfl(sgm_plan plan, double* x, double* e, double* b, double* h, in
    (weights w gamma DF^{-1} DF^{-T} det DF), the separable star with the mean material as
    preconditioner, no host synchronisation; the iteration count is calibrated per star when the
    weights are built (one solve with residual read-back, relative preconditioned residual 1e-14,
-   plus 3; SGM_PCG_ITERS fixes it instead).  The 1-form weights (and the calibration) are redone by
+   plus 3).  The 1-form weights (and the calibration) are redone by
    sgm_plan_set_material while scheme 1 is selected. */
 sgm_status sgm_plan_set_scheme(sgm_plan plan, int scheme);
 
@@ -244,11 +247,27 @@ sgm_status sgm_geometry_greville(int n_el, int degree, double* g_host);
 sgm_status sgm_geometry_interpolate(const int n_el[3], int degree, const double* values_host,
                                     double* ctrl_host);
 
+/* ---- schedule options (sgm_plan_set_options; all off = the production schedule) ----------
+   They change which kernels run, never what is computed (results agree to rounding; the parity
+   tests run every option).  Synchronous; invalidates the captured graphs. */
+#define SGM_OPT_FULL_SCHEDULE 0x1u /* separable stars sweep every axis of every Kronecker factor (no
+                                      diagonal-factor shortcut) */
+#define SGM_OPT_EXACT_SPIKE 0x2u   /* untruncated SPIKE history/future scans (reading Z23 off) */
+#define SGM_OPT_SERIAL 0x4u        /* no concurrent sweep launches */
+#define SGM_OPT_NO_GRAPH 0x8u      /* sgm_step / sgm_step_composed enqueue directly (no graph replay) */
+#define SGM_OPT_FUSED 0x10u        /* separable scheme-2 stars: the Ampere / Faraday update fused into
+                                      the first sweep launch of each half step (fsweep_kernel.cuh;
+                                      4 launches per step instead of 7, 40 instead of 48 B per
+                                      DOF-update; measured slower on B200 at 128^3, DESIGN.md s. 6) */
+sgm_status sgm_plan_set_options(sgm_plan plan, unsigned opts);
+sgm_status sgm_plan_get_options(sgm_plan plan, unsigned* opts);
+
 /* *on = 1 if separable Hodge stars use the reduced schedule (the diagonal 1D
    factors Hat M^{-1} Gamma_B^{p-1} = diag(1/s) and Hat M^{-T} Gamma_C^{p-1} = diag(s), verified at
    plan creation, replace their line sweeps by per-line scalings), 2 if in addition independent
-   sweeps run concurrently on a plan-owned stream (fork/join on events; SGM_FORK=0 disables),
-   0 if every axis is swept. */
+   sweeps run concurrently on a plan-owned stream (default; SGM_OPT_SERIAL disables),
+   3 with the fused update (SGM_OPT_FUSED), 0 if every axis is swept
+   (SGM_OPT_FULL_SCHEDULE or a failed identity). */
 sgm_status sgm_plan_reduced_schedule(sgm_plan plan, int* on);
 
 /* Number of kernels one sgm_step step launches for this plan (for launch accounting). */
@@ -257,20 +276,25 @@ sgm_status sgm_plan_kernels_per_step(sgm_plan plan, int* n);
 /* Per-kernel timing of sgm_step (CUDA events recorded on the launching stream around every
    kernel when enabled).  Kernel classes: */
 typedef enum {
-  /* Separable Hodge stars, reduced schedule with concurrent launches:
-     EPS_Z = strided launch {0, 1 along z; 2 along y}, EPS_Y = {0 along y} and EPS_X = {1, 2 along x}
-     (concurrent), MU_Z = {2 along z, 1 along y} and MU_X = {0 along x} (concurrent; MU_Y unused).
-     Full three-axis schedule (SGM_NODIAG=1) and general-Hodge solves: the z, y, x sweeps. */
+  /* Default (separable stars, reduced schedule): UPDATE, then
+     EPS_Z = {0, 1 along z; 2 along y}, EPS_Y = {0 along y} and EPS_X = {1, 2 along x} (concurrent),
+     UPDATE, MU_Z = {2 along z, 1 along y} and MU_X = {0 along x} (concurrent).
+     SGM_OPT_FUSED: FUSED_EPS = Ampere update fused into {0, 1 along z; 2 along y} d -> t, then
+     EPS_Y || EPS_X as above, FUSED_MU = Faraday update fused into {2 along z; 1 along y; 0 along x}.
+     Full three-axis schedule: the z (or FUSED_*), y and x launches.  General Hodge: UPDATE,
+     HODGE_GENERAL, SOLVE_Z, *_Y, *_X. */
   SGM_K_EPS_Z = 0,     /* eps half, first sweep launch (Gram mat-vec . K1 factor solve), d -> t */
   SGM_K_EPS_Y = 1,     /* eps half, y-line sweep */
-  SGM_K_EPS_X = 2,     /* eps half, x-line sweep (writes e) */
+  SGM_K_EPS_X = 2,     /* eps half, last sweep launch (writes e) */
   SGM_K_MU_Z = 3,      /* mu half, strided sweep (Gram mat-vec . K~1 factor solve), b -> h */
   SGM_K_MU_Y = 4,      /* mu half, y-line sweep (unmerged or full schedule only) */
   SGM_K_MU_X = 5,      /* mu half, x-line sweep (writes h) */
   SGM_K_UPDATE = 6,    /* Ampere / Faraday update d += dt (D~1 h - s j), b -= dt D1 e (both halves) */
   SGM_K_HODGE_GENERAL = 7, /* sum-factorised mass apply with quadrature weights (general Hodge) */
   SGM_K_SOLVE_Z = 8,   /* solve-only z sweep (general-Hodge path) */
-  SGM_K_CLASSES = 9
+  SGM_K_FUSED_EPS = 9, /* Ampere update fused into the first eps sweep launch */
+  SGM_K_FUSED_MU = 10, /* Faraday update fused into the first mu sweep launch */
+  SGM_K_CLASSES = 11
 } sgm_kernel_class;
 sgm_status sgm_plan_set_profiling(sgm_plan plan, int on);
 /* Sums, per class, the event-timed milliseconds and launch counts recorded since the last call

@@ -39,7 +39,10 @@ K1, KT1 = 0, 1
 MASS_EPS, MASS_MU = 0, 1
 CURL_PRIMAL, CURL_DUAL = 0, 1
 EPS, MU = 0, 1
-K_CLASSES = ["eps_z", "eps_y", "eps_x", "mu_z", "mu_y", "mu_x", "update", "hodge_general", "solve_z"]
+K_CLASSES = ["eps_z", "eps_y", "eps_x", "mu_z", "mu_y", "mu_x", "update", "hodge_general", "solve_z",
+             "fused_eps", "fused_mu"]
+# schedule options (sgm.h SGM_OPT_*)
+OPT_FULL_SCHEDULE, OPT_EXACT_SPIKE, OPT_SERIAL, OPT_NO_GRAPH, OPT_FUSED = 0x1, 0x2, 0x4, 0x8, 0x10
 TAB_G, TAB_M, TAB_GAMMA_B1, TAB_GAMMA_C2, TAB_GAMMA_BP, TAB_GAMMA_C1 = range(6)
 
 _SIGS = {
@@ -71,6 +74,8 @@ _SIGS = {
     "sgm_plan_kernels_per_step": [c_void_p, ctypes.POINTER(c_int)],
     "sgm_plan_reduced_schedule": [c_void_p, ctypes.POINTER(c_int)],
     "sgm_plan_set_scheme": [c_void_p, c_int],
+    "sgm_plan_set_options": [c_void_p, ctypes.c_uint],
+    "sgm_plan_get_options": [c_void_p, ctypes.POINTER(ctypes.c_uint)],
     "sgm_geometry_greville": [c_int, c_int, c_void_p],
     "sgm_geometry_interpolate": [c_void_p, c_int, c_void_p, c_void_p],
     "sgm_plan_set_profiling": [c_void_p, c_int],
@@ -235,8 +240,18 @@ class Plan:
         """1: mass-matrix Hodge stars (first scheme), 2: pairing solves (second scheme, default)."""
         check(sgm_plan_set_scheme(self.h, int(scheme)), "sgm_plan_set_scheme")
 
+    def set_options(self, opts):
+        """SGM_OPT_* bits (OPT_FULL_SCHEDULE, OPT_EXACT_SPIKE, OPT_SERIAL, OPT_NO_GRAPH, OPT_FUSED)."""
+        check(sgm_plan_set_options(self.h, int(opts)), "sgm_plan_set_options")
+
+    def options(self):
+        v = ctypes.c_uint(0)
+        check(sgm_plan_get_options(self.h, ctypes.byref(v)), "sgm_plan_get_options")
+        return v.value
+
     def schedule_mode(self):
-        """0: full three-axis sweeps, 1: reduced separable schedule, 2: reduced with concurrent sweeps."""
+        """0: full three-axis sweeps, 1: reduced separable schedule, 2: reduced with concurrent
+        sweeps (default), 3: reduced with the update fused into the first sweeps (OPT_FUSED)."""
         v = c_int(0)
         check(sgm_plan_reduced_schedule(self.h, ctypes.byref(v)), "sgm_plan_reduced_schedule")
         return v.value

@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <initializer_list>
 #include <new>
 #include <string>
 
@@ -39,13 +40,38 @@ sgm_status fail(sgm_status s, const std::string& msg) {
   return s;
 }
 
+// After enqueuing: a CUDA error is sticky for the plan; a launcher that found no compiled kernel
+// configuration (P->launch_fail, e.g. shared memory of the pipelined sweeps at long lines) is
+// reported as SGM_E_UNSUPPORTED (not sticky).
 sgm_status cuda_check(Plan* P, const char* where) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     if (P) P->sticky_cuda_error = true;
     return fail(SGM_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
   }
+  if (P && P->launch_fail) {
+    P->launch_fail = 0;
+    return fail(SGM_E_UNSUPPORTED, std::string(where) +
+                                       ": no compiled sweep configuration fits these line lengths (kernel not launched)");
+  }
   return SGM_OK;
+}
+
+// Drop the captured graphs (their launches embed weights, tables, options)
+void drop_graphs(Plan& P) {
+  if (!(P.graph_exec || P.graph_exec_c) || P.device < 0) return;
+  DeviceGuard g(P.device);
+  if (P.graph_exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P.graph_exec));
+  if (P.graph_exec_c) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P.graph_exec_c));
+  P.graph_exec = nullptr;
+  P.graph_exec_c = nullptr;
+}
+
+// the caller is capturing `st` into its own graph: enqueue directly (no nested capture)
+bool stream_capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (st == nullptr) return false;
+  return cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
 }
 
 inline bool aligned8(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 7) == 0; }
@@ -157,7 +183,7 @@ void sweep_pass(const Plan& P, int kind, int axis, double* const in[3], double* 
     a.comp[c].tslot = own_or(axis, c, 0, 1);
     a.comp[c].scale = scale ? scale[c] : 1.0;
   }
-  launch_sweep(P.p, P.seg[axis], a, st);
+  if (!launch_sweep(P.p, P.seg[axis], a, st)) P.launch_fail = 1;
 }
 
 // diagonal 1D factor of axis `axis`: kind 0 = 1/s (eps own axis), 1 = s (mu other axes)
@@ -226,12 +252,109 @@ void sweep_pass_list(const Plan& P, int kind, const PassComp* pc, int n, cudaStr
     C.dline[0] = q.dg[t0] >= 0 ? diag_factor(P, t0, q.dg[t0]) : nullptr;
     C.dline[1] = q.dg[t1] >= 0 ? diag_factor(P, t1, q.dg[t1]) : nullptr;
   }
-  launch_sweep(wide ? P.p + 1 : P.p, P.seg[pc[0].axis], a, st);
+  if (!launch_sweep(wide ? P.p + 1 : P.p, P.seg[pc[0].axis], a, st)) P.launch_fail = 1;
 }
+
+// The line-operator table of a component: axes with the same element count have bitwise identical
+// tables, so the lowest such axis's copy is used (fewer distinct tables per launch).
+const double* dedup_table(const Plan& P, int axis, int op) {
+  for (int a = 0; a < axis; ++a)
+    if (P.n[a] == P.n[axis]) return table(P, a, op);
+  return table(P, axis, op);
+}
+
+// Partition of a component list into launches: one segment length, one padded table length and at
+// most two distinct tables per launch.  Returns the number of launches; grp[g][0..gn[g]) indices.
+int group_passes(const Plan& P, const PassComp* pc, int n, int grp[3][3], int gn[3]) {
+  bool used[3] = {false, false, false};
+  int ng = 0;
+  for (int i = 0; i < n; ++i) {
+    if (used[i]) continue;
+    int m = 0;
+    const double* tabs[2] = {dedup_table(P, pc[i].axis, pc[i].op), nullptr};
+    grp[ng][m++] = i;
+    used[i] = true;
+    for (int j = i + 1; j < n; ++j) {
+      if (used[j] || P.seg[pc[j].axis] != P.seg[pc[i].axis] || P.rpad[pc[j].axis] != P.rpad[pc[i].axis]) continue;
+      const double* t = dedup_table(P, pc[j].axis, pc[j].op);
+      if (t != tabs[0] && t != tabs[1]) {
+        if (tabs[1]) continue;
+        tabs[1] = t;
+      }
+      grp[ng][m++] = j;
+      used[j] = true;
+    }
+    gn[ng++] = m;
+  }
+  return ng;
+}
+
+// Fused update + first sweep (fsweep_kernel.cuh) over a list of components, each along its own
+// axis, grouped into as few launches as possible (group_passes).  fuse = 1 / 2: the Ampere /
+// Faraday update of each component's state (in[c]) from `pro` (the curl source, j^, s, dt).
+// dry = true only checks that every group has a compiled configuration that fits (alignment,
+// shared memory); returns false (nothing launched) otherwise.
+bool fused_list(const Plan& P, int kind, const PassComp* pc, int n, cudaStream_t st, int reverse, int fuse,
+                const PrologueArgs& pro, int cls, bool dry) {
+  int grp[3][3], gn[3];
+  const int ng = group_passes(P, pc, n, grp, gn);
+  for (int g = 0; g < ng; ++g) {
+    const int* idx = grp[g];
+    const int m = gn[g];
+    const int i = idx[0];
+    const double* tabs[2] = {dedup_table(P, pc[i].axis, pc[i].op), nullptr};
+    for (int k = 1; k < m; ++k) {
+      const double* t = dedup_table(P, pc[idx[k]].axis, pc[idx[k]].op);
+      if (t != tabs[0]) tabs[1] = t;
+    }
+    SweepArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.ncomp = m;
+    a.axis = -1;
+    a.band = 1;
+    a.solve = 1;
+    a.tabs[0] = tabs[0];
+    a.tabs[1] = tabs[1];
+    a.tab_rows = P.rpad[pc[i].axis];
+    a.reverse = reverse;
+    a.pro = pro;
+    a.dry = dry ? 1 : 0;
+    for (int k = 0; k < m; ++k) {
+      const PassComp& q = pc[idx[k]];
+      const int axis = q.axis;
+      const int t0 = (axis == 0) ? 1 : 0, t1 = (axis == 2) ? 1 : 2;
+      a.band_hw = std::max(a.band_hw, P.band_hw[axis][q.op]);
+      a.spike_kh = std::max(a.spike_kh, P.spike_kh[axis][q.op]);
+      a.spike_kf = std::max(a.spike_kf, P.spike_kf[axis][q.op]);
+      SweepComp& C = a.comp[k];
+      comp_shape(P, kind, q.c, C.ext);
+      C.in = const_cast<double*>(q.in);
+      C.out = q.out;
+      C.tab = dedup_table(P, axis, q.op);
+      C.tslot = (a.tabs[1] && C.tab == a.tabs[1]) ? 1 : 0;
+      C.axis = axis;
+      C.cidx = q.c;
+      C.scale = q.scale;
+      C.dline[0] = q.dg[t0] >= 0 ? diag_factor(P, t0, q.dg[t0]) : nullptr;
+      C.dline[1] = q.dg[t1] >= 0 ? diag_factor(P, t1, q.dg[t1]) : nullptr;
+    }
+    if (dry) {
+      if (!launch_fsweep(P.p, P.seg[pc[i].axis], fuse, a, st)) return false;
+      continue;
+    }
+    ProfScope ps(const_cast<Plan&>(P), cls, st);
+    if (!launch_fsweep(P.p, P.seg[pc[i].axis], fuse, a, st)) P.launch_fail = 1;
+  }
+  return true;
+}
+
+inline bool fused_sched(const Plan& P) { return (P.opts & SGM_OPT_FUSED) && P.scheme == 2; }
+inline bool reduced_sched(const Plan& P) { return P.diag_ok && (P.scheme == 1 || !(P.opts & SGM_OPT_FULL_SCHEDULE)); }
+inline bool fork_on(const Plan& P) { return P.fork_enabled && !(P.opts & SGM_OPT_SERIAL); }
 
 // The mu star's z and y sweeps share one launch when their axes have equal table geometry.
 bool mu_merged(const Plan& P) {
-  return P.seg[1] == P.seg[2] && P.rpad[1] == P.rpad[2] && !getenv("SGM_NOMERGE");
+  return P.seg[1] == P.seg[2] && P.rpad[1] == P.rpad[2] && !tune_int("SGM_NOMERGE", 0);
 }
 // ... and so do the eps star's first z- and y-line sweeps
 bool eps_merged(const Plan& P) { return mu_merged(P); }
@@ -286,7 +409,7 @@ void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* 
   if (kind == 0) {
     // scheme 2: Hat G^{-1} Gamma_C^{p-2}; scheme 1: Gamma_B^p^{-1} Hat G^T (own axis: diag(1/s) in both)
     const int op = P.scheme == 1 ? OP_S1_EPS_OTH_W : OP_EPS_OTH;
-    if (P.fork_enabled && eps_merged(P)) {
+    if (fork_on(P) && eps_merged(P)) {
       // strided pass {0 along z, 1 along z, 2 along y}, then concurrently {0 along y} (strided,
       // 1/3 of the SMs) and {1, 2 along x} (2/3 of the SMs, plan-owned stream)
       PassComp a3[3] = {{2, 0, X[0], T[0], op, {-1, -1, -1}, 1.0},
@@ -317,7 +440,7 @@ void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* 
       // z-lines of component 2 and y-lines of component 1 in one strided launch; the x-lines of
       // component 0 (independent) concurrently on the plan-owned stream when forking is enabled
       PassComp zy[2] = {z[0], yy[0]};
-      if (P.fork_enabled) {
+      if (fork_on(P)) {
         // x side: component 0 of b/h, x-extent a
         const Share sd = strided_share(P, 2, 2, 1, (P.ax[0].a % 2) == 0), se = {sd.n - sd.k, sd.n};
         fork_join(P, st, [&](cudaStream_t s1) { ProfScope ps(P, kz, s1); sweep_pass_list(P, 1, zy, 2, s1, 1, sd); },
@@ -331,6 +454,87 @@ void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* 
     }
     { ProfScope ps(P, kx, st); sweep_pass_list(P, 1, xx, 1, st, 1); }
   }
+}
+
+// Whether the fused kernel has a fitting configuration for this plan's half step `which` (shared
+// memory and segments; pointers of a real call are checked again when it is enqueued).
+PrologueArgs make_pro(const Plan& P, int src_kind, const double* src, const double* jhat, const double* s_ptr,
+                      double dt);
+bool fused_fits(const Plan& P, int which, bool with_source) {
+  const int kind = which == SGM_MASS_EPS ? 0 : 1;
+  alignas(16) static double dummy[2];
+  PrologueArgs pro = make_pro(P, 1 - kind, dummy, nullptr, nullptr, 1.0);
+  for (int c = 0; c < 3; ++c) pro.src[c] = dummy;
+  if (kind == 0 && with_source) pro.jhat[0] = pro.jhat[1] = pro.jhat[2] = dummy;
+  PassComp pc[3];
+  const int own = kind == 0 ? OP_EPS_OWN : OP_MU_OWN, oth = kind == 0 ? OP_EPS_OTH : OP_MU_OTH;
+  if (!reduced_sched(P)) {
+    for (int c = 0; c < 3; ++c) pc[c] = {2, c, dummy, dummy, own_or(2, c, own, oth), {-1, -1, -1}, 1.0};
+  } else if (kind == 0) {
+    pc[0] = {2, 0, dummy, dummy, oth, {-1, -1, -1}, 1.0};
+    pc[1] = {2, 1, dummy, dummy, oth, {-1, -1, -1}, 1.0};
+    pc[2] = {1, 2, dummy, dummy, oth, {-1, -1, -1}, 1.0};
+  } else {
+    pc[0] = {2, 2, dummy, dummy, own, {-1, -1, -1}, 1.0};
+    pc[1] = {1, 1, dummy, dummy, own, {-1, -1, -1}, 1.0};
+    pc[2] = {0, 0, dummy, dummy, own, {-1, -1, -1}, 1.0};
+  }
+  return fused_list(P, kind, pc, 3, nullptr, 0, kind + 1, pro, 0, true);
+}
+
+// The fused separable half step (SGM_OPT_FUSED): the Ampere / Faraday update of the state x is
+// fused into the first sweep launch of its Hodge star (fsweep_kernel.cuh, SURVEY 8(d) fused P1):
+//   reduced eps: fused {0, 1 along z; 2 along y} x -> t, then {0 along y} || {1, 2 along x} t -> y
+//                (pipelined sweeps, concurrent as in hodge_star_reduced);
+//   reduced mu:  fused {2 along z; 1 along y; 0 along x} x -> y;
+//   full:        fused z pass (all components) x -> t, then the y and x passes.
+// Returns false (nothing enqueued) when the fused kernel has no fitting configuration.
+bool star_fused(Plan& P, int which, double* x, double* y, double* t, cudaStream_t st, const PrologueArgs& pro) {
+  const int kind = (which == SGM_MASS_EPS) ? 0 : 1;
+  const int fuse = kind + 1;
+  const double* sc = P.mass[which].scale;
+  double *X[3], *Y[3], *T[3];
+  comps_of(P, kind, x, X);
+  comps_of(P, kind, y, Y);
+  comps_of(P, kind, t, T);
+  const int cls = kind == 0 ? SGM_K_FUSED_EPS : SGM_K_FUSED_MU;
+  if (!reduced_sched(P)) {
+    const int own = kind == 0 ? OP_EPS_OWN : OP_MU_OWN, oth = kind == 0 ? OP_EPS_OTH : OP_MU_OTH;
+    PassComp z3[3];
+    for (int c = 0; c < 3; ++c) z3[c] = {2, c, X[c], T[c], own_or(2, c, own, oth), {-1, -1, -1}, 1.0};
+    if (!fused_list(P, kind, z3, 3, st, 1, fuse, pro, cls, true)) return false;
+    fused_list(P, kind, z3, 3, st, 1, fuse, pro, cls, false);
+    const int ky = kind == 0 ? SGM_K_EPS_Y : SGM_K_MU_Y, kx = kind == 0 ? SGM_K_EPS_X : SGM_K_MU_X;
+    { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, true, true, st, 0); }
+    { ProfScope ps(P, kx, st); sweep_pass(P, kind, 0, T, Y, own, oth, sc, true, true, st, 1); }
+    return true;
+  }
+  if (kind == 0) {
+    const int op = OP_EPS_OTH;
+    PassComp a3[3] = {{2, 0, X[0], T[0], op, {-1, -1, -1}, 1.0},
+                      {2, 1, X[1], T[1], op, {-1, -1, -1}, 1.0},
+                      {1, 2, X[2], T[2], op, {-1, -1, -1}, 1.0}};
+    if (!fused_list(P, 0, a3, 3, st, 1, fuse, pro, cls, true)) return false;
+    fused_list(P, 0, a3, 3, st, 1, fuse, pro, cls, false);
+    PassComp b1[1] = {{1, 0, T[0], Y[0], op, {0, -1, -1}, sc[0]}};
+    PassComp c2[2] = {{0, 1, T[1], Y[1], op, {-1, 0, -1}, sc[1]}, {0, 2, T[2], Y[2], op, {-1, -1, 0}, sc[2]}};
+    if (fork_on(P)) {
+      const Share sb = strided_share(P, 1, 1, 2, (P.ax[0].a % 2) == 0), sc2 = {sb.n - sb.k, sb.n};
+      fork_join(P, st, [&](cudaStream_t s1) { ProfScope ps(P, SGM_K_EPS_Y, s1); sweep_pass_list(P, 0, b1, 1, s1, 0, sb); },
+                [&](cudaStream_t s2) { ProfScope ps(P, SGM_K_EPS_X, s2); sweep_pass_list(P, 0, c2, 2, s2, 1, sc2); });
+    } else {
+      { ProfScope ps(P, SGM_K_EPS_Y, st); sweep_pass_list(P, 0, b1, 1, st, 0); }
+      { ProfScope ps(P, SGM_K_EPS_X, st); sweep_pass_list(P, 0, c2, 2, st, 1); }
+    }
+    return true;
+  }
+  const int op = OP_MU_OWN;
+  PassComp m3[3] = {{2, 2, X[2], Y[2], op, {1, 1, -1}, sc[2]},
+                    {1, 1, X[1], Y[1], op, {1, -1, 1}, sc[1]},
+                    {0, 0, X[0], Y[0], op, {-1, 1, 1}, sc[0]}};
+  if (!fused_list(P, 1, m3, 3, st, 1, fuse, pro, cls, true)) return false;
+  fused_list(P, 1, m3, 3, st, 1, fuse, pro, cls, false);
+  return true;
 }
 
 // y = (A_z (x) A_y (x) A_x) x per component with 3 sweeps x -> t -> t -> y (x == y allowed).
@@ -663,6 +867,9 @@ void half_step(Plan& P, int half, double* d, double* e, double* b, double* h, co
   PrologueArgs pa = half == 0 ? make_pro(P, 1, h, jhat, s_ptr, tau) : make_pro(P, 0, e, nullptr, nullptr, tau);
   const MassData& M = P.mass[mass];
   comps_of(P, kind, w.t, T);
+  // fused schedule (SGM_OPT_FUSED): the update runs inside the first sweep launch of the half step
+  // (falls back to the separate update kernel when the fused kernel has no fitting configuration)
+  if (M.kind == HODGE_SEPARABLE && fused_sched(P) && star_fused(P, mass, state[0], outv[0], w.t, st, pa)) return;
   SweepArgs a;
   std::memset(&a, 0, sizeof(a));
   a.ncomp = 3;
@@ -674,7 +881,7 @@ void half_step(Plan& P, int half, double* d, double* e, double* b, double* h, co
   { ProfScope ps(P, SGM_K_UPDATE, st); launch_update(pro, a, st); }
   if (P.scheme == 1 && P.mass1[mass].kind != HODGE_SEPARABLE) {
     { ProfScope ps(P, SGM_K_HODGE_GENERAL, st); pcg_star(P, mass, state[0], outv[0], w, st); }
-  } else if (M.kind == HODGE_SEPARABLE && P.diag_ok) {
+  } else if (M.kind == HODGE_SEPARABLE && reduced_sched(P)) {
     hodge_star_reduced(P, mass, state[0], outv[0], w.t, st);
   } else if (M.kind == HODGE_SEPARABLE) {
     // streaming update kernel, then the three mass . solve sweeps (z, y, x); snake order: update
@@ -725,7 +932,7 @@ sgm_status sgm_plan_create(const sgm_plan_desc* desc, sgm_plan* out) {
   P->p = p;
   P->Q = Q;
   P->device = desc->device;
-  if (const char* ge = getenv("SGM_GRAPH")) P->graph_enabled = atoi(ge) != 0;
+  P->graph_enabled = tune_int("SGM_GRAPH", 1) != 0;
   std::string err;
   for (int a = 0; a < 3; ++a) {
     P->n[a] = desc->n_el[a];
@@ -781,9 +988,8 @@ sgm_status sgm_plan_create(const sgm_plan_desc* desc, sgm_plan* out) {
       P->aux_stream = aux;
       P->ev_fork = e1;
       P->ev_join = e2;
-      const char* f = getenv("SGM_FORK");
-      P->fork_enabled = !(f && atoi(f) == 0);
-      if (const char* it = getenv("SGM_PCG_ITERS")) P->pcg_fixed = std::max(1, atoi(it));
+      P->fork_enabled = tune_int("SGM_FORK", 1) != 0;
+      if (const int it = tune_int("SGM_PCG_ITERS", 0)) P->pcg_fixed = std::max(1, it);
     }
     st = upload_basis(*P);
     if (st != SGM_OK) {
@@ -891,19 +1097,14 @@ sgm_status sgm_plan_set_scheme(sgm_plan plan, int scheme) {
   if (!plan) return fail(SGM_E_INVALID_ARG, "plan is NULL");
   Plan* P = PL(plan);
   if (scheme != 1 && scheme != 2) return fail(SGM_E_INVALID_ARG, "scheme must be 1 or 2");
+  if (scheme == 1 && P->wide_host.empty()) return fail(SGM_E_UNSUPPORTED, "scheme 1 tables missing");
+  if (scheme == 1 && !P->diag_ok) return fail(SGM_E_UNSUPPORTED, "scheme 1 needs the reduced separable schedule");
+  if (scheme == P->scheme) return SGM_OK;  // nothing to rebuild (the graphs stay valid)
+  drop_graphs(*P);                          // captured launches embed the scheme's weights and tables
   if (scheme == 1) {
-    if (P->wide_host.empty()) return fail(SGM_E_UNSUPPORTED, "scheme 1 tables missing");
-    if (!P->diag_ok) return fail(SGM_E_UNSUPPORTED, "scheme 1 needs the reduced separable schedule");
     DeviceGuard g(P->device >= 0 ? P->device : 0);
     sgm_status st = upload_mass1(*P);
     if (st != SGM_OK) return st;
-  }
-  if (P->scheme != scheme && (P->graph_exec || P->graph_exec_c)) {
-    DeviceGuard g(P->device);
-    if (P->graph_exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec));
-    if (P->graph_exec_c) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec_c));
-    P->graph_exec = nullptr;
-    P->graph_exec_c = nullptr;
   }
   P->scheme = scheme;
   return SGM_OK;
@@ -929,18 +1130,38 @@ sgm_status sgm_geometry_interpolate(const int n_el[3], int degree, const double*
 sgm_status sgm_plan_reduced_schedule(sgm_plan plan, int* on) {
   if (!plan || !on) return fail(SGM_E_INVALID_ARG, "NULL argument");
   const Plan& P = *PL(plan);
-  *on = P.diag_ok ? (P.fork_enabled && eps_merged(P) ? 2 : 1) : 0;
+  *on = reduced_sched(P) ? (fused_sched(P) ? 3 : (fork_on(P) && eps_merged(P) ? 2 : 1)) : 0;
+  return SGM_OK;
+}
+
+sgm_status sgm_plan_set_options(sgm_plan plan, unsigned opts) {
+  if (!plan) return fail(SGM_E_INVALID_ARG, "plan is NULL");
+  const unsigned all = SGM_OPT_FULL_SCHEDULE | SGM_OPT_EXACT_SPIKE | SGM_OPT_SERIAL | SGM_OPT_NO_GRAPH | SGM_OPT_FUSED;
+  if (opts & ~all) return fail(SGM_E_INVALID_ARG, "unknown option bits");
+  Plan* P = PL(plan);
+  if (P->device >= 0) {
+    DeviceGuard g(P->device);
+    cudaDeviceSynchronize();
+  }
+  drop_graphs(*P);
+  const bool spike_changed = ((P->opts ^ opts) & SGM_OPT_EXACT_SPIKE) != 0;
+  P->opts = opts;
+  if (spike_changed) {
+    std::string err;
+    const sgm_status st = set_spike_reach(*P, err);
+    if (st != SGM_OK) return fail(st, err);
+  }
+  return SGM_OK;
+}
+
+sgm_status sgm_plan_get_options(sgm_plan plan, unsigned* opts) {
+  if (!plan || !opts) return fail(SGM_E_INVALID_ARG, "NULL argument");
+  *opts = PL(plan)->opts;
   return SGM_OK;
 }
 
 sgm_status sgm_plan_set_material(sgm_plan plan, sgm_material which, const double* values, double c) {
-  if (plan && (PL(plan)->graph_exec || PL(plan)->graph_exec_c)) {  // captured launches embed the old weights
-    DeviceGuard g0(PL(plan)->device);
-    if (PL(plan)->graph_exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(PL(plan)->graph_exec));
-    if (PL(plan)->graph_exec_c) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(PL(plan)->graph_exec_c));
-    PL(plan)->graph_exec = nullptr;
-    PL(plan)->graph_exec_c = nullptr;
-  }
+  if (plan) drop_graphs(*PL(plan));  // captured launches embed the old weights
   sgm_status s = check_plan(plan, false);
   if (s != SGM_OK) return s;
   if (which != SGM_EPS && which != SGM_MU) return fail(SGM_E_INVALID_ARG, "bad material");
@@ -956,6 +1177,7 @@ sgm_status sgm_plan_set_material(sgm_plan plan, sgm_material which, const double
     DeviceGuard g(P->device >= 0 ? P->device : 0);
     s = upload_mass1(*P);
   }
+  drop_graphs(*P);
   return s;
 }
 
@@ -967,10 +1189,36 @@ sgm_status sgm_workspace_bytes(sgm_plan plan, size_t* bytes) {
 
 sgm_status sgm_plan_kernels_per_step(sgm_plan plan, int* n) {
   if (!plan || !n) return fail(SGM_E_INVALID_ARG, "NULL argument");
-  int k = 0;
   const Plan& P = *PL(plan);
-  for (int m = 0; m < 2; ++m)
-    k += (P.mass[m].kind == HODGE_SEPARABLE) ? ((m == SGM_MASS_MU && P.diag_ok && mu_merged(P)) ? 3 : 4) : 5;
+  auto groups = [&](std::initializer_list<std::pair<int, int>> axop) {
+    PassComp pc[3];
+    int m = 0;
+    for (const auto& q : axop) {
+      pc[m] = {q.first, m, nullptr, nullptr, q.second, {-1, -1, -1}, 1.0};
+      ++m;
+    }
+    int grp[3][3], gn[3];
+    return group_passes(P, pc, m, grp, gn);
+  };
+  int k = 0;
+  for (int m = 0; m < 2; ++m) {
+    const int own = m == 0 ? OP_EPS_OWN : OP_MU_OWN, oth = m == 0 ? OP_EPS_OTH : OP_MU_OTH;
+    auto axis_groups = [&](int ax) {
+      return groups({{ax, own_or(ax, 0, own, oth)}, {ax, own_or(ax, 1, own, oth)}, {ax, own_or(ax, 2, own, oth)}});
+    };
+    const bool sep = P.mass[m].kind == HODGE_SEPARABLE;
+    if (sep && fused_sched(P) && fused_fits(P, m, false)) {
+      if (!reduced_sched(P)) k += axis_groups(2) + 2;
+      else if (m == 0) k += groups({{2, oth}, {2, oth}, {1, oth}}) + 2;
+      else k += groups({{2, own}, {1, own}, {0, own}});
+      continue;
+    }
+    k += 1;  // the update kernel
+    if (P.scheme == 1 && P.mass1[m].kind != HODGE_SEPARABLE) k += 4;  // (PCG: counted as one star)
+    else if (sep && reduced_sched(P)) k += (m == SGM_MASS_MU && mu_merged(P)) ? 2 : 3;
+    else if (sep) k += 3;
+    else k += 4;
+  }
   *n = k;
   return SGM_OK;
 }
@@ -997,7 +1245,8 @@ sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h, c
   // legacy default stream (capture is not allowed there) and not while profiling records events.
   // With per-step amplitudes the captured step reads s from j_amp[0]: replayable for n_steps == 1
   // (a caller that refreshes the same device scalar every step, as a simulation loop does).
-  const bool use_graph = !P->profiling && stream != nullptr && P->graph_enabled && (j_amp == nullptr || n_steps == 1);
+  const bool use_graph = !P->profiling && stream != nullptr && P->graph_enabled && !(P->opts & SGM_OPT_NO_GRAPH) &&
+                         (j_amp == nullptr || n_steps == 1) && !stream_capturing(st);
   if (use_graph) {
     const GraphKey key{d, e, b, h, j_hat, j_amp, dt, 1, workspace};
     if (!(P->graph_exec && P->graph_key == key)) {
@@ -1008,8 +1257,13 @@ sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h, c
       cudaGraph_t graph = nullptr;
       if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
         return cuda_check(P, "sgm_step: begin capture");
+      P->launch_fail = 0;
       step_once(*P, d, e, b, h, j_hat, j_amp, dt, w, st);
       if (cudaStreamEndCapture(st, &graph) != cudaSuccess) return cuda_check(P, "sgm_step: end capture");
+      if (P->launch_fail) {  // incomplete step: do not keep (or run) it
+        cudaGraphDestroy(graph);
+        return cuda_check(P, "sgm_step");
+      }
       cudaGraphExec_t exec = nullptr;
       const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
       cudaGraphDestroy(graph);
@@ -1062,7 +1316,8 @@ sgm_status sgm_step_composed(sgm_plan plan, double* d, double* e, double* b, dou
   };
   // the whole call's launch sequence is captured once per argument set and replayed (non-default
   // stream, not profiling, at most 4 composed steps per call so the graph stays small)
-  if (!P->profiling && stream != nullptr && P->graph_enabled && n_steps <= 4) {
+  if (!P->profiling && stream != nullptr && P->graph_enabled && !(P->opts & SGM_OPT_NO_GRAPH) && n_steps <= 4 &&
+      !stream_capturing(st)) {
     const GraphKey key{d, e, b, h, j_hat, j_amp, dt, n_steps, workspace};
     const std::vector<double> wv(weights, weights + n_w);
     if (!(P->graph_exec_c && P->graph_key_c == key && P->graph_w_c == wv)) {
@@ -1073,8 +1328,13 @@ sgm_status sgm_step_composed(sgm_plan plan, double* d, double* e, double* b, dou
       cudaGraph_t graph = nullptr;
       if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
         return cuda_check(P, "sgm_step_composed: begin capture");
+      P->launch_fail = 0;
       enqueue();
       if (cudaStreamEndCapture(st, &graph) != cudaSuccess) return cuda_check(P, "sgm_step_composed: end capture");
+      if (P->launch_fail) {  // incomplete: do not keep (or run) it
+        cudaGraphDestroy(graph);
+        return cuda_check(P, "sgm_step_composed");
+      }
       cudaGraphExec_t exec = nullptr;
       const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
       cudaGraphDestroy(graph);
@@ -1192,7 +1452,7 @@ void hodge_star_impl(const Plan& P, int which, const double* x, double* y, const
   const MassData& M = P.mass[which];
   if (P.scheme == 1 && P.mass1[which].kind != HODGE_SEPARABLE) {
     pcg_star(const_cast<Plan&>(P), which, x, y, w, st);
-  } else if (M.kind == HODGE_SEPARABLE && P.diag_ok) {
+  } else if (M.kind == HODGE_SEPARABLE && reduced_sched(P)) {
     hodge_star_reduced(const_cast<Plan&>(P), which, x, y, w.t, st);
   } else if (M.kind == HODGE_SEPARABLE) {
     kron_pass3(P, kind, x, y, w.t, own, oth, M.scale, true, true, st);

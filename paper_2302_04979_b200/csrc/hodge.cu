@@ -1,10 +1,8 @@
-// General (non-separable) Hodge launchers: brick-tiled sum factorisation (hodge_brick.cuh), the
-// warp-per-pencil kernel (hodge_kernel.cuh, SGM_HODGE_PENCIL=1) and a generic CTA-per-element
-// kernel for quadrature rules other than p+1 points.
+// General (non-separable) Hodge launchers: brick-tiled sum factorisation (hodge_brick.cuh) and a
+// generic CTA-per-element kernel for quadrature rules other than p+1 points.
 #include <cuda_runtime.h>
 
 #include "hodge_brick.cuh"
-#include "hodge_kernel.cuh"
 #include "kernels.cuh"
 #include "launch_util.cuh"
 
@@ -127,35 +125,15 @@ __global__ void hodge_general_kernel(const __grid_constant__ HodgeArgs A) {
   }
 }
 
-template <int P, int Q, bool DUAL, bool FULL>
-void launch_hodge_pencil(const HodgeArgs& a, cudaStream_t st) {
-  constexpr int NL = P + 1, XB = hodge::max_box<P, DUAL>(), VB = Q * NL, CB = (P + 1) * Q * Q,
-                TB = (P + 1) * (P + 1) * Q;
-  const size_t smem = size_t(8) * (6 * XB + 9 * VB + CB + TB) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(hodge::hodge_pencil_kernel<P, Q, DUAL, FULL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
-    attr = true;
-  }
-  const long npen = long(a.nel[0]) * a.nel[1];
-  long grid = (npen + 7) / 8;
-  const long cap = 16L * sm_count();
-  if (grid > cap) grid = cap;
-  hodge::hodge_pencil_kernel<P, Q, DUAL, FULL><<<unsigned(grid), 256, smem, st>>>(a);
-}
-
 template <int P, int Q, int DUAL, bool FULL>
 void launch_hodge_brick(const HodgeArgs& a, cudaStream_t st) {
   constexpr int E = 4;
   using L = brick::Layout<P, Q, DUAL, E>;
   const size_t smem = size_t(L::template total<FULL>()) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
+  static unsigned long long attr = 0;  // per device
+  if (first_on_device(attr))
     cudaFuncSetAttribute(brick::hodge_brick_kernel<P, Q, DUAL, FULL, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          int(smem));
-    attr = true;
-  }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, brick::hodge_brick_kernel<P, Q, DUAL, FULL, E>, 256, smem);
   if (per_sm < 1) per_sm = 1;
@@ -165,7 +143,7 @@ void launch_hodge_brick(const HodgeArgs& a, cudaStream_t st) {
   long bzn = (4 * slots + bricks - 1) / bricks;
   int zchunk = int((a.nel[2] + bzn - 1) / bzn);
   if (zchunk < 4) zchunk = 4;
-  if (const int zc = env_int("SGM_HODGE_ZCHUNK", 0)) zchunk = zc;
+  if (const int zc = tune_int("SGM_HODGE_ZCHUNK", 0)) zchunk = zc;
   const long items = bricks * ((a.nel[2] + zchunk - 1) / zchunk);
   const long grid = items < slots ? items : slots;
   brick::hodge_brick_kernel<P, Q, DUAL, FULL, E><<<unsigned(grid), 256, smem, st>>>(a, zchunk);
@@ -184,29 +162,19 @@ void launch_hodge2(const HodgeArgs& a, cudaStream_t st) {
     }
     return;
   }
-  if (env_int("SGM_HODGE_PENCIL", 0) == 0) {
-    if (a.dual) {
-      if (a.full) launch_hodge_brick<P, Q, 1, true>(a, st);
-      else launch_hodge_brick<P, Q, 1, false>(a, st);
-    } else {
-      if (a.full) launch_hodge_brick<P, Q, 0, true>(a, st);
-      else launch_hodge_brick<P, Q, 0, false>(a, st);
-    }
-    return;
-  }
   if (a.dual) {
-    if (a.full) launch_hodge_pencil<P, Q, true, true>(a, st);
-    else launch_hodge_pencil<P, Q, true, false>(a, st);
+    if (a.full) launch_hodge_brick<P, Q, 1, true>(a, st);
+    else launch_hodge_brick<P, Q, 1, false>(a, st);
   } else {
-    if (a.full) launch_hodge_pencil<P, Q, false, true>(a, st);
-    else launch_hodge_pencil<P, Q, false, false>(a, st);
+    if (a.full) launch_hodge_brick<P, Q, 0, true>(a, st);
+    else launch_hodge_brick<P, Q, 0, false>(a, st);
   }
 }
 
 }  // namespace
 
 void launch_hodge_general(int p, const HodgeArgs& a, cudaStream_t st) {
-  // z-pencil warp kernel (hodge_kernel.cuh) for the default rule Q = p + 1; the generic
+  // brick sum-factorisation kernel (hodge_brick.cuh) for the default rule Q = p + 1; the generic
   // CTA-per-element kernel for larger rules (quad_points > p + 1)
   if (a.Q == p + 1) {
     switch (p) {

@@ -1,5 +1,5 @@
 // General (non-separable) 2-form Hodge apply y += M x by brick-tiled sum factorisation
-// (sm_100a, fp64).  Same operator as hodge_kernel.cuh (P:L360 M~2_{1/eps}, P:L366 M2_{1/mu}):
+// (sm_100a, fp64); the operator of P:L360 (M~2_{1/eps}) and P:L366 (M2_{1/mu}):
 // on element e,  y_c += V_c^T W_{cc'} V_{c'} x_{c'},  V_c the tensor product of the 1D element
 // bases at the Q Gauss points per axis, W = w_q / material * DF^T DF / det DF (FULL) or
 // w_q / material times a per-component constant (SCALAR).

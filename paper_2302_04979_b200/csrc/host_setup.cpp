@@ -406,9 +406,8 @@ void spike_reach(const double* T, int P, int L, int SEG, int& kh, int& kf) {
 int seg_for_line(int L) {
   // segment length of the partitioned line solve: one consumer warp per segment, at most 14
   // segments (16 warps per CTA with the producers); shortest segment that fits (more warps, fewer
-  // registers).  Override for tuning: SGM_SEG.
-  if (const char* e = getenv("SGM_SEG")) {
-    int v = atoi(e);
+  // registers).  Override in a tuning build: SGM_SEG.
+  if (const int v = tune_int("SGM_SEG", 0)) {
     if ((v == 12 || v == 17 || v == 28) && (L + v - 1) / v <= 14) return v;
   }
   const int cands[3] = {12, 17, 28};
@@ -417,8 +416,42 @@ int seg_for_line(int L) {
   return 28;
 }
 
+// Truncated-SPIKE reaches of every table (reading Z23), or the exact untruncated scans with
+// SGM_OPT_EXACT_SPIKE.  Also the band half-widths.  Recomputed by sgm_plan_set_options.
+sgm_status set_spike_reach(Plan& P, std::string& err) {
+  (void)err;
+  const bool noskip = (P.opts & SGM_OPT_EXACT_SPIKE) != 0;
+  const int p = P.p, RS = RowLayoutRT(p).RS;
+  const int Rmax = P.Lmax;
+  for (int a = 0; a < 3; ++a) {
+    const Axis& X = P.ax[a];
+    const int SEG = P.seg[a];
+    auto T = [&](int op) { return P.tables_host.data() + (size_t(a) * OP_COUNT + op) * Rmax * RS; };
+    if (!P.wide_host.empty()) {
+      const int RSw = RowLayoutRT(p + 1).RS;
+      const double* Tw = P.wide_host.data() + size_t(a) * Rmax * RSw;
+      if (noskip) P.wide_kh[a] = P.wide_kf[a] = (X.a + SEG - 1) / SEG;
+      else spike_reach(Tw, p + 1, X.a, SEG, P.wide_kh[a], P.wide_kf[a]);
+    }
+    const int Ls[OP_COUNT] = {X.b, X.a, X.a, X.b, X.b, X.a, X.a, X.b, X.a};
+    for (int op = 0; op < OP_COUNT; ++op) {
+      const int S = (Ls[op] + SEG - 1) / SEG;
+      P.band_hw[a][op] = table_band_hw(T(op), p, Ls[op]);
+      if (noskip || (op >= OP_APPLY_M && op <= OP_APPLY_MT)) {
+        P.spike_kh[a][op] = P.spike_kf[a][op] = S;
+      } else {
+        spike_reach(T(op), p, Ls[op], SEG, P.spike_kh[a][op], P.spike_kf[a][op]);
+      }
+      if (tune_int("SGM_DEBUG_PLAN", 0))
+        fprintf(stderr, "sgm plan: axis %d op %d L %d SEG %d S %d band_hw %d spike reach hist %d fut %d\n", a, op,
+                Ls[op], SEG, S, P.band_hw[a][op], P.spike_kh[a][op], P.spike_kf[a][op]);
+    }
+  }
+  return SGM_OK;
+}
+
 sgm_status build_tables(Plan& P, std::string& err) {
-  P.diag_ok = getenv("SGM_NODIAG") == nullptr || atoi(getenv("SGM_NODIAG")) == 0;
+  P.diag_ok = true;
   const int p = P.p, RS = RowLayoutRT(p).RS;
   int Rmax = 0;
   for (int a = 0; a < 3; ++a) {
@@ -429,7 +462,6 @@ sgm_status build_tables(Plan& P, std::string& err) {
   P.Lmax = Rmax;  // rows per table slot
   P.diag_off = size_t(3) * OP_COUNT * Rmax * RS;
   P.tables_host.assign(P.diag_off + size_t(3) * 2 * Rmax, 0.0);
-  const char* noskip = getenv("SGM_SPIKE_FULL");
   for (int a = 0; a < 3; ++a) {
     const Axis& X = P.ax[a];
     const int R = P.rpad[a], SEG = P.seg[a];
@@ -453,15 +485,13 @@ sgm_status build_tables(Plan& P, std::string& err) {
       double* Tw = P.wide_host.data() + size_t(a) * Rmax * RSw;
       if ((st = fill_table(Tw, p + 1, X.a, R, SEG, &GT, &X.GBp, err)) != SGM_OK) return st;
       P.wide_band_hw[a] = table_band_hw(Tw, p + 1, X.a);
-      if (noskip) P.wide_kh[a] = P.wide_kf[a] = (X.a + SEG - 1) / SEG;
-      else spike_reach(Tw, p + 1, X.a, SEG, P.wide_kh[a], P.wide_kf[a]);
     }
     // Diagonal 1D factors ("reduced separable schedule"): with the CS normalisation
     // D'_k = s_k B'_k, Hat M = Gamma_B^{p-1} diag(s) and Gamma_C^{p-1} =
     // diag(s) Gamma_B^{p-1} diag(s), so the own-axis factor of the eps Hodge star,
     // Hat M^{-1} Gamma_B^{p-1} = diag(1/s), and the other-axis factor of the mu Hodge star,
     // Hat M^{-T} Gamma_C^{p-1} = diag(s), are diagonal.  Checked here; the schedule falls back to
-    // full sweeps on every axis if an identity fails (or with SGM_NODIAG=1).
+    // full sweeps on every axis if an identity fails (SGM_OPT_FULL_SCHEDULE forces them).
     {
       const int L = X.b;
       double* dg_eps = P.tables_host.data() + P.diag_off + size_t(a * 2 + 0) * Rmax;
@@ -483,25 +513,12 @@ sgm_status build_tables(Plan& P, std::string& err) {
         dg_eps[k] = 1.0 / sk[k];
         dg_mu[k] = sk[k];
       }
-      if (getenv("SGM_DEBUG_PLAN"))
+      if (tune_int("SGM_DEBUG_PLAN", 0))
         fprintf(stderr, "sgm plan: axis %d diagonal factors: |M - G diag(s)| %.3g, |Gc - diag(s) G diag(s)| %.3g\n", a,
                 eM / mM, eC / mC);
     }
-    const int Ls[OP_COUNT] = {X.b, X.a, X.a, X.b, X.b, X.a, X.a, X.b, X.a};
-    for (int op = 0; op < OP_COUNT; ++op) {
-      const int S = (Ls[op] + SEG - 1) / SEG;
-      P.band_hw[a][op] = table_band_hw(T(op), p, Ls[op]);
-      if (noskip || (op >= OP_APPLY_M && op <= OP_APPLY_MT)) {
-        P.spike_kh[a][op] = P.spike_kf[a][op] = S;
-      } else {
-        spike_reach(T(op), p, Ls[op], SEG, P.spike_kh[a][op], P.spike_kf[a][op]);
-      }
-      if (getenv("SGM_DEBUG_PLAN"))
-        fprintf(stderr, "sgm plan: axis %d op %d L %d SEG %d S %d band_hw %d spike reach hist %d fut %d\n", a, op,
-                Ls[op], SEG, S, P.band_hw[a][op], P.spike_kh[a][op], P.spike_kf[a][op]);
-    }
   }
-  return SGM_OK;
+  return set_spike_reach(P, err);
 }
 
 // ---- geometry -------------------------------------------------------------------------------

@@ -5,7 +5,7 @@
 //   pairing factor) and a partitioned no-pivot banded LU solve, in persistent warp-specialised CTAs.
 // * Ampere / Faraday updates (integer +-1 curls, eqs. discrete2_ampere / _faraday):
 //   a streaming element-wise kernel.
-// * General Hodge (curved F or variable material, hodge_kernel.cuh): element-wise sum
+// * General Hodge (curved F or variable material, hodge_brick.cuh): element-wise sum
 //   factorisation with the quadrature weights W streamed from HBM.
 // * Curls, divergences (Gauss laws) and deterministic two-pass reductions (energy).
 #include <cuda_runtime.h>
@@ -248,13 +248,17 @@ __global__ void normalize_kernel(double* __restrict__ x, size_t n, const double*
 //   x += sign * (num / den) * p        and        p = z + (num / den) * p
 __global__ void axpy_ratio_kernel(double* __restrict__ x, const double* __restrict__ p, size_t n,
                                   const double* num, const double* den, double sign) {
-  const double a = sign * (__ldg(num) / __ldg(den));
+  // a zero denominator means a zero search direction (converged, or a zero right-hand side):
+  // the step is zero, not NaN
+  const double dn = __ldg(den);
+  const double a = dn != 0.0 ? sign * (__ldg(num) / dn) : 0.0;
   for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
     x[i] = fma(a, p[i], x[i]);
 }
 __global__ void xpby_ratio_kernel(double* __restrict__ p, const double* __restrict__ z, size_t n,
                                   const double* num, const double* den) {
-  const double b = __ldg(num) / __ldg(den);
+  const double dn = __ldg(den);
+  const double b = dn != 0.0 ? __ldg(num) / dn : 0.0;  // r.z = 0: restart from z
   for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
     p[i] = fma(b, p[i], z[i]);
 }
@@ -320,21 +324,30 @@ __global__ void finalize_max_kernel(const double* partials, int n_each, int ngro
 
 int partial_blocks() { return kRedBlocks; }
 
-void launch_sweep(int p, int seg, const SweepArgs& a, cudaStream_t st) {
+bool launch_sweep(int p, int seg, const SweepArgs& a, cudaStream_t st) {
   switch (p) {
-    case 2: launch_sweep_p2(seg, a, st); break;
-    case 3: launch_sweep_p3(seg, a, st); break;
-    case 4: launch_sweep_p4(seg, a, st); break;
-    case 5: launch_sweep_p5(seg, a, st); break;
-    default: break;
+    case 2: return launch_sweep_p2(seg, a, st);
+    case 3: return launch_sweep_p3(seg, a, st);
+    case 4: return launch_sweep_p4(seg, a, st);
+    case 5: return launch_sweep_p5(seg, a, st);
+    default: return false;
+  }
+}
+
+bool launch_fsweep(int p, int seg, int fuse, const SweepArgs& a, cudaStream_t st) {
+  switch (p) {
+    case 2: return launch_fsweep_p2(seg, fuse, a, st);
+    case 3: return launch_fsweep_p3(seg, fuse, a, st);
+    case 4: return launch_fsweep_p4(seg, fuse, a, st);
+    default: return false;
   }
 }
 
 void launch_update(int pro, const SweepArgs& a, cudaStream_t st) {
   UpdArgs U;
   std::memset(&U, 0, sizeof(U));
-  const int minb = env_int("SGM_UPD_MINB", 1);
-  int UU = env_int("SGM_UPD_U", 4);
+  const int minb = tune_int("SGM_UPD_MINB", 1);
+  int UU = tune_int("SGM_UPD_U", 4);
   if (!((UU == 4 && minb == 1) || (UU == 8 && minb == 1) || (UU == 4 && minb == 4) || (UU == 8 && minb == 2) ||
         (UU == 2 && minb == 4)))
     UU = 4;
@@ -365,13 +378,13 @@ void launch_update(int pro, const SweepArgs& a, cudaStream_t st) {
     }
   }
   U.nchunks = chunk;
-  U.reverse = env_int("SGM_SNAKE", 1) ? a.reverse : 0;
+  U.reverse = tune_int("SGM_SNAKE", 1) ? a.reverse : 0;
   U.s_ptr = a.pro.s_ptr;
   U.dt = a.pro.dt;
   // grid: exactly the resident CTAs (a grid-stride loop over equal chunks: no partial last wave;
   // measured 35 us vs 37 us for 8 CTAs per SM at 128^3 p=3); SGM_UPD_GRID = CTAs per SM override
   auto launch = [&](auto kern) {
-    int per_sm = env_int("SGM_UPD_GRID", 0);
+    int per_sm = tune_int("SGM_UPD_GRID", 0);
     if (per_sm <= 0) {
       static thread_local std::map<const void*, int> occ;  // per kernel instance (per host thread)
       int& o = occ[reinterpret_cast<const void*>(kern)];

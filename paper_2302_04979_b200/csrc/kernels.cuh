@@ -21,6 +21,7 @@ struct SweepComp {
   // (y, z) for x-lines (the diagonal 1D factors of the reduced separable schedule, api.cu)
   const double* dline[2];
   int axis;           // strided passes: this component's sweep axis (1 or 2); 0 = SweepArgs::axis
+  int cidx;           // component index 0..2 of the form (fused update: which curl component)
 };
 
 // Element-wise state update of a half step (launch_update):
@@ -50,6 +51,7 @@ struct SweepArgs {
                           // a kernel starts on what its predecessor wrote last, still in L2)
   PrologueArgs pro;       // update kernel only
   int share_k, share_n;   // sweeps: use share_k/share_n of the resident-CTA slots (0/0 = all)
+  int dry;                // fused sweeps: only check that a configuration fits (launch nothing)
 };
 
 // General (non-separable) Hodge apply y = M x by sum factorisation per element.
@@ -71,11 +73,19 @@ struct HodgeArgs {
                          // (M^1_eps, scheme 1), 3 dual 1-form (M~^1_mu, scheme 1)
 };
 
-void launch_sweep(int p, int seg, const SweepArgs& a, cudaStream_t st);
-void launch_sweep_p2(int seg, const SweepArgs& a, cudaStream_t st);  // sweep_p2.cu
-void launch_sweep_p3(int seg, const SweepArgs& a, cudaStream_t st);  // sweep_p3.cu
-void launch_sweep_p4(int seg, const SweepArgs& a, cudaStream_t st);  // sweep_p4.cu
-void launch_sweep_p5(int seg, const SweepArgs& a, cudaStream_t st);  // sweep_p5.cu (scheme-1 layout at p = 4)
+// pipelined (producer/consumer) sweeps; false: no compiled configuration fits, nothing launched
+bool launch_sweep(int p, int seg, const SweepArgs& a, cudaStream_t st);
+bool launch_sweep_p2(int seg, const SweepArgs& a, cudaStream_t st);  // sweep_p2.cu
+bool launch_sweep_p3(int seg, const SweepArgs& a, cudaStream_t st);  // sweep_p3.cu
+bool launch_sweep_p4(int seg, const SweepArgs& a, cudaStream_t st);  // sweep_p4.cu
+bool launch_sweep_p5(int seg, const SweepArgs& a, cudaStream_t st);  // sweep_p5.cu (scheme-1 layout at p = 4)
+// fused update + first sweep (fsweep_kernel.cuh); fuse: 1 Ampere update, 2 Faraday update (the
+// curl source, j^, s and dt in a.pro; every component carries its own axis and cidx).  Returns
+// false when no compiled configuration fits (shared memory, alignment); nothing launched then.
+bool launch_fsweep(int p, int seg, int fuse, const SweepArgs& a, cudaStream_t st);
+bool launch_fsweep_p2(int seg, int fuse, const SweepArgs& a, cudaStream_t st);
+bool launch_fsweep_p3(int seg, int fuse, const SweepArgs& a, cudaStream_t st);
+bool launch_fsweep_p4(int seg, int fuse, const SweepArgs& a, cudaStream_t st);
 void launch_update(int pro, const SweepArgs& a, cudaStream_t st);
 void launch_curl(int kind, const double* const src[3], const int sext[3][3], double* const dst[3],
                  const int dext[3][3], cudaStream_t st);

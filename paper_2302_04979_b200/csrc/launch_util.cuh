@@ -1,4 +1,4 @@
-// Launch helpers shared by the translation units (environment knobs, SM count, PDL launches).
+// Launch helpers shared by the translation units (SM count, per-device attribute flags, PDL launches).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -6,12 +6,11 @@
 #include <cstring>
 #include <utility>
 
+#include "tune.h"
+
 namespace sgm {
 
-inline int env_int(const char* name, int dflt) {
-  const char* s = getenv(name);
-  return s ? atoi(s) : dflt;
-}
+
 
 // Launch with programmatic stream serialization (PDL): the kernel may be scheduled while the
 // previous kernel in the stream drains; it calls griddepcontrol.wait before touching its inputs.
@@ -26,21 +25,35 @@ void launch_pdl(void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t 
   lc.stream = st;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = env_int("SGM_PDL", 1) ? 1 : 0;
+  at[0].val.programmaticStreamSerializationAllowed = tune_int("SGM_PDL", 1) ? 1 : 0;
   lc.attrs = at;
   lc.numAttrs = 1;
   cudaLaunchKernelEx(&lc, kernel, std::forward<Args>(args)...);
 }
 
+// SM count of the current device (cached per device ordinal)
 inline int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
+  static int n[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  if (!n[dev]) {
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev] = v > 0 ? v : 148;
   }
-  return n;
+  return n[dev];
+}
+
+// Once-per-device flags for cudaFuncSetAttribute (the attribute is per device): returns true the
+// first time it is called for (flag word, current device).
+inline bool first_on_device(unsigned long long& mask) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (mask & bit) return false;
+  mask |= bit;
+  return true;
 }
 
 

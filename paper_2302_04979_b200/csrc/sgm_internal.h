@@ -8,6 +8,7 @@
 #include <vector>
 
 #include "../../include/sgm.h"
+#include "tune.h"
 
 namespace sgm {
 
@@ -111,6 +112,8 @@ struct Plan {
   size_t mirror_bytes = 0;
   std::vector<double> tables_host;
   bool sticky_cuda_error = false;
+  unsigned opts = 0;                  // SGM_OPT_* schedule options (sgm_plan_set_options)
+  mutable int launch_fail = 0;             // a launcher found no compiled configuration (set while enqueuing)
   bool graph_enabled = true;          // SGM_GRAPH=0 disables the sgm_step graph cache
   // fork/join of independent sweep launches (reduced separable schedule): the second launch runs on
   // a plan-owned stream on its own share of the SMs; `fork_mu` serialises the enqueue of a fork/join
@@ -140,6 +143,7 @@ sgm_status interpolate_geometry(const int n_el[3], int p, const double* values, 
 sgm_status banded_lu_nopivot(const std::vector<double>& A, int L, int m, std::vector<double>& LU,
                              std::string& err);
 sgm_status build_tables(Plan& P, std::string& err);
+sgm_status set_spike_reach(Plan& P, std::string& err);
 int seg_for_line(int L);
 sgm_status build_geometry(Plan& P, std::string& err);
 void qp_coords(const Plan& P, double* xyz);

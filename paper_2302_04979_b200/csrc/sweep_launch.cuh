@@ -45,7 +45,7 @@ bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
   // x axis: a tile of whole lines is one contiguous range -> one bulk copy in and one out (TMA
   // engine), if the component bases are 16-byte aligned and the component has an even size.
   // (Strided tiles are many small row runs: measured slower on the bulk engine than cp.async.)
-  bool bulk = (MODE == 3) && env_int("SGM_BULK", 1) != 0;
+  bool bulk = (MODE == 3) && tune_int("SGM_BULK", 1) != 0;
   for (int c = 0; c < a.ncomp && bulk; ++c) {
     const SweepComp& C = a.comp[c];
     if ((reinterpret_cast<uintptr_t>(C.in) & 15) || (reinterpret_cast<uintptr_t>(C.out) & 15)) bulk = false;
@@ -53,7 +53,7 @@ bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
   }
   cfg.bulk = bulk ? 1 : 0;
   if (bulk) cfg.NP = 1;
-  else cfg.NP = env_int("SGM_NP", 4);
+  else cfg.NP = tune_int("SGM_NP", 4);
   if (cfg.NP < 1) cfg.NP = 1;
   if (cfg.NC + cfg.NP > 16) cfg.NP = 16 - cfg.NC;
   if (cfg.NP < 1) return false;
@@ -64,7 +64,7 @@ bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
     int bp_max = 0;
     for (int c = 0; c < a.ncomp; ++c) {
       sweep::CompGeom& g = cfg.g[c];
-      g.lbulk = (bulk && (g.L % 4) == 0 && env_int("SGM_LINE_BULK", 1)) ? 1 : 0;
+      g.lbulk = (bulk && (g.L % 4) == 0 && tune_int("SGM_LINE_BULK", 1)) ? 1 : 0;
       g.bpitch = g.lbulk ? g.L + 2 : g.L;
       bp_max = g.bpitch > bp_max ? g.bpitch : bp_max;
     }
@@ -79,23 +79,21 @@ bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
   cfg.slab = (cfg.slab + 1) & ~1;  // keep every slab 16-byte aligned
   cfg.ntabs = (a.tabs[1] != nullptr && a.tabs[1] != a.tabs[0]) ? 2 : 1;
   cfg.tab_dbl = a.tab_rows * RowLayout<P>::RS;
-  cfg.dbg = env_int("SGM_PIPE_DBG", 0);
-  cfg.reverse = env_int("SGM_SNAKE", 1) ? a.reverse : 0;
+  cfg.dbg = tune_int("SGM_PIPE_DBG", 0);
+  cfg.reverse = tune_int("SGM_SNAKE", 1) ? a.reverse : 0;
   constexpr int M = P - 1;
   const size_t smem = (size_t(cfg.ntabs) * cfg.tab_dbl + size_t(2) * cfg.slab + size_t(2) * cfg.NC * M * TW + 4) *
                       sizeof(double);
   if (smem > 227 * 1024) return false;
   const int NT = (cfg.NC + cfg.NP) * 32;
-  static int attr_done = 0;
-  if (!attr_done) {
+  static unsigned long long attr_done = 0;
+  if (first_on_device(attr_done))
     cudaFuncSetAttribute(sweep::sweep_kernel<P, HB, SEG, LPT, MODE, OPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          227 * 1024);
-    attr_done = 1;
-  }
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, sweep::sweep_kernel<P, HB, SEG, LPT, MODE, OPS>, NT, smem);
   if (per_sm < 1) per_sm = 1;
-  const int cap = env_int("SGM_CTAS_PER_SM", 0);
+  const int cap = tune_int("SGM_CTAS_PER_SM", 0);
   if (cap > 0 && cap < per_sm) per_sm = cap;
   long grid = long(per_sm) * sm_count();
   if (a.share_n > 0) grid = (grid * a.share_k + a.share_n / 2) / a.share_n;
@@ -107,41 +105,41 @@ bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
 }
 
 template <int P, int HB, int SEG, int MODE, int OPS>
-void launch_sweep_m(const SweepArgs& a, cudaStream_t st) {
+bool launch_sweep_m(const SweepArgs& a, cudaStream_t st) {
   // two lines per thread when the register budget allows (SEG <= 17) and the slabs fit
   if constexpr (SEG <= 17) {
-    if (env_int("SGM_LPT", 2) == 2 && launch_sweep_t<P, HB, SEG, 2, MODE, OPS>(a, st)) return;
+    if (tune_int("SGM_LPT", 2) == 2 && launch_sweep_t<P, HB, SEG, 2, MODE, OPS>(a, st)) return true;
   }
-  launch_sweep_t<P, HB, SEG, 1, MODE, OPS>(a, st);
+  return launch_sweep_t<P, HB, SEG, 1, MODE, OPS>(a, st);
 }
 
 template <int P, int SEG, int MODE>
-void launch_sweep_o(const SweepArgs& a, cudaStream_t st) {
+bool launch_sweep_o(const SweepArgs& a, cudaStream_t st) {
   // band half-width: P - 1 for the eps-side Grams and the pairing factors, P for the mu-side Gram
   if (a.band && a.solve) {
-    if (a.band_hw >= P) launch_sweep_m<P, P, SEG, MODE, 3>(a, st);
-    else if (P >= 3 && a.band_hw <= P - 2) launch_sweep_m<P, (P >= 3 ? P - 2 : 1), SEG, MODE, 3>(a, st);  // eps Gamma_C^{p-2}
-    else launch_sweep_m<P, P - 1, SEG, MODE, 3>(a, st);
+    if (a.band_hw >= P) return launch_sweep_m<P, P, SEG, MODE, 3>(a, st);
+    if (P >= 3 && a.band_hw <= P - 2) return launch_sweep_m<P, (P >= 3 ? P - 2 : 1), SEG, MODE, 3>(a, st);  // eps Gamma_C^{p-2}
+    return launch_sweep_m<P, P - 1, SEG, MODE, 3>(a, st);
   } else if (a.solve) {
-    launch_sweep_m<P, P - 1, SEG, MODE, 2>(a, st);
-  } else {
-    if (a.band_hw >= P) launch_sweep_m<P, P, SEG, MODE, 1>(a, st);
-    else launch_sweep_m<P, P - 1, SEG, MODE, 1>(a, st);
+    return launch_sweep_m<P, P - 1, SEG, MODE, 2>(a, st);
   }
+  if (a.band_hw >= P) return launch_sweep_m<P, P, SEG, MODE, 1>(a, st);
+  return launch_sweep_m<P, P - 1, SEG, MODE, 1>(a, st);
 }
 
 template <int P, int SEG>
-void launch_sweep_s(const SweepArgs& a, cudaStream_t st) {
-  if (a.axis == 0) launch_sweep_o<P, SEG, 3>(a, st);
-  else launch_sweep_o<P, SEG, 0>(a, st);
+bool launch_sweep_s(const SweepArgs& a, cudaStream_t st) {
+  if (a.axis == 0) return launch_sweep_o<P, SEG, 3>(a, st);
+  return launch_sweep_o<P, SEG, 0>(a, st);
 }
 
+// false: no compiled configuration fits (shared memory); nothing was launched
 template <int P>
-void launch_sweep_p(int seg, const SweepArgs& a, cudaStream_t st) {
+bool launch_sweep_p(int seg, const SweepArgs& a, cudaStream_t st) {
   switch (seg) {
-    case 12: launch_sweep_s<P, 12>(a, st); break;
-    case 17: launch_sweep_s<P, 17>(a, st); break;
-    default: launch_sweep_s<P, 28>(a, st); break;
+    case 12: return launch_sweep_s<P, 12>(a, st);
+    case 17: return launch_sweep_s<P, 17>(a, st);
+    default: return launch_sweep_s<P, 28>(a, st);
   }
 }
 

@@ -1,6 +1,10 @@
 // Line-sweep launchers for degree p = 4 (see sweep_launch.cuh).
 #include "sweep_launch.cuh"
+#include "fsweep_launch.cuh"
 
 namespace sgm {
-void launch_sweep_p4(int seg, const SweepArgs& a, cudaStream_t st) { sweeplaunch::launch_sweep_p<4>(seg, a, st); }
+bool launch_sweep_p4(int seg, const SweepArgs& a, cudaStream_t st) { return sweeplaunch::launch_sweep_p<4>(seg, a, st); }
+bool launch_fsweep_p4(int seg, int fuse, const SweepArgs& a, cudaStream_t st) {
+  return fsweeplaunch::launch_p<4>(seg, fuse, a, st);
+}
 }  // namespace sgm

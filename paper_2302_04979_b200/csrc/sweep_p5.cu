@@ -3,5 +3,5 @@
 #include "sweep_launch.cuh"
 
 namespace sgm {
-void launch_sweep_p5(int seg, const SweepArgs& a, cudaStream_t st) { sweeplaunch::launch_sweep_p<5>(seg, a, st); }
+bool launch_sweep_p5(int seg, const SweepArgs& a, cudaStream_t st) { return sweeplaunch::launch_sweep_p<5>(seg, a, st); }
 }  // namespace sgm

@@ -4,6 +4,7 @@ codes) agrees with the oracle.  No kernel is launched here."""
 import ctypes
 import os
 import re
+import sys
 
 import numpy as np
 import pytest
@@ -125,12 +126,55 @@ def test_plain_c_consumer(tmp_path):
 
 
 @pytest.mark.parametrize("p,n", [(2, 5), (3, (9, 7, 6)), (4, 6), (3, 128)])
-def test_reduced_schedule_identities_hold(p, n, monkeypatch):
+def test_reduced_schedule_identities_hold(p, n):
     """The plan verifies Hat M = Gamma_B^{p-1} diag(s) and Gamma_C^{p-1} = diag(s) Gamma_B^{p-1} diag(s)
-    on every axis (host_setup.cpp) and enables the reduced separable schedule; SGM_NODIAG=1 disables it."""
-    assert S.Plan(n, p, device=-1).reduced_schedule()
-    monkeypatch.setenv("SGM_NODIAG", "1")
-    assert not S.Plan(n, p, device=-1).reduced_schedule()
+    on every axis (host_setup.cpp) and enables the reduced separable schedule (fused direct sweeps by
+    default); SGM_OPT_FULL_SCHEDULE selects the three-axis schedule, SGM_OPT_FUSED the fused update."""
+    pl = S.Plan(n, p, device=-1)
+    assert pl.reduced_schedule() and pl.schedule_mode() in (1, 2)
+    pl.set_options(S.OPT_FULL_SCHEDULE)
+    assert pl.options() == S.OPT_FULL_SCHEDULE and not pl.reduced_schedule()
+    pl.set_options(S.OPT_FUSED)
+    assert pl.schedule_mode() == 3
+    pl.set_options(S.OPT_SERIAL)
+    assert pl.schedule_mode() == 1
+    with pytest.raises(S.SgmError):
+        pl.set_options(0x100)
+
+
+def test_kernels_per_step_fused_schedule():
+    """The default step launches 7 kernels for separable stars on a cube (update, three eps sweep
+    launches, update, two mu sweep launches); with the fused update (SGM_OPT_FUSED) 4 (the Ampere
+    update fused into the first eps launch, the two concurrent second eps launches, the Faraday update
+    fused into the mu launch); a fused launch carries at most two distinct line-operator tables, so
+    three different element counts split the mu launch in two."""
+    pl = S.Plan(32, 3, device=-1)
+    assert pl.kernels_per_step() == 7
+    pl.set_options(S.OPT_FUSED)
+    assert pl.kernels_per_step() == 4
+    pl.set_options(S.OPT_FUSED | S.OPT_FULL_SCHEDULE)
+    assert pl.kernels_per_step() == 6
+    for n, k in (((20, 21, 20), 4), ((20, 21, 22), 5)):
+        pl = S.Plan(n, 3, device=-1)
+        pl.set_options(S.OPT_FUSED)
+        assert pl.kernels_per_step() == k
+
+
+def test_product_library_ignores_tuning_environment():
+    """The tuning knobs (SGM_PIPE_DBG, SGM_NODIAG, SGM_FORK, ... of the round-1 build) are compiled
+    only into a -DSGM_TUNING build: the product library contains none of their names, so no
+    environment variable can change its schedule or skip work; and a plan created with such
+    variables set is the default plan."""
+    import os
+    import subprocess
+    out = subprocess.run(["strings", S.LIB_PATH], capture_output=True, text=True, check=True).stdout
+    knobs = sorted({w for w in out.splitlines() if re.fullmatch(r"SGM_[A-Z0-9_]+", w.strip())})
+    assert knobs == [], knobs
+    env = dict(os.environ, SGM_NODIAG="1", SGM_PIPE_DBG="15", SGM_FORK="0", SGM_SPIKE_FULL="1", SGM_SEG="28")
+    code = ("import paper_2302_04979_b200 as S; pl = S.Plan(32, 3, device=-1); "
+            "print(pl.schedule_mode(), pl.kernels_per_step(), pl.options())")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, cwd=ROOT)
+    assert r.stdout.split() == ["2", "7", "0"], r.stdout + r.stderr
 
 
 def test_rational_map_host_geometry():

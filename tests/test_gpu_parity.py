@@ -390,14 +390,19 @@ def test_step_composed_parity(case):
             assert rel(host(x), y) < (1e-11 if k == 1 else 1e-10), (case, k)
 
 
-@pytest.mark.parametrize("nodiag", ["0", "1"])
+SCHEDULES = [0, S.OPT_FULL_SCHEDULE, S.OPT_FUSED, S.OPT_FUSED | S.OPT_FULL_SCHEDULE, S.OPT_SERIAL,
+             S.OPT_EXACT_SPIKE, S.OPT_NO_GRAPH, S.OPT_FUSED | S.OPT_EXACT_SPIKE]
+
+
+@pytest.mark.parametrize("opts", SCHEDULES)
 @pytest.mark.parametrize("p,n", [(2, (5, 9, 7)), (3, 11), (4, (6, 5, 8))])
-def test_reduced_and_full_schedules(p, n, nodiag, monkeypatch):
-    """Both separable schedules (reduced: diagonal factors as per-line scalings; full: every axis
-    swept) against the oracle: Hodge stars and 30 steps."""
-    monkeypatch.setenv("SGM_NODIAG", nodiag)
+def test_reduced_and_full_schedules(p, n, opts):
+    """Every schedule option (separate or fused update; reduced: diagonal factors
+    as per-line scalings / full: every axis swept; exact or truncated SPIKE; serial; no graph) against
+    the oracle: Hodge stars and 30 steps."""
     pl = S.Plan(n, p)
-    assert pl.reduced_schedule() == (nodiag == "0")
+    pl.set_options(opts)
+    assert pl.reduced_schedule() == (not opts & S.OPT_FULL_SCHEDULE)
     tb = TierB(p, n)
     g = np.random.default_rng(41)
     x = g.standard_normal(tb.N_e)
