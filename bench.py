@@ -79,8 +79,10 @@ def _workload(args):
     if args.config == "c2":
         return 3, 32, "C2 full step p=3 n_el=32^3 identity eps=mu=1", None, None, False
     if args.config == "c3":
-        return 3, 48, "C3 full step p=3 n_el=48^3 curved map, eps in {1,4} inclusion, Gaussian-pulse J", "c3", "c3", True
-    return 4, 96, "C4 full step p=4 n_el=96^3 identity, eps=1+0.5 sin(2pi x)cos(2pi y)", None, "c4", False
+        return (3, 48, "C3 full step p=3 n_el=48^3 curved map, eps in {1,4} inclusion, projected Gaussian J "
+                "with Gaussian pulse s(t), zero initial fields", "c3", "c3", True)
+    return (4, 96, "C4 full step p=4 n_el=96^3 identity, eps=1+0.5 sin(2pi x)cos(2pi y), smooth random E",
+            None, "c4", False)
 
 
 def peaks():
@@ -154,12 +156,35 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
+def device_cfl(pl, S, torch, dev, seed, n_iter=300):
+    """dt_max of the plan's own scheme-2 operator by the library's power iteration (sgm_cfl; SURVEY
+    8(d): start vector rng(100 + k), 300 iterations, Rayleigh quotient; reading Z15)."""
+    import synth
+    x = torch.from_numpy(synth.rng(seed).standard_normal(pl.N_e)).to(dev)
+    e = torch.empty(pl.N_e, dtype=torch.float64, device=dev)
+    b = torch.empty(pl.N_h, dtype=torch.float64, device=dev)
+    h = torch.empty_like(b)
+    out = torch.zeros(2, dtype=torch.float64, device=dev)
+    pl.cfl(x, e, b, h, out, n_iter)
+    return float(out[1].item())
+
+
 def build_inputs(args, torch, S, dev):
+    """The configured workloads (BASELINE.json configs) built with
+    the library and synth only (the bench never executes the oracle outside its CPU legs):
+      C5 / C2: d0, b^{1/2} ~ N(0,1) (rng(5)), e0, h^{1/2} by the discrete Hodge stars;
+      C3: the curved map (library Greville interpolation), eps in {1, 4} inclusion, ZERO initial
+          fields, j^ = D~1 a^ with a^ the oracle-written projected Gaussian (tests/golden/c3_a_hat.npz,
+          scripts/make_c3_source.py), s(t) = exp(-((t - 0.15)/0.05)^2), dt = 0.5 dt_max (sgm_cfl);
+      C4: eps = 1 + 0.5 sin(2 pi x) cos(2 pi y), e0 = the smoothed rng(4) field (synth.smooth_fields),
+          d0 = K1 e0 (the parity tests use d0 = M~2^{-1} K1 e0 by PCG: same smoothness class, one mass
+          solve fewer, throughput unaffected), e0 = K1^{-1} M~2 d0, b^{1/2} = -(dt/2) D1 e0,
+          h^{1/2} = K~1^{-1} M2 b^{1/2}; dt = 0.5 dt_max (sgm_cfl)."""
+    import synth
     p, n, desc, geo, mat, src = workload(args)
     ctrl = None
     if geo == "c3":
         # the closed-form C3 map interpolated at the Greville points by the library (reading Z18)
-        import synth
         ctrl = S.interpolate_geometry(n, p, synth.c3_map)
     pl = S.Plan(n, p, geom_ctrl=ctrl, device=dev.index or 0)
     if getattr(args, "scheme", 2) == 1:
@@ -168,27 +193,42 @@ def build_inputs(args, torch, S, dev):
     if mat is not None:
         X = pl.qp_coords()
         if mat == "c3":
-            import synth
             c_eps, _ = synth.c3_centres()
             eps = np.where(np.linalg.norm(X - c_eps, axis=1) < 0.25, 4.0, 1.0)
         else:
             eps = 1 + 0.5 * np.sin(2 * np.pi * X[:, 0]) * np.cos(2 * np.pi * X[:, 1])
         pl.set_material(S.EPS, eps)
         del X
-    import synth
-    d0, b0 = synth.normal(5, pl.N_e, pl.N_h)
-    d = torch.from_numpy(d0).to(dev)
-    b = torch.from_numpy(b0).to(dev)
-    e = torch.empty_like(d)
-    h = torch.empty_like(b)
-    pl.hodge_star(S.MASS_EPS, d, e)
-    pl.hodge_star(S.MASS_MU, b, h)
     jhat = None
-    if src:
-        a = torch.from_numpy(synth.normal(33, pl.N_h)[0]).to(dev)
-        jhat = torch.empty_like(d)
-        pl.curl(S.CURL_DUAL, a, jhat)          # j = D~1 a: divergence free
-    dt = 0.5 * CFL_N[p] / n * (0.5 if geo or mat else 1.0)
+    if args.config == "c3":
+        dt = 0.5 * device_cfl(pl, S, torch, dev, 103)
+        a = np.load(os.path.join(ROOT, "tests", "golden", "c3_a_hat.npz"))["a_hat"]
+        jhat = torch.empty(pl.N_e, dtype=torch.float64, device=dev)
+        pl.curl(S.CURL_DUAL, torch.from_numpy(a).to(dev), jhat)   # j = D~1 a: divergence free
+        z = [torch.zeros(k, dtype=torch.float64, device=dev) for k in (pl.N_e, pl.N_e, pl.N_h, pl.N_h)]
+        d, e, b, h = z
+    elif args.config == "c4":
+        dt = 0.5 * device_cfl(pl, S, torch, dev, 104)
+        shapes = [tuple(pl.shape(S.FORM_E, c)[::-1]) for c in range(3)]
+        e0 = torch.from_numpy(np.concatenate([f.ravel() for f in synth.smooth_fields(4, shapes)])).to(dev)
+        d = torch.empty_like(e0)
+        pl.pairing_apply(S.K1, e0, d)
+        e = torch.empty_like(d)
+        pl.hodge_star(S.MASS_EPS, d, e)
+        b = torch.empty(pl.N_h, dtype=torch.float64, device=dev)
+        pl.curl(S.CURL_PRIMAL, e, b)
+        b.mul_(-0.5 * dt)
+        h = torch.empty_like(b)
+        pl.hodge_star(S.MASS_MU, b, h)
+    else:
+        d0, b0 = synth.normal(5, pl.N_e, pl.N_h)
+        d = torch.from_numpy(d0).to(dev)
+        b = torch.from_numpy(b0).to(dev)
+        e = torch.empty_like(d)
+        h = torch.empty_like(b)
+        pl.hodge_star(S.MASS_EPS, d, e)
+        pl.hodge_star(S.MASS_MU, b, h)
+        dt = 0.5 * CFL_N[p] / n
     torch.cuda.synchronize()
     return pl, (d, e, b, h), jhat, dt, desc, p, n
 
@@ -249,35 +289,72 @@ def hodge_flops(pl, S, p, n):
     return out
 
 
-def fp64_peak_tflops(sm_mhz):
-    """148 SMs x 64 DFMA lanes per SM per cycle (ncu: sm__sass_thread_inst_executed_op_dfma_pred_on
-    peak_sustained = 64) x 2 FLOPs x clock."""
-    return 148 * 64 * 2 * sm_mhz * 1e6 / 1e12
+def fp64_peak():
+    """The measured fp64 peak (profiles/r2_fp64_peak.json, scripts/fp64_peak.py: the larger of a
+    DFMA-chain kernel and cuBLAS DGEMM), else the derived 148 SMs x 64 DFMA lanes/SM/cycle x 2 FLOPs
+    x max clock."""
+    path = os.path.join(ROOT, "profiles", "r2_fp64_peak.json")
+    try:
+        d = json.load(open(path))
+        v = max(float(d["dfma"]["tflops"]), float(d["dgemm_tflops"]))
+        return v, "measured (profiles/r2_fp64_peak.json: max of a DFMA-chain kernel and cuBLAS DGEMM 8192^3)"
+    except Exception:
+        return 148 * 64 * 2 * peaks_sm_mhz() * 1e6 / 1e12, "derived: 148 SMs x 64 DFMA/SM/cycle x 2 x max SM clock"
+
+
+def oracle_workload(args):
+    """The CPU legs' workload (the oracle's tier B, as it stands): (tier B, state, dt, j^, amplitude
+    function k -> s_k, description).  C3 / C4 follow the same recipes as the GPU inputs of
+    build_inputs (C3: zero fields, projected Gaussian source, pulse; C4: smooth e0 with d0 = K1 e0)."""
+    import synth
+    from oracle import forms
+    from oracle import workloads as Wk
+    from oracle.structured import TierB, TierB1, curl_primal
+    p, n, desc, geo, mat, src = workload(args)
+    dts = {}
+    gpath = os.path.join(ROOT, "tests", "golden", "workload_dt.json")
+    if os.path.exists(gpath):
+        dts = json.load(open(gpath))
+    if args.config == "c3":
+        ctrl, eps, _ = Wk.c3_setup(p, n)
+        tb = TierB(p, n, ctrl=ctrl, inv_eps=1.0 / eps, inv_mu=1.0)
+        dt = dts.get("c3", {}).get("dt", 0.25 * CFL_N[p] / n)
+        jhat = Wk.c3_source(p, n, ctrl)
+        st = tuple(np.zeros(k) for k in (tb.N_e, tb.N_e, tb.N_h, tb.N_h))
+        return tb, st, dt, jhat, (lambda k: float(synth.pulse((k + 0.5) * dt))), desc
+    if args.config == "c4":
+        eps, tb = Wk.c4_setup(p, n)
+        dt = dts.get("c4", {}).get("dt", 0.25 * CFL_N[p] / n)
+        shapes = [tuple(s[::-1]) for s in tb.sh_e]
+        e0 = forms.join(synth.smooth_fields(4, shapes))
+        d0 = forms.join(tb.apply_K1(tb.split_e(e0)))
+        e0 = tb.hodge_eps(d0)
+        bh = -0.5 * dt * forms.join(curl_primal(tb.split_e(e0)))
+        return tb, (d0, e0, bh, tb.hodge_mu(bh)), dt, None, (lambda k: 1.0), desc
+    tb = TierB(p, n) if getattr(args, "scheme", 2) == 2 else TierB1(p, n)
+    d0, b0 = synth.normal(5, tb.N_e, tb.N_h)
+    st = (d0, tb.hodge_eps(d0), b0, tb.hodge_mu(b0))
+    return tb, st, 0.5 * CFL_N[p] / n, None, (lambda k: 1.0), desc
+
+
+def _threads():
+    import threadpoolctl
+    return max([i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()] + [1])
 
 
 def cpu_baseline(args, budget_s=10.0):
     """The oracle (tier B, as it stands) on this host: a bounded sample of the same workload."""
-    import threadpoolctl
-    from oracle.structured import TierB, TierB1
-    import synth
-    p, n, desc, geo, mat, src = workload(args)
-    if geo or mat:
-        return None
-    tb = TierB(p, n) if getattr(args, "scheme", 2) == 2 else TierB1(p, n)
-    d0, b0 = synth.normal(5, tb.N_e, tb.N_h)
-    st = (d0, tb.hodge_eps(d0), b0, tb.hodge_mu(b0))
-    dt = 0.5 * CFL_N[p] / n
-    st = tb.step(*st, dt)  # warm-up
+    tb, st, dt, jhat, amp, desc = oracle_workload(args)
+    st = tb.step(*st, dt, jhat, amp(0))  # warm-up
     t0 = time.perf_counter()
     k = 0
     while True:
-        st = tb.step(*st, dt)
+        st = tb.step(*st, dt, jhat, amp(k + 1))
         k += 1
         if time.perf_counter() - t0 > budget_s and k >= 2:
             break
     t = time.perf_counter() - t0
-    threads = max([i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()] + [1])
-    return {"value": (tb.N_e + tb.N_h) * k / t, "unit": UNIT, "cores": int(threads), "kind": "oracle",
+    return {"value": (tb.N_e + tb.N_h) * k / t, "unit": UNIT, "cores": int(_threads()), "kind": "oracle",
             "sample": f"{k} tier-B oracle steps (setup excluded) of {desc}, {t:.1f} s",
             "host_cpus": os.cpu_count()}
 
@@ -286,35 +363,25 @@ def run_reference(args, rank, world):
     """--impl reference: the CPU oracle timed on the host cores (rank 0 only)."""
     if rank != 0:
         return
-    p, n, desc, geo, mat, src = workload(args)
-    from oracle.structured import TierB, TierB1
-    import synth
-    import threadpoolctl
-    if geo or mat:
-        print(json.dumps({"impl": "reference", "unavailable": "reference arm implemented for separable configs"}))
-        return
-    tb = TierB(p, n) if getattr(args, "scheme", 2) == 2 else TierB1(p, n)
-    d0, b0 = synth.normal(5, tb.N_e, tb.N_h)
-    st = (d0, tb.hodge_eps(d0), b0, tb.hodge_mu(b0))
-    dt = 0.5 * CFL_N[p] / n
-    for _ in range(max(1, min(args.warmup, 2))):
-        st = tb.step(*st, dt)
+    tb, st, dt, jhat, amp, desc = oracle_workload(args)
+    p, n = tb.p, tb.n[0]
+    for i in range(max(1, min(args.warmup, 2))):
+        st = tb.step(*st, dt, jhat, amp(i))
     budget = 120.0
     t0 = time.perf_counter()
     k = 0
     while k < args.steps:
-        st = tb.step(*st, dt)
+        st = tb.step(*st, dt, jhat, amp(k))
         k += 1
         if time.perf_counter() - t0 > budget:
             break
     t = time.perf_counter() - t0
     v = (tb.N_e + tb.N_h) * k / t
-    threads = max([i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()] + [1])
     out = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": k, "warmup": args.warmup,
            "ms_per_step": 1e3 * t / k, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
            "dtype": "f64", "data": "synthetic", "impl": "reference",
            "config": {"workload": desc, "p": p, "n_el": n, "dofs_per_step": tb.N_e + tb.N_h},
-           "cpu_baseline": {"value": v, "unit": UNIT, "cores": int(threads), "kind": "oracle",
+           "cpu_baseline": {"value": v, "unit": UNIT, "cores": int(_threads()), "kind": "oracle",
                             "sample": f"{k} of {args.steps} requested tier-B oracle steps (120 s cap), setup excluded"},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
@@ -343,8 +410,8 @@ def main():
     K, W = args.steps, max(3, args.warmup)
     jamp = None
     if jhat is not None:
-        tt = (np.arange(K + W) + 0.5) * dt
-        jamp = torch.from_numpy(np.exp(-((tt - 0.15) / 0.05) ** 2)).to(dev)
+        import synth
+        jamp = torch.from_numpy(synth.pulse((np.arange(K + W) + 0.5) * dt)).to(dev)   # s(t_{k+1/2})
     stream = torch.cuda.Stream()          # a dedicated stream (sgm_step graph-captures its launches)
     torch.cuda.set_stream(stream)
 
@@ -379,7 +446,10 @@ def main():
     ms = max_over_ranks(ms, dist, dev)
     value = aggregate_value(dofs, K, ms, world)
 
-    # dominant kernel roofline (profiled pass of the same K steps, events on the launching stream)
+    # ---- rooflines per kernel FUNCTION (profiled pass of the same K steps, CUDA events on the
+    # launching stream around every launch).  Sweep launches of all classes are one function
+    # (sweep_kernel / fsweep_kernel); concurrent launches (a fork/join pair) count once, by the longer
+    # side, so the function's time is the wall time of its phases in the step.
     peak, peak_src = peaks()
     lb = launch_bytes(pl, S, N_e, N_h, jhat is not None)
     step_bytes = sum(b for _, b in lb)
@@ -387,15 +457,51 @@ def main():
     for cls, b in lb:
         per_cls.setdefault(cls, []).append(b)
     kernels = {}
-    tot_ms = sum(v[0] for v in prof.values())
     for cls, (kms, cnt) in prof.items():
         per = kms / cnt
-        kernels[cls] = {"launches": cnt, "ms_per_launch": per, "share": kms / tot_ms}
+        kernels[cls] = {"launches": cnt, "ms_per_launch": per}
         if cls in per_cls:
             by = sum(per_cls[cls]) / len(per_cls[cls])
             kernels[cls]["algo_bytes"] = by
             kernels[cls]["gbs"] = by / (per * 1e-3) / 1e9
-    dom = max(prof.items(), key=lambda kv: kv[1][0])[0]
+    mode = pl.schedule_mode()
+    pairs = [("eps_y", "eps_x"), ("mu_z", "mu_x")] if mode in (2, 3) else []
+
+    def phase_ms(classes):
+        """per-step wall milliseconds of these classes (concurrent pairs by their longer side)"""
+        t, seen = 0.0, set()
+        for a, b in pairs:
+            if a in classes and b in classes and a in prof and b in prof:
+                t += max(prof[a][0], prof[b][0]) / K
+                seen |= {a, b}
+        return t + sum(prof[c][0] / K for c in classes if c in prof and c not in seen)
+
+    funcs = {"sweep": [c for c in prof if c.endswith(("_z", "_y", "_x")) or c.startswith("fused_")],
+             "update": [c for c in prof if c == "update"],
+             "hodge_general": [c for c in prof if c == "hodge_general"]}
+    step_phase = phase_ms(list(prof))
+    func = {}
+    for name, cls in funcs.items():
+        if not cls:
+            continue
+        t = phase_ms(cls)
+        by = sum(sum(per_cls.get(c, [])) for c in cls) if name != "hodge_general" else None  # one step
+        rec = {"classes": cls, "ms_per_step": t, "share": t / step_phase}
+        if by:
+            rec.update({"algo_bytes_per_step": by, "gbs": by / (t * 1e-3) / 1e9, "frac": by / (t * 1e-3) / 1e9 / peak})
+        func[name] = rec
+    hf = [f for f in hodge_flops(pl, S, p, n) if f]
+    fpk, fpk_src = fp64_peak()
+    if hf and "hodge_general" in kernels:
+        kernels["hodge_general"]["algo_flops"] = sum(hf) / len(hf)
+        kernels["hodge_general"]["tflops"] = sum(hf) / len(hf) / (kernels["hodge_general"]["ms_per_launch"] * 1e-3) / 1e12
+        wq = pl.qp_count() * (6 if pl.geom else 1) * 8
+        hb = [b for c, b in lb if c == "hodge_general"]
+        func["hodge_general"].update({"tflops": kernels["hodge_general"]["tflops"], "frac_fp64": kernels["hodge_general"]["tflops"] / fpk,
+                                      "gbs": (sum(hb) / len(hb)) / (kernels["hodge_general"]["ms_per_launch"] * 1e-3) / 1e9,
+                                      "weights_bytes": wq})
+        func["hodge_general"]["frac"] = func["hodge_general"]["gbs"] / peak
+    dom = max(func.items(), key=lambda kv: kv[1]["ms_per_step"])[0]
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
@@ -403,28 +509,45 @@ def main():
             traffic = json.load(open(tfile)).get(f"{args.config}_p{p}_n{n}", {}).get(dom)
         except Exception:
             traffic = None
-    achieved = kernels[dom].get("gbs")
-    hf = [f for f in hodge_flops(pl, S, p, n) if f]
-    if hf and "hodge_general" in kernels:
-        kernels["hodge_general"]["algo_flops"] = sum(hf) / len(hf)
-        kernels["hodge_general"]["tflops"] = sum(hf) / len(hf) / (kernels["hodge_general"]["ms_per_launch"] * 1e-3) / 1e12
-    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-            "frac": (achieved / peak) if achieved else None, "traffic": traffic, "peak_source": peak_src,
-            "algo_bytes_per_launch": kernels[dom].get("algo_bytes"),
-            "ms_per_launch": kernels[dom]["ms_per_launch"],
-            "step_algo_bytes": step_bytes, "step_gbs": step_bytes / (ms / K * 1e-3) / 1e9,
-            "step_frac": step_bytes / (ms / K * 1e-3) / 1e9 / peak,
-            "note": "dominant kernel = largest share of the event-profiled pass (a second pass of the same "
-                    "K steps, CUDA events on the launching stream around every launch); step_* = the "
-                    "unprofiled timed pass against the whole step's algorithmic bytes"}
-    if dom == "hodge_general" and "tflops" in kernels[dom]:
+    D = func[dom]
+    t_step = ms / K * 1e-3
+    roof = {"bound": "hbm", "kernel": dom, "achieved": D.get("gbs"), "peak": peak, "unit": "GB/s",
+            "frac": D.get("frac"), "traffic": traffic, "peak_source": peak_src,
+            "algo_bytes_per_step": D.get("algo_bytes_per_step"), "ms_per_step_in_kernel": D["ms_per_step"],
+            "share_of_step": D["share"],
+            "step_algo_bytes": step_bytes, "step_gbs": step_bytes / t_step / 1e9,
+            "step_frac": step_bytes / t_step / 1e9 / peak,
+            "bytes_per_dof_update": step_bytes / dofs,
+            "useful_bytes_frac": 16.0 * dofs / t_step / 1e9 / peak,
+            "functions": func,
+            "note": "dominant = the kernel function (sweeps of every class / update / general Hodge) with the "
+                    "largest wall time per step in the event-profiled pass (concurrent launches counted once); "
+                    "achieved = its algorithmic bytes (DESIGN.md section 6) / that time; step_* = the unprofiled "
+                    "timed pass against the step's algorithmic bytes; useful_bytes_frac = the algorithmic "
+                    "minimum 16 B per DOF-update (read and write d and b once, SURVEY 8(d)) at the measured "
+                    "step time, over the peak"}
+    if dom == "hodge_general" and "tflops" in D:
         # the general Hodge is bound by fp64 arithmetic issue, not HBM: report it against fp64 peak
-        fpk = fp64_peak_tflops(peaks_sm_mhz())
-        roof.update({"bound": "alu", "achieved": kernels[dom]["tflops"], "peak": fpk, "unit": "TFLOP/s",
-                     "frac": kernels[dom]["tflops"] / fpk, "algo_flops_per_launch": kernels[dom]["algo_flops"],
-                     "peak_source": "derived: 148 SMs x 64 DFMA/SM/cycle x 2 x max SM clock (DESIGN.md section 6)",
-                     "hbm_view": {"achieved": achieved, "peak": peak, "unit": "GB/s",
-                                  "frac": (achieved / peak) if achieved else None}})
+        roof.update({"bound": "alu", "achieved": D["tflops"], "peak": fpk, "unit": "TFLOP/s",
+                     "frac": D["frac_fp64"], "algo_flops_per_launch": kernels["hodge_general"]["algo_flops"],
+                     "peak_source": fpk_src,
+                     "hbm_view": {"achieved": D["gbs"], "peak": peak, "unit": "GB/s", "frac": D["frac"]}})
+
+    # the structure-faithful three-axis schedule (every Kronecker factor swept) and the
+    # fused-update schedule, timed the same way on the same state (second and third numbers)
+    variants = {}
+    if pl.separable(S.MASS_EPS) and pl.separable(S.MASS_MU) and not getattr(args, "opts", 0):
+        for name, o in (("full_schedule", S.OPT_FULL_SCHEDULE), ("fused_update", S.OPT_FUSED)):
+            pl.set_options(o)
+            steps(0, W)
+            torch.cuda.synchronize()
+            vms, _ = timed(False)
+            vms = max_over_ranks(vms, dist, dev)
+            variants[name] = {"options": o, "ms_per_step": vms / K, "value": aggregate_value(dofs, K, vms, world),
+                              "kernels_per_step": pl.kernels_per_step(),
+                              "useful_bytes_frac": 16.0 * dofs / (vms / K * 1e-3) / 1e9 / peak}
+        pl.set_options(0)
+    env = {k: v for k, v in os.environ.items() if k.startswith("SGM_")}
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
            "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
@@ -433,7 +556,9 @@ def main():
                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
                       "l2": f"no flush: working set {(2 * N_e + 2 * N_h + max(N_e, N_h)) * 8 / 1e6:.0f} MB "
                             f"(state + workspace) vs 126 MB L2"},
-           "roofline": roof, "kernels": kernels,
+           "roofline": roof, "kernels": kernels, "schedule_variants": variants,
+           "schedule": {"mode": mode, "options": getattr(args, "opts", 0), "kernels_per_step": pl.kernels_per_step(),
+                        "env_SGM": env, "dt": dt},
            "gpu_launches": pl.kernels_per_step() * K,
            "clocks": clk.summary()}
 

@@ -306,6 +306,108 @@ def _ops(tb):
 
 
 # ------------------------------------------------------------------------------------------
+# BASELINE.json configs[2] (C3) and configs[3] (C4), as SURVEY 8(d) and readings Z16/Z28 define them
+# ------------------------------------------------------------------------------------------
+
+C3_SIGMA = 0.05
+
+
+def c3_setup(p=3, n=48):
+    """C3: the map x + 0.1 sin(pi x) sin(pi y) sin(pi z) (1,1,1) interpolated in S_p^3 (reading
+    Z18), eps in {1, 4} with the sphere of radius 0.25 at c_eps = rng(3).uniform(.25, .75, 3)
+    point-sampled at the physical quadrature points (reading Z17), mu = 1.
+    Returns (ctrl, eps at the quadrature points (element-major), physical points [nqp, 3])."""
+    from .assemble import Quad, physical_qp
+    ctrl = interpolate_map(p, n, c3_map)
+    X = physical_qp(Quad(p, forms._n3(n)), ctrl).reshape(-1, 3)
+    c_eps, _ = synth.c3_centres()
+    eps = np.where(np.linalg.norm(X - c_eps, axis=1) < 0.25, 4.0, 1.0)
+    return ctrl, eps, X
+
+
+def c3_source(p, n, ctrl):
+    """C3 source (reading Z16): j^ = D~1 a^ with a^ the unweighted parametric L2 projection onto
+    X~1 of A = z-hat exp(-|F(x^) - c_J|^2 / (2 * 0.05^2)) sampled at the physical quadrature points
+    (reading Z28), c_J the second rng(3) draw.  Divergence free by D~2 D~1 = 0."""
+    _, c_J = synth.c3_centres()
+    Xg = physical_points(p, n, ctrl)
+    a = project_dual1(p, n, synth.gaussian_z(Xg, c_J, C3_SIGMA))
+    tb_n = forms._n3(n)
+    return forms.join(curl_dual(forms.split(a, "dual", 1, p, tb_n)))
+
+
+def c3_amplitudes(dt, n_steps, k0=0):
+    """s(t_{k+1/2}) = exp(-((t - 0.15)/0.05)^2) at t = (k + 1/2) dt, k = k0 .. k0 + n_steps - 1."""
+    return synth.pulse((np.arange(k0, k0 + n_steps) + 0.5) * dt)
+
+
+def c4_eps(X):
+    """C4: eps = 1 + 0.5 sin(2 pi x) cos(2 pi y) at physical points X[..., 3]."""
+    return 1.0 + 0.5 * np.sin(2 * np.pi * X[..., 0]) * np.cos(2 * np.pi * X[..., 1])
+
+
+def pcg_mass_eps(tb, rhs, tol=1e-14, maxit=500):
+    """Solve M~2_{1/eps} d = rhs (tier B, general mass) by preconditioned conjugate gradients with
+    the Kronecker preconditioner: the separable mass of the mean 1/eps, inverted mode by mode
+    ("d0 by tier-B PCG (Kronecker preconditioner, rel. residual 1e-14)")."""
+    from .structured import kron3
+    gbar = float(np.mean(tb.inv_eps))
+    Binv = [np.linalg.inv(G) for G in tb.GamB1]
+    Cinv = [np.linalg.inv(G) for G in tb.GamC2]
+
+    def A(x):
+        return forms.join(tb.mass_eps(tb.split_e(x)))
+
+    def Pinv(r):
+        rc = tb.split_e(r)
+        out = []
+        for c in range(3):
+            F = [Binv[a] if a == c else Cinv[a] for a in range(3)]
+            out.append(kron3(F[0], F[1], F[2], rc[c]) / gbar)
+        return forms.join(out)
+
+    x = np.zeros_like(rhs)
+    r = rhs.copy()
+    z = Pinv(r)
+    pv = z.copy()
+    rz = r @ z
+    nb = np.sqrt(rhs @ rhs)
+    for _ in range(maxit):
+        q = A(pv)
+        al = rz / (pv @ q)
+        x += al * pv
+        r -= al * q
+        if np.sqrt(r @ r) <= tol * nb:
+            break
+        z = Pinv(r)
+        rz_new = r @ z
+        pv = z + (rz_new / rz) * pv
+        rz = rz_new
+    return x
+
+
+def c4_setup(p=4, n=96):
+    """C4: identity map, eps at the quadrature points, mu = 1.  Returns (eps (element-major), tier B)."""
+    from .assemble import Quad, physical_qp
+    X = physical_qp(Quad(p, forms._n3(n))).reshape(-1, 3)
+    eps = c4_eps(X)
+    return eps, TierB(p, n, inv_eps=1.0 / eps)
+
+
+def c4_initial_state(tb, dt):
+    """C4: e0 per component = the smoothed N(0,1) draw of rng(4) (synth.smooth_fields),
+    d0 = M~2^{-1} K1 e0 by PCG, e0 <- K1^{-1} M~2 d0 (exact consistency), H = 0 so b0 = 0,
+    b^{1/2} = -(dt/2) D1 e0 (Taylor half step, reading Z8), h^{1/2} = K~1^{-1} M2 b^{1/2}."""
+    from .structured import curl_primal
+    shapes = [tuple(s[::-1]) for s in tb.sh_e]  # [z][y][x]
+    e0 = forms.join(synth.smooth_fields(4, shapes))
+    d0 = pcg_mass_eps(tb, forms.join(tb.apply_K1(tb.split_e(e0))))
+    e0 = tb.hodge_eps(d0)
+    bh = -0.5 * dt * forms.join(curl_primal(tb.split_e(e0)))
+    return d0, e0, bh, tb.hodge_mu(bh)
+
+
+# ------------------------------------------------------------------------------------------
 # consistent initial state
 # ------------------------------------------------------------------------------------------
 

@@ -45,6 +45,35 @@ def smooth_field(k, shape):
     return idctn(X, norm="ortho")
 
 
+def smooth_fields(k, shapes):
+    """C4 initial E: one N(0,1) draw per component from ONE generator rng(k) (drawn in component
+    order), each filtered like ``smooth_field``: orthonormal DCT-II -> 1/(1+|kappa|^2) -> inverse.
+    ``shapes``: [z][y][x] shape of each component."""
+    from scipy.fft import dctn, idctn
+    g = rng(k)
+    out = []
+    for shape in shapes:
+        x = g.standard_normal(shape)
+        X = dctn(x, norm="ortho")
+        kz, ky, kx = np.meshgrid(*[np.arange(s) for s in shape], indexing="ij")
+        X /= 1.0 + (kx ** 2 + ky ** 2 + kz ** 2)
+        out.append(idctn(X, norm="ortho"))
+    return out
+
+
+def gaussian_z(X, centre, sigma):
+    """The C3 source potential A(x) = z-hat exp(-|x - c|^2 / (2 sigma^2)) at points X[..., 3]."""
+    r2 = np.sum((np.asarray(X) - np.asarray(centre)) ** 2, axis=-1)
+    A = np.zeros(np.shape(X))
+    A[..., 2] = np.exp(-r2 / (2.0 * sigma ** 2))
+    return A
+
+
+def pulse(t, t0=0.15, width=0.05):
+    """C3 source amplitude s(t) = exp(-((t - t0)/width)^2) (reading Z16)."""
+    return np.exp(-((np.asarray(t) - t0) / width) ** 2)
+
+
 def c3_map(X):
     """BASELINE.json configs[2] geometry, a closed-form input: x -> x + 0.1 sin(pi x) sin(pi y)
     sin(pi z) (1, 1, 1) on the unit cube (X[..., 3] -> F[..., 3])."""

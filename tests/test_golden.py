@@ -117,3 +117,35 @@ def test_curved_map_converges_to_cube_spectrum():
         errs.append(np.max(np.abs(got - ref) / ref))
     rates = [np.log(errs[0] / errs[1]) / np.log(4 / 3), np.log(errs[1] / errs[2]) / np.log(5 / 4)]
     assert errs[-1] < 2e-3 and all(3.3 < r < 5.0 for r in rates), (errs, rates)
+
+
+def test_c3_source_fixture_is_the_oracle_recipe():
+    """tests/golden/c3_a_hat.npz (read by bench.py for the C3 source) is exactly what
+    scripts/make_c3_source.py computes from the oracle (readings Z16/Z28), and its dual curl is the
+    divergence-free j^ of oracle.workloads.c3_source."""
+    import synth
+    from oracle import workloads as W
+    from oracle.structured import curl_dual, div_dual
+    z = np.load(os.path.join(G, "c3_a_hat.npz"))
+    p, n = int(z["p"]), int(z["n"])
+    ctrl, _, _ = W.c3_setup(p, n)
+    _, c_J = synth.c3_centres()
+    a = W.project_dual1(p, n, synth.gaussian_z(W.physical_points(p, n, ctrl), c_J, W.C3_SIGMA))
+    assert np.array_equal(a, z["a_hat"])
+    j = forms.join(curl_dual(forms.split(a, "dual", 1, p, (n, n, n))))
+    assert np.array_equal(j, W.c3_source(p, n, ctrl))
+    assert np.abs(div_dual(forms.split(j, "primal", 1, p, (n, n, n)))).max() <= 1e-12 * np.abs(j).max()
+
+
+def test_workload_dt_fixture():
+    """tests/golden/workload_dt.json (scripts/make_workload_dt.py, oracle power iteration) holds
+    dt = dt_max / 2 for each config, C1's dt_max agrees with SURVEY 8(d)'s derived 0.03807, and the
+    quotient has converged to 1e-4 (monotone power iteration, reading Z15)."""
+    d = load("workload_dt.json")
+    assert abs(d["c1"]["dt_max"] - 0.03807) < 1e-4
+    for k, v in d.items():
+        if k.startswith("_"):
+            continue
+        assert abs(v["dt"] - 0.5 * v["dt_max"]) < 1e-15 * v["dt"]
+        assert abs(v["dt_max"] - 2.0 / np.sqrt(v["lambda"])) < 1e-12 * v["dt_max"]
+        assert -1e-12 * v["lambda"] <= v["lambda"] - v["lambda_prev"] < 1e-4 * v["lambda"]

@@ -37,7 +37,7 @@ def _c5_state(tb, pl):
 
 
 @pytest.mark.parametrize("p,n,steps,tol", [(3, 128, 1, 1e-11), (3, 128, 100, 1e-9), (2, 160, 1, 1e-11),
-                                           (4, 128, 1, 1e-11)])
+                                           (2, 160, 100, 1e-9), (4, 128, 1, 1e-11), (4, 128, 100, 1e-9)])
 def test_c5_full_size(p, n, steps, tol):
     pl = S.Plan(n, p)
     tb = TierB(p, n)
@@ -65,59 +65,59 @@ def test_c2_four_modes_200_steps():
         assert rel(host(a), r) < 1e-9
 
 
-def test_c4_variable_eps_full_size():
-    """configs[3]: identity map, p = 4, 96^3, eps = 1 + 0.5 sin(2 pi x) cos(2 pi y) at the quadrature
-    points (general Hodge, scalar weights), smooth random e0; one step."""
+def _golden_dt(cfg):
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", "workload_dt.json")
+    return json.load(open(path))[cfg]["dt"]
+
+
+def test_c4_as_configured_100_steps():
+    """configs[3] exactly as SURVEY 8(d) defines it: identity map, p = 4, 96^3, eps = 1 + 0.5 sin(2 pi x)
+    cos(2 pi y) point-sampled at the quadrature points, mu = 1; e0 = the smoothed rng(4) field
+    (synth.smooth_fields), d0 = M~2^{-1} K1 e0 by tier-B PCG, b^{1/2} = -(dt/2) D1 e0; dt = 0.5 dt_max of
+    this operator (tests/golden/workload_dt.json, written by scripts/make_workload_dt.py from the
+    oracle); 100 steps, every vector <= 1e-9 relative to tier B."""
     p, n = 4, 96
+    eps, tb = W.c4_setup(p, n)
+    dt = _golden_dt("c4")
+    st = W.c4_initial_state(tb, dt)
     pl = S.Plan(n, p)
-    X = pl.qp_coords()
-    eps = 1 + 0.5 * np.sin(2 * np.pi * X[:, 0]) * np.cos(2 * np.pi * X[:, 1])
-    del X
     pl.set_material(S.EPS, eps)
-    tb = TierB(p, n, inv_eps=1.0 / eps)
-    g = np.random.default_rng(4)
-    d0 = g.standard_normal(tb.N_e)
-    b0 = g.standard_normal(tb.N_h)
-    st = (d0, tb.hodge_eps(d0), b0, tb.hodge_mu(b0))
-    dt = 0.25 * CFL_N[p] / n
     dv = [dev(x) for x in st]
-    pl.step(*dv, dt, 1)
-    ref = tb.step(*st, dt)
+    pl.step(*dv, dt, 100)
+    ref = tb.run(*st, dt, 100)
     for a, r in zip(dv, ref):
-        assert rel(host(a), r) < 1e-11
+        assert rel(host(a), r) < 1e-9
 
 
-def test_c3_curved_inclusion_source_full_size():
-    """configs[2]: curved map interpolated in S_3^3 (reading Z18), eps in {1, 4} sphere, divergence-free
-    source j = D~1 a with a Gaussian pulse amplitude (reading Z16); 20 steps."""
+def test_c3_as_configured_200_steps():
+    """configs[2] exactly as SURVEY 8(d) / readings Z16, Z28 define it: the C3 map in S_3^3, eps in {1, 4}
+    (sphere r = 0.25 at rng(3)), zero initial fields, j^ = D~1 of the projected z-Gaussian (sigma 0.05,
+    centre the second rng(3) draw), s(t) = exp(-((t - 0.15)/0.05)^2); dt = 0.5 dt_max of this operator
+    (tests/golden/workload_dt.json); 200 steps, every vector <= 1e-9 relative to tier B, and the
+    Gauss law D~2 d = 0 on the GPU state."""
     p, n = 3, 48
-    ctrl = W.interpolate_map(p, n, W.c3_map)
+    ctrl, eps, _ = W.c3_setup(p, n)
+    jhat = W.c3_source(p, n, ctrl)
+    dt = _golden_dt("c3")
+    steps = 200
+    jamp = W.c3_amplitudes(dt, steps)
     pl = S.Plan(n, p, geom_ctrl=ctrl)
-    X = pl.qp_coords()
-    c_eps, _ = synth.c3_centres()
-    eps = np.where(np.linalg.norm(X - c_eps, axis=1) < 0.25, 4.0, 1.0)
-    del X
     pl.set_material(S.EPS, eps)
     tb = TierB(p, n, ctrl=ctrl, inv_eps=1.0 / eps, inv_mu=1.0)
-    tb.sep_mu = None
-    tb.W_mu = tb._W(1.0)
-    from oracle.structured import curl_dual
-    from oracle import forms
-    a = synth.normal(33, tb.N_h)[0]
-    jhat = forms.join(curl_dual(tb.split_h(a)))
-    steps = 20
-    dt = 0.25 * CFL_N[p] / n
-    tt = (np.arange(steps) + 0.5) * dt
-    jamp = np.exp(-((tt - 0.15 * steps * dt) / (0.05 * steps * dt)) ** 2)
-    g = np.random.default_rng(3)
-    d0 = g.standard_normal(tb.N_e)
-    b0 = g.standard_normal(tb.N_h)
-    st = (d0, tb.hodge_eps(d0), b0, tb.hodge_mu(b0))
+    z = np.zeros
+    st = (z(tb.N_e), z(tb.N_e), z(tb.N_h), z(tb.N_h))
     dv = [dev(x) for x in st]
     pl.step(*dv, dt, steps, j_hat=dev(jhat), j_amp=dev(jamp))
     ref = tb.run(*st, dt, steps, jhat, jamp)
     for x, r in zip(dv, ref):
-        assert rel(host(x), r) < 1e-10
+        assert np.linalg.norm(r) > 0
+        assert rel(host(x), r) < 1e-9
+    out = torch.zeros(2, dtype=torch.float64, device="cuda")
+    pl.gauss(dv[0], dv[2], out)
+    g = host(out)
+    assert g[0] < 1e-12 * np.abs(host(dv[0])).max() and g[1] < 1e-12 * max(np.abs(host(dv[2])).max(), 1e-300)
 
 
 @pytest.mark.parametrize("p", [2, 3])

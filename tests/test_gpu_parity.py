@@ -631,3 +631,63 @@ def test_abi_argument_validation_on_device():
     assert "alias" in S._lib.sgm_last_error().decode() or "distinct" in S._lib.sgm_last_error().decode()
     # a non-solenoidal source is refused by the check (SGM_E_SOURCE_DIVERGENCE = 6)
     assert pl.check_source(dev(np.random.default_rng(5).standard_normal(pl.N_e))) == 6
+
+
+@pytest.mark.parametrize("p,n", [(2, (4, 3, 5)), (3, 5)])
+def test_quadrature_rule_p_plus_2(p, n):
+    """quad_points = p + 2 (sgm_plan_desc.quad_points; the generic CTA-per-element Hodge kernel) on the
+    curved C3 map with a variable eps: Hodge stars and 20 steps against tier B built with the same
+    (p + 2)-point rule (reading Z13: plan and oracle use the same rule)."""
+    Q = p + 2
+    ctrl = W.interpolate_map(p, n, W.c3_map)
+    pl = S.Plan(n, p, geom_ctrl=ctrl, quad_points=Q)
+    X = pl.qp_coords()
+    eps = 1.0 + 0.5 * np.sin(2 * np.pi * X[:, 0]) * np.cos(2 * np.pi * X[:, 1])
+    pl.set_material(S.EPS, eps)
+    tb = TierB(p, n, ctrl=ctrl, inv_eps=1.0 / eps, inv_mu=1.0, Q=Q)
+    g = np.random.default_rng(81)
+    x = g.standard_normal(tb.N_e)
+    y = torch.empty(tb.N_e, dtype=torch.float64, device="cuda")
+    pl.hodge_star(S.MASS_EPS, dev(x), y)
+    assert rel(host(y), tb.hodge_eps(x)) < 1e-11
+    xb = g.standard_normal(tb.N_h)
+    yb = torch.empty(tb.N_h, dtype=torch.float64, device="cuda")
+    pl.hodge_star(S.MASS_MU, dev(xb), yb)
+    assert rel(host(yb), tb.hodge_mu(xb)) < 1e-11
+    st = _state(tb, 82)
+    dt = 0.3 * W.cfl_dt_max(tb)
+    for a, b in zip(_run_gpu(pl, st, dt, 20), tb.run(*st, dt, 20)):
+        assert rel(a, b) < 1e-10
+
+
+def test_c3_recipe_small():
+    """The configs[2] recipe (oracle.workloads.c3_setup / c3_source: curved map, eps inclusion, projected
+    Gaussian source, zero fields, Gaussian pulse in time) at 8^3, 60 steps through the pulse."""
+    p, n = 3, 8
+    ctrl, eps, _ = W.c3_setup(p, n)
+    jhat = W.c3_source(p, n, ctrl)
+    pl = S.Plan(n, p, geom_ctrl=ctrl)
+    pl.set_material(S.EPS, eps)
+    tb = TierB(p, n, ctrl=ctrl, inv_eps=1.0 / eps, inv_mu=1.0)
+    dt = 0.5 * W.cfl_dt_max(tb)
+    steps = 60
+    jamp = W.c3_amplitudes(dt * 6, steps)  # the pulse (t0 = 0.15) inside the run
+    st = tuple(np.zeros(k) for k in (tb.N_e, tb.N_e, tb.N_h, tb.N_h))
+    out = _run_gpu(pl, st, dt, steps, jhat, jamp)
+    for a, b in zip(out, tb.run(*st, dt, steps, jhat, jamp)):
+        assert np.linalg.norm(b) > 0 and rel(a, b) < 1e-10
+
+
+def test_pcg_star_zero_rhs_is_zero():
+    """Scheme-1 PCG stars (curved map) on a zero right-hand side give exactly zero (a zero denominator
+    in the CG ratios is a zero step, not NaN: ADVICE r1), and a zero-field start stays zero."""
+    p, n = 3, 5
+    pl = S.Plan(n, p, geom_ctrl=W.interpolate_map(p, n, W.c3_map))
+    pl.set_scheme(1)
+    z = torch.zeros(pl.N_e, dtype=torch.float64, device="cuda")
+    y = torch.full((pl.N_e,), 7.0, dtype=torch.float64, device="cuda")
+    pl.hodge_star(S.MASS_EPS, z, y)
+    assert torch.count_nonzero(y).item() == 0
+    st = [torch.zeros(k, dtype=torch.float64, device="cuda") for k in (pl.N_e, pl.N_e, pl.N_h, pl.N_h)]
+    pl.step(*st, 0.001, 3)
+    assert all(torch.isfinite(x).all().item() and torch.count_nonzero(x).item() == 0 for x in st)
