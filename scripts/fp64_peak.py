@@ -64,8 +64,8 @@ def main(tag):
            "sm_mhz_after": clk, "sm_max_mhz": clk_max,
            "dfma_lanes_per_sm_per_cycle": (d["tflops"] * 1e12 / 2 / sms / (clk_max * 1e6)) if clk_max else None,
            "how": "scripts/fp64_peak.py: DFMA chains kernel (CUDA events) and torch.matmul float64 8192^3 (cuBLAS)"}
-    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    path = os.path.join(ROOT, "profiles", f"{tag}_fp64_peak.json")
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    path = os.path.join(ROOT, "gpurun_out", f"{tag}_fp64_peak.json")  # copied to profiles/ by hand
     json.dump(out, open(path, "w"), indent=1)
     print(json.dumps(out))
 
