@@ -547,6 +547,23 @@ def main():
                               "kernels_per_step": pl.kernels_per_step(),
                               "useful_bytes_frac": 16.0 * dofs / (vms / K * 1e-3) / 1e9 / peak}
         pl.set_options(0)
+        # the (e,h)-state variant (sgm_step_eh, NEXT #3): two stored vectors, same DOF-updates
+        for name, o in (("eh_state", 0), ("eh_state_fused", S.OPT_FUSED)):
+            pl.set_options(o)
+            e2, h2 = state[1].clone(), state[3].clone()
+            pl.step_eh(e2, h2, dt, W, stream=stream)
+            torch.cuda.synchronize()
+            e0_, e1_ = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0_.record(stream)
+            pl.step_eh(e2, h2, dt, K, stream=stream)
+            e1_.record(stream)
+            torch.cuda.synchronize()
+            vms = max_over_ranks(e0_.elapsed_time(e1_), dist, dev)
+            variants[name] = {"options": o, "ms_per_step": vms / K, "value": aggregate_value(dofs, K, vms, world),
+                              "algo_bytes_per_dof_update": (8.0 if o else 12.0),
+                              "useful_bytes_frac": 16.0 * dofs / (vms / K * 1e-3) / 1e9 / peak}
+            del e2, h2
+        pl.set_options(0)
     env = {k: v for k, v in os.environ.items() if k.startswith("SGM_")}
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,

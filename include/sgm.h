@@ -152,6 +152,17 @@ sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h,
                     const double* j_hat, const double* j_amp, double dt, int n_steps,
                     void* workspace, size_t ws_bytes, void* stream);
 
+/* The (e,h)-state variant of the step (reading Z30 in DESIGN.md): with
+   e = K1^{-1} M~2_{1/eps} d and h = K~1^{-1} M2_{1/mu} b, one step of sgm_step is exactly
+     e <- e + K1^{-1} M~2_{1/eps} (dt (D~1 h - s_k j^))      h <- h - K~1^{-1} M2_{1/mu} (dt D1 e)
+   (the Petrov-Galerkin form in E_h, H_h), so d and b need not be stored: two state
+   vectors instead of four.  e at t_n and h at t_{n+1/2} on entry, advanced by n_steps dt on exit;
+   results equal sgm_step's e, h up to rounding.  Scheme 2 only (SGM_E_UNSUPPORTED otherwise); the
+   energy of eq. P:L240 needs d, b (not available here).  Other arguments as sgm_step.  Async;
+   direct enqueue (no graph). */
+sgm_status sgm_step_eh(sgm_plan plan, double* e, double* h, const double* j_hat, const double* j_amp,
+                       double dt, int n_steps, void* workspace, size_t ws_bytes, void* stream);
+
 /* Higher-order time integration by symmetric composition of leapfrog sub-steps (the paper's
    future work; reading Z25 in DESIGN.md).  Each of the n_steps steps
    applies the kick-drift-kick sub-steps S(w_0 dt) ... S(w_{n_w-1} dt), where S(tau) is

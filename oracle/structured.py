@@ -235,6 +235,27 @@ class TierB:
             d, e, b, h = self.step(d, e, b, h, dt, jhat, s)
         return d, e, b, h
 
+    def step_eh(self, e, h, dt, jhat=None, s=1.0):
+        """The (e,h)-state form of one step (the Petrov-Galerkin scheme in E_h, H_h, P:L395-408,
+        with its typos corrected per reading Z6): e <- e + K1^{-1} M~2_{1/eps} (dt (D~1 h - s j)),
+        h <- h - K~1^{-1} M2_{1/mu} (dt D1 e); the same as step() on e = K1^{-1} M~2 d,
+        h = K~1^{-1} M2 b (eqs. discrete2_*), d and b never formed."""
+        cd = curl_dual(self.split_h(h))
+        if jhat is not None:
+            j = self.split_e(jhat)
+            r = [dt * (cd[c] - s * j[c]) for c in range(3)]
+        else:
+            r = [dt * cd[c] for c in range(3)]
+        e = e + forms.join(self.solve_K1(self.mass_eps(r)))
+        ce = curl_primal(self.split_e(e))
+        h = h - forms.join(self.solve_Kt1(self.mass_mu([dt * ce[c] for c in range(3)])))
+        return e, h
+
+    def run_eh(self, e, h, dt, n_steps, jhat=None, jamp=None):
+        for k in range(n_steps):
+            e, h = self.step_eh(e, h, dt, jhat, 1.0 if jamp is None else jamp[k])
+        return e, h
+
     def hodge_eps(self, d):
         """e = K1^{-1} M~2_{1/eps} d  (eq. discrete2_hodge_eps)."""
         return forms.join(self.solve_K1(self.mass_eps(self.split_e(d))))

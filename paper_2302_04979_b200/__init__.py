@@ -58,6 +58,7 @@ _SIGS = {
     "sgm_workspace_bytes": [c_void_p, ctypes.POINTER(c_size_t)],
     "sgm_step": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int,
                  c_void_p, c_size_t, c_void_p],
+    "sgm_step_eh": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int, c_void_p, c_size_t, c_void_p],
     "sgm_step_host": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int,
                       c_void_p],
     "sgm_step_composed": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int,
@@ -286,6 +287,12 @@ class Plan:
         w = self.workspace() if ws is None else ws
         check(sgm_step(self.h, _ptr(d), _ptr(e), _ptr(b), _ptr(h), _ptr(j_hat), _ptr(j_amp), float(dt),
                        int(n_steps), _ptr(w), w.numel() * 8, _stream(stream)), "sgm_step")
+
+    def step_eh(self, e, h, dt, n_steps=1, j_hat=None, j_amp=None, stream=None, ws=None):
+        """The (e,h)-state variant (sgm_step_eh): only e and h are stored and advanced."""
+        w = self.workspace() if ws is None else ws
+        check(sgm_step_eh(self.h, _ptr(e), _ptr(h), _ptr(j_hat), _ptr(j_amp), float(dt), int(n_steps), _ptr(w),
+                          w.numel() * 8, _stream(stream)), "sgm_step_eh")
 
     def step_composed(self, d, e, b, h, dt, weights=None, n_steps=1, j_hat=None, j_amp=None, stream=None,
                       ws=None):

@@ -161,7 +161,8 @@ struct ProfScope {
 
 // One axis pass over the 3 components of a form (kind 0: e/d shapes, 1: b/h shapes).
 void sweep_pass(const Plan& P, int kind, int axis, double* const in[3], double* const out[3], int op_own,
-                int op_oth, const double* scale, bool band, bool solve, cudaStream_t st, int reverse = 0) {
+                int op_oth, const double* scale, bool band, bool solve, cudaStream_t st, int reverse = 0,
+                int accum = 0) {
   SweepArgs a;
   std::memset(&a, 0, sizeof(a));
   a.ncomp = 3;
@@ -182,6 +183,7 @@ void sweep_pass(const Plan& P, int kind, int axis, double* const in[3], double* 
     a.comp[c].tab = table(P, axis, own_or(axis, c, op_own, op_oth));
     a.comp[c].tslot = own_or(axis, c, 0, 1);
     a.comp[c].scale = scale ? scale[c] : 1.0;
+    a.comp[c].accum = accum;
   }
   if (!launch_sweep(P.p, P.seg[axis], a, st)) P.launch_fail = 1;
 }
@@ -200,6 +202,7 @@ struct PassComp {
   int op;             // line-operator table
   int dg[3];          // per axis: -1 = no diagonal, else the diag_factor kind applied along it
   double scale;
+  int accum = 0;      // 1: out += scale * result ((e,h)-state increments)
 };
 
 // Components of one launch share the line mode (x, or strided y/z) and the padded table rows and
@@ -249,6 +252,7 @@ void sweep_pass_list(const Plan& P, int kind, const PassComp* pc, int n, cudaStr
     C.tslot = (a.tabs[1] && C.tab == a.tabs[1]) ? 1 : 0;
     C.axis = axis;
     C.scale = q.scale;
+    C.accum = q.accum;
     C.dline[0] = q.dg[t0] >= 0 ? diag_factor(P, t0, q.dg[t0]) : nullptr;
     C.dline[1] = q.dg[t1] >= 0 ? diag_factor(P, t1, q.dg[t1]) : nullptr;
   }
@@ -335,6 +339,7 @@ bool fused_list(const Plan& P, int kind, const PassComp* pc, int n, cudaStream_t
       C.axis = axis;
       C.cidx = q.c;
       C.scale = q.scale;
+      C.accum = q.accum;
       C.dline[0] = q.dg[t0] >= 0 ? diag_factor(P, t0, q.dg[t0]) : nullptr;
       C.dline[1] = q.dg[t1] >= 0 ? diag_factor(P, t1, q.dg[t1]) : nullptr;
     }
@@ -395,7 +400,7 @@ void fork_join(Plan& P, cudaStream_t st, F1&& f1, F2&& f2) {
 //   mu  (kind 1): component c is swept (Gamma_B^{p}, LU Hat G^T) along axis c only and scaled by
 //                 s along the other two: strided pass {2 along z, 1 along y} (or two passes), x pass {0}.
 void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* t, cudaStream_t st,
-                        const double* scale = nullptr) {
+                        const double* scale = nullptr, int accum = 0) {
   const int kind = (which == SGM_MASS_EPS) ? 0 : 1;
   struct {
     const double* scale;
@@ -415,8 +420,9 @@ void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* 
       PassComp a3[3] = {{2, 0, X[0], T[0], op, {-1, -1, -1}, 1.0},
                         {2, 1, X[1], T[1], op, {-1, -1, -1}, 1.0},
                         {1, 2, X[2], T[2], op, {-1, -1, -1}, 1.0}};
-      PassComp b1[1] = {{1, 0, T[0], Y[0], op, {0, -1, -1}, M.scale[0]}};
-      PassComp c2[2] = {{0, 1, T[1], Y[1], op, {-1, 0, -1}, M.scale[1]}, {0, 2, T[2], Y[2], op, {-1, -1, 0}, M.scale[2]}};
+      PassComp b1[1] = {{1, 0, T[0], Y[0], op, {0, -1, -1}, M.scale[0], accum}};
+      PassComp c2[2] = {{0, 1, T[1], Y[1], op, {-1, 0, -1}, M.scale[1], accum},
+                        {0, 2, T[2], Y[2], op, {-1, -1, 0}, M.scale[2], accum}};
       { ProfScope ps(P, kz, st); sweep_pass_list(P, 0, a3, 3, st, 1); }
       // x side: components 1, 2 of e/d, x-extent a (P.ax[0].a)
       const Share sb = strided_share(P, 1, 1, 2, (P.ax[0].a % 2) == 0), sc = {sb.n - sb.k, sb.n};
@@ -425,17 +431,18 @@ void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* 
       return;
     }
     PassComp z[2] = {{2, 0, X[0], T[0], op, {-1, -1, -1}, 1.0}, {2, 1, X[1], T[1], op, {-1, -1, -1}, 1.0}};
-    PassComp yy[2] = {{1, 0, T[0], Y[0], op, {0, -1, -1}, M.scale[0]}, {1, 2, X[2], T[2], op, {-1, -1, -1}, 1.0}};
-    PassComp xx[2] = {{0, 1, T[1], Y[1], op, {-1, 0, -1}, M.scale[1]}, {0, 2, T[2], Y[2], op, {-1, -1, 0}, M.scale[2]}};
+    PassComp yy[2] = {{1, 0, T[0], Y[0], op, {0, -1, -1}, M.scale[0], accum}, {1, 2, X[2], T[2], op, {-1, -1, -1}, 1.0}};
+    PassComp xx[2] = {{0, 1, T[1], Y[1], op, {-1, 0, -1}, M.scale[1], accum},
+                      {0, 2, T[2], Y[2], op, {-1, -1, 0}, M.scale[2], accum}};
     { ProfScope ps(P, kz, st); sweep_pass_list(P, 0, z, 2, st, 1); }
     { ProfScope ps(P, ky, st); sweep_pass_list(P, 0, yy, 2, st, 0); }
     { ProfScope ps(P, kx, st); sweep_pass_list(P, 0, xx, 2, st, 1); }
   } else {
     // scheme 2: Hat G^{-T} Gamma_B^p; scheme 1: Gamma_C^{p-2}^{-1} Hat G (other axes: diag(s) in both)
     const int op = P.scheme == 1 ? OP_S1_MU_OWN : OP_MU_OWN;
-    PassComp z[1] = {{2, 2, X[2], Y[2], op, {1, 1, -1}, M.scale[2]}};
-    PassComp yy[1] = {{1, 1, X[1], Y[1], op, {1, -1, 1}, M.scale[1]}};
-    PassComp xx[1] = {{0, 0, X[0], Y[0], op, {-1, 1, 1}, M.scale[0]}};
+    PassComp z[1] = {{2, 2, X[2], Y[2], op, {1, 1, -1}, M.scale[2], accum}};
+    PassComp yy[1] = {{1, 1, X[1], Y[1], op, {1, -1, 1}, M.scale[1], accum}};
+    PassComp xx[1] = {{0, 0, X[0], Y[0], op, {-1, 1, 1}, M.scale[0], accum}};
     if (mu_merged(P)) {
       // z-lines of component 2 and y-lines of component 1 in one strided launch; the x-lines of
       // component 0 (independent) concurrently on the plan-owned stream when forking is enabled
@@ -489,9 +496,13 @@ bool fused_fits(const Plan& P, int which, bool with_source) {
 //   reduced mu:  fused {2 along z; 1 along y; 0 along x} x -> y;
 //   full:        fused z pass (all components) x -> t, then the y and x passes.
 // Returns false (nothing enqueued) when the fused kernel has no fitting configuration.
-bool star_fused(Plan& P, int which, double* x, double* y, double* t, cudaStream_t st, const PrologueArgs& pro) {
+// eh = true: the (e,h)-state step -- x is unused (the curl source in `pro` gives the increment) and
+// the star's output is accumulated into y (y += dt S(curl)).
+bool star_fused(Plan& P, int which, double* x, double* y, double* t, cudaStream_t st, const PrologueArgs& pro,
+                bool eh = false) {
   const int kind = (which == SGM_MASS_EPS) ? 0 : 1;
-  const int fuse = kind + 1;
+  const int fuse = kind + 1 + (eh ? 2 : 0);
+  const int acc = eh ? 1 : 0;
   const double* sc = P.mass[which].scale;
   double *X[3], *Y[3], *T[3];
   comps_of(P, kind, x, X);
@@ -506,7 +517,7 @@ bool star_fused(Plan& P, int which, double* x, double* y, double* t, cudaStream_
     fused_list(P, kind, z3, 3, st, 1, fuse, pro, cls, false);
     const int ky = kind == 0 ? SGM_K_EPS_Y : SGM_K_MU_Y, kx = kind == 0 ? SGM_K_EPS_X : SGM_K_MU_X;
     { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, true, true, st, 0); }
-    { ProfScope ps(P, kx, st); sweep_pass(P, kind, 0, T, Y, own, oth, sc, true, true, st, 1); }
+    { ProfScope ps(P, kx, st); sweep_pass(P, kind, 0, T, Y, own, oth, sc, true, true, st, 1, acc); }
     return true;
   }
   if (kind == 0) {
@@ -516,8 +527,8 @@ bool star_fused(Plan& P, int which, double* x, double* y, double* t, cudaStream_
                       {1, 2, X[2], T[2], op, {-1, -1, -1}, 1.0}};
     if (!fused_list(P, 0, a3, 3, st, 1, fuse, pro, cls, true)) return false;
     fused_list(P, 0, a3, 3, st, 1, fuse, pro, cls, false);
-    PassComp b1[1] = {{1, 0, T[0], Y[0], op, {0, -1, -1}, sc[0]}};
-    PassComp c2[2] = {{0, 1, T[1], Y[1], op, {-1, 0, -1}, sc[1]}, {0, 2, T[2], Y[2], op, {-1, -1, 0}, sc[2]}};
+    PassComp b1[1] = {{1, 0, T[0], Y[0], op, {0, -1, -1}, sc[0], acc}};
+    PassComp c2[2] = {{0, 1, T[1], Y[1], op, {-1, 0, -1}, sc[1], acc}, {0, 2, T[2], Y[2], op, {-1, -1, 0}, sc[2], acc}};
     if (fork_on(P)) {
       const Share sb = strided_share(P, 1, 1, 2, (P.ax[0].a % 2) == 0), sc2 = {sb.n - sb.k, sb.n};
       fork_join(P, st, [&](cudaStream_t s1) { ProfScope ps(P, SGM_K_EPS_Y, s1); sweep_pass_list(P, 0, b1, 1, s1, 0, sb); },
@@ -529,9 +540,9 @@ bool star_fused(Plan& P, int which, double* x, double* y, double* t, cudaStream_
     return true;
   }
   const int op = OP_MU_OWN;
-  PassComp m3[3] = {{2, 2, X[2], Y[2], op, {1, 1, -1}, sc[2]},
-                    {1, 1, X[1], Y[1], op, {1, -1, 1}, sc[1]},
-                    {0, 0, X[0], Y[0], op, {-1, 1, 1}, sc[0]}};
+  PassComp m3[3] = {{2, 2, X[2], Y[2], op, {1, 1, -1}, sc[2], acc},
+                    {1, 1, X[1], Y[1], op, {1, -1, 1}, sc[1], acc},
+                    {0, 0, X[0], Y[0], op, {-1, 1, 1}, sc[0], acc}};
   if (!fused_list(P, 1, m3, 3, st, 1, fuse, pro, cls, true)) return false;
   fused_list(P, 1, m3, 3, st, 1, fuse, pro, cls, false);
   return true;
@@ -899,6 +910,54 @@ void half_step(Plan& P, int half, double* d, double* e, double* b, double* h, co
   }
 }
 
+// One half step of the (e,h)-state variant (reading Z30): with e = K1^{-1} M~2 d
+// and h = K~1^{-1} M2 b the four-vector step is, exactly,
+//   half 0: e <- e + K1^{-1} M~2_{1/eps} (tau (D~1 h - s j^))      (eqs. discrete2_ampere + hodge_eps)
+//   half 1: h <- h - K~1^{-1} M2_{1/mu} (tau D1 e)                  (eqs. discrete2_faraday + hodge_mu)
+// (the Petrov-Galerkin form in E_h, H_h), so d and b are never stored.  The increment's
+// curl is the update kernel in increment mode (or fused into the first sweep with SGM_OPT_FUSED) and
+// the star's last sweeps accumulate into e / h.
+void half_step_eh(Plan& P, int half, double* e, double* h, const double* jhat, const double* s_ptr, double tau,
+                  const WS& w, cudaStream_t st) {
+  const int kind = half;
+  const int mass = half == 0 ? SGM_MASS_EPS : SGM_MASS_MU;
+  const int own = half == 0 ? OP_EPS_OWN : OP_MU_OWN, oth = half == 0 ? OP_EPS_OTH : OP_MU_OTH;
+  const int ky = half == 0 ? SGM_K_EPS_Y : SGM_K_MU_Y, kx = half == 0 ? SGM_K_EPS_X : SGM_K_MU_X;
+  double* out = half == 0 ? e : h;
+  PrologueArgs pa = half == 0 ? make_pro(P, 1, h, jhat, s_ptr, tau) : make_pro(P, 0, e, nullptr, nullptr, tau);
+  const MassData& M = P.mass[mass];
+  if (M.kind == HODGE_SEPARABLE && fused_sched(P) && star_fused(P, mass, nullptr, out, w.t, st, pa, true)) return;
+  // the increment r = tau (D~1 h - s j^) or -tau D1 e into the workspace
+  double* r = M.kind == HODGE_SEPARABLE ? w.r : w.t;
+  SweepArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.ncomp = 3;
+  double* R[3];
+  comps_of(P, kind, r, R);
+  for (int c = 0; c < 3; ++c) {
+    comp_shape(P, kind, c, a.comp[c].ext);
+    a.comp[c].in = R[c];
+  }
+  a.pro = pa;
+  { ProfScope ps(P, SGM_K_UPDATE, st); launch_update(half == 0 ? PRO_AMPERE_INC : PRO_FARADAY_INC, a, st); }
+  double *T[3], *O[3], *Rr[3];
+  comps_of(P, kind, w.t, T);
+  comps_of(P, kind, out, O);
+  if (M.kind == HODGE_SEPARABLE && reduced_sched(P)) {
+    hodge_star_reduced(P, mass, r, out, w.t, st, nullptr, 1);
+  } else if (M.kind == HODGE_SEPARABLE) {
+    { ProfScope ps(P, half == 0 ? SGM_K_EPS_Z : SGM_K_MU_Z, st); sweep_pass(P, kind, 2, R, T, own, oth, nullptr, true, true, st, 1); }
+    { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, true, true, st, 0); }
+    { ProfScope ps(P, kx, st); sweep_pass(P, kind, 0, T, O, own, oth, M.scale, true, true, st, 1, 1); }
+  } else {
+    { ProfScope ps(P, SGM_K_HODGE_GENERAL, st); mass_apply(P, mass, w.t, w.r, nullptr, st); }
+    comps_of(P, kind, w.r, Rr);
+    { ProfScope ps(P, SGM_K_SOLVE_Z, st); sweep_pass(P, kind, 2, Rr, T, own, oth, nullptr, false, true, st); }
+    { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, false, true, st); }
+    { ProfScope ps(P, kx, st); sweep_pass(P, kind, 0, T, O, own, oth, nullptr, false, true, st, 0, 1); }
+  }
+}
+
 // one leapfrog step (eqs. discrete2_*)
 void step_once(Plan& P, double* d, double* e, double* b, double* h, const double* jhat, const double* s_ptr,
                double dt, const WS& w, cudaStream_t st) {
@@ -1017,6 +1076,7 @@ sgm_status sgm_plan_destroy(sgm_plan plan) {
     DeviceGuard g(P->device);
     if (P->graph_exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec));
     if (P->graph_exec_c) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec_c));
+    if (P->graph_exec_e) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec_e));
     cudaFree(P->tables_dev);
     cudaFree(P->wide_dev);
     cudaFree(P->basis_dev);
@@ -1276,6 +1336,29 @@ sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h, c
   }
   for (int k = 0; k < n_steps; ++k) step_once(*P, d, e, b, h, j_hat, j_amp ? j_amp + k : nullptr, dt, w, st);
   return cuda_check(P, "sgm_step");
+}
+
+sgm_status sgm_step_eh(sgm_plan plan, double* e, double* h, const double* j_hat, const double* j_amp, double dt,
+                       int n_steps, void* workspace, size_t ws_bytes, void* stream) {
+  sgm_status s = check_plan(plan, true);
+  if (s != SGM_OK) return s;
+  Plan* P = PL(plan);
+  if (!e || !h || !aligned8(e) || !aligned8(h)) return fail(SGM_E_INVALID_ARG, "state pointers must be non-NULL and 8-byte aligned");
+  if ((j_hat && !aligned8(j_hat)) || (j_amp && !aligned8(j_amp))) return fail(SGM_E_INVALID_ARG, "misaligned source");
+  if (!std::isfinite(dt)) return fail(SGM_E_INVALID_ARG, "dt must be finite");
+  if (n_steps < 0) return fail(SGM_E_INVALID_ARG, "n_steps < 0");
+  if (e == h) return fail(SGM_E_INVALID_ARG, "state vectors alias");
+  if (P->scheme != 2) return fail(SGM_E_UNSUPPORTED, "the (e,h)-state step is built for the second scheme");
+  WS w;
+  if ((s = ws_carve(*P, workspace, ws_bytes, w)) != SGM_OK) return s;
+  DeviceGuard g(P->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int k = 0; k < n_steps; ++k) {
+    const double* sp = j_amp ? j_amp + k : nullptr;
+    half_step_eh(*P, 0, e, h, j_hat, sp, dt, w, st);
+    half_step_eh(*P, 1, e, h, j_hat, sp, dt, w, st);
+  }
+  return cuda_check(P, "sgm_step_eh");
 }
 
 sgm_status sgm_step_composed(sgm_plan plan, double* d, double* e, double* b, double* h, const double* j_hat,

@@ -69,8 +69,9 @@ struct Comp {
   int TD, n1;            // t0 extent (lanes) and t1 extent; tiles = n1 * ceil(TD / 32)
   int tpr;               // tiles per t1 row = ceil(TD / 32)
   int st0, st1, gs;      // state strides (t0, t1, along)
-  int nst;               // staged arrays: [0] state, [1] j^ (if has_j), then curl sources
-  int has_j;
+  int nst;               // staged arrays: the state (if ost >= 0), j^ (if jst >= 0), then curl sources
+  int ost, jst;          // stage of the old state / of j^ (-1: none)
+  int accum;             // 1: out += scale * result ((e,h) state), 0: out = scale * result
   Stage s[kMaxStages];
   Term t[2];
   int tslot;
@@ -133,7 +134,11 @@ __global__ void __launch_bounds__(480, 1) fsweep_kernel(const __grid_constant__ 
   constexpr int M = RL::M;
   constexpr int RS = RL::RS;
   static_assert(HB >= 1 && HB <= P, "band half-width");
-  static_assert(FUSE == 1 || FUSE == 2, "fused kernel");
+  static_assert(FUSE >= 1 && FUSE <= 4, "fused kernel");
+  // FUSE 1 / 2: state update (Ampere / Faraday); 3 / 4: the increments alone (the (e,h)-state step
+  // e += dt S_eps(D~1 h - s j^), h -= dt S_mu(D1 e), sgm_step_eh): no state read or written
+  constexpr bool DUAL = (FUSE == 1 || FUSE == 3);
+  constexpr bool INC = (FUSE >= 3);
   extern __shared__ __align__(16) double sm[];
   const int NC = (blockDim.x >> 5) - A.np;  // consumer warps; the last np warps produce
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -215,7 +220,7 @@ __global__ void __launch_bounds__(480, 1) fsweep_kernel(const __grid_constant__ 
   const int s = warp;
   const int r0 = s * SEG;
   const double dt = A.dt;
-  const double sdt = (FUSE == 1) ? dt * (A.s_ptr ? __ldg(A.s_ptr) : 1.0) : 0.0;
+  const double sdt = DUAL ? dt * (A.s_ptr ? __ldg(A.s_ptr) : 1.0) : 0.0;
   pipe::mbar_wait(tab_mb, 0);
   int it = 0;
   for (int item = blockIdx.x; item < A.nitems; item += G, ++it) {
@@ -250,8 +255,8 @@ __global__ void __launch_bounds__(480, 1) fsweep_kernel(const __grid_constant__ 
       }
       return d;
     };
-    const RD rold = mk(Read{0, 0, 0});
-    const RD rj = mk(Read{C.has_j ? 1 : 0, 0, 0});
+    const RD rold = mk(Read{C.ost >= 0 ? C.ost : 0, 0, 0});
+    const RD rj = mk(Read{C.jst >= 0 ? C.jst : 0, 0, 0});
     const RD rh0 = mk(C.t[0].hi), rl0 = mk(C.t[0].lo), rh1 = mk(C.t[1].hi), rl1 = mk(C.t[1].lo);
     // primal PEC bounds of the transverse terms (constant per line); along-line terms check the row
     bool al[2], hok[2], lk[2];
@@ -271,14 +276,14 @@ __global__ void __launch_bounds__(480, 1) fsweep_kernel(const __grid_constant__ 
       const int r = r0 + k;
       if (!lok || r < 0 || r >= L) return 0.0;
       auto at = [&](const RD& d) { return stg[d.q + k * d.rs + ((k & 1) ? d.po : d.pe)]; };
-      const double old = at(rold);
+      const double old = INC ? 0.0 : at(rold);
       double cu[2];
       const RD* H[2] = {&rh0, &rh1};
       const RD* O[2] = {&rl0, &rl1};
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         double hi, lo;
-        if (FUSE == 1) {  // dual: (dv)_j = v_{j+1} - v_j
+        if (DUAL) {       // dual: (dv)_j = v_{j+1} - v_j
           hi = at(*H[t]);
           lo = at(*O[t]);
         } else {          // primal: (du)_j = u_j - u_{j-1}, u_{-1} = u_a = 0 (PEC)
@@ -288,8 +293,8 @@ __global__ void __launch_bounds__(480, 1) fsweep_kernel(const __grid_constant__ 
         cu[t] = hi - lo;
       }
       const double cc = cu[0] - cu[1];
-      if (FUSE == 1) {
-        const double jv = C.has_j ? at(rj) : 0.0;
+      if (DUAL) {
+        const double jv = C.jst >= 0 ? at(rj) : 0.0;
         return fma(-sdt, jv, fma(dt, cc, old));
       }
       return fma(-dt, cc, old);
@@ -305,7 +310,7 @@ __global__ void __launch_bounds__(480, 1) fsweep_kernel(const __grid_constant__ 
     __syncwarp();
     if (lane == 0) mbar_arrive(empty_mb);
     // updated state rows of this segment (read by no other line: stored directly)
-    if (lok && s < S) {
+    if (!INC && lok && s < S) {
       double* dst = C.state + (long(t0) * C.st0 + long(t1) * C.st1 + long(r0) * C.gs);
       const long gs = C.gs;
 #pragma unroll
@@ -427,7 +432,11 @@ __global__ void __launch_bounds__(480, 1) fsweep_kernel(const __grid_constant__ 
       if (C.dline[1]) sc *= __ldg(C.dline[1] + t1);
       double* dst = C.out + (long(t0) * C.st0 + long(t1) * C.st1 + long(r0) * C.gs);
       const long gs = C.gs;
-      if (r0 + SEG <= L) {
+      if (C.accum) {
+#pragma unroll
+        for (int k = 0; k < SEG; ++k)
+          if (r0 + k < L) dst[k * gs] = fma(sc, v[k], dst[k * gs]);
+      } else if (r0 + SEG <= L) {
 #pragma unroll
         for (int k = 0; k < SEG; ++k) dst[k * gs] = sc * v[k];
       } else {

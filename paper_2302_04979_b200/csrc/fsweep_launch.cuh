@@ -75,18 +75,20 @@ inline bool make_args(const SweepArgs& a, int fuse, int SEG, fsweep::Args& A, in
       soff += C.xmode ? even_up(nl * G.st0 + 4) : nrow * G.pitch;
       return C.nst++;
     };
-    if (!al16(S.in)) return false;
-    add(S.in, str, S.ext, 0, 0, 32, 0, C.L);
-    const double* jh = (fuse == 1) ? a.pro.jhat[c] : nullptr;
+    C.accum = S.accum;
+    C.ost = C.jst = -1;
+    if (fuse <= 2) {  // the old state (updated in place); fuse 3 / 4: increments only
+      if (!al16(S.in)) return false;
+      C.ost = add(S.in, str, S.ext, 0, 0, 32, 0, C.L);
+    }
+    const double* jh = (fuse == 1 || fuse == 3) ? a.pro.jhat[c] : nullptr;
     if (jh) {
       if (!al16(jh)) return false;
-      add(jh, str, S.ext, 0, 0, 32, 0, C.L);
-      C.has_j = 1;
-    } else {
-      // keep stage 1 free so curl stages start at 2 only when j^ is present
+      C.jst = add(jh, str, S.ext, 0, 0, 32, 0, C.L);
     }
     // component c of the curl: d_{a1} src_{c1} - d_{a2} src_{c2}, (a1, c1) = (c+1, c+2),
     // (a2, c2) = (c+2, c+1) mod 3 (SURVEY 8.0 stencils)
+    const bool dual = (fuse == 1 || fuse == 3);
     const int aa[2] = {(c + 1) % 3, (c + 2) % 3}, cc[2] = {(c + 2) % 3, (c + 1) % 3};
     for (int t = 0; t < 2; ++t) {
       const int* se = a.pro.sext[cc[t]];
@@ -100,14 +102,14 @@ inline bool make_args(const SweepArgs& a, int fuse, int SEG, fsweep::Args& A, in
       if (T.where != 0 && se[ax] < C.L) return false;
       if (T.where == 0) {
         const int st = add(src, sstr, se, 0, 0, 32, 0, se[ax]);
-        if (fuse == 1) T.hi = {st, 0, 1}, T.lo = {st, 0, 0};
+        if (dual) T.hi = {st, 0, 1}, T.lo = {st, 0, 0};
         else T.hi = {st, 0, 0}, T.lo = {st, 0, -1};
       } else if (T.where == 1) {
-        const int st = add(src, sstr, se, 0, fuse == 1 ? 0 : -1, 33, 0, C.L);
-        if (fuse == 1) T.hi = {st, 1, 0}, T.lo = {st, 0, 0};
+        const int st = add(src, sstr, se, 0, dual ? 0 : -1, 33, 0, C.L);
+        if (dual) T.hi = {st, 1, 0}, T.lo = {st, 0, 0};
         else T.hi = {st, 0, 0}, T.lo = {st, -1, 0};
       } else {
-        if (fuse == 1) {
+        if (dual) {
           const int s0 = add(src, sstr, se, 0, 0, 32, 0, C.L), s1 = add(src, sstr, se, 1, 0, 32, 0, C.L);
           T.hi = {s1, 0, 0};
           T.lo = {s0, 0, 0};
@@ -158,6 +160,12 @@ bool launch_s(int fuse, const SweepArgs& a, cudaStream_t st) {
     return false;
   }
   if (fuse == 2) return launch_t<P, P, SEG, 2>(a, st);
+  if (fuse == 3) {
+    if (a.band_hw <= HLO) return launch_t<P, HLO, SEG, 3>(a, st);
+    if (a.band_hw <= P - 1) return launch_t<P, P - 1, SEG, 3>(a, st);
+    return false;
+  }
+  if (fuse == 4) return launch_t<P, P, SEG, 4>(a, st);
   return false;
 }
 

@@ -95,7 +95,8 @@ __device__ __forceinline__ unsigned fdiv(unsigned n, unsigned d, unsigned m, uns
 
 template <int PRO, int U, int CC, bool FULL>
 __device__ __forceinline__ void update_chunk(const UpdArgs& A, const UpdComp& C, int e0) {
-  constexpr bool DUAL = (PRO == PRO_AMPERE);
+  constexpr bool DUAL = (PRO == PRO_AMPERE || PRO == PRO_AMPERE_INC);
+  constexpr bool INC = (PRO == PRO_AMPERE_INC || PRO == PRO_FARADAY_INC);
   constexpr int AX[2] = {(CC + 1) % 3, (CC + 2) % 3};  // differentiated axis of each term
   // parameters into registers once (unpredicated)
   const double* __restrict__ src[2] = {C.t[0].src, C.t[1].src};
@@ -130,7 +131,7 @@ __device__ __forceinline__ void update_chunk(const UpdArgs& A, const UpdComp& C,
         vl[k][t] = (in && pa >= 1) ? __ldg(ps - da[t]) : 0.0;
       }
     }
-    old[k] = in ? state[e] : 0.0;
+    old[k] = (in && !INC) ? state[e] : 0.0;
     jv[k] = (DUAL && jhat && in) ? __ldg(jhat + e) : 0.0;
     // advance (x, y, z) by 256 elements
     x += sx;
@@ -356,7 +357,7 @@ void launch_update(int pro, const SweepArgs& a, cudaStream_t st) {
   for (int c = 0; c < 3; ++c) {
     UpdComp& C = U.c[c];
     C.state = a.comp[c].in;
-    C.jhat = (pro == PRO_AMPERE) ? a.pro.jhat[c] : nullptr;
+    C.jhat = (pro == PRO_AMPERE || pro == PRO_AMPERE_INC) ? a.pro.jhat[c] : nullptr;
     C.X = a.comp[c].ext[0];
     C.Y = a.comp[c].ext[1];
     C.N = a.comp[c].ext[0] * a.comp[c].ext[1] * a.comp[c].ext[2];
@@ -399,13 +400,17 @@ void launch_update(int pro, const SweepArgs& a, cudaStream_t st) {
 #define SGM_UPD(UV, MB)                                                         \
   if (UU == UV && minb == MB) {                                                 \
     if (pro == PRO_AMPERE) launch(update_kernel<PRO_AMPERE, UV, MB>);           \
-    else launch(update_kernel<PRO_FARADAY, UV, MB>);                            \
+    else if (pro == PRO_FARADAY) launch(update_kernel<PRO_FARADAY, UV, MB>);    \
+    else if (pro == PRO_AMPERE_INC) launch(update_kernel<PRO_AMPERE_INC, 4, 1>); \
+    else launch(update_kernel<PRO_FARADAY_INC, 4, 1>);                          \
     return;                                                                     \
   }
   SGM_UPD(4, 1) SGM_UPD(8, 1) SGM_UPD(4, 4) SGM_UPD(8, 2) SGM_UPD(2, 4)
 #undef SGM_UPD
   if (pro == PRO_AMPERE) launch(update_kernel<PRO_AMPERE, 4, 1>);
-  else launch(update_kernel<PRO_FARADAY, 4, 1>);
+  else if (pro == PRO_FARADAY) launch(update_kernel<PRO_FARADAY, 4, 1>);
+  else if (pro == PRO_AMPERE_INC) launch(update_kernel<PRO_AMPERE_INC, 4, 1>);
+  else launch(update_kernel<PRO_FARADAY_INC, 4, 1>);
 }
 
 void launch_curl(int kind, const double* const src[3], const int sext[3][3], double* const dst[3],

@@ -22,12 +22,15 @@ struct SweepComp {
   const double* dline[2];
   int axis;           // strided passes: this component's sweep axis (1 or 2); 0 = SweepArgs::axis
   int cidx;           // component index 0..2 of the form (fused update: which curl component)
+  int accum;          // 1: out += scale * result (the (e,h)-state increments), 0: out = scale * result
 };
 
 // Element-wise state update of a half step (launch_update):
 //   AMPERE : in[c] += dt * ((D~1 src)_c - s * jhat[c])   (eq. discrete2_ampere)
 //   FARADAY: in[c] -= dt * (D1 src)_c                    (eq. discrete2_faraday)
-enum Prologue { PRO_NONE = 0, PRO_AMPERE = 1, PRO_FARADAY = 2 };
+//   AMPERE_INC / FARADAY_INC: the increments alone, in[c] = dt ((D~1 src)_c - s jhat[c]) and
+//   in[c] = -dt (D1 src)_c (the (e,h)-state step, sgm_step_eh; in[c] is a workspace array)
+enum Prologue { PRO_NONE = 0, PRO_AMPERE = 1, PRO_FARADAY = 2, PRO_AMPERE_INC = 3, PRO_FARADAY_INC = 4 };
 
 struct PrologueArgs {
   const double* src[3];  // h components (AMPERE) or e components (FARADAY)

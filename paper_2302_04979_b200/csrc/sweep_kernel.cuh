@@ -433,7 +433,8 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
     }
     // ---- phase E: scaled store (constant component scale times optional per-line diagonals)
     const double sc = C.scale;
-    const bool unit = (sc == 1.0) && !C.dline[0] && !C.dline[1];
+    const bool acc = C.accum != 0;  // out += scale * result (the (e,h)-state increments)
+    const bool unit = (sc == 1.0) && !C.dline[0] && !C.dline[1] && !acc;
     double scq[LPT];
 #pragma unroll
     for (int q = 0; q < LPT; ++q) {
@@ -455,7 +456,10 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
           if (l < g.nlines) {
             double* dst = C.out + line_base(g, 0, l) + long(r0) * g.gs;
             const long gs = g.gs;
-            if (r0 + SEG <= L && unit) {
+            if (acc) {
+              for (int k = 0; k < SEG; ++k, dst += gs)
+                if (r0 + k < L) *dst = fma(scq[q], v[k][q], *dst);
+            } else if (r0 + SEG <= L && unit) {
 #pragma unroll
               for (int k = 0; k < SEG; ++k, dst += gs) *dst = v[k][q];
             } else if (r0 + SEG <= L) {
@@ -471,13 +475,22 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
       }
     } else {
       if (!solve) pipe::bar_sync(pipe::kBarCons, NC * 32);  // every halo read before in-place writes
-      if (live) {
+      if (live && !acc) {
 #pragma unroll
         for (int q = 0; q < LPT; ++q) {
           double* cw = const_cast<double*>(cp[q]);
 #pragma unroll
           for (int k = 0; k < SEG; ++k)
             if (r0 + SEG <= L || r0 + k < L) cw[k] = scq[q] * v[k][q];
+        }
+      } else if (live) {
+        // accumulate ((e,h)-state increments): add the old output line (global, this CTA's lines)
+        for (int q = 0; q < LPT; ++q) {
+          double* cw = const_cast<double*>(cp[q]);
+          const int l = min(l0 + lane + 32 * q, g.nlines - 1);
+          const double* prev = C.out + long(l) * g.rowlen + r0;
+          for (int k = 0; k < SEG; ++k)
+            if (r0 + k < L) cw[k] = fma(scq[q], v[k][q], prev[k]);
         }
       }
       if (bulk) {
