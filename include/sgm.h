@@ -158,8 +158,8 @@ sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h,
    (the Petrov-Galerkin form in E_h, H_h), so d and b need not be stored: two state
    vectors instead of four.  e at t_n and h at t_{n+1/2} on entry, advanced by n_steps dt on exit;
    results equal sgm_step's e, h up to rounding.  Scheme 2 only (SGM_E_UNSUPPORTED otherwise); the
-   energy of eq. P:L240 needs d, b (not available here).  Other arguments as sgm_step.  Async;
-   direct enqueue (no graph). */
+   energy of eq. P:L240 needs d, b (not available here).  Other arguments, graph replay and errors
+   as sgm_step.  Async. */
 sgm_status sgm_step_eh(sgm_plan plan, double* e, double* h, const double* j_hat, const double* j_amp,
                        double dt, int n_steps, void* workspace, size_t ws_bytes, void* stream);
 

@@ -59,12 +59,14 @@ sgm_status cuda_check(Plan* P, const char* where) {
 
 // Drop the captured graphs (their launches embed weights, tables, options)
 void drop_graphs(Plan& P) {
-  if (!(P.graph_exec || P.graph_exec_c) || P.device < 0) return;
+  if (!(P.graph_exec || P.graph_exec_c || P.graph_exec_e) || P.device < 0) return;
   DeviceGuard g(P.device);
   if (P.graph_exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P.graph_exec));
   if (P.graph_exec_c) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P.graph_exec_c));
+  if (P.graph_exec_e) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P.graph_exec_e));
   P.graph_exec = nullptr;
   P.graph_exec_c = nullptr;
+  P.graph_exec_e = nullptr;
 }
 
 // the caller is capturing `st` into its own graph: enqueue directly (no nested capture)
@@ -1353,6 +1355,38 @@ sgm_status sgm_step_eh(sgm_plan plan, double* e, double* h, const double* j_hat,
   if ((s = ws_carve(*P, workspace, ws_bytes, w)) != SGM_OK) return s;
   DeviceGuard g(P->device);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (n_steps == 0) return SGM_OK;
+  // one step captured into a CUDA graph and replayed, as sgm_step
+  const bool use_graph = !P->profiling && stream != nullptr && P->graph_enabled && !(P->opts & SGM_OPT_NO_GRAPH) &&
+                         (j_amp == nullptr || n_steps == 1) && !stream_capturing(st);
+  if (use_graph) {
+    const GraphKey key{nullptr, e, nullptr, h, j_hat, j_amp, dt, 1, workspace};
+    if (!(P->graph_exec_e && P->graph_key_e == key)) {
+      if (P->graph_exec_e) {
+        cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec_e));
+        P->graph_exec_e = nullptr;
+      }
+      cudaGraph_t graph = nullptr;
+      if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
+        return cuda_check(P, "sgm_step_eh: begin capture");
+      P->launch_fail = 0;
+      half_step_eh(*P, 0, e, h, j_hat, j_amp, dt, w, st);
+      half_step_eh(*P, 1, e, h, j_hat, j_amp, dt, w, st);
+      if (cudaStreamEndCapture(st, &graph) != cudaSuccess) return cuda_check(P, "sgm_step_eh: end capture");
+      if (P->launch_fail) {
+        cudaGraphDestroy(graph);
+        return cuda_check(P, "sgm_step_eh");
+      }
+      cudaGraphExec_t exec = nullptr;
+      const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ie != cudaSuccess) return cuda_check(P, "sgm_step_eh: graph instantiate");
+      P->graph_exec_e = exec;
+      P->graph_key_e = key;
+    }
+    for (int k = 0; k < n_steps; ++k) cudaGraphLaunch(static_cast<cudaGraphExec_t>(P->graph_exec_e), st);
+    return cuda_check(P, "sgm_step_eh (graph)");
+  }
   for (int k = 0; k < n_steps; ++k) {
     const double* sp = j_amp ? j_amp + k : nullptr;
     half_step_eh(*P, 0, e, h, j_hat, sp, dt, w, st);

@@ -124,6 +124,8 @@ struct Plan {
   std::mutex fork_mu;
   void* graph_exec = nullptr;         // cudaGraphExec_t of the last captured sgm_step call
   GraphKey graph_key{};
+  void* graph_exec_e = nullptr;       // ... of the last captured sgm_step_eh call
+  GraphKey graph_key_e{};
   void* graph_exec_c = nullptr;       // ... of the last captured sgm_step_composed call
   GraphKey graph_key_c{};
   std::vector<double> graph_w_c;      // its weights
