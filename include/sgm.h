@@ -152,6 +152,34 @@ sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h,
                     const double* j_hat, const double* j_amp, double dt, int n_steps,
                     void* workspace, size_t ws_bytes, void* stream);
 
+/* Inhomogeneous Dirichlet data for E (sec. 3.5; the coaxial cable, P:L837-849;
+   SURVEY 8(f) NEXT #2; reading Z29 in DESIGN.md).  E_h = E_{h,0} + E_{h,b} with the lifting
+   E_{h,b}(t) = g(t) e^_b in X^1_h (boundary functions only) and data separable in space and time
+   (P:L838): the boundary contributions are computed once by the caller and enter every step as
+   scaled vectors ("multiplied by a known function of time at each time step"):
+     (K1)_0 e = M~2 d - (K1)_b e_b        ->  e = K1^{-1} M~2_{1/eps} d - g_{n+1} w_e
+     B_h in X^2_h, D1 : X^1_h -> X^2_h     ->  b_0 <- b_0 - dt (D1 e + g_{n+1} c_b)
+                                               b_bnd = b_bnd(0) + beta_{n+1} u_b (implicit)
+     M2 with columns in X^2_h              ->  h = K~1^{-1} M2_{1/mu} b_0 + q0 + beta_{n+1} q1
+   with w_e = (K1)_0^{-1} (K1)_b e^_b (len N_e), c_b / u_b = the interior / boundary rows of D1 e^_b
+   (c_b len N_b; the tangential curl on a face involves only that face's coefficients, so interior e
+   never reaches b_bnd), q0 = K~1^{-1} M2_{0b} b_bnd(0), q1 = K~1^{-1} M2_{0b} u_b (len N_h), and per
+   step k of the call g[k] = g(t_{n+1}), beta[k] = -dt sum_{m <= n+1} g(t_m) (device arrays of
+   n_steps).  d, e, b, h are the interior (X^1_{h,0}, X^2_{h,0}) vectors of sgm_step.  NULL
+   vectors are zero terms (g, beta required).  Scheme 2; the update is not fused (SGM_OPT_FUSED is
+   ignored here); direct enqueue.  Other arguments and errors as sgm_step. */
+typedef struct {
+  const double* w_e;   /* device, N_e */
+  const double* c_b;   /* device, N_b */
+  const double* q0;    /* device, N_h */
+  const double* q1;    /* device, N_h */
+  const double* g;     /* device, n_steps */
+  const double* beta;  /* device, n_steps */
+} sgm_lifting;
+sgm_status sgm_step_lifted(sgm_plan plan, double* d, double* e, double* b, double* h,
+                           const double* j_hat, const double* j_amp, const sgm_lifting* lift,
+                           double dt, int n_steps, void* workspace, size_t ws_bytes, void* stream);
+
 /* The (e,h)-state variant of the step (reading Z30 in DESIGN.md): with
    e = K1^{-1} M~2_{1/eps} d and h = K~1^{-1} M2_{1/mu} b, one step of sgm_step is exactly
      e <- e + K1^{-1} M~2_{1/eps} (dt (D~1 h - s_k j^))      h <- h - K~1^{-1} M2_{1/mu} (dt D1 e)

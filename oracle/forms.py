@@ -23,6 +23,8 @@ def component_spaces(cplx, k):
     """Per-component triples (space_x, space_y, space_z) of the univariate spaces."""
     if cplx == "primal":
         P, L = "Sp", "Sp1"       # degree p (trimmed B-splines), degree p-1 (CS)
+    elif cplx == "primalF":
+        P, L = "SpF", "Sp1"      # the full X^k_h (untrimmed S_p), for the lifting (P:L450-490)
     elif cplx == "dual":
         P, L = "Dp1", "Dp2"      # degree p-1 (B-splines), degree p-2 (CS)
     else:
@@ -96,6 +98,8 @@ def incidence(cplx, k, p, n):
     Univariate factors (reading Z3): with the CS bases,
       primal  S_p(trimmed, dim a) -> S_{p-1} (dim b):  (du)_j = u_j - u_{j-1},  u_{-1} = u_a = 0
       dual    S_{p-1}    (dim b) -> S_{p-2} (dim a):  (dv)_j = v_{j+1} - v_j
+      primalF S_p(full, dim a+2)  -> S_{p-1} (dim b):  (dU)_j = U_{j+1} - U_j  (U_0, U_{a+1}: the
+              boundary functions; the trimmed rule is this one with U_0 = U_{a+1} = 0)
     """
     n = _n3(n)
     sh_in = component_shapes(cplx, k, p, n)

@@ -99,15 +99,17 @@ def gauss_rule(n, Q):
 
 # --- the four univariate spaces of sec. 4.1 -------------------------------------
 
-SPACES = ("Sp", "Sp1", "Dp1", "Dp2")
+SPACES = ("Sp", "Sp1", "Dp1", "Dp2", "SpF")
 """Sp  = primal S_p(Xi) trimmed, B-splines         (dim a = n+p-2)
    Sp1 = primal S_{p-1}(Xi') CS                     (dim b = n+p-1)
    Dp1 = dual   S_{p-1}(Xi') B-splines              (dim b)
-   Dp2 = dual   S_{p-2}(Xi'') CS                    (dim a)"""
+   Dp2 = dual   S_{p-2}(Xi'') CS                    (dim a)
+   SpF = primal S_p(Xi) untrimmed, B-splines       (dim a + 2: the full X^k_h of the lifting,
+         P:L450-490, whose first and last functions carry the boundary values)"""
 
 
 def space_dim(space, p, n):
-    return {"Sp": n + p - 2, "Sp1": n + p - 1, "Dp1": n + p - 1, "Dp2": n + p - 2}[space]
+    return {"Sp": n + p - 2, "Sp1": n + p - 1, "Dp1": n + p - 1, "Dp2": n + p - 2, "SpF": n + p}[space]
 
 
 def space_values(space, p, n, x):
@@ -117,6 +119,8 @@ def space_values(space, p, n, x):
     X2 = derived_knots(X1)
     if space == "Sp":
         return bspline_values(X, p, x)[:, 1:-1]
+    if space == "SpF":
+        return bspline_values(X, p, x)
     if space == "Sp1":
         return bspline_values(X1, p - 1, x) * cs_scale(X1, p - 1)[None, :]
     if space == "Dp1":

@@ -26,6 +26,12 @@ c_int, c_double, c_size_t, c_void_p = ctypes.c_int, ctypes.c_double, ctypes.c_si
 c_dp = ctypes.POINTER(ctypes.c_double)
 
 
+class sgm_lifting(ctypes.Structure):
+    """Time-separable inhomogeneous Dirichlet data (sgm.h, sgm_step_lifted): device pointers."""
+    _fields_ = [("w_e", c_void_p), ("c_b", c_void_p), ("q0", c_void_p), ("q1", c_void_p), ("g", c_void_p),
+                ("beta", c_void_p)]
+
+
 class sgm_plan_desc(ctypes.Structure):
     _fields_ = [("n_el", c_int * 3), ("degree", c_int), ("geom_ctrl", c_void_p),
                 ("quad_points", c_int), ("device", c_int), ("geom_weights", c_void_p)]
@@ -58,6 +64,8 @@ _SIGS = {
     "sgm_workspace_bytes": [c_void_p, ctypes.POINTER(c_size_t)],
     "sgm_step": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int,
                  c_void_p, c_size_t, c_void_p],
+    "sgm_step_lifted": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double,
+                        c_int, c_void_p, c_size_t, c_void_p],
     "sgm_step_eh": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int, c_void_p, c_size_t, c_void_p],
     "sgm_step_host": [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_int,
                       c_void_p],
@@ -287,6 +295,15 @@ class Plan:
         w = self.workspace() if ws is None else ws
         check(sgm_step(self.h, _ptr(d), _ptr(e), _ptr(b), _ptr(h), _ptr(j_hat), _ptr(j_amp), float(dt),
                        int(n_steps), _ptr(w), w.numel() * 8, _stream(stream)), "sgm_step")
+
+    def step_lifted(self, d, e, b, h, dt, n_steps, g, beta, w_e=None, c_b=None, q0=None, q1=None, j_hat=None,
+                    j_amp=None, stream=None, ws=None):
+        """n_steps lifted steps (sgm_step_lifted): g, beta device arrays of n_steps; the precomputed
+        lifting vectors w_e (N_e), c_b (N_b), q0, q1 (N_h) as device tensors or None."""
+        w = self.workspace() if ws is None else ws
+        L = sgm_lifting(_ptr(w_e), _ptr(c_b), _ptr(q0), _ptr(q1), _ptr(g), _ptr(beta))
+        check(sgm_step_lifted(self.h, _ptr(d), _ptr(e), _ptr(b), _ptr(h), _ptr(j_hat), _ptr(j_amp), ctypes.byref(L),
+                              float(dt), int(n_steps), _ptr(w), w.numel() * 8, _stream(stream)), "sgm_step_lifted")
 
     def step_eh(self, e, h, dt, n_steps=1, j_hat=None, j_amp=None, stream=None, ws=None):
         """The (e,h)-state variant (sgm_step_eh): only e and h are stored and advanced."""

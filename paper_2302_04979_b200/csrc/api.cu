@@ -161,10 +161,18 @@ struct ProfScope {
   }
 };
 
+// Affine terms of a Hodge star's last sweeps (sgm_step_lifted): out += sum_i c[i] * (*s[i] or 1) * w[i]
+// (w[i]: whole-form base pointers; per-component offsets are added by the launchers)
+struct Affine {
+  const double* w[2];
+  const double* s[2];
+  double c[2];
+};
+
 // One axis pass over the 3 components of a form (kind 0: e/d shapes, 1: b/h shapes).
 void sweep_pass(const Plan& P, int kind, int axis, double* const in[3], double* const out[3], int op_own,
                 int op_oth, const double* scale, bool band, bool solve, cudaStream_t st, int reverse = 0,
-                int accum = 0) {
+                int accum = 0, const Affine* aff = nullptr) {
   SweepArgs a;
   std::memset(&a, 0, sizeof(a));
   a.ncomp = 3;
@@ -186,6 +194,12 @@ void sweep_pass(const Plan& P, int kind, int axis, double* const in[3], double* 
     a.comp[c].tslot = own_or(axis, c, 0, 1);
     a.comp[c].scale = scale ? scale[c] : 1.0;
     a.comp[c].accum = accum;
+    if (aff)
+      for (int t = 0; t < 2; ++t) {
+        a.comp[c].aw[t] = aff->w[t] ? aff->w[t] + comp_off(P, kind, c) : nullptr;
+        a.comp[c].as[t] = aff->s[t];
+        a.comp[c].ac[t] = aff->c[t];
+      }
   }
   if (!launch_sweep(P.p, P.seg[axis], a, st)) P.launch_fail = 1;
 }
@@ -205,6 +219,7 @@ struct PassComp {
   int dg[3];          // per axis: -1 = no diagonal, else the diag_factor kind applied along it
   double scale;
   int accum = 0;      // 1: out += scale * result ((e,h)-state increments)
+  const Affine* aff = nullptr;  // affine store terms (last sweeps of a lifted star)
 };
 
 // Components of one launch share the line mode (x, or strided y/z) and the padded table rows and
@@ -255,6 +270,12 @@ void sweep_pass_list(const Plan& P, int kind, const PassComp* pc, int n, cudaStr
     C.axis = axis;
     C.scale = q.scale;
     C.accum = q.accum;
+    if (q.aff)
+      for (int t = 0; t < 2; ++t) {
+        C.aw[t] = q.aff->w[t] ? q.aff->w[t] + comp_off(P, kind, q.c) : nullptr;
+        C.as[t] = q.aff->s[t];
+        C.ac[t] = q.aff->c[t];
+      }
     C.dline[0] = q.dg[t0] >= 0 ? diag_factor(P, t0, q.dg[t0]) : nullptr;
     C.dline[1] = q.dg[t1] >= 0 ? diag_factor(P, t1, q.dg[t1]) : nullptr;
   }
@@ -402,7 +423,7 @@ void fork_join(Plan& P, cudaStream_t st, F1&& f1, F2&& f2) {
 //   mu  (kind 1): component c is swept (Gamma_B^{p}, LU Hat G^T) along axis c only and scaled by
 //                 s along the other two: strided pass {2 along z, 1 along y} (or two passes), x pass {0}.
 void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* t, cudaStream_t st,
-                        const double* scale = nullptr, int accum = 0) {
+                        const double* scale = nullptr, int accum = 0, const Affine* aff = nullptr) {
   const int kind = (which == SGM_MASS_EPS) ? 0 : 1;
   struct {
     const double* scale;
@@ -422,9 +443,9 @@ void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* 
       PassComp a3[3] = {{2, 0, X[0], T[0], op, {-1, -1, -1}, 1.0},
                         {2, 1, X[1], T[1], op, {-1, -1, -1}, 1.0},
                         {1, 2, X[2], T[2], op, {-1, -1, -1}, 1.0}};
-      PassComp b1[1] = {{1, 0, T[0], Y[0], op, {0, -1, -1}, M.scale[0], accum}};
-      PassComp c2[2] = {{0, 1, T[1], Y[1], op, {-1, 0, -1}, M.scale[1], accum},
-                        {0, 2, T[2], Y[2], op, {-1, -1, 0}, M.scale[2], accum}};
+      PassComp b1[1] = {{1, 0, T[0], Y[0], op, {0, -1, -1}, M.scale[0], accum, aff}};
+      PassComp c2[2] = {{0, 1, T[1], Y[1], op, {-1, 0, -1}, M.scale[1], accum, aff},
+                        {0, 2, T[2], Y[2], op, {-1, -1, 0}, M.scale[2], accum, aff}};
       { ProfScope ps(P, kz, st); sweep_pass_list(P, 0, a3, 3, st, 1); }
       // x side: components 1, 2 of e/d, x-extent a (P.ax[0].a)
       const Share sb = strided_share(P, 1, 1, 2, (P.ax[0].a % 2) == 0), sc = {sb.n - sb.k, sb.n};
@@ -433,18 +454,18 @@ void hodge_star_reduced(Plan& P, int which, const double* x, double* y, double* 
       return;
     }
     PassComp z[2] = {{2, 0, X[0], T[0], op, {-1, -1, -1}, 1.0}, {2, 1, X[1], T[1], op, {-1, -1, -1}, 1.0}};
-    PassComp yy[2] = {{1, 0, T[0], Y[0], op, {0, -1, -1}, M.scale[0], accum}, {1, 2, X[2], T[2], op, {-1, -1, -1}, 1.0}};
-    PassComp xx[2] = {{0, 1, T[1], Y[1], op, {-1, 0, -1}, M.scale[1], accum},
-                      {0, 2, T[2], Y[2], op, {-1, -1, 0}, M.scale[2], accum}};
+    PassComp yy[2] = {{1, 0, T[0], Y[0], op, {0, -1, -1}, M.scale[0], accum, aff}, {1, 2, X[2], T[2], op, {-1, -1, -1}, 1.0}};
+    PassComp xx[2] = {{0, 1, T[1], Y[1], op, {-1, 0, -1}, M.scale[1], accum, aff},
+                      {0, 2, T[2], Y[2], op, {-1, -1, 0}, M.scale[2], accum, aff}};
     { ProfScope ps(P, kz, st); sweep_pass_list(P, 0, z, 2, st, 1); }
     { ProfScope ps(P, ky, st); sweep_pass_list(P, 0, yy, 2, st, 0); }
     { ProfScope ps(P, kx, st); sweep_pass_list(P, 0, xx, 2, st, 1); }
   } else {
     // scheme 2: Hat G^{-T} Gamma_B^p; scheme 1: Gamma_C^{p-2}^{-1} Hat G (other axes: diag(s) in both)
     const int op = P.scheme == 1 ? OP_S1_MU_OWN : OP_MU_OWN;
-    PassComp z[1] = {{2, 2, X[2], Y[2], op, {1, 1, -1}, M.scale[2], accum}};
-    PassComp yy[1] = {{1, 1, X[1], Y[1], op, {1, -1, 1}, M.scale[1], accum}};
-    PassComp xx[1] = {{0, 0, X[0], Y[0], op, {-1, 1, 1}, M.scale[0], accum}};
+    PassComp z[1] = {{2, 2, X[2], Y[2], op, {1, 1, -1}, M.scale[2], accum, aff}};
+    PassComp yy[1] = {{1, 1, X[1], Y[1], op, {1, -1, 1}, M.scale[1], accum, aff}};
+    PassComp xx[1] = {{0, 0, X[0], Y[0], op, {-1, 1, 1}, M.scale[0], accum, aff}};
     if (mu_merged(P)) {
       // z-lines of component 2 and y-lines of component 1 in one strided launch; the x-lines of
       // component 0 (independent) concurrently on the plan-owned stream when forking is enabled
@@ -574,9 +595,9 @@ PrologueArgs make_pro(const Plan& P, int src_kind, const double* src, const doub
     pa.src[c] = S[c];
     comp_shape(P, src_kind, c, pa.sext[c]);
   }
-  if (jhat) {
+  if (jhat) {  // the source of the updated state: j^ (Ampere, e-shaped) or c_b (Faraday, b-shaped)
     double* J[3];
-    comps_of(P, 0, jhat, J);
+    comps_of(P, 1 - src_kind, jhat, J);
     for (int c = 0; c < 3; ++c) pa.jhat[c] = J[c];
   }
   pa.s_ptr = s_ptr;
@@ -862,8 +883,12 @@ inline Plan* PL(sgm_plan p) { return reinterpret_cast<Plan*>(p); }
 // one half step on device pointers (SURVEY 8(a) a1-a3 for half 0, a4-a6 for half 1):
 //   half 0 (eps, kind 0): d <- d + tau (D~1 h - s j); e <- K1^{-1} M~2_{1/eps} d
 //   half 1 (mu,  kind 1): b <- b - tau D1 e;          h <- K~1^{-1} M2_{1/mu} b
+// lift (sgm_step_lifted, step k of the call): the lifted star and Faraday terms of the time-separable
+// inhomogeneous Dirichlet data (reading Z29):
+//   e <- S_eps d - g_k w_e;   b <- b - tau (D1 e + g_k c_b);   h <- S_mu b + q0 + beta_k q1
 void half_step(Plan& P, int half, double* d, double* e, double* b, double* h, const double* jhat,
-               const double* s_ptr, double tau, const WS& w, cudaStream_t st) {
+               const double* s_ptr, double tau, const WS& w, cudaStream_t st, const sgm_lifting* lift = nullptr,
+               int k = 0) {
   double *D[3], *E[3], *B[3], *H[3], *T[3], *Rr[3];
   comps_of(P, 0, d, D);
   comps_of(P, 0, e, E);
@@ -877,12 +902,23 @@ void half_step(Plan& P, int half, double* d, double* e, double* b, double* h, co
   const int ky = half == 0 ? SGM_K_EPS_Y : SGM_K_MU_Y, kz = half == 0 ? SGM_K_EPS_X : SGM_K_MU_X;
   double** state = half == 0 ? D : B;
   double** outv = half == 0 ? E : H;
-  PrologueArgs pa = half == 0 ? make_pro(P, 1, h, jhat, s_ptr, tau) : make_pro(P, 0, e, nullptr, nullptr, tau);
+  PrologueArgs pa = half == 0 ? make_pro(P, 1, h, jhat, s_ptr, tau)
+                               : make_pro(P, 0, e, lift ? lift->c_b : nullptr, lift ? lift->g + k : nullptr, tau);
   const MassData& M = P.mass[mass];
   comps_of(P, kind, w.t, T);
+  Affine af{};
+  const Affine* aff = nullptr;
+  if (lift && half == 0 && lift->w_e) {
+    af = Affine{{lift->w_e, nullptr}, {lift->g + k, nullptr}, {-1.0, 0.0}};
+    aff = &af;
+  } else if (lift && half == 1 && (lift->q0 || lift->q1)) {
+    af = Affine{{lift->q0, lift->q1}, {nullptr, lift->beta + k}, {1.0, 1.0}};
+    aff = &af;
+  }
   // fused schedule (SGM_OPT_FUSED): the update runs inside the first sweep launch of the half step
   // (falls back to the separate update kernel when the fused kernel has no fitting configuration)
-  if (M.kind == HODGE_SEPARABLE && fused_sched(P) && star_fused(P, mass, state[0], outv[0], w.t, st, pa)) return;
+  if (!lift && M.kind == HODGE_SEPARABLE && fused_sched(P) && star_fused(P, mass, state[0], outv[0], w.t, st, pa))
+    return;
   SweepArgs a;
   std::memset(&a, 0, sizeof(a));
   a.ncomp = 3;
@@ -895,20 +931,20 @@ void half_step(Plan& P, int half, double* d, double* e, double* b, double* h, co
   if (P.scheme == 1 && P.mass1[mass].kind != HODGE_SEPARABLE) {
     { ProfScope ps(P, SGM_K_HODGE_GENERAL, st); pcg_star(P, mass, state[0], outv[0], w, st); }
   } else if (M.kind == HODGE_SEPARABLE && reduced_sched(P)) {
-    hodge_star_reduced(P, mass, state[0], outv[0], w.t, st);
+    hodge_star_reduced(P, mass, state[0], outv[0], w.t, st, nullptr, 0, aff);
   } else if (M.kind == HODGE_SEPARABLE) {
     // streaming update kernel, then the three mass . solve sweeps (z, y, x); snake order: update
     // forward, z backward, y forward, x backward (each kernel starts on the tiles its predecessor
     // wrote last)
     { ProfScope ps(P, kx, st); sweep_pass(P, kind, 2, state, T, own, oth, nullptr, true, true, st, 1); }
     { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, true, true, st, 0); }
-    { ProfScope ps(P, kz, st); sweep_pass(P, kind, 0, T, outv, own, oth, M.scale, true, true, st, 1); }
+    { ProfScope ps(P, kz, st); sweep_pass(P, kind, 0, T, outv, own, oth, M.scale, true, true, st, 1, 0, aff); }
   } else {
     { ProfScope ps(P, SGM_K_HODGE_GENERAL, st); mass_apply(P, mass, state[0], w.r, w.t, st); }
     comps_of(P, kind, w.r, Rr);
     { ProfScope ps(P, SGM_K_SOLVE_Z, st); sweep_pass(P, kind, 2, Rr, T, own, oth, nullptr, false, true, st); }
     { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, false, true, st); }
-    { ProfScope ps(P, kz, st); sweep_pass(P, kind, 0, T, outv, own, oth, nullptr, false, true, st); }
+    { ProfScope ps(P, kz, st); sweep_pass(P, kind, 0, T, outv, own, oth, nullptr, false, true, st, 0, 0, aff); }
   }
 }
 
@@ -1338,6 +1374,35 @@ sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h, c
   }
   for (int k = 0; k < n_steps; ++k) step_once(*P, d, e, b, h, j_hat, j_amp ? j_amp + k : nullptr, dt, w, st);
   return cuda_check(P, "sgm_step");
+}
+
+sgm_status sgm_step_lifted(sgm_plan plan, double* d, double* e, double* b, double* h, const double* j_hat,
+                           const double* j_amp, const sgm_lifting* lift, double dt, int n_steps, void* workspace,
+                           size_t ws_bytes, void* stream) {
+  sgm_status s = check_plan(plan, true);
+  if (s != SGM_OK) return s;
+  Plan* P = PL(plan);
+  if (!lift || !lift->g || !lift->beta) return fail(SGM_E_INVALID_ARG, "lifting descriptor with g and beta required");
+  const double* v[6] = {lift->w_e, lift->c_b, lift->q0, lift->q1, lift->g, lift->beta};
+  for (const double* x : v)
+    if (x && !aligned8(x)) return fail(SGM_E_INVALID_ARG, "misaligned lifting vector");
+  if (!d || !e || !b || !h || !aligned8(d) || !aligned8(e) || !aligned8(b) || !aligned8(h))
+    return fail(SGM_E_INVALID_ARG, "state pointers must be non-NULL and 8-byte aligned");
+  if ((j_hat && !aligned8(j_hat)) || (j_amp && !aligned8(j_amp))) return fail(SGM_E_INVALID_ARG, "misaligned source");
+  if (!std::isfinite(dt)) return fail(SGM_E_INVALID_ARG, "dt must be finite");
+  if (n_steps < 0) return fail(SGM_E_INVALID_ARG, "n_steps < 0");
+  if (d == e || d == b || d == h || e == b || e == h || b == h) return fail(SGM_E_INVALID_ARG, "state vectors alias");
+  if (P->scheme != 2) return fail(SGM_E_UNSUPPORTED, "the lifted step is built for the second scheme");
+  WS w;
+  if ((s = ws_carve(*P, workspace, ws_bytes, w)) != SGM_OK) return s;
+  DeviceGuard g(P->device);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  for (int k = 0; k < n_steps; ++k) {
+    const double* sp = j_amp ? j_amp + k : nullptr;
+    half_step(*P, 0, d, e, b, h, j_hat, sp, dt, w, st, lift, k);
+    half_step(*P, 1, d, e, b, h, j_hat, sp, dt, w, st, lift, k);
+  }
+  return cuda_check(P, "sgm_step_lifted");
 }
 
 sgm_status sgm_step_eh(sgm_plan plan, double* e, double* h, const double* j_hat, const double* j_amp, double dt,

@@ -132,7 +132,7 @@ __device__ __forceinline__ void update_chunk(const UpdArgs& A, const UpdComp& C,
       }
     }
     old[k] = (in && !INC) ? state[e] : 0.0;
-    jv[k] = (DUAL && jhat && in) ? __ldg(jhat + e) : 0.0;
+    jv[k] = (jhat && in) ? __ldg(jhat + e) : 0.0;
     // advance (x, y, z) by 256 elements
     x += sx;
     const int cx = x >= X;
@@ -143,11 +143,11 @@ __device__ __forceinline__ void update_chunk(const UpdArgs& A, const UpdComp& C,
     z += sz + cy;
   }
   const double dt = A.dt;
-  const double sdt = (DUAL && jhat) ? dt * (A.s_ptr ? __ldg(A.s_ptr) : 1.0) : 0.0;
+  const double sdt = jhat ? dt * (A.s_ptr ? __ldg(A.s_ptr) : 1.0) : 0.0;
 #pragma unroll
   for (int k = 0; k < U; ++k) {
     const double cu = (vh[k][0] - vl[k][0]) - (vh[k][1] - vl[k][1]);
-    const double val = DUAL ? fma(-sdt, jv[k], fma(dt, cu, old[k])) : fma(-dt, cu, old[k]);
+    const double val = DUAL ? fma(-sdt, jv[k], fma(dt, cu, old[k])) : fma(-sdt, jv[k], fma(-dt, cu, old[k]));
     if (FULL || e0 + 256 * k < N) state[e0 + 256 * k] = val;
   }
 }
@@ -357,7 +357,7 @@ void launch_update(int pro, const SweepArgs& a, cudaStream_t st) {
   for (int c = 0; c < 3; ++c) {
     UpdComp& C = U.c[c];
     C.state = a.comp[c].in;
-    C.jhat = (pro == PRO_AMPERE || pro == PRO_AMPERE_INC) ? a.pro.jhat[c] : nullptr;
+    C.jhat = a.pro.jhat[c];  // Ampere: j^; Faraday: the lifting's interior curl c_b (sgm_step_lifted)
     C.X = a.comp[c].ext[0];
     C.Y = a.comp[c].ext[1];
     C.N = a.comp[c].ext[0] * a.comp[c].ext[1] * a.comp[c].ext[2];

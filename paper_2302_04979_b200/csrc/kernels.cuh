@@ -23,6 +23,11 @@ struct SweepComp {
   int axis;           // strided passes: this component's sweep axis (1 or 2); 0 = SweepArgs::axis
   int cidx;           // component index 0..2 of the form (fused update: which curl component)
   int accum;          // 1: out += scale * result (the (e,h)-state increments), 0: out = scale * result
+  // affine store terms (time-separable boundary data, sgm_step_lifted): out += sum_i ac[i] *
+  // (as[i] ? *as[i] : 1) * aw[i][same index]; aw[i] = null: no term
+  const double* aw[2];
+  const double* as[2];
+  double ac[2];
 };
 
 // Element-wise state update of a half step (launch_update):

@@ -434,7 +434,14 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
     // ---- phase E: scaled store (constant component scale times optional per-line diagonals)
     const double sc = C.scale;
     const bool acc = C.accum != 0;  // out += scale * result (the (e,h)-state increments)
-    const bool unit = (sc == 1.0) && !C.dline[0] && !C.dline[1] && !acc;
+    const bool aff = C.aw[0] != nullptr || C.aw[1] != nullptr;  // + affine boundary terms (lifting)
+    double af[2] = {0.0, 0.0};
+    if (aff) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        if (C.aw[i]) af[i] = C.ac[i] * (C.as[i] ? __ldg(C.as[i]) : 1.0);
+    }
+    const bool unit = (sc == 1.0) && !C.dline[0] && !C.dline[1] && !acc && !aff;
     double scq[LPT];
 #pragma unroll
     for (int q = 0; q < LPT; ++q) {
@@ -456,9 +463,15 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
           if (l < g.nlines) {
             double* dst = C.out + line_base(g, 0, l) + long(r0) * g.gs;
             const long gs = g.gs;
-            if (acc) {
+            if (acc || aff) {
+              const long off = dst - C.out;
               for (int k = 0; k < SEG; ++k, dst += gs)
-                if (r0 + k < L) *dst = fma(scq[q], v[k][q], *dst);
+                if (r0 + k < L) {
+                  double val = acc ? fma(scq[q], v[k][q], *dst) : scq[q] * v[k][q];
+                  if (C.aw[0]) val = fma(af[0], __ldg(C.aw[0] + off + k * gs), val);
+                  if (C.aw[1]) val = fma(af[1], __ldg(C.aw[1] + off + k * gs), val);
+                  *dst = val;
+                }
             } else if (r0 + SEG <= L && unit) {
 #pragma unroll
               for (int k = 0; k < SEG; ++k, dst += gs) *dst = v[k][q];
@@ -475,7 +488,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
       }
     } else {
       if (!solve) pipe::bar_sync(pipe::kBarCons, NC * 32);  // every halo read before in-place writes
-      if (live && !acc) {
+      if (live && !acc && !aff) {
 #pragma unroll
         for (int q = 0; q < LPT; ++q) {
           double* cw = const_cast<double*>(cp[q]);
@@ -484,13 +497,20 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
             if (r0 + SEG <= L || r0 + k < L) cw[k] = scq[q] * v[k][q];
         }
       } else if (live) {
-        // accumulate ((e,h)-state increments): add the old output line (global, this CTA's lines)
+        // accumulate ((e,h)-state increments: the old output line, global, this CTA's lines) and/or
+        // the affine boundary terms
         for (int q = 0; q < LPT; ++q) {
           double* cw = const_cast<double*>(cp[q]);
           const int l = min(l0 + lane + 32 * q, g.nlines - 1);
-          const double* prev = C.out + long(l) * g.rowlen + r0;
+          const long off = long(l) * g.rowlen + r0;
+          const double* prev = C.out + off;
           for (int k = 0; k < SEG; ++k)
-            if (r0 + k < L) cw[k] = fma(scq[q], v[k][q], prev[k]);
+            if (r0 + k < L) {
+              double val = acc ? fma(scq[q], v[k][q], prev[k]) : scq[q] * v[k][q];
+              if (C.aw[0]) val = fma(af[0], __ldg(C.aw[0] + off + k), val);
+              if (C.aw[1]) val = fma(af[1], __ldg(C.aw[1] + off + k), val);
+              cw[k] = val;
+            }
         }
       }
       if (bulk) {

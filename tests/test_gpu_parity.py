@@ -731,3 +731,50 @@ def test_eh_state_general_hodge():
     pl.step_eh(e, h, dt, 20)
     er, hr = tb.run_eh(e0, h0, dt, 20)
     assert rel(host(e), er) < 1e-10 and rel(host(h), hr) < 1e-10
+
+
+@pytest.mark.parametrize("n", [(3, 4, 2), (5, 6, 4)])
+def test_lifted_coax_tem_step(n):
+    """sgm_step_lifted on the coax (rational quarter annulus 1 < r < sqrt2; general Hodge with the
+    full metric) with the TEM mode's inhomogeneous Dirichlet data on the symmetry planes (lifting,
+    P:L450-490): 60 steps against the literal lifted tier A (full X^2_h, rectangular D1 / M2,
+    (K1)_0 e_0 = M~2 d - (K1)_b e_b); the time-separable vectors are the caller's one-time setup."""
+    from oracle import lifting as Lf
+    p, dt, K = 2, 2e-3, 60
+    A, st, g = Lf.coax_setup(p, n, dt)
+    V = Lf.lifting_vectors(A, st[2], dt)
+    gk = np.array([g((k + 1) * dt) for k in range(K)])
+    beta = -dt * np.cumsum(gk)
+    gg = A.ctrl
+    pl = S.Plan(n, p, geom_ctrl=gg.P, geom_weights=gg.w)
+    d, e, b, h = dev(st[0]), dev(st[1]), dev(st[2][A.b_int]), dev(st[3])
+    pl.step_lifted(d, e, b, h, dt, K, dev(gk), dev(beta), w_e=dev(V["w_e"]), c_b=dev(V["c_b"]),
+                   q0=dev(V["q0"]), q1=dev(V["q1"]))
+    ref = A.run(*st, dt, K, g)
+    for x, r in zip((d, e, b, h), (ref[0], ref[1], ref[2][A.b_int], ref[3])):
+        assert rel(host(x), r) < 1e-10
+
+
+def test_lifted_step_separable_cube():
+    """sgm_step_lifted on the identity cube (separable reduced stars: the affine terms ride on the
+    pipelined sweeps' stores) with synthetic lifting vectors, against the same recurrence in tier B."""
+    p, n, K, dt = 3, (7, 6, 5), 25, 0.01
+    pl = S.Plan(n, p)
+    tb = TierB(p, n)
+    g = np.random.default_rng(95)
+    st = _state(tb, 96)
+    st = (st[0], tb.hodge_eps(st[0]), st[2], tb.hodge_mu(st[2]))
+    w_e, c_b = g.standard_normal(tb.N_e), g.standard_normal(tb.N_h)
+    q0, q1 = g.standard_normal(tb.N_h), g.standard_normal(tb.N_h)
+    gk = np.cos(0.2 * np.arange(1, K + 1))
+    beta = -dt * np.cumsum(gk)
+    dv = [dev(x) for x in st]
+    pl.step_lifted(*dv, dt, K, dev(gk), dev(beta), w_e=dev(w_e), c_b=dev(c_b), q0=dev(q0), q1=dev(q1))
+    d, e, b, h = st
+    for k in range(K):
+        d = d + dt * forms.join(curl_dual(tb.split_h(h)))
+        e = tb.hodge_eps(d) - gk[k] * w_e
+        b = b - dt * (forms.join(curl_primal(tb.split_e(e))) + gk[k] * c_b)
+        h = tb.hodge_mu(b) + q0 + beta[k] * q1
+    for x, r in zip(dv, (d, e, b, h)):
+        assert rel(host(x), r) < 1e-10
