@@ -11,8 +11,11 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std
          "-Xcompiler", "-fPIC,-fopenmp", "-shared", "-lgomp"]
 
 
+MARK = os.path.join(HERE, "libsgm.tuning")  # present while libsgm.so is a tuning build
+
+
 def needs_build():
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or os.path.exists(MARK):
         return True
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
@@ -20,15 +23,21 @@ def needs_build():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False):
+def build(force=False, verbose=False, tuning=None):
     """Compile every translation unit to an object in parallel (the sweep instantiations are split
-    per degree), then link the shared library."""
+    per degree), then link the shared library.  tuning=True (or SGM_BUILD_TUNING=1) compiles the
+    -DSGM_TUNING variant whose launchers read tuning knobs from the environment -- for experiments
+    only; the product library is the default build (tests/test_abi.py refuses a tuning build)."""
+    if tuning is None:
+        tuning = os.environ.get("SGM_BUILD_TUNING", "0") == "1"
+    if tuning:
+        force = True
     if not force and not needs_build():
         return LIB
     from concurrent.futures import ThreadPoolExecutor
     objdir = os.path.join(HERE, "_obj")
     os.makedirs(objdir, exist_ok=True)
-    cflags = [f for f in FLAGS if f not in ("-shared", "-lgomp")]
+    cflags = [f for f in FLAGS if f not in ("-shared", "-lgomp")] + (["-DSGM_TUNING"] if tuning else [])
 
     def compile_one(src):
         obj = os.path.join(objdir, src + ".o")
@@ -46,6 +55,10 @@ def build(force=False, verbose=False):
         print(" ".join(cmd))
     subprocess.run(cmd, check=True, cwd=CSRC)
     os.replace(LIB + ".tmp", LIB)
+    if tuning:
+        open(MARK, "w").write("tuning build (-DSGM_TUNING)\n")
+    elif os.path.exists(MARK):
+        os.remove(MARK)
     return LIB
 
 
