@@ -284,9 +284,11 @@ class Plan:
         return {K_CLASSES[i]: (ms[i], cnt[i]) for i in range(len(K_CLASSES)) if cnt[i]}
 
     def workspace(self):
-        if self._ws is None:
+        """The plan's device workspace (re-sized when set_material / set_scheme grow the need: the
+        general Hodge's deterministic-accumulation scratch lives in it)."""
+        nb = self.workspace_bytes()
+        if self._ws is None or self._ws.numel() * 8 < nb:
             import torch
-            nb = self.workspace_bytes()
             self._ws = torch.empty((nb + 7) // 8, dtype=torch.float64, device=f"cuda:{self.device}")
         return self._ws
 

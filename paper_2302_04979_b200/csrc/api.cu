@@ -106,20 +106,32 @@ struct WS {
   double* t;
   double* r;
   double* partials;
+  double* scratch = nullptr;  // general Hodge output patches (or null)
+  size_t scratch_cap = 0;
 };
 
-size_t ws_need(const Plan& P) {
+size_t ws_base(const Plan& P) {
   size_t nmax = std::max(P.N_e, P.N_h);
   return (2 * nmax + 4 * size_t(partial_blocks()) + 16) * sizeof(double);
 }
+// + the general Hodge's output-patch scratch (bitwise-reproducible accumulation, hodge.cu)
+size_t ws_need(const Plan& P) { return ws_base(P) + P.hodge_scratch * sizeof(double); }
 
 sgm_status ws_carve(const Plan& P, void* ws, size_t bytes, WS& w) {
   if (!ws || !aligned8(ws)) return fail(SGM_E_INVALID_ARG, "workspace is NULL or misaligned");
-  if (bytes < ws_need(P)) return fail(SGM_E_INVALID_ARG, "workspace too small (see sgm_workspace_bytes)");
+  if (bytes < ws_base(P)) return fail(SGM_E_INVALID_ARG, "workspace too small (see sgm_workspace_bytes)");
   size_t nmax = std::max(P.N_e, P.N_h);
   w.t = static_cast<double*>(ws);
   w.r = w.t + nmax;
   w.partials = w.r + nmax;
+  // a workspace sized before set_material may lack the scratch: the general Hodge then accumulates
+  // with atomics (correct, not bitwise reproducible)
+  w.scratch = nullptr;
+  w.scratch_cap = 0;
+  if (P.hodge_scratch && bytes >= ws_need(P)) {
+    w.scratch = reinterpret_cast<double*>(static_cast<char*>(ws) + ws_base(P));
+    w.scratch_cap = P.hodge_scratch;
+  }
   return SGM_OK;
 }
 
@@ -607,8 +619,13 @@ PrologueArgs make_pro(const Plan& P, int src_kind, const double* src, const doub
 
 // form1 = false: the 2-form masses of scheme 2 (eps: dual 2-forms, mu: primal 2-forms);
 // form1 = true:  the 1-form masses of scheme 1 (eps: primal 1-forms of e, mu: dual 1-forms of h)
-void hodge_args(const Plan& P, int which, const double* x, double* y, HodgeArgs& h, bool form1 = false) {
+void hodge_args(const Plan& P, int which, const double* x, double* y, HodgeArgs& h, bool form1 = false,
+                const WS* w = nullptr) {
   std::memset(&h, 0, sizeof(h));
+  if (w) {
+    h.scratch = w->scratch;
+    h.scratch_cap = w->scratch_cap;
+  }
   int kind = (which == SGM_MASS_EPS) ? 0 : 1;
   const MassData& MD = form1 ? P.mass1[which] : P.mass[which];
   double *X[3], *Y[3];
@@ -648,7 +665,8 @@ void hodge_args(const Plan& P, int which, const double* x, double* y, HodgeArgs&
 }
 
 // y = M x for one 2-form mass (separable: Kronecker of 1D Grams; else sum factorisation)
-void mass_apply(const Plan& P, int which, const double* x, double* y, double* t, cudaStream_t st) {
+void mass_apply(const Plan& P, int which, const double* x, double* y, double* t, cudaStream_t st,
+                const WS* w = nullptr) {
   int kind = (which == SGM_MASS_EPS) ? 0 : 1;
   const MassData& M = P.mass[which];
   if (M.kind == HODGE_SEPARABLE) {
@@ -657,18 +675,15 @@ void mass_apply(const Plan& P, int which, const double* x, double* y, double* t,
     kron_pass3(P, kind, x, y, t, own, oth, M.scale, true, false, st);
     return;
   }
-  cudaMemsetAsync(y, 0, form_len(P, kind) * sizeof(double), st);
   HodgeArgs h;
-  hodge_args(P, which, x, y, h);
+  hodge_args(P, which, x, y, h, false, w);
   launch_hodge_general(P.p, h, st);
 }
 
 // y = M^1 x for one scheme-1 1-form mass (sum factorisation with the 1-form weights)
-void mass1_apply(const Plan& P, int which, const double* x, double* y, cudaStream_t st) {
-  const int kind = (which == SGM_MASS_EPS) ? 0 : 1;
-  cudaMemsetAsync(y, 0, form_len(P, kind) * sizeof(double), st);
+void mass1_apply(const Plan& P, int which, const double* x, double* y, cudaStream_t st, const WS* w = nullptr) {
   HodgeArgs h;
-  hodge_args(P, which, x, y, h, true);
+  hodge_args(P, which, x, y, h, true, w);
   launch_hodge_general(P.p, h, st);
 }
 
@@ -713,7 +728,7 @@ void pcg_star(Plan& P, int which, const double* x, double* y, const WS& w, cudaS
   if (trace) record(scal + a);
   const int iters = trace ? 200 : (P.pcg_fixed > 0 ? P.pcg_fixed : P.pcg_iters_m[which]);
   for (int k = 0; k < iters; ++k) {
-    mass1_apply(P, which, pv, q, st);
+    mass1_apply(P, which, pv, q, st, &w);
     launch_dot_partials(pv, q, N, w.partials, 0, st);
     launch_finalize_sum(w.partials, 1, 1.0, scal + 2, st);
     launch_axpy_ratio(y, pv, N, scal + a, scal + 2, 1.0, st);
@@ -838,6 +853,23 @@ sgm_status upload_basis(Plan& P) {
   return cuda_check(&P, "upload_basis");
 }
 
+// workspace doubles of the general Hodge's deterministic accumulation (the largest of the non-separable
+// masses: scheme-2 2-forms, and with scheme 1 its 1-forms); device plans only
+void update_scratch_need(Plan& P) {
+  size_t need = 0;
+  if (P.device >= 0) {
+    for (int m = 0; m < 2; ++m) {
+      if (P.mass[m].kind != HODGE_SEPARABLE)
+        need = std::max(need, hodge_scratch_doubles(P.p, P.Q, m == SGM_MASS_EPS ? 1 : 0,
+                                                    P.mass[m].kind == HODGE_FULL ? 1 : 0, P.n));
+      if (P.scheme == 1 && P.mass1[m].kind != HODGE_SEPARABLE)
+        need = std::max(need, hodge_scratch_doubles(P.p, P.Q, m == SGM_MASS_EPS ? 2 : 3,
+                                                    P.mass1[m].kind == HODGE_FULL ? 1 : 0, P.n));
+    }
+  }
+  P.hodge_scratch = need;
+}
+
 sgm_status set_material_impl(Plan& P, int which, const double* values, double c) {
   std::vector<double> W;
   std::string err;
@@ -867,6 +899,7 @@ sgm_status set_material_impl(Plan& P, int which, const double* values, double c)
       return fail(SGM_E_NOMEM, "cudaMalloc failed for Hodge weights");
     cudaMemcpy(M.W_dev, W.data(), W.size() * sizeof(double), cudaMemcpyHostToDevice);
   }
+  update_scratch_need(P);
   return cuda_check(&P, "set_material");
 }
 
@@ -940,7 +973,7 @@ void half_step(Plan& P, int half, double* d, double* e, double* b, double* h, co
     { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, true, true, st, 0); }
     { ProfScope ps(P, kz, st); sweep_pass(P, kind, 0, T, outv, own, oth, M.scale, true, true, st, 1, 0, aff); }
   } else {
-    { ProfScope ps(P, SGM_K_HODGE_GENERAL, st); mass_apply(P, mass, state[0], w.r, w.t, st); }
+    { ProfScope ps(P, SGM_K_HODGE_GENERAL, st); mass_apply(P, mass, state[0], w.r, w.t, st, &w); }
     comps_of(P, kind, w.r, Rr);
     { ProfScope ps(P, SGM_K_SOLVE_Z, st); sweep_pass(P, kind, 2, Rr, T, own, oth, nullptr, false, true, st); }
     { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, false, true, st); }
@@ -988,7 +1021,7 @@ void half_step_eh(Plan& P, int half, double* e, double* h, const double* jhat, c
     { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, true, true, st, 0); }
     { ProfScope ps(P, kx, st); sweep_pass(P, kind, 0, T, O, own, oth, M.scale, true, true, st, 1, 1); }
   } else {
-    { ProfScope ps(P, SGM_K_HODGE_GENERAL, st); mass_apply(P, mass, w.t, w.r, nullptr, st); }
+    { ProfScope ps(P, SGM_K_HODGE_GENERAL, st); mass_apply(P, mass, w.t, w.r, nullptr, st, &w); }
     comps_of(P, kind, w.r, Rr);
     { ProfScope ps(P, SGM_K_SOLVE_Z, st); sweep_pass(P, kind, 2, Rr, T, own, oth, nullptr, false, true, st); }
     { ProfScope ps(P, ky, st); sweep_pass(P, kind, 1, T, T, own, oth, nullptr, false, true, st); }
@@ -1205,6 +1238,7 @@ sgm_status sgm_plan_set_scheme(sgm_plan plan, int scheme) {
     if (st != SGM_OK) return st;
   }
   P->scheme = scheme;
+  update_scratch_need(*P);
   return SGM_OK;
 }
 
@@ -1274,6 +1308,10 @@ sgm_status sgm_plan_set_material(sgm_plan plan, sgm_material which, const double
   if (s == SGM_OK && P->scheme == 1) {
     DeviceGuard g(P->device >= 0 ? P->device : 0);
     s = upload_mass1(*P);
+  }
+  if (P->device >= 0) {
+    DeviceGuard g(P->device);
+    update_scratch_need(*P);
   }
   drop_graphs(*P);
   return s;
@@ -1622,7 +1660,7 @@ sgm_status sgm_hodge_apply(sgm_plan plan, sgm_mass which, const double* x, doubl
   WS w;
   if ((s = ws_carve(*P, workspace, ws_bytes, w)) != SGM_OK) return s;
   DeviceGuard g(P->device);
-  mass_apply(*P, which, x, y, w.t, static_cast<cudaStream_t>(stream));
+  mass_apply(*P, which, x, y, w.t, static_cast<cudaStream_t>(stream), &w);
   return cuda_check(P, "sgm_hodge_apply");
 }
 
@@ -1639,7 +1677,7 @@ void hodge_star_impl(const Plan& P, int which, const double* x, double* y, const
   } else if (M.kind == HODGE_SEPARABLE) {
     kron_pass3(P, kind, x, y, w.t, own, oth, M.scale, true, true, st);
   } else {
-    mass_apply(P, which, x, w.r, w.t, st);
+    mass_apply(P, which, x, w.r, w.t, st, &w);
     kron_pass3(P, kind, w.r, y, w.t, own, oth, nullptr, false, true, st);
   }
 }

@@ -2,6 +2,8 @@
 // generic CTA-per-element kernel for quadrature rules other than p+1 points.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "hodge_brick.cuh"
 #include "kernels.cuh"
 #include "launch_util.cuh"
@@ -125,11 +127,13 @@ __global__ void hodge_general_kernel(const __grid_constant__ HodgeArgs A) {
   }
 }
 
+// Work decomposition of the brick kernel: bricks of E x E elements in (x, y) times z chunks sized for
+// about four work items per resident CTA (at least 4 element layers per chunk).
 template <int P, int Q, int DUAL, bool FULL>
-void launch_hodge_brick(const HodgeArgs& a, cudaStream_t st) {
+void brick_plan(const int nel[3], int& zchunk, long& items, long& slots, size_t& smem) {
   constexpr int E = 4;
   using L = brick::Layout<P, Q, DUAL, E>;
-  const size_t smem = size_t(L::template total<FULL>()) * sizeof(double);
+  smem = size_t(L::template total<FULL>()) * sizeof(double);
   static unsigned long long attr = 0;  // per device
   if (first_on_device(attr))
     cudaFuncSetAttribute(brick::hodge_brick_kernel<P, Q, DUAL, FULL, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -137,16 +141,48 @@ void launch_hodge_brick(const HodgeArgs& a, cudaStream_t st) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, brick::hodge_brick_kernel<P, Q, DUAL, FULL, E>, 256, smem);
   if (per_sm < 1) per_sm = 1;
-  const long slots = long(per_sm) * sm_count();
-  const long bricks = long((a.nel[0] + E - 1) / E) * ((a.nel[1] + E - 1) / E);
-  // z chunks: about four work items per resident CTA, at least 4 element layers per chunk
+  slots = long(per_sm) * sm_count();
+  const long bricks = long((nel[0] + E - 1) / E) * ((nel[1] + E - 1) / E);
   long bzn = (4 * slots + bricks - 1) / bricks;
-  int zchunk = int((a.nel[2] + bzn - 1) / bzn);
+  zchunk = int((nel[2] + bzn - 1) / bzn);
   if (zchunk < 4) zchunk = 4;
   if (const int zc = tune_int("SGM_HODGE_ZCHUNK", 0)) zchunk = zc;
-  const long items = bricks * ((a.nel[2] + zchunk - 1) / zchunk);
+  items = bricks * ((nel[2] + zchunk - 1) / zchunk);
+}
+
+// y = M x.  With a large enough scratch (the plan's, sized by hodge_scratch_doubles): every work item
+// writes its output patches to the scratch and hodge_gather_kernel sums them in a fixed order --
+// bitwise reproducible.  Otherwise fp64 atomics into a zeroed y.
+template <int P, int Q, int DUAL, bool FULL>
+void launch_hodge_brick(const HodgeArgs& a, cudaStream_t st) {
+  constexpr int E = 4;
+  int zchunk = 0;
+  long items = 0, slots = 0;
+  size_t smem = 0;
+  brick_plan<P, Q, DUAL, FULL>(a.nel, zchunk, items, slots, smem);
   const long grid = items < slots ? items : slots;
-  brick::hodge_brick_kernel<P, Q, DUAL, FULL, E><<<unsigned(grid), 256, smem, st>>>(a, zchunk);
+  const size_t need = size_t(items) * brick::item_stride<P, Q, DUAL, E>(zchunk);
+  HodgeArgs b = a;
+  if (!a.scratch || a.scratch_cap < need) {
+    b.scratch = nullptr;
+    for (int c = 0; c < 3; ++c)
+      cudaMemsetAsync(a.y[c], 0, size_t(a.ext[c][0]) * a.ext[c][1] * a.ext[c][2] * sizeof(double), st);
+  }
+  brick::hodge_brick_kernel<P, Q, DUAL, FULL, E><<<unsigned(grid), 256, smem, st>>>(b, zchunk);
+  if (b.scratch) brick::hodge_gather_kernel<P, Q, DUAL, E><<<unsigned(4 * sm_count()), 256, 0, st>>>(b, zchunk);
+}
+
+template <int P, int Q, int DUAL>
+size_t scratch_of(int full, const int nel[3]) {
+  int zchunk = 0;
+  long items = 0, slots = 0;
+  size_t smem = 0;
+  if (full) {
+    brick_plan<P, Q, DUAL, true>(nel, zchunk, items, slots, smem);
+  } else {
+    brick_plan<P, Q, DUAL, false>(nel, zchunk, items, slots, smem);
+  }
+  return size_t(items) * brick::item_stride<P, Q, DUAL, 4>(zchunk);
 }
 
 template <int P, int Q>
@@ -173,6 +209,25 @@ void launch_hodge2(const HodgeArgs& a, cudaStream_t st) {
 
 }  // namespace
 
+size_t hodge_scratch_doubles(int p, int Q, int form, int full, const int nel[3]) {
+  if (Q != p + 1) return 0;  // the generic kernel accumulates with atomics
+  auto pick = [&](auto pq) -> size_t {
+    constexpr int PP = decltype(pq)::value;
+    switch (form) {
+      case 0: return scratch_of<PP, PP + 1, 0>(full, nel);
+      case 1: return scratch_of<PP, PP + 1, 1>(full, nel);
+      case 2: return scratch_of<PP, PP + 1, 2>(full, nel);
+      default: return scratch_of<PP, PP + 1, 3>(full, nel);
+    }
+  };
+  switch (p) {
+    case 2: return pick(std::integral_constant<int, 2>{});
+    case 3: return pick(std::integral_constant<int, 3>{});
+    case 4: return pick(std::integral_constant<int, 4>{});
+    default: return 0;
+  }
+}
+
 void launch_hodge_general(int p, const HodgeArgs& a, cudaStream_t st) {
   // brick sum-factorisation kernel (hodge_brick.cuh) for the default rule Q = p + 1; the generic
   // CTA-per-element kernel for larger rules (quad_points > p + 1)
@@ -184,6 +239,8 @@ void launch_hodge_general(int p, const HodgeArgs& a, cudaStream_t st) {
       default: break;
     }
   }
+  for (int c = 0; c < 3; ++c)
+    cudaMemsetAsync(a.y[c], 0, size_t(a.ext[c][0]) * a.ext[c][1] * a.ext[c][2] * sizeof(double), st);
   long nel = long(a.nel[0]) * a.nel[1] * a.nel[2];
   int Q = a.Q;
   int M = (p + 1 > Q) ? p + 1 : Q;

@@ -124,9 +124,11 @@ __device__ __forceinline__ void load_layer(const HodgeArgs& A, const CompSm<P, Q
 
 // atomically add the output window slot `sl` (global z index gz) of component C's patch to y and
 // clear the slot for reuse as the top layer
+// scr: this item's patch layers of component C in the scratch (layer rel = gz - first z of the
+// item), or null -> fp64 atomics into y
 template <int P, int Q, int DUAL, int E, int C>
 __device__ __forceinline__ void flush_layer(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int gx0, int gy0,
-                                            int gz, int sl) {
+                                            int gz, int sl, double* scr, int rel) {
   using G = Geo<P, Q, DUAL, E, C>;
   constexpr int LAY = G::PY * G::PX;
   const int* ext = A.ext[C];
@@ -134,8 +136,10 @@ __device__ __forceinline__ void flush_layer(const HodgeArgs& A, const CompSm<P, 
   for (int o = threadIdx.x; o < LAY; o += blockDim.x) {
     const int px = o % G::PX, py = o / G::PX;
     const int gx = gx0 + px, gy = gy0 + py;
-    if (gx >= 0 && gx < ext[0] && gy >= 0 && gy < ext[1] && gz >= 0 && gz < ext[2])
-      atomicAdd(y + gx + long(ext[0]) * (gy + long(ext[1]) * gz), S.Yw[sl * LAY + o]);
+    if (gx >= 0 && gx < ext[0] && gy >= 0 && gy < ext[1] && gz >= 0 && gz < ext[2]) {
+      if (scr) scr[rel * LAY + o] = S.Yw[sl * LAY + o];
+      else atomicAdd(y + gx + long(ext[0]) * (gy + long(ext[1]) * gz), S.Yw[sl * LAY + o]);
+    }
     S.Yw[sl * LAY + o] = 0.0;
   }
 }
@@ -306,7 +310,8 @@ __device__ __forceinline__ void test_z(const CompSm<P, Q, DUAL, E, C>& S, int t)
 template <int P, int Q, int DUAL, int E, int C>
 __device__ __forceinline__ void column_phase(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int t, int gx0,
                                              int gy0, int gz_flush, bool next, int gz_load,
-                                             const double* __restrict__ vz_cur, const double* __restrict__ vz_next) {
+                                             const double* __restrict__ vz_cur, const double* __restrict__ vz_next,
+                                             double* scr, int rel) {
   using G = Geo<P, Q, DUAL, E, C>;
   constexpr int NL = P + 1, LAY = G::PY * G::PX;
   if (t >= LAY) return;
@@ -324,8 +329,10 @@ __device__ __forceinline__ void column_phase(const HodgeArgs& A, const CompSm<P,
 #pragma unroll
     for (int qz = 0; qz < Q; ++qz) acc = fma(__ldg(vz_cur + qz * NL + jz), zv[qz], acc);
     if (jz == 0) {
-      if (inxy && gz_flush >= 0 && gz_flush < ext[2])
-        atomicAdd(A.y[C] + gx + long(ext[0]) * (gy + long(ext[1]) * gz_flush), acc);
+      if (inxy && gz_flush >= 0 && gz_flush < ext[2]) {
+        if (scr) scr[rel * LAY + t] = acc;
+        else atomicAdd(A.y[C] + gx + long(ext[0]) * (gy + long(ext[1]) * gz_flush), acc);
+      }
       S.Yw[sl * LAY + t] = 0.0;
     } else {
       S.Yw[sl * LAY + t] = acc;
@@ -376,6 +383,73 @@ __device__ __forceinline__ void column_phase(const HodgeArgs& A, const CompSm<P,
     __syncthreads();                                                                                 \
   }
 
+// doubles of one work item's output patches in the scratch (all three components, zchunk + NZ - 1
+// layers each)
+template <int P, int Q, int DUAL, int E>
+__host__ __device__ constexpr size_t item_stride(int zchunk) {
+  using G0 = Geo<P, Q, DUAL, E, 0>;
+  using G1 = Geo<P, Q, DUAL, E, 1>;
+  using G2 = Geo<P, Q, DUAL, E, 2>;
+  return size_t(zchunk + G0::NZ - 1) * G0::PY * G0::PX + size_t(zchunk + G1::NZ - 1) * G1::PY * G1::PX +
+         size_t(zchunk + G2::NZ - 1) * G2::PY * G2::PX;
+}
+
+// Second pass of the deterministic accumulation: y_c[g] = sum over the work items whose patches
+// contain g (at most 2 bricks per axis x 2 z chunks), in the fixed order (chunk, brick y, brick x).
+// One thread per output entry; the brick / chunk candidates of an index are the two around
+// g / E (patch origins are the first functions of the bricks' first elements).
+template <int P, int Q, int DUAL, int E, int C>
+__device__ __forceinline__ double gather_one(const HodgeArgs& A, int zchunk, int gx, int gy, int gz) {
+  using G = Geo<P, Q, DUAL, E, C>;
+  const int nx = A.nel[0], ny = A.nel[1], nz = A.nel[2];
+  const int bxn = (nx + E - 1) / E, byn = (ny + E - 1) / E, bzn = (nz + zchunk - 1) / zchunk;
+  const int rx = C == 0 ? 0 : 1, ry = C == 1 ? 0 : 1, rz = C == 2 ? 0 : 1;
+  const size_t stride = item_stride<P, Q, DUAL, E>(zchunk);
+  const size_t coff = C == 0 ? 0
+                    : (C == 1 ? size_t(zchunk + Geo<P, Q, DUAL, E, 0>::NZ - 1) * Geo<P, Q, DUAL, E, 0>::PY * Geo<P, Q, DUAL, E, 0>::PX
+                              : size_t(zchunk + Geo<P, Q, DUAL, E, 0>::NZ - 1) * Geo<P, Q, DUAL, E, 0>::PY * Geo<P, Q, DUAL, E, 0>::PX +
+                                size_t(zchunk + Geo<P, Q, DUAL, E, 1>::NZ - 1) * Geo<P, Q, DUAL, E, 1>::PY * Geo<P, Q, DUAL, E, 1>::PX);
+  double s = 0.0;
+  const int iz0 = max(0, gz / zchunk - 2), iz1 = min(bzn - 1, gz / zchunk + 1);
+  const int by0 = max(0, gy / E - 2), by1 = min(byn - 1, gy / E + 1);
+  const int bx0 = max(0, gx / E - 2), bx1 = min(bxn - 1, gx / E + 1);
+  for (int iz = iz0; iz <= iz1; ++iz) {
+    const int ez0 = iz * zchunk, ez1 = min(nz, ez0 + zchunk);
+    const int z0 = first_of(A, 2, rz, ez0);
+    const int rel = gz - z0;
+    if (rel < 0 || gz > first_of(A, 2, rz, ez1 - 1) + G::NZ - 1) continue;
+    for (int by = by0; by <= by1; ++by) {
+      const int py = gy - first_of(A, 1, ry, by * E);
+      if (py < 0 || py >= G::PY) continue;
+      for (int bx = bx0; bx <= bx1; ++bx) {
+        const int px = gx - first_of(A, 0, rx, bx * E);
+        if (px < 0 || px >= G::PX) continue;
+        const long item = (long(iz) * byn + by) * bxn + bx;
+        s += __ldg(A.scratch + item * stride + coff + (size_t(rel) * G::PY + py) * G::PX + px);
+      }
+    }
+  }
+  return s;
+}
+
+template <int P, int Q, int DUAL, int E>
+__global__ void __launch_bounds__(256) hodge_gather_kernel(const __grid_constant__ HodgeArgs A, int zchunk) {
+  const long n0 = long(A.ext[0][0]) * A.ext[0][1] * A.ext[0][2];
+  const long n1 = long(A.ext[1][0]) * A.ext[1][1] * A.ext[1][2];
+  const long n2 = long(A.ext[2][0]) * A.ext[2][1] * A.ext[2][2];
+  for (long i = long(blockIdx.x) * blockDim.x + threadIdx.x; i < n0 + n1 + n2; i += long(gridDim.x) * blockDim.x) {
+    const int c = i < n0 ? 0 : (i < n0 + n1 ? 1 : 2);
+    const long k = i - (c == 0 ? 0 : (c == 1 ? n0 : n0 + n1));
+    const int X = A.ext[c][0], Y = A.ext[c][1];
+    const int gx = int(k % X), gy = int((k / X) % Y), gz = int(k / (long(X) * Y));
+    double v;
+    if (c == 0) v = gather_one<P, Q, DUAL, E, 0>(A, zchunk, gx, gy, gz);
+    else if (c == 1) v = gather_one<P, Q, DUAL, E, 1>(A, zchunk, gx, gy, gz);
+    else v = gather_one<P, Q, DUAL, E, 2>(A, zchunk, gx, gy, gz);
+    A.y[c][k] = v;
+  }
+}
+
 template <int P, int Q, int DUAL, bool FULL, int E>
 __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_constant__ HodgeArgs A, int zchunk) {
   using L = Layout<P, Q, DUAL, E>;
@@ -422,6 +496,15 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
       for (int i = threadIdx.x; i < (E - 1) * Q * NL; i += 256)
         same = same && fabs(T[Q * NL + i] - T[i % (Q * NL)]) <= 1e-14 * (1.0 + fabs(T[i % (Q * NL)]));
       uni[r] = __syncthreads_and(same) != 0;
+    }
+    // deterministic accumulation: this item's output patches go to the scratch (summed in a fixed
+    // order by hodge_gather_kernel); layer rel of component c at scr_c + rel * PY_c * PX_c
+    double *scr0 = nullptr, *scr1 = nullptr, *scr2 = nullptr;
+    if (A.scratch) {
+      double* b = A.scratch + size_t(it) * item_stride<P, Q, DUAL, E>(zchunk);
+      scr0 = b;
+      scr1 = scr0 + size_t(zchunk + G0::NZ - 1) * G0::PY * G0::PX;
+      scr2 = scr1 + size_t(zchunk + G1::NZ - 1) * G1::PY * G1::PX;
     }
     const int fx[3] = {first_of(A, 0, 0, B.ex0), first_of(A, 0, 1, B.ex0), 0};  // own / other
     const int fy[3] = {first_of(A, 1, 0, B.ey0), first_of(A, 1, 1, B.ey0), 0};
@@ -515,13 +598,15 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
         for (int t = threadIdx.x; t < N0 + N1 + N2; t += 256) {
           if (t < N0)
             column_phase<P, Q, DUAL, E, 0>(A, S0, t, gx0[0], gy0[0], zfirst(0, ez), nx1, zfirst(0, ezn) + G0::NZ - 1,
-                                           vzp(0, ez), vzp(0, ezn));
+                                           vzp(0, ez), vzp(0, ezn), scr0, zfirst(0, ez) - zfirst(0, B.ez0));
           else if (t < N0 + N1)
             column_phase<P, Q, DUAL, E, 1>(A, S1, t - N0, gx0[1], gy0[1], zfirst(1, ez), nx1,
-                                           zfirst(1, ezn) + G1::NZ - 1, vzp(1, ez), vzp(1, ezn));
+                                           zfirst(1, ezn) + G1::NZ - 1, vzp(1, ez), vzp(1, ezn), scr1,
+                                           zfirst(1, ez) - zfirst(1, B.ez0));
           else
             column_phase<P, Q, DUAL, E, 2>(A, S2, t - N0 - N1, gx0[2], gy0[2], zfirst(2, ez), nx1,
-                                           zfirst(2, ezn) + G2::NZ - 1, vzp(2, ez), vzp(2, ezn));
+                                           zfirst(2, ezn) + G2::NZ - 1, vzp(2, ez), vzp(2, ezn), scr2,
+                                           zfirst(2, ez) - zfirst(2, B.ez0));
         }
       }
       S0.base = S0.slot(1);
@@ -531,11 +616,14 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
     }
     // the remaining NZ-1 output layers of the last element layer (layer jz now sits in slot jz-1)
     for (int jz = 1; jz < G0::NZ; ++jz)
-      flush_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, B.ez1 - 1) + jz, S0.slot(jz - 1));
+      flush_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, B.ez1 - 1) + jz, S0.slot(jz - 1), scr0,
+                                    zfirst(0, B.ez1 - 1) + jz - zfirst(0, B.ez0));
     for (int jz = 1; jz < G1::NZ; ++jz)
-      flush_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, B.ez1 - 1) + jz, S1.slot(jz - 1));
+      flush_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, B.ez1 - 1) + jz, S1.slot(jz - 1), scr1,
+                                    zfirst(1, B.ez1 - 1) + jz - zfirst(1, B.ez0));
     for (int jz = 1; jz < G2::NZ; ++jz)
-      flush_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, B.ez1 - 1) + jz, S2.slot(jz - 1));
+      flush_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, B.ez1 - 1) + jz, S2.slot(jz - 1), scr2,
+                                    zfirst(2, B.ez1 - 1) + jz - zfirst(2, B.ez0));
     __syncthreads();
   }
 }

@@ -76,6 +76,8 @@ struct HodgeArgs {
   int first_off[3][2];
   int nel[3];
   int Q;
+  double* scratch;       // brick kernel: per-item output patches (deterministic two-pass
+  size_t scratch_cap;    // accumulation, hodge.cu); null or too small -> fp64 atomics (y += ...)
   int dual;              // 1: dual 2-forms (M~2_{1/eps}), 0: primal 2-forms (M2_{1/mu})
   int form;              // brick kernel form type: 0 primal 2-form, 1 dual 2-form, 2 primal 1-form
                          // (M^1_eps, scheme 1), 3 dual 1-form (M~^1_mu, scheme 1)
@@ -98,6 +100,8 @@ void launch_update(int pro, const SweepArgs& a, cudaStream_t st);
 void launch_curl(int kind, const double* const src[3], const int sext[3][3], double* const dst[3],
                  const int dext[3][3], cudaStream_t st);
 void launch_hodge_general(int p, const HodgeArgs& a, cudaStream_t st);
+// doubles of scratch the deterministic brick Hodge needs for this plan geometry (current device)
+size_t hodge_scratch_doubles(int p, int Q, int form, int full, const int nel[3]);
 void launch_dot_partials(const double* x, const double* y, size_t n, double* partials, int slot, cudaStream_t st);
 void launch_finalize_sum(const double* partials, int nslots, double scale, double* out, cudaStream_t st);
 void launch_div_max(int kind, const double* const src[3], const int sext[3][3], double* partials,

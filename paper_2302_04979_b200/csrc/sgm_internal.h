@@ -113,6 +113,7 @@ struct Plan {
   std::vector<double> tables_host;
   bool sticky_cuda_error = false;
   unsigned opts = 0;                  // SGM_OPT_* schedule options (sgm_plan_set_options)
+  size_t hodge_scratch = 0;           // doubles of workspace for the deterministic general Hodge
   mutable int launch_fail = 0;             // a launcher found no compiled configuration (set while enqueuing)
   bool graph_enabled = true;          // SGM_GRAPH=0 disables the sgm_step graph cache
   // fork/join of independent sweep launches (reduced separable schedule): the second launch runs on
