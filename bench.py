@@ -502,18 +502,23 @@ def main():
                                       "weights_bytes": wq})
         func["hodge_general"]["frac"] = func["hodge_general"]["gbs"] / peak
     dom = max(func.items(), key=lambda kv: kv[1]["ms_per_step"])[0]
+    # ncu DRAM bytes (dram__bytes_read + dram__bytes_write) of the dominant function per step, from the
+    # committed full capture (profiles/traffic.json: per class, per launch)
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tfile):
         try:
-            traffic = json.load(open(tfile)).get(f"{args.config}_p{p}_n{n}", {}).get(dom)
+            tj = json.load(open(tfile)).get(f"{args.config}_p{p}_n{n}", {})
+            if all(c in tj for c in func[dom]["classes"]):
+                traffic = sum(tj[c] * (prof[c][1] / K) for c in func[dom]["classes"])
         except Exception:
             traffic = None
     D = func[dom]
     t_step = ms / K * 1e-3
     roof = {"bound": "hbm", "kernel": dom, "achieved": D.get("gbs"), "peak": peak, "unit": "GB/s",
             "frac": D.get("frac"), "traffic": traffic, "peak_source": peak_src,
-            "algo_bytes_per_step": D.get("algo_bytes_per_step"), "ms_per_step_in_kernel": D["ms_per_step"],
+            "algo_bytes_per_step": D.get("algo_bytes_per_step"), "traffic_unit": "bytes per step (ncu)",
+            "ms_per_step_in_kernel": D["ms_per_step"],
             "share_of_step": D["share"],
             "step_algo_bytes": step_bytes, "step_gbs": step_bytes / t_step / 1e9,
             "step_frac": step_bytes / t_step / 1e9 / peak,
