@@ -58,6 +58,7 @@ def parse():
     ap.add_argument("--n", type=int, default=128)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-variants", action="store_true", help="skip the schedule-variant timings")
     ap.add_argument("--opts", type=lambda v: int(v, 0), default=0,
                     help="SGM_OPT_* schedule option bits (0 = the production schedule)")
     ap.add_argument("--scheme", type=int, default=2, choices=[1, 2],
@@ -541,7 +542,8 @@ def main():
     # the structure-faithful three-axis schedule (every Kronecker factor swept) and the
     # fused-update schedule, timed the same way on the same state (second and third numbers)
     variants = {}
-    if pl.separable(S.MASS_EPS) and pl.separable(S.MASS_MU) and not getattr(args, "opts", 0):
+    if (pl.separable(S.MASS_EPS) and pl.separable(S.MASS_MU) and not getattr(args, "opts", 0)
+            and not args.no_variants):
         for name, o in (("full_schedule", S.OPT_FULL_SCHEDULE), ("fused_update", S.OPT_FUSED)):
             pl.set_options(o)
             steps(0, W)

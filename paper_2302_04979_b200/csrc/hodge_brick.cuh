@@ -409,25 +409,28 @@ __device__ __forceinline__ double gather_one(const HodgeArgs& A, int zchunk, int
                     : (C == 1 ? size_t(zchunk + Geo<P, Q, DUAL, E, 0>::NZ - 1) * Geo<P, Q, DUAL, E, 0>::PY * Geo<P, Q, DUAL, E, 0>::PX
                               : size_t(zchunk + Geo<P, Q, DUAL, E, 0>::NZ - 1) * Geo<P, Q, DUAL, E, 0>::PY * Geo<P, Q, DUAL, E, 0>::PX +
                                 size_t(zchunk + Geo<P, Q, DUAL, E, 1>::NZ - 1) * Geo<P, Q, DUAL, E, 1>::PY * Geo<P, Q, DUAL, E, 1>::PX);
+  // the (at most two) bricks per axis and chunks along z containing the index, with the index's
+  // position in their patches, found once (patch origins are monotone in the brick index)
+  int bxs[2], pxs[2], nbx = 0;
+  for (int bx = max(0, gx / E - 2); bx <= min(bxn - 1, gx / E + 1) && nbx < 2; ++bx) {
+    const int px = gx - first_of(A, 0, rx, bx * E);
+    if (px >= 0 && px < G::PX) bxs[nbx] = bx, pxs[nbx++] = px;
+  }
+  int bys[2], pys[2], nby = 0;
+  for (int by = max(0, gy / E - 2); by <= min(byn - 1, gy / E + 1) && nby < 2; ++by) {
+    const int py = gy - first_of(A, 1, ry, by * E);
+    if (py >= 0 && py < G::PY) bys[nby] = by, pys[nby++] = py;
+  }
   double s = 0.0;
-  const int iz0 = max(0, gz / zchunk - 2), iz1 = min(bzn - 1, gz / zchunk + 1);
-  const int by0 = max(0, gy / E - 2), by1 = min(byn - 1, gy / E + 1);
-  const int bx0 = max(0, gx / E - 2), bx1 = min(bxn - 1, gx / E + 1);
-  for (int iz = iz0; iz <= iz1; ++iz) {
+  for (int iz = max(0, gz / zchunk - 2); iz <= min(bzn - 1, gz / zchunk + 1); ++iz) {
     const int ez0 = iz * zchunk, ez1 = min(nz, ez0 + zchunk);
-    const int z0 = first_of(A, 2, rz, ez0);
-    const int rel = gz - z0;
+    const int rel = gz - first_of(A, 2, rz, ez0);
     if (rel < 0 || gz > first_of(A, 2, rz, ez1 - 1) + G::NZ - 1) continue;
-    for (int by = by0; by <= by1; ++by) {
-      const int py = gy - first_of(A, 1, ry, by * E);
-      if (py < 0 || py >= G::PY) continue;
-      for (int bx = bx0; bx <= bx1; ++bx) {
-        const int px = gx - first_of(A, 0, rx, bx * E);
-        if (px < 0 || px >= G::PX) continue;
-        const long item = (long(iz) * byn + by) * bxn + bx;
-        s += __ldg(A.scratch + item * stride + coff + (size_t(rel) * G::PY + py) * G::PX + px);
+    for (int j = 0; j < nby; ++j)
+      for (int i = 0; i < nbx; ++i) {
+        const long item = (long(iz) * byn + bys[j]) * bxn + bxs[i];
+        s += __ldg(A.scratch + item * stride + coff + (size_t(rel) * G::PY + pys[j]) * G::PX + pxs[i]);
       }
-    }
   }
   return s;
 }

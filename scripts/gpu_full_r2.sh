@@ -14,7 +14,7 @@ for cfg in "--p 2 --n 160" "--p 4 --n 128" "--p 3 --n 64" "--config c2" "--confi
   python bench.py --steps 20 --warmup 5 --no-e2e $cfg >> gpurun_out/bench_sweep_$TAG.jsonl 2>> gpurun_out/bench_sweep_$TAG.err
 done
 python scripts/c5_sweep.py --out gpurun_out/c5_sweep_$TAG.jsonl > gpurun_out/c5_sweep_$TAG.log 2>&1
-ARGS="--steps 3 --warmup 3 --no-cpu --no-e2e"
+ARGS="--steps 3 --warmup 3 --no-cpu --no-e2e --no-variants"
 python bench.py $ARGS > gpurun_out/plain_$TAG.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 500 --csv --log-file gpurun_out/launches_$TAG.csv \
     python bench.py $ARGS > gpurun_out/ncu_launch_$TAG.log 2>&1
