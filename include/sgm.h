@@ -342,6 +342,17 @@ sgm_status sgm_plan_profile(sgm_plan plan, double* ms, int* counts);
 const char* sgm_last_error(void);
 const char* sgm_version(void);
 
+/* ---- verification build --------------------------------------------------------------------
+   Only libsgm_checked.so (compiled with -DSGM_CHECKED, paper_2302_04979_b200/build.py
+   checked=True) checks the producer/consumer and SPIKE-exchange protocols of the pipelined sweeps
+   at run time (csrc/check.cuh: hand-off tags, release counts, slab poisoning, random delays) and
+   counts violations in a library-wide device buffer.  sgm_check_read synchronises the device,
+   writes the number of violations since the last reset to *count and the code of the first one
+   to *first (0: none; 1 stage tag, 2 release count, 3 tails tag, 4 heads tag, 5 fused release
+   count), and zeroes the counters when reset != 0.  count/first: host pointers (either may be
+   NULL).  The product build returns SGM_E_UNSUPPORTED and writes nothing. */
+sgm_status sgm_check_read(int reset, unsigned* count, unsigned* first);
+
 #ifdef __cplusplus
 }
 #endif

@@ -14,7 +14,13 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsgm.so")
+# SGM_LIB_VARIANT=checked selects the verification build libsgm_checked.so (build.py checked=True:
+# run-time protocol checks of the pipelined sweeps, csrc/check.cuh); the default is the product
+# library.  The variant is chosen once, at import.
+VARIANT = os.environ.get("SGM_LIB_VARIANT", "")
+if VARIANT not in ("", "checked"):
+    raise ImportError(f"SGM_LIB_VARIANT={VARIANT!r}: only 'checked' is known")
+LIB_PATH = os.path.join(_HERE, "libsgm_checked.so" if VARIANT == "checked" else "libsgm.so")
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2302_04979_b200.build` "
@@ -89,6 +95,7 @@ _SIGS = {
     "sgm_geometry_interpolate": [c_void_p, c_int, c_void_p, c_void_p],
     "sgm_plan_set_profiling": [c_void_p, c_int],
     "sgm_plan_profile": [c_void_p, c_void_p, c_void_p],
+    "sgm_check_read": [c_int, ctypes.POINTER(ctypes.c_uint), ctypes.POINTER(ctypes.c_uint)],
 }
 for _name, _args in _SIGS.items():
     _f = getattr(_lib, _name)
@@ -114,6 +121,14 @@ class SgmError(RuntimeError):
 def check(status, where="sgm"):
     if status != 0:
         raise SgmError(status, where)
+
+
+def check_read(reset=True):
+    """Verification build only (SGM_LIB_VARIANT=checked): (violations, first code) of the sweep
+    protocol checks since the last reset (sgm.h sgm_check_read); the product build raises."""
+    n, f = ctypes.c_uint(0), ctypes.c_uint(0)
+    check(sgm_check_read(1 if reset else 0, ctypes.byref(n), ctypes.byref(f)), "sgm_check_read")
+    return n.value, f.value
 
 
 def _ptr(t):

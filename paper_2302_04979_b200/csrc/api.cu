@@ -11,6 +11,7 @@
 #include <new>
 #include <string>
 
+#include "check.cuh"
 #include "kernels.cuh"
 #include "sgm_internal.h"
 #include "seg_sweep.cuh"
@@ -19,6 +20,26 @@ namespace sgm {
 
 static thread_local std::string g_err;
 void set_error(const std::string& s) { g_err = s; }
+
+#ifdef SGM_CHECKED
+// verification build (check.cuh): one zeroed [count, first code] violation buffer per device
+unsigned* check_buffer() {
+  static unsigned* bufs[64] = {};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  if (!bufs[dev]) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, 2 * sizeof(unsigned)) != cudaSuccess) return nullptr;
+    cudaMemset(p, 0, 2 * sizeof(unsigned));
+    bufs[dev] = static_cast<unsigned*>(p);
+  }
+  return bufs[dev];
+}
+int check_inject() {
+  const char* v = std::getenv("SGM_CHECK_INJECT");
+  return v ? std::atoi(v) : 0;
+}
+#endif
 
 namespace {
 
@@ -1044,7 +1065,30 @@ using namespace sgm;
 extern "C" {
 
 const char* sgm_last_error(void) { return g_err.c_str(); }
+#ifdef SGM_CHECKED
+const char* sgm_version(void) { return "sgm 0.1 (sm_100a, fp64, checked)"; }
+#else
 const char* sgm_version(void) { return "sgm 0.1 (sm_100a, fp64)"; }
+#endif
+
+sgm_status sgm_check_read(int reset, unsigned* count, unsigned* first) {
+#ifdef SGM_CHECKED
+  unsigned h[2] = {0u, 0u};
+  unsigned* d = sgm::check_buffer();
+  if (!d) return fail(SGM_E_CUDA, "sgm_check_read: no violation buffer");
+  if (cudaDeviceSynchronize() != cudaSuccess || cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return fail(SGM_E_CUDA, "sgm_check_read: device error");
+  if (reset && cudaMemset(d, 0, sizeof(h)) != cudaSuccess) return fail(SGM_E_CUDA, "sgm_check_read: reset failed");
+  if (count) *count = h[0];
+  if (first) *first = h[1];
+  return SGM_OK;
+#else
+  (void)reset;
+  (void)count;
+  (void)first;
+  return fail(SGM_E_UNSUPPORTED, "sgm_check_read: not a verification build (libsgm_checked.so)");
+#endif
+}
 
 sgm_status sgm_plan_create(const sgm_plan_desc* desc, sgm_plan* out) {
   if (!desc || !out) return fail(SGM_E_INVALID_ARG, "desc/out is NULL");
@@ -1085,6 +1129,12 @@ sgm_status sgm_plan_create(const sgm_plan_desc* desc, sgm_plan* out) {
   }
   sgm_status st = build_tables(*P, err);
   if (st == SGM_OK) st = build_geometry(*P, err);
+#ifdef SGM_CHECKED
+  if (st == SGM_OK) {  // allocate the violation buffer now: the launchers may run under stream capture
+    DeviceGuard dg(P->device);
+    if (!check_buffer()) st = SGM_E_CUDA;
+  }
+#endif
   if (st != SGM_OK) {
     delete P;
     return fail(st, err);

@@ -25,6 +25,7 @@
 // phases run on registers), and store the swept line.
 #pragma once
 
+#include "check.cuh"
 #include "kernels.cuh"
 #include "pipe_sweep.cuh"
 #include "seg_sweep.cuh"
@@ -90,6 +91,7 @@ struct Args {
   int np;                // producer warps
   const double* s_ptr;   // Ampere amplitude s_k (device) or null (-> 1)
   double dt;
+  unsigned* ck;          // verification build (check.cuh): violation counters; unused otherwise
 };
 
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
@@ -148,6 +150,10 @@ __global__ void __launch_bounds__(480, 1) fsweep_kernel(const __grid_constant__ 
   double* heads = tails + NC * M * 32;                 // [NC][M][32]
   unsigned long long* mb = reinterpret_cast<unsigned long long*>(heads + NC * M * 32);  // tab, full, empty
   unsigned long long *tab_mb = mb, *full_mb = mb + 1, *empty_mb = mb + 2;
+#ifdef SGM_CHECKED
+  int* rel = reinterpret_cast<int*>(mb + 3);  // consumer-warp releases of the staging area
+  if (threadIdx.x == 0) *rel = 0;
+#endif
   pipe::griddep_launch_dependents();
   if (threadIdx.x == 0) {
     pipe::mbar_init(tab_mb, 1);
@@ -172,6 +178,14 @@ __global__ void __launch_bounds__(480, 1) fsweep_kernel(const __grid_constant__ 
     int it = 0;
     for (int item = blockIdx.x; item < A.nitems; item += G, ++it) {
       if (it > 0) pipe::mbar_wait(empty_mb, unsigned(it - 1) & 1u);
+#ifdef SGM_CHECKED
+      // every consumer warp released every earlier tile; then poison the staging area
+      if (pw == 0 && lane == 0 && *rel != NC * it) check::fail(A.ck, check::kFReleaseCount);
+      check::jitter(unsigned(item * 64 + warp));
+      for (int i = pw * 32 + lane; i < A.stage_dbl; i += A.np * 32) stg[i] = check::kPoison;
+      pipe::fence_proxy_async_smem();
+      pipe::bar_sync(2, A.np * 32);
+#endif
       int c, t1, t0s;
       tile_of(A, item, c, t1, t0s);
       const Comp& C = A.comp[c];
@@ -308,6 +322,10 @@ __global__ void __launch_bounds__(480, 1) fsweep_kernel(const __grid_constant__ 
     for (int j = 0; j < HB; ++j) w[j] = upd(j - HB);
     // staging no longer needed by this warp: release it (the producer streams the next tile)
     __syncwarp();
+#ifdef SGM_CHECKED
+    if (lane == 0) atomicAdd(rel, 1);
+    check::jitter(unsigned(item * 64 + warp + 16));
+#endif
     if (lane == 0) mbar_arrive(empty_mb);
     // updated state rows of this segment (read by no other line: stored directly)
     if (!INC && lok && s < S) {

@@ -134,6 +134,10 @@ bool launch_t(const SweepArgs& a, cudaStream_t st) {
   constexpr int M = P - 1;
   const size_t smem =
       (size_t(A.ntabs) * A.tab_dbl + A.stage_dbl + size_t(2) * NC * M * 32) * sizeof(double) + 32;
+  A.ck = nullptr;
+#ifdef SGM_CHECKED
+  A.ck = check_buffer();
+#endif
   A.np = NC <= 11 ? 4 : 15 - NC;  // producer warps (at most 15 warps per CTA)
   if (smem > 227 * 1024 || NC > 14) return false;
   if (a.dry) return true;

@@ -10,7 +10,8 @@
 //
 // Work unit: a tile of TW = 32*LPT lines of one component; lane j of a consumer warp owns lines
 // j, j+32, ... (LPT lines: independent recurrences interleave, coefficient loads are shared).
-// A CTA is persistent and loops over tiles with two shared-memory slabs:
+// A CTA is persistent and loops over tiles with two shared-memory slabs (one when the lines are
+// too long for two: loads and compute of a CTA then alternate):
 //   * producer warps stage tile t+1 into slab[(t+1)&1]: cp.async (LDGSTS) copies for strided axes,
 //     one bulk copy (TMA engine, mbarrier completion) per tile of whole x-lines;
 //   * consumer warp s owns rows [s*SEG, (s+1)*SEG) of every line of the tile (SPIKE segment s) and
@@ -25,6 +26,7 @@
 //   x axis             : slab[line * pitch + r]   (pitch odd >= R: conflict-free per-lane walks)
 #pragma once
 
+#include "check.cuh"
 #include "kernels.cuh"
 #include "pipe_sweep.cuh"
 #include "seg_sweep.cuh"
@@ -66,6 +68,7 @@ struct Cfg {
   int rows;       // slab rows per line R = NC*SEG + P
   int pitch;      // x axis: slab pitch (odd >= rows)
   int slab;       // doubles per slab
+  int nslab;      // 2: double-buffered slabs; 1: one slab (lines too long for two)
   int tab_dbl;    // doubles per staged table
   int ntabs;      // distinct tables (1 or 2)
   int dbg;        // tuning only (SGM_PIPE_DBG): bit 0 consumers skip work, bit 1 producers skip loads
@@ -73,6 +76,8 @@ struct Cfg {
   int nitems;     // tiles over all components
   int tiles[3];   // tiles per component
   CompGeom g[3];
+  unsigned* ck;   // verification build (check.cuh): violation counters; unused otherwise
+  int inject;     // verification build: fault-injection bits
 };
 
 // l -> (l % X, l / X) without a division instruction sequence
@@ -108,8 +113,9 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bool bulk = cfg.bulk != 0;
   double* tabs = sm;                              // [ntabs][tab_dbl]
-  double* slabs = sm + cfg.ntabs * cfg.tab_dbl;   // [2][slab]
-  double* tails = slabs + 2 * cfg.slab;           // [NC][M][TW]
+  double* slabs = sm + cfg.ntabs * cfg.tab_dbl;   // [nslab][slab]
+  const int NS = cfg.nslab;                       // slabs: 2 (double buffering) or 1 (long lines)
+  double* tails = slabs + NS * cfg.slab;          // [NC][M][TW]
   double* heads = tails + NC * M * TW;            // [NC][M][TW]
   unsigned long long* full_mb = reinterpret_cast<unsigned long long*>(heads + NC * M * TW);  // [2] + tables
   const int G = gridDim.x;
@@ -117,6 +123,12 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
   const int W = cfg.W;  // strided slab row width
 
   unsigned long long* tab_mb = full_mb + 2;
+#ifdef SGM_CHECKED
+  // [0,1] item staged in slab b, [2,3] consumer-warp releases of slab b, [4,20) tails tags,
+  // [20,36) heads tags (check.cuh)
+  int* ckt = reinterpret_cast<int*>(full_mb + 4);
+  if (threadIdx.x < check::kSmemInts) ckt[threadIdx.x] = (threadIdx.x < 2 || threadIdx.x >= 4) ? -1 : 0;
+#endif
   pipe::griddep_launch_dependents();
   // slabs start zeroed: positions never written by a copy hold finite values (zero or stale data),
   // and every coefficient that multiplies such a position is exactly zero
@@ -124,7 +136,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
     double2* s2 = reinterpret_cast<double2*>(slabs);
     const double2 z2 = make_double2(0.0, 0.0);
 #pragma unroll 4
-    for (int i = threadIdx.x; i < cfg.slab; i += blockDim.x) s2[i] = z2;  // 2 slabs = cfg.slab double2
+    for (int i = threadIdx.x; i < NS * cfg.slab / 2; i += blockDim.x) s2[i] = z2;
   }
   if (threadIdx.x == 0) {
     pipe::mbar_init(full_mb, 1);
@@ -146,8 +158,20 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
     const int pw = warp - NC;
     int it = 0;
     for (int item = blockIdx.x; item < cfg.nitems; item += G, ++it) {
-      const int buf = it & 1;
-      if (it >= 2) pipe::bar_sync(pipe::kBarEmpty0 + buf, NT);
+      const int buf = NS == 2 ? (it & 1) : 0;
+      if (it >= NS) pipe::bar_sync(pipe::kBarEmpty0 + buf, NT);
+#ifdef SGM_CHECKED
+      // every consumer warp has released every earlier use of this slab; then poison it
+      if (pw == 0 && lane == 0 && ckt[2 + buf] != NC * (it / NS)) check::fail(cfg.ck, check::kReleaseCount);
+      check::jitter(unsigned(item * 64 + warp));
+      {
+        double* ps = slabs + buf * cfg.slab;
+        for (int i = pw * 32 + lane; i < cfg.slab; i += cfg.NP * 32) ps[i] = check::kPoison;
+        pipe::fence_proxy_async_smem();
+        if (cfg.NP > 1) pipe::bar_sync(6, cfg.NP * 32);
+        else __syncwarp();
+      }
+#endif
       int c = 0, tile = cfg.reverse ? cfg.nitems - 1 - item : item;
       while (c < 2 && tile >= cfg.tiles[c]) tile -= cfg.tiles[c++];
       const CompGeom& g = cfg.g[c];
@@ -159,6 +183,9 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
         // one producer warp drives the bulk-copy engine; completion is counted on full_mb[buf]
         if (pw == 0) {
           const unsigned bytes = unsigned(cnt) * unsigned(g.X) * 8u;
+#ifdef SGM_CHECKED
+          if (lane == 0) ckt[buf] = item;  // released to the consumers by the arrive below
+#endif
           if (lane == 0) pipe::mbar_arrive_expect_tx(full_mb + buf, (cfg.dbg & 2) ? 0u : bytes);
           if (!(cfg.dbg & 2)) {
             if (g.lbulk) {
@@ -223,6 +250,9 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
           for (int q = 0; q < LPT; ++q) slab[i * W + q * 32 + lane] = 0.0;
       }
       pipe::cp_async_wait_all();
+#ifdef SGM_CHECKED
+      if (pw == 0 && lane == 0) ckt[buf] = item;
+#endif
       pipe::bar_arrive(pipe::kBarFull0 + buf, NT);
     }
     return;
@@ -234,9 +264,19 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
   pipe::mbar_wait(tab_mb, 0);
   int it = 0;
   for (int item = blockIdx.x; item < cfg.nitems; item += G, ++it) {
-    const int buf = it & 1;
-    if (bulk) pipe::mbar_wait(full_mb + buf, unsigned(it >> 1) & 1u);
+    const int buf = NS == 2 ? (it & 1) : 0;
+    if (bulk) pipe::mbar_wait(full_mb + buf, unsigned(NS == 2 ? it >> 1 : it) & 1u);
     else pipe::bar_sync(pipe::kBarFull0 + buf, NT);
+#ifdef SGM_CHECKED
+    if (lane == 0 && ckt[buf] != item) check::fail(cfg.ck, check::kStageTag);
+    check::jitter(unsigned(item * 64 + warp + 16));
+    const bool early_release = (cfg.inject & 1) != 0;  // injected fault: release before reading
+    if (early_release) {
+      __syncwarp();
+      if (lane == 0) atomicAdd(&ckt[2 + buf], 1);
+      if (item + NS * G < cfg.nitems) pipe::bar_arrive(pipe::kBarEmpty0 + buf, NT);
+    }
+#endif
     int c = 0, tile = cfg.reverse ? cfg.nitems - 1 - item : item;
     while (c < 2 && tile >= cfg.tiles[c]) tile -= cfg.tiles[c++];
     const CompGeom& g = cfg.g[c];
@@ -249,7 +289,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
     const int S = (L + SEG - 1) / SEG;
     const bool live = s < S;
     if (cfg.dbg & 1) {
-      if (item + 2 * G < cfg.nitems) pipe::bar_arrive(pipe::kBarEmpty0 + buf, NT);
+      if (item + NS * G < cfg.nitems) pipe::bar_arrive(pipe::kBarEmpty0 + buf, NT);
       continue;
     }
     // ---- my lines' segment start in the slab; consecutive line elements are ES apart
@@ -333,6 +373,12 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
       for (int j = 1; j <= M; ++j)
 #pragma unroll
         for (int q = 0; q < LPT; ++q) tails[(s * M + j - 1) * TW + q * 32 + lane] = v[SEG - j][q];
+#ifdef SGM_CHECKED
+      __syncwarp();
+      if (lane == 0) ckt[4 + s] = item;
+      check::jitter(unsigned(item * 64 + warp + 32));
+      if (!(cfg.inject & 2))
+#endif
       pipe::bar_sync(pipe::kBarCons, NC * 32);
       double hist[M][LPT];
 #pragma unroll
@@ -345,6 +391,9 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
       const double* tr = T0 + (tb * SEG + SEG - 1) * RS + RL::F;  // row SEG - 1 of segment tb
       const double* tl = tails + tb * M * TW + lane;
       for (int t = tb; t < s; ++t, tr += SEG * RS, tl += M * TW) {
+#ifdef SGM_CHECKED
+        if (lane == 0 && ckt[4 + t] != item) check::fail(cfg.ck, check::kTailTag);
+#endif
         double nh[M][LPT];
 #pragma unroll
         for (int j = 1; j <= M; ++j) {
@@ -388,6 +437,11 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
       for (int j = 1; j <= M; ++j)
 #pragma unroll
         for (int q = 0; q < LPT; ++q) heads[(s * M + j - 1) * TW + q * 32 + lane] = v[j - 1][q];
+#ifdef SGM_CHECKED
+      __syncwarp();
+      if (lane == 0) ckt[20 + s] = item;
+      check::jitter(unsigned(item * 64 + warp + 48));
+#endif
       pipe::bar_sync(pipe::kBarCons, NC * 32);
       if (s < S - 1) {
         double fut[M][LPT];
@@ -399,6 +453,9 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
         const double* br = T0 + te * SEG * RS + RL::B;  // row 0 of segment te
         const double* hd = heads + te * M * TW + lane;
         for (int t = te; t > s; --t, br -= SEG * RS, hd -= M * TW) {
+#ifdef SGM_CHECKED
+          if (lane == 0 && ckt[20 + t] != item) check::fail(cfg.ck, check::kHeadTag);
+#endif
           double nf[M][LPT];
 #pragma unroll
           for (int j = 1; j <= M; ++j) {
@@ -539,7 +596,12 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
         }
       }
     }
-    if (item + 2 * G < cfg.nitems) pipe::bar_arrive(pipe::kBarEmpty0 + buf, NT);
+#ifdef SGM_CHECKED
+    if (early_release) continue;
+    __syncwarp();
+    if (lane == 0) atomicAdd(&ckt[2 + buf], 1);
+#endif
+    if (item + NS * G < cfg.nitems) pipe::bar_arrive(pipe::kBarEmpty0 + buf, NT);
   }
   if (XAX && bulk && warp == 0) pipe::bulk_wait0();
 }

@@ -13,8 +13,9 @@
 namespace sgm {
 namespace sweeplaunch {
 
+// nslab: 2 double-buffered slabs, 1 a single slab (long lines); a.dry: check the fit only
 template <int P, int HB, int SEG, int LPT, int MODE, int OPS>
-bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
+bool launch_sweep_t(const SweepArgs& a, int nslab, cudaStream_t st) {
   using sweep::Cfg;
   Cfg cfg;
   std::memset(&cfg, 0, sizeof(cfg));
@@ -82,9 +83,16 @@ bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
   cfg.dbg = tune_int("SGM_PIPE_DBG", 0);
   cfg.reverse = tune_int("SGM_SNAKE", 1) ? a.reverse : 0;
   constexpr int M = P - 1;
-  const size_t smem = (size_t(cfg.ntabs) * cfg.tab_dbl + size_t(2) * cfg.slab + size_t(2) * cfg.NC * M * TW + 4) *
-                      sizeof(double);
+  cfg.nslab = nslab;
+  size_t smem = (size_t(cfg.ntabs) * cfg.tab_dbl + size_t(nslab) * cfg.slab + size_t(2) * cfg.NC * M * TW + 4) *
+                sizeof(double);
+#ifdef SGM_CHECKED
+  smem += check::kSmemInts * sizeof(int);
+  cfg.ck = check_buffer();
+  cfg.inject = check_inject();
+#endif
   if (smem > 227 * 1024) return false;
+  if (a.dry) return true;
   const int NT = (cfg.NC + cfg.NP) * 32;
   static unsigned long long attr_done = 0;
   if (first_on_device(attr_done))
@@ -106,11 +114,37 @@ bool launch_sweep_t(const SweepArgs& a, cudaStream_t st) {
 
 template <int P, int HB, int SEG, int MODE, int OPS>
 bool launch_sweep_m(const SweepArgs& a, cudaStream_t st) {
-  // two lines per thread when the register budget allows (SEG <= 17) and the slabs fit
-  if constexpr (SEG <= 17) {
-    if (tune_int("SGM_LPT", 2) == 2 && launch_sweep_t<P, HB, SEG, 2, MODE, OPS>(a, st)) return true;
+  // two lines per thread when the register budget allows (SEG <= 17) and the slabs fit; double
+  // buffering first, then a single slab (long lines)
+  for (int nslab = 2; nslab >= 1; --nslab) {
+    if constexpr (SEG <= 17) {
+      if (tune_int("SGM_LPT", 2) == 2 && launch_sweep_t<P, HB, SEG, 2, MODE, OPS>(a, nslab, st)) return true;
+    }
+    if (launch_sweep_t<P, HB, SEG, 1, MODE, OPS>(a, nslab, st)) return true;
   }
-  return launch_sweep_t<P, HB, SEG, 1, MODE, OPS>(a, st);
+  // two distinct line-operator tables that do not fit together: one launch per table (the
+  // components are independent); both fits are checked before anything is launched
+  if (a.tabs[1] != nullptr && a.tabs[1] != a.tabs[0]) {
+    SweepArgs sub[2];
+    for (int t = 0; t < 2; ++t) {
+      sub[t] = a;
+      sub[t].ncomp = 0;
+      sub[t].tabs[0] = a.tabs[t];
+      sub[t].tabs[1] = nullptr;
+      for (int c = 0; c < a.ncomp; ++c)
+        if (a.comp[c].tslot == t) {
+          sub[t].comp[sub[t].ncomp] = a.comp[c];
+          sub[t].comp[sub[t].ncomp++].tslot = 0;
+        }
+      sub[t].dry = 1;
+      if (sub[t].ncomp > 0 && !launch_sweep_m<P, HB, SEG, MODE, OPS>(sub[t], st)) return false;
+      sub[t].dry = a.dry;
+    }
+    for (int t = 0; t < 2; ++t)
+      if (sub[t].ncomp > 0) launch_sweep_m<P, HB, SEG, MODE, OPS>(sub[t], st);
+    return true;
+  }
+  return false;
 }
 
 template <int P, int SEG, int MODE>

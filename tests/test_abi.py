@@ -177,6 +177,23 @@ def test_product_library_ignores_tuning_environment():
     assert r.stdout.split() == ["2", "7", "0"], r.stdout + r.stderr
 
 
+def test_verification_build_is_separate():
+    """The protocol checks of csrc/check.cuh live only in libsgm_checked.so: the product library
+    answers sgm_check_read with SGM_E_UNSUPPORTED (and reads no SGM_CHECK_INJECT, see above); the
+    verification build, when present, exports the same C ABI."""
+    n, f = ctypes.c_uint(7), ctypes.c_uint(7)
+    assert S.sgm_check_read(1, ctypes.byref(n), ctypes.byref(f)) == 2
+    assert (n.value, f.value) == (7, 7)
+    assert "checked" not in S.sgm_version().decode()
+    chk = os.path.join(os.path.dirname(S.LIB_PATH), "libsgm_checked.so")
+    if os.path.exists(chk):
+        lib = ctypes.CDLL(chk)
+        for nm in _declared():
+            assert hasattr(lib, nm), nm
+        lib.sgm_version.restype = ctypes.c_char_p
+        assert b"checked" in lib.sgm_version()
+
+
 def test_rational_map_host_geometry():
     """A rational (NURBS) map through the C ABI: the plan's physical quadrature points equal the
     oracle's quotient-rule evaluation (quarter annulus), the Hodge stars are general, and

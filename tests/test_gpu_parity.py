@@ -807,3 +807,30 @@ def test_general_hodge_bitwise_reproducible(p, n):
         pl.step(d, e, b, h, 0.001, 5)
         outs.append((d, e, b, h))
     assert all(torch.equal(a, b) for a, b in zip(*outs))
+
+
+@pytest.mark.parametrize("p", [2, 3, 4])
+@pytest.mark.parametrize("axis", [0, 1, 2])
+def test_maximum_line_length(p, axis):
+    """Lines of the maximum length the plan accepts (n_el + p - 1 = 392, include/sgm.h) along each
+    axis: the sweeps fall back to a single slab and, where two line-operator tables do not fit
+    together, to one launch per table (sweep_launch.cuh).  Hodge star and 3 steps against the oracle;
+    scheme 1 at p = 4 (the p + 1 wide-band layout) as well."""
+    from oracle.structured import TierB1
+    n = [3, 2, 4]
+    n[axis] = 393 - p
+    n = tuple(n)
+    schemes = (2, 1) if p == 4 else (2,)
+    for scheme in schemes:
+        pl = S.Plan(n, p)
+        if scheme == 1:
+            pl.set_scheme(1)
+        tb = TierB(p, n) if scheme == 2 else TierB1(p, n)
+        st = _state(tb, 31 + axis)
+        y = torch.empty(tb.N_e, dtype=torch.float64, device="cuda")
+        pl.hodge_star(S.MASS_EPS, dev(st[0]), y)
+        assert rel(host(y), tb.hodge_eps(st[0])) < 1e-10, scheme
+        dt = 0.05 / max(n)
+        out = _run_gpu(pl, st, dt, 3)
+        for a_, b_ in zip(out, tb.run(*st, dt, 3)):
+            assert rel(a_, b_) < 1e-10, scheme
