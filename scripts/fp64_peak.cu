@@ -32,3 +32,40 @@ extern "C" int run_dfma(int blocks, int threads, int iters, float* ms) {
   cudaFree(out);
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
+
+// DMMA (mma.sync m8n8k4 f64) issue throughput: 4 independent accumulator tiles per warp
+extern "C" __global__ void dmma_kernel(double* out, int iters, double a0, double b0) {
+  double a = a0 + threadIdx.x * 1e-12, b = b0 - threadIdx.x * 1e-12;
+  double c[4][2];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) c[t][0] = c[t][1] = t * 1e-9;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                     : "+d"(c[t][0]), "+d"(c[t][1])
+                     : "d"(a), "d"(b));
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int t = 0; t < 4; ++t) s += c[t][0] + c[t][1];
+  if (s == 12345.678) out[blockIdx.x] = s;
+}
+
+extern "C" int run_dmma(int blocks, int threads, int iters, float* ms) {
+  double* out = nullptr;
+  cudaMalloc(&out, sizeof(double) * blocks);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  dmma_kernel<<<blocks, threads>>>(out, iters, 1e-3, 1e-3);
+  cudaEventRecord(e0);
+  dmma_kernel<<<blocks, threads>>>(out, iters, 1e-3, 1e-3);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(ms, e0, e1);
+  cudaFree(out);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}

@@ -33,6 +33,25 @@ def dfma():
     return best, sms
 
 
+def dmma():
+    """mma.sync m8n8k4 f64 (DMMA) throughput: 512 FLOPs per warp instruction."""
+    so = "/tmp/fp64_peak.so"
+    lib = ctypes.CDLL(so)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    best = None
+    for per_sm, threads in ((4, 256), (8, 256), (2, 512), (1, 128), (2, 128)):
+        blocks, iters = per_sm * sms, 2048
+        ms = ctypes.c_float()
+        assert lib.run_dmma(blocks, threads, iters, ctypes.byref(ms)) == 0
+        flops = 512.0 * 8 * 4 * iters * blocks * (threads // 32)
+        tf = flops / (ms.value * 1e-3) / 1e12
+        rec = {"blocks": blocks, "threads": threads, "ms": ms.value, "tflops": tf}
+        print("dmma", rec)
+        if best is None or tf > best["tflops"]:
+            best = rec
+    return best
+
+
 def dgemm(n=8192):
     a = torch.randn(n, n, dtype=torch.float64, device="cuda")
     b = torch.randn(n, n, dtype=torch.float64, device="cuda")
@@ -51,6 +70,7 @@ def dgemm(n=8192):
 
 def main(tag):
     d, sms = dfma()
+    mm = dmma()
     g = dgemm()
     try:
         import pynvml as N
@@ -60,10 +80,10 @@ def main(tag):
         clk_max = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
     except Exception:
         clk = clk_max = None
-    out = {"gpu": torch.cuda.get_device_name(0), "sms": sms, "dfma": d, "dgemm_tflops": g,
+    out = {"gpu": torch.cuda.get_device_name(0), "sms": sms, "dfma": d, "dmma": mm, "dgemm_tflops": g,
            "sm_mhz_after": clk, "sm_max_mhz": clk_max,
            "dfma_lanes_per_sm_per_cycle": (d["tflops"] * 1e12 / 2 / sms / (clk_max * 1e6)) if clk_max else None,
-           "how": "scripts/fp64_peak.py: DFMA chains kernel (CUDA events) and torch.matmul float64 8192^3 (cuBLAS)"}
+           "how": "scripts/fp64_peak.py: DFMA chains kernel, DMMA (mma.sync m8n8k4 f64) chains kernel (CUDA events) and torch.matmul float64 8192^3 (cuBLAS)"}
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     path = os.path.join(ROOT, "gpurun_out", f"{tag}_fp64_peak.json")  # copied to profiles/ by hand
     json.dump(out, open(path, "w"), indent=1)
