@@ -16,8 +16,8 @@
 //   * jitter: random __nanosleep delays at every hand-off point perturb the interleaving of the
 //     warps and CTAs from launch to launch (results must stay bit-identical run to run);
 //   * fault injection (SGM_CHECK_INJECT, checked builds only) breaks one protocol step on purpose
-//     to show that the checks above detect it: bit 0 = consumers release a slab at the start of
-//     their work instead of the end (a WAR race with the next fill), bit 1 = consumers skip the
+//     to show that the checks above detect it: bit 0 = consumers release a slab before reading
+//     their rows from it (a WAR race with the next fill), bit 1 = consumers skip the
 //     barrier in front of the history scan (a RAW race on the tails).
 // Violations are counted in a device buffer (count, first code) read by sgm_check_read (sgm.h).
 // The product build compiles none of this.

@@ -267,15 +267,23 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
     const int buf = NS == 2 ? (it & 1) : 0;
     if (bulk) pipe::mbar_wait(full_mb + buf, unsigned(NS == 2 ? it >> 1 : it) & 1u);
     else pipe::bar_sync(pipe::kBarFull0 + buf, NT);
+    // release of the slab to the producers: strided passes as soon as every consumer warp holds its
+    // rows in registers (the slab is dead after that: results go straight to global memory, and
+    // the producers stage tile t+2 while tile t is computed); x passes after the store (the slab
+    // stages the output lines)
+    bool released = false;
+    auto release = [&]() {
+#ifdef SGM_CHECKED
+      __syncwarp();
+      if (lane == 0) atomicAdd(&ckt[2 + buf], 1);
+#endif
+      if (item + NS * G < cfg.nitems) pipe::bar_arrive(pipe::kBarEmpty0 + buf, NT);
+      released = true;
+    };
 #ifdef SGM_CHECKED
     if (lane == 0 && ckt[buf] != item) check::fail(cfg.ck, check::kStageTag);
     check::jitter(unsigned(item * 64 + warp + 16));
-    const bool early_release = (cfg.inject & 1) != 0;  // injected fault: release before reading
-    if (early_release) {
-      __syncwarp();
-      if (lane == 0) atomicAdd(&ckt[2 + buf], 1);
-      if (item + NS * G < cfg.nitems) pipe::bar_arrive(pipe::kBarEmpty0 + buf, NT);
-    }
+    if (cfg.inject & 1) release();  // injected fault: release before reading
 #endif
     int c = 0, tile = cfg.reverse ? cfg.nitems - 1 - item : item;
     while (c < 2 && tile >= cfg.tiles[c]) tile -= cfg.tiles[c++];
@@ -289,7 +297,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
     const int S = (L + SEG - 1) / SEG;
     const bool live = s < S;
     if (cfg.dbg & 1) {
-      if (item + NS * G < cfg.nitems) pipe::bar_arrive(pipe::kBarEmpty0 + buf, NT);
+      if (!released) release();
       continue;
     }
     // ---- my lines' segment start in the slab; consecutive line elements are ES apart
@@ -320,6 +328,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
         }
       }
     }
+    if (!XAX && !released) release();
     // ---- phase A: band mat-vec fused with the zero-history forward substitution
 #pragma unroll
     for (int k = 0; k < SEG; ++k) {
@@ -596,12 +605,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
         }
       }
     }
-#ifdef SGM_CHECKED
-    if (early_release) continue;
-    __syncwarp();
-    if (lane == 0) atomicAdd(&ckt[2 + buf], 1);
-#endif
-    if (item + NS * G < cfg.nitems) pipe::bar_arrive(pipe::kBarEmpty0 + buf, NT);
+    if (!released) release();
   }
   if (XAX && bulk && warp == 0) pipe::bulk_wait0();
 }
