@@ -65,7 +65,10 @@ typedef enum {
   SGM_E_INVALID_ARG = 1,       /* NULL/misaligned pointer, n_el < 1, dt non-finite, n_steps < 0,
                                   bad enum, too-small workspace, host-only plan */
   SGM_E_UNSUPPORTED = 2,       /* p < 2, p > SGM_PMAX, or extents beyond the kernel
-                                  tiling limits (n_el + p - 1 > 392 along an axis) */
+                                  indexing limit: a form component above 2^31 - 2^20 elements,
+                                  i.e. (n_x+p-1)(n_y+p-1)(n_z+p-1) (n ~ 1285 per axis for a cube).
+                                  Lines longer than 392 (n_el + p - 1) are swept in overlapping
+                                  windows of at most 392 rows */
   SGM_E_GEOMETRY = 3,          /* det DF <= 0 or non-finite at a quadrature point */
   SGM_E_MATERIAL = 4,          /* eps or mu <= 0 or non-finite at a quadrature point */
   SGM_E_SINGULAR = 5,          /* zero pivot or backward error > 1e-13 in a no-pivot 1D LU
@@ -291,7 +294,9 @@ sgm_status sgm_geometry_interpolate(const int n_el[3], int degree, const double*
    tests run every option).  Synchronous; invalidates the captured graphs. */
 #define SGM_OPT_FULL_SCHEDULE 0x1u /* separable stars sweep every axis of every Kronecker factor (no
                                       diagonal-factor shortcut) */
-#define SGM_OPT_EXACT_SPIKE 0x2u   /* untruncated SPIKE history/future scans (reading Z23 off) */
+#define SGM_OPT_EXACT_SPIKE 0x2u   /* untruncated SPIKE history/future scans (reading Z23 off) on
+                                      lines of at most 392 rows (longer lines are windowed: always
+                                      the truncated reach) */
 #define SGM_OPT_SERIAL 0x4u        /* no concurrent sweep launches */
 #define SGM_OPT_NO_GRAPH 0x8u      /* sgm_step / sgm_step_composed enqueue directly (no graph replay) */
 #define SGM_OPT_FUSED 0x10u        /* separable scheme-2 stars: the Ampere / Faraday update fused into

@@ -219,6 +219,7 @@ void sweep_pass(const Plan& P, int kind, int axis, double* const in[3], double* 
   a.reverse = reverse;
   a.spike_kh = std::max(P.spike_kh[axis][op_own], P.spike_kh[axis][op_oth]);
   a.spike_kf = std::max(P.spike_kf[axis][op_own], P.spike_kf[axis][op_oth]);
+  a.wscratch = P.win_scratch;
   for (int c = 0; c < 3; ++c) {
     comp_shape(P, kind, c, a.comp[c].ext);
     a.comp[c].in = in[c];
@@ -286,6 +287,7 @@ void sweep_pass_list(const Plan& P, int kind, const PassComp* pc, int n, cudaStr
   }
   a.tab_rows = P.rpad[pc[0].axis];
   a.reverse = reverse;
+  a.wscratch = P.win_scratch;
   for (int i = 0; i < n; ++i) {
     const PassComp& q = pc[i];
     const int axis = q.axis;
@@ -1099,8 +1101,10 @@ sgm_status sgm_plan_create(const sgm_plan_desc* desc, sgm_plan* out) {
   if (p < SGM_PMIN || p > SGM_PMAX) return fail(SGM_E_UNSUPPORTED, "degree outside the compiled range 2..4");
   int Q = desc->quad_points == 0 ? p + 1 : desc->quad_points;
   if (Q < p + 1 || Q > 8) return fail(SGM_E_INVALID_ARG, "quad_points must be 0 or in [p+1, 8]");
-  for (int a = 0; a < 3; ++a)
-    if (desc->n_el[a] + p - 1 > kMaxLine) return fail(SGM_E_UNSUPPORTED, "line length n_el + p - 1 above 392");
+  // lines longer than kMaxLine are swept in overlapping windows (launch_sweep); the kernels index
+  // the elements of one component with 32-bit integers
+  if (long(desc->n_el[0] + p - 1) * (desc->n_el[1] + p - 1) * (desc->n_el[2] + p - 1) > kMaxCompElems)
+    return fail(SGM_E_UNSUPPORTED, "a form component above 2^31 - 2^20 elements (32-bit indices)");
   Plan* P = new (std::nothrow) Plan();
   if (!P) return fail(SGM_E_NOMEM, "out of host memory");
   P->p = p;
@@ -1159,6 +1163,16 @@ sgm_status sgm_plan_create(const sgm_plan_desc* desc, sgm_plan* out) {
       }
       cudaMemcpy(P->wide_dev, P->wide_host.data(), wb, cudaMemcpyHostToDevice);
     }
+    if (std::max({P->ax[0].b, P->ax[1].b, P->ax[2].b}) > kMaxLine) {
+      // lines swept in windows: in-place sweeps read their input from a copy (launch_sweep)
+      const size_t cb = size_t(P->ax[0].b) * P->ax[1].b * P->ax[2].b * sizeof(double);
+      if (cudaMalloc(&P->win_scratch, cb) != cudaSuccess) {
+        cudaFree(P->tables_dev);
+        cudaFree(P->wide_dev);
+        delete P;
+        return fail(SGM_E_NOMEM, "cudaMalloc failed for the window scratch");
+      }
+    }
     {
       cudaStream_t aux;
       cudaEvent_t e1, e2;
@@ -1200,6 +1214,7 @@ sgm_status sgm_plan_destroy(sgm_plan plan) {
     if (P->graph_exec_e) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec_e));
     cudaFree(P->tables_dev);
     cudaFree(P->wide_dev);
+    cudaFree(P->win_scratch);
     cudaFree(P->basis_dev);
     cudaFree(P->first_dev);
     for (int m = 0; m < 2; ++m) cudaFree(P->mass[m].W_dev);

@@ -8,6 +8,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "kernels.cuh"
 #include "sgm_internal.h"
 #include "seg_sweep.cuh"
 
@@ -430,14 +431,15 @@ sgm_status set_spike_reach(Plan& P, std::string& err) {
     if (!P.wide_host.empty()) {
       const int RSw = RowLayoutRT(p + 1).RS;
       const double* Tw = P.wide_host.data() + size_t(a) * Rmax * RSw;
-      if (noskip) P.wide_kh[a] = P.wide_kf[a] = (X.a + SEG - 1) / SEG;
+      if (noskip && X.a <= kMaxLine) P.wide_kh[a] = P.wide_kf[a] = (X.a + SEG - 1) / SEG;
       else spike_reach(Tw, p + 1, X.a, SEG, P.wide_kh[a], P.wide_kf[a]);
     }
     const int Ls[OP_COUNT] = {X.b, X.a, X.a, X.b, X.b, X.a, X.a, X.b, X.a};
     for (int op = 0; op < OP_COUNT; ++op) {
       const int S = (Ls[op] + SEG - 1) / SEG;
       P.band_hw[a][op] = table_band_hw(T(op), p, Ls[op]);
-      if (noskip || (op >= OP_APPLY_M && op <= OP_APPLY_MT)) {
+      // (lines above kMaxLine run in windows, launch_sweep: always the truncated reach)
+      if ((noskip && Ls[op] <= kMaxLine) || (op >= OP_APPLY_M && op <= OP_APPLY_MT)) {
         P.spike_kh[a][op] = P.spike_kf[a][op] = S;
       } else {
         spike_reach(T(op), p, Ls[op], SEG, P.spike_kh[a][op], P.spike_kf[a][op]);

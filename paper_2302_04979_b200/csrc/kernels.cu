@@ -325,7 +325,78 @@ __global__ void finalize_max_kernel(const double* partials, int n_each, int ngro
 
 int partial_blocks() { return kRedBlocks; }
 
+namespace {
+bool launch_sweep_one(int p, int seg, const SweepArgs& a, cudaStream_t st) {
+  switch (p) {
+    case 2: return launch_sweep_p2(seg, a, st);
+    case 3: return launch_sweep_p3(seg, a, st);
+    case 4: return launch_sweep_p4(seg, a, st);
+    case 5: return launch_sweep_p5(seg, a, st);
+    default: return false;
+  }
+}
+
+// Line length of component c of a sweep launch (its own axis, or the launch's)
+int comp_line(const SweepArgs& a, int c) {
+  const SweepComp& C = a.comp[c];
+  const int ax = (a.axis != 0 && C.axis > 0) ? C.axis : a.axis;
+  return C.ext[ax];
+}
+
+// Lines longer than one CTA holds (kMaxLine = 14 segments) are swept in overlapping windows of at
+// most 14 segments, one launch per component and window.  A window starts on a segment boundary,
+// so its rows of the line-operator table (band, LU, spikes: all defined per row and per segment)
+// are the full line's; it runs the same truncated-SPIKE solve (reading Z23) with zero history
+// before its first segment and zero future after its last.  Segment s of the window then has the
+// full line's history once s > kh (the scan reaches back kh segments, and the first segment's
+// band mat-vec lacks the rows before the window), and the full line's future once s < S_w - 1 - kf
+// (the last segment lacks the rows after the window): the window stores only those segments, plus
+// the true line start / end in the first / last window.  Consecutive windows overlap by kh + kf + 2
+// segments.  Without a solve (band mat-vec only) one segment of margin on each side suffices.
+bool launch_sweep_windows(int p, int seg, const SweepArgs& a, cudaStream_t st) {
+  const int maxs = kMaxLine / seg;  // segments per window
+  const int kh = a.solve ? a.spike_kh + 1 : 1, kf = a.solve ? a.spike_kf + 1 : 1;
+  if (maxs - kh - kf < 1) return false;
+  const int RS = RowLayoutRT(p).RS;
+  for (int c = 0; c < a.ncomp; ++c) {
+    SweepComp C = a.comp[c];
+    if (C.in == C.out && !a.dry) {
+      // in place: the windows overlap, so every window reads the input from a copy
+      if (!a.wscratch) return false;
+      const size_t bytes = size_t(C.ext[0]) * C.ext[1] * C.ext[2] * sizeof(double);
+      if (cudaMemcpyAsync(a.wscratch, C.in, bytes, cudaMemcpyDeviceToDevice, st) != cudaSuccess) return false;
+      C.in = a.wscratch;
+    }
+    const int L = comp_line(a, c);
+    const int S = (L + seg - 1) / seg;
+    const int ax = (a.axis != 0 && C.axis > 0) ? C.axis : a.axis;
+    for (int o = 0;;) {  // o: first segment of the window
+      const int sw = std::min(maxs, S - o);
+      SweepArgs w = a;
+      w.ncomp = 1;
+      w.comp[0] = C;
+      w.comp[0].tslot = 0;
+      w.comp[0].axis = ax;
+      w.comp[0].win0 = o * seg;
+      w.comp[0].wlen = std::min(L - o * seg, sw * seg);
+      const bool last = o + sw >= S;
+      w.comp[0].slo = o == 0 ? 0 : kh * seg;
+      w.comp[0].shi = last ? w.comp[0].wlen : (sw - kf) * seg;
+      w.tabs[0] = C.tab + size_t(o) * seg * RS;
+      w.tabs[1] = nullptr;
+      w.tab_rows = sw * seg;
+      if (!launch_sweep_one(p, seg, w, st)) return false;
+      if (last) break;
+      o += sw - kf - kh;  // the next window stores from where this one stops
+    }
+  }
+  return true;
+}
+}  // namespace
+
 bool launch_sweep(int p, int seg, const SweepArgs& a, cudaStream_t st) {
+  for (int c = 0; c < a.ncomp; ++c)
+    if (comp_line(a, c) > kMaxLine) return launch_sweep_windows(p, seg, a, st);
   switch (p) {
     case 2: return launch_sweep_p2(seg, a, st);
     case 3: return launch_sweep_p3(seg, a, st);

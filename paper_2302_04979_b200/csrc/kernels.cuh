@@ -6,7 +6,9 @@
 
 namespace sgm {
 
-constexpr int kMaxLine = 392;  // <= 14 segments of <= 28 rows (sweep_kernel.cuh)
+constexpr int kMaxLine = 392;  // <= 14 segments of <= 28 rows: the longest line one sweep CTA holds
+                               // (longer lines are swept in overlapping windows, launch_sweep)
+constexpr long kMaxCompElems = (1L << 31) - (1L << 20);  // 32-bit element indices within a component
 
 // One component handled by a line sweep along `axis` (or by the update kernel: `in` = state).
 struct SweepComp {
@@ -28,6 +30,9 @@ struct SweepComp {
   const double* aw[2];
   const double* as[2];
   double ac[2];
+  // window of a long line (launch_sweep): the sweep solves rows [win0, win0 + wlen) of every line
+  // and stores window rows [slo, shi); wlen = 0: the whole line
+  int win0, wlen, slo, shi;
 };
 
 // Element-wise state update of a half step (launch_update):
@@ -60,6 +65,8 @@ struct SweepArgs {
   PrologueArgs pro;       // update kernel only
   int share_k, share_n;   // sweeps: use share_k/share_n of the resident-CTA slots (0/0 = all)
   int dry;                // fused sweeps: only check that a configuration fits (launch nothing)
+  double* wscratch;       // windowed sweeps (lines > kMaxLine) in place: a component-sized buffer the
+                          // input is copied to first (overlapping windows read rows others store)
 };
 
 // General (non-separable) Hodge apply y = M x by sum factorisation per element.

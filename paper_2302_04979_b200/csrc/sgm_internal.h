@@ -94,6 +94,7 @@ struct Plan {
   int scheme = 2;                     // 2: pairing solves; 1: mass solves
   std::vector<double> wide_host;      // scheme-1 eps tables [3][Lmax][RowLayout<p+1>::RS] (p <= 3)
   double* wide_dev = nullptr;
+  double* win_scratch = nullptr;      // one form component: input copy of in-place windowed sweeps (lines > kMaxLine)
   int wide_band_hw[3] = {}, wide_kh[3] = {}, wide_kf[3] = {};
   size_t diag_off = 0;                // offset (doubles) of the diagonal factors [3][2][Lmax]:
                                       // [axis][0] = 1/s (eps own axis), [axis][1] = s (mu other axes)

@@ -59,6 +59,8 @@ struct CompGeom {
   unsigned tmagic;  // floor((2^32 - 1) / TD)
   int bpitch;  // x axis, bulk: slab pitch of this component's lines (= L, or L + 2 when L % 4 == 0)
   int lbulk;   // x axis, bulk: 1 = one bulk copy per line (padded pitch), 0 = one per tile
+  int row0;    // window of a long line: first line element swept (0 = whole line)
+  int slo, shi;  // rows of the (window) line that are stored: [slo, shi)
 };
 
 struct Cfg {
@@ -208,7 +210,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
           const int l = l0 + j;
           double* srow = slab + j * pitch;
           if (l < g.nlines) {
-            const double* src = C.in + long(l) * g.rowlen;
+            const double* src = C.in + long(l) * g.rowlen + g.row0;
             for (int k = lane; k < g.L; k += 32) pipe::cp_async8(srow + k, src + k);
           }
           for (int k = g.L + lane; k < R; k += 32) srow[k] = 0.0;
@@ -224,7 +226,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
           for (int q = 0; q < LPT; ++q) {
             const int l = l0 + lane + 32 * q;
             ok[q] = l < g.nlines;
-            src[q] = C.in + line_base(g, 0, ok[q] ? l : 0) + long(i0) * g.gs;
+            src[q] = C.in + line_base(g, 0, ok[q] ? l : 0) + long(g.row0 + i0) * g.gs;
           }
           const long gs = g.gs;
           double* dst = slab + i0 * TW + lane;
@@ -527,27 +529,27 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
         for (int q = 0; q < LPT; ++q) {
           const int l = l0 + lane + 32 * q;
           if (l < g.nlines) {
-            double* dst = C.out + line_base(g, 0, l) + long(r0) * g.gs;
+            double* dst = C.out + line_base(g, 0, l) + long(g.row0 + r0) * g.gs;
             const long gs = g.gs;
             if (acc || aff) {
               const long off = dst - C.out;
               for (int k = 0; k < SEG; ++k, dst += gs)
-                if (r0 + k < L) {
+                if (r0 + k >= g.slo && r0 + k < g.shi) {
                   double val = acc ? fma(scq[q], v[k][q], *dst) : scq[q] * v[k][q];
                   if (C.aw[0]) val = fma(af[0], __ldg(C.aw[0] + off + k * gs), val);
                   if (C.aw[1]) val = fma(af[1], __ldg(C.aw[1] + off + k * gs), val);
                   *dst = val;
                 }
-            } else if (r0 + SEG <= L && unit) {
+            } else if (r0 >= g.slo && r0 + SEG <= g.shi && unit) {
 #pragma unroll
               for (int k = 0; k < SEG; ++k, dst += gs) *dst = v[k][q];
-            } else if (r0 + SEG <= L) {
+            } else if (r0 >= g.slo && r0 + SEG <= g.shi) {
 #pragma unroll
               for (int k = 0; k < SEG; ++k, dst += gs) *dst = scq[q] * v[k][q];
             } else {
 #pragma unroll
               for (int k = 0; k < SEG; ++k, dst += gs)
-                if (r0 + k < L) *dst = scq[q] * v[k][q];
+                if (r0 + k >= g.slo && r0 + k < g.shi) *dst = scq[q] * v[k][q];
             }
           }
         }
@@ -568,7 +570,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
         for (int q = 0; q < LPT; ++q) {
           double* cw = const_cast<double*>(cp[q]);
           const int l = min(l0 + lane + 32 * q, g.nlines - 1);
-          const long off = long(l) * g.rowlen + r0;
+          const long off = long(l) * g.rowlen + g.row0 + r0;
           const double* prev = C.out + off;
           for (int k = 0; k < SEG; ++k)
             if (r0 + k < L) {
@@ -599,9 +601,9 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
         for (int j = s; j < TW; j += NC) {
           const int l = l0 + j;
           if (l >= g.nlines) break;
-          double* dst = C.out + long(l) * g.rowlen;
+          double* dst = C.out + long(l) * g.rowlen + g.row0;
           const double* srow = slab + j * cfg.pitch;
-          for (int k = lane; k < L; k += 32) dst[k] = srow[k];
+          for (int k = g.slo + lane; k < g.shi; k += 32) dst[k] = srow[k];
         }
       }
     }

@@ -28,9 +28,12 @@ bool launch_sweep_t(const SweepArgs& a, int nslab, cudaStream_t st) {
     const int X = C.ext[0], Y = C.ext[1], Z = C.ext[2];
     // per-component axis (strided passes may mix y- and z-lines of different components)
     const int ax = (MODE != 3 && C.axis > 0) ? C.axis : a.axis;
-    g.L = C.ext[ax];
+    g.L = C.wlen > 0 ? C.wlen : C.ext[ax];  // a window of a long line, or the whole line
+    g.row0 = C.wlen > 0 ? C.win0 : 0;
+    g.slo = C.wlen > 0 ? C.slo : 0;
+    g.shi = C.wlen > 0 ? C.shi : g.L;
     g.magic = 0xffffffffu / unsigned(X);
-    g.nlines = X * Y * Z / g.L;
+    g.nlines = X * Y * Z / C.ext[ax];
     g.X = X;
     g.rowlen = X;
     g.gs = (ax == 0) ? 1 : (ax == 1 ? X : X * Y);
@@ -51,6 +54,7 @@ bool launch_sweep_t(const SweepArgs& a, int nslab, cudaStream_t st) {
     const SweepComp& C = a.comp[c];
     if ((reinterpret_cast<uintptr_t>(C.in) & 15) || (reinterpret_cast<uintptr_t>(C.out) & 15)) bulk = false;
     if ((long(C.ext[0]) * C.ext[1] * C.ext[2]) & 1) bulk = false;
+    if (C.wlen > 0) bulk = false;  // a window of x-lines is not one contiguous range
   }
   cfg.bulk = bulk ? 1 : 0;
   if (bulk) cfg.NP = 1;

@@ -90,6 +90,9 @@ def test_error_codes():
     assert S.sgm_plan_create(ctypes.byref(desc), ctypes.byref(h)) == 1      # n_el < 1
     desc = S.sgm_plan_desc((ctypes.c_int * 3)(4, 4, 4), 3, None, 2, -1)
     assert S.sgm_plan_create(ctypes.byref(desc), ctypes.byref(h)) == 1      # Q < p+1
+    # a form component above 2^31 - 2^20 elements (32-bit indices): unsupported
+    desc = S.sgm_plan_desc((ctypes.c_int * 3)(1300, 1300, 1300), 3, None, 0, -1)
+    assert S.sgm_plan_create(ctypes.byref(desc), ctypes.byref(h)) == 2
     # inverted geometry: det DF < 0
     from oracle.assemble import identity_ctrl
     ctrl = identity_ctrl(2, 3).copy()
@@ -242,3 +245,11 @@ def test_library_geometry_interpolation(p, n):
     assert np.abs(a - W.interpolate_map(p, n, W.c3_map)).max() < 1e-13
     X = np.random.default_rng(3).uniform(size=(7, 3))
     assert np.array_equal(synth.c3_map(X), W.c3_map(X))
+
+
+def test_long_lines_accepted():
+    """Lines above 392 rows are swept in overlapping windows (launch_sweep): plans with n_el + p - 1
+    above 392 along an axis are accepted (the round-1 limit), up to the 32-bit component limit."""
+    for p, n in ((2, (1000, 3, 3)), (3, (3, 700, 4)), (4, (3, 3, 1200))):
+        pl = S.Plan(n, p, device=-1)
+        assert max(max(pl.shape(S.FORM_E, c)) for c in range(3)) == max(n) + p - 1

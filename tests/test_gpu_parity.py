@@ -834,3 +834,47 @@ def test_maximum_line_length(p, axis):
         out = _run_gpu(pl, st, dt, 3)
         for a_, b_ in zip(out, tb.run(*st, dt, 3)):
             assert rel(a_, b_) < 1e-10, scheme
+
+
+@pytest.mark.parametrize("p", [2, 3, 4])
+@pytest.mark.parametrize("axis", [0, 1, 2])
+def test_long_lines_windowed(p, axis):
+    """Lines longer than one CTA holds (n_el + p - 1 > 392) are swept in overlapping windows of at
+    most 14 segments (kernels.cu launch_sweep_windows): n_el = 512 along one axis (and 1000 along x at
+    p = 3), every axis, p = 2-4.  Kronecker solves and transposes, Hodge stars, 3 steps and the full
+    three-axis schedule against the oracle; scheme 1 at p = 3."""
+    from oracle.structured import TierB1
+    n = [3, 2, 4]
+    n[axis] = 1000 if (p == 3 and axis == 0) else 512
+    n = tuple(n)
+    pl = S.Plan(n, p)
+    tb = TierB(p, n)
+    st = _state(tb, 61 + axis)
+    g = np.random.default_rng(71 + axis)
+    for which, N, split, solve in ((S.K1, tb.N_e, tb.split_e, tb.solve_K1), (S.KT1, tb.N_h, tb.split_h, tb.solve_Kt1)):
+        for T in (False, True):
+            r = g.standard_normal(N)
+            x = torch.empty(N, dtype=torch.float64, device="cuda")
+            pl.kron_solve(which, dev(r), x, transpose=T)
+            assert rel(host(x), forms.join(solve(split(r), T=T))) < solve_tol(tb), (which, T)
+    y = torch.empty(tb.N_e, dtype=torch.float64, device="cuda")
+    pl.hodge_star(S.MASS_EPS, dev(st[0]), y)
+    assert rel(host(y), tb.hodge_eps(st[0])) < 1e-10
+    yh = torch.empty(tb.N_h, dtype=torch.float64, device="cuda")
+    pl.hodge_star(S.MASS_MU, dev(st[2]), yh)
+    assert rel(host(yh), tb.hodge_mu(st[2])) < 1e-10
+    dt = 0.05 / max(n)
+    ref = tb.run(*st, dt, 3)
+    for opts in (0, S.OPT_FULL_SCHEDULE):
+        pl.set_options(opts)
+        out = _run_gpu(pl, st, dt, 3)
+        for a_, b_ in zip(out, ref):
+            assert rel(a_, b_) < 1e-10, opts
+    pl.set_options(0)
+    if p == 3:
+        pl1 = S.Plan(n, p)
+        pl1.set_scheme(1)
+        tb1 = TierB1(p, n)
+        out = _run_gpu(pl1, st, dt, 3)
+        for a_, b_ in zip(out, tb1.run(*st, dt, 3)):
+            assert rel(a_, b_) < 1e-10
