@@ -63,3 +63,21 @@ int check_inject();
 
 }  // namespace sgm
 #endif
+
+#ifdef SGM_TUNING
+#include <cuda_runtime.h>
+#include <cstddef>
+namespace sgm {
+#ifdef SGM_TUNING
+// tuning build: timeline of one selected sweep launch, [cta < 160][tile < 16][event < 8]
+constexpr size_t kTraceLen = size_t(160) * 16 * 8;
+unsigned long long* trace_buffer();
+extern unsigned long long* g_trace_ptr;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+}  // namespace sgm
+#endif

@@ -23,6 +23,7 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+
 }  // namespace pipe
 }  // namespace sgm
 

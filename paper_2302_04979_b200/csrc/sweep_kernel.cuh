@@ -13,7 +13,8 @@
 // A CTA is persistent and loops over tiles with two shared-memory slabs (one when the lines are
 // too long for two: loads and compute of a CTA then alternate):
 //   * producer warps stage tile t+1 into slab[(t+1)&1]: cp.async (LDGSTS) copies for strided axes,
-//     one bulk copy (TMA engine, mbarrier completion) per tile of whole x-lines;
+//     one bulk copy (TMA engine, mbarrier completion) per tile of whole x-lines; x tiles are also
+//     stored by the producer warp (bulk copy out of the slab the consumers wrote in place);
 //   * consumer warp s owns rows [s*SEG, (s+1)*SEG) of every line of the tile (SPIKE segment s) and
 //     runs: band mat-vec fused with the zero-history forward substitution -> tail exchange ->
 //     history scan -> spike-corrected backward substitution -> head exchange -> future scan ->
@@ -33,6 +34,18 @@
 
 namespace sgm {
 namespace sweep {
+
+#ifdef SGM_TUNING
+#define SGM_TRACE(it, ev)                                                                          \
+  do {                                                                                            \
+    if (cfg.trace && lane == 0 && blockIdx.x < 160 && (it) < 16)                                  \
+      cfg.trace[(size_t(blockIdx.x) * 16 + (it)) * 8 + (ev)] = gtimer();                          \
+  } while (0)
+#else
+#define SGM_TRACE(it, ev) \
+  do {                    \
+  } while (0)
+#endif
 
 __device__ __forceinline__ double2 ld2(const double* p) { return *reinterpret_cast<const double2*>(p); }
 
@@ -79,6 +92,7 @@ struct Cfg {
   int tiles[3];   // tiles per component
   CompGeom g[3];
   unsigned* ck;   // verification build (check.cuh): violation counters; unused otherwise
+  unsigned long long* trace;  // tuning build: timeline of this launch (check.cuh), or null
   int inject;     // verification build: fault-injection bits
 };
 
@@ -158,10 +172,35 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
   if (warp >= NC) {
     // ================================ producers ================================
     const int pw = warp - NC;
+    // x axis, bulk: the producer warp also stores each output tile (the consumers wrote it into the
+    // slab in place and arrived on EMPTY[slab]); it waits for the copy engine to have read the
+    // slab, then refills it -- the consumers never wait for a store to drain
+    const bool pst = bulk;
+    auto store_tile = [&](int it_s) {
+      const int item_s = blockIdx.x + it_s * G;
+      int c = 0, tile = cfg.reverse ? cfg.nitems - 1 - item_s : item_s;
+      while (c < 2 && tile >= cfg.tiles[c]) tile -= cfg.tiles[c++];
+      const CompGeom& g = cfg.g[c];
+      const double* slab = slabs + (NS == 2 ? (it_s & 1) : 0) * cfg.slab;
+      const int l0 = tile * TW;
+      const int cnt = min(TW, g.nlines - l0);
+      double* out = A.comp[c].out;
+      if (g.lbulk) {
+        for (int j = lane; j < cnt; j += 32) pipe::bulk_s2g(out + long(l0 + j) * g.X, slab + j * g.bpitch, unsigned(g.X) * 8u);
+        pipe::bulk_commit();
+        pipe::bulk_wait_read0();
+      } else if (lane == 0) {
+        pipe::bulk_s2g(out + long(l0) * g.X, slab, unsigned(cnt) * unsigned(g.X) * 8u);
+        pipe::bulk_commit();
+        pipe::bulk_wait_read0();  // the slab may be refilled once its contents have been read
+      }
+      __syncwarp();
+    };
     int it = 0;
     for (int item = blockIdx.x; item < cfg.nitems; item += G, ++it) {
       const int buf = NS == 2 ? (it & 1) : 0;
       if (it >= NS) pipe::bar_sync(pipe::kBarEmpty0 + buf, NT);
+      if (pst && it >= NS && pw == 0) store_tile(it - NS);
 #ifdef SGM_CHECKED
       // every consumer warp has released every earlier use of this slab; then poison it
       if (pw == 0 && lane == 0 && ckt[2 + buf] != NC * (it / NS)) check::fail(cfg.ck, check::kReleaseCount);
@@ -181,6 +220,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
       double* slab = slabs + buf * cfg.slab;
       const int l0 = tile * TW;
       const int cnt = min(TW, g.nlines - l0);
+      if (pw == 0) SGM_TRACE(it, 0);
       if (bulk) {
         // one producer warp drives the bulk-copy engine; completion is counted on full_mb[buf]
         if (pw == 0) {
@@ -255,7 +295,16 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
 #ifdef SGM_CHECKED
       if (pw == 0 && lane == 0) ckt[buf] = item;
 #endif
+      if (pw == 0) SGM_TRACE(it, 1);
       pipe::bar_arrive(pipe::kBarFull0 + buf, NT);
+    }
+    if (pst) {
+      // the last (up to NS) output tiles
+      for (int k = max(0, it - NS); k < it; ++k) {
+        pipe::bar_sync(pipe::kBarEmpty0 + (NS == 2 ? (k & 1) : 0), NT);
+        if (pw == 0) store_tile(k);
+      }
+      if (pw == 0) pipe::bulk_wait0();
     }
     return;
   }
@@ -267,8 +316,10 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
   int it = 0;
   for (int item = blockIdx.x; item < cfg.nitems; item += G, ++it) {
     const int buf = NS == 2 ? (it & 1) : 0;
+    if (s == 0) SGM_TRACE(it, 2);
     if (bulk) pipe::mbar_wait(full_mb + buf, unsigned(NS == 2 ? it >> 1 : it) & 1u);
     else pipe::bar_sync(pipe::kBarFull0 + buf, NT);
+    if (s == 0) SGM_TRACE(it, 3);
     // release of the slab to the producers: strided passes as soon as every consumer warp holds its
     // rows in registers (the slab is dead after that: results go straight to global memory, and
     // the producers stage tile t+2 while tile t is computed); x passes after the store (the slab
@@ -279,7 +330,8 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
       __syncwarp();
       if (lane == 0) atomicAdd(&ckt[2 + buf], 1);
 #endif
-      if (item + NS * G < cfg.nitems) pipe::bar_arrive(pipe::kBarEmpty0 + buf, NT);
+      // (producer-side stores take every slab back, the last ones included)
+      if ((XAX && bulk) || item + NS * G < cfg.nitems) pipe::bar_arrive(pipe::kBarEmpty0 + buf, NT);
       released = true;
     };
 #ifdef SGM_CHECKED
@@ -378,6 +430,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
         for (int q = 0; q < LPT; ++q) v[k][q] = y[q];
       }
     }
+    if (s == 0) SGM_TRACE(it, 4);
     if (solve) {
       // ---- phase B: tails -> true history z_{r0-1..r0-M}
 #pragma unroll
@@ -391,6 +444,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
       if (!(cfg.inject & 2))
 #endif
       pipe::bar_sync(pipe::kBarCons, NC * 32);
+      if (s == 0) SGM_TRACE(it, 5);
       double hist[M][LPT];
 #pragma unroll
       for (int j = 0; j < M; ++j)
@@ -499,6 +553,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
         }
       }
     }
+    if (s == 0) SGM_TRACE(it, 6);
     // ---- phase E: scaled store (constant component scale times optional per-line diagonals)
     const double sc = C.scale;
     const bool acc = C.accum != 0;  // out += scale * result (the (e,h)-state increments)
@@ -582,19 +637,15 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
         }
       }
       if (bulk) {
+        // hand the output tile to the producer warp (it stores the slab, then refills it)
         pipe::fence_proxy_async_smem();
-        pipe::bar_sync(pipe::kBarCons, NC * 32);
-        if (g.lbulk) {
-          if (warp == 0) {
-            for (int j = lane; j < cnt; j += 32)
-              pipe::bulk_s2g(C.out + long(l0 + j) * g.X, slab + j * g.bpitch, unsigned(g.X) * 8u);
-            pipe::bulk_commit();
-            pipe::bulk_wait_read0();
-          }
-        } else if (threadIdx.x == 0) {
-          pipe::bulk_s2g(C.out + long(l0) * g.X, slab, unsigned(cnt) * unsigned(g.X) * 8u);
-          pipe::bulk_commit();
-          pipe::bulk_wait_read0();  // the slab may be refilled once its contents have been read
+        if (!released) {
+#ifdef SGM_CHECKED
+          __syncwarp();
+          if (lane == 0) atomicAdd(&ckt[2 + buf], 1);
+#endif
+          pipe::bar_arrive(pipe::kBarEmpty0 + buf, NT);
+          released = true;
         }
       } else {
         pipe::bar_sync(pipe::kBarCons, NC * 32);
@@ -608,8 +659,8 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
       }
     }
     if (!released) release();
+    if (s == 0) SGM_TRACE(it, 7);
   }
-  if (XAX && bulk && warp == 0) pipe::bulk_wait0();
 }
 
 }  // namespace sweep

@@ -97,6 +97,9 @@ bool launch_sweep_t(const SweepArgs& a, int nslab, cudaStream_t st) {
 #endif
   if (smem > 227 * 1024) return false;
   if (a.dry) return true;
+#ifdef SGM_TUNING
+  cfg.trace = trace_buffer();
+#endif
   const int NT = (cfg.NC + cfg.NP) * 32;
   static unsigned long long attr_done = 0;
   if (first_on_device(attr_done))
