@@ -35,6 +35,9 @@ st = torch.cuda.Stream()
 with torch.cuda.stream(st):
     pl.step(d, e, b, h, 1e-3, args.steps, stream=st)
 torch.cuda.synchronize()
+if not hasattr(S._lib, "sgm_tune_trace") or "SGM_TRACE_LAUNCH" not in os.environ:
+    print("product build or no SGM_TRACE_LAUNCH: steps run, no trace")
+    sys.exit(0)
 fn = S._lib.sgm_tune_trace
 fn.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 buf = np.zeros(160 * 16 * 8, dtype=np.uint64)
