@@ -14,7 +14,8 @@ PR = os.path.join(ROOT, "profiles")
 sys.path.insert(0, os.path.join(ROOT, "scripts"))
 from make_summary import launch_shares  # noqa: E402
 
-UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+UNIT = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3,
+        "ns": 1e-3, "us": 1.0, "ms": 1e3}
 
 
 def ncu_rows(path):
