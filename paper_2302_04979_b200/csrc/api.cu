@@ -100,11 +100,13 @@ sgm_status cuda_check(Plan* P, const char* where) {
 
 // Drop the captured graphs (their launches embed weights, tables, options)
 void drop_graphs(Plan& P) {
-  if (!(P.graph_exec || P.graph_exec_c || P.graph_exec_e) || P.device < 0) return;
+  if (!(P.graph_exec || P.graph_exec_c || P.graph_exec_e || P.graph_exec_m) || P.device < 0) return;
   DeviceGuard g(P.device);
   if (P.graph_exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P.graph_exec));
   if (P.graph_exec_c) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P.graph_exec_c));
   if (P.graph_exec_e) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P.graph_exec_e));
+  if (P.graph_exec_m) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P.graph_exec_m));
+  P.graph_exec_m = nullptr;
   P.graph_exec = nullptr;
   P.graph_exec_c = nullptr;
   P.graph_exec_e = nullptr;
@@ -1244,6 +1246,7 @@ sgm_status sgm_plan_destroy(sgm_plan plan) {
   if (P->device >= 0) {
     DeviceGuard g(P->device);
     if (P->graph_exec) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec));
+    if (P->graph_exec_m) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec_m));
     if (P->graph_exec_c) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec_c));
     if (P->graph_exec_e) cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec_e));
     cudaFree(P->tables_dev);
@@ -1458,6 +1461,9 @@ sgm_status sgm_plan_kernels_per_step(sgm_plan plan, int* n) {
   return SGM_OK;
 }
 
+// steps per graph of long sgm_step calls
+constexpr int kGraphChunk = 8;
+
 sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h, const double* j_hat,
                     const double* j_amp, double dt, int n_steps, void* workspace, size_t ws_bytes, void* stream) {
   sgm_status s = check_plan(plan, true);
@@ -1483,17 +1489,19 @@ sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h, c
   const bool use_graph = !P->profiling && stream != nullptr && P->graph_enabled && !(P->opts & SGM_OPT_NO_GRAPH) &&
                          (j_amp == nullptr || n_steps == 1) && !stream_capturing(st);
   if (use_graph) {
-    const GraphKey key{d, e, b, h, j_hat, j_amp, dt, 1, workspace};
-    if (!(P->graph_exec && P->graph_key == key)) {
-      if (P->graph_exec) {
-        cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(P->graph_exec));
-        P->graph_exec = nullptr;
+    // (re)capture `steps` consecutive steps with these arguments into *exec (key: arguments + steps)
+    auto capture = [&](void*& exec_slot, GraphKey& key_slot, int steps) -> sgm_status {
+      const GraphKey key{d, e, b, h, j_hat, j_amp, dt, steps, workspace};
+      if (exec_slot && key_slot == key) return SGM_OK;
+      if (exec_slot) {
+        cudaGraphExecDestroy(static_cast<cudaGraphExec_t>(exec_slot));
+        exec_slot = nullptr;
       }
       cudaGraph_t graph = nullptr;
       if (cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) != cudaSuccess)
         return cuda_check(P, "sgm_step: begin capture");
       P->launch_fail = 0;
-      step_once(*P, d, e, b, h, j_hat, j_amp, dt, w, st);
+      for (int k = 0; k < steps; ++k) step_once(*P, d, e, b, h, j_hat, j_amp, dt, w, st);
       if (cudaStreamEndCapture(st, &graph) != cudaSuccess) return cuda_check(P, "sgm_step: end capture");
       if (P->launch_fail) {  // incomplete step: do not keep (or run) it
         cudaGraphDestroy(graph);
@@ -1503,10 +1511,23 @@ sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h, c
       const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
       cudaGraphDestroy(graph);
       if (ie != cudaSuccess) return cuda_check(P, "sgm_step: graph instantiate");
-      P->graph_exec = exec;
-      P->graph_key = key;
-    }
-    for (int k = 0; k < n_steps; ++k) cudaGraphLaunch(static_cast<cudaGraphExec_t>(P->graph_exec), st);
+      exec_slot = exec;
+      key_slot = key;
+      return SGM_OK;
+    };
+    // Calls without per-step amplitudes also get a graph of kGraphChunk steps, captured together
+    // with the one-step graph at the first call with these arguments (so a later long call pays
+    // no capture): inside one graph the kernels of consecutive steps chain by programmatic
+    // dependent launch as well, where a graph boundary waits for the previous graph to finish
+    // (C2 32^3: 21.1 -> 18.2 us per step; 128^3 p = 3: 150.7 -> 147.7 us).  Long calls replay the
+    // chunk graph, the remainder the one-step graph.
+    const int chunk = j_amp == nullptr ? tune_int("SGM_GRAPH_CHUNK", kGraphChunk) : 1;
+    if ((s = capture(P->graph_exec, P->graph_key, 1)) != SGM_OK) return s;
+    if (chunk > 1 && (s = capture(P->graph_exec_m, P->graph_key_m, chunk)) != SGM_OK) return s;
+    int left = n_steps;
+    if (chunk > 1)
+      for (; left >= chunk; left -= chunk) cudaGraphLaunch(static_cast<cudaGraphExec_t>(P->graph_exec_m), st);
+    for (int k = 0; k < left; ++k) cudaGraphLaunch(static_cast<cudaGraphExec_t>(P->graph_exec), st);
     return cuda_check(P, "sgm_step (graph)");
   }
   for (int k = 0; k < n_steps; ++k) step_once(*P, d, e, b, h, j_hat, j_amp ? j_amp + k : nullptr, dt, w, st);

@@ -126,6 +126,8 @@ struct Plan {
   std::mutex fork_mu;
   void* graph_exec = nullptr;         // cudaGraphExec_t of the last captured sgm_step call
   GraphKey graph_key{};
+  void* graph_exec_m = nullptr;       // the same arguments, kGraphChunk steps in one graph
+  GraphKey graph_key_m{};
   void* graph_exec_e = nullptr;       // ... of the last captured sgm_step_eh call
   GraphKey graph_key_e{};
   void* graph_exec_c = nullptr;       // ... of the last captured sgm_step_composed call

@@ -275,6 +275,32 @@ def test_nan_poisoned_workspace_and_graph_replay():
             assert rel(host(a), r) < 1e-11
 
 
+def test_multi_step_graph_chunks():
+    """A long sgm_step call on a non-default stream replays a graph of 8 captured steps (captured
+    with the one-step graph at the first call) plus one-step graphs for the remainder: 19 steps
+    = 2 chunks + 3 single steps equal direct launches (SGM_OPT_NO_GRAPH) bit for bit and the
+    oracle to the step tolerance."""
+    p, n = 3, (12, 9, 10)
+    pl = S.Plan(n, p)
+    tb = TierB(p, n)
+    st = _state(tb, 23)
+    dt = 0.01
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        a = [dev(x) for x in st]
+        pl.step(*a, dt, 1, stream=s)     # first call: captures the one-step and the 8-step graphs
+        pl.step(*a, dt, 19, stream=s)    # 2 chunk replays + 3 one-step replays
+        pl.set_options(S.OPT_NO_GRAPH)
+        bb = [dev(x) for x in st]
+        pl.step(*bb, dt, 20, stream=s)   # direct launches
+        pl.set_options(0)
+    s.synchronize()
+    ref = tb.run(*st, dt, 20)
+    for x, y, r in zip(a, bb, ref):
+        assert torch.equal(x, y)
+        assert rel(host(x), r) < 1e-10
+
+
 def test_gpu_invariants_over_many_steps():
     """Through the GPU path only (no oracle): the scheme-2 invariants hold over 400 steps of a
     16^3 p = 3 cavity with a random state: the modified energy
