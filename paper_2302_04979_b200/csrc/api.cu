@@ -1461,8 +1461,9 @@ sgm_status sgm_plan_kernels_per_step(sgm_plan plan, int* n) {
   return SGM_OK;
 }
 
-// steps per graph of long sgm_step calls
+// steps per graph of long sgm_step calls, and the largest plan (N_e + N_h) that uses them
 constexpr int kGraphChunk = 8;
+constexpr double kGraphChunkDofs = 20e6;
 
 sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h, const double* j_hat,
                     const double* j_amp, double dt, int n_steps, void* workspace, size_t ws_bytes, void* stream) {
@@ -1519,9 +1520,11 @@ sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h, c
     // with the one-step graph at the first call with these arguments (so a later long call pays
     // no capture): inside one graph the kernels of consecutive steps chain by programmatic
     // dependent launch as well, where a graph boundary waits for the previous graph to finish
-    // (C2 32^3: 21.1 -> 18.2 us per step; 128^3 p = 3: 150.7 -> 147.7 us).  Long calls replay the
-    // chunk graph, the remainder the one-step graph.
-    const int chunk = j_amp == nullptr ? tune_int("SGM_GRAPH_CHUNK", kGraphChunk) : 1;
+    // (C2 32^3: 21.1 -> 18.2 us per step; 64^3 .. 144^3: 1.4 - 5 % per step).  Long calls replay the
+    // chunk graph, the remainder the one-step graph.  Measured slower from 160^3 on (p = 2, 3:
+    // +10 - 18 %), so plans above kGraphChunkDofs DOFs keep one-step graphs.
+    const bool small = double(P->N_e) + double(P->N_h) <= kGraphChunkDofs;
+    const int chunk = (j_amp == nullptr && small) ? tune_int("SGM_GRAPH_CHUNK", kGraphChunk) : 1;
     if ((s = capture(P->graph_exec, P->graph_key, 1)) != SGM_OK) return s;
     if (chunk > 1 && (s = capture(P->graph_exec_m, P->graph_key_m, chunk)) != SGM_OK) return s;
     int left = n_steps;
