@@ -74,7 +74,6 @@ struct CompGeom {
   int lbulk;   // x axis, bulk: 1 = one bulk copy per line (padded pitch), 0 = one per tile
   int row0;    // window of a long line: first line element swept (0 = whole line)
   int slo, shi;  // rows of the (window) line that are stored: [slo, shi)
-  int vec2;      // strided z-lines, even plane, 16-byte aligned input: 16-byte copies (2 lines a lane)
 };
 
 struct Cfg {
@@ -257,25 +256,7 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
           for (int k = g.L + lane; k < R; k += 32) srow[k] = 0.0;
         }
       } else {
-        if (MODE == 0 && LPT == 2 && g.vec2) {
-          // z-lines with an even x-y plane: a tile row is 64 consecutive doubles in memory (line l
-          // starts at element l of the plane); a lane copies lines 2 lane, 2 lane + 1 of a row with
-          // one 16-byte copy (half the copy instructions)
-          const int rpw = (g.L + NP - 1) / NP;
-          const int i0 = pw * rpw, i1 = min(g.L, i0 + rpw);
-          const int l = l0 + 2 * lane;
-          if (l < g.nlines) {  // (nlines is even: a pair is complete or absent)
-            const double* src = C.in + l + long(g.row0 + i0) * g.gs;
-            const long gs = g.gs;
-            double* dst = slab + i0 * TW + 2 * lane;
-            int i = i0;
-            for (; i + 4 <= i1; i += 4, dst += 4 * TW, src += 4 * gs) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) pipe::cp_async16(dst + k * TW, src + k * gs);
-            }
-            for (; i < i1; ++i, dst += TW, src += gs) pipe::cp_async16(dst, src);
-          }
-        } else if (MODE == 0) {
+        if (MODE == 0) {
           // rows [i0, i1) of every line of the tile; a lane copies its LPT lines, 4 rows per step
           const int rpw = (g.L + NP - 1) / NP;
           const int i0 = pw * rpw, i1 = min(g.L, i0 + rpw);

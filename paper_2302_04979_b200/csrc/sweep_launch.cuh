@@ -40,9 +40,6 @@ bool launch_sweep_t(const SweepArgs& a, int nslab, cudaStream_t st) {
     g.os = (ax == 1) ? X * Y : X;  // transverse index l / X: z (y pass) or y (z pass)
     g.TD = (ax == 0) ? Y : X;      // transverse coordinates of line l: (l % TD, l / TD)
     g.tmagic = 0xffffffffu / unsigned(g.TD);
-    g.vec2 = (MODE == 0 && ax == 2 && LPT == 2 && (g.gs % 2) == 0 && (g.nlines % 2) == 0 &&
-              !(reinterpret_cast<uintptr_t>(C.in) & 15) && tune_int("SGM_VEC2", 1))
-                 ? 1 : 0;
     cfg.tiles[c] = (g.nlines + TW - 1) / TW;
     cfg.nitems += cfg.tiles[c];
     Lmax = g.L > Lmax ? g.L : Lmax;
