@@ -35,6 +35,9 @@
 namespace sgm {
 namespace sweep {
 
+// history / future scan steps unrolled (the truncated reach is 2-3 segments at p = 3)
+constexpr int kScanUnroll = 3;
+
 #ifdef SGM_TUNING
 #define SGM_TRACE(it, ev)                                                                          \
   do {                                                                                            \
@@ -453,12 +456,13 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
       const double* T0 = tabs + (cfg.ntabs > 1 ? C.tslot : 0) * cfg.tab_dbl;
       // (truncated SPIKE: segments more than spike_kh back contribute below rounding, host-checked)
       const int tb = (cfg.dbg & 4) ? s : max(0, s - A.spike_kh);  // dbg bit 2: no history scan (timing only)
-      const double* tr = T0 + (tb * SEG + SEG - 1) * RS + RL::F;  // row SEG - 1 of segment tb
-      const double* tl = tails + tb * M * TW + lane;
-      for (int t = tb; t < s; ++t, tr += SEG * RS, tl += M * TW) {
+      // one step of the history recurrence from segment t (its tails, its forward spikes)
+      auto hstep = [&](int t) {
 #ifdef SGM_CHECKED
         if (lane == 0 && ckt[4 + t] != item) check::fail(cfg.ck, check::kTailTag);
 #endif
+        const double* tr = T0 + (t * SEG + SEG - 1) * RS + RL::F;  // row SEG - 1 of segment t
+        const double* tl = tails + t * M * TW + lane;
         double nh[M][LPT];
 #pragma unroll
         for (int j = 1; j <= M; ++j) {
@@ -476,7 +480,15 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
         for (int j = 0; j < M; ++j)
 #pragma unroll
           for (int q = 0; q < LPT; ++q) hist[j][q] = nh[j][q];
-      }
+      };
+      // the last kScanUnroll steps unrolled with predication (their loads can all be issued ahead of
+      // the dependent FMAs); any older steps by the loop first
+      constexpr int KU = kScanUnroll;
+      const int tu = (cfg.dbg & 16) ? s : max(tb, s - KU);  // dbg bit 4: no unrolled steps (tuning)
+      for (int t = tb; t < tu; ++t) hstep(t);
+#pragma unroll
+      for (int k = 0; k < KU; ++k)
+        if (s - KU + k >= tu) hstep(s - KU + k);
       // ---- phase C: spike-corrected backward substitution (zero future); segment 0 has
       // hist = 0, the correction is applied uniformly (no divergent code path)
 #pragma unroll
@@ -515,12 +527,12 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
 #pragma unroll
           for (int q = 0; q < LPT; ++q) fut[j][q] = 0.0;
         const int te = (cfg.dbg & 4) ? s : min(S - 1, s + A.spike_kf);
-        const double* br = T0 + te * SEG * RS + RL::B;  // row 0 of segment te
-        const double* hd = heads + te * M * TW + lane;
-        for (int t = te; t > s; --t, br -= SEG * RS, hd -= M * TW) {
+        auto fstep = [&](int t) {
 #ifdef SGM_CHECKED
           if (lane == 0 && ckt[20 + t] != item) check::fail(cfg.ck, check::kHeadTag);
 #endif
+          const double* br = T0 + t * SEG * RS + RL::B;  // row 0 of segment t
+          const double* hd = heads + t * M * TW + lane;
           double nf[M][LPT];
 #pragma unroll
           for (int j = 1; j <= M; ++j) {
@@ -538,7 +550,13 @@ __global__ void __launch_bounds__(512, (LPT == 1 ? 2 : 1)) sweep_kernel(const __
           for (int j = 0; j < M; ++j)
 #pragma unroll
             for (int q = 0; q < LPT; ++q) fut[j][q] = nf[j][q];
-        }
+        };
+        constexpr int KU = kScanUnroll;
+        const int tu = (cfg.dbg & 16) ? s : min(te, s + KU);
+        for (int t = te; t > tu; --t) fstep(t);
+#pragma unroll
+        for (int k = 0; k < KU; ++k)
+          if (s + KU - k <= tu) fstep(s + KU - k);
 #pragma unroll
         for (int k = 0; k < SEG; ++k) {
           double b[RL::LW];
