@@ -303,6 +303,9 @@ sgm_status sgm_geometry_interpolate(const int n_el[3], int degree, const double*
                                       the first sweep launch of each half step (fsweep_kernel.cuh;
                                       4 launches per step instead of 7, 40 instead of 48 B per
                                       DOF-update; measured slower on B200 at 128^3, DESIGN.md s. 6) */
+#define SGM_OPT_WIDE_TILES 0x20u   /* sweeps always use 64-line tiles (two lines per thread) where they
+                                      fit; by default a launch with fewer lines than two such tiles
+                                      per SM of its share uses 32-line tiles (latency bound sizes) */
 sgm_status sgm_plan_set_options(sgm_plan plan, unsigned opts);
 sgm_status sgm_plan_get_options(sgm_plan plan, unsigned* opts);
 

@@ -54,7 +54,7 @@ EPS, MU = 0, 1
 K_CLASSES = ["eps_z", "eps_y", "eps_x", "mu_z", "mu_y", "mu_x", "update", "hodge_general", "solve_z",
              "fused_eps", "fused_mu"]
 # schedule options (sgm.h SGM_OPT_*)
-OPT_FULL_SCHEDULE, OPT_EXACT_SPIKE, OPT_SERIAL, OPT_NO_GRAPH, OPT_FUSED = 0x1, 0x2, 0x4, 0x8, 0x10
+OPT_FULL_SCHEDULE, OPT_EXACT_SPIKE, OPT_SERIAL, OPT_NO_GRAPH, OPT_FUSED, OPT_WIDE_TILES = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
 TAB_G, TAB_M, TAB_GAMMA_B1, TAB_GAMMA_C2, TAB_GAMMA_BP, TAB_GAMMA_C1 = range(6)
 
 _SIGS = {
@@ -265,7 +265,8 @@ class Plan:
         check(sgm_plan_set_scheme(self.h, int(scheme)), "sgm_plan_set_scheme")
 
     def set_options(self, opts):
-        """SGM_OPT_* bits (OPT_FULL_SCHEDULE, OPT_EXACT_SPIKE, OPT_SERIAL, OPT_NO_GRAPH, OPT_FUSED)."""
+        """SGM_OPT_* bits (OPT_FULL_SCHEDULE, OPT_EXACT_SPIKE, OPT_SERIAL, OPT_NO_GRAPH, OPT_FUSED,
+        OPT_WIDE_TILES)."""
         check(sgm_plan_set_options(self.h, int(opts)), "sgm_plan_set_options")
 
     def options(self):

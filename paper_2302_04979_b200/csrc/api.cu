@@ -257,6 +257,7 @@ void sweep_pass(const Plan& P, int kind, int axis, double* const in[3], double* 
         a.comp[c].ac[t] = aff->c[t];
       }
   }
+  a.wide = (P.opts & SGM_OPT_WIDE_TILES) ? 1 : 0;
   if (!launch_sweep(P.p, P.seg[axis], a, st)) P.launch_fail = 1;
 }
 
@@ -336,6 +337,7 @@ void sweep_pass_list(const Plan& P, int kind, const PassComp* pc, int n, cudaStr
     C.dline[0] = q.dg[t0] >= 0 ? diag_factor(P, t0, q.dg[t0]) : nullptr;
     C.dline[1] = q.dg[t1] >= 0 ? diag_factor(P, t1, q.dg[t1]) : nullptr;
   }
+  a.wide = (P.opts & SGM_OPT_WIDE_TILES) ? 1 : 0;
   if (!launch_sweep(wide ? P.p + 1 : P.p, P.seg[pc[0].axis], a, st)) P.launch_fail = 1;
 }
 
@@ -1370,7 +1372,8 @@ sgm_status sgm_plan_reduced_schedule(sgm_plan plan, int* on) {
 
 sgm_status sgm_plan_set_options(sgm_plan plan, unsigned opts) {
   if (!plan) return fail(SGM_E_INVALID_ARG, "plan is NULL");
-  const unsigned all = SGM_OPT_FULL_SCHEDULE | SGM_OPT_EXACT_SPIKE | SGM_OPT_SERIAL | SGM_OPT_NO_GRAPH | SGM_OPT_FUSED;
+  const unsigned all = SGM_OPT_FULL_SCHEDULE | SGM_OPT_EXACT_SPIKE | SGM_OPT_SERIAL | SGM_OPT_NO_GRAPH | SGM_OPT_FUSED |
+                       SGM_OPT_WIDE_TILES;
   if (opts & ~all) return fail(SGM_E_INVALID_ARG, "unknown option bits");
   Plan* P = PL(plan);
   if (P->device >= 0) {

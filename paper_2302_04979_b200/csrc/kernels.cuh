@@ -65,6 +65,7 @@ struct SweepArgs {
   PrologueArgs pro;       // update kernel only
   int share_k, share_n;   // sweeps: use share_k/share_n of the resident-CTA slots (0/0 = all)
   int dry;                // fused sweeps: only check that a configuration fits (launch nothing)
+  int wide;               // SGM_OPT_WIDE_TILES: 64-line tiles even for launches with few lines
   double* wscratch;       // windowed sweeps (lines > kMaxLine) in place: a component-sized buffer the
                           // input is copied to first (overlapping windows read rows others store)
 };

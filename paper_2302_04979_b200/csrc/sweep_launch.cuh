@@ -119,13 +119,29 @@ bool launch_sweep_t(const SweepArgs& a, int nslab, cudaStream_t st) {
   return true;
 }
 
+// Lines of the launch over its share of the SMs: below two 64-line tiles per SM the launch is
+// latency bound and 32-line tiles (one line per thread, twice the work items) finish sooner
+// (64^3 p = 2/3/4 and C2 32^3: 16 / 6 / 4 / 6 % per step; from 96^3 on two lines per thread win)
+inline bool few_lines(const SweepArgs& a) {
+  long lines = 0;
+  for (int c = 0; c < a.ncomp; ++c) {
+    const SweepComp& C = a.comp[c];
+    const int ax = (a.axis != 0 && C.axis > 0) ? C.axis : a.axis;
+    lines += long(C.ext[0]) * C.ext[1] * C.ext[2] / C.ext[ax];
+  }
+  double sms = sm_count();
+  if (a.share_n > 0) sms = sms * a.share_k / a.share_n;
+  return lines < 2 * 64 * sms;
+}
+
 template <int P, int HB, int SEG, int MODE, int OPS>
 bool launch_sweep_m(const SweepArgs& a, cudaStream_t st) {
-  // two lines per thread when the register budget allows (SEG <= 17) and the slabs fit; double
-  // buffering first, then a single slab (long lines)
+  // two lines per thread when the register budget allows (SEG <= 17), the slabs fit and the launch
+  // has enough lines; double buffering first, then a single slab (long lines)
+  const int lpt = tune_int("SGM_LPT", (few_lines(a) && !a.wide) ? 1 : 2);
   for (int nslab = 2; nslab >= 1; --nslab) {
     if constexpr (SEG <= 17) {
-      if (tune_int("SGM_LPT", 2) == 2 && launch_sweep_t<P, HB, SEG, 2, MODE, OPS>(a, nslab, st)) return true;
+      if (lpt == 2 && launch_sweep_t<P, HB, SEG, 2, MODE, OPS>(a, nslab, st)) return true;
     }
     if (launch_sweep_t<P, HB, SEG, 1, MODE, OPS>(a, nslab, st)) return true;
   }

@@ -2,7 +2,7 @@
 or the verification build with SGM_LIB_VARIANT=checked: csrc/check.cuh) and save every result.
 
 Each case exercises the pipelined sweeps in one launch configuration: degrees 2-4, strided and
-x-line (bulk and line-by-line bulk) passes, ragged last tiles, several work items per CTA (slab
+x-line (bulk and line-by-line bulk) passes, 32- and 64-line tiles (SGM_OPT_WIDE_TILES), ragged last tiles, several work items per CTA (slab
 reuse), long lines (many consumer warps, truncated SPIKE reach), the schedules (reduced, full,
 serial, fused, exact spikes), the general Hodge path, the (e,h)-state step and the Kronecker
 solves.  Used by tests/test_gpu_checked.py:
@@ -28,6 +28,9 @@ CASES = {
     "p2_ragged": (2, (20, 21, 22), 0, "step"),
     "p3_ragged": (3, (33, 17, 40), 0, "step"),
     "p4_ragged": (4, (24, 30, 19), 0, "step"),
+    "p2_ragged_wide": (2, (20, 21, 22), S.OPT_WIDE_TILES, "step"),
+    "p3_ragged_wide": (3, (33, 17, 40), S.OPT_WIDE_TILES, "step"),
+    "p4_ragged_wide": (4, (24, 30, 19), S.OPT_WIDE_TILES | S.OPT_FULL_SCHEDULE, "step"),
     "p3_128": (3, (128, 128, 128), 0, "step"),
     "p2_96_serial": (2, (96, 96, 96), S.OPT_SERIAL, "step"),
     "p3_full": (3, (64, 48, 40), S.OPT_FULL_SCHEDULE, "step"),

@@ -417,7 +417,8 @@ def test_step_composed_parity(case):
 
 
 SCHEDULES = [0, S.OPT_FULL_SCHEDULE, S.OPT_FUSED, S.OPT_FUSED | S.OPT_FULL_SCHEDULE, S.OPT_SERIAL,
-             S.OPT_EXACT_SPIKE, S.OPT_NO_GRAPH, S.OPT_FUSED | S.OPT_EXACT_SPIKE]
+             S.OPT_EXACT_SPIKE, S.OPT_NO_GRAPH, S.OPT_FUSED | S.OPT_EXACT_SPIKE, S.OPT_WIDE_TILES,
+             S.OPT_WIDE_TILES | S.OPT_FULL_SCHEDULE | S.OPT_SERIAL]
 
 
 @pytest.mark.parametrize("opts", SCHEDULES)
