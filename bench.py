@@ -606,7 +606,7 @@ def main():
             jh.copy_(jhat)
             ja = torch.empty(K, dtype=torch.float64, pin_memory=True)
             ja.copy_(jamp[W:W + K])
-        hs2 = [torch.empty_like(x) for x in hs]
+        hs2 = [torch.empty(x.numel(), dtype=torch.float64, pin_memory=True) for x in hs]  # (empty_like: pageable)
         for a_, b_ in zip(hs2, hs):
             a_.copy_(b_)
         pl.step_host(*hs2, dt, K, j_hat=jh, j_amp=ja, stream=stream)  # allocates the mirrors (untimed)
@@ -618,10 +618,11 @@ def main():
         e1.record(stream)
         torch.cuda.synchronize()
         ems0 = max_over_ranks(e0.elapsed_time(e1), dist, dev)
-        h2d = state_b + (8 * N_e + 8 * K if jh is not None else 0)
+        # sgm_step_host uploads d, b, h (e is recomputed from d before any use, sgm.h) and j^, s_k
+        h2d = 8 * (N_e + 2 * N_h) + (8 * N_e + 8 * K if jh is not None else 0)
         out["e2e"] = {"value": aggregate_value(dofs, K, ems0, world), "unit": UNIT,
                       "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": state_b / K, "steps": K,
-                      "note": "C-ABI sgm_step_host on pinned HOST buffers: d, e, b, h (and j^, s_k) host->device, "
+                      "note": "C-ABI sgm_step_host on pinned HOST buffers: d, b, h (and j^, s_k) host->device, "
                               "K steps, d, e, b, h device->host, all inside the CUDA-event region on the stream"}
         del hs2
         # (2) a simulation loop through the public API: state up once, per step s_k up, sgm_step,

@@ -214,9 +214,10 @@ sgm_status sgm_step_composed(sgm_plan plan, double* d, double* e, double* b, dou
                              const double* j_hat, const double* j_amp, const double* weights,
                              int n_w, double dt, int n_steps, void* workspace, size_t ws_bytes,
                              void* stream);
-/* End-to-end variant on HOST buffers (pinned recommended): copies d,e,b,h (and j_hat, j_amp
+/* End-to-end variant on HOST buffers (pinned recommended): copies d,b,h (and j_hat, j_amp
    if given) host->device into plan-owned mirrors, runs sgm_step, copies d,e,b,h back and
-   synchronises `stream`.  Synchronous. */
+   synchronises `stream`.  Synchronous.  The input e is not copied when n_steps >= 1: a step
+   never reads it (the first half step recomputes e from d). */
 sgm_status sgm_step_host(sgm_plan plan, double* d, double* e, double* b, double* h,
                          const double* j_hat, const double* j_amp, double dt, int n_steps,
                          void* stream);

@@ -1723,7 +1723,9 @@ sgm_status sgm_step_host(sgm_plan plan, double* d, double* e, double* b, double*
   void* ws = ma + std::max(n_steps, 1);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   cudaMemcpyAsync(md, d, ne * sizeof(double), cudaMemcpyHostToDevice, st);
-  cudaMemcpyAsync(me, e, ne * sizeof(double), cudaMemcpyHostToDevice, st);
+  // e is not read by a step (the first half step recomputes it from d: K1 e = M~2 d, or the
+  // scheme-1 star from a zero start), so it is uploaded only when no step runs
+  if (n_steps == 0) cudaMemcpyAsync(me, e, ne * sizeof(double), cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(mb, b, nh * sizeof(double), cudaMemcpyHostToDevice, st);
   cudaMemcpyAsync(mh, h, nh * sizeof(double), cudaMemcpyHostToDevice, st);
   if (j_hat) cudaMemcpyAsync(mj, j_hat, ne * sizeof(double), cudaMemcpyHostToDevice, st);

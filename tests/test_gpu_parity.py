@@ -225,6 +225,17 @@ def test_step_host_equals_device():
     pl.step_host(*hs, dt, 3)
     for a, b in zip(hs, dv):
         assert np.array_equal(a, b)
+    # the input e is never read by a step (not even uploaded): NaN in, the same state out
+    hs = [x.copy() for x in st]
+    hs[1][:] = np.nan
+    pl.step_host(*hs, dt, 3)
+    for a, b in zip(hs, dv):
+        assert np.array_equal(a, b)
+    # n_steps = 0: everything round-trips unchanged
+    hs = [x.copy() for x in st]
+    pl.step_host(*hs, dt, 0)
+    for a, b in zip(hs, st):
+        assert np.array_equal(a, b)
 
 
 def test_c1_cavity_vs_tier_a():
