@@ -1515,6 +1515,9 @@ sgm_status sgm_step(sgm_plan plan, double* d, double* e, double* b, double* h, c
       const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
       cudaGraphDestroy(graph);
       if (ie != cudaSuccess) return cuda_check(P, "sgm_step: graph instantiate");
+      // upload now: otherwise the first launch of the graph pays it (the chunk graph may first
+      // run in a later call)
+      if (cudaGraphUpload(exec, st) != cudaSuccess) return cuda_check(P, "sgm_step: graph upload");
       exec_slot = exec;
       key_slot = key;
       return SGM_OK;
