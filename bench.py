@@ -571,6 +571,21 @@ def main():
                               "useful_bytes_frac": 16.0 * dofs / (vms / K * 1e-3) / 1e9 / peak}
             del e2, h2
         pl.set_options(0)
+    if (args.config == "c3" and not getattr(args, "opts", 0) and not args.no_variants):
+        # on-the-fly DF in the general Hodge (SGM_OPT_OTF_GEOMETRY, NEXT #3): the two curved stars read
+        # w_q / material (1 double per quadrature point) instead of the 6-entry weights
+        n_qp = (n ** 3 if isinstance(n, int) else int(np.prod(n))) * (p + 1) ** 3
+        w_full = 2 * 6 * 8.0 * n_qp / dofs
+        pl.set_options(S.OPT_OTF_GEOMETRY)
+        steps(0, W)
+        torch.cuda.synchronize()
+        vms, _ = timed(False)
+        vms = max_over_ranks(vms, dist, dev)
+        variants["otf_geometry"] = {"options": S.OPT_OTF_GEOMETRY, "ms_per_step": vms / K,
+                                    "value": aggregate_value(dofs, K, vms, world),
+                                    "w_bytes_per_dof_update": w_full / 6.0,
+                                    "w_bytes_per_dof_update_stored": w_full}
+        pl.set_options(0)
     env = {k: v for k, v in os.environ.items() if k.startswith("SGM_")}
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,

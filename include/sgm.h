@@ -307,6 +307,13 @@ sgm_status sgm_geometry_interpolate(const int n_el[3], int degree, const double*
 #define SGM_OPT_WIDE_TILES 0x20u   /* sweeps always use 64-line tiles (two lines per thread) where they
                                       fit; by default a launch with fewer lines than two such tiles
                                       per SM of its share uses 32-line tiles (latency bound sizes) */
+#define SGM_OPT_OTF_GEOMETRY 0x40u /* general Hodge stars on a polynomial (non-rational) curved map,
+                                      default quadrature: the brick kernel evaluates DF at the
+                                      quadrature points from the map's control points (sum
+                                      factorisation) and forms (w_q / material) / det DF * DF^T DF
+                                      itself; the plan stores 1 double per quadrature point instead
+                                      of 6.  Setting or
+                                      clearing it rebuilds the weights from the stored material. */
 sgm_status sgm_plan_set_options(sgm_plan plan, unsigned opts);
 sgm_status sgm_plan_get_options(sgm_plan plan, unsigned* opts);
 

@@ -55,6 +55,7 @@ K_CLASSES = ["eps_z", "eps_y", "eps_x", "mu_z", "mu_y", "mu_x", "update", "hodge
              "fused_eps", "fused_mu"]
 # schedule options (sgm.h SGM_OPT_*)
 OPT_FULL_SCHEDULE, OPT_EXACT_SPIKE, OPT_SERIAL, OPT_NO_GRAPH, OPT_FUSED, OPT_WIDE_TILES = 0x1, 0x2, 0x4, 0x8, 0x10, 0x20
+OPT_OTF_GEOMETRY = 0x40
 TAB_G, TAB_M, TAB_GAMMA_B1, TAB_GAMMA_C2, TAB_GAMMA_BP, TAB_GAMMA_C1 = range(6)
 
 _SIGS = {
@@ -266,7 +267,7 @@ class Plan:
 
     def set_options(self, opts):
         """SGM_OPT_* bits (OPT_FULL_SCHEDULE, OPT_EXACT_SPIKE, OPT_SERIAL, OPT_NO_GRAPH, OPT_FUSED,
-        OPT_WIDE_TILES)."""
+        OPT_WIDE_TILES, OPT_OTF_GEOMETRY)."""
         check(sgm_plan_set_options(self.h, int(opts)), "sgm_plan_set_options")
 
     def options(self):

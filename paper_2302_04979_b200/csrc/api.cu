@@ -689,6 +689,13 @@ void hodge_args(const Plan& P, int which, const double* x, double* y, HodgeArgs&
   }
   h.W = MD.W_dev;
   h.full = (MD.kind == HODGE_FULL) ? 1 : 0;
+  if (!form1 && MD.otf) {
+    h.otf = 1;
+    h.geo_tab = P.geo_dev;
+    for (int r = 0; r < 3; ++r) h.geo_ctrl[r] = P.geo_dev + P.geo_ctrl_off[r];
+    for (int a = 0; a < 3; ++a)
+      for (int sv = 0; sv < 2; ++sv) h.geo_tab_off[a][sv] = int(P.geo_tab_off[a][sv]);
+  }
   // own/other univariate spaces (space ids of basis_values_1d: Sp 0, Sp1 1, Dp1 2, Dp2 3):
   //   dual 2-forms own Dp1, other Dp2; primal 2-forms own Sp, other Sp1   (sec. 4.1)
   //   primal 1-forms own Sp1, other Sp;  dual 1-forms own Dp2, other Dp1
@@ -948,6 +955,14 @@ sgm_status set_material_impl(Plan& P, int which, const double* values, double c)
     if (cudaMalloc(&M.W_dev, W.size() * sizeof(double)) != cudaSuccess)
       return fail(SGM_E_NOMEM, "cudaMalloc failed for Hodge weights");
     cudaMemcpy(M.W_dev, W.data(), W.size() * sizeof(double), cudaMemcpyHostToDevice);
+  }
+  if (M.otf && !P.geo_dev) {
+    // on-the-fly geometry: the map's control points and S_p tables (once per plan)
+    std::vector<double> buf;
+    build_geo_buffer(P, buf, P.geo_ctrl_off, P.geo_tab_off);
+    if (cudaMalloc(&P.geo_dev, buf.size() * sizeof(double)) != cudaSuccess)
+      return fail(SGM_E_NOMEM, "cudaMalloc failed for the map tables");
+    cudaMemcpy(P.geo_dev, buf.data(), buf.size() * sizeof(double), cudaMemcpyHostToDevice);
   }
   update_scratch_need(P);
   return cuda_check(&P, "set_material");
@@ -1257,6 +1272,7 @@ sgm_status sgm_plan_destroy(sgm_plan plan) {
     cudaFree(P->basis_dev);
     cudaFree(P->first_dev);
     for (int m = 0; m < 2; ++m) cudaFree(P->mass[m].W_dev);
+    cudaFree(P->geo_dev);
     for (int m = 0; m < 2; ++m) cudaFree(P->mass1[m].W_dev);
     cudaFree(P->pcg_buf);
     cudaFree(P->mirror);
@@ -1373,7 +1389,7 @@ sgm_status sgm_plan_reduced_schedule(sgm_plan plan, int* on) {
 sgm_status sgm_plan_set_options(sgm_plan plan, unsigned opts) {
   if (!plan) return fail(SGM_E_INVALID_ARG, "plan is NULL");
   const unsigned all = SGM_OPT_FULL_SCHEDULE | SGM_OPT_EXACT_SPIKE | SGM_OPT_SERIAL | SGM_OPT_NO_GRAPH | SGM_OPT_FUSED |
-                       SGM_OPT_WIDE_TILES;
+                       SGM_OPT_WIDE_TILES | SGM_OPT_OTF_GEOMETRY;
   if (opts & ~all) return fail(SGM_E_INVALID_ARG, "unknown option bits");
   Plan* P = PL(plan);
   if (P->device >= 0) {
@@ -1382,7 +1398,18 @@ sgm_status sgm_plan_set_options(sgm_plan plan, unsigned opts) {
   }
   drop_graphs(*P);
   const bool spike_changed = ((P->opts ^ opts) & SGM_OPT_EXACT_SPIKE) != 0;
+  const bool otf_changed = ((P->opts ^ opts) & SGM_OPT_OTF_GEOMETRY) != 0;
   P->opts = opts;
+  if (otf_changed && P->device >= 0) {
+    // rebuild the general 2-form weights in the other representation from the stored material
+    DeviceGuard g(P->device);
+    for (int m = 0; m < 2; ++m) {
+      if (P->mass[m].kind != HODGE_FULL) continue;
+      const std::vector<double> v = P->mass[m].values_host;
+      const sgm_status st = set_material_impl(*P, m, v.empty() ? nullptr : v.data(), P->mass[m].material_c);
+      if (st != SGM_OK) return st;
+    }
+  }
   if (spike_changed) {
     std::string err;
     const sgm_status st = set_spike_reach(*P, err);

@@ -2,6 +2,8 @@
 // generic CTA-per-element kernel for quadrature rules other than p+1 points.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include <type_traits>
 
 #include "hodge_brick.cuh"
@@ -129,17 +131,18 @@ __global__ void hodge_general_kernel(const __grid_constant__ HodgeArgs A) {
 
 // Work decomposition of the brick kernel: bricks of E x E elements in (x, y) times z chunks sized for
 // about four work items per resident CTA (at least 4 element layers per chunk).
-template <int P, int Q, int DUAL, bool FULL>
+template <int P, int Q, int DUAL, bool FULL, bool OTF = false>
 void brick_plan(const int nel[3], int& zchunk, long& items, long& slots, size_t& smem) {
   constexpr int E = 4;
   using L = brick::Layout<P, Q, DUAL, E>;
-  smem = size_t(L::template total<FULL>()) * sizeof(double);
+  smem = size_t(L::template total<FULL, OTF>()) * sizeof(double);
   static unsigned long long attr = 0;  // per device
   if (first_on_device(attr))
-    cudaFuncSetAttribute(brick::hodge_brick_kernel<P, Q, DUAL, FULL, E>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         int(smem));
+    cudaFuncSetAttribute(brick::hodge_brick_kernel<P, Q, DUAL, FULL, E, OTF>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, brick::hodge_brick_kernel<P, Q, DUAL, FULL, E>, 256, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, brick::hodge_brick_kernel<P, Q, DUAL, FULL, E, OTF>, 256,
+                                                smem);
   if (per_sm < 1) per_sm = 1;
   slots = long(per_sm) * sm_count();
   const long bricks = long((nel[0] + E - 1) / E) * ((nel[1] + E - 1) / E);
@@ -153,13 +156,13 @@ void brick_plan(const int nel[3], int& zchunk, long& items, long& slots, size_t&
 // y = M x.  With a large enough scratch (the plan's, sized by hodge_scratch_doubles): every work item
 // writes its output patches to the scratch and hodge_gather_kernel sums them in a fixed order --
 // bitwise reproducible.  Otherwise fp64 atomics into a zeroed y.
-template <int P, int Q, int DUAL, bool FULL>
+template <int P, int Q, int DUAL, bool FULL, bool OTF = false>
 void launch_hodge_brick(const HodgeArgs& a, cudaStream_t st) {
   constexpr int E = 4;
   int zchunk = 0;
   long items = 0, slots = 0;
   size_t smem = 0;
-  brick_plan<P, Q, DUAL, FULL>(a.nel, zchunk, items, slots, smem);
+  brick_plan<P, Q, DUAL, FULL, OTF>(a.nel, zchunk, items, slots, smem);
   const long grid = items < slots ? items : slots;
   const size_t need = size_t(items) * brick::item_stride<P, Q, DUAL, E>(zchunk);
   HodgeArgs b = a;
@@ -168,7 +171,7 @@ void launch_hodge_brick(const HodgeArgs& a, cudaStream_t st) {
     for (int c = 0; c < 3; ++c)
       cudaMemsetAsync(a.y[c], 0, size_t(a.ext[c][0]) * a.ext[c][1] * a.ext[c][2] * sizeof(double), st);
   }
-  brick::hodge_brick_kernel<P, Q, DUAL, FULL, E><<<unsigned(grid), 256, smem, st>>>(b, zchunk);
+  brick::hodge_brick_kernel<P, Q, DUAL, FULL, E, OTF><<<unsigned(grid), 256, smem, st>>>(b, zchunk);
   if (b.scratch) brick::hodge_gather_kernel<P, Q, DUAL, E><<<unsigned(4 * sm_count()), 256, 0, st>>>(b, zchunk);
 }
 
@@ -177,12 +180,20 @@ size_t scratch_of(int full, const int nel[3]) {
   int zchunk = 0;
   long items = 0, slots = 0;
   size_t smem = 0;
+  size_t need = 0;
   if (full) {
     brick_plan<P, Q, DUAL, true>(nel, zchunk, items, slots, smem);
+    need = size_t(items) * brick::item_stride<P, Q, DUAL, 4>(zchunk);
+    if (DUAL <= 1) {
+      // the on-the-fly-geometry kernel (its occupancy, hence z chunks, may differ)
+      brick_plan<P, Q, DUAL, true, DUAL <= 1>(nel, zchunk, items, slots, smem);
+      need = std::max(need, size_t(items) * brick::item_stride<P, Q, DUAL, 4>(zchunk));
+    }
   } else {
     brick_plan<P, Q, DUAL, false>(nel, zchunk, items, slots, smem);
+    need = size_t(items) * brick::item_stride<P, Q, DUAL, 4>(zchunk);
   }
-  return size_t(items) * brick::item_stride<P, Q, DUAL, 4>(zchunk);
+  return need;
 }
 
 template <int P, int Q>
@@ -199,10 +210,12 @@ void launch_hodge2(const HodgeArgs& a, cudaStream_t st) {
     return;
   }
   if (a.dual) {
-    if (a.full) launch_hodge_brick<P, Q, 1, true>(a, st);
+    if (a.full && a.otf) launch_hodge_brick<P, Q, 1, true, true>(a, st);
+    else if (a.full) launch_hodge_brick<P, Q, 1, true>(a, st);
     else launch_hodge_brick<P, Q, 1, false>(a, st);
   } else {
-    if (a.full) launch_hodge_brick<P, Q, 0, true>(a, st);
+    if (a.full && a.otf) launch_hodge_brick<P, Q, 0, true, true>(a, st);
+    else if (a.full) launch_hodge_brick<P, Q, 0, true>(a, st);
     else launch_hodge_brick<P, Q, 0, false>(a, st);
   }
 }

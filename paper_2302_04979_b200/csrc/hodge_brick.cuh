@@ -57,8 +57,16 @@ struct Layout {
   // per component: Xw, Yw, Z1, Z2, U; then tables [role][axis x, y] and [role] z
   static constexpr int OFF1 = G0::TOT, OFF2 = OFF1 + G1::TOT, TAB = OFF2 + G2::TOT;
   static constexpr int WB = TAB + 2 * 2 * VXY + 2 * VZ;  // W of one element layer (cp.async staged)
-  template <bool FULL>
-  static constexpr int total() { return WB + E * E * Q * Q * Q * (FULL ? 6 : 1); }
+  // on-the-fly geometry (OTF): the staged W is w_q / material (1 per point); after it the map's
+  // partial sums A[r][s][qz][py][px] (z contracted, s = value / derivative), B[r][m][qz][Y][px]
+  // (z and y contracted, m = (val,val), (val,der), (der,val)) and the brick's x / y map tables
+  // [axis][s][e][q][k] (S_p values / derivatives at the Gauss points)
+  static constexpr int PM = E + P;  // map control points of the brick per axis (S_p, E elements)
+  static constexpr int MA = 3 * 2 * Q * PM * PM, MB = 3 * 3 * Q * E * Q * PM, MT = 2 * 2 * E * Q * NL;
+  template <bool FULL, bool OTF = false>
+  __host__ __device__ static constexpr int wdoubles() { return E * E * Q * Q * Q * (FULL && !OTF ? 6 : 1); }
+  template <bool FULL, bool OTF = false>
+  __host__ __device__ static constexpr int total() { return WB + wdoubles<FULL, OTF>() + (OTF ? MA + MB + MT : 0); }
 };
 
 struct Brick {
@@ -453,8 +461,9 @@ __global__ void __launch_bounds__(256) hodge_gather_kernel(const __grid_constant
   }
 }
 
-template <int P, int Q, int DUAL, bool FULL, int E>
+template <int P, int Q, int DUAL, bool FULL, int E, bool OTF>
 __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_constant__ HodgeArgs A, int zchunk) {
+  static_assert(!OTF || FULL, "on-the-fly geometry: general maps only");
   using L = Layout<P, Q, DUAL, E>;
   using G0 = Geo<P, Q, DUAL, E, 0>;
   using G1 = Geo<P, Q, DUAL, E, 1>;
@@ -466,6 +475,11 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
   CompSm<P, Q, DUAL, E, 2> S2(sm);
   double* tab = sm + L::TAB;
   double* Wsm = sm + L::WB;
+  // OTF: map partial sums and the brick's x / y map tables (see Layout)
+  double* MAs = Wsm + L::template wdoubles<FULL, OTF>();
+  double* MBs = MAs + (OTF ? L::MA : 0);
+  double* MTs = MBs + (OTF ? L::MB : 0);
+  constexpr int PM = L::PM;
   const int nx = A.nel[0], ny = A.nel[1], nz = A.nel[2];
   const int bx = (nx + E - 1) / E, by = (ny + E - 1) / E, bzn = (nz + zchunk - 1) / zchunk;
   const long items = long(bx) * by * bzn;
@@ -487,6 +501,16 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
       const int eg = (axis == 0 ? B.ex0 : B.ey0) + e;
       const int ng = axis == 0 ? nx : ny;
       tab[o] = (eg < ng) ? __ldg(A.basis + A.basis_off[axis][role] + size_t(eg) * Q * NL + rem) : 0.0;
+    }
+    if (OTF) {
+      // map tables of the brick's x / y elements [axis][s][e][q][k] (zeros past the mesh edge)
+      for (int o = threadIdx.x; o < L::MT; o += 256) {
+        const int axis = o / (2 * E * Q * NL), r = o % (2 * E * Q * NL), sv = r / (E * Q * NL), i = r % (E * Q * NL);
+        const int e = i / (Q * NL), rem = i % (Q * NL);
+        const int eg = (axis == 0 ? B.ex0 : B.ey0) + e;
+        const int ng = axis == 0 ? nx : ny;
+        MTs[o] = (eg < ng) ? __ldg(A.geo_tab + A.geo_tab_off[axis][sv] + size_t(eg) * Q * NL + rem) : 0.0;
+      }
     }
     __syncthreads();
     // uni[role*2 + axis]: all live elements of the brick share element 0's table (and the brick is full)
@@ -531,7 +555,7 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
     load_vz(B.ez0);
     // W of element layer ez -> Wsm (8-byte cp.async; elements past the mesh edge are skipped)
     auto stage_w = [&](int ez) {
-      constexpr int NW = FULL ? 6 : 1;
+      constexpr int NW = (FULL && !OTF) ? 6 : 1;
       // warp w copies elements w, w + 8, ...: each element's W is contiguous in HBM and in Wsm
       for (int el = threadIdx.x >> 5; el < E * E; el += 8) {
         const int ex = el % E, ey = el / E;
@@ -550,6 +574,32 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
       return A.basis + A.basis_off[2][c == 2 ? 0 : 1] + size_t(ez) * Q * NL;
     };
     for (int ez = B.ez0; ez < B.ez1; ++ez) {
+      if (OTF) {
+        // map, z: A[r][s][qz][py][px] = sum_k Tz_s[qz][k] ctrl_r[ez + k][ey0 + py][ex0 + px]
+        // (S_p: element e's functions are e .. e + p; control points past the grid edge: zero)
+        const int NXm = nx + P, NYm = ny + P;
+        const double* tz0 = A.geo_tab + A.geo_tab_off[2][0] + size_t(ez) * Q * NL;
+        const double* tz1 = A.geo_tab + A.geo_tab_off[2][1] + size_t(ez) * Q * NL;
+        for (int t = threadIdx.x; t < 3 * PM * PM; t += 256) {
+          const int r = t / (PM * PM), o = t - r * PM * PM, py = o / PM, px = o - py * PM;
+          const int gx = B.ex0 + px, gy = B.ey0 + py;
+          double c[NL];
+#pragma unroll
+          for (int k = 0; k < NL; ++k)
+            c[k] = (gx < NXm && gy < NYm) ? __ldg(A.geo_ctrl[r] + (size_t(ez + k) * NYm + gy) * NXm + gx) : 0.0;
+#pragma unroll
+          for (int qz = 0; qz < Q; ++qz) {
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int k = 0; k < NL; ++k) {
+              s0 = fma(__ldg(tz0 + qz * NL + k), c[k], s0);
+              s1 = fma(__ldg(tz1 + qz * NL + k), c[k], s1);
+            }
+            MAs[((r * 2 + 0) * Q + qz) * PM * PM + o] = s0;
+            MAs[((r * 2 + 1) * Q + qz) * PM * PM + o] = s1;
+          }
+        }
+      }
       SGM_BRICK_STAGE3U(interp_y, 1, 2 * Q * G0::PX, 2 * Q * G1::PX, 2 * Q * G2::PX)
       // W of this layer (staged by cp.async since the previous layer) must be in shared memory
       // before the x interpolation (scalar W is multiplied there) or the quadrature stage (full W)
@@ -571,6 +621,29 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
             else interp_x<P, Q, DUAL, E, 2, false>(S2, tt, Wm, A.scale[2], B.nex, B.ney);
           }
         }
+        if (OTF) {
+          // map, y: B[r][m][qz][ey*Q+qy][px] = sum_j Ty_sy[ey][qy][j] A[r][sz][qz][ey + j][px],
+          // m = 0: (sz, sy) = (val, val), 1: (val, der), 2: (der, val)
+          for (int t = threadIdx.x; t < 9 * Q * PM; t += 256) {
+            const int rm = t / (Q * PM), o = t - rm * Q * PM, qz = o / PM, px = o - qz * PM;
+            const int r = rm / 3, m = rm - r * 3, sz = m == 2 ? 1 : 0, sy = m == 1 ? 1 : 0;
+            const double* a = MAs + ((r * 2 + sz) * Q + qz) * PM * PM + px;
+            const double* ty = MTs + (1 * 2 + sy) * E * Q * NL;
+            double zv[PM];
+#pragma unroll
+            for (int py = 0; py < PM; ++py) zv[py] = a[py * PM];
+            double* b = MBs + (rm * Q + qz) * EQ * PM + px;
+#pragma unroll
+            for (int ey = 0; ey < E; ++ey)
+#pragma unroll
+              for (int qy = 0; qy < Q; ++qy) {
+                double v = 0.0;
+#pragma unroll
+                for (int j = 0; j < NL; ++j) v = fma(ty[(ey * Q + qy) * NL + j], zv[ey + j], v);
+                b[(ey * Q + qy) * PM] = v;
+              }
+          }
+        }
         __syncthreads();
       }
       if (FULL) {
@@ -579,9 +652,48 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
           const bool live = (el % E) < B.nex && (el / E) < B.ney;  // warp-uniform
           for (int i = el * QQQ + (threadIdx.x & 31); i < (el + 1) * QQQ; i += 32) {
             const double u0 = S0.U[i], u1 = S1.U[i], u2 = S2.U[i];
-            const double* w = Wsm + i * 6;
-            const double wxx = live ? w[0] : 0.0, wyy = live ? w[1] : 0.0, wzz = live ? w[2] : 0.0,
-                         wxy = live ? w[3] : 0.0, wxz = live ? w[4] : 0.0, wyz = live ? w[5] : 0.0;
+            double wxx, wyy, wzz, wxy, wxz, wyz;
+            if (OTF) {
+              // DF at the point from the map's partial sums, then the 2-form pull-back weights
+              // W = (w_q / material) / det DF * DF^T DF, as the host builds them
+              wxx = wyy = wzz = wxy = wxz = wyz = 0.0;
+              if (live) {
+                const int ex = el % E, ey = el / E, rq = i - el * QQQ;
+                const int qzp = rq / (Q * Q), qy = (rq / Q) % Q, qx = rq % Q;
+                const double* tv = MTs + (0 * 2 + 0) * E * Q * NL + (ex * Q + qx) * NL;  // x values
+                const double* td = MTs + (0 * 2 + 1) * E * Q * NL + (ex * Q + qx) * NL;  // x derivatives
+                double D[9];
+#pragma unroll
+                for (int r = 0; r < 3; ++r)
+#pragma unroll
+                  for (int m = 0; m < 3; ++m) {
+                    const double* b = MBs + ((r * 3 + m) * Q + qzp) * EQ * PM + (ey * Q + qy) * PM + ex;
+                    const double* tx = m == 0 ? td : tv;
+                    double v = 0.0;
+#pragma unroll
+                    for (int k = 0; k < NL; ++k) v = fma(tx[k], b[k], v);
+                    D[r * 3 + (m == 0 ? 0 : (m == 1 ? 1 : 2))] = v;  // dF_r / dx^_j
+                  }
+                const double det = D[0] * (D[4] * D[8] - D[5] * D[7]) - D[1] * (D[3] * D[8] - D[5] * D[6]) +
+                                   D[2] * (D[3] * D[7] - D[4] * D[6]);
+                const double g = Wsm[i] / det;
+                auto mm = [&](int a, int c) { return D[0 * 3 + a] * D[0 * 3 + c] + D[1 * 3 + a] * D[1 * 3 + c] + D[2 * 3 + a] * D[2 * 3 + c]; };
+                wxx = g * mm(0, 0);
+                wyy = g * mm(1, 1);
+                wzz = g * mm(2, 2);
+                wxy = g * mm(0, 1);
+                wxz = g * mm(0, 2);
+                wyz = g * mm(1, 2);
+              }
+            } else {
+              const double* w = Wsm + i * 6;
+              wxx = live ? w[0] : 0.0;
+              wyy = live ? w[1] : 0.0;
+              wzz = live ? w[2] : 0.0;
+              wxy = live ? w[3] : 0.0;
+              wxz = live ? w[4] : 0.0;
+              wyz = live ? w[5] : 0.0;
+            }
             S0.U[i] = wxx * u0 + wxy * u1 + wxz * u2;
             S1.U[i] = wxy * u0 + wyy * u1 + wyz * u2;
             S2.U[i] = wxz * u0 + wyz * u1 + wzz * u2;

@@ -728,6 +728,17 @@ sgm_status build_mass(Plan& P, int which, const double* values, double c, std::v
   }
   M.kind = HODGE_FULL;
   for (int k = 0; k < 3; ++k) M.scale[k] = 1.0;
+  M.otf = otf_geometry(P);
+  if (M.otf) {
+    // on-the-fly DF: only the scalar factor w_q / material per point (the brick kernel forms
+    // (w_q / material) / det DF * DF^T DF from the map, hodge_brick.cuh)
+    W.resize(P.n_qp);
+    for_each_qp(P, [&](size_t idx, int ex, int ey, int ez, int qx, int qy, int qz) {
+      double w = P.ax[0].wq[ex * P.Q + qx] * P.ax[1].wq[ey * P.Q + qy] * P.ax[2].wq[ez * P.Q + qz];
+      W[idx] = w / (values ? values[idx] : c);
+    });
+    return SGM_OK;
+  }
   W.resize(P.n_qp * 6);
   GeoEval G(P);
   for_each_qp(P, [&](size_t idx, int ex, int ey, int ez, int qx, int qy, int qz) {
@@ -747,6 +758,32 @@ sgm_status build_mass(Plan& P, int which, const double* values, double c, std::v
     o[5] = g * m(1, 2);
   });
   return SGM_OK;
+}
+
+bool otf_geometry(const Plan& P) {
+  return (P.opts & SGM_OPT_OTF_GEOMETRY) && !P.affine_diag && P.wts.empty() && P.Q == P.p + 1 && P.p >= 2 &&
+         P.p <= 4;
+}
+
+void build_geo_buffer(const Plan& P, std::vector<double>& buf, size_t ctrl_off[3], size_t tab_off[3][2]) {
+  const size_t N0 = size_t(P.n[0] + P.p) * (P.n[1] + P.p) * (P.n[2] + P.p);
+  GeoEval G(P);
+  size_t tot = 3 * N0;
+  for (int a = 0; a < 3; ++a) tot += G.v[a].size() + G.d[a].size();
+  buf.assign(tot, 0.0);
+  for (int r = 0; r < 3; ++r) {
+    ctrl_off[r] = size_t(r) * N0;
+    for (size_t i = 0; i < N0; ++i) buf[ctrl_off[r] + i] = P.ctrl[i * 3 + r];
+  }
+  size_t o = 3 * N0;
+  for (int a = 0; a < 3; ++a) {
+    tab_off[a][0] = o;
+    std::copy(G.v[a].begin(), G.v[a].end(), buf.begin() + o);
+    o += G.v[a].size();
+    tab_off[a][1] = o;
+    std::copy(G.d[a].begin(), G.d[a].end(), buf.begin() + o);
+    o += G.d[a].size();
+  }
 }
 
 // Scheme 1: weights of the 1-form masses M^1_eps (which = EPS, primal 1-forms) and

@@ -89,6 +89,12 @@ struct HodgeArgs {
   int dual;              // 1: dual 2-forms (M~2_{1/eps}), 0: primal 2-forms (M2_{1/mu})
   int form;              // brick kernel form type: 0 primal 2-form, 1 dual 2-form, 2 primal 1-form
                          // (M^1_eps, scheme 1), 3 dual 1-form (M~^1_mu, scheme 1)
+  // on-the-fly geometry (SGM_OPT_OTF_GEOMETRY, polynomial maps, 2-form brick kernel): W holds
+  // w_q / material per point; DF is evaluated from the map's control points
+  int otf;
+  const double* geo_ctrl[3];  // control point coordinate r, [(z * (ny+p) + y) * (nx+p) + x]
+  const double* geo_tab;      // S_p values (s = 0) / derivatives (s = 1) at the Gauss points [n][Q][p+1]
+  int geo_tab_off[3][2];      // [axis][s] offsets (doubles) into geo_tab
 };
 
 // pipelined (producer/consumer) sweeps; false: no compiled configuration fits, nothing launched

@@ -56,6 +56,7 @@ struct MassData {
   bool const_material = true;
   double material_c = 1.0;             // constant material value (eps or mu)
   std::vector<double> values_host;     // the material at the quadrature points (variable case)
+  bool otf = false;                    // FULL with on-the-fly DF: W_dev holds w_q / material (1 per qp)
 };
 
 // Arguments a captured sgm_step graph was recorded with (replayed only for identical calls).
@@ -108,6 +109,11 @@ struct Plan {
   int* first_dev = nullptr;           // per-axis first local global index per element [n]
   size_t basis_off[3][4] = {};        // offsets (doubles) into basis_dev per axis and space
   size_t first_off[3][4] = {};        // offsets (ints) into first_dev per axis and space
+  // on-the-fly geometry (SGM_OPT_OTF_GEOMETRY): control points [3][(nz+p)(ny+p)(nx+p)] then the
+  // S_p value / derivative tables at the Gauss points [axis][s][n][Q][p+1]
+  double* geo_dev = nullptr;
+  size_t geo_ctrl_off[3] = {};
+  size_t geo_tab_off[3][2] = {};
   // plan-owned mirrors for sgm_step_host
   double* mirror = nullptr;
   size_t mirror_bytes = 0;
@@ -144,6 +150,10 @@ struct Plan {
 // host setup (host_setup.cpp)
 sgm_status build_axis(int p, int n, int Q, Axis& out, std::string& err);
 sgm_status build_mass1(Plan& P, int which, std::vector<double>& W, std::string& err);
+// on-the-fly geometry: whether the FULL 2-form weights of this plan may be evaluated in the brick
+// kernel (option set, polynomial map, Q = p + 1, p = 2..4), and the host image of geo_dev
+bool otf_geometry(const Plan& P);
+void build_geo_buffer(const Plan& P, std::vector<double>& buf, size_t ctrl_off[3], size_t tab_off[3][2]);
 std::vector<double> greville(int p, int n);
 sgm_status interpolate_geometry(const int n_el[3], int p, const double* values, double* ctrl, std::string& err);
 sgm_status banded_lu_nopivot(const std::vector<double>& A, int L, int m, std::vector<double>& LU,

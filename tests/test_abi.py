@@ -141,6 +141,8 @@ def test_reduced_schedule_identities_hold(p, n):
     assert pl.schedule_mode() == 3
     pl.set_options(S.OPT_SERIAL)
     assert pl.schedule_mode() == 1
+    pl.set_options(S.OPT_OTF_GEOMETRY)  # host-only plan: recorded, no weights to rebuild
+    assert pl.options() == S.OPT_OTF_GEOMETRY and pl.reduced_schedule()
     with pytest.raises(S.SgmError):
         pl.set_options(0x100)
 

@@ -483,13 +483,17 @@ def test_graph_replay_with_per_step_amplitude():
         assert rel(x, y) < 1e-10
 
 
+@pytest.mark.parametrize("otf", [False, True])
 @pytest.mark.parametrize("n", [(6, 7, 5), 8])
-def test_rational_quarter_annulus(n):
+def test_rational_quarter_annulus(n, otf):
     """The coaxial-cable cross-section as an exact degree-2 NURBS map (quarter annulus): general
-    Hodge applies and 1 / 20 steps against tier B (which evaluates the same rational map itself)."""
+    Hodge applies and 1 / 20 steps against tier B (which evaluates the same rational map itself).
+    SGM_OPT_OTF_GEOMETRY does not apply to rational maps: the stored weights are used."""
     p = 2
     g = W.quarter_annulus(n)
     pl = S.Plan(n, p, geom_ctrl=g)
+    if otf:
+        pl.set_options(S.OPT_OTF_GEOMETRY)
     tb = TierB(p, n, ctrl=g)
     rng = np.random.default_rng(61)
     x = rng.standard_normal(tb.N_e)
@@ -916,3 +920,56 @@ def test_long_lines_windowed(p, axis):
         out = _run_gpu(pl1, st, dt, 3)
         for a_, b_ in zip(out, tb1.run(*st, dt, 3)):
             assert rel(a_, b_) < 1e-10
+
+
+@pytest.mark.parametrize("p,n", [(2, (6, 5, 7)), (3, (9, 10, 11)), (3, (6, 5, 7)), (4, (5, 6, 4))])
+def test_otf_geometry_parity(p, n):
+    """On-the-fly DF in the general Hodge (SGM_OPT_OTF_GEOMETRY): the brick kernel
+    evaluates DF at the quadrature points from the map's control points and forms the 2-form
+    weights itself (1 stored double per point instead of 6).  Curved polynomial map, variable eps,
+    ragged bricks: both Hodge applies against the oracle and against the stored-W kernel, 1 and 20
+    steps against the oracle, bitwise-repeatable applies; clearing the option restores stored W."""
+    ctrl, eps = _curved_case(p, n)
+    tb = TierB(p, n, ctrl=ctrl, inv_eps=1.0 / eps, inv_mu=1.0)
+    tb.sep_mu = None
+    tb.W_mu = tb._W(1.0)
+    ref = S.Plan(n, p, geom_ctrl=ctrl)
+    ref.set_material(S.EPS, eps)
+    pl = S.Plan(n, p, geom_ctrl=ctrl)
+    pl.set_material(S.EPS, eps)
+    pl.set_options(S.OPT_OTF_GEOMETRY)  # rebuilds both general stars from the stored material
+    assert pl.options() == S.OPT_OTF_GEOMETRY
+    g = np.random.default_rng(131)
+    for which, N, mass, split in ((S.MASS_EPS, tb.N_e, tb.mass_eps, tb.split_e),
+                                  (S.MASS_MU, tb.N_h, tb.mass_mu, tb.split_h)):
+        x = g.standard_normal(N)
+        ys = []
+        for plan in (pl, pl, ref):
+            y = torch.empty(N, dtype=torch.float64, device="cuda")
+            plan.hodge_apply(which, dev(x), y)
+            ys.append(y)
+        assert torch.equal(ys[0], ys[1])
+        assert rel(host(ys[0]), forms.join(mass(split(x)))) < 1e-13
+        assert rel(host(ys[0]), host(ys[2])) < 1e-14
+    st = _state(tb, 132)
+    dt = 0.02 / max(forms._n3(n))
+    for k, tol in ((1, 1e-11), (20, 1e-10)):
+        out = _run_gpu(pl, st, dt, k)
+        for a, b in zip(out, tb.run(*st, dt, k)):
+            assert rel(a, b) < tol
+    # the option set before the material: the material upload builds the on-the-fly form directly
+    pl2 = S.Plan(n, p, geom_ctrl=ctrl)
+    pl2.set_options(S.OPT_OTF_GEOMETRY)
+    pl2.set_material(S.EPS, eps)
+    x = g.standard_normal(tb.N_e)
+    y2 = torch.empty(tb.N_e, dtype=torch.float64, device="cuda")
+    pl2.hodge_apply(S.MASS_EPS, dev(x), y2)
+    y1 = torch.empty_like(y2)
+    pl.hodge_apply(S.MASS_EPS, dev(x), y1)
+    assert torch.equal(y1, y2)
+    # cleared: the stored 6-entry weights again, bitwise equal to a plan that never had the option
+    pl.set_options(0)
+    y0 = torch.empty_like(y2)
+    ref.hodge_apply(S.MASS_EPS, dev(x), y0)
+    pl.hodge_apply(S.MASS_EPS, dev(x), y1)
+    assert torch.equal(y0, y1)
