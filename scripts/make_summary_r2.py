@@ -107,6 +107,12 @@ def main(tag):
         L.append(f"| {d['config']['workload']} | {d['value']:.3g} | {d['ms_per_step']:.3f} | {rr['kernel']} "
                  f"{rr['achieved']:.3g} {rr['unit']} ({rr['frac']:.2f}) | {rr.get('step_frac', 0):.2f} | "
                  f"{cb.get('value') or float('nan'):.3g} |")
+    for d in sweep:
+        for k, v in d.get("schedule_variants", {}).items():
+            extra = (f", W bytes per DOF-update {v['w_bytes_per_dof_update_stored']:.0f} -> "
+                     f"{v['w_bytes_per_dof_update']:.0f}" if "w_bytes_per_dof_update" in v else "")
+            L.append(f"* {d['config']['workload'].split(' ')[0]} variant `{k}` (options {v['options']}): "
+                     f"{v['ms_per_step']:.3f} ms per step (default {d['ms_per_step']:.3f}){extra}")
     c5p = os.path.join(PR, "r2_c5_sweep.jsonl")
     if os.path.exists(c5p):
         L.append("\n## configs[4]: K1 wedge solve and full step over p and n (`scripts/c5_sweep.py`)\n")
