@@ -873,6 +873,7 @@ sgm_status upload_mass1(Plan& P) {
     if (M.W_dev) cudaFree(M.W_dev);
     M.W_dev = nullptr;
     if (!W.empty() && P.device >= 0) {
+      if (hodge_uses_brick(P.p, P.Q)) hodge_brick_relayout(P.Q, P.n, int(W.size() / P.n_qp), W);
       if (cudaMalloc(&M.W_dev, W.size() * sizeof(double)) != cudaSuccess)
         return fail(SGM_E_NOMEM, "cudaMalloc failed for scheme-1 weights");
       cudaMemcpy(M.W_dev, W.data(), W.size() * sizeof(double), cudaMemcpyHostToDevice);
@@ -952,6 +953,8 @@ sgm_status set_material_impl(Plan& P, int which, const double* values, double c)
     M.W_dev = nullptr;
   }
   if (!W.empty()) {
+    // the brick kernel's HBM layout (one contiguous chunk per brick and element layer)
+    if (hodge_uses_brick(P.p, P.Q)) hodge_brick_relayout(P.Q, P.n, int(W.size() / P.n_qp), W);
     if (cudaMalloc(&M.W_dev, W.size() * sizeof(double)) != cudaSuccess)
       return fail(SGM_E_NOMEM, "cudaMalloc failed for Hodge weights");
     cudaMemcpy(M.W_dev, W.data(), W.size() * sizeof(double), cudaMemcpyHostToDevice);

@@ -7,6 +7,8 @@
 #include <type_traits>
 
 #include "hodge_brick.cuh"
+#include <vector>
+
 #include "kernels.cuh"
 #include "launch_util.cuh"
 
@@ -24,7 +26,7 @@ __global__ void hodge_general_kernel(const __grid_constant__ HodgeArgs A) {
   const int ex = int(e % nx), ey = int((e / nx) % ny), ez = int(e / (long(nx) * ny));
   const int t = threadIdx.x, nt = blockDim.x;
   const int M = (NL > Q ? NL : Q);
-  extern __shared__ double sm[];
+  extern __shared__ __align__(16) double sm[];
   double* U = sm;                   // [3][M^3]
   double* V = sm + 3 * M * M * M;   // [3][M^3]
   const int MM = M * M * M;
@@ -221,6 +223,40 @@ void launch_hodge2(const HodgeArgs& a, cudaStream_t st) {
 }
 
 }  // namespace
+
+bool hodge_uses_brick(int p, int Q) { return Q == p + 1 && p >= 2 && p <= 4; }
+
+// Element-major weights W[e][point][nw] (e = ex + nx (ey + ny ez), point = (qz Q + qy) Q + qx) ->
+// the brick kernel's HBM layout: per element layer ez and brick (by, bx) one chunk of nw planes of
+// NU = Q * EQ * (EQ + 1) slots (slot of a point: brick::uidx); pad slots and elements past the mesh
+// edge are zero.
+void hodge_brick_relayout(int Q, const int nel[3], int nw, std::vector<double>& W) {
+  constexpr int E = 4;
+  const int EQ = E * Q, RS = EQ + 1;
+  const size_t NU = size_t(Q) * EQ * RS;
+  const int nx = nel[0], ny = nel[1], nz = nel[2];
+  const int bxn = (nx + E - 1) / E, byn = (ny + E - 1) / E;
+  std::vector<double> out(size_t(nz) * byn * bxn * nw * NU, 0.0);
+  const size_t QQQ = size_t(Q) * Q * Q;
+#pragma omp parallel for collapse(2) schedule(static)
+  for (int ez = 0; ez < nz; ++ez)
+    for (int ey = 0; ey < ny; ++ey)
+      for (int ex = 0; ex < nx; ++ex) {
+        const size_t e = size_t(ex) + size_t(nx) * (size_t(ey) + size_t(ny) * ez);
+        const size_t chunk = (size_t(ez) * byn + ey / E) * bxn + ex / E;
+        double* dst = out.data() + chunk * nw * NU;
+        const double* src = W.data() + e * QQQ * nw;
+        const int exl = ex % E, eyl = ey % E;
+        for (int qz = 0; qz < Q; ++qz)
+          for (int qy = 0; qy < Q; ++qy)
+            for (int qx = 0; qx < Q; ++qx) {
+              const size_t slot = (size_t(qz) * EQ + eyl * Q + qy) * RS + exl * Q + qx;
+              const size_t pt = (size_t(qz) * Q + qy) * Q + qx;
+              for (int k = 0; k < nw; ++k) dst[k * NU + slot] = src[pt * nw + k];
+            }
+      }
+  W.swap(out);
+}
 
 size_t hodge_scratch_doubles(int p, int Q, int form, int full, const int nel[3]) {
   if (Q != p + 1) return 0;  // the generic kernel accumulates with atomics

@@ -34,15 +34,24 @@ __host__ __device__ constexpr int nloc() {
                    : (C == AX ? P - 1 : P);
 }
 
+// Shared-memory strides are padded against bank conflicts (fp64: 16 eight-byte bank pairs): a
+// stage whose consecutive tasks t walk a buffer with stride s is conflict-free when s is odd, and a
+// stage whose tasks are (plane, px) pairs when the plane stride is congruent to PX modulo 16.
+__host__ __device__ constexpr int pad_to(int n, int r) { return n + (((r - n) % 16) + 16) % 16; }
+
 template <int P, int Q, int DUAL, int E, int C>
 struct Geo {
   static constexpr int NX = nloc<P, DUAL, C, 0>(), NY = nloc<P, DUAL, C, 1>(), NZ = nloc<P, DUAL, C, 2>();
   static constexpr int PX = E - 1 + NX, PY = E - 1 + NY;
   static constexpr int EQ = E * Q;
   static constexpr int WIN = NZ * PY * PX;   // coefficient / output window
-  static constexpr int Z1 = Q * PY * PX;     // after the z stage: [qz][py][px]
-  static constexpr int Z2 = Q * EQ * PX;     // after the y stage: [qz][Y][px]
-  static constexpr int U = Q * EQ * EQ;      // quadrature values: [qz][Y][X]
+  static constexpr int LAYP = pad_to(PY * PX, PX);  // plane stride of Z1
+  static constexpr int PXP = PX | 1;                 // row stride of Z2
+  static constexpr int Z2P = pad_to(EQ * PXP, PX);   // plane stride of Z2
+  static constexpr int RSU = EQ + 1;                 // row stride of U (EQ = E * Q is even)
+  static constexpr int Z1 = Q * LAYP;        // after the z stage: [qz][py][px]
+  static constexpr int Z2 = Q * Z2P;         // after the y stage: [qz][Y][px]
+  static constexpr int U = Q * EQ * RSU;     // quadrature values: [qz][Y][X]
   static constexpr int TOT = 2 * WIN + Z1 + Z2 + U;
 };
 
@@ -56,7 +65,9 @@ struct Layout {
   static constexpr int VZ = Q * NL;       // one element's z basis of one role
   // per component: Xw, Yw, Z1, Z2, U; then tables [role][axis x, y] and [role] z
   static constexpr int OFF1 = G0::TOT, OFF2 = OFF1 + G1::TOT, TAB = OFF2 + G2::TOT;
-  static constexpr int WB = TAB + 2 * 2 * VXY + 2 * VZ;  // W of one element layer (cp.async staged)
+  // W of one element layer (one bulk copy per layer: 16-byte aligned, hence the even offset)
+  static constexpr int WB = (TAB + 2 * 2 * VXY + 2 * VZ + 1) & ~1;
+  static constexpr int NU = G0::U;  // quadrature-point slots of one component (all components: the same)
   // on-the-fly geometry (OTF): the staged W is w_q / material (1 per point); after it the map's
   // partial sums A[r][s][qz][py][px] (z contracted, s = value / derivative), B[r][m][qz][Y][px]
   // (z and y contracted, m = (val,val), (val,der), (der,val)) and the brick's x / y map tables
@@ -64,7 +75,7 @@ struct Layout {
   static constexpr int PM = E + P;  // map control points of the brick per axis (S_p, E elements)
   static constexpr int MA = 3 * 2 * Q * PM * PM, MB = 3 * 3 * Q * E * Q * PM, MT = 2 * 2 * E * Q * NL;
   template <bool FULL, bool OTF = false>
-  __host__ __device__ static constexpr int wdoubles() { return E * E * Q * Q * Q * (FULL && !OTF ? 6 : 1); }
+  __host__ __device__ static constexpr int wdoubles() { return NU * (FULL && !OTF ? 6 : 1); }
   template <bool FULL, bool OTF = false>
   __host__ __device__ static constexpr int total() { return WB + wdoubles<FULL, OTF>() + (OTF ? MA + MB + MT : 0); }
 };
@@ -74,11 +85,14 @@ struct Brick {
   int ez0, ez1;            // element layers [ez0, ez1)
 };
 
-// quadrature values are stored element-major, U[(ey*E + ex)][qz][qy][qx], the order of W in HBM
+// quadrature values are stored brick-wide, U[qz][Y = ey*Q + qy][X = ex*Q + qx] with rows padded to
+// E*Q + 1 doubles: the x stages' tasks (qz, Y) then walk U with an odd stride (no bank conflicts);
+// W uses the same slots, in HBM as well: per brick and element layer one contiguous chunk of NW
+// planes (entry k of a point in plane k at the point's U slot; pad slots and elements past the
+// mesh edge hold zeros), so a layer's W is staged by a single bulk copy (host: brick_w_relayout)
 template <int Q, int E>
 __device__ __forceinline__ int uidx(int qz, int Yq, int ex, int qx) {
-  const int ey = Yq / Q, qy = Yq - ey * Q;
-  return (ey * E + ex) * Q * Q * Q + (qz * Q + qy) * Q + qx;
+  return (qz * (E * Q) + Yq) * (E * Q + 1) + ex * Q + qx;
 }
 
 // per-component pointers into shared memory
@@ -167,7 +181,7 @@ __device__ __forceinline__ void interp_z(const CompSm<P, Q, DUAL, E, C>& S, int 
     double s = 0.0;
 #pragma unroll
     for (int jz = 0; jz < G::NZ; ++jz) s = fma(S.Vz[qz * NL + jz], xv[jz], s);
-    S.Z1[qz * LAY + t] = s;
+    S.Z1[qz * G::LAYP + t] = s;
   }
 }
 
@@ -202,7 +216,7 @@ __device__ __forceinline__ void interp_y(const CompSm<P, Q, DUAL, E, C>& S, int 
   const Coef<Q, G::NY, NL, UNI> V(S.Vy);
   double zv[EH - 1 + G::NY];
 #pragma unroll
-  for (int py = 0; py < EH - 1 + G::NY; ++py) zv[py] = S.Z1[(qz * G::PY + hf * EH + py) * G::PX + px];
+  for (int py = 0; py < EH - 1 + G::NY; ++py) zv[py] = S.Z1[qz * G::LAYP + (hf * EH + py) * G::PX + px];
 #pragma unroll
   for (int el = 0; el < EH; ++el)
 #pragma unroll
@@ -210,7 +224,7 @@ __device__ __forceinline__ void interp_y(const CompSm<P, Q, DUAL, E, C>& S, int 
       double s = 0.0;
 #pragma unroll
       for (int jy = 0; jy < G::NY; ++jy) s = fma(V(S.Vy, hf * EH + el, qy, jy), zv[el + jy], s);
-      S.Z2[(qz * G::EQ + (hf * EH + el) * Q + qy) * G::PX + px] = s;
+      S.Z2[qz * G::Z2P + ((hf * EH + el) * Q + qy) * G::PXP + px] = s;
     }
 }
 
@@ -228,7 +242,7 @@ __device__ __forceinline__ void interp_x(const CompSm<P, Q, DUAL, E, C>& S, int 
   const Coef<Q, G::NX, NL, UNI> V(S.Vx);
   double zv[EH - 1 + G::NX];
 #pragma unroll
-  for (int px = 0; px < EH - 1 + G::NX; ++px) zv[px] = S.Z2[t * G::PX + hf * EH + px];
+  for (int px = 0; px < EH - 1 + G::NX; ++px) zv[px] = S.Z2[(t / G::EQ) * G::Z2P + (t % G::EQ) * G::PXP + hf * EH + px];
 #pragma unroll
   for (int el = 0; el < EH; ++el)
 #pragma unroll
@@ -265,7 +279,7 @@ __device__ __forceinline__ void test_x(const CompSm<P, Q, DUAL, E, C>& S, int t)
       for (int jx = 0; jx < G::NX; ++jx) acc[ex + jx] = fma(V(S.Vx, ex, qx, jx), u, acc[ex + jx]);
     }
 #pragma unroll
-  for (int px = 0; px < G::PX; ++px) S.Z2[t * G::PX + px] = acc[px];
+  for (int px = 0; px < G::PX; ++px) S.Z2[(t / G::EQ) * G::Z2P + (t % G::EQ) * G::PXP + px] = acc[px];
 }
 
 // y: Z1[qz][py][px] = sum_{ey,qy} Vy[ey][qy][py-ey] Z2[qz][ey*Q+qy][px]   (tasks: qz, px)
@@ -283,12 +297,12 @@ __device__ __forceinline__ void test_y(const CompSm<P, Q, DUAL, E, C>& S, int t)
   for (int ey = 0; ey < E; ++ey)
 #pragma unroll
     for (int qy = 0; qy < Q; ++qy) {
-      const double z = S.Z2[(qz * G::EQ + ey * Q + qy) * G::PX + px];
+      const double z = S.Z2[qz * G::Z2P + (ey * Q + qy) * G::PXP + px];
 #pragma unroll
       for (int jy = 0; jy < G::NY; ++jy) acc[ey + jy] = fma(V(S.Vy, ey, qy, jy), z, acc[ey + jy]);
     }
 #pragma unroll
-  for (int py = 0; py < G::PY; ++py) S.Z1[(qz * G::PY + py) * G::PX + px] = acc[py];
+  for (int py = 0; py < G::PY; ++py) S.Z1[qz * G::LAYP + py * G::PX + px] = acc[py];
 }
 
 // z: Yw[jz][py][px] += sum_qz Vz[qz][jz] Z1[qz][py][px]      (tasks: py, px)
@@ -299,7 +313,7 @@ __device__ __forceinline__ void test_z(const CompSm<P, Q, DUAL, E, C>& S, int t)
   if (t >= LAY) return;
   double zv[Q];
 #pragma unroll
-  for (int qz = 0; qz < Q; ++qz) zv[qz] = S.Z1[qz * LAY + t];
+  for (int qz = 0; qz < Q; ++qz) zv[qz] = S.Z1[qz * G::LAYP + t];
 #pragma unroll
   for (int jz = 0; jz < G::NZ; ++jz) {
     const int sl = S.slot(jz);
@@ -329,7 +343,7 @@ __device__ __forceinline__ void column_phase(const HodgeArgs& A, const CompSm<P,
   const bool inxy = gx >= 0 && gx < ext[0] && gy >= 0 && gy < ext[1];
   double zv[Q];
 #pragma unroll
-  for (int qz = 0; qz < Q; ++qz) zv[qz] = S.Z1[qz * LAY + t];
+  for (int qz = 0; qz < Q; ++qz) zv[qz] = S.Z1[qz * G::LAYP + t];
 #pragma unroll
   for (int jz = 0; jz < G::NZ; ++jz) {
     const int sl = S.slot(jz);
@@ -358,7 +372,7 @@ __device__ __forceinline__ void column_phase(const HodgeArgs& A, const CompSm<P,
     double s = 0.0;
 #pragma unroll
     for (int jz = 0; jz < G::NZ; ++jz) s = fma(__ldg(vz_next + qz * NL + jz), xv[jz], s);
-    S.Z1[qz * LAY + t] = s;
+    S.Z1[qz * G::LAYP + t] = s;
   }
 }
 
@@ -468,8 +482,13 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
   using G0 = Geo<P, Q, DUAL, E, 0>;
   using G1 = Geo<P, Q, DUAL, E, 1>;
   using G2 = Geo<P, Q, DUAL, E, 2>;
-  constexpr int NL = P + 1, QQQ = Q * Q * Q, EQ = E * Q;
-  extern __shared__ double sm[];
+  constexpr int NL = P + 1, EQ = E * Q;
+  extern __shared__ __align__(16) double sm[];
+  __shared__ unsigned long long wbar;  // completion of the staged W (one phase per element layer)
+  unsigned wphase = 0;
+  if (threadIdx.x == 0) pipe::mbar_init(&wbar, 1);
+  pipe::fence_proxy_async_smem();
+  __syncthreads();
   CompSm<P, Q, DUAL, E, 0> S0(sm);
   CompSm<P, Q, DUAL, E, 1> S1(sm);
   CompSm<P, Q, DUAL, E, 2> S2(sm);
@@ -553,18 +572,15 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
       }
     };
     load_vz(B.ez0);
-    // W of element layer ez -> Wsm (8-byte cp.async; elements past the mesh edge are skipped)
+    // W of element layer ez -> Wsm: one bulk copy (TMA engine) of the brick's chunk, completion on
+    // wbar.  Called after the block barrier that follows the last read of the previous layer's W.
     auto stage_w = [&](int ez) {
-      constexpr int NW = (FULL && !OTF) ? 6 : 1;
-      // warp w copies elements w, w + 8, ...: each element's W is contiguous in HBM and in Wsm
-      for (int el = threadIdx.x >> 5; el < E * E; el += 8) {
-        const int ex = el % E, ey = el / E;
-        if (ex < B.nex && ey < B.ney) {
-          const long e = (B.ex0 + ex) + long(nx) * ((B.ey0 + ey) + long(ny) * ez);
-          const double* src = A.W + e * QQQ * NW;
-          double* dst = Wsm + el * QQQ * NW;
-          for (int i = threadIdx.x & 31; i < QQQ * NW; i += 32) pipe::cp_async8(dst + i, src + i);
-        }
+      constexpr unsigned bytes = unsigned(L::template wdoubles<FULL, OTF>()) * 8u;
+      if (threadIdx.x == 0) {
+        const long chunk = (long(ez) * by + B.ey0 / E) * bx + B.ex0 / E;
+        pipe::fence_proxy_async_smem();
+        pipe::mbar_arrive_expect_tx(&wbar, bytes);
+        pipe::bulk_g2s(Wsm, A.W + chunk * (bytes / 8u), bytes, &wbar);
       }
     };
     stage_w(B.ez0);
@@ -603,7 +619,8 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
       SGM_BRICK_STAGE3U(interp_y, 1, 2 * Q * G0::PX, 2 * Q * G1::PX, 2 * Q * G2::PX)
       // W of this layer (staged by cp.async since the previous layer) must be in shared memory
       // before the x interpolation (scalar W is multiplied there) or the quadrature stage (full W)
-      pipe::cp_async_wait_all();
+      pipe::mbar_wait(&wbar, wphase);
+      wphase ^= 1u;
       __syncthreads();
       {
         const bool u0 = uni[0 * 2 + 0], u1 = uni[1 * 2 + 0], u2 = uni[1 * 2 + 0];
@@ -648,9 +665,13 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
       }
       if (FULL) {
         // quadrature points: v_c = sum_c' W_cc' u_c' (the 3 x 3 W couples the components)
-        for (int el = threadIdx.x >> 5; el < E * E; el += 8) {
-          const bool live = (el % E) < B.nex && (el / E) < B.ney;  // warp-uniform
-          for (int i = el * QQQ + (threadIdx.x & 31); i < (el + 1) * QQQ; i += 32) {
+        {
+          // consecutive threads take consecutive U slots (the pad slot of each row is skipped)
+          for (int i = threadIdx.x; i < L::NU; i += 256) {
+            const int X = i % (EQ + 1), row = i / (EQ + 1), Yq = row % EQ;
+            if (X == EQ) continue;
+            const int ex = X / Q, ey = Yq / Q;
+            const bool live = ex < B.nex && ey < B.ney;
             const double u0 = S0.U[i], u1 = S1.U[i], u2 = S2.U[i];
             double wxx, wyy, wzz, wxy, wxz, wyz;
             if (OTF) {
@@ -658,8 +679,7 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
               // W = (w_q / material) / det DF * DF^T DF, as the host builds them
               wxx = wyy = wzz = wxy = wxz = wyz = 0.0;
               if (live) {
-                const int ex = el % E, ey = el / E, rq = i - el * QQQ;
-                const int qzp = rq / (Q * Q), qy = (rq / Q) % Q, qx = rq % Q;
+                const int qzp = row / EQ, qy = Yq - ey * Q, qx = X - ex * Q;
                 const double* tv = MTs + (0 * 2 + 0) * E * Q * NL + (ex * Q + qx) * NL;  // x values
                 const double* td = MTs + (0 * 2 + 1) * E * Q * NL + (ex * Q + qx) * NL;  // x derivatives
                 double D[9];
@@ -686,13 +706,13 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
                 wyz = g * mm(1, 2);
               }
             } else {
-              const double* w = Wsm + i * 6;
-              wxx = live ? w[0] : 0.0;
-              wyy = live ? w[1] : 0.0;
-              wzz = live ? w[2] : 0.0;
-              wxy = live ? w[3] : 0.0;
-              wxz = live ? w[4] : 0.0;
-              wyz = live ? w[5] : 0.0;
+              const double* w = Wsm + i;
+              wxx = live ? w[0 * L::NU] : 0.0;
+              wyy = live ? w[1 * L::NU] : 0.0;
+              wzz = live ? w[2 * L::NU] : 0.0;
+              wxy = live ? w[3 * L::NU] : 0.0;
+              wxz = live ? w[4 * L::NU] : 0.0;
+              wyz = live ? w[5 * L::NU] : 0.0;
             }
             S0.U[i] = wxx * u0 + wxy * u1 + wxz * u2;
             S1.U[i] = wxy * u0 + wyy * u1 + wyz * u2;

@@ -1,5 +1,6 @@
 // Kernel parameter blocks and launcher declarations (sm_100a only).
 #pragma once
+#include <vector>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -116,6 +117,10 @@ void launch_curl(int kind, const double* const src[3], const int sext[3][3], dou
 void launch_hodge_general(int p, const HodgeArgs& a, cudaStream_t st);
 // doubles of scratch the deterministic brick Hodge needs for this plan geometry (current device)
 size_t hodge_scratch_doubles(int p, int Q, int form, int full, const int nel[3]);
+// the brick kernel serves the plan (default rule Q = p + 1, p = 2..4): its weights live in HBM in the
+// brick layout (hodge_brick_relayout converts the element-major host vector in place)
+bool hodge_uses_brick(int p, int Q);
+void hodge_brick_relayout(int Q, const int nel[3], int nw, std::vector<double>& W);
 void launch_dot_partials(const double* x, const double* y, size_t n, double* partials, int slot, cudaStream_t st);
 void launch_finalize_sum(const double* partials, int nslots, double scale, double* out, cudaStream_t st);
 void launch_div_max(int kind, const double* const src[3], const int sext[3][3], double* partials,
