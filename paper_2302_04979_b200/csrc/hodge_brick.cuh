@@ -52,7 +52,10 @@ struct Geo {
   static constexpr int Z1 = Q * LAYP;        // after the z stage: [qz][py][px]
   static constexpr int Z2 = Q * Z2P;         // after the y stage: [qz][Y][px]
   static constexpr int U = Q * EQ * RSU;     // quadrature values: [qz][Y][X]
-  static constexpr int TOT = 2 * WIN + Z1 + Z2 + U;
+  // Z1 (next layer's z interpolation) and T1 (this layer's y testing) are live from the y-testing
+  // interval to the next y-interpolation interval, when U is dead: they alias U
+  static constexpr int TOT = 2 * WIN + Z2 + U;
+  static_assert(2 * Z1 <= U, "Z1 and T1 alias U");
 };
 
 template <int P, int Q, int DUAL, int E>
@@ -99,11 +102,17 @@ __device__ __forceinline__ int uidx(int qz, int Yq, int ex, int qx) {
 template <int P, int Q, int DUAL, int E, int C>
 struct CompSm {
   using G = Geo<P, Q, DUAL, E, C>;
-  double *Xw, *Yw, *Z1, *Z2, *U;
+  double *Xw, *Yw, *Z1, *T1, *Z2, *U;
   const double *Vx, *Vy, *Vz;  // role-selected basis tables
-  int base = 0;                // window slot of layer 0 (circular: layer jz lives in slot (base + jz) % NZ)
-  __device__ __forceinline__ int slot(int jz) const {
-    const int s = base + jz;
+  // window slot of layer 0 (circular: layer jz lives in slot (base + jz) % NZ); the coefficient
+  // window runs one element layer ahead of the output window, hence two bases
+  int xbase = 0, ybase = 0;
+  __device__ __forceinline__ int slotx(int jz) const {
+    const int s = xbase + jz;
+    return s >= G::NZ ? s - G::NZ : s;
+  }
+  __device__ __forceinline__ int sloty(int jz) const {
+    const int s = ybase + jz;
     return s >= G::NZ ? s - G::NZ : s;
   }
   __device__ CompSm(double* sm) {
@@ -111,9 +120,10 @@ struct CompSm {
     double* b = sm + (C == 0 ? 0 : (C == 1 ? L::OFF1 : L::OFF2));
     Xw = b;
     Yw = Xw + G::WIN;
-    Z1 = Yw + G::WIN;
-    Z2 = Z1 + G::Z1;
+    Z2 = Yw + G::WIN;
     U = Z2 + G::Z2;
+    Z1 = U;
+    T1 = U + G::Z1;
     const double* tab = sm + L::TAB;
     // role 0 = own (axis == C), 1 = other
     Vx = tab + ((C == 0 ? 0 : 1) * 2 + 0) * L::VXY;
@@ -175,7 +185,7 @@ __device__ __forceinline__ void interp_z(const CompSm<P, Q, DUAL, E, C>& S, int 
   if (t >= LAY) return;
   double xv[G::NZ];
 #pragma unroll
-  for (int jz = 0; jz < G::NZ; ++jz) xv[jz] = S.Xw[S.slot(jz) * LAY + t];
+  for (int jz = 0; jz < G::NZ; ++jz) xv[jz] = S.Xw[S.slotx(jz) * LAY + t];
 #pragma unroll
   for (int qz = 0; qz < Q; ++qz) {
     double s = 0.0;
@@ -282,7 +292,7 @@ __device__ __forceinline__ void test_x(const CompSm<P, Q, DUAL, E, C>& S, int t)
   for (int px = 0; px < G::PX; ++px) S.Z2[(t / G::EQ) * G::Z2P + (t % G::EQ) * G::PXP + px] = acc[px];
 }
 
-// y: Z1[qz][py][px] = sum_{ey,qy} Vy[ey][qy][py-ey] Z2[qz][ey*Q+qy][px]   (tasks: qz, px)
+// y: T1[qz][py][px] = sum_{ey,qy} Vy[ey][qy][py-ey] Z2[qz][ey*Q+qy][px]   (tasks: qz, px)
 template <int P, int Q, int DUAL, int E, int C, bool UNI>
 __device__ __forceinline__ void test_y(const CompSm<P, Q, DUAL, E, C>& S, int t) {
   using G = Geo<P, Q, DUAL, E, C>;
@@ -302,38 +312,18 @@ __device__ __forceinline__ void test_y(const CompSm<P, Q, DUAL, E, C>& S, int t)
       for (int jy = 0; jy < G::NY; ++jy) acc[ey + jy] = fma(V(S.Vy, ey, qy, jy), z, acc[ey + jy]);
     }
 #pragma unroll
-  for (int py = 0; py < G::PY; ++py) S.Z1[qz * G::LAYP + py * G::PX + px] = acc[py];
+  for (int py = 0; py < G::PY; ++py) S.T1[qz * G::LAYP + py * G::PX + px] = acc[py];
 }
 
-// z: Yw[jz][py][px] += sum_qz Vz[qz][jz] Z1[qz][py][px]      (tasks: py, px)
+// The (py, px) columns of component C.  The same thread owns a column in both functions, which run
+// in different barrier intervals next to the y stages (whose tasks leave threads idle):
+// column_test (with the next layer's y interpolation): test along z of element layer ez,
+//   Yw[jz][py][px] += sum_qz Vz[qz][jz] T1[qz][py][px], and flush of the completed output slot
+//   (scratch or atomics to y; slot cleared).  vz: the z basis (global, [Q][NL]) of layer ez.
 template <int P, int Q, int DUAL, int E, int C>
-__device__ __forceinline__ void test_z(const CompSm<P, Q, DUAL, E, C>& S, int t) {
-  using G = Geo<P, Q, DUAL, E, C>;
-  constexpr int NL = P + 1, LAY = G::PY * G::PX;
-  if (t >= LAY) return;
-  double zv[Q];
-#pragma unroll
-  for (int qz = 0; qz < Q; ++qz) zv[qz] = S.Z1[qz * G::LAYP + t];
-#pragma unroll
-  for (int jz = 0; jz < G::NZ; ++jz) {
-    const int sl = S.slot(jz);
-    double s = S.Yw[sl * LAY + t];
-#pragma unroll
-    for (int qz = 0; qz < Q; ++qz) s = fma(S.Vz[qz * NL + jz], zv[qz], s);
-    S.Yw[sl * LAY + t] = s;
-  }
-}
-
-// One (py, px) column of component C at the end of element layer ez (no block barrier inside: the
-// same thread owns the column in every step):  test along z of layer ez, flush of the completed
-// output slot (atomics to y, slot cleared), then -- if another layer follows -- the new top
-// coefficient into the freed slot and the z interpolation of the next layer.  vz_*: the z bases
-// (global, [Q][NL]) of this layer and of the next.
-template <int P, int Q, int DUAL, int E, int C>
-__device__ __forceinline__ void column_phase(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int t, int gx0,
-                                             int gy0, int gz_flush, bool next, int gz_load,
-                                             const double* __restrict__ vz_cur, const double* __restrict__ vz_next,
-                                             double* scr, int rel) {
+__device__ __forceinline__ void column_test(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int t, int gx0,
+                                            int gy0, int gz_flush, const double* __restrict__ vz, double* scr,
+                                            int rel) {
   using G = Geo<P, Q, DUAL, E, C>;
   constexpr int NL = P + 1, LAY = G::PY * G::PX;
   if (t >= LAY) return;
@@ -343,13 +333,13 @@ __device__ __forceinline__ void column_phase(const HodgeArgs& A, const CompSm<P,
   const bool inxy = gx >= 0 && gx < ext[0] && gy >= 0 && gy < ext[1];
   double zv[Q];
 #pragma unroll
-  for (int qz = 0; qz < Q; ++qz) zv[qz] = S.Z1[qz * G::LAYP + t];
+  for (int qz = 0; qz < Q; ++qz) zv[qz] = S.T1[qz * G::LAYP + t];
 #pragma unroll
   for (int jz = 0; jz < G::NZ; ++jz) {
-    const int sl = S.slot(jz);
+    const int sl = S.sloty(jz);
     double acc = S.Yw[sl * LAY + t];
 #pragma unroll
-    for (int qz = 0; qz < Q; ++qz) acc = fma(__ldg(vz_cur + qz * NL + jz), zv[qz], acc);
+    for (int qz = 0; qz < Q; ++qz) acc = fma(__ldg(vz + qz * NL + jz), zv[qz], acc);
     if (jz == 0) {
       if (inxy && gz_flush >= 0 && gz_flush < ext[2]) {
         if (scr) scr[rel * LAY + t] = acc;
@@ -360,18 +350,32 @@ __device__ __forceinline__ void column_phase(const HodgeArgs& A, const CompSm<P,
       S.Yw[sl * LAY + t] = acc;
     }
   }
-  if (!next) return;
+}
+
+// column_next (with the current layer's y testing): the top coefficient layer of the next element
+// layer (global z index gz_load) into the freed window slot and the next layer's z interpolation,
+// Z1[qz][py][px] = sum_jz Vz[qz][jz] Xw[jz][py][px].  vz: the z basis of the next layer.
+template <int P, int Q, int DUAL, int E, int C>
+__device__ __forceinline__ void column_next(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int t, int gx0,
+                                            int gy0, int gz_load, const double* __restrict__ vz) {
+  using G = Geo<P, Q, DUAL, E, C>;
+  constexpr int NL = P + 1, LAY = G::PY * G::PX;
+  if (t >= LAY) return;
+  const int px = t % G::PX, py = t / G::PX;
+  const int gx = gx0 + px, gy = gy0 + py;
+  const int* ext = A.ext[C];
+  const bool inxy = gx >= 0 && gx < ext[0] && gy >= 0 && gy < ext[1];
   double v = 0.0;
   if (inxy && gz_load >= 0 && gz_load < ext[2]) v = __ldg(A.x[C] + gx + long(ext[0]) * (gy + long(ext[1]) * gz_load));
-  S.Xw[S.slot(0) * LAY + t] = v;
+  S.Xw[S.slotx(0) * LAY + t] = v;
   double xv[G::NZ];
 #pragma unroll
-  for (int jz = 0; jz < G::NZ; ++jz) xv[jz] = (jz + 1 < G::NZ) ? S.Xw[S.slot(jz + 1) * LAY + t] : v;
+  for (int jz = 0; jz < G::NZ; ++jz) xv[jz] = (jz + 1 < G::NZ) ? S.Xw[S.slotx(jz + 1) * LAY + t] : v;
 #pragma unroll
   for (int qz = 0; qz < Q; ++qz) {
     double s = 0.0;
 #pragma unroll
-    for (int jz = 0; jz < G::NZ; ++jz) s = fma(__ldg(vz_next + qz * NL + jz), xv[jz], s);
+    for (int jz = 0; jz < G::NZ; ++jz) s = fma(__ldg(vz + qz * NL + jz), xv[jz], s);
     S.Z1[qz * G::LAYP + t] = s;
   }
 }
@@ -388,7 +392,7 @@ __device__ __forceinline__ void column_phase(const HodgeArgs& A, const CompSm<P,
   }
 // the same with the per-axis uniform-basis flags (own role of component c along the axis when
 // the axis is c's own, else the other role)
-#define SGM_BRICK_STAGE3U(F, AXIS, N0, N1, N2)                                                       \
+#define SGM_BRICK_TASKS3U(F, AXIS, N0, N1, N2)                                                       \
   {                                                                                                  \
     const bool u0 = uni[(AXIS == 0 ? 0 : 1) * 2 + AXIS], u1 = uni[(AXIS == 1 ? 0 : 1) * 2 + AXIS],  \
                u2 = uni[1 * 2 + AXIS];                                                               \
@@ -402,8 +406,10 @@ __device__ __forceinline__ void column_phase(const HodgeArgs& A, const CompSm<P,
         else F<P, Q, DUAL, E, 2, false>(S2, t - (N0) - (N1));                                        \
       }                                                                                              \
     }                                                                                                \
-    __syncthreads();                                                                                 \
   }
+#define SGM_BRICK_STAGE3U(F, AXIS, N0, N1, N2) \
+  SGM_BRICK_TASKS3U(F, AXIS, N0, N1, N2)       \
+  __syncthreads();
 
 // doubles of one work item's output patches in the scratch (all three components, zchunk + NZ - 1
 // layers each)
@@ -558,7 +564,8 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
     const int gx0[3] = {fx[0], fx[1], fx[1]}, gy0[3] = {fy[1], fy[0], fy[1]};
     auto zfirst = [&](int c, int ez) { return first_of(A, 2, c == 2 ? 0 : 1, ez); };
     // zero output windows, load the NZ coefficient layers and z bases of the first element layer
-    S0.base = S1.base = S2.base = 0;
+    S0.xbase = S1.xbase = S2.xbase = 0;
+    S0.ybase = S1.ybase = S2.ybase = 0;
     for (int o = threadIdx.x; o < G0::WIN; o += 256) S0.Yw[o] = 0.0;
     for (int o = threadIdx.x; o < G1::WIN; o += 256) S1.Yw[o] = 0.0;
     for (int o = threadIdx.x; o < G2::WIN; o += 256) S2.Yw[o] = 0.0;
@@ -589,6 +596,38 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
     auto vzp = [&](int c, int ez) {
       return A.basis + A.basis_off[2][c == 2 ? 0 : 1] + size_t(ez) * Q * NL;
     };
+    // the columns' tasks start at thread `shift` (after the y stage's tasks of the same interval)
+    constexpr int NC0 = G0::PY * G0::PX, NC1 = G1::PY * G1::PX, NC2 = G2::PY * G2::PX;
+    auto columns_test = [&](int ezl, int shift) {
+      for (int t = (threadIdx.x + 256 - shift % 256) % 256; t < NC0 + NC1 + NC2; t += 256) {
+        if (t < NC0)
+          column_test<P, Q, DUAL, E, 0>(A, S0, t, gx0[0], gy0[0], zfirst(0, ezl), vzp(0, ezl), scr0,
+                                        zfirst(0, ezl) - zfirst(0, B.ez0));
+        else if (t < NC0 + NC1)
+          column_test<P, Q, DUAL, E, 1>(A, S1, t - NC0, gx0[1], gy0[1], zfirst(1, ezl), vzp(1, ezl), scr1,
+                                        zfirst(1, ezl) - zfirst(1, B.ez0));
+        else
+          column_test<P, Q, DUAL, E, 2>(A, S2, t - NC0 - NC1, gx0[2], gy0[2], zfirst(2, ezl), vzp(2, ezl), scr2,
+                                        zfirst(2, ezl) - zfirst(2, B.ez0));
+      }
+      S0.ybase = S0.sloty(1);
+      S1.ybase = S1.sloty(1);
+      S2.ybase = S2.sloty(1);
+    };
+    auto columns_next = [&](int ezn, int shift) {
+      for (int t = (threadIdx.x + 256 - shift % 256) % 256; t < NC0 + NC1 + NC2; t += 256) {
+        if (t < NC0)
+          column_next<P, Q, DUAL, E, 0>(A, S0, t, gx0[0], gy0[0], zfirst(0, ezn) + G0::NZ - 1, vzp(0, ezn));
+        else if (t < NC0 + NC1)
+          column_next<P, Q, DUAL, E, 1>(A, S1, t - NC0, gx0[1], gy0[1], zfirst(1, ezn) + G1::NZ - 1, vzp(1, ezn));
+        else
+          column_next<P, Q, DUAL, E, 2>(A, S2, t - NC0 - NC1, gx0[2], gy0[2], zfirst(2, ezn) + G2::NZ - 1,
+                                        vzp(2, ezn));
+      }
+      S0.xbase = S0.slotx(1);
+      S1.xbase = S1.slotx(1);
+      S2.xbase = S2.slotx(1);
+    };
     for (int ez = B.ez0; ez < B.ez1; ++ez) {
       if (OTF) {
         // map, z: A[r][s][qz][py][px] = sum_k Tz_s[qz][k] ctrl_r[ez + k][ey0 + py][ex0 + px]
@@ -616,7 +655,10 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
           }
         }
       }
-      SGM_BRICK_STAGE3U(interp_y, 1, 2 * Q * G0::PX, 2 * Q * G1::PX, 2 * Q * G2::PX)
+      // y interpolation of this layer; on the threads it leaves idle, the previous layer's z testing
+      // and flush (T1 of the previous layer is not written again before this layer's y testing)
+      SGM_BRICK_TASKS3U(interp_y, 1, 2 * Q * G0::PX, 2 * Q * G1::PX, 2 * Q * G2::PX)
+      if (ez > B.ez0) columns_test(ez - 1, 2 * Q * (G0::PX + G1::PX + G2::PX));
       // W of this layer (staged by cp.async since the previous layer) must be in shared memory
       // before the x interpolation (scalar W is multiplied there) or the quadrature stage (full W)
       pipe::mbar_wait(&wbar, wphase);
@@ -723,41 +765,24 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
       }
       if (ez + 1 < B.ez1) stage_w(ez + 1);
       SGM_BRICK_STAGE3U(test_x, 0, Q * EQ, Q * EQ, Q * EQ)
-      SGM_BRICK_STAGE3U(test_y, 1, Q * G0::PX, Q * G1::PX, Q * G2::PX)
-      // per column: test along z, flush the completed layer, load the next top layer, interpolate
-      // the next layer along z -- no barrier between these steps
-      {
-        const bool nx1 = ez + 1 < B.ez1;
-        const int ezn = nx1 ? ez + 1 : ez;
-        constexpr int N0 = G0::PY * G0::PX, N1 = G1::PY * G1::PX, N2 = G2::PY * G2::PX;
-        for (int t = threadIdx.x; t < N0 + N1 + N2; t += 256) {
-          if (t < N0)
-            column_phase<P, Q, DUAL, E, 0>(A, S0, t, gx0[0], gy0[0], zfirst(0, ez), nx1, zfirst(0, ezn) + G0::NZ - 1,
-                                           vzp(0, ez), vzp(0, ezn), scr0, zfirst(0, ez) - zfirst(0, B.ez0));
-          else if (t < N0 + N1)
-            column_phase<P, Q, DUAL, E, 1>(A, S1, t - N0, gx0[1], gy0[1], zfirst(1, ez), nx1,
-                                           zfirst(1, ezn) + G1::NZ - 1, vzp(1, ez), vzp(1, ezn), scr1,
-                                           zfirst(1, ez) - zfirst(1, B.ez0));
-          else
-            column_phase<P, Q, DUAL, E, 2>(A, S2, t - N0 - N1, gx0[2], gy0[2], zfirst(2, ez), nx1,
-                                           zfirst(2, ezn) + G2::NZ - 1, vzp(2, ez), vzp(2, ezn), scr2,
-                                           zfirst(2, ez) - zfirst(2, B.ez0));
-        }
-      }
-      S0.base = S0.slot(1);
-      S1.base = S1.slot(1);
-      S2.base = S2.slot(1);
+      // y testing of this layer; on the threads it leaves idle, the next layer's top coefficient
+      // layer and z interpolation (Z1 was last read by this layer's y interpolation)
+      SGM_BRICK_TASKS3U(test_y, 1, Q * G0::PX, Q * G1::PX, Q * G2::PX)
+      if (ez + 1 < B.ez1) columns_next(ez + 1, Q * (G0::PX + G1::PX + G2::PX));
       __syncthreads();
     }
+    // z testing and flush of the last element layer (columns and flush_layer map threads differently)
+    columns_test(B.ez1 - 1, 0);
+    __syncthreads();
     // the remaining NZ-1 output layers of the last element layer (layer jz now sits in slot jz-1)
     for (int jz = 1; jz < G0::NZ; ++jz)
-      flush_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, B.ez1 - 1) + jz, S0.slot(jz - 1), scr0,
+      flush_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, B.ez1 - 1) + jz, S0.sloty(jz - 1), scr0,
                                     zfirst(0, B.ez1 - 1) + jz - zfirst(0, B.ez0));
     for (int jz = 1; jz < G1::NZ; ++jz)
-      flush_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, B.ez1 - 1) + jz, S1.slot(jz - 1), scr1,
+      flush_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, B.ez1 - 1) + jz, S1.sloty(jz - 1), scr1,
                                     zfirst(1, B.ez1 - 1) + jz - zfirst(1, B.ez0));
     for (int jz = 1; jz < G2::NZ; ++jz)
-      flush_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, B.ez1 - 1) + jz, S2.slot(jz - 1), scr2,
+      flush_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, B.ez1 - 1) + jz, S2.sloty(jz - 1), scr2,
                                     zfirst(2, B.ez1 - 1) + jz - zfirst(2, B.ez0));
     __syncthreads();
   }
