@@ -261,10 +261,8 @@ __device__ __forceinline__ void interp_x(const CompSm<P, Q, DUAL, E, C>& S, int 
 #pragma unroll
       for (int jx = 0; jx < G::NX; ++jx) s = fma(V(S.Vx, hf * EH + el, qx, jx), zv[el + jx], s);
       const int ui = uidx<Q, E>(t / G::EQ, t % G::EQ, hf * EH + el, qx);
-      if (Wm) {
-        const bool live = (hf * EH + el) < nex && (t % G::EQ) / Q < ney;
-        s = live ? wsc * Wm[ui] * s : 0.0;
-      }
+      // (W is zero at the slots of elements past the mesh edge, where s is finite: zero tables)
+      if (Wm) s = wsc * Wm[ui] * s;
       S.U[ui] = s;
     }
 }
@@ -748,13 +746,14 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
                 wyz = g * mm(1, 2);
               }
             } else {
+              // (zero at the slots of elements past the mesh edge)
               const double* w = Wsm + i;
-              wxx = live ? w[0 * L::NU] : 0.0;
-              wyy = live ? w[1 * L::NU] : 0.0;
-              wzz = live ? w[2 * L::NU] : 0.0;
-              wxy = live ? w[3 * L::NU] : 0.0;
-              wxz = live ? w[4 * L::NU] : 0.0;
-              wyz = live ? w[5 * L::NU] : 0.0;
+              wxx = w[0 * L::NU];
+              wyy = w[1 * L::NU];
+              wzz = w[2 * L::NU];
+              wxy = w[3 * L::NU];
+              wxz = w[4 * L::NU];
+              wyz = w[5 * L::NU];
             }
             S0.U[i] = wxx * u0 + wxy * u1 + wxz * u2;
             S1.U[i] = wxy * u0 + wyy * u1 + wyz * u2;

@@ -148,6 +148,20 @@ void basis_values_1d(int p, int n, int Q, int space, std::vector<double>& vals, 
       }
     }
   }
+  // Elements whose functions see only uniform knots have the same local table in exact arithmetic;
+  // the evaluation above differs between them by rounding only (about n * 1e-16 relative).  Such an
+  // element takes its predecessor's table bit for bit, so that kernels can hold one element table
+  // in registers for all interior elements (the brick kernel's uniform-basis path).
+  const size_t tl = size_t(Q) * nl;
+  for (int e = 1; e < n; ++e) {
+    if (first[e] - first[e - 1] != 1) continue;
+    const double* prev = &vals[size_t(e - 1) * tl];
+    double* cur = &vals[size_t(e) * tl];
+    bool same = true;
+    for (size_t i = 0; i < tl && same; ++i)
+      same = std::fabs(cur[i] - prev[i]) <= 1e-11 * std::max(std::fabs(prev[i]), std::fabs(cur[i]));
+    if (same) std::copy(prev, prev + tl, cur);
+  }
 }
 
 namespace {
