@@ -715,6 +715,10 @@ void hodge_args(const Plan& P, int which, const double* x, double* y, HodgeArgs&
     h.first_off[a][0] = int(P.first_off[a][own]);
     h.first_off[a][1] = int(P.first_off[a][oth]);
     h.nel[a] = P.n[a];
+    if (a < 2) {
+      std::copy_n(P.basis_mid[a][own], 25, h.uni[0][a]);
+      std::copy_n(P.basis_mid[a][oth], 25, h.uni[1][a]);
+    }
   }
   h.Q = P.Q;
   h.dual = (which == SGM_MASS_EPS) ? 1 : 0;
@@ -899,6 +903,8 @@ sgm_status upload_basis(Plan& P) {
       std::vector<int> f;
       basis_values_1d(P.p, P.n[a], P.Q, s, v, f);
       P.basis_off[a][s] = vals_all.size();
+      if (P.Q * (P.p + 1) <= 25)
+        std::copy_n(v.begin() + size_t(P.n[a] / 2) * P.Q * (P.p + 1), P.Q * (P.p + 1), P.basis_mid[a][s]);
       P.first_off[a][s] = first_all.size();
       vals_all.insert(vals_all.end(), v.begin(), v.end());
       first_all.insert(first_all.end(), f.begin(), f.end());

@@ -160,7 +160,7 @@ __device__ __forceinline__ void load_layer(const HodgeArgs& A, const CompSm<P, Q
 // item), or null -> fp64 atomics into y
 template <int P, int Q, int DUAL, int E, int C>
 __device__ __forceinline__ void flush_layer(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int gx0, int gy0,
-                                            int gz, int sl, double* scr, int rel) {
+                                            int gz, int sl, double* scr, int rel, double sc) {
   using G = Geo<P, Q, DUAL, E, C>;
   constexpr int LAY = G::PY * G::PX;
   const int* ext = A.ext[C];
@@ -169,8 +169,8 @@ __device__ __forceinline__ void flush_layer(const HodgeArgs& A, const CompSm<P, 
     const int px = o % G::PX, py = o / G::PX;
     const int gx = gx0 + px, gy = gy0 + py;
     if (gx >= 0 && gx < ext[0] && gy >= 0 && gy < ext[1] && gz >= 0 && gz < ext[2]) {
-      if (scr) scr[rel * LAY + o] = S.Yw[sl * LAY + o];
-      else atomicAdd(y + gx + long(ext[0]) * (gy + long(ext[1]) * gz), S.Yw[sl * LAY + o]);
+      if (scr) scr[rel * LAY + o] = sc * S.Yw[sl * LAY + o];
+      else atomicAdd(y + gx + long(ext[0]) * (gy + long(ext[1]) * gz), sc * S.Yw[sl * LAY + o]);
     }
     S.Yw[sl * LAY + o] = 0.0;
   }
@@ -198,32 +198,27 @@ __device__ __forceinline__ void interp_z(const CompSm<P, Q, DUAL, E, C>& S, int 
 // y: Z2[qz][ey*Q+qy][px] = sum_jy Vy[ey][qy][jy] Z1[qz][ey+jy][px]   (tasks: qz, px)
 // UNI: every element of the brick has the same 1D basis table along this axis (interior
 // elements of a uniform mesh): the Q x N coefficients live in registers for the whole task.
-template <int Q, int N, int NL, bool UNI>
+// UNI: the interior table of the axis and role comes from the kernel parameters (HodgeArgs::uni),
+// so the FMAs take the coefficients as constant-bank operands: no loads and no registers.
+template <int Q, int N, int NL, bool UNI, int ROLE, int AXIS>
 struct Coef {
-  double c[UNI ? Q * N : 1];
-  __device__ __forceinline__ Coef(const double* V) {
-    if (UNI) {
-#pragma unroll
-      for (int q = 0; q < Q; ++q)
-#pragma unroll
-        for (int j = 0; j < N; ++j) c[q * N + j] = V[q * NL + j];
-    }
-  }
+  const HodgeArgs& A;
+  __device__ __forceinline__ Coef(const HodgeArgs& a) : A(a) {}
   __device__ __forceinline__ double operator()(const double* V, int e, int q, int j) const {
-    return UNI ? c[q * N + j] : V[(e * Q + q) * NL + j];
+    return UNI ? A.uni[ROLE][AXIS][q * NL + j] : V[(e * Q + q) * NL + j];
   }
 };
 
 // (tasks: half, qz, px -- each half of the brick's elements along y is a separate task)
 template <int P, int Q, int DUAL, int E, int C, bool UNI>
-__device__ __forceinline__ void interp_y(const CompSm<P, Q, DUAL, E, C>& S, int t) {
+__device__ __forceinline__ void interp_y(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int t) {
   using G = Geo<P, Q, DUAL, E, C>;
   constexpr int NL = P + 1, EH = E / 2;
   if (t >= 2 * Q * G::PX) return;
   const int hf = t / (Q * G::PX);
   t -= hf * Q * G::PX;
   const int px = t % G::PX, qz = t / G::PX;
-  const Coef<Q, G::NY, NL, UNI> V(S.Vy);
+  const Coef<Q, G::NY, NL, UNI, (C == 1 ? 0 : 1), 1> V(A);
   double zv[EH - 1 + G::NY];
 #pragma unroll
   for (int py = 0; py < EH - 1 + G::NY; ++py) zv[py] = S.Z1[qz * G::LAYP + (hf * EH + py) * G::PX + px];
@@ -240,16 +235,17 @@ __device__ __forceinline__ void interp_y(const CompSm<P, Q, DUAL, E, C>& S, int 
 
 // x: U[qz][Y][ex*Q+qx] = sum_jx Vx[ex][qx][jx] Z2[qz][Y][ex+jx]    (tasks: qz, Y)
 template <int P, int Q, int DUAL, int E, int C, bool UNI>
-__device__ __forceinline__ void interp_x(const CompSm<P, Q, DUAL, E, C>& S, int t, const double* Wm = nullptr,
-                                         double wsc = 1.0, int nex = E, int ney = E) {
+__device__ __forceinline__ void interp_x(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int t, const double* Wm = nullptr,
+                                         int nex = E, int ney = E) {
   // (tasks: half, qz, Y -- each half of the brick's elements along x is a separate task).  With Wm
-  // (scalar W, staged element-major like U) the quadrature multiply u *= wsc * w is fused here.
+  // (scalar W, staged in the U slots) the quadrature multiply u *= w is fused here; the
+  // per-component constant of the scalar Hodge is applied when an output layer is flushed.
   using G = Geo<P, Q, DUAL, E, C>;
   constexpr int NL = P + 1, EH = E / 2;
   if (t >= 2 * Q * G::EQ) return;
   const int hf = t / (Q * G::EQ);
   t -= hf * Q * G::EQ;
-  const Coef<Q, G::NX, NL, UNI> V(S.Vx);
+  const Coef<Q, G::NX, NL, UNI, (C == 0 ? 0 : 1), 0> V(A);
   double zv[EH - 1 + G::NX];
 #pragma unroll
   for (int px = 0; px < EH - 1 + G::NX; ++px) zv[px] = S.Z2[(t / G::EQ) * G::Z2P + (t % G::EQ) * G::PXP + hf * EH + px];
@@ -262,7 +258,7 @@ __device__ __forceinline__ void interp_x(const CompSm<P, Q, DUAL, E, C>& S, int 
       for (int jx = 0; jx < G::NX; ++jx) s = fma(V(S.Vx, hf * EH + el, qx, jx), zv[el + jx], s);
       const int ui = uidx<Q, E>(t / G::EQ, t % G::EQ, hf * EH + el, qx);
       // (W is zero at the slots of elements past the mesh edge, where s is finite: zero tables)
-      if (Wm) s = wsc * Wm[ui] * s;
+      if (Wm) s *= Wm[ui];
       S.U[ui] = s;
     }
 }
@@ -270,11 +266,11 @@ __device__ __forceinline__ void interp_x(const CompSm<P, Q, DUAL, E, C>& S, int 
 // ---- testing stages (transposes of the above) ----
 // x: Z2[qz][Y][px] = sum_{ex,qx} Vx[ex][qx][px-ex] U[qz][Y][ex*Q+qx]   (tasks: qz, Y)
 template <int P, int Q, int DUAL, int E, int C, bool UNI>
-__device__ __forceinline__ void test_x(const CompSm<P, Q, DUAL, E, C>& S, int t) {
+__device__ __forceinline__ void test_x(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int t) {
   using G = Geo<P, Q, DUAL, E, C>;
   constexpr int NL = P + 1;
   if (t >= Q * G::EQ) return;
-  const Coef<Q, G::NX, NL, UNI> V(S.Vx);
+  const Coef<Q, G::NX, NL, UNI, (C == 0 ? 0 : 1), 0> V(A);
   double acc[G::PX];
 #pragma unroll
   for (int px = 0; px < G::PX; ++px) acc[px] = 0.0;
@@ -292,11 +288,11 @@ __device__ __forceinline__ void test_x(const CompSm<P, Q, DUAL, E, C>& S, int t)
 
 // y: T1[qz][py][px] = sum_{ey,qy} Vy[ey][qy][py-ey] Z2[qz][ey*Q+qy][px]   (tasks: qz, px)
 template <int P, int Q, int DUAL, int E, int C, bool UNI>
-__device__ __forceinline__ void test_y(const CompSm<P, Q, DUAL, E, C>& S, int t) {
+__device__ __forceinline__ void test_y(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int t) {
   using G = Geo<P, Q, DUAL, E, C>;
   constexpr int NL = P + 1;
   if (t >= Q * G::PX) return;
-  const Coef<Q, G::NY, NL, UNI> V(S.Vy);
+  const Coef<Q, G::NY, NL, UNI, (C == 1 ? 0 : 1), 1> V(A);
   const int px = t % G::PX, qz = t / G::PX;
   double acc[G::PY];
 #pragma unroll
@@ -321,7 +317,7 @@ __device__ __forceinline__ void test_y(const CompSm<P, Q, DUAL, E, C>& S, int t)
 template <int P, int Q, int DUAL, int E, int C>
 __device__ __forceinline__ void column_test(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int t, int gx0,
                                             int gy0, int gz_flush, const double* __restrict__ vz, double* scr,
-                                            int rel) {
+                                            int rel, double sc) {
   using G = Geo<P, Q, DUAL, E, C>;
   constexpr int NL = P + 1, LAY = G::PY * G::PX;
   if (t >= LAY) return;
@@ -340,8 +336,8 @@ __device__ __forceinline__ void column_test(const HodgeArgs& A, const CompSm<P, 
     for (int qz = 0; qz < Q; ++qz) acc = fma(__ldg(vz + qz * NL + jz), zv[qz], acc);
     if (jz == 0) {
       if (inxy && gz_flush >= 0 && gz_flush < ext[2]) {
-        if (scr) scr[rel * LAY + t] = acc;
-        else atomicAdd(A.y[C] + gx + long(ext[0]) * (gy + long(ext[1]) * gz_flush), acc);
+        if (scr) scr[rel * LAY + t] = sc * acc;
+        else atomicAdd(A.y[C] + gx + long(ext[0]) * (gy + long(ext[1]) * gz_flush), sc * acc);
       }
       S.Yw[sl * LAY + t] = 0.0;
     } else {
@@ -396,12 +392,12 @@ __device__ __forceinline__ void column_next(const HodgeArgs& A, const CompSm<P, 
                u2 = uni[1 * 2 + AXIS];                                                               \
     for (int t = threadIdx.x; t < (N0) + (N1) + (N2); t += 256) {                                    \
       if (t < (N0)) {                                                                                \
-        if (u0) F<P, Q, DUAL, E, 0, true>(S0, t); else F<P, Q, DUAL, E, 0, false>(S0, t);            \
+        if (u0) F<P, Q, DUAL, E, 0, true>(A, S0, t); else F<P, Q, DUAL, E, 0, false>(A, S0, t);            \
       } else if (t < (N0) + (N1)) {                                                                  \
-        if (u1) F<P, Q, DUAL, E, 1, true>(S1, t - (N0)); else F<P, Q, DUAL, E, 1, false>(S1, t - (N0)); \
+        if (u1) F<P, Q, DUAL, E, 1, true>(A, S1, t - (N0)); else F<P, Q, DUAL, E, 1, false>(A, S1, t - (N0)); \
       } else {                                                                                       \
-        if (u2) F<P, Q, DUAL, E, 2, true>(S2, t - (N0) - (N1));                                      \
-        else F<P, Q, DUAL, E, 2, false>(S2, t - (N0) - (N1));                                        \
+        if (u2) F<P, Q, DUAL, E, 2, true>(A, S2, t - (N0) - (N1));                                      \
+        else F<P, Q, DUAL, E, 2, false>(A, S2, t - (N0) - (N1));                                        \
       }                                                                                              \
     }                                                                                                \
   }
@@ -542,9 +538,9 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
     for (int r = 0; r < 4; ++r) {
       const double* T = tab + r * L::VXY;
       bool same = (r % 2 == 0 ? B.nex : B.ney) == E;
-      // (interior elements of the uniform mesh: equal up to the rounding of their construction)
-      for (int i = threadIdx.x; i < (E - 1) * Q * NL; i += 256)
-        same = same && fabs(T[Q * NL + i] - T[i % (Q * NL)]) <= 1e-14 * (1.0 + fabs(T[i % (Q * NL)]));
+      // (interior elements of the uniform mesh share one table bit for bit, host_setup.cpp; the
+      // parameter copy A.uni is that table)
+      for (int i = threadIdx.x; i < E * Q * NL; i += 256) same = same && T[i] == A.uni[r / 2][r % 2][i % (Q * NL)];
       uni[r] = __syncthreads_and(same) != 0;
     }
     // deterministic accumulation: this item's output patches go to the scratch (summed in a fixed
@@ -594,19 +590,21 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
     auto vzp = [&](int c, int ez) {
       return A.basis + A.basis_off[2][c == 2 ? 0 : 1] + size_t(ez) * Q * NL;
     };
+    // output scale: the scalar Hodge's per-component constant (the full W carries everything)
+    const double osc[3] = {FULL ? 1.0 : A.scale[0], FULL ? 1.0 : A.scale[1], FULL ? 1.0 : A.scale[2]};
     // the columns' tasks start at thread `shift` (after the y stage's tasks of the same interval)
     constexpr int NC0 = G0::PY * G0::PX, NC1 = G1::PY * G1::PX, NC2 = G2::PY * G2::PX;
     auto columns_test = [&](int ezl, int shift) {
       for (int t = (threadIdx.x + 256 - shift % 256) % 256; t < NC0 + NC1 + NC2; t += 256) {
         if (t < NC0)
           column_test<P, Q, DUAL, E, 0>(A, S0, t, gx0[0], gy0[0], zfirst(0, ezl), vzp(0, ezl), scr0,
-                                        zfirst(0, ezl) - zfirst(0, B.ez0));
+                                        zfirst(0, ezl) - zfirst(0, B.ez0), osc[0]);
         else if (t < NC0 + NC1)
           column_test<P, Q, DUAL, E, 1>(A, S1, t - NC0, gx0[1], gy0[1], zfirst(1, ezl), vzp(1, ezl), scr1,
-                                        zfirst(1, ezl) - zfirst(1, B.ez0));
+                                        zfirst(1, ezl) - zfirst(1, B.ez0), osc[1]);
         else
           column_test<P, Q, DUAL, E, 2>(A, S2, t - NC0 - NC1, gx0[2], gy0[2], zfirst(2, ezl), vzp(2, ezl), scr2,
-                                        zfirst(2, ezl) - zfirst(2, B.ez0));
+                                        zfirst(2, ezl) - zfirst(2, B.ez0), osc[2]);
       }
       S0.ybase = S0.sloty(1);
       S1.ybase = S1.sloty(1);
@@ -668,14 +666,14 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
         for (int t = threadIdx.x; t < 3 * 2 * Q * EQ; t += 256) {
           const int c = t / (2 * Q * EQ), tt = t % (2 * Q * EQ);
           if (c == 0) {
-            if (u0) interp_x<P, Q, DUAL, E, 0, true>(S0, tt, Wm, A.scale[0], B.nex, B.ney);
-            else interp_x<P, Q, DUAL, E, 0, false>(S0, tt, Wm, A.scale[0], B.nex, B.ney);
+            if (u0) interp_x<P, Q, DUAL, E, 0, true>(A, S0, tt, Wm, B.nex, B.ney);
+            else interp_x<P, Q, DUAL, E, 0, false>(A, S0, tt, Wm, B.nex, B.ney);
           } else if (c == 1) {
-            if (u1) interp_x<P, Q, DUAL, E, 1, true>(S1, tt, Wm, A.scale[1], B.nex, B.ney);
-            else interp_x<P, Q, DUAL, E, 1, false>(S1, tt, Wm, A.scale[1], B.nex, B.ney);
+            if (u1) interp_x<P, Q, DUAL, E, 1, true>(A, S1, tt, Wm, B.nex, B.ney);
+            else interp_x<P, Q, DUAL, E, 1, false>(A, S1, tt, Wm, B.nex, B.ney);
           } else {
-            if (u2) interp_x<P, Q, DUAL, E, 2, true>(S2, tt, Wm, A.scale[2], B.nex, B.ney);
-            else interp_x<P, Q, DUAL, E, 2, false>(S2, tt, Wm, A.scale[2], B.nex, B.ney);
+            if (u2) interp_x<P, Q, DUAL, E, 2, true>(A, S2, tt, Wm, B.nex, B.ney);
+            else interp_x<P, Q, DUAL, E, 2, false>(A, S2, tt, Wm, B.nex, B.ney);
           }
         }
         if (OTF) {
@@ -776,13 +774,13 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
     // the remaining NZ-1 output layers of the last element layer (layer jz now sits in slot jz-1)
     for (int jz = 1; jz < G0::NZ; ++jz)
       flush_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, B.ez1 - 1) + jz, S0.sloty(jz - 1), scr0,
-                                    zfirst(0, B.ez1 - 1) + jz - zfirst(0, B.ez0));
+                                    zfirst(0, B.ez1 - 1) + jz - zfirst(0, B.ez0), osc[0]);
     for (int jz = 1; jz < G1::NZ; ++jz)
       flush_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, B.ez1 - 1) + jz, S1.sloty(jz - 1), scr1,
-                                    zfirst(1, B.ez1 - 1) + jz - zfirst(1, B.ez0));
+                                    zfirst(1, B.ez1 - 1) + jz - zfirst(1, B.ez0), osc[1]);
     for (int jz = 1; jz < G2::NZ; ++jz)
       flush_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, B.ez1 - 1) + jz, S2.sloty(jz - 1), scr2,
-                                    zfirst(2, B.ez1 - 1) + jz - zfirst(2, B.ez0));
+                                    zfirst(2, B.ez1 - 1) + jz - zfirst(2, B.ez0), osc[2]);
     __syncthreads();
   }
 }
