@@ -131,8 +131,7 @@ __global__ void hodge_general_kernel(const __grid_constant__ HodgeArgs A) {
   }
 }
 
-// Work decomposition of the brick kernel: bricks of E x E elements in (x, y) times z chunks sized for
-// about four work items per resident CTA (at least 4 element layers per chunk).
+// Work decomposition of the brick kernel: bricks of E x E elements in (x, y) times z chunks.
 template <int P, int Q, int DUAL, bool FULL, bool OTF = false>
 void brick_plan(const int nel[3], int& zchunk, long& items, long& slots, size_t& smem) {
   constexpr int E = 4;
@@ -143,14 +142,21 @@ void brick_plan(const int nel[3], int& zchunk, long& items, long& slots, size_t&
     cudaFuncSetAttribute(brick::hodge_brick_kernel<P, Q, DUAL, FULL, E, OTF>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, brick::hodge_brick_kernel<P, Q, DUAL, FULL, E, OTF>, 256,
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, brick::hodge_brick_kernel<P, Q, DUAL, FULL, E, OTF>, brick::brick_threads(P),
                                                 smem);
   if (per_sm < 1) per_sm = 1;
   slots = long(per_sm) * sm_count();
   const long bricks = long((nel[0] + E - 1) / E) * ((nel[1] + E - 1) / E);
-  long bzn = (4 * slots + bricks - 1) / bricks;
-  zchunk = int((nel[2] + bzn - 1) / bzn);
-  if (zchunk < 4) zchunk = 4;
+  // z chunks per brick: the count that minimises rounds x (layers per chunk + the per-item cost of
+  // about two layers: tables, window fill, the extra flushed layers), rounds = items over resident
+  // CTAs rounded up; chunks of at least 4 layers
+  long best = -1;
+  for (long bzn = 1; bzn <= std::max(1, nel[2] / 4); ++bzn) {
+    const long zc = (nel[2] + bzn - 1) / bzn;
+    const long its = bricks * ((nel[2] + zc - 1) / zc);
+    const long cost = ((its + slots - 1) / slots) * (zc + 2);
+    if (best < 0 || cost < best) best = cost, zchunk = int(zc);
+  }
   if (const int zc = tune_int("SGM_HODGE_ZCHUNK", 0)) zchunk = zc;
   items = bricks * ((nel[2] + zchunk - 1) / zchunk);
 }
@@ -173,7 +179,7 @@ void launch_hodge_brick(const HodgeArgs& a, cudaStream_t st) {
     for (int c = 0; c < 3; ++c)
       cudaMemsetAsync(a.y[c], 0, size_t(a.ext[c][0]) * a.ext[c][1] * a.ext[c][2] * sizeof(double), st);
   }
-  brick::hodge_brick_kernel<P, Q, DUAL, FULL, E, OTF><<<unsigned(grid), 256, smem, st>>>(b, zchunk);
+  brick::hodge_brick_kernel<P, Q, DUAL, FULL, E, OTF><<<unsigned(grid), brick::brick_threads(P), smem, st>>>(b, zchunk);
   if (b.scratch) brick::hodge_gather_kernel<P, Q, DUAL, E><<<unsigned(4 * sm_count()), 256, 0, st>>>(b, zchunk);
 }
 

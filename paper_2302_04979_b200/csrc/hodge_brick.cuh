@@ -20,6 +20,10 @@
 #include "kernels.cuh"
 #include "pipe_sweep.cuh"
 
+#ifndef SGM_BRICK_NT4
+#define SGM_BRICK_NT4 256
+#endif
+
 namespace sgm {
 namespace brick {
 
@@ -92,7 +96,7 @@ struct Brick {
 // E*Q + 1 doubles: the x stages' tasks (qz, Y) then walk U with an odd stride (no bank conflicts);
 // W uses the same slots, in HBM as well: per brick and element layer one contiguous chunk of NW
 // planes (entry k of a point in plane k at the point's U slot; pad slots and elements past the
-// mesh edge hold zeros), so a layer's W is staged by a single bulk copy (host: brick_w_relayout)
+// mesh edge hold zeros), so a layer's W is staged by a single bulk copy (host: hodge_brick_relayout)
 template <int Q, int E>
 __device__ __forceinline__ int uidx(int qz, int Yq, int ex, int qx) {
   return (qz * (E * Q) + Yq) * (E * Q + 1) + ex * Q + qx;
@@ -377,7 +381,7 @@ __device__ __forceinline__ void column_next(const HodgeArgs& A, const CompSm<P, 
 // run stage F for the three components, tasks of component c offset so that all threads work
 #define SGM_BRICK_STAGE3(F, N0, N1, N2)                                     \
   {                                                                         \
-    for (int t = threadIdx.x; t < (N0) + (N1) + (N2); t += 256) {           \
+    for (int t = threadIdx.x; t < (N0) + (N1) + (N2); t += NT) {           \
       if (t < (N0)) F<P, Q, DUAL, E, 0>(S0, t);                             \
       else if (t < (N0) + (N1)) F<P, Q, DUAL, E, 1>(S1, t - (N0));          \
       else F<P, Q, DUAL, E, 2>(S2, t - (N0) - (N1));                        \
@@ -390,7 +394,7 @@ __device__ __forceinline__ void column_next(const HodgeArgs& A, const CompSm<P, 
   {                                                                                                  \
     const bool u0 = uni[(AXIS == 0 ? 0 : 1) * 2 + AXIS], u1 = uni[(AXIS == 1 ? 0 : 1) * 2 + AXIS],  \
                u2 = uni[1 * 2 + AXIS];                                                               \
-    for (int t = threadIdx.x; t < (N0) + (N1) + (N2); t += 256) {                                    \
+    for (int t = threadIdx.x; t < (N0) + (N1) + (N2); t += NT) {                                    \
       if (t < (N0)) {                                                                                \
         if (u0) F<P, Q, DUAL, E, 0, true>(A, S0, t); else F<P, Q, DUAL, E, 0, false>(A, S0, t);            \
       } else if (t < (N0) + (N1)) {                                                                  \
@@ -475,14 +479,19 @@ __global__ void __launch_bounds__(256) hodge_gather_kernel(const __grid_constant
   }
 }
 
+// threads per CTA.  At p = 4 the x stages have 300 (testing) and 600 (interpolation) tasks: one and
+// two rounds of 320 threads instead of two and three of 256, but 320 threads leave 96 registers per
+// thread (spills) and measured slower (C4 apply 1.12 -> 1.19 ms), so SGM_BRICK_NT4 stays 256
+__host__ __device__ constexpr int brick_threads(int p) { return p == 4 ? SGM_BRICK_NT4 : 256; }
+
 template <int P, int Q, int DUAL, bool FULL, int E, bool OTF>
-__global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_constant__ HodgeArgs A, int zchunk) {
+__global__ void __launch_bounds__(brick_threads(P), 2) hodge_brick_kernel(const __grid_constant__ HodgeArgs A, int zchunk) {
   static_assert(!OTF || FULL, "on-the-fly geometry: general maps only");
   using L = Layout<P, Q, DUAL, E>;
   using G0 = Geo<P, Q, DUAL, E, 0>;
   using G1 = Geo<P, Q, DUAL, E, 1>;
   using G2 = Geo<P, Q, DUAL, E, 2>;
-  constexpr int NL = P + 1, EQ = E * Q;
+  constexpr int NL = P + 1, EQ = E * Q, NT = brick_threads(P);
   extern __shared__ __align__(16) double sm[];
   __shared__ unsigned long long wbar;  // completion of the staged W (one phase per element layer)
   unsigned wphase = 0;
@@ -514,7 +523,7 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
       B.ez1 = min(nz, B.ez0 + zchunk);
     }
     // brick x / y basis tables [role][axis][e][q][k] (elements past the mesh edge: zeros)
-    for (int o = threadIdx.x; o < 2 * 2 * L::VXY; o += 256) {
+    for (int o = threadIdx.x; o < 2 * 2 * L::VXY; o += NT) {
       const int role = o / (2 * L::VXY), r = o % (2 * L::VXY), axis = r / L::VXY, i = r % L::VXY;
       const int e = i / (Q * NL), rem = i % (Q * NL);
       const int eg = (axis == 0 ? B.ex0 : B.ey0) + e;
@@ -523,7 +532,7 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
     }
     if (OTF) {
       // map tables of the brick's x / y elements [axis][s][e][q][k] (zeros past the mesh edge)
-      for (int o = threadIdx.x; o < L::MT; o += 256) {
+      for (int o = threadIdx.x; o < L::MT; o += NT) {
         const int axis = o / (2 * E * Q * NL), r = o % (2 * E * Q * NL), sv = r / (E * Q * NL), i = r % (E * Q * NL);
         const int e = i / (Q * NL), rem = i % (Q * NL);
         const int eg = (axis == 0 ? B.ex0 : B.ey0) + e;
@@ -540,7 +549,7 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
       bool same = (r % 2 == 0 ? B.nex : B.ney) == E;
       // (interior elements of the uniform mesh share one table bit for bit, host_setup.cpp; the
       // parameter copy A.uni is that table)
-      for (int i = threadIdx.x; i < E * Q * NL; i += 256) same = same && T[i] == A.uni[r / 2][r % 2][i % (Q * NL)];
+      for (int i = threadIdx.x; i < E * Q * NL; i += NT) same = same && T[i] == A.uni[r / 2][r % 2][i % (Q * NL)];
       uni[r] = __syncthreads_and(same) != 0;
     }
     // deterministic accumulation: this item's output patches go to the scratch (summed in a fixed
@@ -560,14 +569,14 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
     // zero output windows, load the NZ coefficient layers and z bases of the first element layer
     S0.xbase = S1.xbase = S2.xbase = 0;
     S0.ybase = S1.ybase = S2.ybase = 0;
-    for (int o = threadIdx.x; o < G0::WIN; o += 256) S0.Yw[o] = 0.0;
-    for (int o = threadIdx.x; o < G1::WIN; o += 256) S1.Yw[o] = 0.0;
-    for (int o = threadIdx.x; o < G2::WIN; o += 256) S2.Yw[o] = 0.0;
+    for (int o = threadIdx.x; o < G0::WIN; o += NT) S0.Yw[o] = 0.0;
+    for (int o = threadIdx.x; o < G1::WIN; o += NT) S1.Yw[o] = 0.0;
+    for (int o = threadIdx.x; o < G2::WIN; o += NT) S2.Yw[o] = 0.0;
     for (int jz = 0; jz < G0::NZ; ++jz) load_layer<P, Q, DUAL, E, 0>(A, S0, gx0[0], gy0[0], zfirst(0, B.ez0) + jz, jz);
     for (int jz = 0; jz < G1::NZ; ++jz) load_layer<P, Q, DUAL, E, 1>(A, S1, gx0[1], gy0[1], zfirst(1, B.ez0) + jz, jz);
     for (int jz = 0; jz < G2::NZ; ++jz) load_layer<P, Q, DUAL, E, 2>(A, S2, gx0[2], gy0[2], zfirst(2, B.ez0) + jz, jz);
     auto load_vz = [&](int ez) {
-      for (int o = threadIdx.x; o < 2 * L::VZ; o += 256) {
+      for (int o = threadIdx.x; o < 2 * L::VZ; o += NT) {
         const int role = o / L::VZ;
         tab[4 * L::VXY + o] = __ldg(A.basis + A.basis_off[2][role] + size_t(ez) * Q * NL + (o % L::VZ));
       }
@@ -595,7 +604,7 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
     // the columns' tasks start at thread `shift` (after the y stage's tasks of the same interval)
     constexpr int NC0 = G0::PY * G0::PX, NC1 = G1::PY * G1::PX, NC2 = G2::PY * G2::PX;
     auto columns_test = [&](int ezl, int shift) {
-      for (int t = (threadIdx.x + 256 - shift % 256) % 256; t < NC0 + NC1 + NC2; t += 256) {
+      for (int t = (threadIdx.x + NT - shift % NT) % NT; t < NC0 + NC1 + NC2; t += NT) {
         if (t < NC0)
           column_test<P, Q, DUAL, E, 0>(A, S0, t, gx0[0], gy0[0], zfirst(0, ezl), vzp(0, ezl), scr0,
                                         zfirst(0, ezl) - zfirst(0, B.ez0), osc[0]);
@@ -611,7 +620,7 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
       S2.ybase = S2.sloty(1);
     };
     auto columns_next = [&](int ezn, int shift) {
-      for (int t = (threadIdx.x + 256 - shift % 256) % 256; t < NC0 + NC1 + NC2; t += 256) {
+      for (int t = (threadIdx.x + NT - shift % NT) % NT; t < NC0 + NC1 + NC2; t += NT) {
         if (t < NC0)
           column_next<P, Q, DUAL, E, 0>(A, S0, t, gx0[0], gy0[0], zfirst(0, ezn) + G0::NZ - 1, vzp(0, ezn));
         else if (t < NC0 + NC1)
@@ -631,7 +640,7 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
         const int NXm = nx + P, NYm = ny + P;
         const double* tz0 = A.geo_tab + A.geo_tab_off[2][0] + size_t(ez) * Q * NL;
         const double* tz1 = A.geo_tab + A.geo_tab_off[2][1] + size_t(ez) * Q * NL;
-        for (int t = threadIdx.x; t < 3 * PM * PM; t += 256) {
+        for (int t = threadIdx.x; t < 3 * PM * PM; t += NT) {
           const int r = t / (PM * PM), o = t - r * PM * PM, py = o / PM, px = o - py * PM;
           const int gx = B.ex0 + px, gy = B.ey0 + py;
           double c[NL];
@@ -663,7 +672,7 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
       {
         const bool u0 = uni[0 * 2 + 0], u1 = uni[1 * 2 + 0], u2 = uni[1 * 2 + 0];
         const double* Wm = FULL ? nullptr : Wsm;
-        for (int t = threadIdx.x; t < 3 * 2 * Q * EQ; t += 256) {
+        for (int t = threadIdx.x; t < 3 * 2 * Q * EQ; t += NT) {
           const int c = t / (2 * Q * EQ), tt = t % (2 * Q * EQ);
           if (c == 0) {
             if (u0) interp_x<P, Q, DUAL, E, 0, true>(A, S0, tt, Wm, B.nex, B.ney);
@@ -679,7 +688,7 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
         if (OTF) {
           // map, y: B[r][m][qz][ey*Q+qy][px] = sum_j Ty_sy[ey][qy][j] A[r][sz][qz][ey + j][px],
           // m = 0: (sz, sy) = (val, val), 1: (val, der), 2: (der, val)
-          for (int t = threadIdx.x; t < 9 * Q * PM; t += 256) {
+          for (int t = threadIdx.x; t < 9 * Q * PM; t += NT) {
             const int rm = t / (Q * PM), o = t - rm * Q * PM, qz = o / PM, px = o - qz * PM;
             const int r = rm / 3, m = rm - r * 3, sz = m == 2 ? 1 : 0, sy = m == 1 ? 1 : 0;
             const double* a = MAs + ((r * 2 + sz) * Q + qz) * PM * PM + px;
@@ -704,10 +713,10 @@ __global__ void __launch_bounds__(256, 2) hodge_brick_kernel(const __grid_consta
       if (FULL) {
         // quadrature points: v_c = sum_c' W_cc' u_c' (the 3 x 3 W couples the components)
         {
-          // consecutive threads take consecutive U slots (the pad slot of each row is skipped)
-          for (int i = threadIdx.x; i < L::NU; i += 256) {
-            const int X = i % (EQ + 1), row = i / (EQ + 1), Yq = row % EQ;
-            if (X == EQ) continue;
+          // consecutive threads take consecutive points (U slots but for the pad slot of each row)
+          for (int pt = threadIdx.x; pt < Q * EQ * EQ; pt += NT) {
+            const int X = pt % EQ, row = pt / EQ, Yq = row % EQ;
+            const int i = row * (EQ + 1) + X;  // the point's U slot
             const int ex = X / Q, ey = Yq / Q;
             const bool live = ex < B.nex && ey < B.ney;
             const double u0 = S0.U[i], u1 = S1.U[i], u2 = S2.U[i];
