@@ -714,6 +714,8 @@ void hodge_args(const Plan& P, int which, const double* x, double* y, HodgeArgs&
     h.basis_off[a][1] = int(P.basis_off[a][oth]);
     h.first_off[a][0] = int(P.first_off[a][own]);
     h.first_off[a][1] = int(P.first_off[a][oth]);
+    h.first0[a][0] = P.first0[a][own];
+    h.first0[a][1] = P.first0[a][oth];
     h.nel[a] = P.n[a];
     if (a < 2) {
       std::copy_n(P.basis_mid[a][own], 25, h.uni[0][a]);
@@ -906,6 +908,9 @@ sgm_status upload_basis(Plan& P) {
       if (P.Q * (P.p + 1) <= 25)
         std::copy_n(v.begin() + size_t(P.n[a] / 2) * P.Q * (P.p + 1), P.Q * (P.p + 1), P.basis_mid[a][s]);
       P.first_off[a][s] = first_all.size();
+      P.first0[a][s] = f[0];
+      for (int e = 0; e < P.n[a]; ++e)
+        if (f[e] != f[0] + e) return fail(SGM_E_UNSUPPORTED, "first-index table is not affine");
       vals_all.insert(vals_all.end(), v.begin(), v.end());
       first_all.insert(first_all.end(), f.begin(), f.end());
     }

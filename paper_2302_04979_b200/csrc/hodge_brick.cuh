@@ -137,8 +137,10 @@ struct CompSm {
 };
 
 // first global function index of element e along `axis` for `role`
+// (uniform open knots: first(e) = first(0) + e, checked when the tables are uploaded, so the index
+// is arithmetic on a kernel parameter instead of a table load)
 __device__ __forceinline__ int first_of(const HodgeArgs& A, int axis, int role, int e) {
-  return __ldg(A.first + A.first_off[axis][role] + e);
+  return A.first0[axis][role] + e;
 }
 
 // load coefficient layer jz (global z index gz) of component C's patch into the window

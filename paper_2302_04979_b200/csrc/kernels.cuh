@@ -83,6 +83,7 @@ struct HodgeArgs {
   int basis_off[3][2];   // [axis][own/other] offsets (doubles) of [n][Q][p+1] value blocks
   const int* first;      // per-axis first-index tables
   int first_off[3][2];
+  int first0[3][2];      // first index of element 0 (the tables are affine: first(e) = first0 + e)
   int nel[3];
   int Q;
   double* scratch;       // brick kernel: per-item output patches (deterministic two-pass

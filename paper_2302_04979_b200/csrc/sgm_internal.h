@@ -108,6 +108,7 @@ struct Plan {
   double* basis_dev = nullptr;        // general Hodge: per-axis basis values at qp [n][Q][p+1]
   int* first_dev = nullptr;           // per-axis first local global index per element [n]
   size_t basis_off[3][4] = {};        // offsets (doubles) into basis_dev per axis and space
+  int first0[3][4] = {};              // first index of element 0 per axis and space (first(e) = first0 + e)
   double basis_mid[3][4][25] = {};    // host copy of the middle element's table [Q][p+1] per axis and space
   size_t first_off[3][4] = {};        // offsets (ints) into first_dev per axis and space
   // on-the-fly geometry (SGM_OPT_OTF_GEOMETRY): control points [3][(nz+p)(ny+p)(nx+p)] then the
