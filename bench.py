@@ -533,11 +533,18 @@ def main():
                     "minimum 16 B per DOF-update (read and write d and b once, SURVEY 8(d)) at the measured "
                     "step time, over the peak"}
     if dom == "hodge_general" and "tflops" in D:
-        # the general Hodge is bound by fp64 arithmetic issue, not HBM: report it against fp64 peak
-        roof.update({"bound": "alu", "achieved": D["tflops"], "peak": fpk, "unit": "TFLOP/s",
-                     "frac": D["frac_fp64"], "algo_flops_per_launch": kernels["hodge_general"]["algo_flops"],
-                     "peak_source": fpk_src,
-                     "hbm_view": {"achieved": D["gbs"], "peak": peak, "unit": "GB/s", "frac": D["frac"]}})
+        # the general Hodge is reported against the roof it is nearer to: fp64 arithmetic (scalar W at
+        # p = 4: few W bytes per flop) or HBM (full W: 48 B of W per quadrature point);
+        # the other view rides along
+        alu_view = {"achieved": D["tflops"], "peak": fpk, "unit": "TFLOP/s", "frac": D["frac_fp64"],
+                    "peak_source": fpk_src}
+        if D["frac_fp64"] >= D["frac"]:
+            roof.update({"bound": "alu", "achieved": D["tflops"], "peak": fpk, "unit": "TFLOP/s",
+                         "frac": D["frac_fp64"], "peak_source": fpk_src,
+                         "hbm_view": {"achieved": D["gbs"], "peak": peak, "unit": "GB/s", "frac": D["frac"]}})
+        else:
+            roof["alu_view"] = alu_view
+        roof["algo_flops_per_launch"] = kernels["hodge_general"]["algo_flops"]
 
     # the structure-faithful three-axis schedule (every Kronecker factor swept) and the
     # fused-update schedule, timed the same way on the same state (second and third numbers)
