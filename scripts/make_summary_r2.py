@@ -102,7 +102,10 @@ def main(tag):
     L.append("| workload | DOF-updates/s | ms/step | dominant (frac of its peak) | step HBM frac | CPU oracle DOF-updates/s |")
     L.append("|---|---|---|---|---|---|")
     for d in sweep:
-        rr = d["roofline"]
+        rr = dict(d["roofline"])
+        hv = rr.get("hbm_view")
+        if hv and hv["frac"] > rr["frac"]:  # lines written before bench.py picked the nearer roof itself
+            rr.update({"achieved": hv["achieved"], "unit": hv["unit"], "frac": hv["frac"]})
         cb = d.get("cpu_baseline") or {}
         L.append(f"| {d['config']['workload']} | {d['value']:.3g} | {d['ms_per_step']:.3f} | {rr['kernel']} "
                  f"{rr['achieved']:.3g} {rr['unit']} ({rr['frac']:.2f}) | {rr.get('step_frac', 0):.2f} | "
