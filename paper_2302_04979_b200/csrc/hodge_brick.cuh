@@ -471,8 +471,9 @@ __global__ void __launch_bounds__(256) hodge_gather_kernel(const __grid_constant
   for (long i = long(blockIdx.x) * blockDim.x + threadIdx.x; i < n0 + n1 + n2; i += long(gridDim.x) * blockDim.x) {
     const int c = i < n0 ? 0 : (i < n0 + n1 ? 1 : 2);
     const long k = i - (c == 0 ? 0 : (c == 1 ? n0 : n0 + n1));
-    const int X = A.ext[c][0], Y = A.ext[c][1];
-    const int gx = int(k % X), gy = int((k / X) % Y), gz = int(k / (long(X) * Y));
+    // (a component has fewer than 2^31 entries: 32-bit divisions)
+    const unsigned X = unsigned(A.ext[c][0]), Y = unsigned(A.ext[c][1]), ku = unsigned(k), row = ku / X;
+    const int gx = int(ku - row * X), gz = int(row / Y), gy = int(row - unsigned(gz) * Y);
     double v;
     if (c == 0) v = gather_one<P, Q, DUAL, E, 0>(A, zchunk, gx, gy, gz);
     else if (c == 1) v = gather_one<P, Q, DUAL, E, 1>(A, zchunk, gx, gy, gz);
