@@ -717,10 +717,12 @@ void hodge_args(const Plan& P, int which, const double* x, double* y, HodgeArgs&
     h.first0[a][0] = P.first0[a][own];
     h.first0[a][1] = P.first0[a][oth];
     h.nel[a] = P.n[a];
-    if (a < 2) {
-      std::copy_n(P.basis_mid[a][own], 25, h.uni[0][a]);
-      std::copy_n(P.basis_mid[a][oth], 25, h.uni[1][a]);
-    }
+    std::copy_n(P.basis_mid[a][own], 25, h.uni[0][a]);
+    std::copy_n(P.basis_mid[a][oth], 25, h.uni[1][a]);
+    h.uni_lo[a][0] = P.basis_lo[a][own];
+    h.uni_hi[a][0] = P.basis_hi[a][own];
+    h.uni_lo[a][1] = P.basis_lo[a][oth];
+    h.uni_hi[a][1] = P.basis_hi[a][oth];
   }
   h.Q = P.Q;
   h.dual = (which == SGM_MASS_EPS) ? 1 : 0;
@@ -905,8 +907,17 @@ sgm_status upload_basis(Plan& P) {
       std::vector<int> f;
       basis_values_1d(P.p, P.n[a], P.Q, s, v, f);
       P.basis_off[a][s] = vals_all.size();
-      if (P.Q * (P.p + 1) <= 25)
-        std::copy_n(v.begin() + size_t(P.n[a] / 2) * P.Q * (P.p + 1), P.Q * (P.p + 1), P.basis_mid[a][s]);
+      if (P.Q * (P.p + 1) <= 25) {
+        const size_t tl = size_t(P.Q) * (P.p + 1);
+        const int mid = P.n[a] / 2;
+        std::copy_n(v.begin() + mid * tl, tl, P.basis_mid[a][s]);
+        auto same = [&](int e) { return std::equal(v.begin() + e * tl, v.begin() + (e + 1) * tl, v.begin() + mid * tl); };
+        int lo = mid, hi = mid + 1;
+        while (lo > 0 && same(lo - 1)) --lo;
+        while (hi < P.n[a] && same(hi)) ++hi;
+        P.basis_lo[a][s] = lo;
+        P.basis_hi[a][s] = hi;
+      }
       P.first_off[a][s] = first_all.size();
       P.first0[a][s] = f[0];
       for (int e = 0; e < P.n[a]; ++e)

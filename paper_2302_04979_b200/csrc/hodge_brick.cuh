@@ -319,8 +319,9 @@ __device__ __forceinline__ void test_y(const HodgeArgs& A, const CompSm<P, Q, DU
 // in different barrier intervals next to the y stages (whose tasks leave threads idle):
 // column_test (with the next layer's y interpolation): test along z of element layer ez,
 //   Yw[jz][py][px] += sum_qz Vz[qz][jz] T1[qz][py][px], and flush of the completed output slot
-//   (scratch or atomics to y; slot cleared).  vz: the z basis (global, [Q][NL]) of layer ez.
-template <int P, int Q, int DUAL, int E, int C>
+//   (scratch or atomics to y; slot cleared).  vz: the z basis (global, [Q][NL]) of layer ez; UNIZ:
+//   the layer is interior along z (its table is the parameter copy A.uni[role][2]).
+template <int P, int Q, int DUAL, int E, int C, bool UNIZ>
 __device__ __forceinline__ void column_test(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int t, int gx0,
                                             int gy0, int gz_flush, const double* __restrict__ vz, double* scr,
                                             int rel, double sc) {
@@ -339,7 +340,8 @@ __device__ __forceinline__ void column_test(const HodgeArgs& A, const CompSm<P, 
     const int sl = S.sloty(jz);
     double acc = S.Yw[sl * LAY + t];
 #pragma unroll
-    for (int qz = 0; qz < Q; ++qz) acc = fma(__ldg(vz + qz * NL + jz), zv[qz], acc);
+    for (int qz = 0; qz < Q; ++qz)
+      acc = fma(UNIZ ? A.uni[C == 2 ? 0 : 1][2][qz * NL + jz] : __ldg(vz + qz * NL + jz), zv[qz], acc);
     if (jz == 0) {
       if (inxy && gz_flush >= 0 && gz_flush < ext[2]) {
         if (scr) scr[rel * LAY + t] = sc * acc;
@@ -355,7 +357,7 @@ __device__ __forceinline__ void column_test(const HodgeArgs& A, const CompSm<P, 
 // column_next (with the current layer's y testing): the top coefficient layer of the next element
 // layer (global z index gz_load) into the freed window slot and the next layer's z interpolation,
 // Z1[qz][py][px] = sum_jz Vz[qz][jz] Xw[jz][py][px].  vz: the z basis of the next layer.
-template <int P, int Q, int DUAL, int E, int C>
+template <int P, int Q, int DUAL, int E, int C, bool UNIZ>
 __device__ __forceinline__ void column_next(const HodgeArgs& A, const CompSm<P, Q, DUAL, E, C>& S, int t, int gx0,
                                             int gy0, int gz_load, const double* __restrict__ vz) {
   using G = Geo<P, Q, DUAL, E, C>;
@@ -375,7 +377,8 @@ __device__ __forceinline__ void column_next(const HodgeArgs& A, const CompSm<P, 
   for (int qz = 0; qz < Q; ++qz) {
     double s = 0.0;
 #pragma unroll
-    for (int jz = 0; jz < G::NZ; ++jz) s = fma(__ldg(vz + qz * NL + jz), xv[jz], s);
+    for (int jz = 0; jz < G::NZ; ++jz)
+      s = fma(UNIZ ? A.uni[C == 2 ? 0 : 1][2][qz * NL + jz] : __ldg(vz + qz * NL + jz), xv[jz], s);
     S.Z1[qz * G::LAYP + t] = s;
   }
 }
@@ -544,17 +547,20 @@ __global__ void __launch_bounds__(brick_threads(P), 2) hodge_brick_kernel(const 
       }
     }
     __syncthreads();
-    // uni[role*2 + axis]: all live elements of the brick share element 0's table (and the brick is full)
+    // uni[role*2 + axis]: the brick is full and all its elements lie in the axis' interior range, whose
+    // element tables equal the parameter copy A.uni bit for bit (ranges found on the host)
     bool uni[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      const double* T = tab + r * L::VXY;
-      bool same = (r % 2 == 0 ? B.nex : B.ney) == E;
-      // (interior elements of the uniform mesh share one table bit for bit, host_setup.cpp; the
-      // parameter copy A.uni is that table)
-      for (int i = threadIdx.x; i < E * Q * NL; i += NT) same = same && T[i] == A.uni[r / 2][r % 2][i % (Q * NL)];
-      uni[r] = __syncthreads_and(same) != 0;
+      const int ax = r % 2, role = r / 2, e0 = ax == 0 ? B.ex0 : B.ey0;
+      uni[r] = (ax == 0 ? B.nex : B.ney) == E && e0 >= A.uni_lo[ax][role] && e0 + E <= A.uni_hi[ax][role];
     }
+    auto uniz = [&](int c, int ez) {
+      const int role = c == 2 ? 0 : 1;
+      // (the parameter-bank column variants pay at p <= 3: C3 0.1255 -> 0.1235 ms per apply; at p = 4
+      // their extra code costs more than the loads they save: C4 1.129 -> 1.156 ms)
+      return P <= 3 && ez >= A.uni_lo[2][role] && ez < A.uni_hi[2][role];
+    };
     // deterministic accumulation: this item's output patches go to the scratch (summed in a fixed
     // order by hodge_gather_kernel); layer rel of component c at scr_c + rel * PY_c * PX_c
     double *scr0 = nullptr, *scr1 = nullptr, *scr2 = nullptr;
@@ -608,15 +614,21 @@ __global__ void __launch_bounds__(brick_threads(P), 2) hodge_brick_kernel(const 
     constexpr int NC0 = G0::PY * G0::PX, NC1 = G1::PY * G1::PX, NC2 = G2::PY * G2::PX;
     auto columns_test = [&](int ezl, int shift) {
       for (int t = (threadIdx.x + NT - shift % NT) % NT; t < NC0 + NC1 + NC2; t += NT) {
-        if (t < NC0)
-          column_test<P, Q, DUAL, E, 0>(A, S0, t, gx0[0], gy0[0], zfirst(0, ezl), vzp(0, ezl), scr0,
-                                        zfirst(0, ezl) - zfirst(0, B.ez0), osc[0]);
-        else if (t < NC0 + NC1)
-          column_test<P, Q, DUAL, E, 1>(A, S1, t - NC0, gx0[1], gy0[1], zfirst(1, ezl), vzp(1, ezl), scr1,
-                                        zfirst(1, ezl) - zfirst(1, B.ez0), osc[1]);
-        else
-          column_test<P, Q, DUAL, E, 2>(A, S2, t - NC0 - NC1, gx0[2], gy0[2], zfirst(2, ezl), vzp(2, ezl), scr2,
-                                        zfirst(2, ezl) - zfirst(2, B.ez0), osc[2]);
+#define SGM_COLT(C, S, T, SCR)                                                                              \
+  if (uniz(C, ezl))                                                                                          \
+    column_test<P, Q, DUAL, E, C, true>(A, S, T, gx0[C], gy0[C], zfirst(C, ezl), vzp(C, ezl), SCR,           \
+                                        zfirst(C, ezl) - zfirst(C, B.ez0), osc[C]);                          \
+  else                                                                                                       \
+    column_test<P, Q, DUAL, E, C, false>(A, S, T, gx0[C], gy0[C], zfirst(C, ezl), vzp(C, ezl), SCR,          \
+                                         zfirst(C, ezl) - zfirst(C, B.ez0), osc[C]);
+        if (t < NC0) {
+          SGM_COLT(0, S0, t, scr0)
+        } else if (t < NC0 + NC1) {
+          SGM_COLT(1, S1, t - NC0, scr1)
+        } else {
+          SGM_COLT(2, S2, t - NC0 - NC1, scr2)
+        }
+#undef SGM_COLT
       }
       S0.ybase = S0.sloty(1);
       S1.ybase = S1.sloty(1);
@@ -624,13 +636,19 @@ __global__ void __launch_bounds__(brick_threads(P), 2) hodge_brick_kernel(const 
     };
     auto columns_next = [&](int ezn, int shift) {
       for (int t = (threadIdx.x + NT - shift % NT) % NT; t < NC0 + NC1 + NC2; t += NT) {
-        if (t < NC0)
-          column_next<P, Q, DUAL, E, 0>(A, S0, t, gx0[0], gy0[0], zfirst(0, ezn) + G0::NZ - 1, vzp(0, ezn));
-        else if (t < NC0 + NC1)
-          column_next<P, Q, DUAL, E, 1>(A, S1, t - NC0, gx0[1], gy0[1], zfirst(1, ezn) + G1::NZ - 1, vzp(1, ezn));
-        else
-          column_next<P, Q, DUAL, E, 2>(A, S2, t - NC0 - NC1, gx0[2], gy0[2], zfirst(2, ezn) + G2::NZ - 1,
-                                        vzp(2, ezn));
+#define SGM_COLN(C, S, T, NZC)                                                                             \
+  if (uniz(C, ezn))                                                                                         \
+    column_next<P, Q, DUAL, E, C, true>(A, S, T, gx0[C], gy0[C], zfirst(C, ezn) + NZC - 1, vzp(C, ezn));   \
+  else                                                                                                      \
+    column_next<P, Q, DUAL, E, C, false>(A, S, T, gx0[C], gy0[C], zfirst(C, ezn) + NZC - 1, vzp(C, ezn));
+        if (t < NC0) {
+          SGM_COLN(0, S0, t, G0::NZ)
+        } else if (t < NC0 + NC1) {
+          SGM_COLN(1, S1, t - NC0, G1::NZ)
+        } else {
+          SGM_COLN(2, S2, t - NC0 - NC1, G2::NZ)
+        }
+#undef SGM_COLN
       }
       S0.xbase = S0.slotx(1);
       S1.xbase = S1.slotx(1);

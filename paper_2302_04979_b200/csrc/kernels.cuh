@@ -89,8 +89,10 @@ struct HodgeArgs {
   double* scratch;       // brick kernel: per-item output patches (deterministic two-pass
   size_t scratch_cap;    // accumulation, hodge.cu); null or too small -> fp64 atomics (y += ...)
   // brick kernel: the element table [Q][p+1] shared by the interior elements of the uniform mesh,
-  // [role own/other][axis x/y] (read as constant-bank operands on bricks of interior elements)
-  double uni[2][2][25];
+  // [role own/other][axis] (read as constant-bank operands on bricks / layers of interior elements),
+  // and per [axis][role] the range [uni_lo, uni_hi) of elements whose table equals it bit for bit
+  double uni[2][3][25];
+  int uni_lo[3][2], uni_hi[3][2];
   int dual;              // 1: dual 2-forms (M~2_{1/eps}), 0: primal 2-forms (M2_{1/mu})
   int form;              // brick kernel form type: 0 primal 2-form, 1 dual 2-form, 2 primal 1-form
                          // (M^1_eps, scheme 1), 3 dual 1-form (M~^1_mu, scheme 1)

@@ -109,6 +109,7 @@ struct Plan {
   int* first_dev = nullptr;           // per-axis first local global index per element [n]
   size_t basis_off[3][4] = {};        // offsets (doubles) into basis_dev per axis and space
   int first0[3][4] = {};              // first index of element 0 per axis and space (first(e) = first0 + e)
+  int basis_lo[3][4] = {}, basis_hi[3][4] = {};  // elements [lo, hi) whose table equals basis_mid bit for bit
   double basis_mid[3][4][25] = {};    // host copy of the middle element's table [Q][p+1] per axis and space
   size_t first_off[3][4] = {};        // offsets (ints) into first_dev per axis and space
   // on-the-fly geometry (SGM_OPT_OTF_GEOMETRY): control points [3][(nz+p)(ny+p)(nx+p)] then the
