@@ -119,6 +119,14 @@ struct CompSm {
     const int s = ybase + jz;
     return s >= G::NZ ? s - G::NZ : s;
   }
+  // view of component C2's buffers for the x stages, whose code depends on the component only
+  // through NX and the x role: components 1 and 2 share one instantiation (less code, and warps
+  // whose tasks span both components do not diverge)
+  template <int C2>
+  __device__ __forceinline__ explicit CompSm(const CompSm<P, Q, DUAL, E, C2>& o)
+      : Xw(o.Xw), Yw(o.Yw), Z1(o.Z1), T1(o.T1), Z2(o.Z2), U(o.U), Vx(o.Vx), Vy(o.Vy), Vz(o.Vz) {
+    static_assert(Geo<P, Q, DUAL, E, C2>::NX == G::NX && (C == 0) == (C2 == 0), "x-stage compatible components");
+  }
   __device__ CompSm(double* sm) {
     using L = Layout<P, Q, DUAL, E>;
     double* b = sm + (C == 0 ? 0 : (C == 1 ? L::OFF1 : L::OFF2));
@@ -507,6 +515,7 @@ __global__ void __launch_bounds__(brick_threads(P), 2) hodge_brick_kernel(const 
   CompSm<P, Q, DUAL, E, 0> S0(sm);
   CompSm<P, Q, DUAL, E, 1> S1(sm);
   CompSm<P, Q, DUAL, E, 2> S2(sm);
+  const CompSm<P, Q, DUAL, E, 1> S2x(S2);  // component 2 through component 1's x-stage code
   double* tab = sm + L::TAB;
   double* Wsm = sm + L::WB;
   // OTF: map partial sums and the brick's x / y map tables (see Layout)
@@ -691,19 +700,17 @@ __global__ void __launch_bounds__(brick_threads(P), 2) hodge_brick_kernel(const 
       wphase ^= 1u;
       __syncthreads();
       {
-        const bool u0 = uni[0 * 2 + 0], u1 = uni[1 * 2 + 0], u2 = uni[1 * 2 + 0];
+        const bool u0 = uni[0 * 2 + 0], u1 = uni[1 * 2 + 0];  // (components 1 and 2: the other role along x)
         const double* Wm = FULL ? nullptr : Wsm;
         for (int t = threadIdx.x; t < 3 * 2 * Q * EQ; t += NT) {
           const int c = t / (2 * Q * EQ), tt = t % (2 * Q * EQ);
           if (c == 0) {
             if (u0) interp_x<P, Q, DUAL, E, 0, true>(A, S0, tt, Wm, B.nex, B.ney);
             else interp_x<P, Q, DUAL, E, 0, false>(A, S0, tt, Wm, B.nex, B.ney);
-          } else if (c == 1) {
-            if (u1) interp_x<P, Q, DUAL, E, 1, true>(A, S1, tt, Wm, B.nex, B.ney);
-            else interp_x<P, Q, DUAL, E, 1, false>(A, S1, tt, Wm, B.nex, B.ney);
           } else {
-            if (u2) interp_x<P, Q, DUAL, E, 2, true>(A, S2, tt, Wm, B.nex, B.ney);
-            else interp_x<P, Q, DUAL, E, 2, false>(A, S2, tt, Wm, B.nex, B.ney);
+            const CompSm<P, Q, DUAL, E, 1> Sx = c == 1 ? S1 : S2x;
+            if (u1) interp_x<P, Q, DUAL, E, 1, true>(A, Sx, tt, Wm, B.nex, B.ney);
+            else interp_x<P, Q, DUAL, E, 1, false>(A, Sx, tt, Wm, B.nex, B.ney);
           }
         }
         if (OTF) {
@@ -791,7 +798,22 @@ __global__ void __launch_bounds__(brick_threads(P), 2) hodge_brick_kernel(const 
         __syncthreads();
       }
       if (ez + 1 < B.ez1) stage_w(ez + 1);
-      SGM_BRICK_STAGE3U(test_x, 0, Q * EQ, Q * EQ, Q * EQ)
+      {
+        const bool u0 = uni[0 * 2 + 0], u1 = uni[1 * 2 + 0];
+        for (int t = threadIdx.x; t < 3 * Q * EQ; t += NT) {
+          if (t < Q * EQ) {
+            if (u0) test_x<P, Q, DUAL, E, 0, true>(A, S0, t);
+            else test_x<P, Q, DUAL, E, 0, false>(A, S0, t);
+          } else {
+            const bool second = t >= 2 * Q * EQ;
+            const CompSm<P, Q, DUAL, E, 1> Sx = second ? S2x : S1;
+            const int tt = t - (second ? 2 : 1) * Q * EQ;
+            if (u1) test_x<P, Q, DUAL, E, 1, true>(A, Sx, tt);
+            else test_x<P, Q, DUAL, E, 1, false>(A, Sx, tt);
+          }
+        }
+        __syncthreads();
+      }
       // y testing of this layer; on the threads it leaves idle, the next layer's top coefficient
       // layer and z interpolation (Z1 was last read by this layer's y interpolation)
       SGM_BRICK_TASKS3U(test_y, 1, Q * G0::PX, Q * G1::PX, Q * G2::PX)
