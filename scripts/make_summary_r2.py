@@ -42,31 +42,42 @@ def ncu_rows(path):
     return out
 
 
-def main(tag):
+def main(tag, htag=None):
     cp = lambda src, dst: shutil.copy(os.path.join(G, src), os.path.join(PR, dst))  # noqa: E731
     b = json.load(open(os.path.join(G, f"bench_{tag}.json")))
     ref = json.load(open(os.path.join(G, f"bench_ref_{tag}.json")))
     sweep = [json.loads(l) for l in open(os.path.join(G, f"bench_sweep_{tag}.jsonl")) if l.strip()]
     cp(f"bench_{tag}.json", "r2_bench.json")
     cp(f"bench_ref_{tag}.json", "r2_bench_reference.json")
-    cp(f"bench_sweep_{tag}.jsonl", "r2_bench_sweep.jsonl")
+    if htag:
+        # general-Hodge workloads (C4, C3), the brick kernel's ncu captures and the test logs from a later
+        # call (scripts/gpu_s5e.sh) on the final library
+        sweep = [d for d in sweep if d["roofline"]["kernel"] != "hodge_general"]
+        sweep += [json.loads(l) for l in open(os.path.join(G, f"bench_hodge_{htag}.jsonl")) if l.strip()]
+        with open(os.path.join(PR, "r2_bench_sweep.jsonl"), "w") as fh:
+            for d in sweep:
+                fh.write(json.dumps(d) + "\n")
+    else:
+        cp(f"bench_sweep_{tag}.jsonl", "r2_bench_sweep.jsonl")
     cp(f"launches_{tag}.csv", "r2_ncu_launches.csv")
     cp(f"full_{tag}_raw.csv", "r2_ncu_full_raw.csv")
     for c in ("c3", "c4"):
-        if os.path.exists(os.path.join(G, f"hodge_{c}_{tag}_raw.csv")):
-            cp(f"hodge_{c}_{tag}_raw.csv", f"r2_ncu_hodge_{c}_raw.csv")
+        if os.path.exists(os.path.join(G, f"hodge_{c}_{htag or tag}_raw.csv")):
+            cp(f"hodge_{c}_{htag or tag}_raw.csv", f"r2_ncu_hodge_{c}_raw.csv")
     if os.path.exists(os.path.join(G, f"c5_sweep_{tag}.jsonl")):
         cp(f"c5_sweep_{tag}.jsonl", "r2_c5_sweep.jsonl")
     table = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_traffic.py"),
                             os.path.join(G, f"full_{tag}_raw.csv"), "c5_p3_n128"],
                            capture_output=True, text=True).stdout
     ser, shares = launch_shares(os.path.join(G, f"launches_{tag}.csv"))
-    pyt = open(os.path.join(G, f"pytest_gpu_{tag}.log")).read().strip().splitlines()[-1]
-    smoke = open(os.path.join(G, f"smoke_{tag}.log")).read().strip().splitlines()[-1]
+    pyt = open(os.path.join(G, f"pytest_gpu_{htag or tag}.log")).read().strip().splitlines()[-1]
+    smoke = open(os.path.join(G, f"smoke_{htag or tag}.log")).read().strip().splitlines()[-1]
     r = b["roofline"]
     L = ["# Round 2 profile summary (B200, sm_100a)\n",
          f"From one `gpurun` call (`TAG={tag} bash scripts/gpu_full_r2.sh`), summarised by "
-         f"`python scripts/make_summary_r2.py {tag}`. Round-1 files (`r1_*`) are kept for comparison.\n",
+         f"`python scripts/make_summary_r2.py {tag}`" + (f"; the general-Hodge workloads (C4, C3 lines, brick-kernel "
+         f"ncu captures) and the test / smoke lines below from a later call on the final library "
+         f"(`TAG={htag} bash scripts/gpu_s5e.sh`)" if htag else "") + ". Round-1 files (`r1_*`) are kept for comparison.\n",
          f"Same call: `pytest -m \"gpu and not slow\"` → {pyt}; `smoke()` → {smoke}. The full-size parity "
          "(`-m \"gpu and slow\"`, C3 200 and C4 100 steps as configured, C5 at 100 steps) is in "
          "`r2_parity_fullsize.md`; the measured fp64 peak in `r2_fp64_peak.json`.\n",
@@ -145,4 +156,4 @@ def main(tag):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1])
+    main(*sys.argv[1:3])
