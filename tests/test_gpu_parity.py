@@ -214,6 +214,47 @@ def test_general_hodge_variable_eps_identity():
         assert rel(a, b) < 1e-11
 
 
+@pytest.mark.parametrize("p,axis,curved", [(4, 0, False), (4, 2, False), (3, 1, True), (3, 2, True), (2, 0, True)])
+def test_general_hodge_long_axis_uniform_bricks(p, axis, curved):
+    """100 elements along one axis (5 and 6 along the others: ragged bricks): most bricks / layers
+    along the long axis are interior, so the brick kernel reads their element tables from its
+    parameters (the host makes the interior tables bit-identical: at n ~ 100 their construction
+    rounding, n * 1e-16, is above the 1e-14 the kernel used to test with), W comes from the
+    brick-layout chunks, and along z the chunking is the cost-based one.  Both masses against the
+    oracle's mass applies (scalar W on the identity map, full W on the curved map)."""
+    n = [5, 6, 5]
+    n[axis] = 100
+    n = tuple(n)
+    if curved:
+        ctrl, eps = _curved_case(p, n, incl=False)
+        pl = S.Plan(n, p, geom_ctrl=ctrl)
+        X = pl.qp_coords()
+        eps = 1 + 0.4 * np.sin(2 * np.pi * X[:, 0]) * np.cos(2 * np.pi * X[:, 2])
+        mu = 1 + 0.3 * np.cos(2 * np.pi * X[:, 1])
+        tb = TierB(p, n, ctrl=ctrl, inv_eps=1.0 / eps, inv_mu=1.0 / mu)
+    else:
+        pl = S.Plan(n, p)
+        X = pl.qp_coords()
+        eps = 1 + 0.5 * np.sin(2 * np.pi * X[:, 0]) * np.cos(2 * np.pi * X[:, 1])
+        mu = 1 + 0.25 * np.sin(2 * np.pi * X[:, 2])
+        tb = TierB(p, n, inv_eps=1.0 / eps, inv_mu=1.0 / mu)
+    pl.set_material(S.EPS, eps)
+    pl.set_material(S.MU, mu)
+    assert not pl.separable(S.MASS_EPS) and not pl.separable(S.MASS_MU)
+    g = np.random.default_rng(131 + p + axis)
+    x = g.standard_normal(tb.N_e)
+    y = torch.empty(tb.N_e, dtype=torch.float64, device="cuda")
+    pl.hodge_apply(S.MASS_EPS, dev(x), y)
+    assert rel(host(y), forms.join(tb.mass_eps(tb.split_e(x)))) < 1e-13
+    xb = g.standard_normal(tb.N_h)
+    yb = torch.empty(tb.N_h, dtype=torch.float64, device="cuda")
+    pl.hodge_apply(S.MASS_MU, dev(xb), yb)
+    assert rel(host(yb), forms.join(tb.mass_mu(tb.split_h(xb)))) < 1e-13
+    y2 = torch.empty_like(y)
+    pl.hodge_apply(S.MASS_EPS, dev(x), y2)
+    assert torch.equal(y, y2)
+
+
 def test_step_host_equals_device():
     p, n = 3, 10
     pl = S.Plan(n, p)
