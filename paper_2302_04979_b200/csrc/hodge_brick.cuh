@@ -8,13 +8,17 @@
 // brick's coefficients of each component form a patch of PX x PY functions (consecutive elements
 // share all but one function per axis: PX = E - 1 + NX); along z a window of NZ coefficient layers
 // slides by one layer per element, and the output window accumulates in shared memory, its lowest
-// layer complete (and flushed with fp64 atomics) after each element; both windows are circular
-// (layer jz of the current element in slot (base + jz) % NZ), so nothing is copied.  Per element layer the three
-// interpolation stages (z, y, x), the quadrature-point multiply and the three testing stages
-// (x, y, z) each run over the whole brick with all threads: every 1D contraction is a small
-// register-blocked loop (one thread produces a whole row of outputs from one row of inputs), the
-// basis values are shared-memory broadcasts.  Only the brick's border functions are shared with
-// neighbouring bricks, so far fewer atomics than element-wise accumulation.
+// layer complete after each element and written to the work item's patch in the scratch
+// (hodge_gather_kernel sums the patches in a fixed order: bitwise reproducible; without a scratch
+// the layer is flushed with fp64 atomics).  Both windows are circular (layer jz in slot
+// (base + jz) % NZ), so nothing is copied.  Per element layer: [y interpolation | z testing and
+// flush of the previous layer] -> [x interpolation, scalar W fused] -> ([3 x 3 W multiply]) ->
+// [x testing] -> [y testing | load and z interpolation of the next layer], a block barrier between
+// the intervals.  Every 1D contraction is a small register-blocked loop (one thread produces a
+// row of outputs from a row of inputs); on bricks / layers of interior elements the basis values
+// are kernel parameters (constant-bank FMA operands), else shared-memory broadcasts.  W of a layer
+// arrives by one bulk copy (TMA engine) from its brick-layout chunk in HBM.  Shared-memory strides
+// are padded so that the consecutive tasks of a stage fall on distinct bank pairs.
 #pragma once
 
 #include "kernels.cuh"
